@@ -1,0 +1,155 @@
+"""Instance recipes for BASELINE.json configs[0..4] (seed = config index).
+
+Every instance is a separable QP in the paper's form (P):
+    min 1/2 x^T Q x + c^T x   s.t.  A x = b,  x >= 0,   Q = diag(q).
+A is dense fp64 and stored column-major (numpy order='F'), matching the device layout.
+
+Draw order is fixed and documented per config so both sides (oracle tests and the GPU
+path) see bit-identical inputs.  `make_config(idx, m=.., n=.., ell=..)` produces the same
+recipe at a reduced size for tests; the default sizes are the BASELINE.json ones.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+CONFIG_NAMES = {
+    0: "cfg0_tiny_m100_n400_l20",
+    1: "cfg1_lowrank_m2000_n8000_l50",
+    2: "cfg2_svm_N50000_d1000_l100",
+    3: "cfg3_portfolio_m64_n200000_l64",
+    4: "cfg4_large_m50000_n400000_l200",
+}
+
+FULL_SIZES = {  # (m, n, ell) per BASELINE.json configs
+    0: (100, 400, 20),
+    1: (2000, 8000, 50),
+    2: (50000, 1000, 100),   # (N samples, d features, ell); n = 2d + 2N variables
+    3: (64, 200000, 64),
+    4: (50000, 400000, 200),
+}
+
+
+@dataclass
+class QPInstance:
+    """One seeded QP instance.  `A` is m x n column-major fp64 (dense configs)."""
+    name: str
+    idx: int
+    A: Optional[np.ndarray]          # m x n, order='F' (None for the structured SVM config)
+    q: np.ndarray                    # n, diag of Q (>= 0)
+    b: np.ndarray                    # m
+    c: np.ndarray                    # n
+    ell: int
+    x0: Optional[np.ndarray] = None  # generator's feasible primal point (if any)
+    y0: Optional[np.ndarray] = None
+    z0: Optional[np.ndarray] = None
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def m(self) -> int:
+        return int(self.b.shape[0])
+
+    @property
+    def n(self) -> int:
+        return int(self.c.shape[0])
+
+
+def gaussian_matrix(rng: np.random.Generator, m: int, n: int, scale: float = 1.0) -> np.ndarray:
+    """m x n i.i.d. N(0, scale^2), column-major.  Drawn column by column (column-major order)."""
+    G = rng.standard_normal((n, m)).T  # row-major (n, m) draw == column-major (m, n)
+    if scale != 1.0:
+        G *= scale
+    return np.asfortranarray(G)
+
+
+def _feasible_bc(A, q, x0, y0, z0):
+    # b = A x0 ; c = A^T y0 + z0 - q o x0  (BASELINE.json configs[0]: "gives b=A.x0 and c=...")
+    b = A @ x0
+    c = A.T @ y0 + z0 - q * x0
+    return b, c
+
+
+def make_config(idx: int, m: Optional[int] = None, n: Optional[int] = None,
+                ell: Optional[int] = None, seed: Optional[int] = None) -> QPInstance:
+    fm, fn, fl = FULL_SIZES[idx]
+    m = fm if m is None else int(m)
+    n = fn if n is None else int(n)
+    ell = fl if ell is None else int(ell)
+    seed = idx if seed is None else int(seed)
+    rng = np.random.default_rng(seed)
+    name = CONFIG_NAMES[idx] if (m, n, ell) == (fm, fn, fl) else f"cfg{idx}_m{m}_n{n}_l{ell}"
+
+    if idx == 0:
+        # draw order: A, q, zero-permutation, x0, y0, z0
+        A = gaussian_matrix(rng, m, n, 1.0 / np.sqrt(n))          # A_ij ~ N(0, 1/n)
+        q = rng.uniform(0.0, 1.0, n)
+        q[rng.permutation(n)[: n // 2]] = 0.0                    # exactly floor(n/2) zeros (A22)
+        x0 = rng.uniform(0.5, 1.5, n)
+        y0 = rng.standard_normal(m)
+        z0 = rng.uniform(0.5, 1.5, n)
+        b, c = _feasible_bc(A, q, x0, y0, z0)
+        return QPInstance(name, idx, A, q, b, c, ell, x0, y0, z0)
+
+    if idx in (1, 4):
+        # A = W H + s G ; draw order: W, H, G, q, [zero-permutation], x0, y0, z0
+        r, s = (40, 1e-3) if idx == 1 else (100, 1e-2)
+        r = min(r, m, n)
+        W = gaussian_matrix(rng, m, r)
+        H = gaussian_matrix(rng, r, n)
+        G = gaussian_matrix(rng, m, n)
+        A = np.asfortranarray(W @ H + s * G)
+        del G
+        if idx == 1:
+            q = rng.uniform(1e-3, 1.0, n)
+        else:
+            q = rng.uniform(0.0, 1.0, n)
+            q[rng.permutation(n)[: int(0.3 * n)]] = 0.0          # floor(0.3 n) zeros (A22)
+        x0 = rng.uniform(0.5, 1.5, n)
+        y0 = rng.standard_normal(m)
+        z0 = rng.uniform(0.5, 1.5, n)
+        b, c = _feasible_bc(A, q, x0, y0, z0)
+        return QPInstance(name, idx, A, q, b, c, ell, x0, y0, z0)
+
+    if idx == 3:
+        # portfolio-shaped: A = [1^T ; F], F iid N(0,1) (m-1) x n.
+        # draw order: F, x0-raw, q, c
+        F = gaussian_matrix(rng, m - 1, n)
+        A = np.asfortranarray(np.vstack([np.ones((1, n)), F]))
+        del F
+        x0 = rng.uniform(0.5, 1.5, n) / n
+        x0 /= x0.sum()                                           # exactly feasible budget row (A20)
+        b = A @ x0
+        b[0] = 1.0
+        q = rng.uniform(0.01, 0.1, n)
+        c = -rng.normal(0.05, 0.02, n)                           # 0.02 is the std (A21)
+        return QPInstance(name, idx, A, q, b, c, ell, x0, None, None)
+
+    if idx == 2:
+        # SVM-shaped (A23): labels, X with rows x_i = 0.5 y_i 1_d + g_i; Xt = diag(y) X.
+        # Variables [w+, w-, xi, s] (n_var = 2d + 2N); A = [Xt, -Xt, I, -I]; m = N.
+        N, d = m, n
+        yl = np.where(rng.uniform(size=N) < 0.5, -1.0, 1.0)
+        X = gaussian_matrix(rng, N, d)
+        X += 0.5 * yl[:, None]
+        Xt = np.asfortranarray(yl[:, None] * X)
+        del X
+        nv = 2 * d + 2 * N
+        q = np.concatenate([np.ones(2 * d), np.zeros(2 * N)])
+        Cpen = 1.0
+        c = np.concatenate([np.zeros(2 * d), Cpen * np.ones(N), np.zeros(N)])
+        b = np.ones(N)
+        inst = QPInstance(name, idx, None, q, b, c, ell, extra={"Xt": Xt, "labels": yl, "d": d, "N": N})
+        assert inst.n == nv
+        return inst
+
+    raise ValueError(f"unknown config {idx}")
+
+
+def svm_dense_A(inst: QPInstance) -> np.ndarray:
+    """Materialise A = [Xt, -Xt, I, -I] for SMALL SVM instances only (tests)."""
+    Xt = inst.extra["Xt"]
+    N = Xt.shape[0]
+    I = np.eye(N)
+    return np.asfortranarray(np.hstack([Xt, -Xt, I, -I]))

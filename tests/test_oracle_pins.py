@@ -1,0 +1,431 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (runs without a GPU).
+
+Each test names the passage it pins (P:n = PAPER.md line n, S:n = SPEC.md line n).
+None of these re-types the oracle's own formula: they use closed forms, exact rational
+arithmetic, brute force, textbook invariants or printed paper values.
+"""
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import ippmm, linops, nystrom, pcg as pcgmod, rng
+from oracle.active_set import enumerate_active_sets
+from synth import make_config
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rand_psd_lowrank(rs, m, r, spread=1.0):
+    Q, _ = np.linalg.qr(rs.standard_normal((m, r)))
+    ev = np.logspace(0, -spread, r) * 3.0
+    return (Q * ev) @ Q.T, Q, ev
+
+
+# ------------------------------------------------------------------ normal operator
+def test_normal_matvec_spec_example_s57():
+    # A=[[1,1]], q=0, theta^{-1}=1, rho=0, delta=0.5, v=(1) -> 2.5 (hand arithmetic: 1+1+0.5)
+    A = np.array([[1.0, 1.0]])
+    d = linops.scaling_d(np.zeros(2), np.ones(2), np.ones(2), 0.0)  # z/x = theta^{-1} = 1
+    w = linops.normal_matvec(A, d, np.array([1.0]), 0.5)
+    assert w[0] == 2.5
+
+
+def test_normal_matvec_spec_example_s56_corrected():
+    # S:56 with A=I2, q=(1,1), theta^{-1}=(1,1), rho=0, delta=1, v=(2,2):
+    # d = 1/(1+1) = 1/2, so w = 1/2*2 + 1*2 = 3 (SPEC's printed (2,2) is wrong).
+    d = linops.scaling_d(np.ones(2), np.ones(2), np.ones(2), 0.0)
+    w = linops.normal_matvec(np.eye(2), d, np.array([2.0, 2.0]), 1.0)
+    np.testing.assert_array_equal(w, [3.0, 3.0])
+
+
+def test_normal_matvec_exact_rational():
+    # brute force in exact rational arithmetic on a tiny instance (different arithmetic path)
+    rs = np.random.default_rng(11)
+    m, n = 5, 7
+    A = rs.standard_normal((m, n))
+    d = rs.uniform(0.1, 3.0, n)
+    e = rs.uniform(0.0, 1.0, m)
+    v = rs.standard_normal(m)
+    delta = 0.37
+    F = Fraction
+    exact = []
+    for i in range(m):
+        s = F(0)
+        for j in range(n):
+            t = sum(F(A[k, j]) * F(v[k]) for k in range(m)) * F(d[j])
+            s += F(A[i, j]) * t
+        s += F(e[i]) * F(v[i]) + F(delta) * F(v[i])
+        exact.append(float(s))
+    exact = np.array(exact)
+    w = linops.normal_matvec(A, d, v, delta, e)
+    assert np.linalg.norm(w - exact) <= 1e-15 * np.linalg.norm(exact)
+
+
+def test_sketch_columns_are_matvecs_without_delta():
+    # Alg. 1 line 2 with SURVEY A1: Y = N_k Omega, N_k excludes delta
+    inst = make_config(0)
+    rs = np.random.default_rng(1)
+    d = rs.uniform(0.1, 2.0, inst.n)
+    Om = rs.standard_normal((inst.m, 5))
+    Y = linops.sketch(inst.A, d, Om)
+    for j in range(5):
+        col = linops.normal_matvec(inst.A, d, Om[:, j], 1.0) - Om[:, j]
+        assert np.linalg.norm(Y[:, j] - col) <= 1e-13 * np.linalg.norm(col)
+
+
+def test_operator_is_spd_with_delta_floor():
+    # <v, (N + delta I) v> >= delta ||v||^2
+    inst = make_config(0)
+    rs = np.random.default_rng(2)
+    d = rs.uniform(0.0, 2.0, inst.n)
+    for _ in range(50):
+        v = rs.standard_normal(inst.m)
+        assert v @ linops.normal_matvec(inst.A, d, v, 0.3) >= 0.3 * (v @ v) * (1 - 1e-14)
+
+
+# ------------------------------------------------------------------ Nystrom (Alg. 1)
+def test_nu_is_julia_eps_of_frobenius_norm():
+    # P:376 nu = eps(norm(Y,'fro')) -- Julia eps(x) is the ulp spacing: 2^(floor(log2 x) - 52)
+    Y = np.full((4, 2), 3.0)  # ||Y||_F = 6*sqrt(2) = 8.485..., floor(log2) = 3
+    Om = np.eye(4)[:, :2]
+    _, _, info = nystrom.nystrom_from_sketch(Y + 10 * np.eye(4)[:, :2], Om)
+    Yf = np.linalg.norm(Y + 10 * np.eye(4)[:, :2], "fro")
+    assert info["nu"] == 2.0 ** (np.floor(np.log2(Yf)) - 52)
+
+
+def test_nystrom_identity_gives_unit_eigenvalues():
+    # N = I5, l = 3 -> lambda_hat = (1,1,1)
+    rs = np.random.default_rng(3)
+    Om = rs.standard_normal((5, 3))
+    U, lam, _ = nystrom.nystrom_from_sketch(Om.copy(), Om)
+    np.testing.assert_allclose(lam, 1.0, atol=1e-12)
+    np.testing.assert_allclose(U.T @ U, np.eye(3), atol=1e-13)
+
+
+def test_nystrom_rank2_example_s167():
+    # N = U diag(3,2,0,0) U^T, l = 2 -> lambda_hat = (3,2), N_hat = N
+    rs = np.random.default_rng(4)
+    Q, _ = np.linalg.qr(rs.standard_normal((4, 4)))
+    N = (Q[:, :2] * [3.0, 2.0]) @ Q[:, :2].T
+    Om = rs.standard_normal((4, 2))
+    U, lam, _ = nystrom.nystrom_from_sketch(N @ Om, Om)
+    np.testing.assert_allclose(lam, [3.0, 2.0], rtol=1e-12)
+    np.testing.assert_allclose((U * lam) @ U.T, N, atol=1e-12)
+
+
+@pytest.mark.parametrize("extra", [2, 10])
+def test_nystrom_exact_recovery_above_rank(extra):
+    # Nystrom approximation is exact when l > rank(N) (range(Y) = range(N))
+    rs = np.random.default_rng(5)
+    m, r = 60, 8
+    N, _, _ = _rand_psd_lowrank(rs, m, r, spread=3)
+    Om = rs.standard_normal((m, r + extra))
+    U, lam, _ = nystrom.nystrom_from_sketch(N @ Om, Om)
+    err = np.linalg.norm(N - (U * lam) @ U.T) / np.linalg.norm(N)
+    assert err <= 1e-11
+    np.testing.assert_allclose(U.T @ U, np.eye(r + extra), atol=1e-12)
+
+
+def test_nystrom_is_below_N_in_loewner_order():
+    # N_hat = Y (Omega^T Y)^+ Y^T is a projection of N: 0 <= N_hat <= N (Loewner)
+    rs = np.random.default_rng(6)
+    m = 40
+    B = rs.standard_normal((m, m))
+    N = B @ np.diag(np.logspace(0, -6, m)) @ B.T
+    for ell in (3, 10, 25):
+        Om = rs.standard_normal((m, ell))
+        U, lam, _ = nystrom.nystrom_from_sketch(N @ Om, Om)
+        assert np.all(lam >= 0) and np.all(np.diff(lam) <= 0)
+        ev = np.linalg.eigvalsh(N - (U * lam) @ U.T)
+        assert ev.min() >= -1e-12 * np.linalg.norm(N, 2)
+
+
+def test_nystrom_matches_pseudoinverse_formula_on_wellconditioned_case():
+    # eq.: N_hat = Y (Omega^T Y)^+ Y^T (the unstable textbook formula is fine when
+    # Omega^T Y is well conditioned)
+    rs = np.random.default_rng(7)
+    m, ell = 30, 6
+    B = rs.standard_normal((m, m))
+    N = B @ B.T / m + np.eye(m)
+    Om = rs.standard_normal((m, ell))
+    Y = N @ Om
+    ref = Y @ np.linalg.pinv(Om.T @ Y) @ Y.T
+    U, lam, info = nystrom.nystrom_from_sketch(Y, Om)
+    # lambda_hat subtracts nu: compare with the nu-shifted reference within nu-scale
+    assert np.linalg.norm((U * lam) @ U.T - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+# ------------------------------------------------------------------ preconditioner
+def _factors(seed=8, m=50, ell=7):
+    rs = np.random.default_rng(seed)
+    B = rs.standard_normal((m, m))
+    N = B @ np.diag(np.logspace(2, -3, m)) @ B.T
+    Om = rs.standard_normal((m, ell))
+    U, lam, _ = nystrom.nystrom_from_sketch(N @ Om, Om)
+    return N, U, lam, rs
+
+
+def test_precond_inverse_times_precond_is_identity():
+    N, U, lam, rs = _factors()
+    mu = 0.05
+    for _ in range(5):
+        v = rs.standard_normal(N.shape[0])
+        w = nystrom.precond_inv_apply(U, lam, mu, nystrom.precond_apply(U, lam, mu, v))
+        assert np.linalg.norm(w - v) <= 1e-12 * np.linalg.norm(v)
+
+
+def test_precond_inverse_fixed_directions():
+    # P^{-1} u_l = u_l; v orthogonal to range(U) -> P^{-1} v = v
+    N, U, lam, rs = _factors()
+    mu = 0.2
+    ul = U[:, -1]
+    np.testing.assert_allclose(nystrom.precond_inv_apply(U, lam, mu, ul), ul, atol=1e-13)
+    v = rs.standard_normal(N.shape[0])
+    v -= U @ (U.T @ v)
+    np.testing.assert_allclose(nystrom.precond_inv_apply(U, lam, mu, v), v, atol=1e-13)
+
+
+def test_precond_inverse_spectrum_range():
+    # eig(P^{-1}) in [(lam_l+mu)/(lam_1+mu), 1]
+    N, U, lam, _ = _factors()
+    mu = 0.01
+    ev = np.linalg.eigvalsh(nystrom.precond_inv_dense(U, lam, mu))
+    lo = (lam[-1] + mu) / (lam[0] + mu)
+    assert ev.min() >= lo * (1 - 1e-10) and ev.max() <= 1 + 1e-10
+
+
+def test_preconditioned_condition_number_bound():
+    # kappa(P^{-1/2} N_delta P^{-1/2}) <= (lam_l + delta + ||N - N_hat||_2)/delta
+    N, U, lam, _ = _factors(m=60, ell=10)
+    delta = 1e-2
+    Nd = N + delta * np.eye(N.shape[0])
+    Pi = nystrom.precond_inv_dense(U, lam, delta)
+    w, V = np.linalg.eigh(Pi)
+    S = (V * np.sqrt(w)) @ V.T
+    ev = np.linalg.eigvalsh(S @ Nd @ S)
+    kappa = ev.max() / ev.min()
+    bound = (lam[-1] + delta + np.linalg.norm(N - (U * lam) @ U.T, 2)) / delta
+    assert kappa <= bound * (1 + 1e-8)
+
+
+def test_pcg_one_iteration_when_sketch_exceeds_rank():
+    # l > rank(N): P^{-1}(N + delta I) = (lam_l+delta) I  -> PCG converges in one step
+    rs = np.random.default_rng(9)
+    m, r = 40, 5
+    N, _, _ = _rand_psd_lowrank(rs, m, r, spread=4)
+    Om = rs.standard_normal((m, r + 3))
+    U, lam, _ = nystrom.nystrom_from_sketch(N @ Om, Om)
+    delta = 1e-3
+    b = rs.standard_normal(m)
+    x, info = pcgmod.pcg(lambda v: N @ v + delta * v, b,
+                         lambda v: nystrom.precond_inv_apply(U, lam, delta, v),
+                         tol_abs=1e-10 * np.linalg.norm(b), max_iter=50)
+    assert info["iters"] <= 2  # 1 in exact arithmetic; lam_hat carries nu-level noise
+    assert np.linalg.norm(N @ x + delta * x - b) <= 1e-9 * np.linalg.norm(b)
+
+
+def test_table2_matvec_cost():
+    # Table 2: Nystrom P^{-1} matvec costs 2 l m + m + 5 l flops
+    assert nystrom.precond_apply_flops(2000, 50) == 2 * 50 * 2000 + 2000 + 5 * 50
+
+
+# ------------------------------------------------------------------ PCG
+def test_pcg_identity_one_iteration():
+    b = np.array([1.0, -2.0, 3.0])
+    x, info = pcgmod.pcg(lambda v: v, b, tol_abs=1e-14)
+    assert info["iters"] == 1
+    np.testing.assert_allclose(x, b)
+
+
+def test_pcg_three_distinct_eigenvalues():
+    # diag(1,2,3) converges in <= 3 iterations (CG finite termination)
+    Dg = np.array([1.0, 2.0, 3.0])
+    b = np.random.default_rng(10).standard_normal(3)
+    x, info = pcgmod.pcg(lambda v: Dg * v, b, tol_abs=1e-12)
+    assert info["iters"] <= 3
+    np.testing.assert_allclose(x, b / Dg, rtol=1e-12)
+
+
+def test_pcg_perfect_preconditioner():
+    rs = np.random.default_rng(11)
+    B = rs.standard_normal((20, 20))
+    M = B @ B.T + np.diag(np.logspace(0, 4, 20))
+    Mi = np.linalg.inv(M)
+    b = rs.standard_normal(20)
+    x, info = pcgmod.pcg(lambda v: M @ v, b, lambda v: Mi @ v, tol_abs=1e-9 * np.linalg.norm(b))
+    assert info["iters"] == 1
+
+
+def test_pcg_energy_error_monotone_and_solution():
+    # the energy-norm error is nonincreasing; result matches a dense solve
+    rs = np.random.default_rng(12)
+    B = rs.standard_normal((25, 25))
+    M = B @ B.T + 0.1 * np.eye(25)
+    b = rs.standard_normal(25)
+    xs = np.linalg.solve(M, b)
+    errs = []
+    x, info = pcgmod.pcg(lambda v: M @ v, b, tol_abs=1e-11, max_iter=500,
+                         callback=lambda it, xk, rk: errs.append((xk - xs) @ M @ (xk - xs)))
+    assert all(e2 <= e1 * (1 + 1e-9) + 1e-24 for e1, e2 in zip(errs, errs[1:]))
+    np.testing.assert_allclose(x, xs, rtol=1e-7, atol=1e-9)
+
+
+# ------------------------------------------------------------------ IP-PMM pieces
+def test_stepsize_spec_example():
+    # x=(1,1), dx=(-2,-0.5) -> 0.995*min(1, 0.5, 2) = 0.4975 ; empty set -> 0.995 (A16)
+    assert ippmm.stepsize(np.array([1.0, 1.0]), np.array([-2.0, -0.5])) == pytest.approx(0.4975, abs=1e-15)
+    assert ippmm.stepsize(np.array([1.0, 1.0]), np.array([2.0, 0.5])) == 0.995
+
+
+def test_duality_measure():
+    # P:888 with J empty; S:321 x=z=(1,1) -> 1
+    assert ippmm.duality_measure(np.ones(2), np.ones(2)) == 1.0
+    assert ippmm.duality_measure(np.array([2.0, 4.0]), np.array([3.0, 0.5])) == 4.0
+
+
+def test_newton_direction_block_structure_prop31():
+    # Prop. 3.1: with dx, dz from the closed forms, blocks 1 and 3 of the Newton
+    # system hold to rounding; block 2's residual equals the normal-eq residual.
+    inst = make_config(0)
+    rs = np.random.default_rng(13)
+    n, m = inst.n, inst.m
+    x = rs.uniform(0.1, 2, n)
+    z = rs.uniform(0.1, 2, n)
+    y = rs.standard_normal(m)
+    rho, delta = 0.3, 0.07
+    d = linops.scaling_d(inst.q, x, z, rho)
+    r_d = inst.c + inst.q * x - inst.A.T @ y - z + rho * (x - x[::-1])
+    r_p = inst.b - inst.A @ x - delta * (y - y[::-1])
+    r_xz = -x * z
+    holder = {}
+
+    def solve_loose(xi):  # deliberately inexact: a few CG steps only
+        sol, info = pcgmod.pcg(lambda v: linops.normal_matvec(inst.A, d, v, delta), xi,
+                               tol_abs=0.0, max_iter=3)
+        holder["theta"] = linops.normal_matvec(inst.A, d, sol, delta) - xi
+        return sol, info
+
+    dx, dy, dz, xi, _ = ippmm.newton_direction(inst.A, d, x, z, r_d, r_p, r_xz, solve_loose)
+    b1, b2, b3 = ippmm.newton_block_residuals(inst.A, inst.q, rho, delta, x, z, dx, dy, dz, r_d, r_p, r_xz)
+    scale = np.linalg.norm(r_d) + np.linalg.norm(inst.A.T @ dy) + np.linalg.norm(dz)
+    assert np.linalg.norm(b1) <= 1e-13 * scale
+    assert np.linalg.norm(b3) <= 1e-13 * (np.linalg.norm(r_xz) + np.linalg.norm(z * dx))
+    assert np.linalg.norm(holder["theta"]) > 1e-6                 # the solve really was inexact
+    np.testing.assert_allclose(b2, holder["theta"], rtol=1e-9, atol=1e-12)
+
+
+def test_initial_point_hand_computed_n1():
+    # App. B.2 on min 1/2 x^2 s.t. x = 1, x >= 0 (A=[1], b=1, c=0, q=1):
+    # x~ = 1/11, y~ = (1/11)(1/11) = 1/121, z~ = 0 - 1/121 + 1/11 = 10/121, both >= 0 so
+    # delta_p = delta_d = 0, gamma = 10/1331, delta~_p = 0.5 gamma / (10/121) = 1/22,
+    # delta~_d = 0.5 gamma / (1/11) = 5/121
+    A = np.array([[1.0]])
+    solve = lambda r: (r / 11.0, {"iters": 0})  # noqa: E731 (AA^T + 10 I = 11)
+    x0, y0, z0, _ = ippmm.initial_point(A, np.array([1.0]), np.array([1.0]), np.array([0.0]), solve)
+    assert x0[0] == pytest.approx(1 / 11 + 1 / 22, rel=1e-15)
+    assert y0[0] == pytest.approx(1 / 121, rel=1e-15)
+    assert z0[0] == pytest.approx(10 / 121 + 5 / 121, rel=1e-15)
+
+
+def _read_peu_rows():
+    rows = []
+    with open(os.path.join(GOLDEN, "peu_tables_5_6.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            p, k, r0, d0, r1, d1 = line.split()
+            rows.append((p, int(k), float(r0), float(d0), float(r1), float(d1)))
+    return rows
+
+
+def test_peu_rule_form_matches_tables_5_6():
+    # Tables 5-6: in rows where rho and delta shrink differently, the smaller
+    # factor is (1 - r) (improved) and the larger is (1 - 2/3 r) (not improved), SURVEY A12.
+    rows = _read_peu_rows()
+    checked = 0
+    for p, k, r0, d0, r1, d1 in rows:
+        f_r, f_d = r1 / r0, d1 / d0
+        if abs(f_r - f_d) <= 0.01 * max(f_r, f_d):
+            # equal factors: both improved (or both not) with the same r
+            assert ippmm.peu_factor(True, 1 - f_d) == pytest.approx(f_r, rel=0.02)
+            continue
+        small, large = min(f_r, f_d), max(f_r, f_d)
+        r = 1.0 - small
+        assert ippmm.peu_factor(True, r) == pytest.approx(small, rel=1e-12)
+        assert ippmm.peu_factor(False, r) == pytest.approx(large, rel=0.03), (p, k)
+        checked += 1
+    assert checked >= 10
+
+
+def test_peu_floor_value():
+    # Tables 5-6 floor 5.00e-10
+    assert ippmm.Options().reg_floor == 5e-10
+
+
+# ------------------------------------------------------------------ end to end
+def test_hand_kkt_n1_solution():
+    # min 1/2 x^2, x = 1, x >= 0 -> x* = 1, y* = 1, z* = 0
+    r = ippmm.solve(np.array([[1.0]]), np.array([1.0]), np.array([1.0]), np.array([0.0]),
+                    ippmm.Options(path="krylov", ell=1))
+    assert r.status == "optimal"
+    assert r.x[0] == pytest.approx(1.0, abs=1e-7)
+    assert r.y[0] == pytest.approx(1.0, abs=1e-6)
+    assert r.z[0] == pytest.approx(0.0, abs=1e-7)
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("path,ell", [("direct", 0), ("krylov", 2), ("krylov", 0)])
+def test_tiny_qp_matches_active_set_enumeration(seed, path, ell):
+    # S:425 / S:535-543: random tiny separable QPs vs brute-force active-set enumeration
+    rs = np.random.default_rng(100 + seed)
+    m, n = 3, 8
+    A = rs.standard_normal((m, n))
+    x0 = rs.uniform(0.2, 1.5, n)
+    x0[rs.permutation(n)[:3]] = 0.0
+    b = A @ x0
+    q = rs.uniform(0.1, 2.0, n)           # Q > 0: unique x*
+    c = rs.standard_normal(n)
+    ref = enumerate_active_sets(A, q, b, c)
+    r = ippmm.solve(A, q, b, c, ippmm.Options(path=path, ell=ell))
+    assert r.status == "optimal"
+    assert abs(r.obj - ref["obj"]) <= 1e-6 * max(1.0, abs(ref["obj"]))
+    np.testing.assert_allclose(r.x, ref["x"], atol=1e-5)
+
+
+def test_config0_direct_and_krylov_agree_and_bracket():
+    inst = make_config(0)
+    lo = inst.b @ inst.y0 - 0.5 * inst.x0 @ (inst.q * inst.x0)     # dual objective of (x0, y0, z0)
+    hi = 0.5 * inst.x0 @ (inst.q * inst.x0) + inst.c @ inst.x0      # primal objective of x0
+    rd = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="direct"))
+    rk = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
+    for r in (rd, rk):
+        assert r.status == "optimal"
+        assert lo - 1e-9 <= r.obj <= hi + 1e-9
+        assert r.rel_p <= 1e-8 and r.rel_d <= 1e-8 and r.mu <= 1e-8
+        assert abs(r.obj - r.dual_obj) <= 1e-6 * (1 + abs(r.obj))
+    assert abs(rd.obj - rk.obj) <= 1e-7 * abs(rd.obj)
+
+
+# ------------------------------------------------------------------ Philox
+def test_philox_known_answer_vectors():
+    with open(os.path.join(GOLDEN, "philox4x32_10_kat.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            h = [int(t, 16) for t in line.split()]
+            out = rng.philox4x32_10([h[0]], [h[1]], [h[2]], [h[3]], h[4], h[5])
+            assert [int(o[0]) for o in out] == h[6:10]
+
+
+def test_gaussian_omega_moments_and_layout():
+    Om = rng.gaussian_omega(2000, 40, seed=5, stream=3)
+    assert Om.shape == (2000, 40) and Om.flags["F_CONTIGUOUS"]
+    assert abs(Om.mean()) < 0.01 and abs(Om.std() - 1) < 0.01
+    # different streams / seeds are different matrices; same args reproduce bit-for-bit
+    assert not np.array_equal(Om, rng.gaussian_omega(2000, 40, seed=5, stream=4))
+    assert np.array_equal(Om, rng.gaussian_omega(2000, 40, seed=5, stream=3))
+    # column-major linear index: a taller matrix has the first column's prefix as prefix
+    Om2 = rng.gaussian_omega(2000, 41, seed=5, stream=3)
+    np.testing.assert_array_equal(Om2[:, :40], Om)
