@@ -1,0 +1,506 @@
+// K1 — fused fp64 normal-equation matvec  w = A diag(d) A^T v (+ e o v + delta v)
+// (PAPER.md:201 N_k = A (Q + Theta^{-1} + rho I)^{-1} A^T, P:835 the PCG operator).
+//
+// ONE pass over A.  A is column-major; a "panel" is BN consecutive columns.  A CTA (or a
+// thread-block cluster of CL CTAs splitting the rows, for m > 8192) owns whole panels:
+//   1. a producer warp streams each column segment (contiguous in memory) into a shared
+//      memory stage with 1-D bulk async copies (cp.async.bulk, L2 evict_first) completing on
+//      an mbarrier; S stages are in flight;
+//   2. consumer threads copy their rows of the stage into registers and release the stage;
+//   3. column dots (A^T v)_j: FMA in registers, warp shuffles, a per-group shared reduction
+//      and (CL > 1) a DSMEM exchange of the CTA partials through remote mbarrier arrives;
+//      every CTA sums the CL partials in rank order, so t_j = d_j (A^T v)_j is identical on
+//      all CTAs of the cluster;
+//   4. the same registers are reused for the rank-BN update  w_acc += A_panel t_panel.
+// Each cluster writes its m-slice partial w to a workspace row; `mv_finalize` sums the
+// partials in a fixed order (deterministic) and applies (delta + e) v, additive terms and
+// the optional PCG dot p^T w / alpha = rz / p^T w.
+//
+// The same kernel also provides the T-only pass (A^T v with IPM epilogues) and the N-only
+// pass (A u) that Alg. 4 needs.
+#include "nys_common.cuh"
+
+namespace nys {
+
+struct MatvecParams {
+  const double* A;
+  int64_t lda, m, n;
+  const double* z;
+  const double* p;
+  const double* beta;
+  double* p_out;
+  const double* d;
+  const double* u;
+  double* Wp;
+  int64_t wp_ld;
+  int tep;
+  double* t1;
+  double* t2;
+  const double *ta, *tb, *tc, *td, *tx, *tdd;
+  const double* done;
+  int64_t rs;
+  int64_t npanels;
+  int stages;
+  int cl;
+};
+
+__device__ __forceinline__ void t_epilogue(const MatvecParams& P, int64_t j, double s) {
+  if (P.tep == TE_PLAIN) {
+    P.t1[j] = s;
+  } else if (P.tep == TE_DX) {
+    // Alg. 4 (P:840, P:842 / A15): dx = d (A^T dy - r_d - xi_au);  dz = (r_xz - z dx) / x
+    double rd = P.ta ? P.ta[j] : 0.0;
+    double dx = P.tdd[j] * (s - rd - P.tb[j]);
+    P.t1[j] = dx;
+    P.t2[j] = (P.tc[j] - P.td[j] * dx) / P.tx[j];
+  } else {  // TE_RD: r_D = c + q x - A^T y - z
+    double zz = P.td ? P.td[j] : 0.0;
+    P.t1[j] = P.ta[j] + P.tb[j] * P.tc[j] - s - zz;
+  }
+}
+
+template <int T, int GT, int RPT, int CPG, int MODE, bool VS>
+__global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P) {
+  constexpr int NG = T / GT;
+  constexpr int WPG = GT / 32;
+  constexpr int BN = NG * CPG;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+
+  if (P.done != nullptr && *P.done != 0.0) return;  // grid-uniform early exit (PCG converged)
+
+  const int S = P.stages;
+  const int64_t rs = P.rs;
+  const int cl = P.cl;
+  double* stage = reinterpret_cast<double*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage + (size_t)S * BN * rs);
+  uint64_t* empty = full + S;
+  uint64_t* dotbar = empty + S;
+  double* red = reinterpret_cast<double*>(dotbar + S);
+  double* slots = red + 2 * NG * WPG * CPG;
+  double* vsm = slots + (size_t)S * cl * CPG;  // VS: the operand slice v (rs doubles)
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const uint32_t crank = cl > 1 ? cluster_ctarank() : 0u;
+  const uint32_t cid = cl > 1 ? cluster_id_x() : blockIdx.x;
+  const uint32_t ncl = cl > 1 ? ncluster_x() : gridDim.x;
+  const int64_t r0 = (int64_t)crank * rs;
+  int64_t rows_valid = P.m - r0;
+  rows_valid = rows_valid < 0 ? 0 : (rows_valid > rs ? rs : rows_valid);
+  const uint32_t copy_bytes = (uint32_t)(((rows_valid + 1) & ~int64_t(1)) * 8);
+  const int64_t niter = (cid < P.npanels) ? (P.npanels - cid + ncl - 1) / ncl : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], T / 32);
+      mbar_init(&dotbar[s], (uint32_t)(cl * CPG));
+    }
+    fence_mbar_init();
+  }
+  if (cl > 1) cluster_sync_all(); else __syncthreads();
+
+  const int g = tid / GT;
+  const int lig = tid % GT;
+  double vreg[VS ? 1 : RPT];
+  double wacc[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) { if (!VS) vreg[i] = 0.0; wacc[i] = 0.0; }
+
+  if (warp == T / 32) {
+    // ------------------------------ producer warp ------------------------------------------
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      for (int64_t it = 0; it < niter; ++it) {
+        const int s = (int)(it % S);
+        if (it >= S) mbar_wait(&empty[s], (uint32_t)(((it / S) - 1) & 1));
+        const int64_t col0 = (int64_t)(cid + it * ncl) * BN;
+        int64_t ncols = P.n - col0;
+        ncols = ncols > BN ? BN : ncols;
+        const uint32_t bytes = (uint32_t)ncols * copy_bytes;
+        if (bytes > 0) {
+          mbar_arrive_expect_tx(&full[s], bytes);
+          for (int c = 0; c < ncols; ++c)
+            bulk_g2s(stage + ((size_t)s * BN + c) * rs, P.A + (col0 + c) * P.lda + r0, copy_bytes, &full[s], pol);
+        } else {
+          mbar_arrive(&full[s]);
+        }
+      }
+    }
+  } else {
+    // ------------------------------ consumers ----------------------------------------------
+    if (MODE != MV_NONLY) {
+      const double bval = (P.beta != nullptr) ? *P.beta : 0.0;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t rl = lig + (int64_t)GT * i;
+        if (rl < rs) {
+          double v = 0.0;
+          if (rl < rows_valid) {
+            const int64_t r = r0 + rl;
+            v = P.z[r];
+            if (P.p != nullptr) v += bval * P.p[r];
+            if (P.p_out != nullptr && cid == 0 && g == 0) P.p_out[r] = v;
+          }
+          if (VS) { if (g == 0) vsm[rl] = v; } else vreg[i] = v;
+        }
+      }
+    }
+    if (VS) named_bar_sync(1, T);  // vsm complete (NG == 1 for VS)
+    for (int64_t it = 0; it < niter; ++it) {
+      const int s = (int)(it % S);
+      const uint32_t par = (uint32_t)((it / S) & 1);
+      const int64_t col0 = (int64_t)(cid + it * ncl) * BN + (int64_t)g * CPG;
+      mbar_wait(&full[s], par);
+      double a[CPG][RPT];
+      const double* sb = stage + ((size_t)s * BN + (size_t)g * CPG) * rs;
+#pragma unroll
+      for (int c = 0; c < CPG; ++c) {
+        const bool cv = (col0 + c) < P.n;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const int64_t rl = lig + (int64_t)GT * i;
+          a[c][i] = (cv && rl < rows_valid) ? sb[(size_t)c * rs + rl] : 0.0;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+
+      double t[CPG];
+      if (MODE != MV_NONLY) {
+        double pd[CPG];
+#pragma unroll
+        for (int c = 0; c < CPG; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            const int64_t rl = lig + (int64_t)GT * i;
+            const double vv = VS ? ((rl < rs) ? vsm[rl] : 0.0) : vreg[VS ? 0 : i];
+            acc = fma(a[c][i], vv, acc);
+          }
+          pd[c] = warp_sum(acc);
+        }
+        if (WPG > 1) {
+          double* rb = red + ((size_t)(it & 1) * NG + g) * WPG * CPG;
+          if (lane == 0) {
+#pragma unroll
+            for (int c = 0; c < CPG; ++c) rb[(warp % WPG) * CPG + c] = pd[c];
+          }
+          named_bar_sync(1 + g, GT);
+#pragma unroll
+          for (int c = 0; c < CPG; ++c) {
+            double tot = 0.0;
+#pragma unroll
+            for (int w = 0; w < WPG; ++w) tot += rb[w * CPG + c];
+            pd[c] = tot;
+          }
+        }
+        if (cl > 1) {  // NG == 1 here: exchange CTA partials through DSMEM
+#pragma unroll
+          for (int c = 0; c < CPG; ++c) {
+            if (tid == c) {
+              const uint32_t my_slot = smem_u32(&slots[((size_t)s * cl + crank) * CPG + c]);
+              const uint32_t my_bar = smem_u32(&dotbar[s]);
+              for (int peer = 0; peer < cl; ++peer) {
+                st_cluster_f64(mapa_shared(my_slot, (uint32_t)peer), pd[c]);
+                mbar_arrive_remote(mapa_shared(my_bar, (uint32_t)peer));
+              }
+            }
+          }
+          mbar_wait_cluster(&dotbar[s], par);
+#pragma unroll
+          for (int c = 0; c < CPG; ++c) {
+            double tot = 0.0;
+            for (int r = 0; r < cl; ++r) tot += slots[((size_t)s * cl + r) * CPG + c];
+            pd[c] = tot;
+          }
+        }
+        if (MODE == MV_FUSED) {
+#pragma unroll
+          for (int c = 0; c < CPG; ++c) t[c] = (col0 + c < P.n) ? P.d[col0 + c] * pd[c] : 0.0;
+        } else {  // MV_TONLY
+          if (crank == 0) {
+#pragma unroll
+            for (int c = 0; c < CPG; ++c)
+              if (lig == c && col0 + c < P.n) t_epilogue(P, col0 + c, pd[c]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CPG; ++c) t[c] = (col0 + c < P.n) ? P.u[col0 + c] : 0.0;
+      }
+      if (MODE != MV_TONLY) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          double acc = wacc[i];
+#pragma unroll
+          for (int c = 0; c < CPG; ++c) acc = fma(a[c][i], t[c], acc);
+          wacc[i] = acc;
+        }
+      }
+    }
+  }
+
+  if (MODE != MV_TONLY) {
+    __syncthreads();  // all bulk copies consumed: the stage memory is free for the group sum
+    double* outp = P.Wp + (size_t)cid * P.wp_ld + r0;
+    if (NG == 1) {
+      if (tid < T) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const int64_t rl = lig + (int64_t)GT * i;
+          if (rl < rows_valid) outp[rl] = wacc[i];
+        }
+      }
+    } else {
+      double* wsum = stage;
+      if (tid < T) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const int64_t rl = lig + (int64_t)GT * i;
+          if (rl < rows_valid) wsum[(size_t)g * rs + rl] = wacc[i];
+        }
+      }
+      __syncthreads();
+      for (int64_t r = tid; r < rows_valid; r += T + 32) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg) sacc += wsum[(size_t)gg * rs + r];
+        outp[r] = sacc;
+      }
+    }
+  }
+  if (cl > 1) {
+    __syncwarp();
+    cluster_sync_all();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// finalize: out_i = sgn * sum_k Wp[k][i] + (delta + e_i) v_i + add_i ; optional PCG dot
+// ------------------------------------------------------------------------------------------
+struct FinParams {
+  const double* Wp;
+  int64_t wp_ld;
+  int nparts;
+  int64_t m;
+  double sgn;
+  double delta;
+  int use_delta;
+  const double* e;
+  const double* v;      // operand vector (p for PCG)
+  const double* add;
+  double* out;
+  int pcg_alpha;
+  double* sc;           // scalar slots
+  double* part;         // per-block partials (pcg dot)
+  unsigned int* counter;
+  const double* done;
+};
+
+__global__ void __launch_bounds__(256) mv_finalize(const FinParams F) {
+  if (F.done != nullptr && *F.done != 0.0) return;
+  __shared__ double sred[8];
+  __shared__ bool am_last;
+  double dot = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.m; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < F.nparts; ++k) s += F.Wp[(size_t)k * F.wp_ld + i];
+    s *= F.sgn;
+    if (F.use_delta) s += (F.delta + (F.e ? F.e[i] : 0.0)) * F.v[i];
+    if (F.add) s += F.add[i];
+    F.out[i] = s;
+    if (F.pcg_alpha) dot = fma(F.v[i], s, dot);
+  }
+  if (!F.pcg_alpha) return;
+  dot = warp_sum(dot);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = dot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += sred[w];
+    F.part[blockIdx.x] = b;
+    __threadfence();
+    const unsigned prev = atomicAdd(F.counter, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (am_last && threadIdx.x == 0) {
+    __threadfence();
+    double pw = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) pw += ((volatile double*)F.part)[b];
+    *F.counter = 0u;
+    F.sc[S_PW] = pw;
+    if (!(pw > 0.0) || !isfinite(pw)) {
+      F.sc[S_STATUS] = (double)NYS_EBREAKDOWN;
+      F.sc[S_DONE] = 1.0;
+      F.sc[S_ALPHA] = 0.0;
+    } else {
+      F.sc[S_ALPHA] = F.sc[S_RZ] / pw;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// host dispatch
+// ------------------------------------------------------------------------------------------
+struct MvCfg {
+  int T, GT, RPT, CPG;
+};
+
+static MvCfg pick_cfg(int64_t rs) {
+  if (rs <= 64) return {256, 32, 2, 4};
+  if (rs <= 128) return {256, 32, 4, 2};
+  if (rs <= 256) return {256, 64, 4, 2};
+  if (rs <= 1024) return {256, 128, 8, 2};
+  if (rs <= 2048) return {256, 256, 8, 4};
+  if (rs <= 4096) return {512, 512, 8, 2};
+  return {512, 512, 16, 1};
+}
+
+typedef void (*MvKernel)(const MatvecParams);
+
+template <int MODE>
+static MvKernel kernel_for(const MvCfg& c) {
+  if (c.T == 256 && c.GT == 32 && c.RPT == 2 && c.CPG == 4) return matvec_kernel<256, 32, 2, 4, MODE, false>;
+  if (c.T == 256 && c.GT == 32 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<256, 32, 4, 2, MODE, false>;
+  if (c.T == 256 && c.GT == 64 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<256, 64, 4, 2, MODE, false>;
+  if (c.T == 256 && c.GT == 128 && c.RPT == 8 && c.CPG == 2) return matvec_kernel<256, 128, 8, 2, MODE, false>;
+  if (c.T == 256 && c.GT == 256 && c.RPT == 8 && c.CPG == 4) return matvec_kernel<256, 256, 8, 4, MODE, false>;
+  if (c.T == 512 && c.GT == 512 && c.RPT == 8 && c.CPG == 2) return matvec_kernel<512, 512, 8, 2, MODE, false>;
+  return matvec_kernel<512, 512, 16, 1, MODE, true>;
+}
+
+struct MvPlan {
+  MvCfg cfg;
+  int cl = 1;
+  int64_t rs = 0;
+  int stages = 2;
+  size_t smem = 0;
+  int64_t npanels = 0;
+  int grid = 0;       // CTAs
+  int nparts = 0;     // clusters (= partial rows)
+};
+
+static bool cfg_vs(const MvCfg& c) { return c.RPT >= 16; }
+
+static size_t mv_smem_bytes(const MvCfg& c, int64_t rs, int stages, int cl) {
+  const int NG = c.T / c.GT, WPG = c.GT / 32, BN = NG * c.CPG;
+  size_t b = (size_t)stages * BN * rs * 8;
+  b += (size_t)3 * stages * 8;
+  b += (size_t)2 * NG * WPG * c.CPG * 8;
+  b += (size_t)stages * cl * c.CPG * 8;
+  if (cfg_vs(c)) b += (size_t)rs * 8;
+  return b;
+}
+
+static std::map<std::tuple<int, int, int, int, int, int64_t, int64_t>, MvPlan> g_plans;
+
+static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, MvPlan& pl) {
+  auto key = std::make_tuple(ctx->device, mode, 0, 0, 0, m, n);
+  auto itp = g_plans.find(key);
+  if (itp != g_plans.end()) { pl = itp->second; return NYS_OK; }
+  int cl = 1;
+  while ((m + cl - 1) / cl > 8192 && cl < 16) cl *= 2;
+  int64_t rs = (m + cl - 1) / cl;
+  rs = (rs + 1) & ~int64_t(1);
+  MvCfg c = pick_cfg(rs);
+  const int NG = c.T / c.GT, BN = NG * c.CPG;
+  const size_t stage_bytes = (size_t)BN * rs * 8;
+  size_t budget = (rs <= 1024) ? 96 * 1024 : 200 * 1024;
+  if (cfg_vs(c)) budget -= (size_t)rs * 8;
+  int stages = (int)(budget / stage_bytes);
+  stages = stages > 8 ? 8 : stages;
+  if (stages < 2) stages = 2;
+  size_t smem = mv_smem_bytes(c, rs, stages, cl);
+  MvKernel k = (mode == MV_FUSED) ? kernel_for<MV_FUSED>(c) : (mode == MV_TONLY) ? kernel_for<MV_TONLY>(c) : kernel_for<MV_NONLY>(c);
+  NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (cl > 8) NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  const int64_t npanels = (n + BN - 1) / BN;
+  int grid = 0;
+  if (cl == 1) {
+    int occ = 0;
+    NYS_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c.T + 32, smem));
+    if (occ < 1) occ = 1;
+    int64_t g = (int64_t)ctx->num_sms * occ;
+    grid = (int)(npanels < g ? npanels : g);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(cl * ctx->num_sms));
+    cfg.blockDim = dim3((unsigned)(c.T + 32));
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    NYS_CUDA_TRY(ctx, cudaOccupancyMaxActiveClusters(&ncl, k, &cfg));
+    if (ncl < 1) { ctx->set_error("matvec: cluster configuration does not fit on the device"); return NYS_ECUDA; }
+    int64_t g = ncl;
+    g = npanels < g ? npanels : g;
+    grid = (int)(g * cl);
+  }
+  if (grid < cl) grid = cl;
+  pl.cfg = c; pl.cl = cl; pl.rs = rs; pl.stages = stages; pl.smem = smem; pl.npanels = npanels;
+  pl.grid = grid; pl.nparts = grid / cl;
+  g_plans[key] = pl;
+  return NYS_OK;
+}
+
+int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
+  if (c.m <= 0) return NYS_OK;
+  MvPlan pl;
+  NYS_TRY(make_plan(ctx, c.mode, c.m, c.n, pl));
+  const int64_t wp_ld = (c.m + 1) & ~int64_t(1);
+  double* Wp = nullptr;
+  if (c.mode != MV_TONLY) Wp = ctx->wsd("mv_partials", (size_t)pl.nparts * wp_ld);
+  if (c.n > 0 || c.mode == MV_TONLY) {
+    MatvecParams P{};
+    P.A = c.A; P.lda = c.lda; P.m = c.m; P.n = c.n;
+    P.z = c.z; P.p = c.p; P.beta = c.beta; P.p_out = c.p_out; P.d = c.d; P.u = c.u;
+    P.Wp = Wp; P.wp_ld = wp_ld;
+    P.tep = c.tep; P.t1 = c.t1; P.t2 = c.t2; P.ta = c.ta; P.tb = c.tb; P.tc = c.tc; P.td = c.td; P.tx = c.tx; P.tdd = c.tdd;
+    P.done = c.done; P.rs = pl.rs; P.npanels = pl.npanels; P.stages = pl.stages; P.cl = pl.cl;
+    MvKernel k = (c.mode == MV_FUSED) ? kernel_for<MV_FUSED>(pl.cfg) : (c.mode == MV_TONLY) ? kernel_for<MV_TONLY>(pl.cfg) : kernel_for<MV_NONLY>(pl.cfg);
+    if (c.n > 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)pl.grid);
+      cfg.blockDim = dim3((unsigned)(pl.cfg.T + 32));
+      cfg.dynamicSmemBytes = pl.smem;
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = pl.cl;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, P));
+      ctx->launches++;
+      if (c.mode == MV_FUSED) ctx->matvecs++;
+    }
+  }
+  if (c.mode == MV_TONLY) return NYS_OK;
+  if (c.n <= 0) {  // empty shard: zero partial
+    NYS_CUDA_TRY(ctx, cudaMemsetAsync(Wp, 0, sizeof(double) * (size_t)pl.nparts * wp_ld, ctx->stream));
+  }
+  if (c.out == nullptr) return NYS_OK;
+  FinParams F{};
+  F.Wp = Wp; F.wp_ld = wp_ld; F.nparts = pl.nparts; F.m = c.m; F.sgn = c.sgn;
+  F.delta = c.delta; F.use_delta = c.use_delta ? 1 : 0; F.e = c.e;
+  F.v = (c.p_out != nullptr) ? c.p_out : c.z;
+  F.add = c.add; F.out = c.out; F.pcg_alpha = c.pcg_alpha ? 1 : 0; F.sc = ctx->sc;
+  F.counter = ctx->counters + 0;
+  F.done = c.done;
+  int fgrid = (int)((c.m + 255) / 256);
+  if (fgrid > 2 * ctx->num_sms) fgrid = 2 * ctx->num_sms;
+  F.part = ctx->wsd("fin_part", (size_t)fgrid);
+  mv_finalize<<<fgrid, 256, 0, ctx->stream>>>(F);
+  ctx->launches++;
+  return ctx->check_launch("mv_finalize");
+}
+
+}  // namespace nys

@@ -1,0 +1,367 @@
+// Small dense kernels of Alg. 1: the shift nu = eps(||Y||_F), Y_nu, the
+// ell x ell Cholesky + triangular inverse (lines 5-6), triangular products, and the thin SVD
+// of B = Y_nu C^{-1} finished on the ell x ell triangular factor by one-sided Jacobi.
+// All ell x ell routines run in ONE CTA (1024 threads) with the matrices in shared memory
+// when they fit, else in an L2-resident global workspace.
+#include "k_vec.cuh"
+
+namespace nys {
+
+// ------------------------------------------------------------------------------------------
+// ||Y||_F and nu = eps(||Y||_F) = 2^(floor(log2 ||Y||_F) - 52)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) fro_kernel(int64_t m, int ell, const double* Y, int64_t ldy, double* part,
+                                                  unsigned int* counter, double* sc) {
+  double acc = 0.0;
+  const int64_t total = m * (int64_t)ell;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    const double v = Y[i + j * ldy];
+    acc = fma(v, v, acc);
+  }
+  acc = warp_sum(acc);
+  __shared__ double sh[32];
+  __shared__ bool last;
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+    part[blockIdx.x] = s;
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += ((volatile double*)part)[b];
+    *counter = 0u;
+    const double f = sqrt(s);
+    sc[S_FRO] = f;
+    double nu;
+    if (f > 0.0 && isfinite(f)) {
+      nu = ldexp(1.0, ilogb(f) - 52);
+      if (nu == 0.0) nu = 4.9406564584124654e-324;
+    } else {
+      nu = 4.9406564584124654e-324;
+    }
+    sc[S_NU] = nu;
+  }
+}
+
+int launch_fro_nu(nys_ctx* ctx, int64_t m, int ell, const double* Y, int64_t ldy, int /*unused*/) {
+  int64_t total = m * ell;
+  int g = (int)((total + 1023) / 1024);
+  if (g > 2 * ctx->num_sms) g = 2 * ctx->num_sms;
+  if (g < 1) g = 1;
+  double* part = ctx->wsd("fro_part", (size_t)g);
+  fro_kernel<<<g, 256, 0, ctx->stream>>>(m, ell, Y, ldy, part, ctx->counters + 3, ctx->sc);
+  ctx->launches++;
+  return ctx->check_launch("fro");
+}
+
+// Y_nu = Y + nu Omega
+__global__ void ynu_kernel(int64_t m, int ell, const double* Y, const double* Om, double* Ynu, int64_t ld,
+                           const double* sc) {
+  const double nu = sc[S_NU];
+  const int64_t total = m * (int64_t)ell;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    Ynu[i + j * ld] = fma(nu, Om[i + j * ld], Y[i + j * ld]);
+  }
+}
+int launch_ynu(nys_ctx* ctx, int64_t m, int ell, const double* Y, const double* Om, double* Ynu, int64_t ld) {
+  int64_t total = m * ell;
+  int g = (int)((total + 255) / 256);
+  if (g > 4 * ctx->num_sms) g = 4 * ctx->num_sms;
+  if (g < 1) g = 1;
+  ynu_kernel<<<g, 256, 0, ctx->stream>>>(m, ell, Y, Om, Ynu, ld, ctx->sc);
+  ctx->launches++;
+  return ctx->check_launch("ynu");
+}
+
+// Y += e o Omega (multi-GPU sketch: the diagonal term is added once, after the all-reduce)
+__global__ void add_eomega_kernel(int64_t m, int ell, const double* e, const double* Om, double* Y, int64_t ld) {
+  const int64_t total = m * (int64_t)ell;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q % m, j = q / m;
+    Y[i + j * ld] = fma(e[i], Om[i + j * ld], Y[i + j * ld]);
+  }
+}
+int launch_add_eomega(nys_ctx* ctx, int64_t m, int ell, const double* e, const double* Om, double* Y, int64_t ld) {
+  int64_t total = m * ell;
+  int g = (int)((total + 255) / 256);
+  if (g > 4 * ctx->num_sms) g = 4 * ctx->num_sms;
+  if (g < 1) g = 1;
+  add_eomega_kernel<<<g, 256, 0, ctx->stream>>>(m, ell, e, Om, Y, ld);
+  ctx->launches++;
+  return ctx->check_launch("add_eomega");
+}
+
+// ------------------------------------------------------------------------------------------
+// Cholesky G = R^T R (R upper) of the symmetrised G (+ optional CholeskyQR shift), and R^{-1}.
+// G (ell x ell, ld ldg) is overwritten with R (upper; strict lower zeroed).
+// shift_mode 0: none (Alg. 1 line 5, A3 symmetrisation).
+// shift_mode 1: shifted CholeskyQR (Fukaya et al. 2020): s = 11 (m ell + ell(ell+1)) u tr(G)
+//               with m passed in sc[S_SHIFT] as a double on entry.
+// Failure (non-positive / non-finite pivot) sets sc[S_CHOLFAIL] = 1.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) chol_inv_kernel(int ell, double* G, int ldg, double* Rinv, int ldr,
+                                                        int shift_mode, double* sc, double* gws, int use_smem) {
+  extern __shared__ double csm[];
+  double* W = use_smem ? csm : gws;  // ell x ell, ld = ell
+  const int n = ell;
+  __shared__ int fail;
+  __shared__ double shift;
+  if (threadIdx.x == 0) fail = 0;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    W[i + j * n] = 0.5 * (G[i + j * ldg] + G[j + i * ldg]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    if (shift_mode == 1) {
+      double tr = 0.0;
+      for (int i = 0; i < n; ++i) tr += W[i + i * n];
+      const double mrows = sc[S_SHIFT];
+      s = 11.0 * (mrows * n + (double)n * (n + 1)) * 0x1p-53 * tr;
+    }
+    shift = s;
+  }
+  __syncthreads();
+  if (shift_mode == 1) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) W[i + i * n] += shift;
+    __syncthreads();
+  }
+  // right-looking Cholesky on the upper triangle: W(k,k) = sqrt, row k scaled, trailing update
+  for (int k = 0; k < n; ++k) {
+    if (threadIdx.x == 0) {
+      const double piv = W[k + k * n];
+      if (!(piv > 0.0) || !isfinite(piv)) fail = 1;
+      else W[k + k * n] = sqrt(piv);
+    }
+    __syncthreads();
+    if (fail) break;
+    const double rkk = W[k + k * n];
+    for (int j = k + 1 + threadIdx.x; j < n; j += blockDim.x) W[k + j * n] /= rkk;
+    __syncthreads();
+    const int rem = n - k - 1;
+    const int tri = rem * (rem + 1) / 2;
+    for (int e = threadIdx.x; e < tri; e += blockDim.x) {
+      // map e -> (i, j) with k < i <= j, column-major over the upper trailing triangle
+      int jj = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while ((jj + 1) * (jj + 2) / 2 <= e) ++jj;
+      while (jj * (jj + 1) / 2 > e) --jj;
+      const int ii = e - jj * (jj + 1) / 2;
+      const int i = k + 1 + ii, j = k + 1 + jj;
+      W[i + j * n] -= W[k + i * n] * W[k + j * n];
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (threadIdx.x == 0) sc[S_CHOLFAIL] = 1.0;
+    return;
+  }
+  // write R (upper) back into G
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    G[i + j * ldg] = (i <= j) ? W[i + j * n] : 0.0;
+  }
+  __syncthreads();
+  // R^{-1} (upper) by backward substitution, one row i per step, all columns j >= i in parallel:
+  // X(i,j) = (delta_ij - sum_{k=i+1..j} R(i,k) X(k,j)) / R(i,i); X stored in Rinv.
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    Rinv[i + j * ldr] = 0.0;
+  }
+  __syncthreads();
+  for (int i = n - 1; i >= 0; --i) {
+    const double rii = W[i + i * n];
+    for (int j = i + threadIdx.x; j < n; j += blockDim.x) {
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int k = i + 1; k <= j; ++k) s -= W[i + k * n] * Rinv[k + j * ldr];
+      Rinv[i + j * ldr] = s / rii;
+    }
+    __syncthreads();
+  }
+}
+
+int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int ldr, int shift_mode) {
+  const size_t need = (size_t)ell * ell * sizeof(double);
+  const int use_smem = need <= 160 * 1024 ? 1 : 0;
+  double* gws = use_smem ? nullptr : ctx->wsd("chol_ws", (size_t)ell * ell);
+  if (use_smem) {
+    static size_t set = 0;
+    if (need > set) {
+      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(160 * 1024)));
+      set = 160 * 1024;
+    }
+  }
+  chol_inv_kernel<<<1, 1024, use_smem ? need : 0, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc, gws,
+                                                                   use_smem);
+  ctx->launches++;
+  return ctx->check_launch("chol_inv");
+}
+
+
+// Out = R1 * R2 for upper-triangular ell x ell (all with leading dimension ld)
+__global__ void trmm_upper_kernel(int n, int ld, const double* R1, const double* R2, double* Out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int i = e % n, j = e / n;
+    double s = 0.0;
+    if (i <= j)
+      for (int k = i; k <= j; ++k) s = fma(R1[i + k * ld], R2[k + j * ld], s);
+    Out[i + j * ld] = s;
+  }
+}
+int launch_trmm_upper(nys_ctx* ctx, int ell, int ld, const double* R1, const double* R2, double* Out) {
+  int g = (ell * ell + 255) / 256;
+  trmm_upper_kernel<<<g, 256, 0, ctx->stream>>>(ell, ld, R1, R2, Out);
+  ctx->launches++;
+  return ctx->check_launch("trmm_upper");
+}
+
+// ------------------------------------------------------------------------------------------
+// one-sided Jacobi on X = R^T (ell x ell): X V = U_X Sigma; then R = V Sigma U_X^T, so the LEFT
+// singular vectors of R are the accumulated rotations V (orthonormal to rounding).
+// Round-robin (circle) ordering: ell/2 disjoint pairs per round, one warp per pair.
+// Output: V (ell x ell, ld ell) and sigma sorted descending (columns of V permuted to match).
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, int ldr, double* Vout, int ldv,
+                                                      double* sigma, double* gws, int use_smem) {
+  extern __shared__ double jsm[];
+  double* X = use_smem ? jsm : gws;
+  double* V = X + (size_t)n * n;
+  __shared__ int rotated;
+  __shared__ double sv[256];
+  __shared__ int order[256];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    X[i + j * n] = R[j + i * ldr];  // X = R^T
+    V[i + j * n] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int P = (n % 2 == 0) ? n : n + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const double tol = 1e-15;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    for (int r = 0; r < P - 1; ++r) {
+      for (int pi = warp; pi < P / 2; pi += nw) {
+        int a, b;
+        if (pi == 0) { a = r; b = P - 1; }
+        else { a = (r + pi) % (P - 1); b = (r - pi + (P - 1)) % (P - 1); }
+        if (a >= n || b >= n) continue;
+        const int p = a < b ? a : b, q = a < b ? b : a;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < n; i += 32) {
+          const double xp = X[i + p * n], xq = X[i + q * n];
+          al = fma(xp, xp, al);
+          be = fma(xq, xq, be);
+          ga = fma(xp, xq, ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (fabs(ga) > tol * sqrt(al * be) && ga != 0.0) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t);
+          const double s = c * t;
+          for (int i = lane; i < n; i += 32) {
+            const double xp = X[i + p * n], xq = X[i + q * n];
+            X[i + p * n] = c * xp - s * xq;
+            X[i + q * n] = s * xp + c * xq;
+            const double vp = V[i + p * n], vq = V[i + q * n];
+            V[i + p * n] = c * vp - s * vq;
+            V[i + q * n] = s * vp + c * vq;
+          }
+          if (lane == 0) rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  // sigma_j = ||x_j||, then sort descending (rank sort, ties by index)
+  for (int j = warp; j < n; j += nw) {
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s = fma(X[i + j * n], X[i + j * n], s);
+    s = warp_sum(s);
+    if (lane == 0) sv[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    int rk = 0;
+    for (int k = 0; k < n; ++k) rk += (sv[k] > sv[j]) || (sv[k] == sv[j] && k < j);
+    order[rk] = j;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) sigma[j] = sv[order[j]];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    Vout[i + j * ldv] = V[i + order[j] * n];
+  }
+}
+
+int launch_jacobi_svd(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+  const size_t need = 2 * (size_t)ell * ell * sizeof(double);
+  const int use_smem = need <= 200 * 1024 ? 1 : 0;
+  double* gws = use_smem ? nullptr : ctx->wsd("jacobi_ws", 2 * (size_t)ell * ell);
+  if (use_smem) {
+    static bool set = false;
+    if (!set) {
+      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      set = true;
+    }
+  }
+  jacobi_kernel<<<1, 1024, use_smem ? need : 0, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, gws, use_smem);
+  ctx->launches++;
+  return ctx->check_launch("jacobi");
+}
+
+// lambda_hat = max{0, sigma^2 - nu}
+__global__ void lambda_kernel(int ell, const double* sigma, double* lam, const double* sc) {
+  const double nu = sc[S_NU];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ell) lam[i] = fmax(0.0, sigma[i] * sigma[i] - nu);
+}
+int launch_lambda_from_sigma(nys_ctx* ctx, int ell, const double* sigma, double* lam) {
+  lambda_kernel<<<(ell + 127) / 128, 128, 0, ctx->stream>>>(ell, sigma, lam, ctx->sc);
+  ctx->launches++;
+  return ctx->check_launch("lambda");
+}
+
+// ||U^T U - I||_F from a Gram matrix already computed into G (ell x ell)
+__global__ void orth_err_kernel(int ell, const double* G, int ldg, double* sc, int slot) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < ell * ell; e += blockDim.x) {
+    const int i = e % ell, j = e / ell;
+    const double v = G[i + j * ldg] - (i == j ? 1.0 : 0.0);
+    acc = fma(v, v, acc);
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+    sc[slot] = sqrt(s);
+  }
+}
+int launch_orth_err(nys_ctx* ctx, int64_t m, int ell, const double* U, int64_t ldu, int slot) {
+  double* G = ctx->wsd("orth_gram", (size_t)ell * ell);
+  GemmCall g;
+  g.M = ell; g.N = ell; g.K = m; g.A = U; g.lda = ldu; g.a_kmajor = true; g.B = U; g.ldb = ldu; g.C = G; g.ldc = ell;
+  NYS_TRY(launch_gemm(ctx, g));
+  orth_err_kernel<<<1, 256, 0, ctx->stream>>>(ell, G, ell, ctx->sc, slot);
+  ctx->launches++;
+  return ctx->check_launch("orth_err");
+}
+
+}  // namespace nys

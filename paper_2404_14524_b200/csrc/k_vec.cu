@@ -1,0 +1,697 @@
+// Vector kernels of the hot path: PCG updates with the fused Nystrom preconditioner apply,
+// IPM elementwise work of Alg. 4 / Alg. 5, deterministic reductions, the Gaussian test
+// matrix generator.  All reductions are two-level (block partials + last-block sum in a
+// fixed order) so results are bitwise reproducible run to run.
+#include "k_vec.cuh"
+
+namespace nys {
+
+// ------------------------------------------------------------------------------------------
+// Philox4x32-10 + Box-Muller (Salmon et al. SC'11).  Same published generator as
+// the oracle's numpy implementation (no shared code).
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, uint32_t k0,
+                                             uint32_t k1) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint32_t hi0 = __umulhi(M0, c0), lo0 = M0 * c0;
+  const uint32_t hi1 = __umulhi(M1, c2), lo1 = M1 * c2;
+  const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+  c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+}
+
+__global__ void gaussian_kernel(double* __restrict__ O, int64_t total, uint64_t seed, uint64_t stream) {
+  const int64_t npairs = (total + 1) >> 1;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c0 = (uint32_t)p, c1 = (uint32_t)((uint64_t)p >> 32), c2 = (uint32_t)stream, c3 = (uint32_t)(stream >> 32);
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+      philox_round(c0, c1, c2, c3, k0, k1);
+    }
+    const uint64_t a = ((((uint64_t)c0) << 32) | c1) >> 11;
+    const uint64_t b = ((((uint64_t)c2) << 32) | c3) >> 11;
+    const double u1 = ((double)a + 0.5) * 0x1p-53;
+    const double u2 = (double)b * 0x1p-53;
+    const double r = sqrt(-2.0 * log(u1));
+    const double th = 2.0 * 3.141592653589793 * u2;
+    const int64_t L = 2 * p;
+    O[L] = r * cos(th);
+    if (L + 1 < total) O[L + 1] = r * sin(th);
+  }
+}
+
+int launch_gaussian(nys_ctx* ctx, double* O, int64_t total, uint64_t seed, uint64_t stream) {
+  if (total <= 0) return NYS_OK;
+  int64_t npairs = (total + 1) / 2;
+  int grid = (int)((npairs + 255) / 256);
+  if (grid > 8 * ctx->num_sms) grid = 8 * ctx->num_sms;
+  gaussian_kernel<<<grid, 256, 0, ctx->stream>>>(O, total, seed, stream);
+  ctx->launches++;
+  return ctx->check_launch("gaussian");
+}
+
+// ------------------------------------------------------------------------------------------
+// generic deterministic block reduction helpers
+// ------------------------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void block_sum_to_part(double (&v)[NV], double* part, int stride) {
+  __shared__ double sh[NV][32];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sh[k][w] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = 0.0;
+      for (int i = 0; i < nw; ++i) s += sh[k][i];
+      part[(size_t)k * stride + blockIdx.x] = s;
+    }
+  }
+}
+
+__device__ __forceinline__ bool last_block_arrive(unsigned int* counter) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(counter, 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+// sum of part[0..nb) by thread 0 in order
+__device__ __forceinline__ double ordered_sum(const double* part, int nb) {
+  double s = 0.0;
+  for (int i = 0; i < nb; ++i) s += ((volatile const double*)part)[i];
+  return s;
+}
+
+// ------------------------------------------------------------------------------------------
+// dots: out_slot[k] = sum_i a_k[i] * b_k[i]   (b_k == nullptr -> a_k[i]^2), k < 4
+// optional affine pre-map: a_k[i] + alpha_k * da_k[i]  (for mu_aff)
+// ------------------------------------------------------------------------------------------
+struct DotArgs {
+  int nv;
+  int64_t n;
+  const double* a[4];
+  const double* b[4];
+  const double* da[4];
+  const double* db[4];
+  int sa[4], sb[4];   // slot indices of the step lengths for da / db (-1 = none)
+  int out[4];
+  double* sc;
+  double* part;
+  unsigned int* counter;
+  int post;           // post-processing of the slots on the last block
+  double post_a;
+};
+
+enum DotPost { DP_NONE = 0, DP_MUAFF = 1 };
+
+__global__ void __launch_bounds__(256) dots_kernel(const DotArgs D) {
+  double v[4] = {0, 0, 0, 0};
+  double al[4], bl[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    al[k] = (k < D.nv && D.sa[k] >= 0) ? D.sc[D.sa[k]] : 0.0;
+    bl[k] = (k < D.nv && D.sb[k] >= 0) ? D.sc[D.sb[k]] : 0.0;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < D.n; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < D.nv) {
+        double x = D.a[k][i];
+        if (D.da[k]) x += al[k] * D.da[k][i];
+        double y = x;
+        if (D.b[k]) {
+          y = D.b[k][i];
+          if (D.db[k]) y += bl[k] * D.db[k][i];
+        }
+        v[k] = fma(x, y, v[k]);
+      }
+    }
+  }
+  block_sum_to_part<4>(v, D.part, gridDim.x);
+  if (last_block_arrive(D.counter) && threadIdx.x == 0) {
+    for (int k = 0; k < D.nv; ++k) D.sc[D.out[k]] = ordered_sum(D.part + (size_t)k * gridDim.x, gridDim.x);
+    *D.counter = 0u;
+    if (D.post == DP_MUAFF) {
+      // mu_aff = (x + ap dx)^T (z + ad dz) / n_total ; mu~ = mu_aff^3 / mu^2
+      const double muaff = D.sc[D.out[0]] / D.post_a;
+      const double mu = D.sc[S_MUCUR];
+      D.sc[S_MUAFF] = muaff;
+      D.sc[S_MUT] = muaff * muaff * muaff / (mu * mu);
+    }
+  }
+}
+
+static int reduce_grid(nys_ctx* ctx, int64_t n) {
+  int g = (int)((n + 1023) / 1024);
+  if (g < 1) g = 1;
+  if (g > 2 * ctx->num_sms) g = 2 * ctx->num_sms;
+  return g;
+}
+
+int launch_dots(nys_ctx* ctx, int64_t n, int nv, const double* const* a, const double* const* b, const int* out,
+                int counter_slot) {
+  DotArgs D{};
+  D.nv = nv; D.n = n;
+  for (int k = 0; k < 4; ++k) { D.sa[k] = -1; D.sb[k] = -1; }
+  for (int k = 0; k < nv; ++k) { D.a[k] = a[k]; D.b[k] = b ? b[k] : nullptr; D.out[k] = out[k]; }
+  D.sc = ctx->sc;
+  const int g = reduce_grid(ctx, n);
+  D.part = ctx->wsd("dot_part", (size_t)4 * g);
+  D.counter = ctx->counters + counter_slot;
+  D.post = DP_NONE;
+  dots_kernel<<<g, 256, 0, ctx->stream>>>(D);
+  ctx->launches++;
+  return ctx->check_launch("dots");
+}
+
+int launch_muaff(nys_ctx* ctx, int64_t n, const double* x, const double* dx, const double* z, const double* dz,
+                 double n_total, int counter_slot) {
+  DotArgs D{};
+  D.nv = 1; D.n = n;
+  for (int k = 0; k < 4; ++k) { D.sa[k] = -1; D.sb[k] = -1; }
+  D.a[0] = x; D.da[0] = dx; D.sa[0] = S_AP;
+  D.b[0] = z; D.db[0] = dz; D.sb[0] = S_AD;
+  D.out[0] = S_TMP7;
+  D.sc = ctx->sc;
+  const int g = reduce_grid(ctx, n);
+  D.part = ctx->wsd("dot_part", (size_t)4 * g);
+  D.counter = ctx->counters + counter_slot;
+  D.post = ctx->world > 1 ? DP_NONE : DP_MUAFF;
+  D.post_a = n_total;
+  dots_kernel<<<g, 256, 0, ctx->stream>>>(D);
+  ctx->launches++;
+  return ctx->check_launch("muaff");
+}
+
+__global__ void muaff_post_kernel(double* sc, double n_total) {
+  const double muaff = sc[S_TMP7] / n_total;
+  const double mu = sc[S_MUCUR];
+  sc[S_MUAFF] = muaff;
+  sc[S_MUT] = muaff * muaff * muaff / (mu * mu);
+}
+int launch_muaff_post(nys_ctx* ctx, double n_total) {
+  muaff_post_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc, n_total);
+  ctx->launches++;
+  return ctx->check_launch("muaff_post");
+}
+
+// ------------------------------------------------------------------------------------------
+// ratio test: min over dv_i < 0 of -v_i / dv_i for two pairs -> raw minima in
+// slots (S_TMP0, S_TMP1); alpha = 0.995 min(1, .) applied by steps_post (after a possible
+// cross-rank min).  Optionally forms dv = dv1 + dv2 on the fly and stores it.
+// ------------------------------------------------------------------------------------------
+struct RatioArgs {
+  int64_t n;
+  const double* x;
+  double* dx;
+  const double* dx1;
+  const double* dx2;
+  const double* z;
+  double* dz;
+  const double* dz1;
+  const double* dz2;
+  double* sc;
+  double* part;
+  unsigned int* counter;
+};
+
+__global__ void __launch_bounds__(256) ratio_kernel(const RatioArgs R) {
+  double mp = 1.0e300, md = 1.0e300;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R.n; i += (int64_t)gridDim.x * blockDim.x) {
+    double dx, dz;
+    if (R.dx1) { dx = R.dx1[i] + R.dx2[i]; R.dx[i] = dx; } else dx = R.dx[i];
+    if (R.dz1) { dz = R.dz1[i] + R.dz2[i]; R.dz[i] = dz; } else dz = R.dz[i];
+    if (dx < 0.0) mp = fmin(mp, -R.x[i] / dx);
+    if (dz < 0.0) md = fmin(md, -R.z[i] / dz);
+  }
+  __shared__ double sh[2][32];
+  mp = warp_min(mp);
+  md = warp_min(md);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { sh[0][w] = mp; sh[1][w] = md; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 1.0e300, b = 1.0e300;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { a = fmin(a, sh[0][i]); b = fmin(b, sh[1][i]); }
+    R.part[blockIdx.x] = a;
+    R.part[gridDim.x + blockIdx.x] = b;
+  }
+  if (last_block_arrive(R.counter) && threadIdx.x == 0) {
+    double a = 1.0e300, b = 1.0e300;
+    for (unsigned i = 0; i < gridDim.x; ++i) {
+      a = fmin(a, ((volatile double*)R.part)[i]);
+      b = fmin(b, ((volatile double*)R.part)[gridDim.x + i]);
+    }
+    *R.counter = 0u;
+    R.sc[S_TMP0] = a;
+    R.sc[S_TMP1] = b;
+  }
+}
+
+__global__ void steps_post_kernel(double* sc) {
+  sc[S_AP] = 0.995 * fmin(1.0, sc[S_TMP0]);
+  sc[S_AD] = 0.995 * fmin(1.0, sc[S_TMP1]);
+}
+
+int launch_ratio(nys_ctx* ctx, int64_t n, const double* x, double* dx, const double* dx1, const double* dx2,
+                 const double* z, double* dz, const double* dz1, const double* dz2, int counter_slot) {
+  RatioArgs R{};
+  R.n = n; R.x = x; R.dx = dx; R.dx1 = dx1; R.dx2 = dx2; R.z = z; R.dz = dz; R.dz1 = dz1; R.dz2 = dz2;
+  R.sc = ctx->sc;
+  const int g = reduce_grid(ctx, n);
+  R.part = ctx->wsd("ratio_part", (size_t)2 * g);
+  R.counter = ctx->counters + counter_slot;
+  ratio_kernel<<<g, 256, 0, ctx->stream>>>(R);
+  ctx->launches++;
+  return ctx->check_launch("ratio");
+}
+int launch_steps_post(nys_ctx* ctx) {
+  steps_post_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc);
+  ctx->launches++;
+  return ctx->check_launch("steps_post");
+}
+
+// ------------------------------------------------------------------------------------------
+// PCG kernels
+// ------------------------------------------------------------------------------------------
+// update: (init) x = 0, r = rhs  |  (iter) x += alpha p, r -= alpha w ;
+//         rr = r^T r ; g = U^T r ; last block: convergence, h = s o g  (P^{-1} coefficients)
+struct PcgUpdArgs {
+  int init;
+  int64_t m;
+  double* x;
+  double* r;
+  const double* rhs;
+  const double* p;
+  const double* w;
+  const double* U;
+  int64_t ldu;
+  int ell;
+  const double* s;     // ell coefficients: (lam_l + mu)/(lam_i + mu) - 1
+  double* h;           // ell out
+  double* sc;
+  double* part;        // (1 + ell) x grid
+  unsigned int* counter;
+  int max_iter;
+  int64_t rows_per_block;
+};
+
+__global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
+  if (A.sc[S_DONE] != 0.0) return;
+  extern __shared__ double rsh[];  // rows_per_block
+  const int64_t i0 = blockIdx.x * A.rows_per_block;
+  int64_t i1 = i0 + A.rows_per_block;
+  if (i1 > A.m) i1 = A.m;
+  const double alpha = A.init ? 0.0 : A.sc[S_ALPHA];
+  double rr = 0.0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    double ri;
+    if (A.init) {
+      ri = A.rhs[i];
+      A.x[i] = 0.0;
+    } else {
+      A.x[i] = fma(alpha, A.p[i], A.x[i]);
+      ri = fma(-alpha, A.w[i], A.r[i]);
+    }
+    A.r[i] = ri;
+    rsh[i - i0] = ri;
+    rr = fma(ri, ri, rr);
+  }
+  double v[1] = {rr};
+  block_sum_to_part<1>(v, A.part, gridDim.x);
+  __syncthreads();
+  // g partials: warp per column
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = w; c < A.ell; c += nw) {
+    double acc = 0.0;
+    const double* Uc = A.U + (size_t)c * A.ldu;
+    for (int64_t i = i0 + l; i < i1; i += 32) acc = fma(Uc[i], rsh[i - i0], acc);
+    acc = warp_sum(acc);
+    if (l == 0) A.part[(size_t)(1 + c) * gridDim.x + blockIdx.x] = acc;
+  }
+  if (last_block_arrive(A.counter)) {
+    __shared__ int conv;
+    if (threadIdx.x == 0) {
+      const double rrt = ordered_sum(A.part, gridDim.x);
+      A.sc[S_RR] = rrt;
+      double iters = A.sc[S_ITERS];
+      if (!A.init) iters += 1.0;
+      A.sc[S_ITERS] = iters;
+      const double tol = A.sc[S_TOL];
+      int cv = (sqrt(rrt) <= tol) ? 1 : 0;
+      if (!isfinite(rrt)) { A.sc[S_STATUS] = (double)NYS_EBREAKDOWN; cv = 1; }
+      if (cv || iters >= (double)A.max_iter) A.sc[S_DONE] = 1.0;
+      if (A.ell == 0 && !cv) {  // P = I: z = r, rz_new = rr
+        const double rzold = A.sc[S_RZ];
+        A.sc[S_BETA] = A.init ? 0.0 : rrt / rzold;
+        A.sc[S_RZ] = rrt;
+      }
+      conv = cv;
+      *A.counter = 0u;
+    }
+    __syncthreads();
+    if (!conv) {
+      for (int c = threadIdx.x; c < A.ell; c += blockDim.x) A.h[c] = A.s[c] * ordered_sum(A.part + (size_t)(1 + c) * gridDim.x, gridDim.x);
+    }
+  }
+}
+
+// precond: z = r + U h  (= P^{-1} r, P:418 rewritten as v + U((lam_l+mu)/(Lam+mu) - 1) U^T v);
+//          rz = r^T z ; last block: beta = rz_new / rz_old
+struct PcgPrecArgs {
+  int init;
+  int64_t m;
+  const double* r;
+  double* z;
+  const double* U;
+  int64_t ldu;
+  int ell;
+  const double* h;
+  double* sc;
+  double* part;
+  unsigned int* counter;
+};
+
+__global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
+  if (A.sc[S_DONE] != 0.0) return;
+  extern __shared__ double hsh[];
+  for (int c = threadIdx.x; c < A.ell; c += blockDim.x) hsh[c] = A.h[c];
+  __syncthreads();
+  double rz = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.m; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < A.ell; ++c) acc = fma(A.U[(size_t)c * A.ldu + i], hsh[c], acc);
+    const double ri = A.r[i];
+    const double zi = ri + acc;
+    A.z[i] = zi;
+    rz = fma(ri, zi, rz);
+  }
+  double v[1] = {rz};
+  block_sum_to_part<1>(v, A.part, gridDim.x);
+  if (last_block_arrive(A.counter) && threadIdx.x == 0) {
+    const double rzn = ordered_sum(A.part, gridDim.x);
+    const double rzo = A.sc[S_RZ];
+    A.sc[S_BETA] = A.init ? 0.0 : rzn / rzo;
+    A.sc[S_RZ] = rzn;
+    if (!(rzn > 0.0) || !isfinite(rzn)) { A.sc[S_STATUS] = (double)NYS_EBREAKDOWN; A.sc[S_DONE] = 1.0; }
+    *A.counter = 0u;
+  }
+}
+
+int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, const double* rhs, const double* p,
+                      const double* w, const double* U, int64_t ldu, int ell, const double* s, double* h,
+                      int max_iter) {
+  PcgUpdArgs A{};
+  A.init = init; A.m = m; A.x = x; A.r = r; A.rhs = rhs; A.p = p; A.w = w; A.U = U; A.ldu = ldu; A.ell = ell;
+  A.s = s; A.h = h; A.sc = ctx->sc; A.max_iter = max_iter;
+  int64_t rpb = 256;
+  int64_t g = (m + rpb - 1) / rpb;
+  if (g > ctx->num_sms) { g = ctx->num_sms; rpb = (m + g - 1) / g; }
+  A.rows_per_block = rpb;
+  A.part = ctx->wsd("pcg_upd_part", (size_t)(1 + ell) * g);
+  A.counter = ctx->counters + 1;
+  pcg_update_kernel<<<(unsigned)g, 256, rpb * sizeof(double), ctx->stream>>>(A);
+  ctx->launches++;
+  return ctx->check_launch("pcg_update");
+}
+
+int launch_pcg_precond(nys_ctx* ctx, int init, int64_t m, const double* r, double* z, const double* U, int64_t ldu,
+                       int ell, const double* h) {
+  PcgPrecArgs A{};
+  A.init = init; A.m = m; A.r = r; A.z = z; A.U = U; A.ldu = ldu; A.ell = ell; A.h = h; A.sc = ctx->sc;
+  int g = (int)((m + 255) / 256);
+  if (g > ctx->num_sms) g = ctx->num_sms;
+  A.part = ctx->wsd("pcg_prec_part", (size_t)g);
+  A.counter = ctx->counters + 2;
+  pcg_precond_kernel<<<g, 256, (size_t)(ell > 0 ? ell : 1) * sizeof(double), ctx->stream>>>(A);
+  ctx->launches++;
+  return ctx->check_launch("pcg_precond");
+}
+
+// s_i = (lam_l + mu) / (lam_i + mu) - 1
+__global__ void prec_coef_kernel(const double* lam, int ell, double mu, double* s) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ell) s[i] = (lam[ell - 1] + mu) / (lam[i] + mu) - 1.0;
+}
+int launch_prec_coef(nys_ctx* ctx, const double* lam, int ell, double mu, double* s) {
+  if (ell <= 0) return NYS_OK;
+  prec_coef_kernel<<<(ell + 127) / 128, 128, 0, ctx->stream>>>(lam, ell, mu, s);
+  ctx->launches++;
+  return ctx->check_launch("prec_coef");
+}
+
+// PCG tolerance (A8'): tau = max(floor (1+|b|), min(0.1 |xi|, c mu (1+|b|))) from device scalars
+__global__ void pcg_setup_kernel(double* sc, int mode, double tol_abs, double c, double floor_, int xi_slot,
+                                 int b_slot, int mu_slot, double init_rel) {
+  double tol;
+  if (mode == 0) {
+    tol = tol_abs;
+  } else if (mode == 1) {
+    const double xin = sqrt(sc[xi_slot]);
+    const double bn = sqrt(sc[b_slot]);
+    const double mu = sc[mu_slot];
+    tol = fmax(floor_ * (1.0 + bn), fmin(0.1 * xin, c * mu * (1.0 + bn)));
+  } else {  // initial point: init_rel * |rhs|
+    tol = init_rel * sqrt(sc[xi_slot]);
+  }
+  sc[S_TOL] = tol;
+  sc[S_DONE] = 0.0;
+  sc[S_ITERS] = 0.0;
+  sc[S_STATUS] = 0.0;
+  sc[S_RZ] = 0.0;
+  sc[S_BETA] = 0.0;
+  sc[S_ALPHA] = 0.0;
+}
+int launch_pcg_setup(nys_ctx* ctx, int mode, double tol_abs, double c, double floor_, int xi_slot, int b_slot,
+                     int mu_slot, double init_rel) {
+  pcg_setup_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc, mode, tol_abs, c, floor_, xi_slot, b_slot, mu_slot, init_rel);
+  ctx->launches++;
+  return ctx->check_launch("pcg_setup");
+}
+
+// ------------------------------------------------------------------------------------------
+// IPM elementwise kernels (Alg. 4 / Alg. 5 for I-only variables)
+// ------------------------------------------------------------------------------------------
+// d_j = 1 / (q_j + z_j / x_j + rho)
+__global__ void scaling_kernel(int64_t n, const double* q, const double* x, const double* z, double rho, double* d) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    d[j] = 1.0 / (q[j] + z[j] / x[j] + rho);
+}
+
+// predictor: r_d = c + q x - A^T y - z + rho (x - zeta) [aty = A^T y given];
+// r_xz = -x z ; xi_au = -r_xz / x (= z) ; t = d (r_d + xi_au)
+__global__ void pred_rhs_n_kernel(int64_t n, const double* c, const double* q, const double* x, const double* z,
+                                  const double* zeta, const double* aty, double rho, const double* d, double* rd,
+                                  double* rxz, double* xiau, double* t) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double xj = x[j], zj = z[j];
+    const double r = c[j] + q[j] * xj - aty[j] - zj + rho * (xj - zeta[j]);
+    const double rx = -xj * zj;
+    const double xa = -rx / xj;
+    rd[j] = r;
+    rxz[j] = rx;
+    xiau[j] = xa;
+    t[j] = d[j] * (r + xa);
+  }
+}
+// r_p = b - A x - delta (y - lambda) [ax = A x given]
+__global__ void pred_rhs_m_kernel(int64_t m, const double* b, const double* ax, const double* y, const double* lam,
+                                  double delta, double* rp) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    rp[i] = b[i] - ax[i] - delta * (y[i] - lam[i]);
+}
+// corrector: r_d = r_p = 0 ; r_xz = mu~ - dxp dzp ; xi_au = -r_xz / x ; t = d xi_au
+__global__ void corr_rhs_kernel(int64_t n, const double* x, const double* dxp, const double* dzp, const double* sc,
+                                const double* d, double* rxz, double* xiau, double* t) {
+  const double mut = sc[S_MUT];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double rx = mut - dxp[j] * dzp[j];
+    const double xa = -rx / x[j];
+    rxz[j] = rx;
+    xiau[j] = xa;
+    t[j] = d[j] * xa;
+  }
+}
+// iterate update: x += ap dx ; z += ad dz   (n-space)  and  y += ad dy (m-space)
+__global__ void update_n_kernel(int64_t n, double* x, const double* dx, double* z, const double* dz, const double* sc) {
+  const double ap = sc[S_AP], ad = sc[S_AD];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    x[j] = fma(ap, dx[j], x[j]);
+    z[j] = fma(ad, dz[j], z[j]);
+  }
+}
+__global__ void update_m_kernel(int64_t m, double* y, const double* dy1, const double* dy2, const double* sc) {
+  const double ad = sc[S_AD];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(ad, dy1[i] + dy2[i], y[i]);
+}
+// r = b - ax  (m) ;  generic axpby: out = a*u + b*v
+__global__ void axpby_kernel(int64_t n, double a, const double* u, double b, const double* v, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a * u[i] + (v ? b * v[i] : 0.0);
+}
+// out = u o v
+__global__ void mul_kernel(int64_t n, const double* u, const double* v, double* out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = u[j] * v[j];
+}
+// t = c + q o x  (initial point rhs) ; shift: out = u + s (scalar)
+__global__ void cpqx_kernel(int64_t n, const double* c, const double* q, const double* x, double* t) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    t[j] = c[j] + q[j] * x[j];
+}
+__global__ void shift_kernel(int64_t n, double* u, double s) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    u[j] += s;
+}
+// min of a vector (raw) -> slot ; sums -> slot : generic "minsum"
+__global__ void __launch_bounds__(256) minsum_kernel(int64_t n, const double* u, double shift, double* sc, int min_slot,
+                                                     int sum_slot, double* part, unsigned int* counter) {
+  double mn = 1.0e300, sm = 0.0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double v = u[j];
+    mn = fmin(mn, v);
+    sm += v + shift;
+  }
+  __shared__ double sh[2][32];
+  mn = warp_min(mn);
+  sm = warp_sum(sm);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { sh[0][w] = mn; sh[1][w] = sm; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 1.0e300, b = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { a = fmin(a, sh[0][i]); b += sh[1][i]; }
+    part[blockIdx.x] = a;
+    part[gridDim.x + blockIdx.x] = b;
+  }
+  if (last_block_arrive(counter) && threadIdx.x == 0) {
+    double a = 1.0e300, b = 0.0;
+    for (unsigned i = 0; i < gridDim.x; ++i) {
+      a = fmin(a, ((volatile double*)part)[i]);
+      b += ((volatile double*)part)[gridDim.x + i];
+    }
+    *counter = 0u;
+    if (min_slot >= 0) sc[min_slot] = a;
+    if (sum_slot >= 0) sc[sum_slot] = b;
+  }
+}
+
+static int ew_grid(nys_ctx* ctx, int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g < 1) g = 1;
+  if (g > 4 * ctx->num_sms) g = 4 * ctx->num_sms;
+  return (int)g;
+}
+
+int launch_scaling(nys_ctx* ctx, int64_t n, const double* q, const double* x, const double* z, double rho, double* d) {
+  if (n <= 0) return NYS_OK;
+  scaling_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, q, x, z, rho, d);
+  ctx->launches++;
+  return ctx->check_launch("scaling");
+}
+int launch_pred_rhs_n(nys_ctx* ctx, int64_t n, const double* c, const double* q, const double* x, const double* z,
+                      const double* zeta, const double* aty, double rho, const double* d, double* rd, double* rxz,
+                      double* xiau, double* t) {
+  if (n <= 0) return NYS_OK;
+  pred_rhs_n_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, c, q, x, z, zeta, aty, rho, d, rd, rxz, xiau, t);
+  ctx->launches++;
+  return ctx->check_launch("pred_rhs_n");
+}
+int launch_pred_rhs_m(nys_ctx* ctx, int64_t m, const double* b, const double* ax, const double* y, const double* lam,
+                      double delta, double* rp) {
+  pred_rhs_m_kernel<<<ew_grid(ctx, m), 256, 0, ctx->stream>>>(m, b, ax, y, lam, delta, rp);
+  ctx->launches++;
+  return ctx->check_launch("pred_rhs_m");
+}
+int launch_corr_rhs(nys_ctx* ctx, int64_t n, const double* x, const double* dxp, const double* dzp, const double* d,
+                    double* rxz, double* xiau, double* t) {
+  if (n <= 0) return NYS_OK;
+  corr_rhs_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, x, dxp, dzp, ctx->sc, d, rxz, xiau, t);
+  ctx->launches++;
+  return ctx->check_launch("corr_rhs");
+}
+int launch_update_n(nys_ctx* ctx, int64_t n, double* x, const double* dx, double* z, const double* dz) {
+  if (n <= 0) return NYS_OK;
+  update_n_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, x, dx, z, dz, ctx->sc);
+  ctx->launches++;
+  return ctx->check_launch("update_n");
+}
+int launch_update_m(nys_ctx* ctx, int64_t m, double* y, const double* dy1, const double* dy2) {
+  update_m_kernel<<<ew_grid(ctx, m), 256, 0, ctx->stream>>>(m, y, dy1, dy2, ctx->sc);
+  ctx->launches++;
+  return ctx->check_launch("update_m");
+}
+int launch_axpby(nys_ctx* ctx, int64_t n, double a, const double* u, double b, const double* v, double* out) {
+  if (n <= 0) return NYS_OK;
+  axpby_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, a, u, b, v, out);
+  ctx->launches++;
+  return ctx->check_launch("axpby");
+}
+int launch_mul(nys_ctx* ctx, int64_t n, const double* u, const double* v, double* out) {
+  if (n <= 0) return NYS_OK;
+  mul_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, u, v, out);
+  ctx->launches++;
+  return ctx->check_launch("mul");
+}
+int launch_cpqx(nys_ctx* ctx, int64_t n, const double* c, const double* q, const double* x, double* t) {
+  if (n <= 0) return NYS_OK;
+  cpqx_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, c, q, x, t);
+  ctx->launches++;
+  return ctx->check_launch("cpqx");
+}
+int launch_shift(nys_ctx* ctx, int64_t n, double* u, double s) {
+  if (n <= 0) return NYS_OK;
+  shift_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, u, s);
+  ctx->launches++;
+  return ctx->check_launch("shift");
+}
+int launch_minsum(nys_ctx* ctx, int64_t n, const double* u, double shift, int min_slot, int sum_slot, int counter_slot) {
+  const int g = reduce_grid(ctx, n);
+  double* part = ctx->wsd("minsum_part", (size_t)2 * g);
+  minsum_kernel<<<g, 256, 0, ctx->stream>>>(n, u, shift, ctx->sc, min_slot, sum_slot, part, ctx->counters + counter_slot);
+  ctx->launches++;
+  return ctx->check_launch("minsum");
+}
+
+// positivity check of d (nys_check_scaling): first bad index -> slot
+__global__ void check_pos_kernel(int64_t n, const double* d, unsigned long long* bad) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double v = d[j];
+    if (!(v > 0.0) || !isfinite(v)) atomicMin(bad, (unsigned long long)j);
+  }
+}
+int launch_check_pos(nys_ctx* ctx, int64_t n, const double* d, unsigned long long* bad) {
+  if (n <= 0) return NYS_OK;
+  check_pos_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, d, bad);
+  ctx->launches++;
+  return ctx->check_launch("check_pos");
+}
+
+// set scalar slots from host values (one tiny kernel, stream ordered)
+__global__ void set_slots_kernel(double* sc, int k0, double v0, int k1, double v1, int k2, double v2) {
+  if (k0 >= 0) sc[k0] = v0;
+  if (k1 >= 0) sc[k1] = v1;
+  if (k2 >= 0) sc[k2] = v2;
+}
+int launch_set_slots(nys_ctx* ctx, int k0, double v0, int k1, double v1, int k2, double v2) {
+  set_slots_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc, k0, v0, k1, v1, k2, v2);
+  ctx->launches++;
+  return ctx->check_launch("set_slots");
+}
+
+}  // namespace nys

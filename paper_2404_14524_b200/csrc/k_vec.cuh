@@ -1,0 +1,73 @@
+// launchers of k_vec.cu, k_gemm.cu and k_small.cu (internal)
+#pragma once
+#include "nys_common.cuh"
+
+namespace nys {
+// k_vec.cu
+int launch_gaussian(nys_ctx* ctx, double* O, int64_t total, uint64_t seed, uint64_t stream);
+int launch_dots(nys_ctx* ctx, int64_t n, int nv, const double* const* a, const double* const* b, const int* out,
+                int counter_slot);
+int launch_muaff(nys_ctx* ctx, int64_t n, const double* x, const double* dx, const double* z, const double* dz,
+                 double n_total, int counter_slot);
+int launch_muaff_post(nys_ctx* ctx, double n_total);
+int launch_ratio(nys_ctx* ctx, int64_t n, const double* x, double* dx, const double* dx1, const double* dx2,
+                 const double* z, double* dz, const double* dz1, const double* dz2, int counter_slot);
+int launch_steps_post(nys_ctx* ctx);
+int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, const double* rhs, const double* p,
+                      const double* w, const double* U, int64_t ldu, int ell, const double* s, double* h,
+                      int max_iter);
+int launch_pcg_precond(nys_ctx* ctx, int init, int64_t m, const double* r, double* z, const double* U, int64_t ldu,
+                       int ell, const double* h);
+int launch_prec_coef(nys_ctx* ctx, const double* lam, int ell, double mu, double* s);
+int launch_pcg_setup(nys_ctx* ctx, int mode, double tol_abs, double c, double floor_, int xi_slot, int b_slot,
+                     int mu_slot, double init_rel);
+int launch_scaling(nys_ctx* ctx, int64_t n, const double* q, const double* x, const double* z, double rho, double* d);
+int launch_pred_rhs_n(nys_ctx* ctx, int64_t n, const double* c, const double* q, const double* x, const double* z,
+                      const double* zeta, const double* aty, double rho, const double* d, double* rd, double* rxz,
+                      double* xiau, double* t);
+int launch_pred_rhs_m(nys_ctx* ctx, int64_t m, const double* b, const double* ax, const double* y, const double* lam,
+                      double delta, double* rp);
+int launch_corr_rhs(nys_ctx* ctx, int64_t n, const double* x, const double* dxp, const double* dzp, const double* d,
+                    double* rxz, double* xiau, double* t);
+int launch_update_n(nys_ctx* ctx, int64_t n, double* x, const double* dx, double* z, const double* dz);
+int launch_update_m(nys_ctx* ctx, int64_t m, double* y, const double* dy1, const double* dy2);
+int launch_axpby(nys_ctx* ctx, int64_t n, double a, const double* u, double b, const double* v, double* out);
+int launch_mul(nys_ctx* ctx, int64_t n, const double* u, const double* v, double* out);
+int launch_cpqx(nys_ctx* ctx, int64_t n, const double* c, const double* q, const double* x, double* t);
+int launch_shift(nys_ctx* ctx, int64_t n, double* u, double s);
+int launch_minsum(nys_ctx* ctx, int64_t n, const double* u, double shift, int min_slot, int sum_slot, int counter_slot);
+int launch_check_pos(nys_ctx* ctx, int64_t n, const double* d, unsigned long long* bad);
+int launch_set_slots(nys_ctx* ctx, int k0, double v0, int k1 = -1, double v1 = 0, int k2 = -1, double v2 = 0);
+
+// k_gemm.cu — fp64 DMMA GEMM  C(MxN, col-major) = Aop(MxK) * Bop(KxN)
+//   a_kmajor = true : Aop(i,k) = A[i*lda + k]      (e.g. A^T of a column-major matrix)
+//   a_kmajor = false: Aop(i,k) = A[i + k*lda]      (column-major)
+//   Bop(k,j) = B[k + j*ldb]                         (column-major, K contiguous)
+//   epilogue: C = row_scale o acc (+ add_scale * addv_i * addm(i,j))
+struct GemmCall {
+  int64_t M = 0, N = 0, K = 0;
+  const double* A = nullptr;
+  int64_t lda = 0;
+  bool a_kmajor = false;
+  const double* B = nullptr;
+  int64_t ldb = 0;
+  double* C = nullptr;
+  int64_t ldc = 0;
+  const double* row_scale = nullptr;  // length M or null
+  const double* addv = nullptr;       // C(i,j) += addv[i] * addm[i + j*ldadd]
+  const double* addm = nullptr;
+  int64_t ldadd = 0;
+  int splits = 0;                     // 0 = auto
+};
+int launch_gemm(nys_ctx* ctx, const GemmCall& g);
+
+// k_small.cu — ell x ell dense routines (single CTA) and sketch helpers
+int launch_fro_nu(nys_ctx* ctx, int64_t m, int ell, const double* Y, int64_t ldy, int retry_scale_slot);
+int launch_add_eomega(nys_ctx* ctx, int64_t m, int ell, const double* e, const double* Om, double* Y, int64_t ld);
+int launch_ynu(nys_ctx* ctx, int64_t m, int ell, const double* Y, const double* Om, double* Ynu, int64_t ld);
+int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int ldr, int shift_mode);
+int launch_trmm_upper(nys_ctx* ctx, int ell, int ld, const double* R1, const double* R2, double* Out);  // R1 * R2
+int launch_jacobi_svd(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma);
+int launch_lambda_from_sigma(nys_ctx* ctx, int ell, const double* sigma, double* lam);
+int launch_orth_err(nys_ctx* ctx, int64_t m, int ell, const double* U, int64_t ldu, int slot);
+}  // namespace nys

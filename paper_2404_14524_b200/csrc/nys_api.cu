@@ -1,0 +1,984 @@
+// C ABI of libnysipm.so (include/nysipm.h) and the host-side drivers:
+//   * sketch_impl  — Alg. 1 on the device
+//   * pcg_impl     — PCG with device-resident scalars; the host only polls the
+//                    convergence flag once per batch of iterations
+//   * ipm_impl     — Alg. 3 / 4 / 5 + App. B for x >= 0
+// Multi-GPU: A is column-sharded, m-space objects are replicated; the only exchanges are
+// NCCL all-reduces of m-vectors (matvec partials), the m x l sketch, and a few scalars.
+#include <dlfcn.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "k_vec.cuh"
+#include "nccl.h"
+
+using namespace nys;
+
+namespace {
+struct NysException {
+  int code;
+};
+}  // namespace
+
+void* nys_ctx::ws(const char* name, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  auto it = bufs.find(name);
+  if (it != bufs.end() && it->second.second >= bytes) return it->second.first;
+  if (it != bufs.end()) {
+    cudaFree(it->second.first);
+    bufs.erase(it);
+  }
+  void* p = nullptr;
+  size_t alloc = bytes < 256 ? 256 : bytes;
+  cudaError_t e = cudaMalloc(&p, alloc);
+  if (e != cudaSuccess) {
+    last_error = std::string("workspace '") + name + "': " + cudaGetErrorString(e);
+    cudaGetLastError();
+    throw NysException{NYS_ENOMEM};
+  }
+  bufs[name] = {p, alloc};
+  return p;
+}
+
+int nys_ctx::check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return NYS_ECUDA;
+  }
+  return NYS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// NCCL (dlopen'ed only for world > 1)
+// ------------------------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) { err = "dlopen(libnccl.so.2) failed"; return false; }
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+    getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+    if (!commInitRank || !allReduce || !commDestroy) { err = "NCCL symbols missing"; return false; }
+    return true;
+  }
+};
+NcclApi g_nccl;
+
+int allreduce(nys_ctx* ctx, double* buf, size_t count, bool is_min = false) {
+  if (ctx->world <= 1 || count == 0) return NYS_OK;
+  ncclResult_t r = g_nccl.allReduce(buf, buf, count, ncclFloat64, is_min ? ncclMin : ncclSum,
+                                    (ncclComm_t)ctx->nccl_comm, ctx->stream);
+  if (r != ncclSuccess) {
+    ctx->set_error(std::string("ncclAllReduce: ") + (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?"));
+    return NYS_ENCCL;
+  }
+  return NYS_OK;
+}
+int allreduce_slots(nys_ctx* ctx, int first, int count, bool is_min = false) {
+  return allreduce(ctx, ctx->sc + first, (size_t)count, is_min);
+}
+
+inline int64_t even(int64_t v) { return (v + 1) & ~int64_t(1); }
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+int read_slots(nys_ctx* ctx) {
+  NYS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_sc, ctx->sc, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return NYS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// normal operator (A, d, e, delta) applied to p with the PCG epilogue (or plain)
+// ------------------------------------------------------------------------------------------
+struct NormalOp {
+  int64_t m, n, lda;
+  const double* A;
+  const double* d;
+  const double* e;
+  double delta;
+};
+
+// w = N_delta v  where v = z + beta*p (beta slot / p may be null); p_out receives v.
+// world > 1: local partial sum, all-reduce, then the replicated terms (+ PCG dot) are added
+// by launch_finalize_terms (apply_normal_full).
+int apply_normal(nys_ctx* ctx, const NormalOp& op, const double* z, const double* p, const double* beta,
+                 double* p_out, double* w, bool pcg_alpha, const double* done) {
+  MatvecCall c;
+  c.mode = MV_FUSED;
+  c.m = op.m; c.n = op.n; c.lda = op.lda; c.A = op.A;
+  c.z = z; c.p = p; c.beta = beta; c.p_out = p_out; c.d = op.d; c.done = done;
+  c.out = w;
+  if (ctx->world == 1) {
+    c.use_delta = true; c.delta = op.delta; c.e = op.e; c.pcg_alpha = pcg_alpha;
+    return launch_matvec(ctx, c);
+  }
+  c.use_delta = false; c.pcg_alpha = false;
+  NYS_TRY(launch_matvec(ctx, c));
+  return allreduce(ctx, w, (size_t)op.m);
+}
+}  // namespace
+
+namespace nys {
+int launch_finalize_terms(nys_ctx* ctx, int64_t m, double* w, const double* v, double delta, const double* e,
+                          bool pcg_alpha, const double* done);
+}
+
+namespace {
+int apply_normal_full(nys_ctx* ctx, const NormalOp& op, const double* z, const double* p, const double* beta,
+                      double* p_out, double* w, bool pcg_alpha, const double* done) {
+  NYS_TRY(apply_normal(ctx, op, z, p, beta, p_out, w, pcg_alpha, done));
+  if (ctx->world > 1) {
+    const double* v = p_out ? p_out : z;
+    NYS_TRY(launch_finalize_terms(ctx, op.m, w, v, op.delta, op.e, pcg_alpha, done));
+  }
+  return NYS_OK;
+}
+
+// y = sgn * A u (+ add)   (N-only pass, summed over ranks)
+int apply_A(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* u, double* out,
+            double sgn, const double* add) {
+  MatvecCall c;
+  c.mode = MV_NONLY;
+  c.m = m; c.n = n; c.lda = lda; c.A = A; c.u = u; c.out = out; c.sgn = sgn;
+  if (ctx->world == 1) {
+    c.add = add;
+    return launch_matvec(ctx, c);
+  }
+  c.add = nullptr;
+  NYS_TRY(launch_matvec(ctx, c));
+  NYS_TRY(allreduce(ctx, out, (size_t)m));
+  if (add) NYS_TRY(launch_axpby(ctx, m, 1.0, out, 1.0, add, out));
+  return NYS_OK;
+}
+
+// T-only pass with an epilogue (local columns only: no exchange needed)
+int apply_At(nys_ctx* ctx, const MatvecCall& c) { return launch_matvec(ctx, c); }
+
+// ------------------------------------------------------------------------------------------
+// Alg. 1: Nystrom factors from the sketch Y (m x l, ld mp) and Omega (ld mp)
+// ------------------------------------------------------------------------------------------
+int nystrom_factor(nys_ctx* ctx, int64_t m, int ell, const double* Y, const double* Om, int64_t mp, double* U,
+                   double* lam, nys_sketch_info* info) {
+  const int ldl = (int)even(ell);
+  double* Ynu = ctx->wsd("nf_Ynu", (size_t)mp * ell);
+  double* Bm = ctx->wsd("nf_B", (size_t)mp * ell);
+  double* Qm = ctx->wsd("nf_Q", (size_t)mp * ell);
+  double* G = ctx->wsd("nf_G", (size_t)ldl * ell);
+  double* Gi = ctx->wsd("nf_Gi", (size_t)ldl * ell);
+  double* R1 = ctx->wsd("nf_R1", (size_t)ldl * ell);
+  double* R2 = ctx->wsd("nf_R2", (size_t)ldl * ell);
+  double* R3 = ctx->wsd("nf_R3", (size_t)ldl * ell);
+  double* Rt = ctx->wsd("nf_Rt", (size_t)ldl * ell);
+  double* W = ctx->wsd("nf_W", (size_t)ldl * ell);
+  double* sig = ctx->wsd("nf_sig", (size_t)ell);
+
+  NYS_TRY(launch_fro_nu(ctx, m, ell, Y, mp, 0));                      // line 3
+  int retries = 0;
+  for (;;) {
+    NYS_TRY(launch_ynu(ctx, m, ell, Y, Om, Ynu, mp));                 // line 4
+    GemmCall g;                                                        // Omega^T Y_nu
+    g.M = ell; g.N = ell; g.K = m; g.A = Om; g.lda = mp; g.a_kmajor = true; g.B = Ynu; g.ldb = mp; g.C = G; g.ldc = ldl;
+    NYS_TRY(launch_gemm(ctx, g));
+    NYS_TRY(launch_set_slots(ctx, S_CHOLFAIL, 0.0));
+    NYS_TRY(launch_chol_inv(ctx, ell, G, ldl, Gi, ldl, 0));           // line 5: C (in G), C^{-1}
+    NYS_TRY(read_slots(ctx));
+    if (ctx->h_sc[S_CHOLFAIL] == 0.0) break;
+    if (retries >= 3) {
+      ctx->set_error("nys_sketch: Omega^T Y_nu not positive definite after 3 retries");
+      return NYS_ECHOL;
+    }
+    ++retries;
+    NYS_TRY(launch_set_slots(ctx, S_NU, ctx->h_sc[S_NU] * 10.0));     // A4
+  }
+  {                                                                    // line 6: B = Y_nu C^{-1}
+    GemmCall g;
+    g.M = m; g.N = ell; g.K = ell; g.A = Ynu; g.lda = mp; g.a_kmajor = false; g.B = Gi; g.ldb = ldl; g.C = Bm; g.ldc = mp;
+    NYS_TRY(launch_gemm(ctx, g));
+  }
+  // line 7: thin SVD of B.  Shifted CholeskyQR3 (B = Q R), then one-sided Jacobi on R.
+  NYS_TRY(launch_set_slots(ctx, S_SHIFT, (double)m, S_CHOLFAIL, 0.0));
+  double* src = Bm;
+  double* dst = Qm;
+  double* Rs[3] = {R1, R2, R3};
+  for (int pass = 0; pass < 3; ++pass) {
+    GemmCall g;
+    g.M = ell; g.N = ell; g.K = m; g.A = src; g.lda = mp; g.a_kmajor = true; g.B = src; g.ldb = mp; g.C = Rs[pass]; g.ldc = ldl;
+    NYS_TRY(launch_gemm(ctx, g));
+    NYS_TRY(launch_chol_inv(ctx, ell, Rs[pass], ldl, Gi, ldl, pass == 0 ? 1 : 0));
+    GemmCall h;
+    h.M = m; h.N = ell; h.K = ell; h.A = src; h.lda = mp; h.a_kmajor = false; h.B = Gi; h.ldb = ldl; h.C = dst; h.ldc = mp;
+    NYS_TRY(launch_gemm(ctx, h));
+    double* tmp = src; src = dst; dst = tmp;
+  }
+  // src now holds Q; R = R3 R2 R1
+  NYS_TRY(launch_trmm_upper(ctx, ell, ldl, R2, R1, Rt));
+  NYS_TRY(launch_trmm_upper(ctx, ell, ldl, R3, Rt, G));
+  NYS_TRY(launch_jacobi_svd(ctx, ell, G, ldl, W, ldl, sig));
+  {                                                                    // U = Q W
+    GemmCall g;
+    g.M = m; g.N = ell; g.K = ell; g.A = src; g.lda = mp; g.a_kmajor = false; g.B = W; g.ldb = ldl; g.C = U; g.ldc = mp;
+    NYS_TRY(launch_gemm(ctx, g));
+  }
+  NYS_TRY(launch_lambda_from_sigma(ctx, ell, sig, lam));              // line 8
+  if (info) {
+    NYS_TRY(launch_orth_err(ctx, m, ell, U, mp, S_TMP6));
+    NYS_TRY(read_slots(ctx));
+    if (ctx->h_sc[S_CHOLFAIL] != 0.0) {
+      ctx->set_error("nys_sketch: CholeskyQR of B failed");
+      return NYS_ECHOL;
+    }
+    info->nu = ctx->h_sc[S_NU];
+    info->chol_retries = retries;
+    info->orth_err = ctx->h_sc[S_TMP6];
+  }
+  return NYS_OK;
+}
+
+// Y = A (d o (A^T Omega)) (+ e o Omega), summed over ranks   (Alg. 1 line 2)
+int sketch_Y(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
+             int ell, const double* Om, double* Y) {
+  const int64_t mp = even(m), np_ = even(n);
+  double* T = ctx->wsd("sk_T", (size_t)(np_ > 0 ? np_ : 2) * ell);
+  {
+    GemmCall g;  // T = diag(d) A^T Omega  (n x l)
+    g.M = n; g.N = ell; g.K = m; g.A = A; g.lda = lda; g.a_kmajor = true; g.B = Om; g.ldb = mp; g.C = T; g.ldc = np_;
+    g.row_scale = d;
+    NYS_TRY(launch_gemm(ctx, g));
+  }
+  {
+    GemmCall g;  // Y = A T (+ e o Omega)
+    g.M = m; g.N = ell; g.K = n; g.A = A; g.lda = lda; g.a_kmajor = false; g.B = T; g.ldb = np_; g.C = Y; g.ldc = mp;
+    if (ctx->world == 1 && e) { g.addv = e; g.addm = Om; g.ldadd = mp; }
+    if (n == 0) NYS_CUDA_TRY(ctx, cudaMemsetAsync(Y, 0, sizeof(double) * mp * ell, ctx->stream));
+    else NYS_TRY(launch_gemm(ctx, g));
+  }
+  if (ctx->world > 1) {
+    NYS_TRY(allreduce(ctx, Y, (size_t)mp * ell));
+    if (e) NYS_TRY(launch_add_eomega(ctx, m, ell, e, Om, Y, mp));
+  }
+  return NYS_OK;
+}
+
+// Alg. 1: sketch, then lines 3-8
+int sketch_impl(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
+                int ell, const double* Om, double* U, double* lam, nys_sketch_info* info) {
+  double* Y = ctx->wsd("sk_Y", (size_t)even(m) * ell);
+  NYS_TRY(sketch_Y(ctx, m, n, A, lda, d, e, ell, Om, Y));
+  return nystrom_factor(ctx, m, ell, Y, Om, even(m), U, lam, info);
+}
+
+// ------------------------------------------------------------------------------------------
+// PCG with device scalars (tolerance already in S_TOL via launch_pcg_setup)
+// ------------------------------------------------------------------------------------------
+struct PcgResult {
+  int iters = 0;
+  int status = 0;
+  double rr = 0.0;
+};
+
+int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t ldu, const double* s,
+             const double* rhs, double* x, int max_iter, PcgResult& res) {
+  const int64_t m = op.m;
+  const int64_t mp = even(m);
+  double* r = ctx->wsd("pcg_r", (size_t)mp);
+  double* z = ell > 0 ? ctx->wsd("pcg_z", (size_t)mp) : r;
+  double* P0 = ctx->wsd("pcg_p0", (size_t)mp);
+  double* P1 = ctx->wsd("pcg_p1", (size_t)mp);
+  double* w = ctx->wsd("pcg_w", (size_t)mp);
+  double* h = ctx->wsd("pcg_h", (size_t)(ell > 0 ? ell : 1));
+  double* Pp[2] = {P0, P1};
+  const double* done = ctx->sc + S_DONE;
+  NYS_TRY(launch_pcg_update(ctx, 1, m, x, r, rhs, nullptr, nullptr, U, ldu, ell, s, h, max_iter));
+  if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 1, m, r, z, U, ldu, ell, h));
+  int it = 0;
+  int batch = 4;
+  for (;;) {
+    for (int b = 0; b < batch; ++b, ++it) {
+      const double* pold = (it == 0) ? nullptr : Pp[it & 1];
+      double* pnew = Pp[(it + 1) & 1];
+      NYS_TRY(apply_normal_full(ctx, op, z, pold, ctx->sc + S_BETA, pnew, w, true, done));
+      NYS_TRY(launch_pcg_update(ctx, 0, m, x, r, nullptr, pnew, w, U, ldu, ell, s, h, max_iter));
+      if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 0, m, r, z, U, ldu, ell, h));
+    }
+    NYS_TRY(read_slots(ctx));
+    if (ctx->h_sc[S_DONE] != 0.0) break;
+    if (batch < 32) batch *= 2;
+  }
+  res.iters = (int)ctx->h_sc[S_ITERS];
+  res.status = (int)ctx->h_sc[S_STATUS];
+  res.rr = ctx->h_sc[S_RR];
+  return NYS_OK;
+}
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// finalize_terms for world > 1 (w := w + (delta + e) v ; optional pcg dot / alpha)
+// ------------------------------------------------------------------------------------------
+namespace nys {
+__global__ void finalize_terms_kernel(int64_t m, double* w, const double* v, double delta, const double* e, int pcg,
+                                      double* sc, double* part, unsigned int* counter, const double* done) {
+  if (done && *done != 0.0) return;
+  double dot = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const double s = w[i] + (delta + (e ? e[i] : 0.0)) * v[i];
+    w[i] = s;
+    dot = fma(v[i], s, dot);
+  }
+  if (!pcg) return;
+  __shared__ double sh[32];
+  __shared__ bool last;
+  dot = warp_sum(dot);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = dot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) b += sh[i];
+    part[blockIdx.x] = b;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double pw = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) pw += ((volatile double*)part)[b];
+    *counter = 0u;
+    sc[S_PW] = pw;
+    if (!(pw > 0.0) || !isfinite(pw)) { sc[S_STATUS] = (double)NYS_EBREAKDOWN; sc[S_DONE] = 1.0; sc[S_ALPHA] = 0.0; }
+    else sc[S_ALPHA] = sc[S_RZ] / pw;
+  }
+}
+int launch_finalize_terms(nys_ctx* ctx, int64_t m, double* w, const double* v, double delta, const double* e,
+                          bool pcg_alpha, const double* done) {
+  int g = (int)((m + 255) / 256);
+  if (g > 2 * ctx->num_sms) g = 2 * ctx->num_sms;
+  double* part = ctx->wsd("fin_part2", (size_t)g);
+  finalize_terms_kernel<<<g, 256, 0, ctx->stream>>>(m, w, v, delta, e, pcg_alpha ? 1 : 0, ctx->sc, part,
+                                                    ctx->counters + 4, done);
+  ctx->launches++;
+  return ctx->check_launch("finalize_terms");
+}
+}  // namespace nys
+
+// ------------------------------------------------------------------------------------------
+// Nys-IP-PMM driver
+// ------------------------------------------------------------------------------------------
+namespace {
+// Omega_k (m x l, column-major ld = m semantics of the generator) into a buffer with ld = even(m)
+int gen_omega(nys_ctx* ctx, int64_t m, int ell, uint64_t seed, uint64_t stream, double* Om) {
+  const int64_t mp = even(m);
+  if (mp == m) return launch_gaussian(ctx, Om, m * (int64_t)ell, seed, stream);
+  double* tmp = ctx->wsd("ipm_Omtmp", (size_t)m * ell);
+  NYS_TRY(launch_gaussian(ctx, tmp, m * (int64_t)ell, seed, stream));
+  NYS_CUDA_TRY(ctx, cudaMemcpy2DAsync(Om, mp * 8, tmp, m * 8, m * 8, ell, cudaMemcpyDeviceToDevice, ctx->stream));
+  return NYS_OK;
+}
+
+struct Dots {
+  nys_ctx* ctx;
+  int dot(int64_t n, const double* a, const double* b, int slot) {
+    const double* aa[1] = {a};
+    const double* bb[1] = {b};
+    int out[1] = {slot};
+    return launch_dots(ctx, n, 1, aa, bb, out, 5);
+  }
+};
+
+int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solution* sol, nys_report* rep) {
+  auto t_start = std::chrono::steady_clock::now();
+  const int64_t m = qp_in->m, n = qp_in->n;
+  const int64_t mp = even(m), np_ = even(n);
+  const int ell = opt->ell;
+  const int64_t launches0 = ctx->launches, matvecs0 = ctx->matvecs;
+  // ---- problem data on the device --------------------------------------------------------
+  const double *A = qp_in->A, *q = qp_in->q, *b = qp_in->b, *c = qp_in->c;
+  int64_t lda = qp_in->lda;
+  if (qp_in->host_ptrs) {
+    const int64_t ldd = even(m);
+    double* Ad = ctx->wsd("ipm_A", (size_t)ldd * (n > 0 ? n : 1));
+    if (n > 0)
+      NYS_CUDA_TRY(ctx, cudaMemcpy2DAsync(Ad, ldd * 8, qp_in->A, qp_in->lda * 8, m * 8, n, cudaMemcpyHostToDevice, ctx->stream));
+    double* qd = ctx->wsd("ipm_q", (size_t)np_ + 2);
+    double* cd = ctx->wsd("ipm_c", (size_t)np_ + 2);
+    double* bd = ctx->wsd("ipm_b", (size_t)mp);
+    if (n > 0) {
+      NYS_CUDA_TRY(ctx, cudaMemcpyAsync(qd, qp_in->q, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+      NYS_CUDA_TRY(ctx, cudaMemcpyAsync(cd, qp_in->c, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(bd, qp_in->b, m * 8, cudaMemcpyHostToDevice, ctx->stream));
+    A = Ad; lda = ldd; q = qd; b = bd; c = cd;
+  }
+  // ---- iterate and work vectors ------------------------------------------------------------
+  const size_t nn = (size_t)np_ + 2, mm = (size_t)mp;
+  double *x = ctx->wsd("ipm_x", nn), *z = ctx->wsd("ipm_z", nn), *zeta = ctx->wsd("ipm_zeta", nn);
+  double *d = ctx->wsd("ipm_d", nn), *rD = ctx->wsd("ipm_rD", nn), *rd = ctx->wsd("ipm_rd", nn);
+  double *rxz = ctx->wsd("ipm_rxz", nn), *xiau = ctx->wsd("ipm_xiau", nn), *t = ctx->wsd("ipm_t", nn);
+  double *dxp = ctx->wsd("ipm_dxp", nn), *dzp = ctx->wsd("ipm_dzp", nn), *dxc = ctx->wsd("ipm_dxc", nn);
+  double *dzc = ctx->wsd("ipm_dzc", nn), *dx = ctx->wsd("ipm_dx", nn), *dz = ctx->wsd("ipm_dz", nn);
+  double *ones = ctx->wsd("ipm_ones", nn);
+  double *y = ctx->wsd("ipm_y", mm), *lam = ctx->wsd("ipm_lam", mm), *ax = ctx->wsd("ipm_ax", mm);
+  double *rP = ctx->wsd("ipm_rP", mm), *rp = ctx->wsd("ipm_rp", mm), *xi = ctx->wsd("ipm_xi", mm);
+  double *dyp = ctx->wsd("ipm_dyp", mm), *dyc = ctx->wsd("ipm_dyc", mm), *u1 = ctx->wsd("ipm_u1", mm);
+  const int le = ell > 0 ? ell : 1;
+  double *Om = ctx->wsd("ipm_Om", (size_t)mp * le), *U = ctx->wsd("ipm_U", (size_t)mp * le);
+  double *lamh = ctx->wsd("ipm_lamh", (size_t)le), *scoef = ctx->wsd("ipm_s", (size_t)le);
+  Dots D{ctx};
+  double n_total = (double)n;
+  {
+    // global variable count (for mu = x^T z / n)
+    NYS_TRY(launch_set_slots(ctx, S_TMP5, (double)n));
+    NYS_TRY(allreduce_slots(ctx, S_TMP5, 1));
+    NYS_TRY(read_slots(ctx));
+    n_total = ctx->h_sc[S_TMP5];
+  }
+  nys_report R{};
+  R.max_records = rep ? rep->max_records : 0;
+  R.records = rep ? rep->records : nullptr;
+  double t_sketch = 0, t_pcg = 0;
+
+  // ---- norms of b and c ------------------------------------------------------------------
+  NYS_TRY(D.dot(m, b, b, S_BNORM));
+  NYS_TRY(D.dot(n, c, c, S_TMP4));
+  NYS_TRY(allreduce_slots(ctx, S_TMP4, 1));
+  NYS_TRY(read_slots(ctx));
+  const double bnorm = std::sqrt(ctx->h_sc[S_BNORM]);
+  const double cnorm = std::sqrt(ctx->h_sc[S_TMP4]);
+  int total_inner = 0;
+
+  // ---- initial point (App. B.2; u = 0) --------------------------------------
+  NYS_CUDA_TRY(ctx, cudaMemsetAsync(ones, 0, nn * sizeof(double), ctx->stream));
+  NYS_TRY(launch_shift(ctx, n, ones, 1.0));
+  NormalOp op0{m, n, lda, A, ones, nullptr, opt->init_delta};
+  if (ell > 0) {
+    auto ts = std::chrono::steady_clock::now();
+    NYS_TRY(gen_omega(ctx, m, ell, opt->seed, 0, Om));                 // stream 0
+    NYS_TRY(sketch_impl(ctx, m, n, A, lda, ones, nullptr, ell, Om, U, lamh, nullptr));
+    NYS_TRY(launch_prec_coef(ctx, lamh, ell, opt->init_delta, scoef));
+    t_sketch += ms_since(ts);
+  }
+  auto tp = std::chrono::steady_clock::now();
+  PcgResult pr;
+  NYS_TRY(D.dot(m, b, b, S_XINORM));
+  NYS_TRY(launch_pcg_setup(ctx, 2, 0, 0, 0, S_XINORM, 0, 0, opt->init_tol_rel));
+  NYS_TRY(pcg_impl(ctx, op0, ell, U, mp, scoef, b, u1, opt->pcg_max_iter, pr));
+  total_inner += pr.iters;
+  {  // x~ = A^T u1
+    MatvecCall mc;
+    mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = u1; mc.tep = TE_PLAIN; mc.t1 = x;
+    NYS_TRY(apply_At(ctx, mc));
+  }
+  NYS_TRY(launch_cpqx(ctx, n, c, q, x, t));                          // c + Q x~
+  NYS_TRY(apply_A(ctx, m, n, A, lda, t, xi, 1.0, nullptr));          // A (c + Q x~)
+  NYS_TRY(D.dot(m, xi, xi, S_XINORM));
+  NYS_TRY(launch_pcg_setup(ctx, 2, 0, 0, 0, S_XINORM, 0, 0, opt->init_tol_rel));
+  NYS_TRY(pcg_impl(ctx, op0, ell, U, mp, scoef, xi, y, opt->pcg_max_iter, pr));
+  total_inner += pr.iters;
+  t_pcg += ms_since(tp);
+  {  // z~ = c - A^T y~ + Q x~
+    MatvecCall mc;
+    mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = y; mc.tep = TE_RD;
+    mc.t1 = z; mc.ta = c; mc.tb = q; mc.tc = x; mc.td = nullptr;
+    NYS_TRY(apply_At(ctx, mc));
+  }
+  NYS_TRY(launch_minsum(ctx, n, x, 0.0, S_TMP0, S_TMP1, 6));
+  NYS_TRY(launch_minsum(ctx, n, z, 0.0, S_TMP2, S_TMP3, 7));
+  NYS_TRY(D.dot(n, x, z, S_TMP4));
+  if (ctx->world > 1) {
+    NYS_TRY(allreduce_slots(ctx, S_TMP0, 1, true));
+    NYS_TRY(allreduce_slots(ctx, S_TMP2, 1, true));
+    NYS_TRY(allreduce_slots(ctx, S_TMP1, 1));
+    NYS_TRY(allreduce_slots(ctx, S_TMP3, 1));
+    NYS_TRY(allreduce_slots(ctx, S_TMP4, 1));
+  }
+  NYS_TRY(read_slots(ctx));
+  {
+    const double minx = ctx->h_sc[S_TMP0], sumx = ctx->h_sc[S_TMP1];
+    const double minz = ctx->h_sc[S_TMP2], sumz = ctx->h_sc[S_TMP3], xz = ctx->h_sc[S_TMP4];
+    const double dp = std::max(-1.5 * minx, 0.0);
+    const double dd = std::max(-1.5 * minz, 0.0);
+    const double gamma = xz + dd * sumx + dp * sumz + n_total * dp * dd;  // P:1470 expanded
+    const double sz = sumz + n_total * dd, sx = sumx + n_total * dp;  // A13
+    double dpt = dp + (sz > 0 ? 0.5 * gamma / sz : 0.0);
+    double ddt = dd + (sx > 0 ? 0.5 * gamma / sx : 0.0);
+    if (minx + dpt <= 0.0) dpt += 1.0;                                // IPg
+    if (minz + ddt <= 0.0) ddt += 1.0;
+    NYS_TRY(launch_shift(ctx, n, x, dpt));
+    NYS_TRY(launch_shift(ctx, n, z, ddt));
+  }
+  // ---- PMM parameters --------------------------------------------------------------
+  NYS_CUDA_TRY(ctx, cudaMemcpyAsync(lam, y, m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (n > 0) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(zeta, x, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  double rho = opt->rho0, delta = opt->delta0;
+
+  auto residuals = [&]() -> int {
+    // r_P = b - A x ; r_D = c + Q x - A^T y - z ; ||r_P||^2, ||r_D||^2, x^T z
+    NYS_TRY(apply_A(ctx, m, n, A, lda, x, ax, 1.0, nullptr));
+    NYS_TRY(launch_axpby(ctx, m, 1.0, b, -1.0, ax, rP));
+    MatvecCall mc;
+    mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = y; mc.tep = TE_RD;
+    mc.t1 = rD; mc.ta = c; mc.tb = q; mc.tc = x; mc.td = z;
+    NYS_TRY(apply_At(ctx, mc));
+    NYS_TRY(D.dot(m, rP, rP, S_TMP0));
+    NYS_TRY(D.dot(n, rD, rD, S_TMP1));
+    NYS_TRY(D.dot(n, x, z, S_TMP2));
+    NYS_TRY(allreduce_slots(ctx, S_TMP1, 2));
+    NYS_TRY(read_slots(ctx));
+    return NYS_OK;
+  };
+  NYS_TRY(residuals());
+  double nrP = std::sqrt(ctx->h_sc[S_TMP0]), nrD = std::sqrt(ctx->h_sc[S_TMP1]);
+  double mu = ctx->h_sc[S_TMP2] / n_total;
+  double nrP_ref = nrP, nrD_ref = nrD;
+  int status = NYS_EMAXITER;
+  int k = 0;
+  for (k = 0; k <= opt->max_outer; ++k) {
+    const double rel_p = nrP / (1.0 + bnorm), rel_d = nrD / (1.0 + cnorm);
+    if (rel_p <= opt->tol && rel_d <= opt->tol && mu <= opt->tol) { status = NYS_OK; break; }   // A11
+    if (k == opt->max_outer) break;
+    if (!std::isfinite(mu) || !std::isfinite(nrP) || !std::isfinite(nrD)) { status = NYS_EBREAKDOWN; break; }
+    nys_iter_record rec{};
+    rec.k = k; rec.mu = mu; rec.rel_p = rel_p; rec.rel_d = rel_d; rec.rho = rho; rec.delta = delta;
+    auto t_it = std::chrono::steady_clock::now();
+    NYS_TRY(launch_scaling(ctx, n, q, x, z, rho, d));
+    if (ell > 0) {                                                    // P:759, Alg. 2
+      auto ts = std::chrono::steady_clock::now();
+      NYS_TRY(gen_omega(ctx, m, ell, opt->seed, (uint64_t)k + 1, Om));
+      NYS_TRY(sketch_impl(ctx, m, n, A, lda, d, nullptr, ell, Om, U, lamh, nullptr));
+      NYS_TRY(launch_prec_coef(ctx, lamh, ell, delta, scoef));        // mu_prec = delta_k (A7)
+      NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      rec.t_sketch_ms = ms_since(ts);
+      t_sketch += rec.t_sketch_ms;
+    }
+    NormalOp op{m, n, lda, A, d, nullptr, delta};
+    NYS_TRY(launch_set_slots(ctx, S_MUCUR, mu));
+    // ---- predictor ----
+    NYS_TRY(launch_pred_rhs_n(ctx, n, c, q, x, z, zeta, rD, rho, d, rd, rxz, xiau, t));
+    NYS_TRY(launch_pred_rhs_m(ctx, m, b, ax, y, lam, delta, rp));
+    NYS_TRY(apply_A(ctx, m, n, A, lda, t, xi, 1.0, rp));             // xi = r_p + A d (r_d + xi_au)
+    NYS_TRY(D.dot(m, xi, xi, S_XINORM));
+    NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
+    auto tp1 = std::chrono::steady_clock::now();
+    NYS_TRY(pcg_impl(ctx, op, ell, U, mp, scoef, xi, dyp, opt->pcg_max_iter, pr));
+    rec.t_pcg_ms += ms_since(tp1);
+    if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
+    rec.pcg_pred = pr.iters;
+    {
+      MatvecCall mc;  // dx = d (A^T dy - r_d - xi_au); dz = (r_xz - z dx)/x
+      mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = dyp; mc.tep = TE_DX;
+      mc.t1 = dxp; mc.t2 = dzp; mc.ta = rd; mc.tb = xiau; mc.tc = rxz; mc.td = z; mc.tx = x; mc.tdd = d;
+      NYS_TRY(apply_At(ctx, mc));
+    }
+    NYS_TRY(launch_ratio(ctx, n, x, dxp, nullptr, nullptr, z, dzp, nullptr, nullptr, 8));
+    NYS_TRY(allreduce_slots(ctx, S_TMP0, 2, true));
+    NYS_TRY(launch_steps_post(ctx));
+    NYS_TRY(launch_muaff(ctx, n, x, dxp, z, dzp, n_total, 9));
+    if (ctx->world > 1) {
+      NYS_TRY(allreduce_slots(ctx, S_TMP7, 1));
+      NYS_TRY(launch_muaff_post(ctx, n_total));
+    }
+    // ---- corrector ----
+    NYS_TRY(launch_corr_rhs(ctx, n, x, dxp, dzp, d, rxz, xiau, t));
+    NYS_TRY(apply_A(ctx, m, n, A, lda, t, xi, 1.0, nullptr));
+    NYS_TRY(D.dot(m, xi, xi, S_XINORM));
+    NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
+    auto tp2 = std::chrono::steady_clock::now();
+    NYS_TRY(pcg_impl(ctx, op, ell, U, mp, scoef, xi, dyc, opt->pcg_max_iter, pr));
+    rec.t_pcg_ms += ms_since(tp2);
+    if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
+    rec.pcg_corr = pr.iters;
+    {
+      MatvecCall mc;
+      mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = dyc; mc.tep = TE_DX;
+      mc.t1 = dxc; mc.t2 = dzc; mc.ta = nullptr; mc.tb = xiau; mc.tc = rxz; mc.td = z; mc.tx = x; mc.tdd = d;
+      NYS_TRY(apply_At(ctx, mc));
+    }
+    // ---- combine, stepsizes, update ----
+    NYS_TRY(launch_ratio(ctx, n, x, dx, dxp, dxc, z, dz, dzp, dzc, 8));
+    NYS_TRY(allreduce_slots(ctx, S_TMP0, 2, true));
+    NYS_TRY(launch_steps_post(ctx));
+    NYS_TRY(launch_update_n(ctx, n, x, dx, z, dz));
+    NYS_TRY(launch_update_m(ctx, m, y, dyp, dyc));
+    NYS_TRY(residuals());
+    rec.alpha_p = ctx->h_sc[S_AP];
+    rec.alpha_d = ctx->h_sc[S_AD];
+    const double mu_new = ctx->h_sc[S_TMP2] / n_total;
+    nrP = std::sqrt(ctx->h_sc[S_TMP0]);
+    nrD = std::sqrt(ctx->h_sc[S_TMP1]);
+    // ---- PEU (A12) ----
+    double r = (mu > 0) ? std::min(std::max(1.0 - mu_new / mu, 0.0), 1.0) : 0.0;
+    const bool p_imp = nrP <= 0.95 * nrP_ref;
+    const bool d_imp = nrD <= 0.95 * nrD_ref;
+    if (p_imp) {
+      NYS_CUDA_TRY(ctx, cudaMemcpyAsync(lam, y, m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+      nrP_ref = nrP;
+    }
+    if (d_imp) {
+      if (n > 0) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(zeta, x, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+      nrD_ref = nrD;
+    }
+    delta = std::max(opt->reg_floor, (p_imp ? (1.0 - r) : (1.0 - 2.0 / 3.0 * r)) * delta);
+    rho = std::max(opt->reg_floor, (d_imp ? (1.0 - r) : (1.0 - 2.0 / 3.0 * r)) * rho);
+    total_inner += rec.pcg_pred + rec.pcg_corr;
+    mu = mu_new;
+    rec.t_other_ms = ms_since(t_it) - rec.t_sketch_ms - rec.t_pcg_ms;
+    t_pcg += rec.t_pcg_ms;
+    if (opt->verbose)
+      fprintf(stderr, "[nys] k=%3d mu=%.3e rp=%.3e rd=%.3e ap=%.3f ad=%.3f pcg=%d/%d rho=%.2e delta=%.2e\n", k,
+              rec.mu, rec.rel_p, rec.rel_d, rec.alpha_p, rec.alpha_d, rec.pcg_pred, rec.pcg_corr, rho, delta);
+    if (R.records && R.n_records < R.max_records) R.records[R.n_records++] = rec;
+  }
+  // ---- objective and solution out ----------------------------------------------------------
+  {
+    double* qx = t;
+    NYS_TRY(launch_mul(ctx, n, q, x, qx));
+    NYS_TRY(D.dot(n, x, qx, S_TMP3));
+    NYS_TRY(D.dot(n, c, x, S_TMP4));
+    NYS_TRY(D.dot(m, b, y, S_TMP5));
+    NYS_TRY(allreduce_slots(ctx, S_TMP3, 2));
+    NYS_TRY(read_slots(ctx));
+    const double xqx = ctx->h_sc[S_TMP3], cx = ctx->h_sc[S_TMP4], by = ctx->h_sc[S_TMP5];
+    if (sol) {
+      sol->obj = 0.5 * xqx + cx;
+      sol->dual_obj = by - 0.5 * xqx;
+      const cudaMemcpyKind kind = qp_in->host_ptrs ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+      if (sol->x && n > 0) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(sol->x, x, n * 8, kind, ctx->stream));
+      if (sol->z && n > 0) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(sol->z, z, n * 8, kind, ctx->stream));
+      if (sol->y) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(sol->y, y, m * 8, kind, ctx->stream));
+      NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+  }
+  if (rep) {
+    rep->status = status;
+    rep->outer_iters = k;
+    rep->inner_iters = total_inner;
+    rep->rel_p = nrP / (1.0 + bnorm);
+    rep->rel_d = nrD / (1.0 + cnorm);
+    rep->mu = mu;
+    rep->t_total_ms = ms_since(t_start);
+    rep->t_sketch_ms = t_sketch;
+    rep->t_pcg_ms = t_pcg;
+    rep->t_other_ms = rep->t_total_ms - t_sketch - t_pcg;
+    rep->n_records = R.n_records;
+    rep->matvecs = ctx->matvecs - matvecs0;
+    rep->kernel_launches = ctx->launches - launches0;
+  }
+  return status == NYS_EMAXITER ? NYS_EMAXITER : status;
+}
+}  // namespace
+
+// ==========================================================================================
+// extern "C" ABI
+// ==========================================================================================
+#define NYS_GUARD_BEGIN try {
+#define NYS_GUARD_END                 \
+  }                                   \
+  catch (const NysException& ex) {    \
+    return ex.code;                   \
+  }                                   \
+  catch (...) {                       \
+    return NYS_ECUDA;                 \
+  }
+
+extern "C" {
+
+const char* nys_strerror(int code) {
+  switch (code) {
+    case NYS_OK: return "ok";
+    case NYS_NOTCONV: return "PCG did not converge within max_iter";
+    case NYS_EINVAL: return "invalid argument";
+    case NYS_ENONPOS: return "non-positive or non-finite scaling d_j";
+    case NYS_ECHOL: return "sketch core not positive definite (Cholesky failed)";
+    case NYS_EBREAKDOWN: return "PCG breakdown (p^T N p <= 0 or non-finite)";
+    case NYS_EMAXITER: return "IP-PMM outer iteration limit reached";
+    case NYS_ECUDA: return "CUDA error";
+    case NYS_ENCCL: return "NCCL error";
+    case NYS_ENOMEM: return "device allocation failed";
+    default: return "unknown error";
+  }
+}
+
+const char* nys_last_error(nys_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+int64_t nys_kernel_launches(nys_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void nys_default_options(nys_options* o) {
+  if (!o) return;
+  o->tol = 1e-8;
+  o->ell = 0;
+  o->seed = 0;
+  o->max_outer = 100;
+  o->pcg_max_iter = 20000;
+  o->rho0 = 8.0;
+  o->delta0 = 8.0;
+  o->reg_floor = 5e-10;
+  o->pcg_c = 1e-3;
+  o->pcg_floor = 1e-10;
+  o->init_delta = 10.0;
+  o->init_tol_rel = 1e-8;
+  o->verbose = 0;
+}
+
+int nys_create(nys_ctx** out, int device, void* cuda_stream, const void* nccl_unique_id, int rank, int world) {
+  if (!out) return NYS_EINVAL;
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return NYS_EINVAL;
+  if (world > 1 && !nccl_unique_id) return NYS_EINVAL;
+  nys_ctx* ctx = new nys_ctx();
+  ctx->device = device;
+  ctx->rank = rank;
+  ctx->world = world;
+  auto fail = [&](int code) {
+    *out = ctx;  // keep for nys_last_error; caller destroys
+    return code;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) { ctx->set_error("cudaSetDevice failed"); return fail(NYS_ECUDA); }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) { ctx->set_error("cudaGetDeviceProperties failed"); return fail(NYS_ECUDA); }
+  ctx->num_sms = prop.multiProcessorCount;
+  if (cuda_stream) {
+    ctx->stream = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(NYS_ECUDA);
+    ctx->own_stream = true;
+  }
+  if (cudaMalloc(&ctx->sc, S_COUNT * sizeof(double)) != cudaSuccess) return fail(NYS_ENOMEM);
+  if (cudaMalloc(&ctx->counters, kMaxCounters * sizeof(unsigned int)) != cudaSuccess) return fail(NYS_ENOMEM);
+  cudaMemset(ctx->sc, 0, S_COUNT * sizeof(double));
+  cudaMemset(ctx->counters, 0, kMaxCounters * sizeof(unsigned int));
+  if (cudaMallocHost(&ctx->h_sc, S_COUNT * sizeof(double)) != cudaSuccess) return fail(NYS_ENOMEM);
+  cudaEventCreate(&ctx->ev0);
+  cudaEventCreate(&ctx->ev1);
+  if (world > 1) {
+    std::string err;
+    if (!g_nccl.load(err)) { ctx->set_error(err); return fail(NYS_ENCCL); }
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    ncclComm_t comm;
+    ncclResult_t r = g_nccl.commInitRank(&comm, world, id, rank);
+    if (r != ncclSuccess) { ctx->set_error("ncclCommInitRank failed"); return fail(NYS_ENCCL); }
+    ctx->nccl_comm = comm;
+  }
+  cudaDeviceSynchronize();
+  *out = ctx;
+  return NYS_OK;
+}
+
+int nys_nccl_unique_id(void* out128) {
+  if (!out128) return NYS_EINVAL;
+  std::string err;
+  if (!g_nccl.load(err) || !g_nccl.getUniqueId) return NYS_ENCCL;
+  ncclUniqueId id;
+  if (g_nccl.getUniqueId(&id) != ncclSuccess) return NYS_ENCCL;
+  std::memcpy(out128, &id, sizeof(id));
+  return NYS_OK;
+}
+
+int nys_destroy(nys_ctx* ctx) {
+  if (!ctx) return NYS_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
+  if (ctx->sc) cudaFree(ctx->sc);
+  if (ctx->counters) cudaFree(ctx->counters);
+  if (ctx->h_sc) cudaFreeHost(ctx->h_sc);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)ctx->nccl_comm);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return NYS_OK;
+}
+
+static int check_A(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda) {
+  if (!ctx) return NYS_EINVAL;
+  if (m < 1 || n < 0 || lda < m || (lda & 1)) { ctx->set_error("bad m / n / lda (lda must be >= m and even)"); return NYS_EINVAL; }
+  if (n > 0 && (!A || !aligned16(A))) { ctx->set_error("A must be a 16-byte aligned device pointer"); return NYS_EINVAL; }
+  return NYS_OK;
+}
+
+int nys_normal_matvec(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                      const double* e, double delta, const double* v, double* w) {
+  NYS_GUARD_BEGIN
+  NYS_TRY(check_A(ctx, m, n, A, lda));
+  if (!v || !w || (n > 0 && !d) || delta < 0 || v == w) { ctx->set_error("bad vector arguments"); return NYS_EINVAL; }
+  cudaSetDevice(ctx->device);
+  NormalOp op{m, n, lda, A, d, e, delta};
+  NYS_TRY(apply_normal_full(ctx, op, v, nullptr, nullptr, nullptr, w, false, nullptr));
+  return NYS_OK;
+  NYS_GUARD_END
+}
+
+int nys_check_scaling(nys_ctx* ctx, int64_t n, const double* d, int64_t* bad_index) {
+  NYS_GUARD_BEGIN
+  if (!ctx || n < 0 || (n > 0 && !d)) return NYS_EINVAL;
+  cudaSetDevice(ctx->device);
+  unsigned long long* bad = (unsigned long long*)ctx->ws("chk_bad", 8);
+  unsigned long long init = ~0ULL, hv = 0;
+  NYS_CUDA_TRY(ctx, cudaMemcpyAsync(bad, &init, 8, cudaMemcpyHostToDevice, ctx->stream));
+  NYS_TRY(launch_check_pos(ctx, n, d, bad));
+  NYS_CUDA_TRY(ctx, cudaMemcpyAsync(&hv, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (bad_index) *bad_index = (hv == ~0ULL) ? -1 : (int64_t)hv;
+  if (hv != ~0ULL) {
+    ctx->set_error("d has a non-positive or non-finite entry at index " + std::to_string(hv));
+    return NYS_ENONPOS;
+  }
+  return NYS_OK;
+  NYS_GUARD_END
+}
+
+int nys_gaussian(nys_ctx* ctx, int64_t m, int ell, uint64_t seed, uint64_t stream, double* Omega) {
+  NYS_GUARD_BEGIN
+  if (!ctx || m < 0 || ell < 0 || (m * ell > 0 && !Omega)) return NYS_EINVAL;
+  cudaSetDevice(ctx->device);
+  return launch_gaussian(ctx, Omega, m * (int64_t)ell, seed, stream);
+  NYS_GUARD_END
+}
+
+int nys_sketch(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
+               double delta, int ell, const double* Omega, double* U, double* lambda, nys_sketch_info* info) {
+  NYS_GUARD_BEGIN
+  NYS_TRY(check_A(ctx, m, n, A, lda));
+  if (ell < 1 || ell > m || ell > 256 || !(delta > 0) || !Omega || !U || !lambda || (n > 0 && !d)) {
+    ctx->set_error("nys_sketch: need 1 <= ell <= min(m, 256), delta > 0, non-null buffers");
+    return NYS_EINVAL;
+  }
+  cudaSetDevice(ctx->device);
+  NYS_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  const int64_t mp = even(m);
+  const double* Om = Omega;
+  double* Uo = U;
+  if (mp != m || !aligned16(Omega) || !aligned16(U)) {
+    double* Omw = ctx->wsd("sk_Om_in", (size_t)mp * ell);
+    NYS_CUDA_TRY(ctx, cudaMemcpy2DAsync(Omw, mp * 8, Omega, m * 8, m * 8, ell, cudaMemcpyDeviceToDevice, ctx->stream));
+    Om = Omw;
+    Uo = ctx->wsd("sk_U_out", (size_t)mp * ell);
+  }
+  nys_sketch_info tmp{};
+  NYS_TRY(sketch_impl(ctx, m, n, A, lda, d, e, ell, Om, Uo, lambda, &tmp));
+  if (Uo != U)
+    NYS_CUDA_TRY(ctx, cudaMemcpy2DAsync(U, m * 8, Uo, mp * 8, m * 8, ell, cudaMemcpyDeviceToDevice, ctx->stream));
+  NYS_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+  NYS_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  tmp.t_ms = ms;
+  if (info) *info = tmp;
+  return NYS_OK;
+  NYS_GUARD_END
+}
+
+int nys_sketch_apply(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                     const double* e, int ell, const double* Omega, double* Y) {
+  NYS_GUARD_BEGIN
+  NYS_TRY(check_A(ctx, m, n, A, lda));
+  if (ell < 1 || !Omega || !Y || (n > 0 && !d)) { ctx->set_error("nys_sketch_apply: bad arguments"); return NYS_EINVAL; }
+  cudaSetDevice(ctx->device);
+  const int64_t mp = even(m);
+  const double* Om = Omega;
+  double* Yo = Y;
+  if (mp != m || !aligned16(Omega) || !aligned16(Y)) {
+    double* Omw = ctx->wsd("sk_Om_in", (size_t)mp * ell);
+    NYS_CUDA_TRY(ctx, cudaMemcpy2DAsync(Omw, mp * 8, Omega, m * 8, m * 8, ell, cudaMemcpyDeviceToDevice, ctx->stream));
+    Om = Omw;
+    Yo = ctx->wsd("sk_Y_out", (size_t)mp * ell);
+  }
+  NYS_TRY(sketch_Y(ctx, m, n, A, lda, d, e, ell, Om, Yo));
+  if (Yo != Y)
+    NYS_CUDA_TRY(ctx, cudaMemcpy2DAsync(Y, m * 8, Yo, mp * 8, m * 8, ell, cudaMemcpyDeviceToDevice, ctx->stream));
+  return NYS_OK;
+  NYS_GUARD_END
+}
+
+int nys_pcg_solve(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
+                  double delta, int ell, const double* U, const double* lambda, double mu_prec, const double* rhs,
+                  double* x, double tol_abs, int max_iter, nys_pcg_info* info) {
+  NYS_GUARD_BEGIN
+  NYS_TRY(check_A(ctx, m, n, A, lda));
+  if (ell < 0 || ell > m || ell > 256 || (ell > 0 && (!U || !lambda)) || !rhs || !x || max_iter < 0 || delta < 0 ||
+      (n > 0 && !d) || (ell > 0 && !(mu_prec > 0))) {
+    ctx->set_error("nys_pcg_solve: bad arguments");
+    return NYS_EINVAL;
+  }
+  cudaSetDevice(ctx->device);
+  NYS_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  const int64_t mp = even(m);
+  const double* Uu = U;
+  if (ell > 0 && (mp != m || !aligned16(U))) {
+    double* Uw = ctx->wsd("pcg_U_in", (size_t)mp * ell);
+    NYS_CUDA_TRY(ctx, cudaMemcpy2DAsync(Uw, mp * 8, U, m * 8, m * 8, ell, cudaMemcpyDeviceToDevice, ctx->stream));
+    Uu = Uw;
+  }
+  double* s = ctx->wsd("pcg_s", (size_t)(ell > 0 ? ell : 1));
+  if (ell > 0) NYS_TRY(launch_prec_coef(ctx, lambda, ell, mu_prec, s));
+  NYS_TRY(launch_pcg_setup(ctx, 0, tol_abs, 0, 0, 0, 0, 0, 0));
+  NormalOp op{m, n, lda, A, d, e, delta};
+  PcgResult pr;
+  NYS_TRY(pcg_impl(ctx, op, ell, Uu, mp, s, rhs, x, max_iter, pr));
+  // true residual at exit: ||rhs - N x||
+  double* w = ctx->wsd("pcg_truew", (size_t)mp);
+  NYS_TRY(apply_normal_full(ctx, op, x, nullptr, nullptr, nullptr, w, false, nullptr));
+  NYS_TRY(launch_axpby(ctx, m, 1.0, rhs, -1.0, w, w));
+  {
+    const double* aa[1] = {w};
+    const double* bb[1] = {w};
+    int out[1] = {S_TMP6};
+    NYS_TRY(launch_dots(ctx, m, 1, aa, bb, out, 10));
+  }
+  NYS_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+  NYS_TRY(read_slots(ctx));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  const bool conv = std::sqrt(pr.rr) <= tol_abs;
+  if (info) {
+    info->iters = pr.iters;
+    info->converged = conv ? 1 : 0;
+    info->res_norm = std::sqrt(pr.rr);
+    info->true_res_norm = std::sqrt(ctx->h_sc[S_TMP6]);
+    info->t_ms = ms;
+  }
+  if (pr.status == NYS_EBREAKDOWN) { ctx->set_error("PCG breakdown"); return NYS_EBREAKDOWN; }
+  return conv ? NYS_OK : NYS_NOTCONV;
+  NYS_GUARD_END
+}
+
+int nys_ipppmm_solve(nys_ctx* ctx, const nys_qp* qp, const nys_options* opt, nys_solution* sol, nys_report* rep) {
+  NYS_GUARD_BEGIN
+  if (!ctx || !qp || !opt) return NYS_EINVAL;
+  if (qp->m < 1 || qp->n < 0 || qp->lda < qp->m || !qp->b || (qp->n > 0 && (!qp->A || !qp->q || !qp->c))) {
+    ctx->set_error("nys_ipppmm_solve: bad problem");
+    return NYS_EINVAL;
+  }
+  if (!qp->host_ptrs) NYS_TRY(check_A(ctx, qp->m, qp->n, qp->A, qp->lda));
+  if (opt->ell < 0 || opt->ell > qp->m || opt->ell > 256 || !(opt->tol > 0)) {
+    ctx->set_error("nys_ipppmm_solve: bad options");
+    return NYS_EINVAL;
+  }
+  cudaSetDevice(ctx->device);
+  return ipm_impl(ctx, qp, opt, sol, rep);
+  NYS_GUARD_END
+}
+
+}  // extern "C"

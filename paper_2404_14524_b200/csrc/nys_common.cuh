@@ -1,0 +1,216 @@
+// Internal header of libnysipm.so (sm_100a).  Not part of the public ABI (include/nysipm.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "nysipm.h"
+
+// ------------------------------------------------------------------------------------------
+// error plumbing
+// ------------------------------------------------------------------------------------------
+#define NYS_CUDA_TRY(ctx, expr)                                                            \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      (ctx)->set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));                \
+      return NYS_ECUDA;                                                                    \
+    }                                                                                      \
+  } while (0)
+
+#define NYS_TRY(expr)               \
+  do {                              \
+    int _rc = (expr);               \
+    if (_rc < 0) return _rc;        \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+// device scalar slots (one fp64 array in device memory per context)
+// ------------------------------------------------------------------------------------------
+namespace nys {
+enum Slot : int {
+  // PCG
+  S_RZ = 0, S_PW, S_ALPHA, S_RR, S_BETA, S_TOL, S_DONE, S_ITERS, S_STATUS, S_MU, S_LAML,
+  // reductions / IPM
+  S_TMP0, S_TMP1, S_TMP2, S_TMP3, S_TMP4, S_TMP5, S_TMP6, S_TMP7,
+  S_AP, S_AD, S_MUAFF, S_MUT, S_MUCUR, S_XINORM, S_BNORM,
+  S_NU, S_SHIFT, S_CHOLFAIL, S_FRO,
+  S_COUNT = 64
+};
+constexpr int kMaxCounters = 64;
+}  // namespace nys
+
+// ------------------------------------------------------------------------------------------
+// context
+// ------------------------------------------------------------------------------------------
+struct nys_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, world = 1;
+  void* nccl_comm = nullptr;
+  int num_sms = 148;
+  int64_t launches = 0;
+  int64_t matvecs = 0;
+  std::string last_error;
+  std::map<std::string, std::pair<void*, size_t>> bufs;
+  double* sc = nullptr;           // device scalars [S_COUNT]
+  unsigned int* counters = nullptr;  // device counters for last-block reductions
+  double* h_sc = nullptr;         // pinned host mirror
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  void set_error(const std::string& s) { last_error = s; }
+  // named workspace, grown monotonically; contents are NOT preserved on growth
+  void* ws(const char* name, size_t bytes);
+  double* wsd(const char* name, size_t count) { return (double*)ws(name, count * sizeof(double)); }
+  int check_launch(const char* what);
+};
+
+// ------------------------------------------------------------------------------------------
+// PTX helpers (sm_90+/sm_100a): mbarrier, bulk async copy, cluster / DSMEM
+// ------------------------------------------------------------------------------------------
+namespace nys {
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  const uint32_t a = smem_u32(bar);
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  const uint32_t a = smem_u32(bar);
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// 1-D bulk async copy global -> shared (own CTA), completion on mbarrier (tx bytes)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t ncluster_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+}  // namespace nys
+
+// ------------------------------------------------------------------------------------------
+// internal launchers (implemented in k_*.cu)
+// ------------------------------------------------------------------------------------------
+namespace nys {
+
+enum MatvecMode { MV_FUSED = 0, MV_TONLY = 1, MV_NONLY = 2 };
+enum TEpilogue { TE_PLAIN = 0, TE_DX = 1, TE_RD = 2 };
+
+struct MatvecCall {
+  int mode = MV_FUSED;
+  int64_t m = 0, n = 0, lda = 0;
+  const double* A = nullptr;
+  // operand vector v = z + (*beta) * p   (beta/p may be null)
+  const double* z = nullptr;
+  const double* p = nullptr;
+  const double* beta = nullptr;
+  double* p_out = nullptr;          // if set: v is written here (by cluster 0)
+  const double* d = nullptr;        // FUSED: t_j = d_j (A^T v)_j
+  const double* u = nullptr;        // NONLY: t_j = u_j
+  // FUSED / NONLY finalize: out_i = sgn * (A t)_i + (delta + e_i) v_i + add_i ;
+  // optional dot out^T v -> scalar slot (PCG: p^T w, then alpha = rz / pw)
+  double* out = nullptr;
+  double sgn = 1.0;
+  double delta = 0.0;
+  bool use_delta = false;
+  const double* e = nullptr;
+  const double* add = nullptr;
+  bool pcg_alpha = false;           // compute pw and alpha (slots S_PW, S_ALPHA) ; breakdown -> S_STATUS
+  // TONLY epilogue
+  int tep = TE_PLAIN;
+  double* t1 = nullptr;             // PLAIN: (A^T v)_j ; DX: dx ; RD: rD
+  double* t2 = nullptr;             // DX: dz
+  const double* ta = nullptr;       // DX: r_d (or null)   RD: c
+  const double* tb = nullptr;       // DX: xi_au           RD: q
+  const double* tc = nullptr;       // DX: r_xz            RD: x
+  const double* td = nullptr;       // DX: z               RD: z (or null)
+  const double* tx = nullptr;       // DX: x
+  const double* tdd = nullptr;      // DX: d
+  const double* done = nullptr;     // early-exit flag (device scalar), or null
+};
+int launch_matvec(nys_ctx* ctx, const MatvecCall& c);
+
+}  // namespace nys

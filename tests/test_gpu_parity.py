@@ -1,0 +1,298 @@
+"""GPU parity: libnysipm.so (through the C ABI) vs the CPU oracle on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star / DESIGN.md "Parity"):
+  * normal matvec and sketch Y: normwise relative error <= 1e-12
+  * Nystrom factors: operator N_hat and P^{-1} agree <= 1e-10 (U is unique only up to rotation,
+    SURVEY A5), U^T U = I to 1e-12
+  * PCG: same iteration count (+-1) and ||x_gpu - x_ref|| <= 2 tol / delta (both residuals <= tol)
+  * Nys-IP-PMM: same status, objective within 1e-7 relative, rel_p / rel_d / mu <= 1e-8
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import ippmm, linops, nystrom, rng as orng  # noqa: E402
+from oracle.pcg import pcg as oracle_pcg  # noqa: E402
+from oracle.active_set import enumerate_active_sets  # noqa: E402
+from synth import make_config  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2404_14524_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+
+
+def dev_cm(M):
+    """column-major m x k numpy -> device tensor (k, m) (ld = m)"""
+    return dev(np.asarray(M, dtype=np.float64).T.copy())
+
+
+def host_cm(t, m):
+    return t.cpu().numpy().T[:m].copy()
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+# ------------------------------------------------------------------------ normal matvec (K1)
+MV_SHAPES = [(1, 5), (2, 0), (2, 3), (37, 401), (64, 3001), (100, 400), (130, 257), (300, 999), (1000, 1201),
+             (2000, 801), (2001, 333), (4096, 300), (5000, 129), (8193, 70), (20000, 40), (50000, 17)]
+
+
+@pytest.mark.parametrize("m,n", MV_SHAPES)
+def test_normal_matvec_parity(ctx, m, n):
+    from paper_2404_14524_b200 import colmajor_device
+    rs = np.random.default_rng(m * 7 + n)
+    A = rs.standard_normal((m, n))
+    d = rs.uniform(0.01, 3.0, n)
+    e = rs.uniform(0.0, 1.0, m)
+    v = rs.standard_normal(m)
+    delta = 0.3
+    Ad, lda = colmajor_device(A)
+    w = torch.empty(m, dtype=torch.float64, device="cuda")
+    for use_e in (False, True):
+        ctx.nys_normal_matvec(Ad, lda, m, dev(d) if n else dev(np.zeros(1)), dev(e) if use_e else None, delta,
+                              dev(v), w)
+        torch.cuda.synchronize()
+        ref = linops.normal_matvec(A, d, v, delta, e if use_e else None)
+        assert rel(w.cpu().numpy(), ref) <= 1e-12, (m, n, use_e)
+
+
+def test_normal_matvec_config_shapes_full(ctx):
+    """BASELINE configs 1 and 3 at full size (the bench launch configuration)."""
+    from paper_2404_14524_b200 import colmajor_device
+    for idx in (1, 3):
+        inst = make_config(idx)
+        rs = np.random.default_rng(idx)
+        d = rs.uniform(0.01, 2.0, inst.n)
+        v = rs.standard_normal(inst.m)
+        Ad, lda = colmajor_device(inst.A)
+        w = torch.empty(inst.m, dtype=torch.float64, device="cuda")
+        ctx.nys_normal_matvec(Ad, lda, inst.m, dev(d), None, 1e-3, dev(v), w)
+        torch.cuda.synchronize()
+        ref = linops.normal_matvec(inst.A, d, v, 1e-3)
+        assert rel(w.cpu().numpy(), ref) <= 1e-12
+
+
+def test_normal_matvec_rejects_bad_lda(ctx):
+    from paper_2404_14524_b200 import NysError
+    A = torch.zeros((4, 5), dtype=torch.float64, device="cuda")
+    w = torch.empty(5, dtype=torch.float64, device="cuda")
+    with pytest.raises(NysError):
+        ctx.nys_normal_matvec(A, 5, 5, dev(np.ones(4)), None, 0.1, dev(np.ones(5)), w)  # odd lda
+
+
+# ------------------------------------------------------------------------ Omega generator
+@pytest.mark.parametrize("m,ell,seed,stream", [(100, 20, 0, 1), (2000, 50, 3, 7), (37, 5, 2**40 + 3, 2**33 + 1)])
+def test_gaussian_matches_oracle_philox(ctx, m, ell, seed, stream):
+    O = torch.empty((ell, m), dtype=torch.float64, device="cuda")
+    ctx.nys_gaussian(m, ell, seed, stream, O)
+    torch.cuda.synchronize()
+    ref = orng.gaussian_omega(m, ell, seed, stream)
+    np.testing.assert_allclose(host_cm(O, m), ref, rtol=0, atol=5e-14)
+
+
+# ------------------------------------------------------------------------ sketch (K2/K3)
+SK_SHAPES = [(100, 400, 20), (64, 5000, 64), (257, 1031, 33), (2000, 8000, 50), (5000, 3000, 100), (20000, 700, 40)]
+
+
+@pytest.mark.parametrize("m,n,ell", SK_SHAPES)
+def test_sketch_apply_parity(ctx, m, n, ell):
+    from paper_2404_14524_b200 import colmajor_device
+    rs = np.random.default_rng(m + n + ell)
+    A = rs.standard_normal((m, n))
+    d = rs.uniform(0.01, 3.0, n)
+    e = rs.uniform(0.0, 1.0, m)
+    Om = orng.gaussian_omega(m, ell, 5, 9)
+    Ad, lda = colmajor_device(A)
+    Y = torch.empty((ell, m), dtype=torch.float64, device="cuda")
+    for ee in (None, e):
+        ctx.nys_sketch_apply(Ad, lda, m, dev(d), dev(ee) if ee is not None else None, ell, dev_cm(Om), Y)
+        torch.cuda.synchronize()
+        ref = linops.sketch(A, d, Om, ee)
+        assert rel(host_cm(Y, m), ref) <= 1e-12
+
+
+def _nys_gpu(ctx, A, d, ell, Om, delta=1e-2):
+    from paper_2404_14524_b200 import colmajor_device
+    m = A.shape[0]
+    Ad, lda = colmajor_device(A)
+    U = torch.empty((ell, m), dtype=torch.float64, device="cuda")
+    lam = torch.empty(ell, dtype=torch.float64, device="cuda")
+    info = ctx.nys_sketch(Ad, lda, m, dev(d), None, delta, ell, dev_cm(Om), U, lam)
+    torch.cuda.synchronize()
+    return host_cm(U, m), lam.cpu().numpy(), info
+
+
+@pytest.mark.parametrize("m,n,ell,r", [(100, 400, 20, 100), (300, 900, 40, 12), (2000, 8000, 50, 40),
+                                       (64, 3000, 64, 64), (501, 2000, 30, 500)])
+def test_nystrom_factors_parity(ctx, m, n, ell, r):
+    rs = np.random.default_rng(m + ell)
+    W = rs.standard_normal((m, r))
+    H = rs.standard_normal((r, n))
+    A = W @ H / np.sqrt(n) + 1e-3 * rs.standard_normal((m, n))
+    d = rs.uniform(0.05, 2.0, n)
+    Om = orng.gaussian_omega(m, ell, 1, 2)
+    U, lam, info = _nys_gpu(ctx, A, d, ell, Om)
+    Uo, lamo, io = nystrom.nystrom_from_sketch(linops.sketch(A, d, Om), Om)
+    assert info.orth_err <= 1e-12
+    assert np.linalg.norm(U.T @ U - np.eye(ell)) <= 1e-12
+    assert np.all(np.diff(lam) <= 0) and np.all(lam >= 0)
+    assert info.nu == io["nu"]
+    np.testing.assert_allclose(lam, lamo, rtol=0, atol=1e-10 * lamo[0])
+    Nh, Nho = (U * lam) @ U.T, (Uo * lamo) @ Uo.T
+    assert rel(Nh, Nho) <= 1e-10
+    delta = 1e-2
+    for _ in range(3):
+        v = rs.standard_normal(m)
+        a = nystrom.precond_inv_apply(U, lam, delta, v)
+        b = nystrom.precond_inv_apply(Uo, lamo, delta, v)
+        assert rel(a, b) <= 1e-10
+
+
+def test_nystrom_exact_recovery_lowrank(ctx):
+    rs = np.random.default_rng(3)
+    m, n, r, ell = 400, 600, 10, 16
+    A = rs.standard_normal((m, r)) @ rs.standard_normal((r, n))
+    d = rs.uniform(0.5, 1.5, n)
+    U, lam, _ = _nys_gpu(ctx, A, d, ell, orng.gaussian_omega(m, ell, 4, 4))
+    N = (A * d) @ A.T
+    assert rel((U * lam) @ U.T, N) <= 1e-11
+
+
+# ------------------------------------------------------------------------ PCG
+@pytest.mark.parametrize("cfg,kw", [(0, {}), (1, dict(m=300, n=1200, ell=30)), (3, dict(m=16, n=4000, ell=8))])
+@pytest.mark.parametrize("use_prec", [True, False])
+def test_pcg_parity(ctx, cfg, kw, use_prec):
+    from paper_2404_14524_b200 import colmajor_device
+    inst = make_config(cfg, **kw)
+    A, m, n, ell = inst.A, inst.m, inst.n, inst.ell
+    rs = np.random.default_rng(cfg)
+    x = rs.uniform(0.01, 2.0, n)
+    z = rs.uniform(0.01, 2.0, n)
+    d = linops.scaling_d(inst.q, x, z, 1e-2)
+    delta = 1e-3
+    rhs = rs.standard_normal(m)
+    Om = orng.gaussian_omega(m, ell, 0, 1)
+    Uo, lamo, _ = nystrom.nystrom_from_sketch(linops.sketch(A, d, Om), Om)
+    tol = 1e-9 * np.linalg.norm(rhs)
+    pinv = (lambda v: nystrom.precond_inv_apply(Uo, lamo, delta, v)) if use_prec else None
+    xo, io = oracle_pcg(lambda v: linops.normal_matvec(A, d, v, delta), rhs, pinv, tol_abs=tol, max_iter=5000)
+    Ad, lda = colmajor_device(A)
+    xg = torch.empty(m, dtype=torch.float64, device="cuda")
+    info = ctx.nys_pcg_solve(Ad, lda, m, dev(d), None, delta, ell if use_prec else 0, dev_cm(Uo), dev(lamo), delta,
+                             dev(rhs), xg, tol, 5000)
+    xg = xg.cpu().numpy()
+    assert info.converged == 1 and io["converged"]
+    assert abs(info.iters - io["iters"]) <= max(1, io["iters"] // 50)
+    assert np.linalg.norm(xg - xo) <= 2 * tol / delta
+    assert info.true_res_norm <= 1.5 * tol
+
+
+def test_pcg_zero_rhs_and_maxiter(ctx):
+    from paper_2404_14524_b200 import colmajor_device
+    inst = make_config(0)
+    Ad, lda = colmajor_device(inst.A)
+    d = dev(np.ones(inst.n))
+    x = torch.empty(inst.m, dtype=torch.float64, device="cuda")
+    info = ctx.nys_pcg_solve(Ad, lda, inst.m, d, None, 1.0, 0, None, None, 1.0, dev(np.zeros(inst.m)), x, 1e-12, 100)
+    assert info.iters == 0 and info.converged == 1 and float(x.abs().max()) == 0.0
+    info = ctx.nys_pcg_solve(Ad, lda, inst.m, d, None, 1e-8, 0, None, None, 1.0, dev(np.ones(inst.m)), x, 1e-300, 3)
+    assert info.iters == 3 and info.converged == 0
+
+
+# ------------------------------------------------------------------------ Nys-IP-PMM end to end
+def _solve_gpu(ctx, inst, ell, host=False, **kw):
+    from paper_2404_14524_b200 import colmajor_device
+    if host:
+        lda = ((inst.m + 31) // 32) * 32
+        Ah = np.zeros((inst.n, lda))
+        Ah[:, :inst.m] = inst.A.T
+        return ctx.nys_ipppmm_solve(Ah, lda, inst.m, inst.q, inst.b, inst.c, ell=ell, host=True, **kw)
+    Ad, lda = colmajor_device(inst.A)
+    return ctx.nys_ipppmm_solve(Ad, lda, inst.m, dev(inst.q), dev(inst.b), dev(inst.c), ell=ell, **kw)
+
+
+IPM_CASES = [(0, {}, None), (1, dict(m=200, n=800, ell=20), None), (3, dict(m=16, n=2000, ell=16), None),
+             (0, {}, 0), (1, dict(m=200, n=800, ell=20), 0)]
+
+
+@pytest.mark.parametrize("cfg,kw,ell_override", IPM_CASES)
+def test_ipppmm_parity(ctx, cfg, kw, ell_override):
+    inst = make_config(cfg, **kw)
+    ell = inst.ell if ell_override is None else ell_override
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=ell))
+    g = _solve_gpu(ctx, inst, ell)
+    assert ref.status == "optimal" and g["status"] == 0
+    assert g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    assert abs(g["obj"] - ref.obj) <= 1e-7 * max(1.0, abs(ref.obj))
+    assert abs(g["outer"] - ref.outer) <= 1
+    x = g["x"].cpu().numpy()
+    assert np.min(x) > 0
+    # KKT certificate recomputed on the host from the GPU iterate
+    y, z = g["y"].cpu().numpy(), g["z"].cpu().numpy()
+    assert np.linalg.norm(inst.b - inst.A @ x) / (1 + np.linalg.norm(inst.b)) <= 1e-8
+    rD = inst.c + inst.q * x - inst.A.T @ y - z
+    assert np.linalg.norm(rD) / (1 + np.linalg.norm(inst.c)) <= 1e-8
+
+
+def test_ipppmm_config1_full(ctx):
+    inst = make_config(1)
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
+    g = _solve_gpu(ctx, inst, inst.ell)
+    assert g["status"] == 0
+    assert abs(g["obj"] - ref.obj) <= 1e-7 * abs(ref.obj)
+    assert abs(g["outer"] - ref.outer) <= 1
+
+
+def test_ipppmm_host_pointers_match_device(ctx):
+    inst = make_config(0)
+    a = _solve_gpu(ctx, inst, inst.ell)
+    b = _solve_gpu(ctx, inst, inst.ell, host=True)
+    assert a["obj"] == b["obj"] and a["outer"] == b["outer"]
+    np.testing.assert_array_equal(a["x"].cpu().numpy(), b["x"])
+
+
+def test_ipppmm_hand_kkt_and_active_set(ctx):
+    class I:  # n = 1: min 1/2 x^2, x = 1, x >= 0
+        A = np.array([[1.0]]); q = np.array([1.0]); b = np.array([1.0]); c = np.array([0.0]); m = 1; n = 1
+    g = _solve_gpu(ctx, I, 1)
+    assert g["status"] == 0
+    assert abs(g["x"].item() - 1) <= 1e-7 and abs(g["y"].item() - 1) <= 1e-6 and abs(g["z"].item()) <= 1e-7
+    for seed in range(4):
+        rs = np.random.default_rng(100 + seed)
+        m, n = 3, 8
+        A = rs.standard_normal((m, n))
+        x0 = rs.uniform(0.2, 1.5, n)
+        x0[rs.permutation(n)[:3]] = 0.0
+
+        class J:
+            pass
+        J.A, J.m, J.n = A, m, n
+        J.b = A @ x0
+        J.q = rs.uniform(0.1, 2.0, n)
+        J.c = rs.standard_normal(n)
+        ref = enumerate_active_sets(J.A, J.q, J.b, J.c)
+        g = _solve_gpu(ctx, J, 2)
+        assert g["status"] == 0
+        assert abs(g["obj"] - ref["obj"]) <= 1e-6 * max(1, abs(ref["obj"]))
+        np.testing.assert_allclose(g["x"].cpu().numpy(), ref["x"], atol=1e-5)
+
+
+def test_kernel_launch_accounting(ctx):
+    before = ctx.kernel_launches
+    inst = make_config(0)
+    _solve_gpu(ctx, inst, inst.ell)
+    assert ctx.kernel_launches > before
