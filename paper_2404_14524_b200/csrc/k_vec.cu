@@ -492,14 +492,14 @@ __global__ void scaling_kernel(int64_t n, const double* q, const double* x, cons
     d[j] = 1.0 / (q[j] + z[j] / x[j] + rho);
 }
 
-// predictor: r_d = c + q x - A^T y - z + rho (x - zeta) [aty = A^T y given];
-// r_xz = -x z ; xi_au = -r_xz / x (= z) ; t = d (r_d + xi_au)
-__global__ void pred_rhs_n_kernel(int64_t n, const double* c, const double* q, const double* x, const double* z,
-                                  const double* zeta, const double* aty, double rho, const double* d, double* rd,
-                                  double* rxz, double* xiau, double* t) {
+// predictor: r_d = c + q x - A^T y - z + rho (x - zeta) = rD + rho (x - zeta)
+// [rD = dual residual at the current iterate]; r_xz = -x z ; xi_au = -r_xz / x (= z) ;
+// t = d (r_d + xi_au)
+__global__ void pred_rhs_n_kernel(int64_t n, const double* x, const double* z, const double* zeta, const double* rD,
+                                  double rho, const double* d, double* rd, double* rxz, double* xiau, double* t) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const double xj = x[j], zj = z[j];
-    const double r = c[j] + q[j] * xj - aty[j] - zj + rho * (xj - zeta[j]);
+    const double r = rD[j] + rho * (xj - zeta[j]);
     const double rx = -xj * zj;
     const double xa = -rx / xj;
     rd[j] = r;
@@ -604,11 +604,10 @@ int launch_scaling(nys_ctx* ctx, int64_t n, const double* q, const double* x, co
   ctx->launches++;
   return ctx->check_launch("scaling");
 }
-int launch_pred_rhs_n(nys_ctx* ctx, int64_t n, const double* c, const double* q, const double* x, const double* z,
-                      const double* zeta, const double* aty, double rho, const double* d, double* rd, double* rxz,
-                      double* xiau, double* t) {
+int launch_pred_rhs_n(nys_ctx* ctx, int64_t n, const double* x, const double* z, const double* zeta, const double* rD,
+                      double rho, const double* d, double* rd, double* rxz, double* xiau, double* t) {
   if (n <= 0) return NYS_OK;
-  pred_rhs_n_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, c, q, x, z, zeta, aty, rho, d, rd, rxz, xiau, t);
+  pred_rhs_n_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, x, z, zeta, rD, rho, d, rd, rxz, xiau, t);
   ctx->launches++;
   return ctx->check_launch("pred_rhs_n");
 }

@@ -22,9 +22,8 @@ int launch_prec_coef(nys_ctx* ctx, const double* lam, int ell, double mu, double
 int launch_pcg_setup(nys_ctx* ctx, int mode, double tol_abs, double c, double floor_, int xi_slot, int b_slot,
                      int mu_slot, double init_rel);
 int launch_scaling(nys_ctx* ctx, int64_t n, const double* q, const double* x, const double* z, double rho, double* d);
-int launch_pred_rhs_n(nys_ctx* ctx, int64_t n, const double* c, const double* q, const double* x, const double* z,
-                      const double* zeta, const double* aty, double rho, const double* d, double* rd, double* rxz,
-                      double* xiau, double* t);
+int launch_pred_rhs_n(nys_ctx* ctx, int64_t n, const double* x, const double* z, const double* zeta, const double* rD,
+                      double rho, const double* d, double* rd, double* rxz, double* xiau, double* t);
 int launch_pred_rhs_m(nys_ctx* ctx, int64_t m, const double* b, const double* ax, const double* y, const double* lam,
                       double delta, double* rp);
 int launch_corr_rhs(nys_ctx* ctx, int64_t n, const double* x, const double* dxp, const double* dzp, const double* d,

@@ -574,7 +574,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NormalOp op{m, n, lda, A, d, nullptr, delta};
     NYS_TRY(launch_set_slots(ctx, S_MUCUR, mu));
     // ---- predictor ----
-    NYS_TRY(launch_pred_rhs_n(ctx, n, c, q, x, z, zeta, rD, rho, d, rd, rxz, xiau, t));
+    NYS_TRY(launch_pred_rhs_n(ctx, n, x, z, zeta, rD, rho, d, rd, rxz, xiau, t));
     NYS_TRY(launch_pred_rhs_m(ctx, m, b, ax, y, lam, delta, rp));
     NYS_TRY(apply_A(ctx, m, n, A, lda, t, xi, 1.0, rp));             // xi = r_p + A d (r_d + xi_au)
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
