@@ -42,6 +42,10 @@ struct MatvecParams {
   int64_t npanels;
   int stages;
   int cl;
+  double* pwp;          // FUSED: per-CTA partial of v^T (A D A^T + delta I + diag e) v  (or null)
+  double delta;
+  const double* e;
+  double* tbuf;         // TONLY: raw column dots (A^T v)_j, epilogue applied after the loop
 };
 
 __device__ __forceinline__ void t_epilogue(const MatvecParams& P, int64_t j, double s) {
@@ -104,6 +108,7 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
   const int lig = tid % GT;
   double vreg[VS ? 1 : RPT];
   double wacc[RPT];
+  double pwacc = 0.0;
 #pragma unroll
   for (int i = 0; i < RPT; ++i) { if (!VS) vreg[i] = 0.0; wacc[i] = 0.0; }
 
@@ -218,11 +223,15 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
         if (MODE == MV_FUSED) {
 #pragma unroll
           for (int c = 0; c < CPG; ++c) t[c] = (col0 + c < P.n) ? P.d[col0 + c] * pd[c] : 0.0;
-        } else {  // MV_TONLY
+          if (lig == 0 && crank == 0) {
+#pragma unroll
+            for (int c = 0; c < CPG; ++c) pwacc = fma(t[c], pd[c], pwacc);  // d_j (a_j^T v)^2
+          }
+        } else {  // MV_TONLY: raw dot to global; the epilogue runs after the loop (no stall here)
           if (crank == 0) {
 #pragma unroll
             for (int c = 0; c < CPG; ++c)
-              if (lig == c && col0 + c < P.n) t_epilogue(P, col0 + c, pd[c]);
+              if (lig == c && col0 + c < P.n) P.tbuf[col0 + c] = pd[c];
           }
         }
       } else {
@@ -241,6 +250,39 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
     }
   }
 
+  if (MODE == MV_TONLY) {
+    __syncthreads();  // this CTA's raw dots are visible to all its threads
+    if (crank == 0) {
+      for (int64_t it = 0; it < niter; ++it) {
+        const int64_t c0 = (int64_t)(cid + it * ncl) * BN;
+        for (int c = tid; c < BN; c += T + 32)
+          if (c0 + c < P.n) t_epilogue(P, c0 + c, P.tbuf[c0 + c]);
+      }
+    }
+  }
+  if (MODE == MV_FUSED && P.pwp != nullptr) {
+    // row part of v^T (delta I + diag e) v, once (cluster 0, group 0), then CTA partial
+    if (cid == 0 && g == 0 && tid < T) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t rl = lig + (int64_t)GT * i;
+        if (rl < rows_valid) {
+          const double v = VS ? vsm[rl] : vreg[VS ? 0 : i];
+          pwacc = fma((P.delta + (P.e ? P.e[r0 + rl] : 0.0)) * v, v, pwacc);
+        }
+      }
+    }
+    __shared__ double pws[32];
+    const double wsum = warp_sum(pwacc);
+    __syncthreads();
+    if (lane == 0) pws[warp] = wsum;
+    __syncthreads();
+    if (tid == 0) {
+      double b = 0.0;
+      for (int w = 0; w < (T + 32) / 32; ++w) b += pws[w];
+      P.pwp[blockIdx.x] = b;
+    }
+  }
   if (MODE != MV_TONLY) {
     __syncthreads();  // all bulk copies consumed: the stage memory is free for the group sum
     double* outp = P.Wp + (size_t)cid * P.wp_ld + r0;
@@ -298,34 +340,44 @@ struct FinParams {
   const double* done;
 };
 
+// 64 rows x 4 partial groups per 256-thread block; fixed summation order (deterministic)
 __global__ void __launch_bounds__(256) mv_finalize(const FinParams F) {
   if (F.done != nullptr && *F.done != 0.0) return;
+  __shared__ double red[4][64];
   __shared__ double sred[8];
   __shared__ bool am_last;
+  const int tid = threadIdx.x, row = tid & 63, grp = tid >> 6;
   double dot = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.m; i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < F.nparts; ++k) s += F.Wp[(size_t)k * F.wp_ld + i];
-    s *= F.sgn;
-    if (F.use_delta) s += (F.delta + (F.e ? F.e[i] : 0.0)) * F.v[i];
-    if (F.add) s += F.add[i];
-    F.out[i] = s;
-    if (F.pcg_alpha) dot = fma(F.v[i], s, dot);
+  for (int64_t i0 = (int64_t)blockIdx.x * 64; i0 < F.m; i0 += (int64_t)gridDim.x * 64) {
+    const int64_t i = i0 + row;
+    double acc = 0.0;
+    if (i < F.m)
+      for (int k = grp; k < F.nparts; k += 4) acc += F.Wp[(size_t)k * F.wp_ld + i];
+    red[grp][row] = acc;
+    __syncthreads();
+    if (tid < 64 && i < F.m) {
+      double s = ((red[0][row] + red[1][row]) + (red[2][row] + red[3][row])) * F.sgn;
+      if (F.use_delta) s += (F.delta + (F.e ? F.e[i] : 0.0)) * F.v[i];
+      if (F.add) s += F.add[i];
+      F.out[i] = s;
+      if (F.pcg_alpha) dot = fma(F.v[i], s, dot);
+    }
+    __syncthreads();
   }
   if (!F.pcg_alpha) return;
   dot = warp_sum(dot);
-  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = dot;
+  if ((tid & 31) == 0) sred[tid >> 5] = dot;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     double b = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += sred[w];
+    for (int w = 0; w < 8; ++w) b += sred[w];
     F.part[blockIdx.x] = b;
     __threadfence();
     const unsigned prev = atomicAdd(F.counter, 1u);
     am_last = (prev == gridDim.x - 1);
   }
   __syncthreads();
-  if (am_last && threadIdx.x == 0) {
+  if (am_last && tid == 0) {
     __threadfence();
     double pw = 0.0;
     for (unsigned b = 0; b < gridDim.x; ++b) pw += ((volatile double*)F.part)[b];
@@ -457,6 +509,9 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
   const int64_t wp_ld = (c.m + 1) & ~int64_t(1);
   double* Wp = nullptr;
   if (c.mode != MV_TONLY) Wp = ctx->wsd("mv_partials", (size_t)pl.nparts * wp_ld);
+  double* pwp = nullptr;
+  if (c.mode == MV_FUSED && c.pcg_fused) pwp = ctx->wsd("mv_pwp", (size_t)pl.grid);
+  double* tbuf = (c.mode == MV_TONLY) ? ctx->wsd("mv_tbuf", (size_t)(c.n > 0 ? c.n : 1)) : nullptr;
   if (c.n > 0 || c.mode == MV_TONLY) {
     MatvecParams P{};
     P.A = c.A; P.lda = c.lda; P.m = c.m; P.n = c.n;
@@ -464,6 +519,7 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
     P.Wp = Wp; P.wp_ld = wp_ld;
     P.tep = c.tep; P.t1 = c.t1; P.t2 = c.t2; P.ta = c.ta; P.tb = c.tb; P.tc = c.tc; P.td = c.td; P.tx = c.tx; P.tdd = c.tdd;
     P.done = c.done; P.rs = pl.rs; P.npanels = pl.npanels; P.stages = pl.stages; P.cl = pl.cl;
+    P.pwp = pwp; P.delta = c.delta; P.e = c.e; P.tbuf = tbuf;
     MvKernel k = (c.mode == MV_FUSED) ? kernel_for<MV_FUSED>(pl.cfg) : (c.mode == MV_TONLY) ? kernel_for<MV_TONLY>(pl.cfg) : kernel_for<MV_NONLY>(pl.cfg);
     if (c.n > 0) {
       cudaLaunchConfig_t cfg = {};
@@ -487,6 +543,13 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
   if (c.n <= 0) {  // empty shard: zero partial
     NYS_CUDA_TRY(ctx, cudaMemsetAsync(Wp, 0, sizeof(double) * (size_t)pl.nparts * wp_ld, ctx->stream));
   }
+  if (c.pcg_fused) {  // the PCG update kernel consumes the partials directly (no finalize)
+    if (c.fused_out) {
+      c.fused_out->Wp = Wp; c.fused_out->wp_ld = wp_ld; c.fused_out->nparts = pl.nparts;
+      c.fused_out->pwp = pwp; c.fused_out->npw = pl.grid;
+    }
+    return NYS_OK;
+  }
   if (c.out == nullptr) return NYS_OK;
   FinParams F{};
   F.Wp = Wp; F.wp_ld = wp_ld; F.nparts = pl.nparts; F.m = c.m; F.sgn = c.sgn;
@@ -495,7 +558,7 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
   F.add = c.add; F.out = c.out; F.pcg_alpha = c.pcg_alpha ? 1 : 0; F.sc = ctx->sc;
   F.counter = ctx->counters + 0;
   F.done = c.done;
-  int fgrid = (int)((c.m + 255) / 256);
+  int fgrid = (int)((c.m + 63) / 64);
   if (fgrid > 2 * ctx->num_sms) fgrid = 2 * ctx->num_sms;
   F.part = ctx->wsd("fin_part", (size_t)fgrid);
   mv_finalize<<<fgrid, 256, 0, ctx->stream>>>(F);

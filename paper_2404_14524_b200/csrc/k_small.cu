@@ -110,14 +110,16 @@ int launch_add_eomega(nys_ctx* ctx, int64_t m, int ell, const double* e, const d
 __global__ void __launch_bounds__(1024) chol_inv_kernel(int ell, double* G, int ldg, double* Rinv, int ldr,
                                                         int shift_mode, double* sc, double* gws, int use_smem) {
   extern __shared__ double csm[];
-  double* W = use_smem ? csm : gws;  // ell x ell, ld = ell
   const int n = ell;
+  double* W = use_smem ? csm : gws;      // ell x ell, ld = ell : the factor R
+  double* X = W + (size_t)n * n;         // ell x ell, ld = ell : R^{-1}
   __shared__ int fail;
   __shared__ double shift;
   if (threadIdx.x == 0) fail = 0;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e % n, j = e / n;
     W[i + j * n] = 0.5 * (G[i + j * ldg] + G[j + i * ldg]);
+    X[i + j * n] = 0.0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(int ell, double* G, int 
     for (int i = threadIdx.x; i < n; i += blockDim.x) W[i + i * n] += shift;
     __syncthreads();
   }
-  // right-looking Cholesky on the upper triangle: W(k,k) = sqrt, row k scaled, trailing update
+  // right-looking Cholesky on the upper triangle: R(k,k) = sqrt, row k scaled, trailing update
   for (int k = 0; k < n; ++k) {
     if (threadIdx.x == 0) {
       const double piv = W[k + k * n];
@@ -148,15 +150,9 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(int ell, double* G, int 
     for (int j = k + 1 + threadIdx.x; j < n; j += blockDim.x) W[k + j * n] /= rkk;
     __syncthreads();
     const int rem = n - k - 1;
-    const int tri = rem * (rem + 1) / 2;
-    for (int e = threadIdx.x; e < tri; e += blockDim.x) {
-      // map e -> (i, j) with k < i <= j, column-major over the upper trailing triangle
-      int jj = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-      while ((jj + 1) * (jj + 2) / 2 <= e) ++jj;
-      while (jj * (jj + 1) / 2 > e) --jj;
-      const int ii = e - jj * (jj + 1) / 2;
-      const int i = k + 1 + ii, j = k + 1 + jj;
-      W[i + j * n] -= W[k + i * n] * W[k + j * n];
+    for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
+      const int i = k + 1 + e % rem, j = k + 1 + e / rem;
+      if (i <= j) W[i + j * n] -= W[k + i * n] * W[k + j * n];
     }
     __syncthreads();
   }
@@ -164,39 +160,38 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(int ell, double* G, int 
     if (threadIdx.x == 0) sc[S_CHOLFAIL] = 1.0;
     return;
   }
-  // write R (upper) back into G
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e % n, j = e / n;
-    G[i + j * ldg] = (i <= j) ? W[i + j * n] : 0.0;
-  }
-  __syncthreads();
-  // R^{-1} (upper) by backward substitution, one row i per step, all columns j >= i in parallel:
-  // X(i,j) = (delta_ij - sum_{k=i+1..j} R(i,k) X(k,j)) / R(i,i); X stored in Rinv.
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e % n, j = e / n;
-    Rinv[i + j * ldr] = 0.0;
-  }
-  __syncthreads();
+  // R^{-1} (upper) by backward substitution, row i per step, all columns j >= i in parallel:
+  // X(i,j) = (delta_ij - sum_{k=i+1..j} R(i,k) X(k,j)) / R(i,i)
   for (int i = n - 1; i >= 0; --i) {
     const double rii = W[i + i * n];
     for (int j = i + threadIdx.x; j < n; j += blockDim.x) {
-      double s = (i == j) ? 1.0 : 0.0;
-      for (int k = i + 1; k <= j; ++k) s -= W[i + k * n] * Rinv[k + j * ldr];
-      Rinv[i + j * ldr] = s / rii;
+      double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0;
+      int k = i + 1;
+      for (; k + 1 <= j; k += 2) {
+        s0 -= W[i + k * n] * X[k + j * n];
+        s1 -= W[i + (k + 1) * n] * X[(k + 1) + j * n];
+      }
+      if (k <= j) s0 -= W[i + k * n] * X[k + j * n];
+      X[i + j * n] = (s0 + s1) / rii;
     }
     __syncthreads();
+  }
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    G[i + j * ldg] = (i <= j) ? W[i + j * n] : 0.0;
+    Rinv[i + j * ldr] = X[i + j * n];
   }
 }
 
 int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int ldr, int shift_mode) {
-  const size_t need = (size_t)ell * ell * sizeof(double);
-  const int use_smem = need <= 160 * 1024 ? 1 : 0;
-  double* gws = use_smem ? nullptr : ctx->wsd("chol_ws", (size_t)ell * ell);
+  const size_t need = 2 * (size_t)ell * ell * sizeof(double);
+  const int use_smem = need <= 200 * 1024 ? 1 : 0;
+  double* gws = use_smem ? nullptr : ctx->wsd("chol_ws", 2 * (size_t)ell * ell);
   if (use_smem) {
-    static size_t set = 0;
-    if (need > set) {
-      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(160 * 1024)));
-      set = 160 * 1024;
+    static bool set = false;
+    if (!set) {
+      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      set = true;
     }
   }
   chol_inv_kernel<<<1, 1024, use_smem ? need : 0, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc, gws,
@@ -204,7 +199,6 @@ int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int
   ctx->launches++;
   return ctx->check_launch("chol_inv");
 }
-
 
 // Out = R1 * R2 for upper-triangular ell x ell (all with leading dimension ld)
 __global__ void trmm_upper_kernel(int n, int ld, const double* R1, const double* R2, double* Out) {
@@ -245,8 +239,8 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
   __syncthreads();
   const int P = (n % 2 == 0) ? n : n + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const double tol = 1e-15;
-  for (int sweep = 0; sweep < 40; ++sweep) {
+  const double tol = fmax(1e-15, (double)n * 0x1p-53);
+  for (int sweep = 0; sweep < 30; ++sweep) {
     if (threadIdx.x == 0) rotated = 0;
     __syncthreads();
     for (int r = 0; r < P - 1; ++r) {

@@ -286,10 +286,12 @@ int launch_steps_post(nys_ctx* ctx) {
 }
 
 // ------------------------------------------------------------------------------------------
-// PCG kernels
+// PCG kernels.  Rows are processed in chunks of 64 (a block owns `nsub` consecutive chunks).
 // ------------------------------------------------------------------------------------------
-// update: (init) x = 0, r = rhs  |  (iter) x += alpha p, r -= alpha w ;
-//         rr = r^T r ; g = U^T r ; last block: convergence, h = s o g  (P^{-1} coefficients)
+// update:  alpha = rz / p^T w  (p^T w from the matvec's per-CTA partials, summed identically by
+//          every block) ; w_i = sum_c Wp[c][i] + (delta + e_i) p_i  (or given) ;
+//          x += alpha p ; r -= alpha w  |  (init) x = 0, r = rhs ;
+//          rr = r^T r ; g = U^T r ; last block: convergence test, h = s o g  (P^{-1} coefficients)
 struct PcgUpdArgs {
   int init;
   int64_t m;
@@ -297,55 +299,126 @@ struct PcgUpdArgs {
   double* r;
   const double* rhs;
   const double* p;
-  const double* w;
+  const double* w;      // given w (multi-GPU path) or null
+  const double* Wp;     // fused partials (world == 1)
+  int64_t wp_ld;
+  int nparts;
+  const double* pwp;
+  int npw;
+  double delta;
+  const double* e;
   const double* U;
   int64_t ldu;
   int ell;
-  const double* s;     // ell coefficients: (lam_l + mu)/(lam_i + mu) - 1
-  double* h;           // ell out
+  const double* s;
+  double* h;
   double* sc;
-  double* part;        // (1 + ell) x grid
+  double* part;         // (1 + ell) x grid
   unsigned int* counter;
   int max_iter;
-  int64_t rows_per_block;
+  int nsub;             // 64-row chunks per block
 };
+
+constexpr int PCG_RB = 64;
+constexpr int PCG_MAXCW = 32;  // max columns per warp (ell <= 256 with 8 warps)
 
 __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
   if (A.sc[S_DONE] != 0.0) return;
-  extern __shared__ double rsh[];  // rows_per_block
-  const int64_t i0 = blockIdx.x * A.rows_per_block;
-  int64_t i1 = i0 + A.rows_per_block;
-  if (i1 > A.m) i1 = A.m;
-  const double alpha = A.init ? 0.0 : A.sc[S_ALPHA];
-  double rr = 0.0;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    double ri;
-    if (A.init) {
-      ri = A.rhs[i];
-      A.x[i] = 0.0;
-    } else {
-      A.x[i] = fma(alpha, A.p[i], A.x[i]);
-      ri = fma(-alpha, A.w[i], A.r[i]);
+  __shared__ double red[4][PCG_RB];
+  __shared__ double rsh[PCG_RB];
+  __shared__ double s_alpha;
+  __shared__ int s_ok;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (!A.init) {
+    if (warp == 0) {
+      double pw;
+      if (A.w != nullptr) {
+        pw = A.sc[S_PW];
+      } else {
+        double acc = 0.0;
+        for (int b = lane; b < A.npw; b += 32) acc += A.pwp[b];
+        pw = warp_sum(acc);
+      }
+      if (lane == 0) {
+        const bool ok = (pw > 0.0) && isfinite(pw);
+        s_ok = ok ? 1 : 0;
+        s_alpha = ok ? A.sc[S_RZ] / pw : 0.0;
+        if (blockIdx.x == 0) {
+          A.sc[S_PW] = pw;
+          A.sc[S_ALPHA] = s_alpha;
+        }
+      }
     }
-    A.r[i] = ri;
-    rsh[i - i0] = ri;
-    rr = fma(ri, ri, rr);
+    __syncthreads();
+    if (!s_ok) {
+      if (blockIdx.x == 0 && tid == 0) { A.sc[S_STATUS] = (double)NYS_EBREAKDOWN; A.sc[S_DONE] = 1.0; }
+      return;
+    }
+  }
+  const double alpha = A.init ? 0.0 : s_alpha;
+  double gacc[PCG_MAXCW];
+#pragma unroll
+  for (int k = 0; k < PCG_MAXCW; ++k) gacc[k] = 0.0;
+  double rr = 0.0;
+  const int row = tid & (PCG_RB - 1), grp = tid >> 6;  // 64 rows x 4 groups
+  for (int sub = 0; sub < A.nsub; ++sub) {
+    const int64_t i0 = ((int64_t)blockIdx.x * A.nsub + sub) * PCG_RB;
+    if (i0 >= A.m) break;
+    const int64_t i = i0 + row;
+    if (!A.init && A.w == nullptr) {
+      double acc = 0.0;
+      if (i < A.m)
+        for (int c = grp; c < A.nparts; c += 4) acc += A.Wp[(size_t)c * A.wp_ld + i];
+      red[grp][row] = acc;
+    }
+    __syncthreads();
+    if (tid < PCG_RB) {
+      double ri = 0.0;
+      if (i < A.m) {
+        if (A.init) {
+          ri = A.rhs[i];
+          A.x[i] = 0.0;
+        } else {
+          const double pi = A.p[i];
+          double wi;
+          if (A.w != nullptr) wi = A.w[i];
+          else wi = ((red[0][row] + red[1][row]) + (red[2][row] + red[3][row])) + (A.delta + (A.e ? A.e[i] : 0.0)) * pi;
+          A.x[i] = fma(alpha, pi, A.x[i]);
+          ri = fma(-alpha, wi, A.r[i]);
+        }
+        A.r[i] = ri;
+      }
+      rsh[row] = ri;
+      rr = fma(ri, ri, rr);
+    }
+    __syncthreads();
+    // U^T r partial over this chunk: warp w owns columns w, w+8, ...
+#pragma unroll
+    for (int k = 0; k < PCG_MAXCW; ++k) {
+      const int c = warp + 8 * k;
+      if (c < A.ell) {
+        const double* Uc = A.U + (size_t)c * A.ldu;
+        double a = 0.0;
+        if (i0 + lane < A.m) a = Uc[i0 + lane] * rsh[lane];
+        if (i0 + lane + 32 < A.m) a = fma(Uc[i0 + lane + 32], rsh[lane + 32], a);
+        gacc[k] += a;
+      }
+    }
+    __syncthreads();
   }
   double v[1] = {rr};
   block_sum_to_part<1>(v, A.part, gridDim.x);
-  __syncthreads();
-  // g partials: warp per column
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int c = w; c < A.ell; c += nw) {
-    double acc = 0.0;
-    const double* Uc = A.U + (size_t)c * A.ldu;
-    for (int64_t i = i0 + l; i < i1; i += 32) acc = fma(Uc[i], rsh[i - i0], acc);
-    acc = warp_sum(acc);
-    if (l == 0) A.part[(size_t)(1 + c) * gridDim.x + blockIdx.x] = acc;
+#pragma unroll
+  for (int k = 0; k < PCG_MAXCW; ++k) {
+    const int c = warp + 8 * k;
+    if (c < A.ell) {
+      const double g = warp_sum(gacc[k]);
+      if (lane == 0) A.part[(size_t)(1 + c) * gridDim.x + blockIdx.x] = g;
+    }
   }
   if (last_block_arrive(A.counter)) {
     __shared__ int conv;
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       const double rrt = ordered_sum(A.part, gridDim.x);
       A.sc[S_RR] = rrt;
       double iters = A.sc[S_ITERS];
@@ -365,7 +438,8 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
     }
     __syncthreads();
     if (!conv) {
-      for (int c = threadIdx.x; c < A.ell; c += blockDim.x) A.h[c] = A.s[c] * ordered_sum(A.part + (size_t)(1 + c) * gridDim.x, gridDim.x);
+      for (int c = tid; c < A.ell; c += blockDim.x)
+        A.h[c] = A.s[c] * ordered_sum(A.part + (size_t)(1 + c) * gridDim.x, gridDim.x);
     }
   }
 }
@@ -384,21 +458,34 @@ struct PcgPrecArgs {
   double* sc;
   double* part;
   unsigned int* counter;
+  int nsub;
 };
 
 __global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
   if (A.sc[S_DONE] != 0.0) return;
-  extern __shared__ double hsh[];
-  for (int c = threadIdx.x; c < A.ell; c += blockDim.x) hsh[c] = A.h[c];
+  __shared__ double hsh[256];
+  __shared__ double red[4][PCG_RB];
+  const int tid = threadIdx.x;
+  for (int c = tid; c < A.ell; c += blockDim.x) hsh[c] = A.h[c];
   __syncthreads();
+  const int row = tid & (PCG_RB - 1), grp = tid >> 6;
   double rz = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.m; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int sub = 0; sub < A.nsub; ++sub) {
+    const int64_t i0 = ((int64_t)blockIdx.x * A.nsub + sub) * PCG_RB;
+    if (i0 >= A.m) break;
+    const int64_t i = i0 + row;
     double acc = 0.0;
-    for (int c = 0; c < A.ell; ++c) acc = fma(A.U[(size_t)c * A.ldu + i], hsh[c], acc);
-    const double ri = A.r[i];
-    const double zi = ri + acc;
-    A.z[i] = zi;
-    rz = fma(ri, zi, rz);
+    if (i < A.m)
+      for (int c = grp; c < A.ell; c += 4) acc = fma(A.U[(size_t)c * A.ldu + i], hsh[c], acc);
+    red[grp][row] = acc;
+    __syncthreads();
+    if (tid < PCG_RB && i < A.m) {
+      const double ri = A.r[i];
+      const double zi = ri + ((red[0][row] + red[1][row]) + (red[2][row] + red[3][row]));
+      A.z[i] = zi;
+      rz = fma(ri, zi, rz);
+    }
+    __syncthreads();
   }
   double v[1] = {rz};
   block_sum_to_part<1>(v, A.part, gridDim.x);
@@ -412,19 +499,28 @@ __global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
   }
 }
 
+static void pcg_grid(nys_ctx* ctx, int64_t m, int& grid, int& nsub) {
+  const int64_t chunks = (m + PCG_RB - 1) / PCG_RB;
+  nsub = (int)((chunks + ctx->num_sms - 1) / ctx->num_sms);
+  if (nsub < 1) nsub = 1;
+  grid = (int)((chunks + nsub - 1) / nsub);
+  if (grid < 1) grid = 1;
+}
+
 int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, const double* rhs, const double* p,
-                      const double* w, const double* U, int64_t ldu, int ell, const double* s, double* h,
-                      int max_iter) {
+                      const double* w, const FusedPartials* fp, double delta, const double* e, const double* U,
+                      int64_t ldu, int ell, const double* s, double* h, int max_iter) {
   PcgUpdArgs A{};
-  A.init = init; A.m = m; A.x = x; A.r = r; A.rhs = rhs; A.p = p; A.w = w; A.U = U; A.ldu = ldu; A.ell = ell;
-  A.s = s; A.h = h; A.sc = ctx->sc; A.max_iter = max_iter;
-  int64_t rpb = 256;
-  int64_t g = (m + rpb - 1) / rpb;
-  if (g > ctx->num_sms) { g = ctx->num_sms; rpb = (m + g - 1) / g; }
-  A.rows_per_block = rpb;
+  A.init = init; A.m = m; A.x = x; A.r = r; A.rhs = rhs; A.p = p; A.w = w;
+  if (fp) { A.Wp = fp->Wp; A.wp_ld = fp->wp_ld; A.nparts = fp->nparts; A.pwp = fp->pwp; A.npw = fp->npw; }
+  A.delta = delta; A.e = e;
+  A.U = U; A.ldu = ldu; A.ell = ell; A.s = s; A.h = h; A.sc = ctx->sc; A.max_iter = max_iter;
+  int g, nsub;
+  pcg_grid(ctx, m, g, nsub);
+  A.nsub = nsub;
   A.part = ctx->wsd("pcg_upd_part", (size_t)(1 + ell) * g);
   A.counter = ctx->counters + 1;
-  pcg_update_kernel<<<(unsigned)g, 256, rpb * sizeof(double), ctx->stream>>>(A);
+  pcg_update_kernel<<<(unsigned)g, 256, 0, ctx->stream>>>(A);
   ctx->launches++;
   return ctx->check_launch("pcg_update");
 }
@@ -433,11 +529,12 @@ int launch_pcg_precond(nys_ctx* ctx, int init, int64_t m, const double* r, doubl
                        int ell, const double* h) {
   PcgPrecArgs A{};
   A.init = init; A.m = m; A.r = r; A.z = z; A.U = U; A.ldu = ldu; A.ell = ell; A.h = h; A.sc = ctx->sc;
-  int g = (int)((m + 255) / 256);
-  if (g > ctx->num_sms) g = ctx->num_sms;
+  int g, nsub;
+  pcg_grid(ctx, m, g, nsub);
+  A.nsub = nsub;
   A.part = ctx->wsd("pcg_prec_part", (size_t)g);
   A.counter = ctx->counters + 2;
-  pcg_precond_kernel<<<g, 256, (size_t)(ell > 0 ? ell : 1) * sizeof(double), ctx->stream>>>(A);
+  pcg_precond_kernel<<<g, 256, 0, ctx->stream>>>(A);
   ctx->launches++;
   return ctx->check_launch("pcg_precond");
 }

@@ -14,8 +14,8 @@ int launch_ratio(nys_ctx* ctx, int64_t n, const double* x, double* dx, const dou
                  const double* z, double* dz, const double* dz1, const double* dz2, int counter_slot);
 int launch_steps_post(nys_ctx* ctx);
 int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, const double* rhs, const double* p,
-                      const double* w, const double* U, int64_t ldu, int ell, const double* s, double* h,
-                      int max_iter);
+                      const double* w, const FusedPartials* fp, double delta, const double* e, const double* U,
+                      int64_t ldu, int ell, const double* s, double* h, int max_iter);
 int launch_pcg_precond(nys_ctx* ctx, int init, int64_t m, const double* r, double* z, const double* U, int64_t ldu,
                        int ell, const double* h);
 int launch_prec_coef(nys_ctx* ctx, const double* lam, int ell, double mu, double* s);

@@ -306,16 +306,32 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
   double* h = ctx->wsd("pcg_h", (size_t)(ell > 0 ? ell : 1));
   double* Pp[2] = {P0, P1};
   const double* done = ctx->sc + S_DONE;
-  NYS_TRY(launch_pcg_update(ctx, 1, m, x, r, rhs, nullptr, nullptr, U, ldu, ell, s, h, max_iter));
+  NYS_TRY(launch_pcg_update(ctx, 1, m, x, r, rhs, nullptr, nullptr, nullptr, op.delta, op.e, U, ldu, ell, s, h,
+                            max_iter));
   if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 1, m, r, z, U, ldu, ell, h));
   int it = 0;
   int batch = 4;
+  const bool fused = (ctx->world == 1);
   for (;;) {
     for (int b = 0; b < batch; ++b, ++it) {
       const double* pold = (it == 0) ? nullptr : Pp[it & 1];
       double* pnew = Pp[(it + 1) & 1];
-      NYS_TRY(apply_normal_full(ctx, op, z, pold, ctx->sc + S_BETA, pnew, w, true, done));
-      NYS_TRY(launch_pcg_update(ctx, 0, m, x, r, nullptr, pnew, w, U, ldu, ell, s, h, max_iter));
+      if (fused) {
+        // K1 leaves per-cluster w partials and per-CTA p^T N p partials; pcg_update consumes them
+        MatvecCall c;
+        c.mode = MV_FUSED; c.m = m; c.n = op.n; c.lda = op.lda; c.A = op.A; c.z = z; c.p = pold;
+        c.beta = ctx->sc + S_BETA; c.p_out = pnew; c.d = op.d; c.done = done; c.delta = op.delta; c.e = op.e;
+        c.pcg_fused = true;
+        FusedPartials fp;
+        c.fused_out = &fp;
+        NYS_TRY(launch_matvec(ctx, c));
+        NYS_TRY(launch_pcg_update(ctx, 0, m, x, r, nullptr, pnew, nullptr, &fp, op.delta, op.e, U, ldu, ell, s, h,
+                                  max_iter));
+      } else {
+        NYS_TRY(apply_normal_full(ctx, op, z, pold, ctx->sc + S_BETA, pnew, w, true, done));
+        NYS_TRY(launch_pcg_update(ctx, 0, m, x, r, nullptr, pnew, w, nullptr, op.delta, op.e, U, ldu, ell, s, h,
+                                  max_iter));
+      }
       if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 0, m, r, z, U, ldu, ell, h));
     }
     NYS_TRY(read_slots(ctx));

@@ -177,6 +177,15 @@ __device__ __forceinline__ double warp_min(double v) {
 namespace nys {
 
 enum MatvecMode { MV_FUSED = 0, MV_TONLY = 1, MV_NONLY = 2 };
+
+// where the fused PCG matvec left its per-cluster w partials and per-CTA p^T N p partials
+struct FusedPartials {
+  const double* Wp = nullptr;
+  int64_t wp_ld = 0;
+  int nparts = 0;
+  const double* pwp = nullptr;
+  int npw = 0;
+};
 enum TEpilogue { TE_PLAIN = 0, TE_DX = 1, TE_RD = 2 };
 
 struct MatvecCall {
@@ -210,6 +219,8 @@ struct MatvecCall {
   const double* tx = nullptr;       // DX: x
   const double* tdd = nullptr;      // DX: d
   const double* done = nullptr;     // early-exit flag (device scalar), or null
+  bool pcg_fused = false;           // FUSED for PCG (world == 1): partials only, consumed by pcg_update
+  FusedPartials* fused_out = nullptr;
 };
 int launch_matvec(nys_ctx* ctx, const MatvecCall& c);
 
