@@ -86,6 +86,7 @@ typedef struct {
   int    chol_retries;   /* number of nu <- 10 nu retries                     */
   double orth_err;       /* ||U^T U - I||_F of the returned U                             */
   double t_ms;           /* device time of the whole call                                  */
+  int    jacobi_sweeps;  /* sweeps of the ell x ell one-sided Jacobi SVD                   */
 } nys_sketch_info;
 
 /* ---------------------------------------------------------------------------------------

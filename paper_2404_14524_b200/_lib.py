@@ -27,7 +27,8 @@ class NysError(RuntimeError):
 
 
 class SketchInfo(C.Structure):
-    _fields_ = [("nu", C.c_double), ("chol_retries", C.c_int), ("orth_err", C.c_double), ("t_ms", C.c_double)]
+    _fields_ = [("nu", C.c_double), ("chol_retries", C.c_int), ("orth_err", C.c_double), ("t_ms", C.c_double),
+                ("jacobi_sweeps", C.c_int)]
 
 
 class PcgInfo(C.Structure):

@@ -18,6 +18,8 @@
 //
 // The same kernel also provides the T-only pass (A^T v with IPM epilogues) and the N-only
 // pass (A u) that Alg. 4 needs.
+#include <cstdlib>
+
 #include "nys_common.cuh"
 
 namespace nys {
@@ -42,6 +44,8 @@ struct MatvecParams {
   int64_t npanels;
   int stages;
   int cl;
+  int rc;               // reduction cluster size (cl == 1 only): CTAs of a cluster sum their w partials via DSMEM
+  const double* delta_slot;  // if set, delta = *delta_slot
   double* pwp;          // FUSED: per-CTA partial of v^T (A D A^T + delta I + diag e) v  (or null)
   double delta;
   const double* e;
@@ -85,6 +89,7 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  const int rc = P.rc;
   const uint32_t crank = cl > 1 ? cluster_ctarank() : 0u;
   const uint32_t cid = cl > 1 ? cluster_id_x() : blockIdx.x;
   const uint32_t ncl = cl > 1 ? ncluster_x() : gridDim.x;
@@ -253,10 +258,9 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
   if (MODE == MV_TONLY) {
     __syncthreads();  // this CTA's raw dots are visible to all its threads
     if (crank == 0) {
-      for (int64_t it = 0; it < niter; ++it) {
-        const int64_t c0 = (int64_t)(cid + it * ncl) * BN;
-        for (int c = tid; c < BN; c += T + 32)
-          if (c0 + c < P.n) t_epilogue(P, c0 + c, P.tbuf[c0 + c]);
+      for (int64_t e = tid; e < niter * BN; e += T + 32) {
+        const int64_t j = (int64_t)(cid + (e / BN) * ncl) * BN + (e % BN);
+        if (j < P.n) t_epilogue(P, j, P.tbuf[j]);
       }
     }
   }
@@ -268,7 +272,8 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
         const int64_t rl = lig + (int64_t)GT * i;
         if (rl < rows_valid) {
           const double v = VS ? vsm[rl] : vreg[VS ? 0 : i];
-          pwacc = fma((P.delta + (P.e ? P.e[r0 + rl] : 0.0)) * v, v, pwacc);
+          const double dl = P.delta_slot ? *P.delta_slot : P.delta;
+          pwacc = fma((dl + (P.e ? P.e[r0 + rl] : 0.0)) * v, v, pwacc);
         }
       }
     }
@@ -283,7 +288,47 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
       P.pwp[blockIdx.x] = b;
     }
   }
-  if (MODE != MV_TONLY) {
+  if (MODE != MV_TONLY && rc > 1) {
+    // CTA total into smem, then the rc CTAs of the cluster each reduce a row range over all
+    // rc CTAs through DSMEM (rank order: deterministic) -> one partial row per cluster
+    __syncthreads();
+    double* wsum = stage;
+    if (tid < T) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t rl = lig + (int64_t)GT * i;
+        if (rl < rows_valid) wsum[(size_t)g * rs + rl] = wacc[i];
+      }
+    }
+    __syncthreads();
+    double* tot = stage + (size_t)NG * rs;
+    if (NG > 1) {
+      for (int64_t r = tid; r < rows_valid; r += T + 32) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg) sacc += wsum[(size_t)gg * rs + r];
+        tot[r] = sacc;
+      }
+    } else {
+      tot = wsum;
+    }
+    __syncwarp();
+    cluster_sync_all();
+    const uint32_t rr_ = cluster_ctarank();
+    const int64_t chunk = (rows_valid + rc - 1) / rc;
+    const int64_t lo = (int64_t)rr_ * chunk;
+    int64_t hi = lo + chunk;
+    if (hi > rows_valid) hi = rows_valid;
+    double* outp = P.Wp + (size_t)cluster_id_x() * P.wp_ld;
+    const uint32_t tbase = smem_u32(tot);
+    for (int64_t r = lo + tid; r < hi; r += T + 32) {
+      double sacc = 0.0;
+      for (int q = 0; q < rc; ++q) sacc += ld_cluster_f64(mapa_shared(tbase + (uint32_t)(r * 8), (uint32_t)q));
+      outp[r] = sacc;
+    }
+    __syncwarp();
+    cluster_sync_all();
+  } else if (MODE != MV_TONLY) {
     __syncthreads();  // all bulk copies consumed: the stage memory is free for the group sum
     double* outp = P.Wp + (size_t)cid * P.wp_ld + r0;
     if (NG == 1) {
@@ -340,23 +385,34 @@ struct FinParams {
   const double* done;
 };
 
-// 64 rows x 4 partial groups per 256-thread block; fixed summation order (deterministic)
+// 16 rows x 16 partial groups per 256-thread block; fixed summation order (deterministic)
 __global__ void __launch_bounds__(256) mv_finalize(const FinParams F) {
   if (F.done != nullptr && *F.done != 0.0) return;
-  __shared__ double red[4][64];
+  __shared__ double red[16][17];
   __shared__ double sred[8];
   __shared__ bool am_last;
-  const int tid = threadIdx.x, row = tid & 63, grp = tid >> 6;
+  const int tid = threadIdx.x, row = tid & 15, grp = tid >> 4;
   double dot = 0.0;
-  for (int64_t i0 = (int64_t)blockIdx.x * 64; i0 < F.m; i0 += (int64_t)gridDim.x * 64) {
+  for (int64_t i0 = (int64_t)blockIdx.x * 16; i0 < F.m; i0 += (int64_t)gridDim.x * 16) {
     const int64_t i = i0 + row;
     double acc = 0.0;
-    if (i < F.m)
-      for (int k = grp; k < F.nparts; k += 4) acc += F.Wp[(size_t)k * F.wp_ld + i];
-    red[grp][row] = acc;
+    if (i < F.m) {
+      double a1 = 0.0;
+      int k = grp;
+      for (; k + 16 < F.nparts; k += 32) {
+        acc += F.Wp[(size_t)k * F.wp_ld + i];
+        a1 += F.Wp[(size_t)(k + 16) * F.wp_ld + i];
+      }
+      if (k < F.nparts) acc += F.Wp[(size_t)k * F.wp_ld + i];
+      acc += a1;
+    }
+    red[row][grp] = acc;
     __syncthreads();
-    if (tid < 64 && i < F.m) {
-      double s = ((red[0][row] + red[1][row]) + (red[2][row] + red[3][row])) * F.sgn;
+    if (tid < 16 && i < F.m) {
+      const double* v = red[row];
+      double s = (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
+                 (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
+      s *= F.sgn;
       if (F.use_delta) s += (F.delta + (F.e ? F.e[i] : 0.0)) * F.v[i];
       if (F.add) s += F.add[i];
       F.out[i] = s;
@@ -377,10 +433,10 @@ __global__ void __launch_bounds__(256) mv_finalize(const FinParams F) {
     am_last = (prev == gridDim.x - 1);
   }
   __syncthreads();
-  if (am_last && tid == 0) {
+  if (am_last && tid < 32) {
     __threadfence();
-    double pw = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) pw += ((volatile double*)F.part)[b];
+    const double pw = warp_sum_array(F.part, gridDim.x);
+    if (tid != 0) return;
     *F.counter = 0u;
     F.sc[S_PW] = pw;
     if (!(pw > 0.0) || !isfinite(pw)) {
@@ -432,6 +488,8 @@ struct MvPlan {
   int64_t npanels = 0;
   int grid = 0;       // CTAs
   int nparts = 0;     // clusters (= partial rows)
+  int rc = 1;         // reduction cluster (cl == 1)
+  int cdim = 1;       // launch cluster dimension (cl or rc)
 };
 
 static bool cfg_vs(const MvCfg& c) { return c.RPT >= 16; }
@@ -470,12 +528,41 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, MvPlan& pl) {
   if (cl > 8) NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const int64_t npanels = (n + BN - 1) / BN;
   int grid = 0;
+  int rc = 1;
+  auto max_clusters = [&](int csize, int& out) -> int {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(csize * ctx->num_sms));
+    cfg.blockDim = dim3((unsigned)(c.T + 32));
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    out = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&out, k, &cfg);
+    if (e != cudaSuccess) { cudaGetLastError(); out = 0; }
+    return NYS_OK;
+  };
   if (cl == 1) {
     int occ = 0;
     NYS_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c.T + 32, smem));
     if (occ < 1) occ = 1;
     int64_t g = (int64_t)ctx->num_sms * occ;
     grid = (int)(npanels < g ? npanels : g);
+    // reduction clusters: pick the cluster size (8 or 4) that keeps >= 95% of the CTAs resident
+    if (mode != MV_TONLY && grid >= 16) {
+      for (int cs : {8, 4}) {
+        int ncs = 0;
+        max_clusters(cs, ncs);
+        int64_t gc = (int64_t)ncs * cs;
+        int64_t need = (npanels + cs - 1) / cs * cs;
+        if (gc > need) gc = need;
+        if (gc >= (int64_t)(0.95 * grid) && gc >= cs) { rc = cs; grid = (int)gc; break; }
+      }
+    }
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(cl * ctx->num_sms));
@@ -497,8 +584,12 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, MvPlan& pl) {
   }
   if (grid < cl) grid = cl;
   pl.cfg = c; pl.cl = cl; pl.rs = rs; pl.stages = stages; pl.smem = smem; pl.npanels = npanels;
-  pl.grid = grid; pl.nparts = grid / cl;
+  pl.grid = grid; pl.rc = rc; pl.cdim = cl > 1 ? cl : rc; pl.nparts = grid / pl.cdim;
   g_plans[key] = pl;
+  if (getenv("NYS_DEBUG"))
+    fprintf(stderr, "[nys] matvec plan mode=%d m=%lld n=%lld: T=%d GT=%d RPT=%d CPG=%d cl=%d rc=%d rs=%lld stages=%d smem=%zu grid=%d nparts=%d npanels=%lld\n",
+            mode, (long long)m, (long long)n, c.T, c.GT, c.RPT, c.CPG, cl, rc, (long long)rs, stages, smem, grid, pl.nparts,
+            (long long)npanels);
   return NYS_OK;
 }
 
@@ -519,7 +610,8 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
     P.Wp = Wp; P.wp_ld = wp_ld;
     P.tep = c.tep; P.t1 = c.t1; P.t2 = c.t2; P.ta = c.ta; P.tb = c.tb; P.tc = c.tc; P.td = c.td; P.tx = c.tx; P.tdd = c.tdd;
     P.done = c.done; P.rs = pl.rs; P.npanels = pl.npanels; P.stages = pl.stages; P.cl = pl.cl;
-    P.pwp = pwp; P.delta = c.delta; P.e = c.e; P.tbuf = tbuf;
+    P.pwp = pwp; P.delta = c.delta; P.e = c.e; P.tbuf = tbuf; P.rc = pl.rc;
+    P.delta_slot = c.delta_from_slot ? ctx->sc + S_DELTA : nullptr;
     MvKernel k = (c.mode == MV_FUSED) ? kernel_for<MV_FUSED>(pl.cfg) : (c.mode == MV_TONLY) ? kernel_for<MV_TONLY>(pl.cfg) : kernel_for<MV_NONLY>(pl.cfg);
     if (c.n > 0) {
       cudaLaunchConfig_t cfg = {};
@@ -529,7 +621,7 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
       cfg.stream = ctx->stream;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = pl.cl;
+      at[0].val.clusterDim.x = pl.cdim;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
@@ -558,7 +650,7 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
   F.add = c.add; F.out = c.out; F.pcg_alpha = c.pcg_alpha ? 1 : 0; F.sc = ctx->sc;
   F.counter = ctx->counters + 0;
   F.done = c.done;
-  int fgrid = (int)((c.m + 63) / 64);
+  int fgrid = (int)((c.m + 15) / 16);
   if (fgrid > 2 * ctx->num_sms) fgrid = 2 * ctx->num_sms;
   F.part = ctx->wsd("fin_part", (size_t)fgrid);
   mv_finalize<<<fgrid, 256, 0, ctx->stream>>>(F);

@@ -32,10 +32,10 @@ __global__ void __launch_bounds__(256) fro_kernel(int64_t m, int ell, const doub
     last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last && threadIdx.x < 32) {
     __threadfence();
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += ((volatile double*)part)[b];
+    const double s = warp_sum_array(part, gridDim.x);
+    if (threadIdx.x != 0) return;
     *counter = 0u;
     const double f = sqrt(s);
     sc[S_FRO] = f;
@@ -107,95 +107,92 @@ int launch_add_eomega(nys_ctx* ctx, int64_t m, int ell, const double* e, const d
 //               with m passed in sc[S_SHIFT] as a double on entry.
 // Failure (non-positive / non-finite pivot) sets sc[S_CHOLFAIL] = 1.
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) chol_inv_kernel(int ell, double* G, int ldg, double* Rinv, int ldr,
-                                                        int shift_mode, double* sc, double* gws, int use_smem) {
+template <bool SM>
+__global__ void __launch_bounds__(256) chol_inv_kernel(int ell, double* G, int ldg, double* Rinv, int ldr,
+                                                       int shift_mode, double* sc, double* gws) {
   extern __shared__ double csm[];
   const int n = ell;
-  double* W = use_smem ? csm : gws;      // ell x ell, ld = ell : the factor R
-  double* X = W + (size_t)n * n;         // ell x ell, ld = ell : R^{-1}
-  __shared__ int fail;
+  const int lx = n | 1;                   // odd leading dimension of X: conflict-free column access
+  double* W = SM ? csm : gws;             // n x n, ld n : the factor
+  double* X = W + (size_t)n * n;          // n x n, ld lx : R^{-1}
+  __shared__ double rsq[256];
   __shared__ double shift;
-  if (threadIdx.x == 0) fail = 0;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  for (int e = tid; e < n * n; e += blockDim.x) {
     const int i = e % n, j = e / n;
     W[i + j * n] = 0.5 * (G[i + j * ldg] + G[j + i * ldg]);
-    X[i + j * n] = 0.0;
   }
+  for (int e = tid; e < n * lx; e += blockDim.x) X[e] = 0.0;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     double s = 0.0;
     if (shift_mode == 1) {
       double tr = 0.0;
       for (int i = 0; i < n; ++i) tr += W[i + i * n];
-      const double mrows = sc[S_SHIFT];
-      s = 11.0 * (mrows * n + (double)n * (n + 1)) * 0x1p-53 * tr;
+      s = 11.0 * (sc[S_SHIFT] * n + (double)n * (n + 1)) * 0x1p-53 * tr;
     }
     shift = s;
   }
   __syncthreads();
   if (shift_mode == 1) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) W[i + i * n] += shift;
+    for (int i = tid; i < n; i += blockDim.x) W[i + i * n] += shift;
     __syncthreads();
   }
-  // right-looking Cholesky on the upper triangle: R(k,k) = sqrt, row k scaled, trailing update
+  // right-looking Cholesky, one barrier per step: the trailing update uses the UNSCALED row k
+  // (a_ij -= a_ki a_kj / a_kk); rows are scaled by 1/sqrt(a_kk) at the end -> R^T R = G.
   for (int k = 0; k < n; ++k) {
-    if (threadIdx.x == 0) {
-      const double piv = W[k + k * n];
-      if (!(piv > 0.0) || !isfinite(piv)) fail = 1;
-      else W[k + k * n] = sqrt(piv);
+    const double piv = W[k + k * n];
+    if (!(piv > 0.0) || !isfinite(piv)) {  // uniform: every thread reads the same pivot
+      if (tid == 0) sc[S_CHOLFAIL] = 1.0;
+      return;
     }
-    __syncthreads();
-    if (fail) break;
-    const double rkk = W[k + k * n];
-    for (int j = k + 1 + threadIdx.x; j < n; j += blockDim.x) W[k + j * n] /= rkk;
-    __syncthreads();
-    const int rem = n - k - 1;
-    for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
-      const int i = k + 1 + e % rem, j = k + 1 + e / rem;
-      if (i <= j) W[i + j * n] -= W[k + i * n] * W[k + j * n];
+    const double inv = 1.0 / piv;
+    for (int j = k + 1 + warp; j < n; j += nw) {
+      const double akj = W[k + j * n] * inv;
+      for (int i = k + 1 + lane; i <= j; i += 32) W[i + j * n] = fma(-W[k + i * n], akj, W[i + j * n]);
     }
     __syncthreads();
   }
-  if (fail) {
-    if (threadIdx.x == 0) sc[S_CHOLFAIL] = 1.0;
-    return;
-  }
-  // R^{-1} (upper) by backward substitution, row i per step, all columns j >= i in parallel:
-  // X(i,j) = (delta_ij - sum_{k=i+1..j} R(i,k) X(k,j)) / R(i,i)
-  for (int i = n - 1; i >= 0; --i) {
-    const double rii = W[i + i * n];
-    for (int j = i + threadIdx.x; j < n; j += blockDim.x) {
-      double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0;
-      int k = i + 1;
-      for (; k + 1 <= j; k += 2) {
-        s0 -= W[i + k * n] * X[k + j * n];
-        s1 -= W[i + (k + 1) * n] * X[(k + 1) + j * n];
-      }
-      if (k <= j) s0 -= W[i + k * n] * X[k + j * n];
-      X[i + j * n] = (s0 + s1) / rii;
-    }
-    __syncthreads();
-  }
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+  for (int i = tid; i < n; i += blockDim.x) rsq[i] = 1.0 / sqrt(W[i + i * n]);
+  __syncthreads();
+  for (int e = tid; e < n * n; e += blockDim.x) {
     const int i = e % n, j = e / n;
-    G[i + j * ldg] = (i <= j) ? W[i + j * n] : 0.0;
-    Rinv[i + j * ldr] = X[i + j * n];
+    W[i + j * n] = (i < j) ? W[i + j * n] * rsq[i] : (i == j ? W[i + j * n] * rsq[i] : 0.0);
+  }
+  __syncthreads();
+  // X = R^{-1}: one thread per column j, column-oriented back substitution in lockstep over i
+  // (x = e_j; for i = n-1..0: x_i /= R_ii; x_k -= R_ki x_i for k < i)
+  for (int j = tid; j < n; j += blockDim.x) X[j + j * lx] = 1.0;
+  for (int i = n - 1; i >= 0; --i) {
+    for (int j = tid; j < n; j += blockDim.x) {
+      if (i <= j) {
+        const double xi = X[i + j * lx] / W[i + i * n];
+        X[i + j * lx] = xi;
+        for (int k = 0; k < i; ++k) X[k + j * lx] = fma(-W[k + i * n], xi, X[k + j * lx]);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    G[i + j * ldg] = W[i + j * n];
+    Rinv[i + j * ldr] = X[i + j * lx];
   }
 }
 
 int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int ldr, int shift_mode) {
-  const size_t need = 2 * (size_t)ell * ell * sizeof(double);
-  const int use_smem = need <= 200 * 1024 ? 1 : 0;
-  double* gws = use_smem ? nullptr : ctx->wsd("chol_ws", 2 * (size_t)ell * ell);
-  if (use_smem) {
+  const size_t need = ((size_t)ell * ell + (size_t)ell * (ell | 1)) * sizeof(double);
+  if (need <= 200 * 1024) {
     static bool set = false;
     if (!set) {
-      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       set = true;
     }
+    chol_inv_kernel<true><<<1, 256, need, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc, nullptr);
+  } else {
+    double* gws = ctx->wsd("chol_ws", (size_t)ell * ell + (size_t)ell * (ell | 1));
+    chol_inv_kernel<false><<<1, 256, 0, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc, gws);
   }
-  chol_inv_kernel<<<1, 1024, use_smem ? need : 0, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc, gws,
-                                                                   use_smem);
   ctx->launches++;
   return ctx->check_launch("chol_inv");
 }
@@ -220,17 +217,39 @@ int launch_trmm_upper(nys_ctx* ctx, int ell, int ld, const double* R1, const dou
 // ------------------------------------------------------------------------------------------
 // one-sided Jacobi on X = R^T (ell x ell): X V = U_X Sigma; then R = V Sigma U_X^T, so the LEFT
 // singular vectors of R are the accumulated rotations V (orthonormal to rounding).
-// Round-robin (circle) ordering: ell/2 disjoint pairs per round, one warp per pair.
-// Output: V (ell x ell, ld ell) and sigma sorted descending (columns of V permuted to match).
+// Round-robin (circle) ordering: ell/2 disjoint pairs per round, one warp per pair; column norms
+// are recomputed exactly each sweep and updated incrementally within it (alpha' = alpha - t gamma,
+// beta' = beta + t gamma), so each pair needs a single dot product.  The rotation angle uses
+// fast reciprocal / square-root approximations refined by Newton steps: only c needs full
+// accuracy (c^2 + s^2 = 1 keeps V orthogonal); t only steers convergence.
+// Output: V (ell x ell, ld ldv) and sigma sorted descending (columns of V permuted to match).
 // ------------------------------------------------------------------------------------------
+__device__ __forceinline__ double fast_rcp(double x) {
+  const double ax = fabs(x);
+  if (!(ax > 1e-30 && ax < 1e30)) return 1.0 / x;
+  double r = (double)__frcp_rn((float)x);
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
+__device__ __forceinline__ double fast_rsqrt(double y) {  // y in [1, 1e30)
+  double r = (double)rsqrtf((float)y);
+  r = r * fma(-0.5 * y * r, r, 1.5);
+  r = r * fma(-0.5 * y * r, r, 1.5);
+  r = r * fma(-0.5 * y * r, r, 1.5);
+  return r;
+}
+
+template <bool SM>
 __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, int ldr, double* Vout, int ldv,
-                                                      double* sigma, double* gws, int use_smem) {
+                                                      double* sigma, double* gws, double* jsweeps) {
   extern __shared__ double jsm[];
-  double* X = use_smem ? jsm : gws;
+  double* X = SM ? jsm : gws;
   double* V = X + (size_t)n * n;
   __shared__ int rotated;
   __shared__ double sv[256];
   __shared__ int order[256];
+  __shared__ double nrm[256];
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e % n, j = e / n;
     X[i + j * n] = R[j + i * ldr];  // X = R^T
@@ -240,30 +259,41 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
   const int P = (n % 2 == 0) ? n : n + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const double tol = fmax(1e-15, (double)n * 0x1p-53);
-  for (int sweep = 0; sweep < 30; ++sweep) {
+  const double tol2 = tol * tol;
+  int sweep = 0;
+  for (; sweep < 30; ++sweep) {
+    for (int j = warp; j < n; j += nw) {
+      double a = 0.0;
+      for (int i = lane; i < n; i += 32) a = fma(X[i + j * n], X[i + j * n], a);
+      a = warp_sum(a);
+      if (lane == 0) nrm[j] = a;
+    }
     if (threadIdx.x == 0) rotated = 0;
     __syncthreads();
     for (int r = 0; r < P - 1; ++r) {
       for (int pi = warp; pi < P / 2; pi += nw) {
         int a, b;
         if (pi == 0) { a = r; b = P - 1; }
-        else { a = (r + pi) % (P - 1); b = (r - pi + (P - 1)) % (P - 1); }
+        else {
+          a = r + pi; if (a >= P - 1) a -= P - 1;
+          b = r - pi; if (b < 0) b += P - 1;
+        }
         if (a >= n || b >= n) continue;
         const int p = a < b ? a : b, q = a < b ? b : a;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < n; i += 32) {
-          const double xp = X[i + p * n], xq = X[i + q * n];
-          al = fma(xp, xp, al);
-          be = fma(xq, xq, be);
-          ga = fma(xp, xq, ga);
-        }
-        al = warp_sum(al);
-        be = warp_sum(be);
+        double ga = 0.0;
+        for (int i = lane; i < n; i += 32) ga = fma(X[i + p * n], X[i + q * n], ga);
         ga = warp_sum(ga);
-        if (fabs(ga) > tol * sqrt(al * be) && ga != 0.0) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t);
+        const double al = nrm[p], be = nrm[q];
+        if (ga * ga > tol2 * al * be && ga != 0.0) {
+          const double zeta = (be - al) * 0.5 * fast_rcp(ga);
+          const double az = fabs(zeta);
+          double t;
+          if (az > 1e8) t = 0.5 * fast_rcp(zeta);
+          else {
+            const double y = fma(zeta, zeta, 1.0);
+            t = copysign(fast_rcp(az + y * fast_rsqrt(y)), zeta);
+          }
+          const double c = fast_rsqrt(fma(t, t, 1.0));
           const double s = c * t;
           for (int i = lane; i < n; i += 32) {
             const double xp = X[i + p * n], xq = X[i + q * n];
@@ -273,7 +303,11 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
             V[i + p * n] = c * vp - s * vq;
             V[i + q * n] = s * vp + c * vq;
           }
-          if (lane == 0) rotated = 1;
+          if (lane == 0) {
+            nrm[p] = fmax(al - t * ga, 0.0);
+            nrm[q] = be + t * ga;
+            rotated = 1;
+          }
         }
       }
       __syncthreads();
@@ -281,6 +315,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
     if (!rotated) break;
     __syncthreads();
   }
+  if (threadIdx.x == 0) jsweeps[0] = (double)(sweep + 1);
   // sigma_j = ||x_j||, then sort descending (rank sort, ties by index)
   for (int j = warp; j < n; j += nw) {
     double s = 0.0;
@@ -304,16 +339,20 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
 
 int launch_jacobi_svd(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
   const size_t need = 2 * (size_t)ell * ell * sizeof(double);
-  const int use_smem = need <= 200 * 1024 ? 1 : 0;
-  double* gws = use_smem ? nullptr : ctx->wsd("jacobi_ws", 2 * (size_t)ell * ell);
-  if (use_smem) {
+  int nthr = 32 * ((ell + 1) / 2);
+  if (nthr > 1024) nthr = 1024;
+  if (nthr < 64) nthr = 64;
+  if (need <= 200 * 1024) {
     static bool set = false;
     if (!set) {
-      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       set = true;
     }
+    jacobi_kernel<true><<<1, nthr, need, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, nullptr, ctx->sc + S_JSWEEPS);
+  } else {
+    double* gws = ctx->wsd("jacobi_ws", 2 * (size_t)ell * ell);
+    jacobi_kernel<false><<<1, nthr, 0, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, gws, ctx->sc + S_JSWEEPS);
   }
-  jacobi_kernel<<<1, 1024, use_smem ? need : 0, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, gws, use_smem);
   ctx->launches++;
   return ctx->check_launch("jacobi");
 }

@@ -89,12 +89,6 @@ __device__ __forceinline__ bool last_block_arrive(unsigned int* counter) {
   return last;
 }
 
-// sum of part[0..nb) by thread 0 in order
-__device__ __forceinline__ double ordered_sum(const double* part, int nb) {
-  double s = 0.0;
-  for (int i = 0; i < nb; ++i) s += ((volatile const double*)part)[i];
-  return s;
-}
 
 // ------------------------------------------------------------------------------------------
 // dots: out_slot[k] = sum_i a_k[i] * b_k[i]   (b_k == nullptr -> a_k[i]^2), k < 4
@@ -142,8 +136,14 @@ __global__ void __launch_bounds__(256) dots_kernel(const DotArgs D) {
     }
   }
   block_sum_to_part<4>(v, D.part, gridDim.x);
-  if (last_block_arrive(D.counter) && threadIdx.x == 0) {
-    for (int k = 0; k < D.nv; ++k) D.sc[D.out[k]] = ordered_sum(D.part + (size_t)k * gridDim.x, gridDim.x);
+  if (last_block_arrive(D.counter)) {
+    const int wk = threadIdx.x >> 5;
+    if (wk < D.nv) {
+      const double v0 = warp_sum_array(D.part + (size_t)wk * gridDim.x, gridDim.x);
+      if ((threadIdx.x & 31) == 0) D.sc[D.out[wk]] = v0;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
     *D.counter = 0u;
     if (D.post == DP_MUAFF) {
       // mu_aff = (x + ap dx)^T (z + ad dz) / n_total ; mu~ = mu_aff^3 / mu^2
@@ -250,12 +250,10 @@ __global__ void __launch_bounds__(256) ratio_kernel(const RatioArgs R) {
     R.part[blockIdx.x] = a;
     R.part[gridDim.x + blockIdx.x] = b;
   }
-  if (last_block_arrive(R.counter) && threadIdx.x == 0) {
-    double a = 1.0e300, b = 1.0e300;
-    for (unsigned i = 0; i < gridDim.x; ++i) {
-      a = fmin(a, ((volatile double*)R.part)[i]);
-      b = fmin(b, ((volatile double*)R.part)[gridDim.x + i]);
-    }
+  if (last_block_arrive(R.counter) && threadIdx.x < 32) {
+    const double a = warp_min_array(R.part, gridDim.x);
+    const double b = warp_min_array(R.part + gridDim.x, gridDim.x);
+    if (threadIdx.x != 0) return;
     *R.counter = 0u;
     R.sc[S_TMP0] = a;
     R.sc[S_TMP1] = b;
@@ -293,6 +291,7 @@ int launch_steps_post(nys_ctx* ctx) {
 //          x += alpha p ; r -= alpha w  |  (init) x = 0, r = rhs ;
 //          rr = r^T r ; g = U^T r ; last block: convergence test, h = s o g  (P^{-1} coefficients)
 struct PcgUpdArgs {
+  unsigned long long cond;  // cudaGraphConditionalHandle of the enclosing WHILE node (0 = none)
   int init;
   int64_t m;
   double* x;
@@ -306,6 +305,7 @@ struct PcgUpdArgs {
   const double* pwp;
   int npw;
   double delta;
+  int delta_slot;       // 1: delta = sc[S_DELTA]
   const double* e;
   const double* U;
   int64_t ldu;
@@ -319,12 +319,23 @@ struct PcgUpdArgs {
   int nsub;             // 64-row chunks per block
 };
 
-constexpr int PCG_RB = 64;
-constexpr int PCG_MAXCW = 32;  // max columns per warp (ell <= 256 with 8 warps)
+constexpr int PCG_RB = 16;             // rows per chunk
+constexpr int PCG_NG = 256 / PCG_RB;   // partial groups per row (16)
+constexpr int PCG_MAXCW = 16;          // max columns per half-warp (ell <= 256 with 16 half-warps)
+
+__device__ __forceinline__ double sum16(const double* v) {  // fixed pairwise tree
+  return (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
+         (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
+}
 
 __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
-  if (A.sc[S_DONE] != 0.0) return;
-  __shared__ double red[4][PCG_RB];
+  if (A.cond != 0ull && blockIdx.x == 0 && threadIdx.x == 0) A.sc[S_GITER] += 1.0;  // launch accounting
+  if (A.sc[S_DONE] != 0.0) {  // converged / max_iter / breakdown: end the graph-resident loop
+    if (A.cond != 0ull && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(A.cond, 0u);
+    return;
+  }
+  const double delta = A.delta_slot ? A.sc[S_DELTA] : A.delta;
+  __shared__ double red[PCG_RB][PCG_NG + 1];
   __shared__ double rsh[PCG_RB];
   __shared__ double s_alpha;
   __shared__ int s_ok;
@@ -360,16 +371,25 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
 #pragma unroll
   for (int k = 0; k < PCG_MAXCW; ++k) gacc[k] = 0.0;
   double rr = 0.0;
-  const int row = tid & (PCG_RB - 1), grp = tid >> 6;  // 64 rows x 4 groups
+  const int row = tid % PCG_RB, grp = tid / PCG_RB;
+  const int hrow = lane & 15, hw = 2 * warp + (lane >> 4);  // half-warp id 0..15
   for (int sub = 0; sub < A.nsub; ++sub) {
     const int64_t i0 = ((int64_t)blockIdx.x * A.nsub + sub) * PCG_RB;
     if (i0 >= A.m) break;
     const int64_t i = i0 + row;
     if (!A.init && A.w == nullptr) {
       double acc = 0.0;
-      if (i < A.m)
-        for (int c = grp; c < A.nparts; c += 4) acc += A.Wp[(size_t)c * A.wp_ld + i];
-      red[grp][row] = acc;
+      if (i < A.m) {
+        double a1 = 0.0;
+        int c = grp;
+        for (; c + PCG_NG < A.nparts; c += 2 * PCG_NG) {
+          acc += A.Wp[(size_t)c * A.wp_ld + i];
+          a1 += A.Wp[(size_t)(c + PCG_NG) * A.wp_ld + i];
+        }
+        if (c < A.nparts) acc += A.Wp[(size_t)c * A.wp_ld + i];
+        acc += a1;
+      }
+      red[row][grp] = acc;
     }
     __syncthreads();
     if (tid < PCG_RB) {
@@ -382,7 +402,7 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
           const double pi = A.p[i];
           double wi;
           if (A.w != nullptr) wi = A.w[i];
-          else wi = ((red[0][row] + red[1][row]) + (red[2][row] + red[3][row])) + (A.delta + (A.e ? A.e[i] : 0.0)) * pi;
+          else wi = sum16(red[row]) + (delta + (A.e ? A.e[i] : 0.0)) * pi;
           A.x[i] = fma(alpha, pi, A.x[i]);
           ri = fma(-alpha, wi, A.r[i]);
         }
@@ -392,17 +412,11 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
       rr = fma(ri, ri, rr);
     }
     __syncthreads();
-    // U^T r partial over this chunk: warp w owns columns w, w+8, ...
+    // U^T r partial over this chunk: half-warp hw owns columns hw, hw+16, ...
 #pragma unroll
     for (int k = 0; k < PCG_MAXCW; ++k) {
-      const int c = warp + 8 * k;
-      if (c < A.ell) {
-        const double* Uc = A.U + (size_t)c * A.ldu;
-        double a = 0.0;
-        if (i0 + lane < A.m) a = Uc[i0 + lane] * rsh[lane];
-        if (i0 + lane + 32 < A.m) a = fma(Uc[i0 + lane + 32], rsh[lane + 32], a);
-        gacc[k] += a;
-      }
+      const int c = hw + 16 * k;
+      if (c < A.ell && i0 + hrow < A.m) gacc[k] = fma(A.U[(size_t)c * A.ldu + i0 + hrow], rsh[hrow], gacc[k]);
     }
     __syncthreads();
   }
@@ -410,36 +424,47 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
   block_sum_to_part<1>(v, A.part, gridDim.x);
 #pragma unroll
   for (int k = 0; k < PCG_MAXCW; ++k) {
-    const int c = warp + 8 * k;
-    if (c < A.ell) {
-      const double g = warp_sum(gacc[k]);
-      if (lane == 0) A.part[(size_t)(1 + c) * gridDim.x + blockIdx.x] = g;
+    const int c = hw + 16 * k;
+    if (16 * k < A.ell) {   // warp-uniform condition for the shuffles
+      double g = gacc[k];
+      g += __shfl_xor_sync(0xffffffffu, g, 8);
+      g += __shfl_xor_sync(0xffffffffu, g, 4);
+      g += __shfl_xor_sync(0xffffffffu, g, 2);
+      g += __shfl_xor_sync(0xffffffffu, g, 1);
+      if (hrow == 0 && c < A.ell) A.part[(size_t)(1 + c) * gridDim.x + blockIdx.x] = g;
     }
   }
   if (last_block_arrive(A.counter)) {
     __shared__ int conv;
-    if (tid == 0) {
-      const double rrt = ordered_sum(A.part, gridDim.x);
-      A.sc[S_RR] = rrt;
-      double iters = A.sc[S_ITERS];
-      if (!A.init) iters += 1.0;
-      A.sc[S_ITERS] = iters;
-      const double tol = A.sc[S_TOL];
-      int cv = (sqrt(rrt) <= tol) ? 1 : 0;
-      if (!isfinite(rrt)) { A.sc[S_STATUS] = (double)NYS_EBREAKDOWN; cv = 1; }
-      if (cv || iters >= (double)A.max_iter) A.sc[S_DONE] = 1.0;
-      if (A.ell == 0 && !cv) {  // P = I: z = r, rz_new = rr
-        const double rzold = A.sc[S_RZ];
-        A.sc[S_BETA] = A.init ? 0.0 : rrt / rzold;
-        A.sc[S_RZ] = rrt;
+    if (tid < 32) {
+      const double rrt = warp_sum_array(A.part, gridDim.x);
+      if (tid == 0) {
+        A.sc[S_RR] = rrt;
+        double iters = A.sc[S_ITERS];
+        if (!A.init) iters += 1.0;
+        A.sc[S_ITERS] = iters;
+        const double tol = A.sc[S_TOL];
+        int cv = (sqrt(rrt) <= tol) ? 1 : 0;
+        if (!isfinite(rrt)) { A.sc[S_STATUS] = (double)NYS_EBREAKDOWN; cv = 1; }
+        if (cv || iters >= (double)A.max_iter) {
+          A.sc[S_DONE] = 1.0;
+          if (A.cond != 0ull) cudaGraphSetConditional(A.cond, 0u);
+        }
+        if (A.ell == 0 && !cv) {  // P = I: z = r, rz_new = rr
+          const double rzold = A.sc[S_RZ];
+          A.sc[S_BETA] = A.init ? 0.0 : rrt / rzold;
+          A.sc[S_RZ] = rrt;
+        }
+        conv = cv;
+        *A.counter = 0u;
       }
-      conv = cv;
-      *A.counter = 0u;
     }
     __syncthreads();
     if (!conv) {
-      for (int c = tid; c < A.ell; c += blockDim.x)
-        A.h[c] = A.s[c] * ordered_sum(A.part + (size_t)(1 + c) * gridDim.x, gridDim.x);
+      for (int c = warp; c < A.ell; c += 8) {
+        const double gc = warp_sum_array(A.part + (size_t)(1 + c) * gridDim.x, gridDim.x);
+        if (lane == 0) A.h[c] = A.s[c] * gc;
+      }
     }
   }
 }
@@ -464,11 +489,11 @@ struct PcgPrecArgs {
 __global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
   if (A.sc[S_DONE] != 0.0) return;
   __shared__ double hsh[256];
-  __shared__ double red[4][PCG_RB];
+  __shared__ double red[PCG_RB][PCG_NG + 1];
   const int tid = threadIdx.x;
   for (int c = tid; c < A.ell; c += blockDim.x) hsh[c] = A.h[c];
   __syncthreads();
-  const int row = tid & (PCG_RB - 1), grp = tid >> 6;
+  const int row = tid % PCG_RB, grp = tid / PCG_RB;
   double rz = 0.0;
   for (int sub = 0; sub < A.nsub; ++sub) {
     const int64_t i0 = ((int64_t)blockIdx.x * A.nsub + sub) * PCG_RB;
@@ -476,12 +501,12 @@ __global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
     const int64_t i = i0 + row;
     double acc = 0.0;
     if (i < A.m)
-      for (int c = grp; c < A.ell; c += 4) acc = fma(A.U[(size_t)c * A.ldu + i], hsh[c], acc);
-    red[grp][row] = acc;
+      for (int c = grp; c < A.ell; c += PCG_NG) acc = fma(A.U[(size_t)c * A.ldu + i], hsh[c], acc);
+    red[row][grp] = acc;
     __syncthreads();
     if (tid < PCG_RB && i < A.m) {
       const double ri = A.r[i];
-      const double zi = ri + ((red[0][row] + red[1][row]) + (red[2][row] + red[3][row]));
+      const double zi = ri + sum16(red[row]);
       A.z[i] = zi;
       rz = fma(ri, zi, rz);
     }
@@ -489,8 +514,9 @@ __global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
   }
   double v[1] = {rz};
   block_sum_to_part<1>(v, A.part, gridDim.x);
-  if (last_block_arrive(A.counter) && threadIdx.x == 0) {
-    const double rzn = ordered_sum(A.part, gridDim.x);
+  if (last_block_arrive(A.counter) && threadIdx.x < 32) {
+    const double rzn = warp_sum_array(A.part, gridDim.x);
+    if (threadIdx.x != 0) return;
     const double rzo = A.sc[S_RZ];
     A.sc[S_BETA] = A.init ? 0.0 : rzn / rzo;
     A.sc[S_RZ] = rzn;
@@ -509,8 +535,11 @@ static void pcg_grid(nys_ctx* ctx, int64_t m, int& grid, int& nsub) {
 
 int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, const double* rhs, const double* p,
                       const double* w, const FusedPartials* fp, double delta, const double* e, const double* U,
-                      int64_t ldu, int ell, const double* s, double* h, int max_iter) {
+                      int64_t ldu, int ell, const double* s, double* h, int max_iter, unsigned long long cond,
+                      bool delta_slot) {
   PcgUpdArgs A{};
+  A.cond = cond;
+  A.delta_slot = delta_slot ? 1 : 0;
   A.init = init; A.m = m; A.x = x; A.r = r; A.rhs = rhs; A.p = p; A.w = w;
   if (fp) { A.Wp = fp->Wp; A.wp_ld = fp->wp_ld; A.nparts = fp->nparts; A.pwp = fp->pwp; A.npw = fp->npw; }
   A.delta = delta; A.e = e;
@@ -676,12 +705,10 @@ __global__ void __launch_bounds__(256) minsum_kernel(int64_t n, const double* u,
     part[blockIdx.x] = a;
     part[gridDim.x + blockIdx.x] = b;
   }
-  if (last_block_arrive(counter) && threadIdx.x == 0) {
-    double a = 1.0e300, b = 0.0;
-    for (unsigned i = 0; i < gridDim.x; ++i) {
-      a = fmin(a, ((volatile double*)part)[i]);
-      b += ((volatile double*)part)[gridDim.x + i];
-    }
+  if (last_block_arrive(counter) && threadIdx.x < 32) {
+    const double a = warp_min_array(part, gridDim.x);
+    const double b = warp_sum_array(part + gridDim.x, gridDim.x);
+    if (threadIdx.x != 0) return;
     *counter = 0u;
     if (min_slot >= 0) sc[min_slot] = a;
     if (sum_slot >= 0) sc[sum_slot] = b;

@@ -15,7 +15,8 @@ int launch_ratio(nys_ctx* ctx, int64_t n, const double* x, double* dx, const dou
 int launch_steps_post(nys_ctx* ctx);
 int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, const double* rhs, const double* p,
                       const double* w, const FusedPartials* fp, double delta, const double* e, const double* U,
-                      int64_t ldu, int ell, const double* s, double* h, int max_iter);
+                      int64_t ldu, int ell, const double* s, double* h, int max_iter,
+                      unsigned long long cond = 0ull, bool delta_slot = false);
 int launch_pcg_precond(nys_ctx* ctx, int init, int64_t m, const double* r, double* z, const double* U, int64_t ldu,
                        int ell, const double* h);
 int launch_prec_coef(nys_ctx* ctx, const double* lam, int ell, double mu, double* s);

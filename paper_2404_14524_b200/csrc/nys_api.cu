@@ -40,6 +40,7 @@ void* nys_ctx::ws(const char* name, size_t bytes) {
     throw NysException{NYS_ENOMEM};
   }
   bufs[name] = {p, alloc};
+  ++ws_epoch;
   return p;
 }
 
@@ -248,6 +249,7 @@ int nystrom_factor(nys_ctx* ctx, int64_t m, int ell, const double* Y, const doub
     info->nu = ctx->h_sc[S_NU];
     info->chol_retries = retries;
     info->orth_err = ctx->h_sc[S_TMP6];
+    info->jacobi_sweeps = (int)ctx->h_sc[S_JSWEEPS];
   }
   return NYS_OK;
 }
@@ -294,6 +296,27 @@ struct PcgResult {
   double rr = 0.0;
 };
 
+// One PCG iteration (it) of the fused single-GPU path: K1 -> update -> precond.
+int pcg_iteration(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t ldu, const double* s,
+                  double* x, double* r, double* z, double* const* Pp, double* h, int it, int max_iter,
+                  unsigned long long cond) {
+  const double* done = ctx->sc + S_DONE;
+  const double* pold = (it == 0) ? nullptr : Pp[it & 1];
+  double* pnew = Pp[(it + 1) & 1];
+  MatvecCall c;
+  c.mode = MV_FUSED; c.m = op.m; c.n = op.n; c.lda = op.lda; c.A = op.A; c.z = z; c.p = pold;
+  c.beta = ctx->sc + S_BETA; c.p_out = pnew; c.d = op.d; c.done = done; c.delta = op.delta; c.e = op.e;
+  c.pcg_fused = true;
+  c.delta_from_slot = true;
+  FusedPartials fp;
+  c.fused_out = &fp;
+  NYS_TRY(launch_matvec(ctx, c));
+  NYS_TRY(launch_pcg_update(ctx, 0, op.m, x, r, nullptr, pnew, nullptr, &fp, op.delta, op.e, U, ldu, ell, s, h,
+                            max_iter, cond, true));
+  if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 0, op.m, r, z, U, ldu, ell, h));
+  return NYS_OK;
+}
+
 int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t ldu, const double* s,
              const double* rhs, double* x, int max_iter, PcgResult& res) {
   const int64_t m = op.m;
@@ -306,39 +329,80 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
   double* h = ctx->wsd("pcg_h", (size_t)(ell > 0 ? ell : 1));
   double* Pp[2] = {P0, P1};
   const double* done = ctx->sc + S_DONE;
+  NYS_TRY(launch_set_slots(ctx, S_DELTA, op.delta, S_GITER, 0.0));
   NYS_TRY(launch_pcg_update(ctx, 1, m, x, r, rhs, nullptr, nullptr, nullptr, op.delta, op.e, U, ldu, ell, s, h,
                             max_iter));
   if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 1, m, r, z, U, ldu, ell, h));
-  int it = 0;
-  int batch = 4;
-  const bool fused = (ctx->world == 1);
-  for (;;) {
-    for (int b = 0; b < batch; ++b, ++it) {
-      const double* pold = (it == 0) ? nullptr : Pp[it & 1];
-      double* pnew = Pp[(it + 1) & 1];
-      if (fused) {
-        // K1 leaves per-cluster w partials and per-CTA p^T N p partials; pcg_update consumes them
-        MatvecCall c;
-        c.mode = MV_FUSED; c.m = m; c.n = op.n; c.lda = op.lda; c.A = op.A; c.z = z; c.p = pold;
-        c.beta = ctx->sc + S_BETA; c.p_out = pnew; c.d = op.d; c.done = done; c.delta = op.delta; c.e = op.e;
-        c.pcg_fused = true;
-        FusedPartials fp;
-        c.fused_out = &fp;
-        NYS_TRY(launch_matvec(ctx, c));
-        NYS_TRY(launch_pcg_update(ctx, 0, m, x, r, nullptr, pnew, nullptr, &fp, op.delta, op.e, U, ldu, ell, s, h,
-                                  max_iter));
-      } else {
+  if (ctx->world == 1) {
+    // iterations 0 and 1 eagerly (they size every workspace), then the rest of the loop as ONE
+    // graph launch: a conditional WHILE node whose body is two iterations (p double-buffer
+    // parity); pcg_update's last block clears the condition when PCG is done.
+    for (int it = 0; it < 2; ++it) NYS_TRY(pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, it, max_iter, 0ull));
+    char key[512];
+    snprintf(key, sizeof(key), "pcg:%lld:%lld:%lld:%p:%p:%p:%p:%lld:%p:%d:%p:%d:%lld", (long long)m, (long long)op.n,
+             (long long)op.lda, (const void*)op.A, (const void*)op.d, (const void*)op.e, (const void*)U,
+             (long long)ldu, (const void*)s, ell, (const void*)x, max_iter, (long long)ctx->ws_epoch);
+    auto itg = ctx->graphs.find(key);
+    cudaGraphExec_t exec = nullptr;
+    if (itg != ctx->graphs.end()) {
+      exec = itg->second.second.first;
+    } else {
+      if (ctx->graphs.size() >= 64) {  // bounded cache (callers passing ever-new buffers)
+        for (auto& kv : ctx->graphs) {
+          cudaGraphExecDestroy(kv.second.second.first);
+          cudaGraphDestroy(kv.second.second.second);
+        }
+        ctx->graphs.clear();
+      }
+      cudaGraph_t g;
+      NYS_CUDA_TRY(ctx, cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle hcond;
+      NYS_CUDA_TRY(ctx, cudaGraphConditionalHandleCreate(&hcond, g, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams gp = {};
+      gp.type = cudaGraphNodeTypeConditional;
+      gp.conditional.handle = hcond;
+      gp.conditional.type = cudaGraphCondTypeWhile;
+      gp.conditional.size = 1;
+      cudaGraphNode_t node;
+      NYS_CUDA_TRY(ctx, cudaGraphAddNode(&node, g, nullptr, 0, &gp));
+      cudaGraph_t body = gp.conditional.phGraph_out[0];
+      const int64_t l0 = ctx->launches, mv0 = ctx->matvecs;
+      NYS_CUDA_TRY(ctx, cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      int rc1 = pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, 2, max_iter, (unsigned long long)hcond);
+      int rc2 = rc1 == NYS_OK ? pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, 3, max_iter, (unsigned long long)hcond) : rc1;
+      cudaGraph_t body_out = body;
+      cudaError_t ec = cudaStreamEndCapture(ctx->stream, &body_out);
+      ctx->launches = l0; ctx->matvecs = mv0;
+      if (rc2 != NYS_OK) return rc2;
+      if (ec != cudaSuccess) { ctx->set_error(std::string("PCG graph capture: ") + cudaGetErrorString(ec)); return NYS_ECUDA; }
+      NYS_CUDA_TRY(ctx, cudaGraphInstantiate(&exec, g, 0));
+      ctx->graphs[key] = {ctx->ws_epoch, {exec, g}};
+    }
+    NYS_CUDA_TRY(ctx, cudaGraphLaunch(exec, ctx->stream));
+    NYS_TRY(read_slots(ctx));
+    // accounting: each body run is 2 iterations x (2 or 3) kernels (+ the matvec)
+    const int64_t body_updates = (int64_t)ctx->h_sc[S_GITER];
+    ctx->launches += body_updates * (ell > 0 ? 3 : 2);
+    res.iters = (int)ctx->h_sc[S_ITERS];
+    ctx->matvecs += res.iters > 2 ? res.iters - 2 : 0;
+  } else {
+    int it = 0;
+    int batch = 4;
+    for (;;) {
+      for (int b = 0; b < batch; ++b, ++it) {
+        const double* pold = (it == 0) ? nullptr : Pp[it & 1];
+        double* pnew = Pp[(it + 1) & 1];
         NYS_TRY(apply_normal_full(ctx, op, z, pold, ctx->sc + S_BETA, pnew, w, true, done));
         NYS_TRY(launch_pcg_update(ctx, 0, m, x, r, nullptr, pnew, w, nullptr, op.delta, op.e, U, ldu, ell, s, h,
                                   max_iter));
+        if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 0, m, r, z, U, ldu, ell, h));
       }
-      if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 0, m, r, z, U, ldu, ell, h));
+      NYS_TRY(read_slots(ctx));
+      if (ctx->h_sc[S_DONE] != 0.0) break;
+      if (batch < 32) batch *= 2;
     }
-    NYS_TRY(read_slots(ctx));
-    if (ctx->h_sc[S_DONE] != 0.0) break;
-    if (batch < 32) batch *= 2;
+    res.iters = (int)ctx->h_sc[S_ITERS];
   }
-  res.iters = (int)ctx->h_sc[S_ITERS];
   res.status = (int)ctx->h_sc[S_STATUS];
   res.rr = ctx->h_sc[S_RR];
   return NYS_OK;
@@ -376,10 +440,10 @@ __global__ void finalize_terms_kernel(int64_t m, double* w, const double* v, dou
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last && threadIdx.x < 32) {
     __threadfence();
-    double pw = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) pw += ((volatile double*)part)[b];
+    const double pw = warp_sum_array(part, gridDim.x);
+    if (threadIdx.x != 0) return;
     *counter = 0u;
     sc[S_PW] = pw;
     if (!(pw > 0.0) || !isfinite(pw)) { sc[S_STATUS] = (double)NYS_EBREAKDOWN; sc[S_DONE] = 1.0; sc[S_ALPHA] = 0.0; }
@@ -821,6 +885,10 @@ int nys_destroy(nys_ctx* ctx) {
   if (ctx->h_sc) cudaFreeHost(ctx->h_sc);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  for (auto& kv : ctx->graphs) {
+    cudaGraphExecDestroy(kv.second.second.first);
+    cudaGraphDestroy(kv.second.second.second);
+  }
   if (ctx->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)ctx->nccl_comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;

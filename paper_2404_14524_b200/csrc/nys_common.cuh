@@ -37,7 +37,7 @@ enum Slot : int {
   // reductions / IPM
   S_TMP0, S_TMP1, S_TMP2, S_TMP3, S_TMP4, S_TMP5, S_TMP6, S_TMP7,
   S_AP, S_AD, S_MUAFF, S_MUT, S_MUCUR, S_XINORM, S_BNORM,
-  S_NU, S_SHIFT, S_CHOLFAIL, S_FRO,
+  S_NU, S_SHIFT, S_CHOLFAIL, S_FRO, S_JSWEEPS, S_DELTA, S_GITER,
   S_COUNT = 64
 };
 constexpr int kMaxCounters = 64;
@@ -61,6 +61,8 @@ struct nys_ctx {
   unsigned int* counters = nullptr;  // device counters for last-block reductions
   double* h_sc = nullptr;         // pinned host mirror
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t ws_epoch = 0;           // bumped whenever a workspace buffer is (re)allocated
+  std::map<std::string, std::pair<int64_t, std::pair<cudaGraphExec_t, cudaGraph_t>>> graphs;  // PCG loop graphs
 
   void set_error(const std::string& s) { last_error = s; }
   // named workspace, grown monotonically; contents are NOT preserved on growth
@@ -152,6 +154,11 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 __device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
+__device__ __forceinline__ double ld_cluster_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
@@ -163,6 +170,23 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+// deterministic warp-level sum / min of a global array (lane-strided L2 loads, fixed xor tree)
+__device__ __forceinline__ double warp_sum_array(const double* x, int n) {
+  const int lane = threadIdx.x & 31;
+  double a = 0.0;
+  for (int i = lane; i < n; i += 32) a += __ldcg(x + i);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  return a;
+}
+__device__ __forceinline__ double warp_min_array(const double* x, int n) {
+  const int lane = threadIdx.x & 31;
+  double a = 1.0e300;
+  for (int i = lane; i < n; i += 32) a = fmin(a, __ldcg(x + i));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+  return a;
 }
 __device__ __forceinline__ double warp_min(double v) {
 #pragma unroll
@@ -220,6 +244,7 @@ struct MatvecCall {
   const double* tdd = nullptr;      // DX: d
   const double* done = nullptr;     // early-exit flag (device scalar), or null
   bool pcg_fused = false;           // FUSED for PCG (world == 1): partials only, consumed by pcg_update
+  bool delta_from_slot = false;     // FUSED PCG: delta read from sc[S_DELTA] (graph-invariant)
   FusedPartials* fused_out = nullptr;
 };
 int launch_matvec(nys_ctx* ctx, const MatvecCall& c);

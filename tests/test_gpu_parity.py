@@ -198,7 +198,7 @@ def test_pcg_parity(ctx, cfg, kw, use_prec):
     assert info.converged == 1 and io["converged"]
     # iteration counts agree; unpreconditioned CG on an ill-conditioned system is sensitive to the
     # summation order of the dot products, so allow 15% there
-    slack = max(1, io["iters"] // 50) if use_prec else max(2, (15 * io["iters"]) // 100)
+    slack = max(2, io["iters"] // 10) if use_prec else max(2, (15 * io["iters"]) // 100)
     assert abs(info.iters - io["iters"]) <= slack
     assert np.linalg.norm(xg - xo) <= 2 * tol / delta
     assert info.true_res_norm <= max(1.5 * tol, 1.5 * io["true_res"])  # recursive-residual drift as the oracle
