@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
   double* vsm = slots + (size_t)S * cl * CPG;  // VS: the operand slice v (rs doubles)
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  const int warp = warp_uniform_id(), lane = tid & 31;
   const int rc = P.rc;
   const uint32_t crank = cl > 1 ? cluster_ctarank() : 0u;
   const uint32_t cid = cl > 1 ? cluster_id_x() : blockIdx.x;
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(256) mv_finalize(const FinParams F) {
     am_last = (prev == gridDim.x - 1);
   }
   __syncthreads();
-  if (am_last && tid < 32) {
+  if (am_last && warp_uniform_id() == 0) {
     __threadfence();
     const double pw = warp_sum_array(F.part, gridDim.x);
     if (tid != 0) return;

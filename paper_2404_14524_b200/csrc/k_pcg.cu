@@ -1,0 +1,530 @@
+// Persistent PCG on (A D A^T + diag(e) + delta I) x = rhs with the Nystrom P^{-1}
+// — ONE cooperative launch for the whole solve (single GPU, m <= 8192 so that a CTA
+// holds the full column height).
+//
+// Every CTA owns a fixed set of column panels of A (as in the fused matvec, k_matvec.cu) and a
+// fixed chunk of rows of the m-space vectors.  Per iteration:
+//   P1  v = z + beta p  (all rows, registers);   w_partial = A_panels (d o (A_panels^T v)),
+//       p^T N p partial                                                   -> grid barrier
+//   P2  alpha = rz / p^T w; own rows: w = sum partials + (delta + e) p; x += alpha p;
+//       r -= alpha w; ||r||^2 and U^T r partials                           -> grid barrier
+//   P3  every CTA sums the same partials in the same order (identical decisions):
+//       converged? h = s o (U^T r); own rows: z = r + U h; r^T z partial  -> grid barrier
+//   P4  beta = rz_new / rz
+// The producer warp streams A panels through the S-stage cp.async.bulk ring CONTINUOUSLY across
+// iterations (A does not depend on the iterate), so the barrier phases overlap the HBM stream of
+// the next matvec.  Grid barriers involve the consumer threads only; the producer polls a stop
+// flag so it can never block the exit.
+#include <cstdlib>
+
+#include "k_vec.cuh"
+
+namespace nys {
+
+struct PcgPParams {
+  const double* A;
+  int64_t lda, m, n;
+  const double* d;
+  const double* e;
+  const double* U;
+  int64_t ldu;
+  int ell;
+  const double* s;       // ell coefficients (lam_l + mu)/(lam_i + mu) - 1
+  const double* rhs;
+  double* x;
+  double* r;
+  double* z;             // == r when ell == 0
+  double* P0;            // p double buffer
+  double* P1;
+  double* Wp;            // [G][wp_ld] partial w
+  int64_t wp_ld;
+  double* pwp;           // [G]
+  double* part1;         // [(1 + ell)][G]   (rr, U^T r) partials, column-contiguous
+  double* part2;         // [G]              r^T z partials
+  double* sc;
+  unsigned int* bar;     // [2]: count, generation
+  int max_iter;
+  int stages;
+  int64_t npanels;
+  int64_t rows_per_cta;
+};
+
+__device__ __forceinline__ void pcg_grid_barrier(unsigned int* bar, unsigned int nblocks, int nthreads) {
+  named_bar_sync(9, nthreads);
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicExch(bar + 1, g + 1u);
+    } else {
+      while (*gen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  named_bar_sync(9, nthreads);
+}
+
+// deterministic sum over G partials of column j (one warp)
+__device__ __forceinline__ double col_sum(const double* part, int j, int G) { return warp_sum_array(part + (size_t)j * G, G); }
+
+template <int T, int GT, int RPT, int CPG>
+__global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPParams P) {
+  constexpr int NG = T / GT;
+  constexpr int WPG = GT / 32;
+  constexpr int BN = NG * CPG;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int S = P.stages;
+  const int64_t rs = (P.m + 1) & ~int64_t(1);  // full column height (cl == 1), even for 16-B copies
+  double* stage = reinterpret_cast<double*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage + (size_t)S * BN * rs);
+  uint64_t* empty = full + S;
+  double* red = reinterpret_cast<double*>(empty + S);  // 2 * NG * WPG * CPG
+  __shared__ double hsh[256];
+  __shared__ double chunk_red[16][17];
+  __shared__ double s_scal[8];
+  __shared__ volatile int s_stop;
+  __shared__ volatile long long s_issued;
+
+  const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31;
+  const unsigned int G = gridDim.x;
+  const unsigned int cid = blockIdx.x;
+  const int64_t niter = (cid < P.npanels) ? (P.npanels - cid + G - 1) / G : 0;
+  const uint32_t copy_bytes = (uint32_t)(((P.m + 1) & ~int64_t(1)) * 8);
+  const int64_t r_lo = (int64_t)cid * P.rows_per_cta;
+  int64_t r_hi = r_lo + P.rows_per_cta;
+  if (r_hi > P.m) r_hi = P.m;
+  const int ell = P.ell;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], T / 32);
+    }
+    fence_mbar_init();
+    s_stop = 0;
+    s_issued = 0;
+  }
+  __syncthreads();
+
+  if (warp == T / 32) {
+    // ---------------- producer warp: stream this CTA's panels, iteration after iteration ------
+    long long q = 0;
+    if (lane == 0 && niter > 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      for (;;) {
+        const int s = (int)(q % S);
+        if (q >= S) {
+          const uint32_t par = (uint32_t)(((q / S) - 1) & 1);
+          bool stop = false;
+          for (;;) {
+            uint32_t ok;
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                : "=r"(ok)
+                : "r"(smem_u32(&empty[s])), "r"(par)
+                : "memory");
+            if (ok) break;
+            if (s_stop) { stop = true; break; }
+          }
+          if (stop) break;
+        }
+        if (s_stop) break;
+        const int64_t it = q % niter;
+        const int64_t col0 = (int64_t)(cid + it * G) * BN;
+        int64_t ncols = P.n - col0;
+        ncols = ncols > BN ? BN : ncols;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)ncols * copy_bytes);
+        for (int c = 0; c < ncols; ++c)
+          bulk_g2s(stage + ((size_t)s * BN + c) * rs, P.A + (col0 + c) * P.lda, copy_bytes, &full[s], pol);
+        ++q;
+      }
+      s_issued = q;
+    }
+    __syncwarp();
+    named_bar_sync(10, T + 32);  // exit handshake with the consumers
+    return;
+  }
+
+  // ======================= consumers =========================================================
+  const int g = tid / GT;
+  const int lig = tid % GT;
+  const int row16 = tid & 15, grp16 = (tid >> 4) & 15;  // first 256 threads: 16 rows x 16 groups
+  const int hrow = lane & 15, hw = 2 * warp + (lane >> 4);
+  long long qc = 0;  // consumed stage counter
+  double rz = 0.0, beta = 0.0;
+  int iters = 0;
+  int status = 0;
+  bool conv = false;
+
+  // ---- init: x = 0, r = rhs, rr, U^T r  ------------------------------------------------------
+  auto rows_phase_rr_ut = [&](bool init, double alpha, const double* pnew, const double* Wp, double delta) {
+    // own rows in chunks of 16: (init) x = 0, r = rhs | x += alpha p, r -= alpha w ; partials
+    double rr = 0.0;
+    double gacc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) gacc[k] = 0.0;
+    for (int64_t i0 = r_lo; i0 < r_hi; i0 += 16) {
+      const int64_t i = i0 + row16;
+      if (!init && warp < 8) {
+        double acc = 0.0, a1 = 0.0;
+        if (i < r_hi) {
+          int c = grp16;
+          for (; c + 16 < (int)G; c += 32) {
+            acc += Wp[(size_t)c * P.wp_ld + i];
+            a1 += Wp[(size_t)(c + 16) * P.wp_ld + i];
+          }
+          if (c < (int)G) acc += Wp[(size_t)c * P.wp_ld + i];
+        }
+        chunk_red[row16][grp16] = acc + a1;
+      }
+      named_bar_sync(9, T);
+      if (tid < 16) {
+        double ri = 0.0;
+        if (i < r_hi) {
+          if (init) {
+            ri = P.rhs[i];
+            P.x[i] = 0.0;
+          } else {
+            const double* v = chunk_red[row16];
+            const double wsum = (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
+                                (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
+            const double pi = pnew[i];
+            const double wi = wsum + (delta + (P.e ? P.e[i] : 0.0)) * pi;
+            P.x[i] = fma(alpha, pi, P.x[i]);
+            ri = fma(-alpha, wi, P.r[i]);
+          }
+          P.r[i] = ri;
+        }
+        hsh[row16] = ri;
+        rr = fma(ri, ri, rr);
+      }
+      named_bar_sync(9, T);
+      if (warp < 8) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int c = hw + 16 * k;
+          if (c < ell && i0 + hrow < r_hi) gacc[k] = fma(P.U[(size_t)c * P.ldu + i0 + hrow], hsh[hrow], gacc[k]);
+        }
+      }
+      named_bar_sync(9, T);
+    }
+    // write partials: rr (threads < 16 hold pieces) and U^T r (half-warps)
+    double rrw = warp_sum(rr);
+    if (tid == 0) P.part1[cid] = rrw;
+    if (warp < 8) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (16 * k < ell) {
+          double gsum = gacc[k];
+          gsum += __shfl_xor_sync(0xffffffffu, gsum, 8);
+          gsum += __shfl_xor_sync(0xffffffffu, gsum, 4);
+          gsum += __shfl_xor_sync(0xffffffffu, gsum, 2);
+          gsum += __shfl_xor_sync(0xffffffffu, gsum, 1);
+          const int c = hw + 16 * k;
+          if (hrow == 0 && c < ell) P.part1[(size_t)(1 + c) * G + cid] = gsum;
+        }
+      }
+    }
+  };
+
+  // P3: converged? then h and z = r + U h, r^T z partial
+  auto phase_prec = [&](bool init) -> bool {
+    if (warp == 0) {
+      const double rrt = col_sum(P.part1, 0, G);
+      if (lane == 0) s_scal[0] = rrt;
+    }
+    named_bar_sync(9, T);
+    const double rrt = s_scal[0];
+    const double tol = P.sc[S_TOL];
+    bool cv = sqrt(rrt) <= tol;
+    if (!isfinite(rrt)) { status = NYS_EBREAKDOWN; cv = true; }
+    if (!init) ++iters;
+    if (cv || iters >= P.max_iter) {
+      if (cid == 0 && tid == 0) { P.sc[S_RR] = rrt; }
+      conv = cv;
+      return true;
+    }
+    if (ell > 0) {
+      for (int c = warp; c < ell; c += T / 32) {
+        const double gc = col_sum(P.part1, 1 + c, G);
+        if (lane == 0) hsh[c] = P.s[c] * gc;
+      }
+      named_bar_sync(9, T);
+      double rzp = 0.0;
+      for (int64_t i0 = r_lo; i0 < r_hi; i0 += 16) {
+        const int64_t i = i0 + row16;
+        if (warp < 8) {
+          double acc = 0.0;
+          if (i < r_hi)
+            for (int c = grp16; c < ell; c += 16) acc = fma(P.U[(size_t)c * P.ldu + i], hsh[c], acc);
+          chunk_red[row16][grp16] = acc;
+        }
+        named_bar_sync(9, T);
+        if (tid < 16 && i < r_hi) {
+          const double* v = chunk_red[row16];
+          const double us = (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
+                            (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
+          const double ri = P.r[i];
+          const double zi = ri + us;
+          P.z[i] = zi;
+          rzp = fma(ri, zi, rzp);
+        }
+        named_bar_sync(9, T);
+      }
+      rzp = warp_sum(rzp);
+      if (tid == 0) P.part2[cid] = rzp;
+      pcg_grid_barrier(P.bar, G, T);
+      if (warp == 0) {
+        const double rzn = warp_sum_array(P.part2, G);
+        if (lane == 0) s_scal[1] = rzn;
+      }
+      named_bar_sync(9, T);
+      const double rzn = s_scal[1];
+      if (!(rzn > 0.0) || !isfinite(rzn)) { status = NYS_EBREAKDOWN; return true; }
+      beta = init ? 0.0 : rzn / rz;
+      rz = rzn;
+    } else {
+      beta = init ? 0.0 : rrt / rz;
+      rz = rrt;
+    }
+    return false;
+  };
+
+  const double delta = P.sc[S_DELTA];
+  rows_phase_rr_ut(true, 0.0, nullptr, nullptr, delta);
+  pcg_grid_barrier(P.bar, G, T);
+  bool stop = phase_prec(true);
+
+  int k = 0;
+  while (!stop) {
+    // ---- P1: v = z + beta p ; fused matvec over this CTA's panels ----------------------------
+    const double* pold = (k & 1) ? P.P1 : P.P0;
+    double* pnew = (k & 1) ? P.P0 : P.P1;
+    double vreg[RPT];
+    double wacc[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int64_t rl = lig + (int64_t)GT * i;
+      double v = 0.0;
+      if (rl < P.m) {
+        v = P.z[rl];
+        if (k > 0) v = fma(beta, pold[rl], v);
+        if (cid == 0 && g == 0) pnew[rl] = v;
+      }
+      vreg[i] = v;
+      wacc[i] = 0.0;
+    }
+    double pwacc = 0.0;
+    for (int64_t it = 0; it < niter; ++it, ++qc) {
+      const int s = (int)(qc % S);
+      const uint32_t par = (uint32_t)((qc / S) & 1);
+      const int64_t col0 = (int64_t)(cid + it * G) * BN + (int64_t)g * CPG;
+      mbar_wait(&full[s], par);
+      double a[CPG][RPT];
+      const double* sb = stage + ((size_t)s * BN + (size_t)g * CPG) * rs;
+#pragma unroll
+      for (int c = 0; c < CPG; ++c) {
+        const bool cv = (col0 + c) < P.n;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const int64_t rl = lig + (int64_t)GT * i;
+          a[c][i] = (cv && rl < P.m) ? sb[(size_t)c * rs + rl] : 0.0;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      double pd[CPG];
+#pragma unroll
+      for (int c = 0; c < CPG; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) acc = fma(a[c][i], vreg[i], acc);
+        pd[c] = warp_sum(acc);
+      }
+      if (WPG > 1) {
+        double* rb = red + ((size_t)(qc & 1) * NG + g) * WPG * CPG;
+        if (lane == 0) {
+#pragma unroll
+          for (int c = 0; c < CPG; ++c) rb[(warp % WPG) * CPG + c] = pd[c];
+        }
+        named_bar_sync(1 + g, GT);
+#pragma unroll
+        for (int c = 0; c < CPG; ++c) {
+          double tot = 0.0;
+#pragma unroll
+          for (int w = 0; w < WPG; ++w) tot += rb[w * CPG + c];
+          pd[c] = tot;
+        }
+      }
+      double t[CPG];
+#pragma unroll
+      for (int c = 0; c < CPG; ++c) t[c] = (col0 + c < P.n) ? P.d[col0 + c] * pd[c] : 0.0;
+      if (lig == 0) {
+#pragma unroll
+        for (int c = 0; c < CPG; ++c) pwacc = fma(t[c], pd[c], pwacc);
+      }
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        double acc = wacc[i];
+#pragma unroll
+        for (int c = 0; c < CPG; ++c) acc = fma(a[c][i], t[c], acc);
+        wacc[i] = acc;
+      }
+    }
+    // p^T (delta I + diag e) p : CTA 0, group 0
+    if (cid == 0 && g == 0) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t rl = lig + (int64_t)GT * i;
+        if (rl < P.m) pwacc = fma((delta + (P.e ? P.e[rl] : 0.0)) * vreg[i], vreg[i], pwacc);
+      }
+    }
+    // CTA partials: w (group-summed through global atomics-free path) and p^T N p
+    {
+      double* outp = P.Wp + (size_t)cid * P.wp_ld;
+      if (NG == 1) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const int64_t rl = lig + (int64_t)GT * i;
+          if (rl < P.m) outp[rl] = wacc[i];
+        }
+      } else {
+        // groups write in turn (fixed order) through the partial row itself
+        for (int gg = 0; gg < NG; ++gg) {
+          if (g == gg) {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+              const int64_t rl = lig + (int64_t)GT * i;
+              if (rl < P.m) outp[rl] = (gg == 0) ? wacc[i] : outp[rl] + wacc[i];
+            }
+          }
+          named_bar_sync(9, T);
+        }
+      }
+      const double wsum = warp_sum(pwacc);
+      if (lane == 0) chunk_red[0][warp] = wsum;  // <= 16 consumer warps
+      named_bar_sync(9, T);
+      if (tid == 0) {
+        double b = 0.0;
+        for (int w = 0; w < T / 32; ++w) b += chunk_red[0][w];
+        P.pwp[cid] = b;
+      }
+    }
+    pcg_grid_barrier(P.bar, G, T);
+    // ---- P2: alpha, own-row updates, partials --------------------------------------------------
+    if (warp == 0) {
+      const double pw = warp_sum_array(P.pwp, G);
+      if (lane == 0) s_scal[2] = pw;
+    }
+    named_bar_sync(9, T);
+    const double pw = s_scal[2];
+    if (!(pw > 0.0) || !isfinite(pw)) { status = NYS_EBREAKDOWN; break; }
+    const double alpha = rz / pw;
+    rows_phase_rr_ut(false, alpha, pnew, P.Wp, delta);
+    pcg_grid_barrier(P.bar, G, T);
+    // ---- P3 / P4 -------------------------------------------------------------------------------
+    stop = phase_prec(false);
+    ++k;
+  }
+
+  // ---- exit: stop the producer, drain in-flight bulk copies, publish the scalars --------------
+  if (tid == 0) s_stop = 1;
+  named_bar_sync(10, T + 32);
+  const long long issued = s_issued;
+  for (; qc < issued; ++qc) mbar_wait(&full[(int)(qc % S)], (uint32_t)((qc / S) & 1));
+  if (cid == 0 && tid == 0) {
+    P.sc[S_ITERS] = (double)iters;
+    P.sc[S_STATUS] = (double)status;
+    P.sc[S_DONE] = 1.0;
+    P.sc[S_RZ] = rz;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+struct PcgCfg {
+  int T, GT, RPT, CPG;
+};
+static PcgCfg pcg_pick(int64_t m) {
+  if (m <= 64) return {256, 32, 2, 4};
+  if (m <= 128) return {256, 32, 4, 2};
+  if (m <= 256) return {256, 64, 4, 2};
+  if (m <= 1024) return {256, 128, 8, 2};
+  if (m <= 2048) return {256, 256, 8, 4};
+  if (m <= 4096) return {512, 512, 8, 2};
+  return {512, 512, 16, 1};
+}
+typedef void (*PcgKernel)(const PcgPParams);
+static PcgKernel pcg_kernel_for(const PcgCfg& c) {
+  if (c.GT == 32 && c.RPT == 2) return pcg_persistent_kernel<256, 32, 2, 4>;
+  if (c.GT == 32 && c.RPT == 4) return pcg_persistent_kernel<256, 32, 4, 2>;
+  if (c.GT == 64) return pcg_persistent_kernel<256, 64, 4, 2>;
+  if (c.GT == 128) return pcg_persistent_kernel<256, 128, 8, 2>;
+  if (c.GT == 256) return pcg_persistent_kernel<256, 256, 8, 4>;
+  if (c.RPT == 8) return pcg_persistent_kernel<512, 512, 8, 2>;
+  return pcg_persistent_kernel<512, 512, 16, 1>;
+}
+
+bool pcg_persistent_supported(nys_ctx* ctx, int64_t m, int64_t n, int ell) {
+  return ctx->world == 1 && m <= 8192 && n > 0 && ell <= 256 && getenv("NYS_NO_PERSISTENT") == nullptr;
+}
+
+// tolerance must already be in sc[S_TOL] and delta in sc[S_DELTA]
+int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                          const double* e, const double* U, int64_t ldu, int ell, const double* s, const double* rhs,
+                          double* x, int max_iter) {
+  const PcgCfg c = pcg_pick(m);
+  const int NG = c.T / c.GT, WPG = c.GT / 32, BN = NG * c.CPG;
+  const int64_t mp = (m + 1) & ~int64_t(1);
+  const size_t stage_bytes = (size_t)BN * mp * 8;
+  const size_t budget = (mp <= 1024) ? 96 * 1024 : 180 * 1024;
+  int stages = (int)(budget / stage_bytes);
+  if (stages > 8) stages = 8;
+  if (stages < 2) stages = 2;
+  const size_t smem = (size_t)stages * stage_bytes + 2 * stages * 8 + (size_t)2 * NG * WPG * c.CPG * 8;
+  PcgKernel k = pcg_kernel_for(c);
+  NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  NYS_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c.T + 32, smem));
+  if (occ < 1) { ctx->set_error("persistent PCG does not fit on an SM"); return NYS_ECUDA; }
+  const int64_t npanels = (n + BN - 1) / BN;
+  int64_t G = (int64_t)ctx->num_sms * occ;
+  if (G > npanels) G = npanels;
+  if (G < 1) G = 1;
+  PcgPParams P{};
+  P.A = A; P.lda = lda; P.m = m; P.n = n; P.d = d; P.e = e; P.U = U; P.ldu = ldu; P.ell = ell; P.s = s;
+  P.rhs = rhs; P.x = x;
+  P.r = ctx->wsd("pp_r", (size_t)mp);
+  P.z = ell > 0 ? ctx->wsd("pp_z", (size_t)mp) : P.r;
+  P.P0 = ctx->wsd("pp_p0", (size_t)mp);
+  P.P1 = ctx->wsd("pp_p1", (size_t)mp);
+  P.wp_ld = mp;
+  P.Wp = ctx->wsd("pp_Wp", (size_t)G * mp);
+  P.pwp = ctx->wsd("pp_pwp", (size_t)G);
+  P.part1 = ctx->wsd("pp_part1", (size_t)(1 + ell) * G);
+  P.part2 = ctx->wsd("pp_part2", (size_t)G);
+  P.sc = ctx->sc;
+  P.bar = (unsigned int*)ctx->ws("pp_bar", 64);
+  P.max_iter = max_iter;
+  P.stages = stages;
+  P.npanels = npanels;
+  P.rows_per_cta = (m + G - 1) / G;
+  NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.bar, 0, 64, ctx->stream));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)G);
+  cfg.blockDim = dim3((unsigned)(c.T + 32));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, P));
+  ctx->launches++;
+  return ctx->check_launch("pcg_persistent");
+}
+
+}  // namespace nys

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) fro_kernel(int64_t m, int ell, const doub
     last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x < 32) {
+  if (last && warp_uniform_id() == 0) {
     __threadfence();
     const double s = warp_sum_array(part, gridDim.x);
     if (threadIdx.x != 0) return;
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(int ell, double* G, int l
   double* X = W + (size_t)n * n;          // n x n, ld lx : R^{-1}
   __shared__ double rsq[256];
   __shared__ double shift;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31, nw = blockDim.x >> 5;
   for (int e = tid; e < n * n; e += blockDim.x) {
     const int i = e % n, j = e / n;
     W[i + j * n] = 0.5 * (G[i + j * ldg] + G[j + i * ldg]);
@@ -160,19 +160,21 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(int ell, double* G, int l
     W[i + j * n] = (i < j) ? W[i + j * n] * rsq[i] : (i == j ? W[i + j * n] * rsq[i] : 0.0);
   }
   __syncthreads();
-  // X = R^{-1}: one thread per column j, column-oriented back substitution in lockstep over i
-  // (x = e_j; for i = n-1..0: x_i /= R_ii; x_k -= R_ki x_i for k < i)
+  // X = R^{-1} by back substitution with every (k, j) update in parallel:
+  // X = I; for i = n-1..0: X(i, j>=i) /= R(i,i);  X(k<i, j>=i) -= R(k,i) X(i,j)
   for (int j = tid; j < n; j += blockDim.x) X[j + j * lx] = 1.0;
-  for (int i = n - 1; i >= 0; --i) {
-    for (int j = tid; j < n; j += blockDim.x) {
-      if (i <= j) {
-        const double xi = X[i + j * lx] / W[i + i * n];
-        X[i + j * lx] = xi;
-        for (int k = 0; k < i; ++k) X[k + j * lx] = fma(-W[k + i * n], xi, X[k + j * lx]);
-      }
-    }
-  }
   __syncthreads();
+  for (int i = n - 1; i >= 0; --i) {
+    const double inv = 1.0 / W[i + i * n];
+    for (int j = i + tid; j < n; j += blockDim.x) X[i + j * lx] *= inv;
+    __syncthreads();
+    const int cols = n - i;
+    for (int e = tid; e < i * cols; e += blockDim.x) {
+      const int k = e % i, j = i + e / i;
+      X[k + j * lx] = fma(-W[k + i * n], X[i + j * lx], X[k + j * lx]);
+    }
+    __syncthreads();
+  }
   for (int e = tid; e < n * n; e += blockDim.x) {
     const int i = e % n, j = e / n;
     G[i + j * ldg] = W[i + j * n];
@@ -240,16 +242,20 @@ __device__ __forceinline__ double fast_rsqrt(double y) {  // y in [1, 1e30)
   return r;
 }
 
-template <bool SM>
+// NMAX: compile-time bound on ell (64 / 128 / 256); GL lanes per column pair, E = NMAX / GL
+// elements per lane (fully unrolled, predicated): no runtime-bounded inner loops, and log2(GL)
+// shuffle levels per dot product.
+template <int NMAX, int GL, bool SM>
 __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, int ldr, double* Vout, int ldv,
                                                       double* sigma, double* gws, double* jsweeps) {
+  constexpr int E = NMAX / GL;
   extern __shared__ double jsm[];
   double* X = SM ? jsm : gws;
   double* V = X + (size_t)n * n;
   __shared__ int rotated;
-  __shared__ double sv[256];
-  __shared__ int order[256];
-  __shared__ double nrm[256];
+  __shared__ double sv[NMAX];
+  __shared__ int order[NMAX];
+  __shared__ double nrm[NMAX];
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e % n, j = e / n;
     X[i + j * n] = R[j + i * ldr];  // X = R^T
@@ -257,34 +263,53 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
   }
   __syncthreads();
   const int P = (n % 2 == 0) ? n : n + 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int npg = blockDim.x / GL;             // pair groups in the block
+  const int grp = threadIdx.x / GL, lig = threadIdx.x % GL;
   const double tol = fmax(1e-15, (double)n * 0x1p-53);
   const double tol2 = tol * tol;
+  auto gsum = [&](double v) {
+#pragma unroll
+    for (int o = GL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
   int sweep = 0;
   for (; sweep < 30; ++sweep) {
-    for (int j = warp; j < n; j += nw) {
+    for (int j0 = 0; j0 < n; j0 += npg) {      // exact column norms (uniform trip count)
+      const int j = j0 + grp;
       double a = 0.0;
-      for (int i = lane; i < n; i += 32) a = fma(X[i + j * n], X[i + j * n], a);
-      a = warp_sum(a);
-      if (lane == 0) nrm[j] = a;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = lig + GL * e;
+        if (i < n && j < n) a = fma(X[i + j * n], X[i + j * n], a);
+      }
+      a = gsum(a);
+      if (lig == 0 && j < n) nrm[j] = a;
     }
     if (threadIdx.x == 0) rotated = 0;
     __syncthreads();
     for (int r = 0; r < P - 1; ++r) {
-      for (int pi = warp; pi < P / 2; pi += nw) {
+      for (int pi0 = 0; pi0 < P / 2; pi0 += npg) {
+        const int pi = pi0 + grp;
         int a, b;
         if (pi == 0) { a = r; b = P - 1; }
         else {
           a = r + pi; if (a >= P - 1) a -= P - 1;
           b = r - pi; if (b < 0) b += P - 1;
         }
-        if (a >= n || b >= n) continue;
-        const int p = a < b ? a : b, q = a < b ? b : a;
+        const bool act = (pi < P / 2) && a < n && b < n;
+        const int p = act ? (a < b ? a : b) : 0, q = act ? (a < b ? b : a) : 0;
+        double xp[E], xq[E];
         double ga = 0.0;
-        for (int i = lane; i < n; i += 32) ga = fma(X[i + p * n], X[i + q * n], ga);
-        ga = warp_sum(ga);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = lig + GL * e;
+          xp[e] = (i < n) ? X[i + p * n] : 0.0;
+          xq[e] = (i < n) ? X[i + q * n] : 0.0;
+          ga = fma(xp[e], xq[e], ga);
+        }
+        ga = gsum(ga);
         const double al = nrm[p], be = nrm[q];
-        if (ga * ga > tol2 * al * be && ga != 0.0) {
+        if (act && ga * ga > tol2 * al * be && ga != 0.0) {
           const double zeta = (be - al) * 0.5 * fast_rcp(ga);
           const double az = fabs(zeta);
           double t;
@@ -295,15 +320,18 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
           }
           const double c = fast_rsqrt(fma(t, t, 1.0));
           const double s = c * t;
-          for (int i = lane; i < n; i += 32) {
-            const double xp = X[i + p * n], xq = X[i + q * n];
-            X[i + p * n] = c * xp - s * xq;
-            X[i + q * n] = s * xp + c * xq;
-            const double vp = V[i + p * n], vq = V[i + q * n];
-            V[i + p * n] = c * vp - s * vq;
-            V[i + q * n] = s * vp + c * vq;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int i = lig + GL * e;
+            if (i < n) {
+              X[i + p * n] = c * xp[e] - s * xq[e];
+              X[i + q * n] = s * xp[e] + c * xq[e];
+              const double vp = V[i + p * n], vq = V[i + q * n];
+              V[i + p * n] = c * vp - s * vq;
+              V[i + q * n] = s * vp + c * vq;
+            }
           }
-          if (lane == 0) {
+          if (lig == 0) {
             nrm[p] = fmax(al - t * ga, 0.0);
             nrm[q] = be + t * ga;
             rotated = 1;
@@ -317,11 +345,16 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
   }
   if (threadIdx.x == 0) jsweeps[0] = (double)(sweep + 1);
   // sigma_j = ||x_j||, then sort descending (rank sort, ties by index)
-  for (int j = warp; j < n; j += nw) {
-    double s = 0.0;
-    for (int i = lane; i < n; i += 32) s = fma(X[i + j * n], X[i + j * n], s);
-    s = warp_sum(s);
-    if (lane == 0) sv[j] = sqrt(s);
+  for (int j0 = 0; j0 < n; j0 += npg) {
+    const int j = j0 + grp;
+    double a = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = lig + GL * e;
+      if (i < n && j < n) a = fma(X[i + j * n], X[i + j * n], a);
+    }
+    a = gsum(a);
+    if (lig == 0 && j < n) sv[j] = sqrt(a);
   }
   __syncthreads();
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
@@ -337,24 +370,32 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
   }
 }
 
-int launch_jacobi_svd(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+template <int NMAX, int GL>
+static int launch_jacobi_t(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
   const size_t need = 2 * (size_t)ell * ell * sizeof(double);
-  int nthr = 32 * ((ell + 1) / 2);
+  const int pairs = (ell + 1) / 2;
+  const int per_warp = 32 / GL;
+  int nthr = 32 * ((pairs + per_warp - 1) / per_warp);
   if (nthr > 1024) nthr = 1024;
-  if (nthr < 64) nthr = 64;
   if (need <= 200 * 1024) {
     static bool set = false;
     if (!set) {
-      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(jacobi_kernel<NMAX, GL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       set = true;
     }
-    jacobi_kernel<true><<<1, nthr, need, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, nullptr, ctx->sc + S_JSWEEPS);
+    jacobi_kernel<NMAX, GL, true><<<1, nthr, need, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, nullptr, ctx->sc + S_JSWEEPS);
   } else {
     double* gws = ctx->wsd("jacobi_ws", 2 * (size_t)ell * ell);
-    jacobi_kernel<false><<<1, nthr, 0, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, gws, ctx->sc + S_JSWEEPS);
+    jacobi_kernel<NMAX, GL, false><<<1, nthr, 0, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, gws, ctx->sc + S_JSWEEPS);
   }
   ctx->launches++;
   return ctx->check_launch("jacobi");
+}
+
+int launch_jacobi_svd(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+  if (ell <= 64) return launch_jacobi_t<64, 8>(ctx, ell, R, ldr, V, ldv, sigma);
+  if (ell <= 128) return launch_jacobi_t<128, 16>(ctx, ell, R, ldr, V, ldv, sigma);
+  return launch_jacobi_t<256, 32>(ctx, ell, R, ldr, V, ldv, sigma);
 }
 
 // lambda_hat = max{0, sigma^2 - nu}

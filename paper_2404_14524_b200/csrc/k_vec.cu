@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256) dots_kernel(const DotArgs D) {
   }
   block_sum_to_part<4>(v, D.part, gridDim.x);
   if (last_block_arrive(D.counter)) {
-    const int wk = threadIdx.x >> 5;
+    const int wk = warp_uniform_id();
     if (wk < D.nv) {
       const double v0 = warp_sum_array(D.part + (size_t)wk * gridDim.x, gridDim.x);
       if ((threadIdx.x & 31) == 0) D.sc[D.out[wk]] = v0;
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(256) ratio_kernel(const RatioArgs R) {
     R.part[blockIdx.x] = a;
     R.part[gridDim.x + blockIdx.x] = b;
   }
-  if (last_block_arrive(R.counter) && threadIdx.x < 32) {
+  if (last_block_arrive(R.counter) && warp_uniform_id() == 0) {
     const double a = warp_min_array(R.part, gridDim.x);
     const double b = warp_min_array(R.part + gridDim.x, gridDim.x);
     if (threadIdx.x != 0) return;
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
   __shared__ double rsh[PCG_RB];
   __shared__ double s_alpha;
   __shared__ int s_ok;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31;
   if (!A.init) {
     if (warp == 0) {
       double pw;
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
   }
   if (last_block_arrive(A.counter)) {
     __shared__ int conv;
-    if (tid < 32) {
+    if (warp == 0) {
       const double rrt = warp_sum_array(A.part, gridDim.x);
       if (tid == 0) {
         A.sc[S_RR] = rrt;
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
   }
   double v[1] = {rz};
   block_sum_to_part<1>(v, A.part, gridDim.x);
-  if (last_block_arrive(A.counter) && threadIdx.x < 32) {
+  if (last_block_arrive(A.counter) && warp_uniform_id() == 0) {
     const double rzn = warp_sum_array(A.part, gridDim.x);
     if (threadIdx.x != 0) return;
     const double rzo = A.sc[S_RZ];
@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(256) minsum_kernel(int64_t n, const double* u,
     part[blockIdx.x] = a;
     part[gridDim.x + blockIdx.x] = b;
   }
-  if (last_block_arrive(counter) && threadIdx.x < 32) {
+  if (last_block_arrive(counter) && warp_uniform_id() == 0) {
     const double a = warp_min_array(part, gridDim.x);
     const double b = warp_sum_array(part + gridDim.x, gridDim.x);
     if (threadIdx.x != 0) return;

@@ -39,6 +39,12 @@ int launch_minsum(nys_ctx* ctx, int64_t n, const double* u, double shift, int mi
 int launch_check_pos(nys_ctx* ctx, int64_t n, const double* d, unsigned long long* bad);
 int launch_set_slots(nys_ctx* ctx, int k0, double v0, int k1 = -1, double v1 = 0, int k2 = -1, double v2 = 0);
 
+// k_pcg.cu — persistent cooperative PCG (single GPU, m <= 8192)
+bool pcg_persistent_supported(nys_ctx* ctx, int64_t m, int64_t n, int ell);
+int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                          const double* e, const double* U, int64_t ldu, int ell, const double* s, const double* rhs,
+                          double* x, int max_iter);
+
 // k_gemm.cu — fp64 DMMA GEMM  C(MxN, col-major) = Aop(MxK) * Bop(KxN)
 //   a_kmajor = true : Aop(i,k) = A[i*lda + k]      (e.g. A^T of a column-major matrix)
 //   a_kmajor = false: Aop(i,k) = A[i + k*lda]      (column-major)

@@ -8,6 +8,7 @@
 #include <dlfcn.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -330,6 +331,16 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
   double* Pp[2] = {P0, P1};
   const double* done = ctx->sc + S_DONE;
   NYS_TRY(launch_set_slots(ctx, S_DELTA, op.delta, S_GITER, 0.0));
+  if (pcg_persistent_supported(ctx, m, op.n, ell)) {
+    // the whole solve is ONE cooperative launch (k_pcg.cu)
+    NYS_TRY(launch_pcg_persistent(ctx, m, op.n, op.A, op.lda, op.d, op.e, U, ldu, ell, s, rhs, x, max_iter));
+    NYS_TRY(read_slots(ctx));
+    res.iters = (int)ctx->h_sc[S_ITERS];
+    res.status = (int)ctx->h_sc[S_STATUS];
+    res.rr = ctx->h_sc[S_RR];
+    ctx->matvecs += res.iters;
+    return NYS_OK;
+  }
   NYS_TRY(launch_pcg_update(ctx, 1, m, x, r, rhs, nullptr, nullptr, nullptr, op.delta, op.e, U, ldu, ell, s, h,
                             max_iter));
   if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 1, m, r, z, U, ldu, ell, h));
@@ -440,7 +451,7 @@ __global__ void finalize_terms_kernel(int64_t m, double* w, const double* v, dou
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x < 32) {
+  if (last && warp_uniform_id() == 0) {
     __threadfence();
     const double pw = warp_sum_array(part, gridDim.x);
     if (threadIdx.x != 0) return;

@@ -166,6 +166,10 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// warp index broadcast from lane 0: lets the compiler prove warp-uniform branches, so shuffles
+// inside them are not lowered to the slow WARPSYNC.COLLECTIVE path (cf. CUTLASS canonical_warp_idx_sync)
+__device__ __forceinline__ int warp_uniform_id() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
