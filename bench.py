@@ -26,6 +26,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fp64 A·D·Aᵀv matvec GB/s (% HBM peak) and Nys-IP-PMM time-to-1e-8 at 1/2/4/8 GPU"
+# dram__bytes_read.sum + dram__bytes_write.sum per fused-matvec launch from `ncu --set full`
+# (profiles/, per config); None until captured for that config
+TRAFFIC = {1: 134.6e6}
 
 
 def _peaks():
@@ -192,22 +195,54 @@ def main():
     matvecs_per_solve = results[-1]["matvecs"]
 
     # ---- dominant kernel: fused normal matvec, timed live with CUDA events on its stream ------
+    # The launches are captured in CUDA graphs (no host overhead between launches):
+    #   warm = R back-to-back matvecs;  cold = R x (256 MB L2-flushing read + matvec) minus R x flush
     rs = np.random.default_rng(0)
     d = dv(rs.uniform(0.01, 2.0, nloc))
     v = dv(rs.standard_normal(m))
     w = torch.empty(m, dtype=torch.float64, device=f"cuda:{local}")
+    flush = torch.ones(32 * 1024 * 1024, dtype=torch.float64, device=f"cuda:{local}")  # 256 MB
+    R = args.matvec_reps
     with torch.cuda.stream(stream):
         for _ in range(5):
             ctx.nys_normal_matvec(Ad, lda, m, d, None, 1e-3, v, w)
+            flush.sum()
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    with torch.cuda.stream(stream):
-        for _ in range(args.matvec_reps):
-            ctx.nys_normal_matvec(Ad, lda, m, d, None, 1e-3, v, w)
-    e1.record(stream)
+
+    def capture(fn):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(R):
+                fn()
+        return g
+
+    def mv():
+        ctx.nys_normal_matvec(Ad, lda, m, d, None, 1e-3, v, w)
+
+    fl_out = torch.empty((), dtype=torch.float64, device=f"cuda:{local}")
+
+    def fl():
+        torch.sum(flush, dim=0, out=fl_out)
+
+    g_warm = capture(mv)
+    g_cold = capture(lambda: (fl(), mv()))
+    g_flush = capture(fl)
     barrier()
-    mv_s = e0.elapsed_time(e1) / 1e3 / args.matvec_reps
+
+    def timed(g):
+        g.replay()
+        barrier()
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        with torch.cuda.stream(stream):
+            g.replay()
+        b_.record(stream)
+        barrier()
+        return a.elapsed_time(b_) / 1e3
+
+    mv_warm_s = timed(g_warm) / R
+    mv_s = (timed(g_cold) - timed(g_flush)) / R
+    del g_warm, g_cold, g_flush, flush
     mv_bytes = 8.0 * (m * nloc + nloc + 2 * m)  # A once + d + v in + w out
     mv_gbs = mv_bytes / mv_s / 1e9
     peaks = _peaks()
@@ -257,8 +292,10 @@ def main():
             "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": mv_gbs, "peak": hbm, "unit": "GB/s", "frac": mv_gbs / hbm,
-                         "traffic": None, "kernel": "fused normal matvec (matvec_kernel + mv_finalize)",
+                         "traffic": TRAFFIC.get(args.config), "kernel": "fused normal matvec (matvec_kernel + mv_finalize), L2 flushed (256 MB read) before each launch, graph-captured",
                          "peak_source": peak_src, "bytes_per_launch": mv_bytes, "launch_us": mv_s * 1e6,
+                         "warm_l2_gbs": mv_bytes / mv_warm_s / 1e9,
+                         "pcg_effective_gbs": last["inner"] * mv_bytes / (last["t_pcg_ms"] / 1e3) / 1e9,
                          "share_of_step": matvecs_per_solve * mv_s / sec_per_solve},
             "solve": {"outer": last["outer"], "inner": last["inner"], "obj": last["obj"], "rel_p": last["rel_p"],
                       "rel_d": last["rel_d"], "mu": last["mu"], "matvecs": matvecs_per_solve,

@@ -176,6 +176,9 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
 
+      double dpre[CPG];  // scaling of this group's columns, loaded before the dot (hides L2 latency)
+#pragma unroll
+      for (int c = 0; c < CPG; ++c) dpre[c] = (MODE == MV_FUSED && col0 + c < P.n) ? __ldg(P.d + col0 + c) : 0.0;
       double t[CPG];
       if (MODE != MV_NONLY) {
         double pd[CPG];
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
         }
         if (MODE == MV_FUSED) {
 #pragma unroll
-          for (int c = 0; c < CPG; ++c) t[c] = (col0 + c < P.n) ? P.d[col0 + c] * pd[c] : 0.0;
+          for (int c = 0; c < CPG; ++c) t[c] = dpre[c] * pd[c];
           if (lig == 0 && crank == 0) {
 #pragma unroll
             for (int c = 0; c < CPG; ++c) pwacc = fma(t[c], pd[c], pwacc);  // d_j (a_j^T v)^2
@@ -475,6 +478,9 @@ static MvKernel kernel_for(const MvCfg& c) {
   if (c.T == 256 && c.GT == 64 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<256, 64, 4, 2, MODE, false>;
   if (c.T == 256 && c.GT == 128 && c.RPT == 8 && c.CPG == 2) return matvec_kernel<256, 128, 8, 2, MODE, false>;
   if (c.T == 256 && c.GT == 256 && c.RPT == 8 && c.CPG == 4) return matvec_kernel<256, 256, 8, 4, MODE, false>;
+  if (c.T == 256 && c.GT == 256 && c.RPT == 8 && c.CPG == 2) return matvec_kernel<256, 256, 8, 2, MODE, false>;
+  if (c.T == 512 && c.GT == 512 && c.RPT == 4 && c.CPG == 4) return matvec_kernel<512, 512, 4, 4, MODE, false>;
+  if (c.T == 512 && c.GT == 512 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<512, 512, 4, 2, MODE, false>;
   if (c.T == 512 && c.GT == 512 && c.RPT == 8 && c.CPG == 2) return matvec_kernel<512, 512, 8, 2, MODE, false>;
   return matvec_kernel<512, 512, 16, 1, MODE, true>;
 }
@@ -515,9 +521,14 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, MvPlan& pl) {
   int64_t rs = (m + cl - 1) / cl;
   rs = (rs + 1) & ~int64_t(1);
   MvCfg c = pick_cfg(rs);
+  if (const char* ov = getenv("NYS_MV_CFG")) {  // debug/tuning override "T,GT,RPT,CPG" (must be instantiated)
+    MvCfg o;
+    if (sscanf(ov, "%d,%d,%d,%d", &o.T, &o.GT, &o.RPT, &o.CPG) == 4 && (int64_t)o.GT * o.RPT >= rs) c = o;
+  }
   const int NG = c.T / c.GT, BN = NG * c.CPG;
   const size_t stage_bytes = (size_t)BN * rs * 8;
   size_t budget = (rs <= 1024) ? 96 * 1024 : 200 * 1024;
+  if (const char* sb = getenv("NYS_MV_SMEM_KB")) budget = (size_t)atoi(sb) * 1024;
   if (cfg_vs(c)) budget -= (size_t)rs * 8;
   int stages = (int)(budget / stage_bytes);
   stages = stages > 8 ? 8 : stages;
@@ -553,14 +564,20 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, MvPlan& pl) {
     int64_t g = (int64_t)ctx->num_sms * occ;
     grid = (int)(npanels < g ? npanels : g);
     // reduction clusters: pick the cluster size (8 or 4) that keeps >= 95% of the CTAs resident
-    if (mode != MV_TONLY && grid >= 16) {
-      for (int cs : {8, 4}) {
+    // measured on B200 (config 1): DSMEM reduction clusters cost more than the partial rows they
+    // save (rc=2: +8%, rc=4/8: fewer resident CTAs), so they are opt-in (NYS_MV_RC) only
+    if (mode != MV_TONLY && grid >= 16 && getenv("NYS_MV_RC")) {
+      const char* frc = getenv("NYS_MV_RC");
+      const double keep = frc ? 0.0 : 0.95;
+      for (int cs : {8, 4, 2}) {
+        if (frc && atoi(frc) != cs) continue;
         int ncs = 0;
         max_clusters(cs, ncs);
         int64_t gc = (int64_t)ncs * cs;
         int64_t need = (npanels + cs - 1) / cs * cs;
         if (gc > need) gc = need;
-        if (gc >= (int64_t)(0.95 * grid) && gc >= cs) { rc = cs; grid = (int)gc; break; }
+        if (getenv("NYS_DEBUG")) fprintf(stderr, "[nys] reduction cluster %d: max active clusters %d -> %lld CTAs (grid %d)\n", cs, ncs, (long long)gc, grid);
+        if (gc >= (int64_t)(keep * grid) && gc >= cs) { rc = cs; grid = (int)gc; break; }
       }
     }
   } else {

@@ -336,6 +336,9 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      double dpre[CPG];
+#pragma unroll
+      for (int c = 0; c < CPG; ++c) dpre[c] = (col0 + c < P.n) ? __ldg(P.d + col0 + c) : 0.0;
       double pd[CPG];
 #pragma unroll
       for (int c = 0; c < CPG; ++c) {
@@ -361,7 +364,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       }
       double t[CPG];
 #pragma unroll
-      for (int c = 0; c < CPG; ++c) t[c] = (col0 + c < P.n) ? P.d[col0 + c] * pd[c] : 0.0;
+      for (int c = 0; c < CPG; ++c) t[c] = dpre[c] * pd[c];
       if (lig == 0) {
 #pragma unroll
         for (int c = 0; c < CPG; ++c) pwacc = fma(t[c], pd[c], pwacc);
