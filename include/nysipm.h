@@ -159,6 +159,12 @@ typedef struct {
   const double* b;       /* m (replicated)                                                 */
   const double* c;       /* n (local)                                                      */
   int host_ptrs;         /* 1: A, q, b, c are HOST pointers (copied in by the library)     */
+  int structure;         /* 0: A is dense m x n.  1: SVM-shaped (BASELINE configs[2], SURVEY
+                            A23): A = [Xt, -Xt, I_m, -I_m] with the dense block Xt (m x nd,
+                            column-major, lda) passed in `A`; n = 2 nd + 2 m variables ordered
+                            [w+, w-, xi, s].  The identity blocks are never materialised: they
+                            contribute the diagonal term e = d_xi + d_s of the normal operator.   */
+  int64_t nd;            /* structure 1: number of dense columns (features) d              */
 } nys_qp;
 
 typedef struct {

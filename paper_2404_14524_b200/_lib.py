@@ -38,7 +38,8 @@ class PcgInfo(C.Structure):
 
 class QP(C.Structure):
     _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("A", C.c_void_p), ("lda", C.c_int64), ("q", C.c_void_p),
-                ("b", C.c_void_p), ("c", C.c_void_p), ("host_ptrs", C.c_int)]
+                ("b", C.c_void_p), ("c", C.c_void_p), ("host_ptrs", C.c_int), ("structure", C.c_int),
+                ("nd", C.c_int64)]
 
 
 class Options(C.Structure):
@@ -225,10 +226,12 @@ class Context:
 
     def nys_ipppmm_solve(self, A, lda: int, m: int, q, b, c, ell: int = 0, tol: float = 1e-8, seed: int = 0,
                          max_outer: int = 100, host: bool = False, max_records: int = 256, verbose: bool = False,
-                         **opt_overrides):
-        """A: device tensor (n, lda) [or host numpy (n, lda) when host=True]; q, c: n; b: m."""
+                         structure: int = 0, **opt_overrides):
+        """A: device tensor (ncols, lda) [or host numpy when host=True]; q, c: n; b: m.
+        structure=1: A holds the dense block Xt (nd columns) of A = [Xt, -Xt, I, -I]; n = 2 nd + 2 m."""
         import torch
-        n = A.shape[0]
+        nd = A.shape[0]
+        n = q.shape[0]
         opts = Options()
         self.lib.nys_default_options(C.byref(opts))
         opts.ell, opts.tol, opts.seed, opts.max_outer, opts.verbose = ell, tol, seed, max_outer, int(verbose)
@@ -245,7 +248,7 @@ class Context:
             x = torch.zeros(n, dtype=torch.float64, device=A.device)
             y = torch.zeros(m, dtype=torch.float64, device=A.device)
             z = torch.zeros(n, dtype=torch.float64, device=A.device)
-        qp = QP(m, n, _ptr(A), lda, _ptr(q), _ptr(b), _ptr(c), 1 if host else 0)
+        qp = QP(m, n, _ptr(A), lda, _ptr(q), _ptr(b), _ptr(c), 1 if host else 0, structure, nd if structure else 0)
         recs = (IterRecord * max_records)()
         rep = Report()
         rep.max_records = max_records

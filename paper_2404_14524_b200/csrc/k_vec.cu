@@ -791,6 +791,87 @@ int launch_minsum(nys_ctx* ctx, int64_t n, const double* u, double shift, int mi
   return ctx->check_launch("minsum");
 }
 
+// ------------------------------------------------------------------------------------------
+// SVM-structured A = [Xt, -Xt, I, -I]: variables [w+ (nd), w- (nd), xi (m), s (m)]
+// ------------------------------------------------------------------------------------------
+// A^T y = [Xt^T y ; -Xt^T y ; y ; -y]   from g = Xt^T y
+__global__ void svm_expand_kernel(int64_t nd, int64_t m, const double* g, const double* y, double* atv) {
+  const int64_t n = 2 * nd + 2 * m;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double v;
+    if (j < nd) v = g[j];
+    else if (j < 2 * nd) v = -g[j - nd];
+    else if (j < 2 * nd + m) v = y[j - 2 * nd];
+    else v = -y[j - 2 * nd - m];
+    atv[j] = v;
+  }
+}
+// A u = Xt (u_w+ - u_w-) + u_xi - u_s :  uw (nd) and the diagonal part addm (m) (+ add)
+__global__ void svm_fold_kernel(int64_t nd, int64_t m, const double* u, const double* add, double* uw, double* addm) {
+  const int64_t tot = nd + m;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < tot; j += (int64_t)gridDim.x * blockDim.x) {
+    if (j < nd) uw[j] = u[j] - u[nd + j];
+    else {
+      const int64_t i = j - nd;
+      addm[i] = u[2 * nd + i] - u[2 * nd + m + i] + (add ? add[i] : 0.0);
+    }
+  }
+}
+// normal operator of the structured A: N = Xt diag(d_w+ + d_w-) Xt^T + diag(d_xi + d_s)
+__global__ void svm_scaling_fold_kernel(int64_t nd, int64_t m, const double* d, double* dw, double* e) {
+  const int64_t tot = nd + m;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < tot; j += (int64_t)gridDim.x * blockDim.x) {
+    if (j < nd) dw[j] = d[j] + d[nd + j];
+    else {
+      const int64_t i = j - nd;
+      e[i] = d[2 * nd + i] + d[2 * nd + m + i];
+    }
+  }
+}
+// generic IPM epilogues on an explicit A^T v (n-vector)
+__global__ void epi_rd_kernel(int64_t n, const double* c, const double* q, const double* x, const double* atv,
+                              const double* z, double* out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = c[j] + q[j] * x[j] - atv[j] - (z ? z[j] : 0.0);
+}
+__global__ void epi_dx_kernel(int64_t n, const double* atv, const double* rd, const double* xiau, const double* rxz,
+                              const double* z, const double* x, const double* d, double* dx, double* dz) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double v = d[j] * (atv[j] - (rd ? rd[j] : 0.0) - xiau[j]);
+    dx[j] = v;
+    dz[j] = (rxz[j] - z[j] * v) / x[j];
+  }
+}
+int launch_svm_expand(nys_ctx* ctx, int64_t nd, int64_t m, const double* g, const double* y, double* atv) {
+  svm_expand_kernel<<<ew_grid(ctx, 2 * nd + 2 * m), 256, 0, ctx->stream>>>(nd, m, g, y, atv);
+  ctx->launches++;
+  return ctx->check_launch("svm_expand");
+}
+int launch_svm_fold(nys_ctx* ctx, int64_t nd, int64_t m, const double* u, const double* add, double* uw, double* addm) {
+  svm_fold_kernel<<<ew_grid(ctx, nd + m), 256, 0, ctx->stream>>>(nd, m, u, add, uw, addm);
+  ctx->launches++;
+  return ctx->check_launch("svm_fold");
+}
+int launch_svm_scaling_fold(nys_ctx* ctx, int64_t nd, int64_t m, const double* d, double* dw, double* e) {
+  svm_scaling_fold_kernel<<<ew_grid(ctx, nd + m), 256, 0, ctx->stream>>>(nd, m, d, dw, e);
+  ctx->launches++;
+  return ctx->check_launch("svm_scaling_fold");
+}
+int launch_epi_rd(nys_ctx* ctx, int64_t n, const double* c, const double* q, const double* x, const double* atv,
+                  const double* z, double* out) {
+  if (n <= 0) return NYS_OK;
+  epi_rd_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, c, q, x, atv, z, out);
+  ctx->launches++;
+  return ctx->check_launch("epi_rd");
+}
+int launch_epi_dx(nys_ctx* ctx, int64_t n, const double* atv, const double* rd, const double* xiau, const double* rxz,
+                  const double* z, const double* x, const double* d, double* dx, double* dz) {
+  if (n <= 0) return NYS_OK;
+  epi_dx_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, atv, rd, xiau, rxz, z, x, d, dx, dz);
+  ctx->launches++;
+  return ctx->check_launch("epi_dx");
+}
+
 // positivity check of d (nys_check_scaling): first bad index -> slot
 __global__ void check_pos_kernel(int64_t n, const double* d, unsigned long long* bad) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {

@@ -36,6 +36,13 @@ int launch_mul(nys_ctx* ctx, int64_t n, const double* u, const double* v, double
 int launch_cpqx(nys_ctx* ctx, int64_t n, const double* c, const double* q, const double* x, double* t);
 int launch_shift(nys_ctx* ctx, int64_t n, double* u, double s);
 int launch_minsum(nys_ctx* ctx, int64_t n, const double* u, double shift, int min_slot, int sum_slot, int counter_slot);
+int launch_svm_expand(nys_ctx* ctx, int64_t nd, int64_t m, const double* g, const double* y, double* atv);
+int launch_svm_fold(nys_ctx* ctx, int64_t nd, int64_t m, const double* u, const double* add, double* uw, double* addm);
+int launch_svm_scaling_fold(nys_ctx* ctx, int64_t nd, int64_t m, const double* d, double* dw, double* e);
+int launch_epi_rd(nys_ctx* ctx, int64_t n, const double* c, const double* q, const double* x, const double* atv,
+                  const double* z, double* out);
+int launch_epi_dx(nys_ctx* ctx, int64_t n, const double* atv, const double* rd, const double* xiau, const double* rxz,
+                  const double* z, const double* x, const double* d, double* dx, double* dz);
 int launch_check_pos(nys_ctx* ctx, int64_t n, const double* d, unsigned long long* bad);
 int launch_set_slots(nys_ctx* ctx, int k0, double v0, int k1 = -1, double v1 = 0, int k2 = -1, double v2 = 0);
 

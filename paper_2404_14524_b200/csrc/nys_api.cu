@@ -497,6 +497,70 @@ struct Dots {
   }
 };
 
+// A-products of the driver for a dense A (structure 0) or the SVM-shaped A = [Xt, -Xt, I, -I]
+// (structure 1; Xt = the dense block, never materialising the identity blocks).
+struct AOps {
+  nys_ctx* ctx;
+  int structure;
+  int64_t m, n, nd;        // n = variables; nd = columns of the dense block (n for structure 0)
+  const double* A;         // dense block, column-major, lda
+  int64_t lda;
+  double *g, *atv, *uw, *addm, *dw, *e;  // structure-1 work vectors
+  // normal operator for the scaling d (n): dense -> (A, d); structured -> (Xt, d_w+ + d_w-, e)
+  int normal_op(const double* d, double delta, NormalOp& op) {
+    if (structure == 0) { op = NormalOp{m, n, lda, A, d, nullptr, delta}; return NYS_OK; }
+    NYS_TRY(launch_svm_scaling_fold(ctx, nd, m, d, dw, e));
+    op = NormalOp{m, nd, lda, A, dw, e, delta};
+    return NYS_OK;
+  }
+  // out = A u (+ add)
+  int Ax(const double* u, double* out, const double* add) {
+    if (structure == 0) return apply_A(ctx, m, n, A, lda, u, out, 1.0, add);
+    NYS_TRY(launch_svm_fold(ctx, nd, m, u, add, uw, addm));
+    return apply_A(ctx, m, nd, A, lda, uw, out, 1.0, addm);
+  }
+  // structured: atv = A^T y (n-vector)
+  int At_vec(const double* y) {
+    MatvecCall mc;
+    mc.mode = MV_TONLY; mc.m = m; mc.n = nd; mc.lda = lda; mc.A = A; mc.z = y; mc.tep = TE_PLAIN; mc.t1 = g;
+    NYS_TRY(apply_At(ctx, mc));
+    return launch_svm_expand(ctx, nd, m, g, y, atv);
+  }
+  int At_plain(const double* y, double* out) {
+    if (structure == 0) {
+      MatvecCall mc;
+      mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = y; mc.tep = TE_PLAIN; mc.t1 = out;
+      return apply_At(ctx, mc);
+    }
+    NYS_TRY(At_vec(y));
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(out, atv, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    return NYS_OK;
+  }
+  // out = c + q x - A^T y - z   (z may be null)
+  int At_rd(const double* y, const double* c, const double* q, const double* x, const double* z, double* out) {
+    if (structure == 0) {
+      MatvecCall mc;
+      mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = y; mc.tep = TE_RD;
+      mc.t1 = out; mc.ta = c; mc.tb = q; mc.tc = x; mc.td = z;
+      return apply_At(ctx, mc);
+    }
+    NYS_TRY(At_vec(y));
+    return launch_epi_rd(ctx, n, c, q, x, atv, z, out);
+  }
+  // dx = d (A^T dy - r_d - xi_au); dz = (r_xz - z dx) / x
+  int At_dx(const double* dy, const double* rd, const double* xiau, const double* rxz, const double* z,
+            const double* x, const double* d, double* dx, double* dz) {
+    if (structure == 0) {
+      MatvecCall mc;
+      mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = dy; mc.tep = TE_DX;
+      mc.t1 = dx; mc.t2 = dz; mc.ta = rd; mc.tb = xiau; mc.tc = rxz; mc.td = z; mc.tx = x; mc.tdd = d;
+      return apply_At(ctx, mc);
+    }
+    NYS_TRY(At_vec(dy));
+    return launch_epi_dx(ctx, n, atv, rd, xiau, rxz, z, x, d, dx, dz);
+  }
+};
+
 int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solution* sol, nys_report* rep) {
   auto t_start = std::chrono::steady_clock::now();
   const int64_t m = qp_in->m, n = qp_in->n;
@@ -506,11 +570,12 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   // ---- problem data on the device --------------------------------------------------------
   const double *A = qp_in->A, *q = qp_in->q, *b = qp_in->b, *c = qp_in->c;
   int64_t lda = qp_in->lda;
+  const int64_t ncolA = qp_in->structure == 1 ? qp_in->nd : n;  // dense columns stored
   if (qp_in->host_ptrs) {
     const int64_t ldd = even(m);
-    double* Ad = ctx->wsd("ipm_A", (size_t)ldd * (n > 0 ? n : 1));
-    if (n > 0)
-      NYS_CUDA_TRY(ctx, cudaMemcpy2DAsync(Ad, ldd * 8, qp_in->A, qp_in->lda * 8, m * 8, n, cudaMemcpyHostToDevice, ctx->stream));
+    double* Ad = ctx->wsd("ipm_A", (size_t)ldd * (ncolA > 0 ? ncolA : 1));
+    if (ncolA > 0)
+      NYS_CUDA_TRY(ctx, cudaMemcpy2DAsync(Ad, ldd * 8, qp_in->A, qp_in->lda * 8, m * 8, ncolA, cudaMemcpyHostToDevice, ctx->stream));
     double* qd = ctx->wsd("ipm_q", (size_t)np_ + 2);
     double* cd = ctx->wsd("ipm_c", (size_t)np_ + 2);
     double* bd = ctx->wsd("ipm_b", (size_t)mp);
@@ -536,6 +601,15 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   double *Om = ctx->wsd("ipm_Om", (size_t)mp * le), *U = ctx->wsd("ipm_U", (size_t)mp * le);
   double *lamh = ctx->wsd("ipm_lamh", (size_t)le), *scoef = ctx->wsd("ipm_s", (size_t)le);
   Dots D{ctx};
+  AOps AO{ctx, qp_in->structure, m, n, ncolA, A, lda, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (AO.structure == 1) {
+    AO.g = ctx->wsd("svm_g", (size_t)even(ncolA) + 2);
+    AO.atv = ctx->wsd("svm_atv", nn);
+    AO.uw = ctx->wsd("svm_uw", (size_t)even(ncolA) + 2);
+    AO.addm = ctx->wsd("svm_addm", mm);
+    AO.dw = ctx->wsd("svm_dw", (size_t)even(ncolA) + 2);
+    AO.e = ctx->wsd("svm_e", mm);
+  }
   double n_total = (double)n;
   {
     // global variable count (for mu = x^T z / n)
@@ -561,11 +635,12 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   // ---- initial point (App. B.2; u = 0) --------------------------------------
   NYS_CUDA_TRY(ctx, cudaMemsetAsync(ones, 0, nn * sizeof(double), ctx->stream));
   NYS_TRY(launch_shift(ctx, n, ones, 1.0));
-  NormalOp op0{m, n, lda, A, ones, nullptr, opt->init_delta};
+  NormalOp op0;
+  NYS_TRY(AO.normal_op(ones, opt->init_delta, op0));
   if (ell > 0) {
     auto ts = std::chrono::steady_clock::now();
     NYS_TRY(gen_omega(ctx, m, ell, opt->seed, 0, Om));                 // stream 0
-    NYS_TRY(sketch_impl(ctx, m, n, A, lda, ones, nullptr, ell, Om, U, lamh, nullptr));
+    NYS_TRY(sketch_impl(ctx, m, op0.n, op0.A, op0.lda, op0.d, op0.e, ell, Om, U, lamh, nullptr));
     NYS_TRY(launch_prec_coef(ctx, lamh, ell, opt->init_delta, scoef));
     t_sketch += ms_since(ts);
   }
@@ -575,24 +650,15 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   NYS_TRY(launch_pcg_setup(ctx, 2, 0, 0, 0, S_XINORM, 0, 0, opt->init_tol_rel));
   NYS_TRY(pcg_impl(ctx, op0, ell, U, mp, scoef, b, u1, opt->pcg_max_iter, pr));
   total_inner += pr.iters;
-  {  // x~ = A^T u1
-    MatvecCall mc;
-    mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = u1; mc.tep = TE_PLAIN; mc.t1 = x;
-    NYS_TRY(apply_At(ctx, mc));
-  }
+  NYS_TRY(AO.At_plain(u1, x));                                       // x~ = A^T u1
   NYS_TRY(launch_cpqx(ctx, n, c, q, x, t));                          // c + Q x~
-  NYS_TRY(apply_A(ctx, m, n, A, lda, t, xi, 1.0, nullptr));          // A (c + Q x~)
+  NYS_TRY(AO.Ax(t, xi, nullptr));                                    // A (c + Q x~)
   NYS_TRY(D.dot(m, xi, xi, S_XINORM));
   NYS_TRY(launch_pcg_setup(ctx, 2, 0, 0, 0, S_XINORM, 0, 0, opt->init_tol_rel));
   NYS_TRY(pcg_impl(ctx, op0, ell, U, mp, scoef, xi, y, opt->pcg_max_iter, pr));
   total_inner += pr.iters;
   t_pcg += ms_since(tp);
-  {  // z~ = c - A^T y~ + Q x~
-    MatvecCall mc;
-    mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = y; mc.tep = TE_RD;
-    mc.t1 = z; mc.ta = c; mc.tb = q; mc.tc = x; mc.td = nullptr;
-    NYS_TRY(apply_At(ctx, mc));
-  }
+  NYS_TRY(AO.At_rd(y, c, q, x, nullptr, z));                         // z~ = c - A^T y~ + Q x~
   NYS_TRY(launch_minsum(ctx, n, x, 0.0, S_TMP0, S_TMP1, 6));
   NYS_TRY(launch_minsum(ctx, n, z, 0.0, S_TMP2, S_TMP3, 7));
   NYS_TRY(D.dot(n, x, z, S_TMP4));
@@ -625,12 +691,9 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
 
   auto residuals = [&]() -> int {
     // r_P = b - A x ; r_D = c + Q x - A^T y - z ; ||r_P||^2, ||r_D||^2, x^T z
-    NYS_TRY(apply_A(ctx, m, n, A, lda, x, ax, 1.0, nullptr));
+    NYS_TRY(AO.Ax(x, ax, nullptr));
     NYS_TRY(launch_axpby(ctx, m, 1.0, b, -1.0, ax, rP));
-    MatvecCall mc;
-    mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = y; mc.tep = TE_RD;
-    mc.t1 = rD; mc.ta = c; mc.tb = q; mc.tc = x; mc.td = z;
-    NYS_TRY(apply_At(ctx, mc));
+    NYS_TRY(AO.At_rd(y, c, q, x, z, rD));
     NYS_TRY(D.dot(m, rP, rP, S_TMP0));
     NYS_TRY(D.dot(n, rD, rD, S_TMP1));
     NYS_TRY(D.dot(n, x, z, S_TMP2));
@@ -653,21 +716,22 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     rec.k = k; rec.mu = mu; rec.rel_p = rel_p; rec.rel_d = rel_d; rec.rho = rho; rec.delta = delta;
     auto t_it = std::chrono::steady_clock::now();
     NYS_TRY(launch_scaling(ctx, n, q, x, z, rho, d));
+    NormalOp op;
+    NYS_TRY(AO.normal_op(d, delta, op));
     if (ell > 0) {                                                    // P:759, Alg. 2
       auto ts = std::chrono::steady_clock::now();
       NYS_TRY(gen_omega(ctx, m, ell, opt->seed, (uint64_t)k + 1, Om));
-      NYS_TRY(sketch_impl(ctx, m, n, A, lda, d, nullptr, ell, Om, U, lamh, nullptr));
+      NYS_TRY(sketch_impl(ctx, m, op.n, op.A, op.lda, op.d, op.e, ell, Om, U, lamh, nullptr));
       NYS_TRY(launch_prec_coef(ctx, lamh, ell, delta, scoef));        // mu_prec = delta_k (A7)
       NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
       rec.t_sketch_ms = ms_since(ts);
       t_sketch += rec.t_sketch_ms;
     }
-    NormalOp op{m, n, lda, A, d, nullptr, delta};
     NYS_TRY(launch_set_slots(ctx, S_MUCUR, mu));
     // ---- predictor ----
     NYS_TRY(launch_pred_rhs_n(ctx, n, x, z, zeta, rD, rho, d, rd, rxz, xiau, t));
     NYS_TRY(launch_pred_rhs_m(ctx, m, b, ax, y, lam, delta, rp));
-    NYS_TRY(apply_A(ctx, m, n, A, lda, t, xi, 1.0, rp));             // xi = r_p + A d (r_d + xi_au)
+    NYS_TRY(AO.Ax(t, xi, rp));                                        // xi = r_p + A d (r_d + xi_au)
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
     NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
     auto tp1 = std::chrono::steady_clock::now();
@@ -675,12 +739,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     rec.t_pcg_ms += ms_since(tp1);
     if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
     rec.pcg_pred = pr.iters;
-    {
-      MatvecCall mc;  // dx = d (A^T dy - r_d - xi_au); dz = (r_xz - z dx)/x
-      mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = dyp; mc.tep = TE_DX;
-      mc.t1 = dxp; mc.t2 = dzp; mc.ta = rd; mc.tb = xiau; mc.tc = rxz; mc.td = z; mc.tx = x; mc.tdd = d;
-      NYS_TRY(apply_At(ctx, mc));
-    }
+    NYS_TRY(AO.At_dx(dyp, rd, xiau, rxz, z, x, d, dxp, dzp));        // dx, dz (A15)
     NYS_TRY(launch_ratio(ctx, n, x, dxp, nullptr, nullptr, z, dzp, nullptr, nullptr, 8));
     NYS_TRY(allreduce_slots(ctx, S_TMP0, 2, true));
     NYS_TRY(launch_steps_post(ctx));
@@ -691,7 +750,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     }
     // ---- corrector ----
     NYS_TRY(launch_corr_rhs(ctx, n, x, dxp, dzp, d, rxz, xiau, t));
-    NYS_TRY(apply_A(ctx, m, n, A, lda, t, xi, 1.0, nullptr));
+    NYS_TRY(AO.Ax(t, xi, nullptr));
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
     NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
     auto tp2 = std::chrono::steady_clock::now();
@@ -699,12 +758,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     rec.t_pcg_ms += ms_since(tp2);
     if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
     rec.pcg_corr = pr.iters;
-    {
-      MatvecCall mc;
-      mc.mode = MV_TONLY; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A; mc.z = dyc; mc.tep = TE_DX;
-      mc.t1 = dxc; mc.t2 = dzc; mc.ta = nullptr; mc.tb = xiau; mc.tc = rxz; mc.td = z; mc.tx = x; mc.tdd = d;
-      NYS_TRY(apply_At(ctx, mc));
-    }
+    NYS_TRY(AO.At_dx(dyc, nullptr, xiau, rxz, z, x, d, dxc, dzc));
     // ---- combine, stepsizes, update ----
     NYS_TRY(launch_ratio(ctx, n, x, dx, dxp, dxc, z, dz, dzp, dzc, 8));
     NYS_TRY(allreduce_slots(ctx, S_TMP0, 2, true));
@@ -1066,7 +1120,11 @@ int nys_ipppmm_solve(nys_ctx* ctx, const nys_qp* qp, const nys_options* opt, nys
     ctx->set_error("nys_ipppmm_solve: bad problem");
     return NYS_EINVAL;
   }
-  if (!qp->host_ptrs) NYS_TRY(check_A(ctx, qp->m, qp->n, qp->A, qp->lda));
+  if (qp->structure != 0 && (qp->structure != 1 || qp->nd < 0 || qp->n != 2 * qp->nd + 2 * qp->m)) {
+    ctx->set_error("nys_ipppmm_solve: structure 1 needs n = 2 nd + 2 m");
+    return NYS_EINVAL;
+  }
+  if (!qp->host_ptrs) NYS_TRY(check_A(ctx, qp->m, qp->structure == 1 ? qp->nd : qp->n, qp->A, qp->lda));
   if (opt->ell < 0 || opt->ell > qp->m || opt->ell > 256 || !(opt->tol > 0)) {
     ctx->set_error("nys_ipppmm_solve: bad options");
     return NYS_EINVAL;

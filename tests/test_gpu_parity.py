@@ -312,3 +312,31 @@ def test_kernel_launch_accounting(ctx):
     inst = make_config(0)
     _solve_gpu(ctx, inst, inst.ell)
     assert ctx.kernel_launches > before
+
+
+# ------------------------------------------------------------------------ config 2 (SVM-structured A)
+@pytest.mark.parametrize("N,d,ell", [(300, 20, 10), (1000, 50, 30)])
+def test_ipppmm_svm_structured_parity(ctx, N, d, ell):
+    from paper_2404_14524_b200 import colmajor_device
+    from synth.configs import svm_dense_A
+    inst = make_config(2, m=N, n=d, ell=ell)
+    A = svm_dense_A(inst)
+    ref = ippmm.solve(A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=ell))
+    Xd, lda = colmajor_device(inst.extra["Xt"])
+    g = ctx.nys_ipppmm_solve(Xd, lda, N, dev(inst.q), dev(inst.b), dev(inst.c), ell=ell, structure=1)
+    assert ref.status == "optimal" and g["status"] == 0
+    assert g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    assert obj_agree(g, ref)
+    x, y, z = g["x"].cpu().numpy(), g["y"].cpu().numpy(), g["z"].cpu().numpy()
+    assert np.linalg.norm(inst.b - A @ x) / (1 + np.linalg.norm(inst.b)) <= 1e-8
+    assert np.linalg.norm(inst.c + inst.q * x - A.T @ y - z) / (1 + np.linalg.norm(inst.c)) <= 1e-8
+
+
+def test_ipppmm_config3_full(ctx):
+    """BASELINE configs[3] at full size (m=64, n=200000, l=64 = m: the Nystrom P^{-1} is exact)."""
+    inst = make_config(3)
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
+    g = _solve_gpu(ctx, inst, inst.ell)
+    assert ref.status == "optimal" and g["status"] == 0
+    assert obj_agree(g, ref)
+    assert abs(g["outer"] - ref.outer) <= 2

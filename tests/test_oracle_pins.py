@@ -429,3 +429,34 @@ def test_gaussian_omega_moments_and_layout():
     # column-major linear index: a taller matrix has the first column's prefix as prefix
     Om2 = rng.gaussian_omega(2000, 41, seed=5, stream=3)
     np.testing.assert_array_equal(Om2[:, :40], Om)
+
+
+def test_svm_instance_structure():
+    # BASELINE configs[2] / SURVEY A23: A = [Xt, -Xt, I, -I], Xt = diag(y) X, b = 1, Q = diag(1 on w, 0 on xi, s)
+    from synth.configs import svm_dense_A
+    inst = make_config(2, m=40, n=6, ell=5)
+    A = svm_dense_A(inst)
+    N, d = 40, 6
+    assert A.shape == (N, 2 * d + 2 * N) and inst.n == 2 * d + 2 * N
+    Xt = inst.extra["Xt"]
+    np.testing.assert_array_equal(A[:, :d], Xt)
+    np.testing.assert_array_equal(A[:, d:2 * d], -Xt)
+    np.testing.assert_array_equal(A[:, 2 * d:2 * d + N], np.eye(N))
+    np.testing.assert_array_equal(A[:, 2 * d + N:], -np.eye(N))
+    yl = inst.extra["labels"]
+    # rows of diag(y) X are y_i (0.5 y_i 1 + g_i): mean of y_i * row over features is ~0.5
+    assert abs(np.mean(Xt) - 0.5) < 0.2
+    assert set(np.unique(yl)) <= {-1.0, 1.0}
+    np.testing.assert_array_equal(inst.b, np.ones(N))
+    np.testing.assert_array_equal(inst.q, np.r_[np.ones(2 * d), np.zeros(2 * N)])
+
+
+def test_svm_tiny_qp_against_active_set():
+    # the structured SVM QP solved by the oracle equals brute force on a tiny instance
+    from synth.configs import svm_dense_A
+    inst = make_config(2, m=4, n=2, ell=2)
+    A = svm_dense_A(inst)
+    ref = enumerate_active_sets(A, inst.q, inst.b, inst.c)
+    r = ippmm.solve(A, inst.q, inst.b, inst.c, ippmm.Options(path="direct"))
+    assert r.status == "optimal"
+    assert abs(r.obj - ref["obj"]) <= 1e-6 * max(1.0, abs(ref["obj"]))
