@@ -67,32 +67,33 @@ __device__ __forceinline__ void t_epilogue(const MatvecParams& P, int64_t j, dou
   }
 }
 
-template <int T, int GT, int RPT, int CPG, int MODE, bool VS>
+template <int T, int GT, int RPT, int CPG, int MODE, bool VS, bool CLU>
 __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P) {
   constexpr int NG = T / GT;
   constexpr int WPG = GT / 32;
   constexpr int BN = NG * CPG;
+  constexpr int DB = 4;  // depth of the cluster dot-exchange ring (>= 4: see the lag-1 argument below)
   extern __shared__ __align__(128) unsigned char smem_raw[];
 
   if (P.done != nullptr && *P.done != 0.0) return;  // grid-uniform early exit (PCG converged)
 
   const int S = P.stages;
   const int64_t rs = P.rs;
-  const int cl = P.cl;
+  const int cl = CLU ? P.cl : 1;
   double* stage = reinterpret_cast<double*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(stage + (size_t)S * BN * rs);
   uint64_t* empty = full + S;
-  uint64_t* dotbar = empty + S;
-  double* red = reinterpret_cast<double*>(dotbar + S);
-  double* slots = red + 2 * NG * WPG * CPG;
-  double* vsm = slots + (size_t)S * cl * CPG;  // VS: the operand slice v (rs doubles)
+  uint64_t* dotbar = empty + S;                       // DB barriers (CLU)
+  double* red = reinterpret_cast<double*>(dotbar + DB);
+  double* slots = red + 2 * NG * WPG * CPG;           // [DB][cl][CPG] (CLU)
+  double* vsm = slots + (size_t)DB * cl * CPG;        // VS: the operand slice v (rs doubles)
 
   const int tid = threadIdx.x;
   const int warp = warp_uniform_id(), lane = tid & 31;
   const int rc = P.rc;
-  const uint32_t crank = cl > 1 ? cluster_ctarank() : 0u;
-  const uint32_t cid = cl > 1 ? cluster_id_x() : blockIdx.x;
-  const uint32_t ncl = cl > 1 ? ncluster_x() : gridDim.x;
+  const uint32_t crank = CLU ? cluster_ctarank() : 0u;
+  const uint32_t cid = CLU ? cluster_id_x() : blockIdx.x;
+  const uint32_t ncl = CLU ? ncluster_x() : gridDim.x;
   const int64_t r0 = (int64_t)crank * rs;
   int64_t rows_valid = P.m - r0;
   rows_valid = rows_valid < 0 ? 0 : (rows_valid > rs ? rs : rows_valid);
@@ -103,11 +104,12 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], T / 32);
-      mbar_init(&dotbar[s], (uint32_t)(cl * CPG));
     }
+    if (CLU)
+      for (int s = 0; s < DB; ++s) mbar_init(&dotbar[s], 1);  // own arrive.expect_tx; peers complete_tx
     fence_mbar_init();
   }
-  if (cl > 1) cluster_sync_all(); else __syncthreads();
+  if (CLU) cluster_sync_all(); else __syncthreads();
 
   const int g = tid / GT;
   const int lig = tid % GT;
@@ -121,19 +123,26 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
     // ------------------------------ producer warp ------------------------------------------
     if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
-      for (int64_t it = 0; it < niter; ++it) {
-        const int s = (int)(it % S);
-        if (it >= S) mbar_wait(&empty[s], (uint32_t)(((it / S) - 1) & 1));
+      // contiguous panels (no cluster split, column stride == smem stride): one copy per stage
+      const bool contig = !CLU && P.lda == rs;
+      int s = 0;
+      uint32_t eph = 1u;  // parity of the empty-barrier phase to wait for (first pass: none)
+      for (int64_t it = 0; it < niter; ++it, ++s) {
+        if (s == S) { s = 0; eph ^= 1u; }
+        if (it >= S) mbar_wait(&empty[s], eph);
         const int64_t col0 = (int64_t)(cid + it * ncl) * BN;
         int64_t ncols = P.n - col0;
         ncols = ncols > BN ? BN : ncols;
-        const uint32_t bytes = (uint32_t)ncols * copy_bytes;
-        if (bytes > 0) {
+        if (ncols <= 0) {
+          mbar_arrive(&full[s]);
+        } else if (contig) {
+          const uint32_t bytes = (uint32_t)((ncols - 1) * rs * 8) + copy_bytes;  // lda even: 16-B multiple
           mbar_arrive_expect_tx(&full[s], bytes);
+          bulk_g2s(stage + (size_t)s * BN * rs, P.A + col0 * P.lda, bytes, &full[s], pol);
+        } else {
+          mbar_arrive_expect_tx(&full[s], (uint32_t)ncols * copy_bytes);
           for (int c = 0; c < ncols; ++c)
             bulk_g2s(stage + ((size_t)s * BN + c) * rs, P.A + (col0 + c) * P.lda + r0, copy_bytes, &full[s], pol);
-        } else {
-          mbar_arrive(&full[s]);
         }
       }
     }
@@ -157,9 +166,130 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
       }
     }
     if (VS) named_bar_sync(1, T);  // vsm complete (NG == 1 for VS)
+
+    if (CLU && MODE != MV_NONLY) {
+      // ---- cluster path (rows split over cl CTAs; NG == 1; v in registers).  Lag-1 software
+      // pipeline: the CTA partial dots of panel `it` are pushed to every peer with st.async
+      // (completing bytes on the peer's dotbar), and the rank-CPG update of panel it-1 runs
+      // while they travel, so no CTA waits a DSMEM round trip on the critical path.  The dot and
+      // the update both read the panel from its shared-memory stage (no panel registers: the
+      // 512-thread CTA has ~120 registers per thread); a stage is released after its update.
+      // Per-panel critical path kept short: 4 independent FMA chains, xor-tree reductions
+      // (warp, then CTA by warp 0), one peer per lane for the publish.
+      // Ring safety: a peer publishes panel j+DB only after consuming j+DB-2, which needs our
+      // publish of j+DB-2, issued after our consume of j+DB-3 >= j for DB >= 3 (DB = 4 here).
+      static_assert(WPG <= 32, "one lane per warp partial");
+      double dprev[CPG];
+      int64_t cprev = 0;
+#pragma unroll
+      for (int c = 0; c < CPG; ++c) dprev[c] = 0.0;
+      int s = 0, sp = 0;
+      uint32_t ph = 0;
+      for (int64_t it = 0; it <= niter; ++it) {
+        double dcur[CPG];
+        const int64_t col0 = (int64_t)(cid + it * ncl) * BN;
+        if (it < niter) {
+          mbar_wait(&full[s], ph);
+          const double* sb = stage + (size_t)s * BN * rs;
+#pragma unroll
+          for (int c = 0; c < CPG; ++c) dcur[c] = (MODE == MV_FUSED && col0 + c < P.n) ? __ldg(P.d + col0 + c) : 0.0;
+          double pd[CPG];
+#pragma unroll
+          for (int c = 0; c < CPG; ++c) {
+            const bool cv = (col0 + c) < P.n;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+              const int rl = lig + GT * i;
+              const double a = (cv && rl < (int)rows_valid) ? sb[c * (int)rs + rl] : 0.0;
+              acc[i & 3] = fma(a, vreg[VS ? 0 : i], acc[i & 3]);
+            }
+            pd[c] = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+          }
+          const int db = (int)(it & (DB - 1));
+          double* rb = red + (size_t)(it & 1) * WPG * CPG;
+          if (lane == 0) {
+#pragma unroll
+            for (int c = 0; c < CPG; ++c) rb[c * WPG + warp] = pd[c];
+          }
+          if (tid == 0) mbar_arrive_expect_tx(&dotbar[db], (uint32_t)(cl * CPG * 8));
+          named_bar_sync(1, T);
+          if (warp == 0) {
+            const uint32_t my_bar = smem_u32(&dotbar[db]);
+#pragma unroll
+            for (int c = 0; c < CPG; ++c) {
+              double x = (lane < WPG) ? rb[c * WPG + lane] : 0.0;
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+              if (lane < cl) {
+                const uint32_t my_slot = smem_u32(&slots[((size_t)db * cl + crank) * CPG + c]);
+                st_async_f64(mapa_shared(my_slot, (uint32_t)lane), x, mapa_shared(my_bar, (uint32_t)lane));
+              }
+            }
+          }
+        }
+        if (it >= 1) {
+          const int64_t j = it - 1;
+          const int db = (int)(j & (DB - 1));
+          mbar_wait(&dotbar[db], (uint32_t)((j / DB) & 1));
+          double pd[CPG];
+#pragma unroll
+          for (int c = 0; c < CPG; ++c) {
+            // pairwise tree in rank order (identical on every CTA of the cluster)
+            const double* sl = &slots[(size_t)db * cl * CPG + c];
+            double part[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) part[r] = (r < cl) ? sl[r * CPG] : 0.0;
+#pragma unroll
+            for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+              for (int r = 0; r < w; ++r) part[r] += part[r + w];
+            pd[c] = part[0];
+          }
+          if (MODE == MV_FUSED) {
+            double t[CPG];
+#pragma unroll
+            for (int c = 0; c < CPG; ++c) t[c] = dprev[c] * pd[c];
+            if (lig == 0 && crank == 0) {
+#pragma unroll
+              for (int c = 0; c < CPG; ++c) pwacc = fma(t[c], pd[c], pwacc);  // d_j (a_j^T v)^2
+            }
+            const double* sb = stage + (size_t)sp * BN * rs;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+              const int rl = lig + GT * i;
+              double acc = wacc[i];
+#pragma unroll
+              for (int c = 0; c < CPG; ++c) {
+                const double a = (cprev + c < P.n && rl < (int)rows_valid) ? sb[c * (int)rs + rl] : 0.0;
+                acc = fma(a, t[c], acc);
+              }
+              wacc[i] = acc;
+            }
+          } else {  // MV_TONLY: raw dot to global; epilogue after the loop
+            if (crank == 0) {
+#pragma unroll
+              for (int c = 0; c < CPG; ++c)
+                if (lig == c && cprev + c < P.n) P.tbuf[cprev + c] = pd[c];
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[sp]);
+        }
+        if (it < niter) {
+#pragma unroll
+          for (int c = 0; c < CPG; ++c) dprev[c] = dcur[c];
+          cprev = col0;
+          sp = s;
+          if (++s == S) { s = 0; ph ^= 1u; }
+        }
+      }
+    } else {
+    int s = -1;
+    uint32_t par = 1u;
     for (int64_t it = 0; it < niter; ++it) {
-      const int s = (int)(it % S);
-      const uint32_t par = (uint32_t)((it / S) & 1);
+      if (++s == S) s = 0;
+      if (s == 0) par ^= 1u;
       const int64_t col0 = (int64_t)(cid + it * ncl) * BN + (int64_t)g * CPG;
       mbar_wait(&full[s], par);
       double a[CPG][RPT];
@@ -208,26 +338,6 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
             pd[c] = tot;
           }
         }
-        if (cl > 1) {  // NG == 1 here: exchange CTA partials through DSMEM
-#pragma unroll
-          for (int c = 0; c < CPG; ++c) {
-            if (tid == c) {
-              const uint32_t my_slot = smem_u32(&slots[((size_t)s * cl + crank) * CPG + c]);
-              const uint32_t my_bar = smem_u32(&dotbar[s]);
-              for (int peer = 0; peer < cl; ++peer) {
-                st_cluster_f64(mapa_shared(my_slot, (uint32_t)peer), pd[c]);
-                mbar_arrive_remote(mapa_shared(my_bar, (uint32_t)peer));
-              }
-            }
-          }
-          mbar_wait_cluster(&dotbar[s], par);
-#pragma unroll
-          for (int c = 0; c < CPG; ++c) {
-            double tot = 0.0;
-            for (int r = 0; r < cl; ++r) tot += slots[((size_t)s * cl + r) * CPG + c];
-            pd[c] = tot;
-          }
-        }
         if (MODE == MV_FUSED) {
 #pragma unroll
           for (int c = 0; c < CPG; ++c) t[c] = dpre[c] * pd[c];
@@ -256,8 +366,8 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
         }
       }
     }
+    }
   }
-
   if (MODE == MV_TONLY) {
     __syncthreads();  // this CTA's raw dots are visible to all its threads
     if (crank == 0) {
@@ -459,7 +569,12 @@ struct MvCfg {
   int T, GT, RPT, CPG;
 };
 
-static MvCfg pick_cfg(int64_t rs) {
+static MvCfg pick_cfg(int64_t rs, bool clu) {
+  if (clu) {  // cluster path: rows split over the cluster, one group of 512 threads
+    if (rs <= 4096) return {512, 512, 8, 2};
+    if (rs <= 6656) return {512, 512, 13, 1};
+    return {512, 512, 16, 1};
+  }
   if (rs <= 64) return {256, 32, 2, 4};
   if (rs <= 128) return {256, 32, 4, 2};
   if (rs <= 256) return {256, 64, 4, 2};
@@ -472,17 +587,22 @@ static MvCfg pick_cfg(int64_t rs) {
 typedef void (*MvKernel)(const MatvecParams);
 
 template <int MODE>
-static MvKernel kernel_for(const MvCfg& c) {
-  if (c.T == 256 && c.GT == 32 && c.RPT == 2 && c.CPG == 4) return matvec_kernel<256, 32, 2, 4, MODE, false>;
-  if (c.T == 256 && c.GT == 32 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<256, 32, 4, 2, MODE, false>;
-  if (c.T == 256 && c.GT == 64 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<256, 64, 4, 2, MODE, false>;
-  if (c.T == 256 && c.GT == 128 && c.RPT == 8 && c.CPG == 2) return matvec_kernel<256, 128, 8, 2, MODE, false>;
-  if (c.T == 256 && c.GT == 256 && c.RPT == 8 && c.CPG == 4) return matvec_kernel<256, 256, 8, 4, MODE, false>;
-  if (c.T == 256 && c.GT == 256 && c.RPT == 8 && c.CPG == 2) return matvec_kernel<256, 256, 8, 2, MODE, false>;
-  if (c.T == 512 && c.GT == 512 && c.RPT == 4 && c.CPG == 4) return matvec_kernel<512, 512, 4, 4, MODE, false>;
-  if (c.T == 512 && c.GT == 512 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<512, 512, 4, 2, MODE, false>;
-  if (c.T == 512 && c.GT == 512 && c.RPT == 8 && c.CPG == 2) return matvec_kernel<512, 512, 8, 2, MODE, false>;
-  return matvec_kernel<512, 512, 16, 1, MODE, true>;
+static MvKernel kernel_for(const MvCfg& c, bool clu) {
+  if (clu) {
+    if (c.RPT == 8 && c.CPG == 2) return matvec_kernel<512, 512, 8, 2, MODE, false, true>;
+    if (c.RPT == 13) return matvec_kernel<512, 512, 13, 1, MODE, false, true>;
+    return matvec_kernel<512, 512, 16, 1, MODE, false, true>;
+  }
+  if (c.T == 256 && c.GT == 32 && c.RPT == 2 && c.CPG == 4) return matvec_kernel<256, 32, 2, 4, MODE, false, false>;
+  if (c.T == 256 && c.GT == 32 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<256, 32, 4, 2, MODE, false, false>;
+  if (c.T == 256 && c.GT == 64 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<256, 64, 4, 2, MODE, false, false>;
+  if (c.T == 256 && c.GT == 128 && c.RPT == 8 && c.CPG == 2) return matvec_kernel<256, 128, 8, 2, MODE, false, false>;
+  if (c.T == 256 && c.GT == 256 && c.RPT == 8 && c.CPG == 4) return matvec_kernel<256, 256, 8, 4, MODE, false, false>;
+  if (c.T == 256 && c.GT == 256 && c.RPT == 8 && c.CPG == 2) return matvec_kernel<256, 256, 8, 2, MODE, false, false>;
+  if (c.T == 512 && c.GT == 512 && c.RPT == 4 && c.CPG == 4) return matvec_kernel<512, 512, 4, 4, MODE, false, false>;
+  if (c.T == 512 && c.GT == 512 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<512, 512, 4, 2, MODE, false, false>;
+  if (c.T == 512 && c.GT == 512 && c.RPT == 8 && c.CPG == 2) return matvec_kernel<512, 512, 8, 2, MODE, false, false>;
+  return matvec_kernel<512, 512, 16, 1, MODE, true, false>;
 }
 
 struct MvPlan {
@@ -498,43 +618,57 @@ struct MvPlan {
   int cdim = 1;       // launch cluster dimension (cl or rc)
 };
 
-static bool cfg_vs(const MvCfg& c) { return c.RPT >= 16; }
+static bool cfg_vs(const MvCfg& c, bool clu) { return !clu && c.RPT >= 16; }
 
-static size_t mv_smem_bytes(const MvCfg& c, int64_t rs, int stages, int cl) {
+static size_t mv_smem_bytes(const MvCfg& c, int64_t rs, int stages, int cl, bool clu) {
   const int NG = c.T / c.GT, WPG = c.GT / 32, BN = NG * c.CPG;
+  constexpr int DB = 4;
   size_t b = (size_t)stages * BN * rs * 8;
-  b += (size_t)3 * stages * 8;
+  b += (size_t)2 * stages * 8 + (size_t)DB * 8;
   b += (size_t)2 * NG * WPG * c.CPG * 8;
-  b += (size_t)stages * cl * c.CPG * 8;
-  if (cfg_vs(c)) b += (size_t)rs * 8;
+  b += (size_t)DB * cl * c.CPG * 8;
+  if (cfg_vs(c, clu)) b += (size_t)rs * 8;
   return b;
 }
 
-static std::map<std::tuple<int, int, int, int, int, int64_t, int64_t>, MvPlan> g_plans;
+static std::map<std::tuple<int, int, int64_t, int64_t, int64_t>, MvPlan> g_plans;
 
-static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, MvPlan& pl) {
-  auto key = std::make_tuple(ctx->device, mode, 0, 0, 0, m, n);
+static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, MvPlan& pl) {
+  auto key = std::make_tuple(ctx->device, mode, m, n, lda);
   auto itp = g_plans.find(key);
   if (itp != g_plans.end()) { pl = itp->second; return NYS_OK; }
+  // m <= 8192: whole columns per CTA.  Larger m: split the rows over a cluster of cl CTAs,
+  // <= 6656 rows each (13 rows per thread: the register budget of the pipelined cluster path)
   int cl = 1;
-  while ((m + cl - 1) / cl > 8192 && cl < 16) cl *= 2;
+  if (m > 8192) {
+    cl = 2;
+    while ((m + cl - 1) / cl > 6656 && cl < 16) cl *= 2;
+  }
+  if (const char* oc = getenv("NYS_MV_CL")) {  // tuning override of the cluster split (m > 4096)
+    const int o = atoi(oc);
+    if ((o == 2 || o == 4 || o == 8 || o == 16) && m > 4096) cl = o;
+  }
   int64_t rs = (m + cl - 1) / cl;
   rs = (rs + 1) & ~int64_t(1);
-  MvCfg c = pick_cfg(rs);
+  // whole-column CTAs with a near-tight lda: stride the stage by lda so a panel (BN consecutive
+  // columns) is ONE contiguous bulk copy (the padding rows are masked off in the kernel)
+  if (cl == 1 && lda >= rs && lda <= rs + 32) rs = lda;
+  const bool clu = cl > 1;
+  MvCfg c = pick_cfg(rs, clu);
   if (const char* ov = getenv("NYS_MV_CFG")) {  // debug/tuning override "T,GT,RPT,CPG" (must be instantiated)
     MvCfg o;
     if (sscanf(ov, "%d,%d,%d,%d", &o.T, &o.GT, &o.RPT, &o.CPG) == 4 && (int64_t)o.GT * o.RPT >= rs) c = o;
   }
   const int NG = c.T / c.GT, BN = NG * c.CPG;
   const size_t stage_bytes = (size_t)BN * rs * 8;
-  size_t budget = (rs <= 1024) ? 96 * 1024 : 200 * 1024;
+  size_t budget = clu ? 212 * 1024 : (rs <= 1024) ? 96 * 1024 : 200 * 1024;
   if (const char* sb = getenv("NYS_MV_SMEM_KB")) budget = (size_t)atoi(sb) * 1024;
-  if (cfg_vs(c)) budget -= (size_t)rs * 8;
+  if (cfg_vs(c, clu)) budget -= (size_t)rs * 8;
   int stages = (int)(budget / stage_bytes);
   stages = stages > 8 ? 8 : stages;
   if (stages < 2) stages = 2;
-  size_t smem = mv_smem_bytes(c, rs, stages, cl);
-  MvKernel k = (mode == MV_FUSED) ? kernel_for<MV_FUSED>(c) : (mode == MV_TONLY) ? kernel_for<MV_TONLY>(c) : kernel_for<MV_NONLY>(c);
+  size_t smem = mv_smem_bytes(c, rs, stages, cl, clu);
+  MvKernel k = (mode == MV_FUSED) ? kernel_for<MV_FUSED>(c, clu) : (mode == MV_TONLY) ? kernel_for<MV_TONLY>(c, clu) : kernel_for<MV_NONLY>(c, clu);
   NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (cl > 8) NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const int64_t npanels = (n + BN - 1) / BN;
@@ -613,7 +747,7 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, MvPlan& pl) {
 int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
   if (c.m <= 0) return NYS_OK;
   MvPlan pl;
-  NYS_TRY(make_plan(ctx, c.mode, c.m, c.n, pl));
+  NYS_TRY(make_plan(ctx, c.mode, c.m, c.n, c.lda, pl));
   const int64_t wp_ld = (c.m + 1) & ~int64_t(1);
   double* Wp = nullptr;
   if (c.mode != MV_TONLY) Wp = ctx->wsd("mv_partials", (size_t)pl.nparts * wp_ld);
@@ -629,7 +763,7 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
     P.done = c.done; P.rs = pl.rs; P.npanels = pl.npanels; P.stages = pl.stages; P.cl = pl.cl;
     P.pwp = pwp; P.delta = c.delta; P.e = c.e; P.tbuf = tbuf; P.rc = pl.rc;
     P.delta_slot = c.delta_from_slot ? ctx->sc + S_DELTA : nullptr;
-    MvKernel k = (c.mode == MV_FUSED) ? kernel_for<MV_FUSED>(pl.cfg) : (c.mode == MV_TONLY) ? kernel_for<MV_TONLY>(pl.cfg) : kernel_for<MV_NONLY>(pl.cfg);
+    MvKernel k = (c.mode == MV_FUSED) ? kernel_for<MV_FUSED>(pl.cfg, pl.cl > 1) : (c.mode == MV_TONLY) ? kernel_for<MV_TONLY>(pl.cfg, pl.cl > 1) : kernel_for<MV_NONLY>(pl.cfg, pl.cl > 1);
     if (c.n > 0) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)pl.grid);

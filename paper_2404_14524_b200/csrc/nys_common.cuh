@@ -159,6 +159,14 @@ __device__ __forceinline__ double ld_cluster_f64(uint32_t addr) {
   asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
   return v;
 }
+// async remote store into a peer CTA's shared memory; completes `bytes` of transaction on the
+// peer's mbarrier (the receiver waits with a plain cta-scope try_wait: no cluster-scope acquire,
+// hence no L1 invalidation per wait)
+__device__ __forceinline__ void st_async_f64(uint32_t cluster_addr, double v, uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(cluster_addr),
+               "d"(v), "r"(cluster_bar)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }

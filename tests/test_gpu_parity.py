@@ -48,7 +48,8 @@ def rel(a, b):
 
 # ------------------------------------------------------------------------ normal matvec (K1)
 MV_SHAPES = [(1, 5), (2, 0), (2, 3), (37, 401), (64, 3001), (100, 400), (130, 257), (300, 999), (1000, 1201),
-             (2000, 801), (2001, 333), (4096, 300), (5000, 129), (8193, 70), (20000, 40), (50000, 17)]
+             (2000, 801), (2001, 333), (4096, 300), (5000, 129), (8192, 77), (8193, 70), (13313, 150),
+             (16384, 151), (20000, 40), (33001, 99), (50000, 17), (50000, 301), (70000, 33)]
 
 
 @pytest.mark.parametrize("m,n", MV_SHAPES)
