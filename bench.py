@@ -1,16 +1,20 @@
 #!/usr/bin/env python
-"""Benchmark: Nys-IP-PMM time-to-1e-8 on BASELINE.json configs[1] (m=2000, n=8000, l=50) on B200,
-with the fused fp64 normal matvec (the dominant kernel) reported against the HBM roofline.
+"""Benchmark: Nys-IP-PMM time-to-1e-8 on B200, with the fused fp64 normal matvec (the dominant
+kernel) reported against the HBM roofline.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
-A "step" is one complete Nys-IP-PMM solve to tol 1e-8 (every SURVEY §8(a) row: D-update,
-sketch + Nystrom factorisation, PCG with the fused matvec and preconditioner, Newton RHS /
-recovery, predictor-corrector, residuals/TC/PEU, initial point) with the problem resident in
-HBM.  `value` = seconds per solve (time-to-1e-8, lower is better); `e2e` = the same solve through
-the C ABI with HOST buffers (H2D of A, q, b, c and D2H of x, y, z inside the timed region).
-Multi-GPU (torchrun, N > 1): A's columns are sharded over ranks (strong scaling of the same
-problem); timing is on the device, max over ranks.
+Default workload: BASELINE.json configs[1] (m=2000, n=8000, l=50), the largest config whose full
+solve fits a few-minute bench on one GPU.  --config 0|1|2|3 selects another BASELINE config;
+--config 4 runs configs[4] (m=50000, l=200) with --n-per-gpu columns per rank (default 50000:
+at N=1 the one-GPU slice of SURVEY A25, at N=8 the full n=400000 problem) -> "scaling": "weak".
+
+A "step" is one complete Nys-IP-PMM solve to tol 1e-8 (every SURVEY §8(a) row: D-update, sketch
++ Nystrom factorisation, PCG with the fused matvec and preconditioner, Newton RHS / recovery,
+predictor-corrector, residuals/TC/PEU, initial point) with the problem resident in HBM.
+`value` = seconds per solve (lower is better); `e2e` = the same solve through the C ABI with HOST
+buffers (H2D of A, q, b, c and D2H of x, y, z inside the timed region).  Multi-GPU (torchrun):
+A's columns are sharded over ranks; timing is on the device, max over ranks.
 """
 from __future__ import annotations
 
@@ -27,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fp64 A·D·Aᵀv matvec GB/s (% HBM peak) and Nys-IP-PMM time-to-1e-8 at 1/2/4/8 GPU"
 # dram__bytes_read.sum + dram__bytes_write.sum per fused-matvec launch from `ncu --set full`
-# (profiles/, per config); None until captured for that config
+# (profiles/, per config and shape); None until captured for that config
 TRAFFIC = {1: 134.6e6}
 
 
@@ -83,44 +87,152 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def load_instance(cfg: int, rank: int, world: int):
-    from synth import make_config
-    inst = make_config(cfg)
-    n = inst.n
-    lo, hi = (n * rank) // world, (n * (rank + 1)) // world
-    return inst, lo, hi
+# ------------------------------------------------------------------------------------------------
+# workloads
+# ------------------------------------------------------------------------------------------------
+class Workload:
+    """This rank's share of one BASELINE config, resident on the device, plus what the e2e leg
+    and the CPU baseline need.  Input generation only (synth/); no method arithmetic here."""
+
+    def __init__(self, cfg: int, rank: int, world: int, device, n_per_gpu: int, dist=None):
+        import numpy as np
+        import torch
+        self.cfg = cfg
+        self.structure = 0
+        self.inst = None
+        dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+        if cfg == 4:
+            from synth import large
+            n = n_per_gpu * world
+            lo, hi = large.shard_bounds(n, rank, world)
+            sh = large.generate_shard(large.FULL_M, n, lo, hi, n_gen=large.FULL_N, device=device)
+            b = sh.b_part
+            if world > 1:
+                dist.all_reduce(b)
+            self.m, self.n, self.lo, self.hi, self.ell = large.FULL_M, n, lo, hi, large.ELL
+            self.At, self.lda, self.q, self.b, self.c = sh.At, sh.lda, sh.q, b, sh.c
+            self.name = (f"cfg4_large_m50000_l200_{n_per_gpu}cols_per_gpu"
+                         + ("_slice_A25" if world == 1 and n < large.FULL_N else "")
+                         + ("_full_n400000" if n == large.FULL_N else ""))
+            self.scaling = "weak"
+            return
+        from paper_2404_14524_b200 import colmajor_device
+        from synth import make_config
+        inst = make_config(cfg)
+        self.inst = inst
+        self.m, self.ell, self.name = inst.m, inst.ell, inst.name
+        self.scaling = "strong"
+        if cfg == 2:
+            # SVM-structured A = [Xt, -Xt, I, -I] (SURVEY A23): the dense block Xt is the operand
+            if world > 1:
+                raise SystemExit("config 2 (structured SVM operator) is single-GPU in this build")
+            Xt = inst.extra["Xt"]
+            self.structure = 1
+            self.n, self.lo, self.hi = inst.n, 0, inst.n
+            self.At, self.lda = colmajor_device(Xt, device=device)
+            self.q, self.b, self.c = dv(inst.q), dv(inst.b), dv(inst.c)
+            self.A_dense_block = Xt
+            return
+        n = inst.n
+        self.n = n
+        self.lo, self.hi = (n * rank) // world, (n * (rank + 1)) // world
+        self.At, self.lda = colmajor_device(np.asfortranarray(inst.A[:, self.lo:self.hi]), device=device)
+        self.q, self.b, self.c = dv(inst.q[self.lo:self.hi]), dv(inst.b), dv(inst.c[self.lo:self.hi])
+
+    @property
+    def ncols(self):
+        return self.At.shape[0]
+
+    def a_bytes(self):
+        return 8.0 * self.m * self.ncols
 
 
 def run_reference(args):
     """--impl reference: the CPU oracle (numpy/scipy fp64) as it stands, on this host's cores."""
     import numpy as np
-    from oracle import ippmm
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    inst, _, _ = load_instance(args.config, 0, 1)
-    K = min(args.steps, 2)
-    W = min(args.warmup, 1)
-    times = []
-    res = None
-    for i in range(W + K):
-        t0 = time.perf_counter()
-        res = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
-        dt = time.perf_counter() - t0
-        if i >= W:
-            times.append(dt)
-    v = float(np.mean(times))
     cores = os.cpu_count()
-    sample = (f"full oracle Nys-IP-PMM solve of {inst.name} per step ({res.outer} outer / {res.inner_total} PCG "
-              f"iterations); {K} timed + {W} warm-up of the requested {args.steps}+{args.warmup}")
+    if args.config in (0, 1, 3):
+        from oracle import ippmm
+        from synth import make_config
+        inst = make_config(args.config)
+        K = min(args.steps, 2)
+        W = min(args.warmup, 1)
+        times = []
+        res = None
+        for i in range(W + K):
+            t0 = time.perf_counter()
+            res = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
+            dt = time.perf_counter() - t0
+            if i >= W:
+                times.append(dt)
+        v = float(np.mean(times))
+        sample = (f"full oracle Nys-IP-PMM solve of {inst.name} per step ({res.outer} outer / {res.inner_total} PCG "
+                  f"iterations); {K} timed + {W} warm-up of the requested {args.steps}+{args.warmup}")
+        config = {"workload": inst.name, "m": inst.m, "n": inst.n, "ell": inst.ell, "tol": 1e-8}
+    else:
+        # the oracle cannot finish these solves in minutes: bounded sample projected to one solve
+        proj = cpu_projection(args.config, args.n_per_gpu * max(1, args.gpus), outer=40, matvecs=4000)
+        v = proj["value"]
+        sample = proj["sample"]
+        config = {"workload": proj["workload"], "tol": 1e-8}
+        K, W = 1, 0
     line = {"metric": METRIC, "value": v, "unit": "s", "impl": "reference", "n_gpus": args.gpus, "steps": K,
-            "warmup": W, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": inst.name, "m": inst.m, "n": inst.n, "ell": inst.ell, "tol": 1e-8},
+            "warmup": W, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "weak" if args.config == 4 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
             "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_projection(cfg: int, n: int, outer: int, matvecs: int):
+    """Oracle time for one solve projected from a bounded sample (~10-30 s of CPU work): the oracle's
+    normal matvec and its sketch + Nystrom factorisation timed on a column sample of the same
+    workload, scaled by n / sample columns and by the GPU solve's matvec / outer-iteration counts."""
+    import numpy as np
+    from oracle import linops, nystrom
+    from oracle.rng import gaussian_omega
+    if cfg == 4:
+        import torch
+        from synth import large
+        cols = 1000
+        sh = large.generate_shard(large.FULL_M, n, 0, cols, n_gen=large.FULL_N, device="cpu")
+        A = np.asfortranarray(sh.At[:, :large.FULL_M].numpy().T)
+        e = None
+        m, ell, scale = large.FULL_M, large.ELL, n / cols
+        workload = f"cfg4 m=50000 n={n} l=200"
+        del sh, torch
+    else:
+        from synth import make_config
+        inst = make_config(cfg)
+        A = inst.extra["Xt"] if cfg == 2 else inst.A
+        m, ell, scale = inst.m, inst.ell, 1.0
+        e = np.ones(m) if cfg == 2 else None
+        workload = inst.name
+    rs = np.random.default_rng(0)
+    d = rs.uniform(0.1, 2.0, A.shape[1])
+    v = rs.standard_normal(m)
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        linops.normal_matvec(A, d, v, 1e-3, e)
+    t_mv = (time.perf_counter() - t0) / reps * scale
+    Om = gaussian_omega(m, ell, 0, 1)
+    t0 = time.perf_counter()
+    Y = linops.sketch(A, d, Om, e)
+    t_sk = (time.perf_counter() - t0) * scale
+    t0 = time.perf_counter()
+    nystrom.nystrom_from_sketch(Y * scale, Om)
+    t_fac = time.perf_counter() - t0
+    value = matvecs * t_mv + outer * (t_sk + t_fac)
+    sample = (f"oracle normal matvec (x{reps}) and sketch+Nystrom on {A.shape[1]} of {int(A.shape[1] * scale)} "
+              f"columns of {workload}: {t_mv:.3g} s/matvec, {t_sk + t_fac:.3g} s/sketch at full size; projected to "
+              f"{matvecs} matvecs + {outer} sketches (the GPU solve's counts)")
+    return {"value": value, "sample": sample, "workload": workload}
 
 
 def main():
@@ -130,7 +242,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--n-per-gpu", type=int, default=50000, help="config 4: columns of A per rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--matvec-reps", type=int, default=50)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -140,12 +254,13 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2404_14524_b200 import Context, colmajor_device, nccl_unique_id
+    from paper_2404_14524_b200 import Context, nccl_unique_id
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    device = f"cuda:{local}"
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         obj = [nccl_unique_id() if rank == 0 else None]
@@ -156,12 +271,9 @@ def main():
     stream = torch.cuda.Stream(local)
     ctx = Context(local, stream=stream, nccl_id=nid, rank=rank, world=world)
 
-    inst, lo, hi = load_instance(args.config, rank, world)
-    A_loc = np.asfortranarray(inst.A[:, lo:hi])
-    Ad, lda = colmajor_device(A_loc, device=f"cuda:{local}")
-    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{local}")  # noqa: E731
-    q, b, c = dv(inst.q[lo:hi]), dv(inst.b), dv(inst.c[lo:hi])
-    m, nloc = inst.m, hi - lo
+    wl = Workload(args.config, rank, world, device, args.n_per_gpu, dist if world > 1 else None)
+    torch.cuda.synchronize()
+    m, nloc, lda = wl.m, wl.ncols, wl.lda
 
     def barrier():
         if world > 1:
@@ -170,10 +282,11 @@ def main():
 
     def one_solve():
         with torch.cuda.stream(stream):
-            return ctx.nys_ipppmm_solve(Ad, lda, m, q, b, c, ell=inst.ell)
+            return ctx.nys_ipppmm_solve(wl.At, lda, m, wl.q, wl.b, wl.c, ell=wl.ell, structure=wl.structure)
 
     # ---- warm-up ------------------------------------------------------------------------------
-    for _ in range(max(args.warmup, 3)):
+    W = max(args.warmup, 3)
+    for _ in range(W):
         g = one_solve()
     assert g["status"] == 0, f"solve status {g['status']}"
     # ---- timed region: K complete solves, CUDA events on the library's stream ------------------
@@ -188,61 +301,67 @@ def main():
     launches = ctx.kernel_launches - launches0
     t_dev = ev0.elapsed_time(ev1) / 1e3
     if world > 1:
-        tt = torch.tensor([t_dev], device=f"cuda:{local}")
+        tt = torch.tensor([t_dev], device=device)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_dev = float(tt.item())
     sec_per_solve = t_dev / args.steps
-    matvecs_per_solve = results[-1]["matvecs"]
+    last = results[-1]
+    matvecs_per_solve = last["matvecs"]
 
     # ---- dominant kernel: fused normal matvec, timed live with CUDA events on its stream ------
-    # The launches are captured in CUDA graphs (no host overhead between launches):
-    #   warm = R back-to-back matvecs;  cold = R x (256 MB L2-flushing read + matvec) minus R x flush
+    # Launches captured in CUDA graphs (no host gaps).  If A fits in L2 (< 1 GB), each launch is
+    # preceded by a 256 MB L2-flushing read and that read's own time is subtracted; otherwise
+    # A itself is larger than L2 and the launches are back to back.
     rs = np.random.default_rng(0)
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
     d = dv(rs.uniform(0.01, 2.0, nloc))
     v = dv(rs.standard_normal(m))
-    w = torch.empty(m, dtype=torch.float64, device=f"cuda:{local}")
-    flush = torch.ones(32 * 1024 * 1024, dtype=torch.float64, device=f"cuda:{local}")  # 256 MB
-    R = args.matvec_reps
-    with torch.cuda.stream(stream):
-        for _ in range(5):
-            ctx.nys_normal_matvec(Ad, lda, m, d, None, 1e-3, v, w)
-            flush.sum()
-    barrier()
-
-    def capture(fn):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            for _ in range(R):
-                fn()
-        return g
+    w = torch.empty(m, dtype=torch.float64, device=device)
+    e_diag = dv(np.ones(m)) if wl.structure == 1 else None
+    small = wl.a_bytes() < 1e9
+    R = args.matvec_reps if small else max(3, min(args.matvec_reps, int(2e10 / wl.a_bytes())))
+    flush = torch.ones(32 * 1024 * 1024, dtype=torch.float64, device=device) if small else None
+    fl_out = torch.empty((), dtype=torch.float64, device=device)
 
     def mv():
-        ctx.nys_normal_matvec(Ad, lda, m, d, None, 1e-3, v, w)
-
-    fl_out = torch.empty((), dtype=torch.float64, device=f"cuda:{local}")
+        ctx.nys_normal_matvec(wl.At, lda, m, d, e_diag, 1e-3, v, w)
 
     def fl():
         torch.sum(flush, dim=0, out=fl_out)
 
-    g_warm = capture(mv)
-    g_cold = capture(lambda: (fl(), mv()))
-    g_flush = capture(fl)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            mv()
     barrier()
 
-    def timed(g):
-        g.replay()
+    def capture(fn):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=stream):
+            for _ in range(R):
+                fn()
+        return gr
+
+    def timed(gr):
+        gr.replay()
         barrier()
         a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         with torch.cuda.stream(stream):
-            g.replay()
+            gr.replay()
         b_.record(stream)
         barrier()
         return a.elapsed_time(b_) / 1e3
 
+    g_warm = capture(mv)
     mv_warm_s = timed(g_warm) / R
-    mv_s = (timed(g_cold) - timed(g_flush)) / R
-    del g_warm, g_cold, g_flush, flush
+    if small:
+        g_cold = capture(lambda: (fl(), mv()))
+        g_flush = capture(fl)
+        mv_s = (timed(g_cold) - timed(g_flush)) / R
+        del g_cold, g_flush
+    else:
+        mv_s = mv_warm_s
+    del g_warm, flush
     mv_bytes = 8.0 * (m * nloc + nloc + 2 * m)  # A once + d + v in + w out
     mv_gbs = mv_bytes / mv_s / 1e9
     peaks = _peaks()
@@ -250,52 +369,73 @@ def main():
     peak_src = "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
 
     # ---- e2e: the same solve through the C ABI with host buffers --------------------------------
-    A_host = np.zeros((nloc, lda))
-    A_host[:, :m] = A_loc.T
-    qh, bh, ch = inst.q[lo:hi].copy(), inst.b.copy(), inst.c[lo:hi].copy()
-    barrier()
-    t0 = time.perf_counter()
-    E_STEPS = max(1, min(args.steps, 3))
-    for _ in range(E_STEPS):
-        with torch.cuda.stream(stream):
-            ge = ctx.nys_ipppmm_solve(A_host, lda, m, qh, bh, ch, ell=inst.ell, host=True)
-    barrier()
-    t_e2e = (time.perf_counter() - t0) / E_STEPS
-    if world > 1:
-        tt = torch.tensor([t_e2e], device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = float(tt.item())
-    h2d = 8 * (m * nloc + 2 * nloc + m)
-    d2h = 8 * (2 * nloc + m)
+    e2e = None
+    if not args.no_e2e:
+        need = wl.a_bytes() * 1.2
+        try:
+            import psutil
+            avail = psutil.virtual_memory().available / max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
+        except Exception:
+            avail = float("inf")
+        if need < 0.6 * avail:
+            A_host = wl.At.cpu().numpy()
+            qh, bh, ch = wl.q.cpu().numpy(), wl.b.cpu().numpy(), wl.c.cpu().numpy()
+            barrier()
+            t0 = time.perf_counter()
+            E_STEPS = max(1, min(args.steps, 3))
+            for _ in range(E_STEPS):
+                with torch.cuda.stream(stream):
+                    ctx.nys_ipppmm_solve(A_host, lda, m, qh, bh, ch, ell=wl.ell, host=True, structure=wl.structure)
+            barrier()
+            t_e2e = (time.perf_counter() - t0) / E_STEPS
+            if world > 1:
+                tt = torch.tensor([t_e2e], device=device)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t_e2e = float(tt.item())
+            nq = qh.shape[0]
+            e2e = {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": int(A_host.nbytes + 8 * (2 * nq + m)),
+                   "d2h_bytes_per_step": int(8 * (2 * nq + m))}
+            del A_host
+        else:
+            e2e = {"value": None, "unit": "s", "skipped": f"host RAM: need {need / 1e9:.0f} GB pinned-able, "
+                                                          f"{avail / 1e9:.0f} GB available per rank"}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) --------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import ippmm
-        t0 = time.perf_counter()
-        r = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
-        tc = time.perf_counter() - t0
-        cpu = {"value": tc, "unit": "s", "cores": os.cpu_count(), "kind": "oracle",
-               "sample": f"one full oracle solve of {inst.name} ({r.outer} outer, {r.inner_total} PCG iters, "
-                         f"obj {r.obj:.12g} vs GPU {results[-1]['obj']:.12g})"}
+        if args.config in (0, 1, 3):
+            from oracle import ippmm
+            inst = wl.inst
+            t0 = time.perf_counter()
+            r = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
+            tc = time.perf_counter() - t0
+            cpu = {"value": tc, "unit": "s", "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"one full oracle solve of {inst.name} ({r.outer} outer, {r.inner_total} PCG iters, "
+                             f"obj {r.obj:.12g} vs GPU {last['obj']:.12g})"}
+        else:
+            proj = cpu_projection(args.config, wl.n, outer=last["outer"], matvecs=matvecs_per_solve)
+            cpu = {"value": proj["value"], "unit": "s", "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": proj["sample"]}
 
     if rank == 0:
-        last = results[-1]
         line = {
             "metric": METRIC, "value": sec_per_solve, "unit": "s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": sec_per_solve * 1e3, "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": inst.name, "m": m, "n": inst.n, "ell": inst.ell, "tol": 1e-8,
+            "warmup": W, "ms_per_step": sec_per_solve * 1e3, "higher_is_better": False,
+            "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.name, "m": m, "n": wl.n, "ell": wl.ell, "tol": 1e-8,
                        "parallelism": f"column-shard x{world}",
-                       "l2": "inputs larger than L2 (A = %.0f MB vs 126 MB L2), A streamed with L2 evict_first" % (8 * m * inst.n / 1e6)},
+                       "l2": ("A = %.0f MB vs 126 MB L2: roofline launches L2-flushed (256 MB read) before each"
+                              % (wl.a_bytes() * world / 1e6)) if small else
+                             ("A = %.1f GB per GPU >> 126 MB L2 (streamed with L2 evict_first)" % (wl.a_bytes() / 1e9))},
             "clocks": clk.summary(),
-            "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": e2e,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": mv_gbs, "peak": hbm, "unit": "GB/s", "frac": mv_gbs / hbm,
-                         "traffic": TRAFFIC.get(args.config), "kernel": "fused normal matvec (matvec_kernel + mv_finalize), L2 flushed (256 MB read) before each launch, graph-captured",
+                         "traffic": TRAFFIC.get(args.config) if args.config != 4 else None,
+                         "kernel": "fused normal matvec (matvec_kernel + mv_finalize), graph-captured",
                          "peak_source": peak_src, "bytes_per_launch": mv_bytes, "launch_us": mv_s * 1e6,
                          "warm_l2_gbs": mv_bytes / mv_warm_s / 1e9,
-                         "pcg_effective_gbs": last["inner"] * mv_bytes / (last["t_pcg_ms"] / 1e3) / 1e9,
+                         "pcg_effective_gbs": (last["inner"] * mv_bytes / (last["t_pcg_ms"] / 1e3) / 1e9) if last["t_pcg_ms"] > 0 else None,
                          "share_of_step": matvecs_per_solve * mv_s / sec_per_solve},
             "solve": {"outer": last["outer"], "inner": last["inner"], "obj": last["obj"], "rel_p": last["rel_p"],
                       "rel_d": last["rel_d"], "mu": last["mu"], "matvecs": matvecs_per_solve,

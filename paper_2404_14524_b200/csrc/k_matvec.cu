@@ -573,7 +573,7 @@ static MvCfg pick_cfg(int64_t rs, bool clu) {
   if (clu) {  // cluster path: rows split over the cluster, one group of 512 threads
     if (rs <= 4096) return {512, 512, 8, 2};
     if (rs <= 6656) return {512, 512, 13, 1};
-    return {512, 512, 16, 1};
+    return {512, 512, 17, 1};
   }
   if (rs <= 64) return {256, 32, 2, 4};
   if (rs <= 128) return {256, 32, 4, 2};
@@ -591,7 +591,7 @@ static MvKernel kernel_for(const MvCfg& c, bool clu) {
   if (clu) {
     if (c.RPT == 8 && c.CPG == 2) return matvec_kernel<512, 512, 8, 2, MODE, false, true>;
     if (c.RPT == 13) return matvec_kernel<512, 512, 13, 1, MODE, false, true>;
-    return matvec_kernel<512, 512, 16, 1, MODE, false, true>;
+    return matvec_kernel<512, 512, 17, 1, MODE, false, true>;
   }
   if (c.T == 256 && c.GT == 32 && c.RPT == 2 && c.CPG == 4) return matvec_kernel<256, 32, 2, 4, MODE, false, false>;
   if (c.T == 256 && c.GT == 32 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<256, 32, 4, 2, MODE, false, false>;
@@ -637,40 +637,96 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, 
   auto key = std::make_tuple(ctx->device, mode, m, n, lda);
   auto itp = g_plans.find(key);
   if (itp != g_plans.end()) { pl = itp->second; return NYS_OK; }
-  // m <= 8192: whole columns per CTA.  Larger m: split the rows over a cluster of cl CTAs,
-  // <= 6656 rows each (13 rows per thread: the register budget of the pipelined cluster path)
+  // Geometry for a cluster split cl: rows per CTA rs, thread config, stages, smem, kernel.
+  struct Geo {
+    int64_t rs;
+    MvCfg c;
+    int stages;
+    size_t smem;
+    MvKernel k;
+  };
+  auto derive = [&](int cl_, Geo& G) -> int {
+    int64_t rs_ = (m + cl_ - 1) / cl_;
+    rs_ = (rs_ + 1) & ~int64_t(1);
+    // whole-column CTAs with a near-tight lda: stride the stage by lda so a panel (BN consecutive
+    // columns) is ONE contiguous bulk copy (the padding rows are masked off in the kernel)
+    if (cl_ == 1 && lda >= rs_ && lda <= rs_ + 32) rs_ = lda;
+    const bool clu_ = cl_ > 1;
+    MvCfg c_ = pick_cfg(rs_, clu_);
+    if (const char* ov = getenv("NYS_MV_CFG")) {  // debug/tuning override "T,GT,RPT,CPG" (must be instantiated)
+      MvCfg o;
+      if (sscanf(ov, "%d,%d,%d,%d", &o.T, &o.GT, &o.RPT, &o.CPG) == 4 && (int64_t)o.GT * o.RPT >= rs_) c_ = o;
+    }
+    const int BN_ = (c_.T / c_.GT) * c_.CPG;
+    const size_t stage_bytes = (size_t)BN_ * rs_ * 8;
+    size_t budget = clu_ ? 212 * 1024 : (rs_ <= 1024) ? 96 * 1024 : 200 * 1024;
+    if (const char* sb = getenv("NYS_MV_SMEM_KB")) budget = (size_t)atoi(sb) * 1024;
+    if (cfg_vs(c_, clu_)) budget -= (size_t)rs_ * 8;
+    int st = (int)(budget / stage_bytes);
+    st = st > 8 ? 8 : st;
+    if (st < 2) st = 2;
+    G.rs = rs_; G.c = c_; G.stages = st;
+    G.smem = mv_smem_bytes(c_, rs_, st, cl_, clu_);
+    G.k = (mode == MV_FUSED) ? kernel_for<MV_FUSED>(c_, clu_) : (mode == MV_TONLY) ? kernel_for<MV_TONLY>(c_, clu_) : kernel_for<MV_NONLY>(c_, clu_);
+    NYS_TRY(ensure_max_smem(ctx, (const void*)G.k, G.smem));
+    if (cl_ > 8) NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(G.k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    return NYS_OK;
+  };
+  auto resident_ctas = [&](int cl_, const Geo& G) -> int {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(cl_ * ctx->num_sms));
+    cfg.blockDim = dim3((unsigned)(G.c.T + 32));
+    cfg.dynamicSmemBytes = G.smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl_;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl_ = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl_, G.k, &cfg) != cudaSuccess) { cudaGetLastError(); ncl_ = 0; }
+    return ncl_ * cl_;
+  };
+  // m <= 8192: whole columns per CTA.  Larger m: split the rows over a cluster of cl CTAs with
+  // <= 8704 rows each (17 rows per thread: the register budget of the pipelined cluster path).
+  // Cluster sizes need not be powers of two; GPCs do not hold equal numbers of clusters of every
+  // size, so pick the SMALLEST cl (largest row slice: per-panel overheads amortised over more
+  // bytes) whose resident CTA count is within 5% of the best over all admissible cl
+  // (measured on B200, m = 50000: cl = 6 -> 132 CTAs, 6.68 TB/s; cl = 8 -> 120 CTAs, 5.59 TB/s).
   int cl = 1;
+  Geo geo;
   if (m > 8192) {
-    cl = 2;
-    while ((m + cl - 1) / cl > 6656 && cl < 16) cl *= 2;
+    int clmin = (int)((m + 8703) / 8704);
+    if (clmin < 2) clmin = 2;
+    if (clmin > 16) { ctx->set_error("matvec: m too large for the cluster split (m <= 16 * 8704)"); return NYS_EINVAL; }
+    int forced = 0;
+    if (const char* oc = getenv("NYS_MV_CL")) {  // tuning override of the cluster split
+      const int o = atoi(oc);
+      if (o >= clmin && o <= 16) forced = o;
+    }
+    int res[17] = {0};
+    int best = 0;
+    for (int k = clmin; k <= 16; ++k) {
+      if (forced && k != forced) continue;
+      Geo G;
+      NYS_TRY(derive(k, G));
+      res[k] = resident_ctas(k, G);
+      if (res[k] > best) best = res[k];
+    }
+    if (best == 0) { ctx->set_error("matvec: no cluster configuration fits on the device"); return NYS_ECUDA; }
+    for (int k = clmin; k <= 16; ++k)
+      if (res[k] > 0 && res[k] * 20 >= best * 19) { cl = k; break; }
   }
-  if (const char* oc = getenv("NYS_MV_CL")) {  // tuning override of the cluster split (m > 4096)
-    const int o = atoi(oc);
-    if ((o == 2 || o == 4 || o == 8 || o == 16) && m > 4096) cl = o;
-  }
-  int64_t rs = (m + cl - 1) / cl;
-  rs = (rs + 1) & ~int64_t(1);
-  // whole-column CTAs with a near-tight lda: stride the stage by lda so a panel (BN consecutive
-  // columns) is ONE contiguous bulk copy (the padding rows are masked off in the kernel)
-  if (cl == 1 && lda >= rs && lda <= rs + 32) rs = lda;
+  NYS_TRY(derive(cl, geo));
   const bool clu = cl > 1;
-  MvCfg c = pick_cfg(rs, clu);
-  if (const char* ov = getenv("NYS_MV_CFG")) {  // debug/tuning override "T,GT,RPT,CPG" (must be instantiated)
-    MvCfg o;
-    if (sscanf(ov, "%d,%d,%d,%d", &o.T, &o.GT, &o.RPT, &o.CPG) == 4 && (int64_t)o.GT * o.RPT >= rs) c = o;
-  }
+  const int64_t rs = geo.rs;
+  const MvCfg c = geo.c;
+  const int stages = geo.stages;
+  const size_t smem = geo.smem;
+  MvKernel k = geo.k;
   const int NG = c.T / c.GT, BN = NG * c.CPG;
-  const size_t stage_bytes = (size_t)BN * rs * 8;
-  size_t budget = clu ? 212 * 1024 : (rs <= 1024) ? 96 * 1024 : 200 * 1024;
-  if (const char* sb = getenv("NYS_MV_SMEM_KB")) budget = (size_t)atoi(sb) * 1024;
-  if (cfg_vs(c, clu)) budget -= (size_t)rs * 8;
-  int stages = (int)(budget / stage_bytes);
-  stages = stages > 8 ? 8 : stages;
-  if (stages < 2) stages = 2;
-  size_t smem = mv_smem_bytes(c, rs, stages, cl, clu);
-  MvKernel k = (mode == MV_FUSED) ? kernel_for<MV_FUSED>(c, clu) : (mode == MV_TONLY) ? kernel_for<MV_TONLY>(c, clu) : kernel_for<MV_NONLY>(c, clu);
-  NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (cl > 8) NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  (void)clu;
   const int64_t npanels = (n + BN - 1) / BN;
   int grid = 0;
   int rc = 1;
@@ -741,6 +797,16 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, 
     fprintf(stderr, "[nys] matvec plan mode=%d m=%lld n=%lld: T=%d GT=%d RPT=%d CPG=%d cl=%d rc=%d rs=%lld stages=%d smem=%zu grid=%d nparts=%d npanels=%lld\n",
             mode, (long long)m, (long long)n, c.T, c.GT, c.RPT, c.CPG, cl, rc, (long long)rs, stages, smem, grid, pl.nparts,
             (long long)npanels);
+  return NYS_OK;
+}
+
+int ensure_max_smem(nys_ctx* ctx, const void* fn, size_t bytes) {
+  static std::map<std::pair<int, const void*>, size_t> set;
+  auto key = std::make_pair(ctx->device, fn);
+  auto it = set.find(key);
+  if (it != set.end() && it->second >= bytes) return NYS_OK;
+  NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  set[key] = bytes;
   return NYS_OK;
 }
 

@@ -488,7 +488,7 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
   if (stages < 2) stages = 2;
   const size_t smem = (size_t)stages * stage_bytes + 2 * stages * 8 + (size_t)2 * NG * WPG * c.CPG * 8;
   PcgKernel k = pcg_kernel_for(c);
-  NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  NYS_TRY(ensure_max_smem(ctx, (const void*)k, smem));
   int occ = 0;
   NYS_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c.T + 32, smem));
   if (occ < 1) { ctx->set_error("persistent PCG does not fit on an SM"); return NYS_ECUDA; }

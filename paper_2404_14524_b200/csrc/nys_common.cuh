@@ -212,6 +212,11 @@ __device__ __forceinline__ double warp_min(double v) {
 // ------------------------------------------------------------------------------------------
 namespace nys {
 
+// Raise (never lower) a kernel's dynamic shared-memory limit on the context's device: several
+// plans share one kernel instantiation with different stage counts, so the attribute must stay
+// >= every plan's launch size.
+int ensure_max_smem(nys_ctx* ctx, const void* fn, size_t bytes);
+
 enum MatvecMode { MV_FUSED = 0, MV_TONLY = 1, MV_NONLY = 2 };
 
 // where the fused PCG matvec left its per-cluster w partials and per-CTA p^T N p partials

@@ -92,20 +92,26 @@ def make_config(idx: int, m: Optional[int] = None, n: Optional[int] = None,
         b, c = _feasible_bc(A, q, x0, y0, z0)
         return QPInstance(name, idx, A, q, b, c, ell, x0, y0, z0)
 
-    if idx in (1, 4):
-        # A = W H + s G ; draw order: W, H, G, q, [zero-permutation], x0, y0, z0
-        r, s = (40, 1e-3) if idx == 1 else (100, 1e-2)
+    if idx == 4:
+        # counter-based, shardable recipe (synth/large.py); the QP uses generator columns [0, n)
+        from .large import generate_shard
+        if m * n > 2e8:
+            raise ValueError("config 4 at this size is generated per shard on the device (synth.large)")
+        sh = generate_shard(m, n, 0, n, n_gen=n, seed=seed)
+        A = np.asfortranarray(sh.At[:, :m].numpy().T)
+        return QPInstance(name, idx, A, sh.q.numpy(), sh.b_part.numpy(), sh.c.numpy(), ell,
+                          sh.x0.numpy(), sh.y0.numpy(), sh.z0.numpy())
+
+    if idx == 1:
+        # A = W H + s G ; draw order: W, H, G, q, x0, y0, z0
+        r, s = 40, 1e-3
         r = min(r, m, n)
         W = gaussian_matrix(rng, m, r)
         H = gaussian_matrix(rng, r, n)
         G = gaussian_matrix(rng, m, n)
         A = np.asfortranarray(W @ H + s * G)
         del G
-        if idx == 1:
-            q = rng.uniform(1e-3, 1.0, n)
-        else:
-            q = rng.uniform(0.0, 1.0, n)
-            q[rng.permutation(n)[: int(0.3 * n)]] = 0.0          # floor(0.3 n) zeros (A22)
+        q = rng.uniform(1e-3, 1.0, n)
         x0 = rng.uniform(0.5, 1.5, n)
         y0 = rng.standard_normal(m)
         z0 = rng.uniform(0.5, 1.5, n)

@@ -1,0 +1,70 @@
+"""Seeded input generators (synth/) — CPU checks: the counter-based config-4 generator reproduces
+the published Philox4x32-10 known answers, is shard-invariant, and builds a feasible QP exactly as
+BASELINE.json configs[4] prescribes (b = A x0, c = A^T y0 + z0 - q x0, floor(0.3 n) zeros in q)."""
+import os
+
+import numpy as np
+import torch
+
+from synth import large, make_config
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_synth_philox_known_answers():
+    # Salmon et al. SC'11 / Random123 kat_vectors (tests/golden/philox4x32_10_kat.txt)
+    n = 0
+    for line in open(os.path.join(GOLDEN, "philox4x32_10_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        v = [int(x, 16) for x in line.split()]
+        ctr = [torch.tensor([x], dtype=torch.int64) for x in v[:4]]
+        out = large.philox4x32_10(*ctr, v[4], v[5])
+        assert [int(o) for o in out] == v[6:10]
+        n += 1
+    assert n >= 3
+
+
+def test_normals_stream_offsets_and_moments():
+    full = large.normals(4, large.G_ID, 0, 200001)
+    for s, c in [(0, 7), (1, 10), (12345, 999), (200000, 1)]:
+        assert torch.equal(large.normals(4, large.G_ID, s, c), full[s:s + c])
+    z = full.numpy()
+    assert abs(z.mean()) < 0.01 and abs(z.std() - 1.0) < 0.01
+    # different matrix ids / seeds give different streams
+    assert not torch.equal(large.normals(4, large.W_ID, 0, 100), large.normals(4, large.H_ID, 0, 100))
+    assert not torch.equal(large.normals(4, large.W_ID, 0, 100), large.normals(5, large.W_ID, 0, 100))
+
+
+def test_config4_shards_reassemble_the_instance():
+    m, n = 120, 701
+    full = large.generate_shard(m, n, 0, n, chunk_elems=5000)
+    parts = [large.generate_shard(m, n, *large.shard_bounds(n, r, 3), chunk_elems=3000) for r in range(3)]
+    assert torch.equal(torch.cat([p.At for p in parts]), full.At)
+    assert torch.equal(torch.cat([p.c for p in parts]), full.c)
+    bsum = sum(p.b_part for p in parts)
+    assert torch.allclose(bsum, full.b_part, rtol=1e-13, atol=1e-9)
+    # padding rows of the library layout are zero
+    assert torch.count_nonzero(full.At[:, m:]) == 0
+
+
+def test_config4_feasible_point_and_zero_pattern():
+    inst = make_config(4, m=200, n=1500, ell=30)
+    A = inst.A
+    assert np.linalg.norm(A @ inst.x0 - inst.b) <= 1e-13 * np.linalg.norm(inst.b)
+    assert np.linalg.norm(A.T @ inst.y0 + inst.z0 - inst.q * inst.x0 - inst.c) <= 1e-13 * np.linalg.norm(inst.c)
+    assert int((inst.q == 0).sum()) == int(0.3 * 1500)          # A22
+    assert inst.x0.min() >= 0.5 and inst.z0.min() >= 0.5
+    # A = W H + 1e-2 G with W, H rank 100: 100 dominant singular values, then the noise level
+    s = np.linalg.svd(A, compute_uv=False)
+    assert s[99] > 20 * s[100]
+    assert 0.5 * 1e-2 * (np.sqrt(1500) - np.sqrt(200)) < s[100] < 2 * 1e-2 * (np.sqrt(1500) + np.sqrt(200))
+
+
+def test_config4_slice_is_restriction_of_the_generator():
+    # A25: the slice QP uses generator columns [0, n) with the same y0 and restricted q, x0, z0
+    m, n_gen, n = 100, 900, 300
+    full = large.generate_shard(m, n_gen, 0, n_gen, n_gen=n_gen)
+    sl = large.generate_shard(m, n, 0, n, n_gen=n_gen)
+    assert torch.equal(sl.At, full.At[:n])
+    assert torch.equal(sl.q, full.q[:n]) and torch.equal(sl.x0, full.x0[:n]) and torch.equal(sl.y0, full.y0)
