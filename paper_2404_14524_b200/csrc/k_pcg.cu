@@ -39,33 +39,41 @@ struct PcgPParams {
   double* Wp;            // [G][wp_ld] partial w
   int64_t wp_ld;
   double* pwp;           // [G]
-  double* part1;         // [(1 + ell)][G]   (rr, U^T r) partials, column-contiguous
+  double* part1;         // [G][(1 + ell)]   (rr, U^T r) partial row per CTA
   double* part2;         // [G]              r^T z partials
+  double* gtot;          // [ceil(G/RG)][1 + ell] group totals of part1
+  double* tot;           // [1 + ell] grand totals
+  unsigned int* rbar;    // [66]: group arrival counters [0, 64), top counter [64], publish flag [65]
   double* sc;
   unsigned int* bar;     // [2]: count, generation
   int max_iter;
   int stages;
+  int l2_prefetch;            // panels prefetched into L2 ahead of the smem ring
+  unsigned long long* trace;  // debug (NYS_PCG_TRACE): [2 CTAs][32 iters][8] globaltimer stamps
   int64_t npanels;
   int64_t rows_per_cta;
 };
 
-__device__ __forceinline__ void pcg_grid_barrier(unsigned int* bar, unsigned int nblocks, int nthreads) {
+// Grid barrier on a monotonically increasing arrival counter (zeroed before the launch): each CTA
+// adds 1 (fire-and-forget reduction) and polls until the counter reaches epoch * G.  No "last
+// arriver" reset round trip, no sleep granularity on the release.
+__device__ __forceinline__ void pcg_grid_barrier(unsigned int* bar, unsigned int nblocks, int nthreads,
+                                                 unsigned int& epoch) {
   named_bar_sync(9, nthreads);
   if (threadIdx.x == 0) {
-    volatile unsigned int* gen = bar + 1;
-    const unsigned int g = *gen;
+    ++epoch;
+    const unsigned int target = epoch * nblocks;
     __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      bar[0] = 0u;
-      __threadfence();
-      atomicExch(bar + 1, g + 1u);
-    } else {
-      while (*gen == g) __nanosleep(20);
+    atomicAdd(bar, 1u);
+    volatile unsigned int* cnt = bar;
+    while (*cnt < target) {
     }
     __threadfence();
   }
   named_bar_sync(9, nthreads);
 }
+
+constexpr int RG = 16;  // CTAs per first-level reduction group (G <= 64 * RG)
 
 // deterministic sum over G partials of column j (one warp)
 __device__ __forceinline__ double col_sum(const double* part, int j, int G) { return warp_sum_array(part + (size_t)j * G, G); }
@@ -83,6 +91,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   uint64_t* empty = full + S;
   double* red = reinterpret_cast<double*>(empty + S);  // 2 * NG * WPG * CPG
   __shared__ double hsh[256];
+  __shared__ int s_role;
   __shared__ double chunk_red[16][17];
   __shared__ double s_scal[8];
   __shared__ volatile int s_stop;
@@ -114,8 +123,19 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     long long q = 0;
     if (lane == 0 && niter > 0) {
       const uint64_t pol = l2_evict_first_policy();
+      // L2 prefetch runs PF panels ahead of the smem ring: the reduction / barrier phases of an
+      // iteration leave HBM idle, so the next matvec's panels are pulled into L2 meanwhile
+      long long pf = 0;
+      const int PF = P.l2_prefetch;
       for (;;) {
         const int s = (int)(q % S);
+        for (; pf < q + S + PF; ++pf) {
+          const int64_t itp = pf % niter;
+          const int64_t c0 = (int64_t)(cid + itp * G) * BN;
+          int64_t nc = P.n - c0;
+          nc = nc > BN ? BN : nc;
+          if (pf >= q + S) bulk_prefetch_l2(P.A + c0 * P.lda, (uint32_t)(((nc - 1) * P.lda) * 8) + copy_bytes);
+        }
         if (q >= S) {
           const uint32_t par = (uint32_t)(((q / S) - 1) & 1);
           bool stop = false;
@@ -154,6 +174,16 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   const int row16 = tid & 15, grp16 = (tid >> 4) & 15;  // first 256 threads: 16 rows x 16 groups
   const int hrow = lane & 15, hw = 2 * warp + (lane >> 4);
   long long qc = 0;  // consumed stage counter
+  unsigned int bar_epoch = 0;  // grid barriers passed (thread 0)
+  unsigned int red_epoch = 0;  // column reductions done (thread 0)
+  int trace_k = 0;
+  auto stamp = [&](int slot) {
+    if (P.trace != nullptr && tid == 0 && (cid == 0 || cid == G - 1) && trace_k < 32) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      P.trace[((cid == 0 ? 0 : 1) * 32 + trace_k) * 16 + slot] = t;
+    }
+  };
   double rz = 0.0, beta = 0.0;
   int iters = 0;
   int status = 0;
@@ -169,16 +199,19 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     for (int64_t i0 = r_lo; i0 < r_hi; i0 += 16) {
       const int64_t i = i0 + row16;
       if (!init && warp < 8) {
-        double acc = 0.0, a1 = 0.0;
+        double acc = 0.0;
         if (i < r_hi) {
-          int c = grp16;
-          for (; c + 16 < (int)G; c += 32) {
-            acc += Wp[(size_t)c * P.wp_ld + i];
-            a1 += Wp[(size_t)(c + 16) * P.wp_ld + i];
+          for (int c0 = grp16; c0 < (int)G; c0 += 128) {  // 8 independent L2 loads per round
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int c = c0 + 16 * u;
+              v[u] = (c < (int)G) ? __ldcg(Wp + (size_t)c * P.wp_ld + i) : 0.0;
+            }
+            acc += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
           }
-          if (c < (int)G) acc += Wp[(size_t)c * P.wp_ld + i];
         }
-        chunk_red[row16][grp16] = acc + a1;
+        chunk_red[row16][grp16] = acc;
       }
       named_bar_sync(9, T);
       if (tid < 16) {
@@ -191,7 +224,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
             const double* v = chunk_red[row16];
             const double wsum = (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
                                 (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
-            const double pi = pnew[i];
+            const double pi = __ldcg(pnew + i);
             const double wi = wsum + (delta + (P.e ? P.e[i] : 0.0)) * pi;
             P.x[i] = fma(alpha, pi, P.x[i]);
             ri = fma(-alpha, wi, P.r[i]);
@@ -213,7 +246,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     }
     // write partials: rr (threads < 16 hold pieces) and U^T r (half-warps)
     double rrw = warp_sum(rr);
-    if (tid == 0) P.part1[cid] = rrw;
+    if (tid == 0) P.part1[(size_t)cid * (1 + ell)] = rrw;
     if (warp < 8) {
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
@@ -224,7 +257,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
           gsum += __shfl_xor_sync(0xffffffffu, gsum, 2);
           gsum += __shfl_xor_sync(0xffffffffu, gsum, 1);
           const int c = hw + 16 * k;
-          if (hrow == 0 && c < ell) P.part1[(size_t)(1 + c) * G + cid] = gsum;
+          if (hrow == 0 && c < ell) P.part1[(size_t)cid * (1 + ell) + 1 + c] = gsum;
         }
       }
     }
@@ -232,11 +265,76 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
 
   // P3: converged? then h and z = r + U h, r^T z partial
   auto phase_prec = [&](bool init) -> bool {
-    if (warp == 0) {
-      const double rrt = col_sum(P.part1, 0, G);
-      if (lane == 0) s_scal[0] = rrt;
+    // all 1 + ell sums of the CTA partial rows part1[cid][.] (||r||^2, U^T r): two-level "last
+    // arriver reduces" (groups of RG CTAs, then the groups), fixed order -> deterministic; every CTA
+    // then reads the ncol totals.  Replaces a grid barrier + every CTA re-reading all G partials.
+    {
+      const int ncol = 1 + ell;
+      const unsigned int ngr = (G + RG - 1) / RG;
+      const unsigned int grp = cid / RG;
+      const unsigned int gsz = (grp + 1 == ngr) ? G - grp * RG : RG;
+      named_bar_sync(9, T);  // this CTA's partial row is written
+      if (tid == 0) {
+        ++red_epoch;
+        __threadfence();
+        const unsigned int old = atomicAdd(P.rbar + grp, 1u);
+        __threadfence();
+        s_role = (old + 1 == red_epoch * gsz) ? 1 : 0;
+      }
+      named_bar_sync(9, T);
+      if (s_role) {  // last CTA of its group: group totals
+        for (int c = tid; c < ncol; c += T) {
+          double v[RG];
+#pragma unroll
+          for (int u = 0; u < RG; ++u)
+            v[u] = (u < (int)gsz) ? __ldcg(P.part1 + (size_t)(grp * RG + u) * ncol + c) : 0.0;
+#pragma unroll
+          for (int w = RG / 2; w > 0; w >>= 1)
+#pragma unroll
+            for (int u = 0; u < w; ++u) v[u] += v[u + w];
+          P.gtot[(size_t)grp * ncol + c] = v[0];
+        }
+        named_bar_sync(9, T);
+        if (tid == 0) {
+          __threadfence();
+          const unsigned int old = atomicAdd(P.rbar + 64, 1u);
+          __threadfence();
+          s_role = (old + 1 == red_epoch * ngr) ? 2 : 1;
+        }
+        named_bar_sync(9, T);
+        if (s_role == 2) {  // last group: grand totals, then publish
+          for (int c = tid; c < ncol; c += T) {
+            double acc = 0.0;
+            for (unsigned int g0 = 0; g0 < ngr; g0 += 8) {
+              double v[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) v[u] = (g0 + u < ngr) ? __ldcg(P.gtot + (size_t)(g0 + u) * ncol + c) : 0.0;
+              acc += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+            }
+            P.tot[c] = acc;
+          }
+          named_bar_sync(9, T);
+          if (tid == 0) {
+            __threadfence();
+            atomicExch(P.rbar + 65, red_epoch);
+          }
+        }
+      }
+      if (tid == 0) {
+        volatile unsigned int* fl = P.rbar + 65;
+        while (*fl < red_epoch) {
+        }
+        __threadfence();
+      }
+      named_bar_sync(9, T);
+      for (int c = tid; c < ncol; c += T) {
+        const double sum = __ldcg(P.tot + c);
+        if (c == 0) s_scal[0] = sum;
+        else hsh[c - 1] = P.s[c - 1] * sum;
+      }
+      named_bar_sync(9, T);
     }
-    named_bar_sync(9, T);
+    if (!init) stamp(6);
     const double rrt = s_scal[0];
     const double tol = P.sc[S_TOL];
     bool cv = sqrt(rrt) <= tol;
@@ -248,11 +346,6 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       return true;
     }
     if (ell > 0) {
-      for (int c = warp; c < ell; c += T / 32) {
-        const double gc = col_sum(P.part1, 1 + c, G);
-        if (lane == 0) hsh[c] = P.s[c] * gc;
-      }
-      named_bar_sync(9, T);
       double rzp = 0.0;
       for (int64_t i0 = r_lo; i0 < r_hi; i0 += 16) {
         const int64_t i = i0 + row16;
@@ -276,7 +369,8 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       }
       rzp = warp_sum(rzp);
       if (tid == 0) P.part2[cid] = rzp;
-      pcg_grid_barrier(P.bar, G, T);
+      if (!init) stamp(7);
+      pcg_grid_barrier(P.bar, G, T, bar_epoch);
       if (warp == 0) {
         const double rzn = warp_sum_array(P.part2, G);
         if (lane == 0) s_scal[1] = rzn;
@@ -295,11 +389,12 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
 
   const double delta = P.sc[S_DELTA];
   rows_phase_rr_ut(true, 0.0, nullptr, nullptr, delta);
-  pcg_grid_barrier(P.bar, G, T);
   bool stop = phase_prec(true);
 
   int k = 0;
   while (!stop) {
+    trace_k = k;
+    stamp(0);
     // ---- P1: v = z + beta p ; fused matvec over this CTA's panels ----------------------------
     const double* pold = (k & 1) ? P.P1 : P.P0;
     double* pnew = (k & 1) ? P.P0 : P.P1;
@@ -310,19 +405,23 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       const int64_t rl = lig + (int64_t)GT * i;
       double v = 0.0;
       if (rl < P.m) {
-        v = P.z[rl];
-        if (k > 0) v = fma(beta, pold[rl], v);
+        v = __ldcg(P.z + rl);  // written by other CTAs in this launch: read through L2
+        if (k > 0) v = fma(beta, __ldcg(pold + rl), v);
         if (cid == 0 && g == 0) pnew[rl] = v;
       }
       vreg[i] = v;
       wacc[i] = 0.0;
     }
     double pwacc = 0.0;
+    stamp(8);
     for (int64_t it = 0; it < niter; ++it, ++qc) {
       const int s = (int)(qc % S);
       const uint32_t par = (uint32_t)((qc / S) & 1);
       const int64_t col0 = (int64_t)(cid + it * G) * BN + (int64_t)g * CPG;
       mbar_wait(&full[s], par);
+      if (it == 0) stamp(9);
+      if (it == niter / 2) stamp(10);
+      if (it == niter - 1) stamp(11);
       double a[CPG][RPT];
       const double* sb = stage + ((size_t)s * BN + (size_t)g * CPG) * rs;
 #pragma unroll
@@ -416,7 +515,9 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
         P.pwp[cid] = b;
       }
     }
-    pcg_grid_barrier(P.bar, G, T);
+    stamp(1);
+    pcg_grid_barrier(P.bar, G, T, bar_epoch);
+    stamp(2);
     // ---- P2: alpha, own-row updates, partials --------------------------------------------------
     if (warp == 0) {
       const double pw = warp_sum_array(P.pwp, G);
@@ -427,9 +528,11 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     if (!(pw > 0.0) || !isfinite(pw)) { status = NYS_EBREAKDOWN; break; }
     const double alpha = rz / pw;
     rows_phase_rr_ut(false, alpha, pnew, P.Wp, delta);
-    pcg_grid_barrier(P.bar, G, T);
+    stamp(3);
+    stamp(4);
     // ---- P3 / P4 -------------------------------------------------------------------------------
     stop = phase_prec(false);
+    stamp(5);
     ++k;
   }
 
@@ -482,7 +585,7 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
   const int NG = c.T / c.GT, WPG = c.GT / 32, BN = NG * c.CPG;
   const int64_t mp = (m + 1) & ~int64_t(1);
   const size_t stage_bytes = (size_t)BN * mp * 8;
-  const size_t budget = (mp <= 1024) ? 96 * 1024 : 180 * 1024;
+  const size_t budget = (mp <= 1024) ? 96 * 1024 : 196 * 1024;
   int stages = (int)(budget / stage_bytes);
   if (stages > 8) stages = 8;
   if (stages < 2) stages = 2;
@@ -509,12 +612,24 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
   P.part1 = ctx->wsd("pp_part1", (size_t)(1 + ell) * G);
   P.part2 = ctx->wsd("pp_part2", (size_t)G);
   P.sc = ctx->sc;
-  P.bar = (unsigned int*)ctx->ws("pp_bar", 64);
+  P.bar = (unsigned int*)ctx->ws("pp_bar", 64 + 66 * 4);
+  P.rbar = P.bar + 16;
+  P.gtot = ctx->wsd("pp_gtot", (size_t)((G + RG - 1) / RG) * (1 + ell));
+  P.tot = ctx->wsd("pp_tot", (size_t)(1 + ell));
   P.max_iter = max_iter;
   P.stages = stages;
   P.npanels = npanels;
   P.rows_per_cta = (m + G - 1) / G;
-  NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.bar, 0, 64, ctx->stream));
+  {
+    // prefetch depth: keep about half of L2 (~60 MB) of A in flight ahead of the ring
+    const double panel_bytes = (double)BN * lda * 8.0;
+    int pfd = (int)(60e6 / (panel_bytes * (double)G));
+    if (pfd > 64) pfd = 64;
+    if (pfd < 0) pfd = 0;
+    if (const char* e = getenv("NYS_PCG_PF")) pfd = atoi(e);
+    P.l2_prefetch = pfd;
+  }
+  NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.bar, 0, 64 + 66 * 4, ctx->stream));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)G);
   cfg.blockDim = dim3((unsigned)(c.T + 32));
@@ -525,8 +640,28 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  const bool trace = getenv("NYS_PCG_TRACE") != nullptr;
+  if (trace) {
+    P.trace = (unsigned long long*)ctx->ws("pp_trace", 2 * 32 * 16 * 8);
+    NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.trace, 0, 2 * 32 * 16 * 8, ctx->stream));
+  }
   NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, P));
   ctx->launches++;
+  if (trace) {
+    unsigned long long h[2 * 32 * 16];
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(h, P.trace, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int c = 0; c < 2; ++c)
+      for (int it = 0; it < 32; ++it) {
+        const unsigned long long* r = h + (c * 32 + it) * 16;
+        if (r[0] == 0 || r[5] == 0) continue;
+        fprintf(stderr, "[pcgtrace] cta=%s it=%d vset=%.2f first=%.2f half=%.2f last=%.2f\n", c ? "last" : "0", it,
+                (r[8] - r[0]) * 1e-3, (r[9] - r[8]) * 1e-3, (r[10] - r[9]) * 1e-3, (r[11] - r[10]) * 1e-3);
+        fprintf(stderr, "[pcgtrace] cta=%s it=%d matvec=%.2f bar1=%.2f rows=%.2f bar2=%.2f colsum=%.2f zrows=%.2f bar3=%.2f total=%.2f us\n",
+                c ? "last" : "0", it, (r[1] - r[0]) * 1e-3, (r[2] - r[1]) * 1e-3, (r[3] - r[2]) * 1e-3,
+                (r[4] - r[3]) * 1e-3, (r[6] - r[4]) * 1e-3, (r[7] - r[6]) * 1e-3, (r[5] - r[7]) * 1e-3, (r[5] - r[0]) * 1e-3);
+      }
+  }
   return ctx->check_launch("pcg_persistent");
 }
 

@@ -242,17 +242,34 @@ __device__ __forceinline__ double fast_rsqrt(double y) {  // y in [1, 1e30)
   return r;
 }
 
-// NMAX: compile-time bound on ell (64 / 128 / 256); GL lanes per column pair, E = NMAX / GL
-// elements per lane (fully unrolled, predicated): no runtime-bounded inner loops, and log2(GL)
-// shuffle levels per dot product.
-template <int NMAX, int GL, bool SM>
+// One warp per column pair (E = NMAX / 32 elements per lane, fully unrolled and predicated): a
+// round costs one dot product (5 shuffle levels), one rotation and the two column updates.
+// Rotation (symmetric Schur, fp64): zeta = (beta - alpha) / (2 gamma),
+// t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), c = (1 + t^2)^{-1/2}, s = c t; the reciprocal and
+// rsqrt come from fp32 seeds refined by Newton steps to fp64 (t must be accurate: the column norms
+// are updated incrementally as alpha - t gamma, beta + t gamma).
+__device__ __forceinline__ void jacobi_rotation(double al, double be, double ga, double& c, double& s, double& t) {
+  const double zeta = (be - al) * 0.5 * fast_rcp(ga);
+  const double az = fabs(zeta);
+  if (az > 1e8) {
+    t = 0.5 * fast_rcp(zeta);
+  } else {
+    const double y = fma(zeta, zeta, 1.0);
+    t = copysign(fast_rcp(az + y * fast_rsqrt(y)), zeta);
+  }
+  c = fast_rsqrt(fma(t, t, 1.0));
+  s = c * t;
+}
+
+template <int NMAX, bool SM>
 __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, int ldr, double* Vout, int ldv,
                                                       double* sigma, double* gws, double* jsweeps) {
-  constexpr int E = NMAX / GL;
+  constexpr int E = NMAX / 32;
   extern __shared__ double jsm[];
   double* X = SM ? jsm : gws;
   double* V = X + (size_t)n * n;
   __shared__ int rotated;
+  __shared__ double abs_floor;
   __shared__ double sv[NMAX];
   __shared__ int order[NMAX];
   __shared__ double nrm[NMAX];
@@ -263,75 +280,78 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
   }
   __syncthreads();
   const int P = (n % 2 == 0) ? n : n + 1;
-  const int npg = blockDim.x / GL;             // pair groups in the block
-  const int grp = threadIdx.x / GL, lig = threadIdx.x % GL;
+  const int nwarp = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double tol = fmax(1e-15, (double)n * 0x1p-53);
   const double tol2 = tol * tol;
-  auto gsum = [&](double v) {
+  auto wsum = [&](double v) {
 #pragma unroll
-    for (int o = GL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
   };
   int sweep = 0;
   for (; sweep < 30; ++sweep) {
-    for (int j0 = 0; j0 < n; j0 += npg) {      // exact column norms (uniform trip count)
-      const int j = j0 + grp;
+    for (int j = warp; j < n; j += nwarp) {    // exact column norms
       double a = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const int i = lig + GL * e;
-        if (i < n && j < n) a = fma(X[i + j * n], X[i + j * n], a);
+        const int i = lane + 32 * e;
+        if (i < n) a = fma(X[i + j * n], X[i + j * n], a);
       }
-      a = gsum(a);
-      if (lig == 0 && j < n) nrm[j] = a;
+      a = wsum(a);
+      if (lane == 0) nrm[j] = a;
     }
     if (threadIdx.x == 0) rotated = 0;
     __syncthreads();
+    // absolute floor of the rotation test: a coupling |x_p^T x_q| below eps^2-level of the largest
+    // column norm^2 changes X^T X = R R^T by far less than the Nystrom shift nu (~eps ||Y||) that
+    // Alg. 1 line 8 subtracts anyway, so such pairs are left alone (pairs of noise-level columns
+    // otherwise keep rotating on rounding for the full sweep cap)
+    if (warp == 0) {
+      double mx = 0.0;
+      for (int j = lane; j < n; j += 32) mx = fmax(mx, nrm[j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) abs_floor = 1e-2 * 0x1p-52 * mx;
+    }
+    __syncthreads();
+    const double floor_g = abs_floor;
     for (int r = 0; r < P - 1; ++r) {
-      for (int pi0 = 0; pi0 < P / 2; pi0 += npg) {
-        const int pi = pi0 + grp;
+      for (int pi = warp; pi < P / 2; pi += nwarp) {
         int a, b;
         if (pi == 0) { a = r; b = P - 1; }
         else {
           a = r + pi; if (a >= P - 1) a -= P - 1;
           b = r - pi; if (b < 0) b += P - 1;
         }
-        const bool act = (pi < P / 2) && a < n && b < n;
-        const int p = act ? (a < b ? a : b) : 0, q = act ? (a < b ? b : a) : 0;
+        if (a >= n || b >= n) continue;         // the dummy column of odd n (warp-uniform)
+        const int p = a < b ? a : b, q = a < b ? b : a;
         double xp[E], xq[E];
         double ga = 0.0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          const int i = lig + GL * e;
+          const int i = lane + 32 * e;
           xp[e] = (i < n) ? X[i + p * n] : 0.0;
           xq[e] = (i < n) ? X[i + q * n] : 0.0;
           ga = fma(xp[e], xq[e], ga);
         }
-        ga = gsum(ga);
+        ga = wsum(ga);
         const double al = nrm[p], be = nrm[q];
-        if (act && ga * ga > tol2 * al * be && ga != 0.0) {
-          const double zeta = (be - al) * 0.5 * fast_rcp(ga);
-          const double az = fabs(zeta);
-          double t;
-          if (az > 1e8) t = 0.5 * fast_rcp(zeta);
-          else {
-            const double y = fma(zeta, zeta, 1.0);
-            t = copysign(fast_rcp(az + y * fast_rsqrt(y)), zeta);
-          }
-          const double c = fast_rsqrt(fma(t, t, 1.0));
-          const double s = c * t;
+        if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {   // warp-uniform
+          double c, sn, t;
+          jacobi_rotation(al, be, ga, c, sn, t);
 #pragma unroll
           for (int e = 0; e < E; ++e) {
-            const int i = lig + GL * e;
+            const int i = lane + 32 * e;
             if (i < n) {
-              X[i + p * n] = c * xp[e] - s * xq[e];
-              X[i + q * n] = s * xp[e] + c * xq[e];
+              X[i + p * n] = c * xp[e] - sn * xq[e];
+              X[i + q * n] = sn * xp[e] + c * xq[e];
               const double vp = V[i + p * n], vq = V[i + q * n];
-              V[i + p * n] = c * vp - s * vq;
-              V[i + q * n] = s * vp + c * vq;
+              V[i + p * n] = c * vp - sn * vq;
+              V[i + q * n] = sn * vp + c * vq;
             }
           }
-          if (lig == 0) {
+          if (lane == 0) {
             nrm[p] = fmax(al - t * ga, 0.0);
             nrm[q] = be + t * ga;
             rotated = 1;
@@ -345,16 +365,15 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
   }
   if (threadIdx.x == 0) jsweeps[0] = (double)(sweep + 1);
   // sigma_j = ||x_j||, then sort descending (rank sort, ties by index)
-  for (int j0 = 0; j0 < n; j0 += npg) {
-    const int j = j0 + grp;
+  for (int j = warp; j < n; j += nwarp) {
     double a = 0.0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const int i = lig + GL * e;
-      if (i < n && j < n) a = fma(X[i + j * n], X[i + j * n], a);
+      const int i = lane + 32 * e;
+      if (i < n) a = fma(X[i + j * n], X[i + j * n], a);
     }
-    a = gsum(a);
-    if (lig == 0 && j < n) sv[j] = sqrt(a);
+    a = wsum(a);
+    if (lane == 0) sv[j] = sqrt(a);
   }
   __syncthreads();
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
@@ -370,32 +389,27 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
   }
 }
 
-template <int NMAX, int GL>
+template <int NMAX>
 static int launch_jacobi_t(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
   const size_t need = 2 * (size_t)ell * ell * sizeof(double);
   const int pairs = (ell + 1) / 2;
-  const int per_warp = 32 / GL;
-  int nthr = 32 * ((pairs + per_warp - 1) / per_warp);
+  int nthr = 32 * pairs;
   if (nthr > 1024) nthr = 1024;
   if (need <= 200 * 1024) {
-    static bool set = false;
-    if (!set) {
-      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(jacobi_kernel<NMAX, GL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      set = true;
-    }
-    jacobi_kernel<NMAX, GL, true><<<1, nthr, need, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, nullptr, ctx->sc + S_JSWEEPS);
+    NYS_TRY(ensure_max_smem(ctx, (const void*)jacobi_kernel<NMAX, true>, 200 * 1024));
+    jacobi_kernel<NMAX, true><<<1, nthr, need, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, nullptr, ctx->sc + S_JSWEEPS);
   } else {
     double* gws = ctx->wsd("jacobi_ws", 2 * (size_t)ell * ell);
-    jacobi_kernel<NMAX, GL, false><<<1, nthr, 0, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, gws, ctx->sc + S_JSWEEPS);
+    jacobi_kernel<NMAX, false><<<1, nthr, 0, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, gws, ctx->sc + S_JSWEEPS);
   }
   ctx->launches++;
   return ctx->check_launch("jacobi");
 }
 
 int launch_jacobi_svd(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
-  if (ell <= 64) return launch_jacobi_t<64, 8>(ctx, ell, R, ldr, V, ldv, sigma);
-  if (ell <= 128) return launch_jacobi_t<128, 16>(ctx, ell, R, ldr, V, ldv, sigma);
-  return launch_jacobi_t<256, 32>(ctx, ell, R, ldr, V, ldv, sigma);
+  if (ell <= 64) return launch_jacobi_t<64>(ctx, ell, R, ldr, V, ldv, sigma);
+  if (ell <= 128) return launch_jacobi_t<128>(ctx, ell, R, ldr, V, ldv, sigma);
+  return launch_jacobi_t<256>(ctx, ell, R, ldr, V, ldv, sigma);
 }
 
 // lambda_hat = max{0, sigma^2 - nu}

@@ -128,6 +128,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// prefetch a contiguous global range into L2 (bulk, no completion tracking); 16-byte multiple
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -183,11 +187,17 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-// deterministic warp-level sum / min of a global array (lane-strided L2 loads, fixed xor tree)
+// deterministic warp-level sum / min of a global array (lane-strided L2 loads issued 8 at a time so
+// that a round costs one L2 latency, not eight; fixed pairwise + xor trees)
 __device__ __forceinline__ double warp_sum_array(const double* x, int n) {
   const int lane = threadIdx.x & 31;
   double a = 0.0;
-  for (int i = lane; i < n; i += 32) a += __ldcg(x + i);
+  for (int i0 = lane; i0 < n; i0 += 256) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = (i0 + 32 * u < n) ? __ldcg(x + i0 + 32 * u) : 0.0;
+    a += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
   return a;
@@ -195,7 +205,12 @@ __device__ __forceinline__ double warp_sum_array(const double* x, int n) {
 __device__ __forceinline__ double warp_min_array(const double* x, int n) {
   const int lane = threadIdx.x & 31;
   double a = 1.0e300;
-  for (int i = lane; i < n; i += 32) a = fmin(a, __ldcg(x + i));
+  for (int i0 = lane; i0 < n; i0 += 256) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = (i0 + 32 * u < n) ? __ldcg(x + i0 + 32 * u) : 1.0e300;
+    a = fmin(a, fmin(fmin(fmin(v[0], v[1]), fmin(v[2], v[3])), fmin(fmin(v[4], v[5]), fmin(v[6], v[7]))));
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
   return a;
