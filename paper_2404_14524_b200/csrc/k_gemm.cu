@@ -94,8 +94,11 @@ __global__ void __launch_bounds__(128) dgemm_kernel(const GemmParams G) {
   extern __shared__ __align__(128) double gsm[];
   double* Asm = gsm;
   double* Bsm = gsm + GST * A_STAGE;
-  const int64_t i0 = (int64_t)blockIdx.x * GBM;
-  const int64_t j0 = (int64_t)blockIdx.y * GBN;
+  // N-tiles vary fastest across the grid: the CTAs that share an A tile (the ceil(N/64) <= 4
+  // column blocks of a sketch with l <= 256) run together, so A streams from HBM once and the
+  // other reads hit L2
+  const int64_t i0 = (int64_t)blockIdx.y * GBM;
+  const int64_t j0 = (int64_t)blockIdx.x * GBN;
   const int64_t kbeg = (int64_t)blockIdx.z * G.kchunk;
   int64_t kend = kbeg + G.kchunk;
   if (kend > G.K) kend = G.K;
@@ -176,6 +179,180 @@ __global__ void __launch_bounds__(128) dgemm_kernel(const GemmParams G) {
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// N-adaptive DMMA GEMM: CTA tile 128 x (8 NT), 4 warps x 32 rows, m16n8k8 f64 MMAs (A fragment
+// rows g, g+8 / cols t, t+4; B fragment k = t, t+4, n = g; layouts checked on B200 by
+// scratch/dmma_probe.cu).  NT is picked per call so that 8 NT tiles the sketch width l with the
+// least padding (l = 200 -> NT = 5 exactly; a 64-wide tile would compute 256 columns), BK = 16,
+// 3-stage cp.async ring.  Padded smem rows: K-major leading dimension = 20 doubles (row stride 4
+// banks-of-8B mod 16 -> the minimum 2 wavefronts per fragment load), M-major = BM + 8.
+// ------------------------------------------------------------------------------------------
+constexpr int HBM_ = 128, HBK = 16, HST = 3;
+constexpr int HLD_K = HBK + 4;      // [rows][HLD_K] for K-major tiles (A when AK, and B)
+constexpr int HLD_M = HBM_ + 8;     // [HBK][HLD_M] for M-major A
+constexpr int HA_STAGE = (HBM_ * HLD_K > HBK * HLD_M) ? HBM_ * HLD_K : HBK * HLD_M;
+
+__device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+template <int NT, bool AK>
+__device__ __forceinline__ void hload_stage(const GemmParams& G, double* As, double* Bs, int64_t i0, int64_t j0,
+                                            int64_t k0, int64_t kend) {
+  const int tid = threadIdx.x;
+  // A: 128 x 16 doubles = 1024 chunks of 16 B, 8 per thread
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int ch = tid + q * 128;
+    if (AK) {
+      const int r = ch >> 3, kc = ch & 7;
+      const int64_t gi = i0 + r, gk = k0 + 2 * kc;
+      const int nb = (gi < G.M) ? clamp_bytes(kend - gk) : 0;
+      const double* src = nb ? (G.A + gi * G.lda + gk) : G.A;
+      cp_async16(As + r * HLD_K + 2 * kc, src, nb);
+    } else {
+      const int k = ch >> 6, ic = ch & 63;
+      const int64_t gi = i0 + 2 * ic, gk = k0 + k;
+      const int nb = (gk < kend) ? clamp_bytes(G.M - gi) : 0;
+      const double* src = nb ? (G.A + gi + gk * G.lda) : G.A;
+      cp_async16(As + k * HLD_M + 2 * ic, src, nb);
+    }
+  }
+  // B: (8 NT) x 16 doubles, K contiguous = 64 NT chunks
+#pragma unroll
+  for (int q = 0; q < (64 * NT + 127) / 128; ++q) {
+    const int ch = tid + q * 128;
+    if (ch < 64 * NT) {
+      const int j = ch >> 3, kc = ch & 7;
+      const int64_t gj = j0 + j, gk = k0 + 2 * kc;
+      const int nb = (gj < G.N) ? clamp_bytes(kend - gk) : 0;
+      const double* src = nb ? (G.B + gk + gj * G.ldb) : G.B;
+      cp_async16(Bs + j * HLD_K + 2 * kc, src, nb);
+    }
+  }
+}
+
+template <int NT, bool AK>
+__global__ void __launch_bounds__(128) dgemm_nt_kernel(const GemmParams G) {
+  constexpr int BN = 8 * NT;
+  constexpr int B_ST = BN * HLD_K;
+  extern __shared__ __align__(128) double gsm[];
+  double* Asm = gsm;
+  double* Bsm = gsm + HST * HA_STAGE;
+  const int64_t j0 = (int64_t)blockIdx.x * BN;      // N-tiles fastest: CTAs sharing an A tile run together
+  const int64_t i0 = (int64_t)blockIdx.y * HBM_;
+  const int64_t kbeg = (int64_t)blockIdx.z * G.kchunk;
+  int64_t kend = kbeg + G.kchunk;
+  if (kend > G.K) kend = G.K;
+  const int nk = (kend > kbeg) ? (int)((kend - kbeg + HBK - 1) / HBK) : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  double acc[2][NT][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+
+#pragma unroll
+  for (int st = 0; st < HST - 1; ++st) {
+    if (st < nk) hload_stage<NT, AK>(G, Asm + st * HA_STAGE, Bsm + st * B_ST, i0, j0, kbeg + (int64_t)st * HBK, kend);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<HST - 2>();
+    __syncthreads();
+    const int nxt = kt + HST - 1;
+    if (nxt < nk)
+      hload_stage<NT, AK>(G, Asm + (nxt % HST) * HA_STAGE, Bsm + (nxt % HST) * B_ST, i0, j0, kbeg + (int64_t)nxt * HBK,
+                          kend);
+    cp_async_commit();
+    const double* As = Asm + (kt % HST) * HA_STAGE;
+    const double* Bs = Bsm + (kt % HST) * B_ST;
+#pragma unroll
+    for (int kk = 0; kk < HBK / 8; ++kk) {
+      const int k = 8 * kk + tq;
+      double af[2][4], bf[NT][2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int r = 32 * warp + 16 * mt + gq;
+        if (AK) {
+          af[mt][0] = As[r * HLD_K + k];
+          af[mt][1] = As[(r + 8) * HLD_K + k];
+          af[mt][2] = As[r * HLD_K + k + 4];
+          af[mt][3] = As[(r + 8) * HLD_K + k + 4];
+        } else {
+          af[mt][0] = As[k * HLD_M + r];
+          af[mt][1] = As[k * HLD_M + r + 8];
+          af[mt][2] = As[(k + 4) * HLD_M + r];
+          af[mt][3] = As[(k + 4) * HLD_M + r + 8];
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        bf[nt][0] = Bs[(8 * nt + gq) * HLD_K + k];
+        bf[nt][1] = Bs[(8 * nt + gq) * HLD_K + k + 4];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma_16x8x8(acc[mt][nt], af[mt], bf[nt]);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int64_t row = i0 + 32 * warp + 16 * mt + gq + 8 * (c >> 1);
+        const int64_t col = j0 + 8 * nt + 2 * tq + (c & 1);
+        if (row < G.M && col < G.N) {
+          double v = acc[mt][nt][c];
+          if (G.partial) {
+            G.C[(size_t)blockIdx.z * G.M * G.N + row + col * G.M] = v;
+          } else {
+            if (G.row_scale) v *= G.row_scale[row];
+            if (G.addv) v += G.addv[row] * G.addm[row + col * G.ldadd];
+            G.C[row + col * G.ldc] = v;
+          }
+        }
+      }
+    }
+  }
+}
+
+typedef void (*DgemmKernel)(const GemmParams);
+template <bool AK>
+static DgemmKernel nt_kernel(int nt) {
+  switch (nt) {
+    case 1: return dgemm_nt_kernel<1, AK>;
+    case 2: return dgemm_nt_kernel<2, AK>;
+    case 3: return dgemm_nt_kernel<3, AK>;
+    case 4: return dgemm_nt_kernel<4, AK>;
+    case 5: return dgemm_nt_kernel<5, AK>;
+    case 6: return dgemm_nt_kernel<6, AK>;
+    case 7: return dgemm_nt_kernel<7, AK>;
+    default: return dgemm_nt_kernel<8, AK>;
+  }
+}
+// pick NT (1..8) minimising the padded width ceil(N / 8NT) * 8NT, ties -> larger NT
+static int pick_nt(int64_t N) {
+  int best = 8;
+  int64_t best_w = ((N + 63) / 64) * 64;
+  for (int nt = 7; nt >= 1; --nt) {
+    const int64_t w = ((N + 8 * nt - 1) / (8 * nt)) * (8 * nt);
+    if (w < best_w) { best_w = w; best = nt; }
+  }
+  return best;
+}
+
 __global__ void gemm_reduce_kernel(int64_t M, int64_t N, int splits, const double* P, double* C, int64_t ldc,
                                    const double* row_scale, const double* addv, const double* addm, int64_t ldadd) {
   const int64_t total = M * N;
@@ -189,17 +366,66 @@ __global__ void gemm_reduce_kernel(int64_t M, int64_t N, int splits, const doubl
   }
 }
 
+static int launch_gemm_old(nys_ctx* ctx, const GemmCall& g);
+
 int launch_gemm(nys_ctx* ctx, const GemmCall& g) {
   if (g.M <= 0 || g.N <= 0) return NYS_OK;
-  const size_t smem = (size_t)GST * (A_STAGE + B_STAGE) * sizeof(double);
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[g.a_kmajor ? 1 : 0]) {
-    if (g.a_kmajor)
-      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(dgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    else
-      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(dgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set[g.a_kmajor ? 1 : 0] = true;
+  // the 128-row kernel pays off on tall products (the sketch at large n or m); short-M products
+  // (split-K Gram / Y = A T at small m) keep the 64 x 64 kernel (measured on B200)
+  if (g.M < 2048 || g.K < 512 || getenv("NYS_GEMM_OLD")) return launch_gemm_old(ctx, g);
+  const int NT = pick_nt(g.N);
+  const int BN = 8 * NT;
+  const size_t smem = (size_t)HST * (HA_STAGE + BN * HLD_K) * sizeof(double);
+  DgemmKernel k = g.a_kmajor ? nt_kernel<true>(NT) : nt_kernel<false>(NT);
+  NYS_TRY(ensure_max_smem(ctx, (const void*)k, smem));
+  const int64_t mt = (g.M + HBM_ - 1) / HBM_, nt = (g.N + BN - 1) / BN;
+  const int64_t kslabs = (g.K + HBK - 1) / HBK;
+  int splits = g.splits;
+  if (splits <= 0) {
+    const int64_t target = 2LL * ctx->num_sms;
+    int64_t sp = (target + mt * nt - 1) / (mt * nt);
+    const int64_t smax = kslabs / 8 > 0 ? kslabs / 8 : 1;
+    if (sp > smax) sp = smax;
+    if (sp < 1) sp = 1;
+    if (sp > 256) sp = 256;
+    splits = (int)sp;
   }
+  int64_t kchunk = (g.K + splits - 1) / splits;
+  kchunk = ((kchunk + HBK - 1) / HBK) * HBK;
+  if (kchunk < HBK) kchunk = HBK;
+  splits = (int)((g.K + kchunk - 1) / kchunk);
+  if (splits < 1) splits = 1;
+  GemmParams P{};
+  P.M = g.M; P.N = g.N; P.K = g.K; P.A = g.A; P.lda = g.lda; P.B = g.B; P.ldb = g.ldb;
+  P.row_scale = g.row_scale; P.addv = g.addv; P.addm = g.addm; P.ldadd = g.ldadd; P.kchunk = kchunk;
+  double* part = nullptr;
+  if (splits > 1) {
+    part = ctx->wsd("gemm_part", (size_t)splits * g.M * g.N);
+    P.C = part; P.ldc = g.M; P.partial = 1;
+  } else {
+    P.C = g.C; P.ldc = g.ldc; P.partial = 0;
+  }
+  if (mt > 65535) { ctx->set_error("dgemm: M too large for the grid"); return NYS_EINVAL; }
+  dim3 grid((unsigned)nt, (unsigned)mt, (unsigned)splits);
+  k<<<grid, 128, smem, ctx->stream>>>(P);
+  ctx->launches++;
+  NYS_TRY(ctx->check_launch("dgemm"));
+  if (splits > 1) {
+    int64_t tot = g.M * g.N;
+    int rg = (int)((tot + 255) / 256);
+    if (rg > 4 * ctx->num_sms) rg = 4 * ctx->num_sms;
+    gemm_reduce_kernel<<<rg, 256, 0, ctx->stream>>>(g.M, g.N, splits, part, g.C, g.ldc, g.row_scale, g.addv, g.addm,
+                                                     g.ldadd);
+    ctx->launches++;
+    NYS_TRY(ctx->check_launch("gemm_reduce"));
+  }
+  return NYS_OK;
+}
+
+static int launch_gemm_old(nys_ctx* ctx, const GemmCall& g) {
+  const size_t smem = (size_t)GST * (A_STAGE + B_STAGE) * sizeof(double);
+  if (g.a_kmajor) NYS_TRY(ensure_max_smem(ctx, (const void*)dgemm_kernel<true>, smem));
+  else NYS_TRY(ensure_max_smem(ctx, (const void*)dgemm_kernel<false>, smem));
   const int64_t mt = (g.M + GBM - 1) / GBM, nt = (g.N + GBN - 1) / GBN;
   const int64_t kslabs = (g.K + GBK - 1) / GBK;
   int splits = g.splits;
@@ -227,7 +453,8 @@ int launch_gemm(nys_ctx* ctx, const GemmCall& g) {
   } else {
     P.C = g.C; P.ldc = g.ldc; P.partial = 0;
   }
-  dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)splits);
+  if (mt > 65535) { ctx->set_error("dgemm: M too large for the grid"); return NYS_EINVAL; }
+  dim3 grid((unsigned)nt, (unsigned)mt, (unsigned)splits);
   if (g.K <= 0) {
     // empty contraction: C = 0 (+ add)
     NYS_CUDA_TRY(ctx, cudaMemsetAsync(part ? part : g.C, 0, 0, ctx->stream));

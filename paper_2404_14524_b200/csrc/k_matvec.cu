@@ -24,6 +24,124 @@
 
 namespace nys {
 
+// ------------------------------------------------------------------------------------------
+// finalize: out_i = sgn * sum_k Wp[k][i] + (delta + e_i) v_i + add_i ; optional PCG dot
+// ------------------------------------------------------------------------------------------
+struct FinParams {
+  const double* Wp;
+  int64_t wp_ld;
+  int nparts;
+  int64_t m;
+  double sgn;
+  double delta;
+  int use_delta;
+  const double* e;
+  const double* v;      // operand vector (p for PCG)
+  const double* add;
+  double* out;
+  int pcg_alpha;
+  double* sc;           // scalar slots
+  double* part;         // per-block partials (pcg dot)
+  unsigned int* counter;
+  const double* done;
+};
+
+// 16 rows x 16 partial groups per 256 threads (tid < 256); fixed summation order (deterministic).
+// Row blocks b, b + nb, ... of 16 rows; the partial rows are read through L2 (they may have been
+// written by other CTAs of the same launch).  Then the optional PCG dot (last-block pattern).
+__device__ __forceinline__ void fin_rows(const FinParams& F, int b, int nb, double (*red)[17], double* sred,
+                                         bool* am_last) {
+  const int tid = threadIdx.x, row = tid & 15, grp = (tid >> 4) & 15;
+  const bool act = tid < 256;
+  double dot = 0.0;
+  for (int64_t i0 = (int64_t)b * 16; i0 < F.m; i0 += (int64_t)nb * 16) {
+    const int64_t i = i0 + row;
+    if (act) {
+      double acc = 0.0;
+      if (i < F.m) {
+        for (int k0 = grp; k0 < F.nparts; k0 += 128) {  // 8 independent L2 loads per round
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int k = k0 + 16 * u;
+            v[u] = (k < F.nparts) ? __ldcg(F.Wp + (size_t)k * F.wp_ld + i) : 0.0;
+          }
+          acc += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+        }
+      }
+      red[row][grp] = acc;
+    }
+    __syncthreads();
+    if (tid < 16 && i < F.m) {
+      const double* v = red[row];
+      double s = (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
+                 (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
+      s *= F.sgn;
+      const double vi = (F.use_delta || F.pcg_alpha) ? __ldcg(F.v + i) : 0.0;  // may be p_out of this launch
+      if (F.use_delta) s += (F.delta + (F.e ? F.e[i] : 0.0)) * vi;
+      if (F.add) s += F.add[i];
+      F.out[i] = s;
+      if (F.pcg_alpha) dot = fma(vi, s, dot);
+    }
+    __syncthreads();
+  }
+  if (!F.pcg_alpha) return;
+  dot = warp_sum(dot);
+  if (act && (tid & 31) == 0) sred[tid >> 5] = dot;
+  __syncthreads();
+  if (tid == 0) {
+    double bs = 0.0;
+    for (int w = 0; w < 8; ++w) bs += sred[w];
+    F.part[b] = bs;
+    __threadfence();
+    const unsigned prev = atomicAdd(F.counter, 1u);
+    *am_last = (prev == (unsigned)nb - 1);
+  }
+  __syncthreads();
+  if (*am_last && warp_uniform_id() == 0) {
+    __threadfence();
+    const double pw = warp_sum_array(F.part, nb);
+    if (tid != 0) return;
+    *F.counter = 0u;
+    F.sc[S_PW] = pw;
+    if (!(pw > 0.0) || !isfinite(pw)) {
+      F.sc[S_STATUS] = (double)NYS_EBREAKDOWN;
+      F.sc[S_DONE] = 1.0;
+      F.sc[S_ALPHA] = 0.0;
+    } else {
+      F.sc[S_ALPHA] = F.sc[S_RZ] / pw;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) mv_finalize(const FinParams F) {
+  if (F.done != nullptr && *F.done != 0.0) return;
+  __shared__ double red[16][17];
+  __shared__ double sred[8];
+  __shared__ bool am_last;
+  fin_rows(F, blockIdx.x, gridDim.x, red, sred, &am_last);
+}
+
+// self-resetting grid barrier (count, generation); the launch is cooperative (all CTAs resident)
+__device__ __forceinline__ void mv_grid_sync(unsigned int* bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicExch(bar + 1, g + 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 struct MatvecParams {
   const double* A;
   int64_t lda, m, n;
@@ -50,6 +168,9 @@ struct MatvecParams {
   double delta;
   const double* e;
   double* tbuf;         // TONLY: raw column dots (A^T v)_j, epilogue applied after the loop
+  int fuse_fin;         // cl == 1, rc == 1: finalize in-kernel after a grid barrier (cooperative launch)
+  FinParams fin;
+  unsigned int* gbar;   // [2] grid barrier (count, generation)
 };
 
 __device__ __forceinline__ void t_epilogue(const MatvecParams& P, int64_t j, double s) {
@@ -470,95 +591,17 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
       }
     }
   }
+  if (!CLU && MODE != MV_TONLY && P.fuse_fin) {
+    // every partial row is complete after the grid barrier; this CTA finalizes its row blocks
+    __shared__ double fred[16][17];
+    __shared__ double fsred[8];
+    __shared__ bool fam_last;
+    mv_grid_sync(P.gbar, gridDim.x);
+    fin_rows(P.fin, blockIdx.x, gridDim.x, fred, fsred, &fam_last);
+  }
   if (cl > 1) {
     __syncwarp();
     cluster_sync_all();
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// finalize: out_i = sgn * sum_k Wp[k][i] + (delta + e_i) v_i + add_i ; optional PCG dot
-// ------------------------------------------------------------------------------------------
-struct FinParams {
-  const double* Wp;
-  int64_t wp_ld;
-  int nparts;
-  int64_t m;
-  double sgn;
-  double delta;
-  int use_delta;
-  const double* e;
-  const double* v;      // operand vector (p for PCG)
-  const double* add;
-  double* out;
-  int pcg_alpha;
-  double* sc;           // scalar slots
-  double* part;         // per-block partials (pcg dot)
-  unsigned int* counter;
-  const double* done;
-};
-
-// 16 rows x 16 partial groups per 256-thread block; fixed summation order (deterministic)
-__global__ void __launch_bounds__(256) mv_finalize(const FinParams F) {
-  if (F.done != nullptr && *F.done != 0.0) return;
-  __shared__ double red[16][17];
-  __shared__ double sred[8];
-  __shared__ bool am_last;
-  const int tid = threadIdx.x, row = tid & 15, grp = tid >> 4;
-  double dot = 0.0;
-  for (int64_t i0 = (int64_t)blockIdx.x * 16; i0 < F.m; i0 += (int64_t)gridDim.x * 16) {
-    const int64_t i = i0 + row;
-    double acc = 0.0;
-    if (i < F.m) {
-      double a1 = 0.0;
-      int k = grp;
-      for (; k + 16 < F.nparts; k += 32) {
-        acc += F.Wp[(size_t)k * F.wp_ld + i];
-        a1 += F.Wp[(size_t)(k + 16) * F.wp_ld + i];
-      }
-      if (k < F.nparts) acc += F.Wp[(size_t)k * F.wp_ld + i];
-      acc += a1;
-    }
-    red[row][grp] = acc;
-    __syncthreads();
-    if (tid < 16 && i < F.m) {
-      const double* v = red[row];
-      double s = (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
-                 (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
-      s *= F.sgn;
-      if (F.use_delta) s += (F.delta + (F.e ? F.e[i] : 0.0)) * F.v[i];
-      if (F.add) s += F.add[i];
-      F.out[i] = s;
-      if (F.pcg_alpha) dot = fma(F.v[i], s, dot);
-    }
-    __syncthreads();
-  }
-  if (!F.pcg_alpha) return;
-  dot = warp_sum(dot);
-  if ((tid & 31) == 0) sred[tid >> 5] = dot;
-  __syncthreads();
-  if (tid == 0) {
-    double b = 0.0;
-    for (int w = 0; w < 8; ++w) b += sred[w];
-    F.part[blockIdx.x] = b;
-    __threadfence();
-    const unsigned prev = atomicAdd(F.counter, 1u);
-    am_last = (prev == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (am_last && warp_uniform_id() == 0) {
-    __threadfence();
-    const double pw = warp_sum_array(F.part, gridDim.x);
-    if (tid != 0) return;
-    *F.counter = 0u;
-    F.sc[S_PW] = pw;
-    if (!(pw > 0.0) || !isfinite(pw)) {
-      F.sc[S_STATUS] = (double)NYS_EBREAKDOWN;
-      F.sc[S_DONE] = 1.0;
-      F.sc[S_ALPHA] = 0.0;
-    } else {
-      F.sc[S_ALPHA] = F.sc[S_RZ] / pw;
-    }
   }
 }
 
@@ -820,6 +863,29 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
   double* pwp = nullptr;
   if (c.mode == MV_FUSED && c.pcg_fused) pwp = ctx->wsd("mv_pwp", (size_t)pl.grid);
   double* tbuf = (c.mode == MV_TONLY) ? ctx->wsd("mv_tbuf", (size_t)(c.n > 0 ? c.n : 1)) : nullptr;
+  // finalize parameters (used in-kernel when fusable, else by mv_finalize)
+  FinParams F{};
+  int fgrid = (int)((c.m + 15) / 16);
+  if (fgrid > 2 * ctx->num_sms) fgrid = 2 * ctx->num_sms;
+  const bool want_fin = c.mode != MV_TONLY && !c.pcg_fused && c.out != nullptr;
+  const bool fuse = want_fin && c.n > 0 && pl.cl == 1 && pl.rc == 1 && getenv("NYS_FUSED_FIN") != nullptr;
+  // (measured on B200, m = 2000: the in-kernel grid barrier costs what the separate finalize
+  //  launch does inside a CUDA graph, so the fused variant is opt-in)
+  if (want_fin) {
+    F.Wp = Wp; F.wp_ld = wp_ld; F.nparts = pl.nparts; F.m = c.m; F.sgn = c.sgn;
+    F.delta = c.delta; F.use_delta = c.use_delta ? 1 : 0; F.e = c.e;
+    F.v = (c.p_out != nullptr) ? c.p_out : c.z;
+    F.add = c.add; F.out = c.out; F.pcg_alpha = c.pcg_alpha ? 1 : 0; F.sc = ctx->sc;
+    F.counter = ctx->counters + 0;
+    F.done = c.done;
+    F.part = ctx->wsd("fin_part", (size_t)(fuse ? pl.grid : fgrid));
+  }
+  unsigned int* gbar = nullptr;
+  if (fuse) {
+    const bool fresh = ctx->bufs.find("mv_gbar") == ctx->bufs.end();
+    gbar = (unsigned int*)ctx->ws("mv_gbar", 64);
+    if (fresh) NYS_CUDA_TRY(ctx, cudaMemsetAsync(gbar, 0, 64, ctx->stream));
+  }
   if (c.n > 0 || c.mode == MV_TONLY) {
     MatvecParams P{};
     P.A = c.A; P.lda = c.lda; P.m = c.m; P.n = c.n;
@@ -829,6 +895,9 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
     P.done = c.done; P.rs = pl.rs; P.npanels = pl.npanels; P.stages = pl.stages; P.cl = pl.cl;
     P.pwp = pwp; P.delta = c.delta; P.e = c.e; P.tbuf = tbuf; P.rc = pl.rc;
     P.delta_slot = c.delta_from_slot ? ctx->sc + S_DELTA : nullptr;
+    P.fuse_fin = fuse ? 1 : 0;
+    P.fin = F;
+    P.gbar = gbar;
     MvKernel k = (c.mode == MV_FUSED) ? kernel_for<MV_FUSED>(pl.cfg, pl.cl > 1) : (c.mode == MV_TONLY) ? kernel_for<MV_TONLY>(pl.cfg, pl.cl > 1) : kernel_for<MV_NONLY>(pl.cfg, pl.cl > 1);
     if (c.n > 0) {
       cudaLaunchConfig_t cfg = {};
@@ -837,10 +906,15 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
       cfg.dynamicSmemBytes = pl.smem;
       cfg.stream = ctx->stream;
       cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = pl.cdim;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
+      if (fuse) {  // grid barrier inside: all CTAs must be co-resident
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+      } else {
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = pl.cdim;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+      }
       cfg.attrs = at;
       cfg.numAttrs = 1;
       NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, P));
@@ -859,17 +933,7 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
     }
     return NYS_OK;
   }
-  if (c.out == nullptr) return NYS_OK;
-  FinParams F{};
-  F.Wp = Wp; F.wp_ld = wp_ld; F.nparts = pl.nparts; F.m = c.m; F.sgn = c.sgn;
-  F.delta = c.delta; F.use_delta = c.use_delta ? 1 : 0; F.e = c.e;
-  F.v = (c.p_out != nullptr) ? c.p_out : c.z;
-  F.add = c.add; F.out = c.out; F.pcg_alpha = c.pcg_alpha ? 1 : 0; F.sc = ctx->sc;
-  F.counter = ctx->counters + 0;
-  F.done = c.done;
-  int fgrid = (int)((c.m + 15) / 16);
-  if (fgrid > 2 * ctx->num_sms) fgrid = 2 * ctx->num_sms;
-  F.part = ctx->wsd("fin_part", (size_t)fgrid);
+  if (!want_fin || fuse) return NYS_OK;
   mv_finalize<<<fgrid, 256, 0, ctx->stream>>>(F);
   ctx->launches++;
   return ctx->check_launch("mv_finalize");
