@@ -33,6 +33,9 @@ METRIC = "fp64 A·D·Aᵀv matvec GB/s (% HBM peak) and Nys-IP-PMM time-to-1e-8 
 # dram__bytes_read.sum + dram__bytes_write.sum per fused-matvec launch from `ncu --set full`
 # (profiles/, per config and shape); None until captured for that config
 TRAFFIC = {1: 134.6e6}
+# persistent PCG kernel, dram__bytes_read.sum + dram__bytes_write.sum per ITERATION (ncu --set full of
+# a 20-iteration launch, config 1: 2.535 GB + 20.9 MB; profiles/r01_pcg_persistent_cfg1_20it_full.ncu-rep)
+PCG_TRAFFIC_PER_IT = {1: 127.8e6}
 
 
 def _peaks():
@@ -397,7 +400,8 @@ def main():
         it_bytes = mv_bytes + 16.0 * m * ell + 80.0 * m
         pcg_gbs = info.iters * it_bytes / t_call / 1e9
         pcg_roof = {"bound": "hbm", "achieved": pcg_gbs, "peak": hbm, "unit": "GB/s", "frac": pcg_gbs / hbm,
-                    "traffic": None, "kernel": "pcg_persistent_kernel (whole PCG solve in one cooperative launch)",
+                    "traffic": (PCG_TRAFFIC_PER_IT[args.config] * info.iters) if args.config in PCG_TRAFFIC_PER_IT else None,
+                    "kernel": "pcg_persistent_kernel (whole PCG solve in one cooperative launch)",
                     "peak_source": peak_src, "iterations_per_launch": info.iters,
                     "bytes_per_iteration": it_bytes, "launch_us": t_call * 1e6, "us_per_iteration": t_call / info.iters * 1e6,
                     "share_of_step": (last["t_pcg_ms"] / 1e3) / sec_per_solve}

@@ -49,6 +49,7 @@ struct PcgPParams {
   int max_iter;
   int stages;
   int l2_prefetch;            // panels prefetched into L2 ahead of the smem ring
+  int l2_keep;                // panels per CTA copied with evict_last (L2-resident across iterations)
   unsigned long long* trace;  // debug (NYS_PCG_TRACE): [2 CTAs][32 iters][8] globaltimer stamps
   int64_t npanels;
   int64_t rows_per_cta;
@@ -122,7 +123,11 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     // ---------------- producer warp: stream this CTA's panels, iteration after iteration ------
     long long q = 0;
     if (lane == 0 && niter > 0) {
-      const uint64_t pol = l2_evict_first_policy();
+      const uint64_t pol_stream = l2_evict_first_policy();
+      // the first `l2_keep` panels of this CTA's set are re-read every iteration from L2: they are
+      // copied with evict_last so that they stay resident across iterations (A is about L2-sized
+      // at the small configs); the rest streams with evict_first
+      const uint64_t pol_keep = l2_evict_last_policy();
       // L2 prefetch runs PF panels ahead of the smem ring: the reduction / barrier phases of an
       // iteration leave HBM idle, so the next matvec's panels are pulled into L2 meanwhile
       long long pf = 0;
@@ -158,7 +163,8 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
         ncols = ncols > BN ? BN : ncols;
         mbar_arrive_expect_tx(&full[s], (uint32_t)ncols * copy_bytes);
         for (int c = 0; c < ncols; ++c)
-          bulk_g2s(stage + ((size_t)s * BN + c) * rs, P.A + (col0 + c) * P.lda, copy_bytes, &full[s], pol);
+          bulk_g2s(stage + ((size_t)s * BN + c) * rs, P.A + (col0 + c) * P.lda, copy_bytes, &full[s],
+                   it < P.l2_keep ? pol_keep : pol_stream);
         ++q;
       }
       s_issued = q;
@@ -626,8 +632,13 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
     int pfd = (int)(60e6 / (panel_bytes * (double)G));
     if (pfd > 64) pfd = 64;
     if (pfd < 0) pfd = 0;
+    pfd = 0;  // measured on B200 (config 1): no gain from L2 prefetch or evict_last residency -> off
+    (void)pfd;
     if (const char* e = getenv("NYS_PCG_PF")) pfd = atoi(e);
     P.l2_prefetch = pfd;
+    int keep = 0;
+    if (const char* e = getenv("NYS_PCG_KEEP")) keep = atoi(e);
+    P.l2_keep = keep;
   }
   NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.bar, 0, 64 + 66 * 4, ctx->stream));
   cudaLaunchConfig_t cfg = {};
