@@ -1,0 +1,118 @@
+"""BASELINE.json configs[4] at FULL per-GPU size (m = 50000, n = 50000 columns = the one-GPU slice of
+SURVEY A25, 20 GB of A), in the launch configuration bench.py --config 4 times (same m, n, lda).
+
+The oracle cannot run this solve (days of CPU time), so parity is checked on sampled
+outputs and on properties that hold at any size:
+  * the device-generated instance is the documented recipe (sampled columns regenerated on the host
+    by the same counter-based generator);
+  * the fused normal matvec against the oracle's definition, evaluated on the host over column
+    blocks (N = sum_j d_j a_j a_j^T is a sum over columns), normwise <= 1e-12;
+  * sampled sketch columns Y[:, j] = N omega_j against the oracle, normwise <= 1e-12;
+  * the Nystrom factors: U^T U = I (1e-12) and N_hat <= N on random vectors (P:1075 ordering);
+  * a capped Nys-IP-PMM run: the residual norms the GPU reports agree with a host recomputation
+    from the returned x, y, z.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import linops  # noqa: E402
+from synth import large  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+M, N, ELL = large.FULL_M, large.SLICE_N, large.ELL
+
+
+@pytest.fixture(scope="module")
+def setup():
+    from paper_2404_14524_b200 import Context
+    st = torch.cuda.Stream()
+    ctx = Context(0, stream=st)
+    sh = large.generate_shard(M, N, 0, N, n_gen=large.FULL_N, device="cuda")
+    torch.cuda.synchronize()
+    At_host = sh.At[:, :M].cpu().numpy()          # (n, m) = A^T, row-major
+    yield ctx, st, sh, At_host
+    ctx.close()
+
+
+def _host_normal_matvec(At_host, d, v, delta, blk=5000):
+    """oracle normal matvec as a sum over column blocks: sum_b A_b (d_b o (A_b^T v)) + delta v."""
+    w = np.zeros(At_host.shape[1])
+    for j0 in range(0, At_host.shape[0], blk):
+        Ab = At_host[j0:j0 + blk].T
+        w += linops.normal_matvec(Ab, d[j0:j0 + blk], v, 0.0)
+    return w + delta * v
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def test_config4_instance_is_the_recipe(setup):
+    _, _, sh, At_host = setup
+    for j in (0, 1, 12345, N - 1):
+        col = large.generate_shard(M, N, j, j + 1, n_gen=large.FULL_N, device="cpu").At[0, :M].numpy()
+        assert _rel(At_host[j], col) <= 1e-13
+    b_host = At_host.T @ sh.x0.cpu().numpy()
+    assert _rel(sh.b_part.cpu().numpy(), b_host) <= 1e-13
+
+
+def test_config4_normal_matvec_full(setup):
+    ctx, st, sh, At_host = setup
+    rs = np.random.default_rng(44)
+    d = rs.uniform(0.01, 3.0, N)
+    v = rs.standard_normal(M)
+    w = torch.empty(M, dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(st):
+        ctx.nys_normal_matvec(sh.At, sh.lda, M, torch.from_numpy(d).cuda(), None, 0.37, torch.from_numpy(v).cuda(), w)
+    torch.cuda.synchronize()
+    ref = _host_normal_matvec(At_host, d, v, 0.37)
+    assert _rel(w.cpu().numpy(), ref) <= 1e-12
+
+
+def test_config4_sketch_sampled_columns_and_factors(setup):
+    ctx, st, sh, At_host = setup
+    rs = np.random.default_rng(45)
+    d = rs.uniform(0.01, 3.0, N)
+    dd = torch.from_numpy(d).cuda()
+    Om = torch.empty((ELL, M), dtype=torch.float64, device="cuda")
+    Y = torch.empty((ELL, M), dtype=torch.float64, device="cuda")
+    U = torch.empty((ELL, M), dtype=torch.float64, device="cuda")
+    lam = torch.empty(ELL, dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(st):
+        ctx.nys_gaussian(M, ELL, 4, 1, Om)
+        ctx.nys_sketch_apply(sh.At, sh.lda, M, dd, None, ELL, Om, Y)
+        info = ctx.nys_sketch(sh.At, sh.lda, M, dd, None, 1e-3, ELL, Om, U, lam)
+    torch.cuda.synchronize()
+    Omh, Yh = Om.cpu().numpy(), Y.cpu().numpy()
+    for j in (0, 77, ELL - 1):   # Y[:, j] = N omega_j (A1: no delta)
+        ref = _host_normal_matvec(At_host, d, Omh[j], 0.0)
+        assert _rel(Yh[j], ref) <= 1e-12
+    Uh, lh = U.cpu().numpy(), lam.cpu().numpy()
+    assert np.abs(Uh @ Uh.T - np.eye(ELL)).max() <= 1e-12
+    assert info.orth_err <= 1e-12
+    assert np.all(lh >= 0) and np.all(np.diff(lh) <= 0)
+    # N_hat = U diag(lam) U^T <= N: v^T N v >= v^T N_hat v on random vectors
+    for k in range(2):
+        v = rs.standard_normal(M)
+        nv = v @ _host_normal_matvec(At_host, d, v, 0.0)
+        nhv = np.sum(lh * (Uh @ v) ** 2)
+        assert nhv <= nv * (1 + 1e-12)
+
+
+def test_config4_capped_solve_residuals_match_host(setup):
+    ctx, st, sh, At_host = setup
+    with torch.cuda.stream(st):
+        g = ctx.nys_ipppmm_solve(sh.At, sh.lda, M, sh.q, sh.b_part, sh.c, ell=ELL, max_outer=3)
+    torch.cuda.synchronize()
+    assert g["status"] in (0, -5) and g["outer"] == 3
+    x, y, z = (t.cpu().numpy() for t in (g["x"], g["y"], g["z"]))
+    q, b, c = sh.q.cpu().numpy(), sh.b_part.cpu().numpy(), sh.c.cpu().numpy()
+    assert x.min() > 0 and z.min() > 0
+    rel_p = np.linalg.norm(b - At_host.T @ x) / (1 + np.linalg.norm(b))
+    rel_d = np.linalg.norm(c + q * x - At_host @ y - z) / (1 + np.linalg.norm(c))
+    assert abs(rel_p - g["rel_p"]) <= 1e-6 * rel_p + 1e-14
+    assert abs(rel_d - g["rel_d"]) <= 1e-6 * rel_d + 1e-14
+    assert abs(x @ z / N - g["mu"]) <= 1e-10 * (x @ z / N)
