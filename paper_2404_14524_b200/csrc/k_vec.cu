@@ -316,18 +316,15 @@ struct PcgUpdArgs {
   double* part;         // (1 + ell) x grid
   unsigned int* counter;
   int max_iter;
-  int nsub;             // 64-row chunks per block
+  int64_t rows_per_block;
 };
 
-constexpr int PCG_RB = 16;             // rows per chunk
-constexpr int PCG_NG = 256 / PCG_RB;   // partial groups per row (16)
-constexpr int PCG_MAXCW = 16;          // max columns per half-warp (ell <= 256 with 16 half-warps)
-
-__device__ __forceinline__ double sum16(const double* v) {  // fixed pairwise tree
-  return (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
-         (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
-}
-
+// Row-parallel update: a block owns `rows_per_block` consecutive rows, one row per thread per
+// 256-row tile (no serial 16-row chunks).  w_i sums the matvec's partial rows with independent
+// L2 loads; U^T r partials: for every column a warp reduces its 32 rows with shuffles and
+// accumulates in its own shared-memory row (tile after tile), then the 8 warp rows are summed in
+// a fixed order -> one (1 + ell)-row of block partials.  pcg_hred_kernel (one block per column)
+// finishes the reduction: rr, the convergence test, h = s o (U^T r).
 __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
   if (A.cond != 0ull && blockIdx.x == 0 && threadIdx.x == 0) A.sc[S_GITER] += 1.0;  // launch accounting
   if (A.sc[S_DONE] != 0.0) {  // converged / max_iter / breakdown: end the graph-resident loop
@@ -335,21 +332,16 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
     return;
   }
   const double delta = A.delta_slot ? A.sc[S_DELTA] : A.delta;
-  __shared__ double red[PCG_RB][PCG_NG + 1];
-  __shared__ double rsh[PCG_RB];
+  __shared__ double wred[8][257];   // [warp][1 + c] : rr and U^T r partials of this block
+  __shared__ double rsh[256];
   __shared__ double s_alpha;
   __shared__ int s_ok;
   const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31;
   if (!A.init) {
     if (warp == 0) {
       double pw;
-      if (A.w != nullptr) {
-        pw = A.sc[S_PW];
-      } else {
-        double acc = 0.0;
-        for (int b = lane; b < A.npw; b += 32) acc += A.pwp[b];
-        pw = warp_sum(acc);
-      }
+      if (A.w != nullptr) pw = A.sc[S_PW];
+      else pw = warp_sum_array(A.pwp, A.npw);
       if (lane == 0) {
         const bool ok = (pw > 0.0) && isfinite(pw);
         s_ok = ok ? 1 : 0;
@@ -360,117 +352,132 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
         }
       }
     }
-    __syncthreads();
-    if (!s_ok) {
-      if (blockIdx.x == 0 && tid == 0) { A.sc[S_STATUS] = (double)NYS_EBREAKDOWN; A.sc[S_DONE] = 1.0; }
-      return;
-    }
+  }
+  const int ncol = 1 + A.ell;
+  for (int c = lane; c < ncol; c += 32) wred[warp][c] = 0.0;
+  __syncthreads();
+  if (!A.init && !s_ok) {
+    if (blockIdx.x == 0 && tid == 0) { A.sc[S_STATUS] = (double)NYS_EBREAKDOWN; A.sc[S_DONE] = 1.0; }
+    return;
   }
   const double alpha = A.init ? 0.0 : s_alpha;
-  double gacc[PCG_MAXCW];
-#pragma unroll
-  for (int k = 0; k < PCG_MAXCW; ++k) gacc[k] = 0.0;
-  double rr = 0.0;
-  const int row = tid % PCG_RB, grp = tid / PCG_RB;
-  const int hrow = lane & 15, hw = 2 * warp + (lane >> 4);  // half-warp id 0..15
-  for (int sub = 0; sub < A.nsub; ++sub) {
-    const int64_t i0 = ((int64_t)blockIdx.x * A.nsub + sub) * PCG_RB;
-    if (i0 >= A.m) break;
-    const int64_t i = i0 + row;
-    if (!A.init && A.w == nullptr) {
-      double acc = 0.0;
-      if (i < A.m) {
-        double a1 = 0.0;
-        int c = grp;
-        for (; c + PCG_NG < A.nparts; c += 2 * PCG_NG) {
-          acc += A.Wp[(size_t)c * A.wp_ld + i];
-          a1 += A.Wp[(size_t)(c + PCG_NG) * A.wp_ld + i];
-        }
-        if (c < A.nparts) acc += A.Wp[(size_t)c * A.wp_ld + i];
-        acc += a1;
-      }
-      red[row][grp] = acc;
-    }
-    __syncthreads();
-    if (tid < PCG_RB) {
-      double ri = 0.0;
-      if (i < A.m) {
-        if (A.init) {
-          ri = A.rhs[i];
-          A.x[i] = 0.0;
+  const int64_t lo = (int64_t)blockIdx.x * A.rows_per_block;
+  int64_t hi = lo + A.rows_per_block;
+  if (hi > A.m) hi = A.m;
+  for (int64_t t0 = lo; t0 < hi; t0 += 256) {
+    const int64_t i = t0 + tid;
+    double ri = 0.0;
+    if (i < hi) {
+      if (A.init) {
+        ri = A.rhs[i];
+        A.x[i] = 0.0;
+      } else {
+        const double pi = A.p[i];
+        double wi;
+        if (A.w != nullptr) {
+          wi = A.w[i];
         } else {
-          const double pi = A.p[i];
-          double wi;
-          if (A.w != nullptr) wi = A.w[i];
-          else wi = sum16(red[row]) + (delta + (A.e ? A.e[i] : 0.0)) * pi;
-          A.x[i] = fma(alpha, pi, A.x[i]);
-          ri = fma(-alpha, wi, A.r[i]);
-        }
-        A.r[i] = ri;
-      }
-      rsh[row] = ri;
-      rr = fma(ri, ri, rr);
-    }
-    __syncthreads();
-    // U^T r partial over this chunk: half-warp hw owns columns hw, hw+16, ...
+          double acc = 0.0;
+          for (int c0 = 0; c0 < A.nparts; c0 += 8) {   // 8 independent L2 loads per round
+            double v[8];
 #pragma unroll
-    for (int k = 0; k < PCG_MAXCW; ++k) {
-      const int c = hw + 16 * k;
-      if (c < A.ell && i0 + hrow < A.m) gacc[k] = fma(A.U[(size_t)c * A.ldu + i0 + hrow], rsh[hrow], gacc[k]);
+            for (int u = 0; u < 8; ++u) v[u] = (c0 + u < A.nparts) ? __ldcg(A.Wp + (size_t)(c0 + u) * A.wp_ld + i) : 0.0;
+            acc += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+          }
+          wi = acc + (delta + (A.e ? A.e[i] : 0.0)) * pi;
+        }
+        A.x[i] = fma(alpha, pi, A.x[i]);
+        ri = fma(-alpha, wi, A.r[i]);
+      }
+      A.r[i] = ri;
+    }
+    // rr: this warp's 32 rows
+    const double rrw = warp_sum(ri * ri);
+    if (lane == 0) wred[warp][0] += rrw;
+    rsh[tid] = ri;  // rows past hi hold 0
+    __syncthreads();
+    // U^T r with U stored ROW-major (Ut[i][c], row stride ldu): warp w takes tile rows w, w+8, ...;
+    // lane L accumulates columns L, L+32, ... (contiguous 256-B reads of each row, no shuffles)
+    {
+      double gacc[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) gacc[k] = 0.0;
+      const int tile_rows = (int)((hi - t0) < 256 ? (hi - t0) : 256);
+      for (int rr0 = warp; rr0 < tile_rows; rr0 += 32) {
+        double uv[4][8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int row = rr0 + 8 * q;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int c = lane + 32 * k;
+            uv[q][k] = (row < tile_rows && c < A.ell) ? A.U[(size_t)(t0 + row) * A.ldu + c] : 0.0;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int row = rr0 + 8 * q;
+          const double rv = (row < tile_rows) ? rsh[row] : 0.0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) gacc[k] = fma(uv[q][k], rv, gacc[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int c = lane + 32 * k;
+        if (c < A.ell) wred[warp][1 + c] += gacc[k];
+      }
     }
     __syncthreads();
   }
-  double v[1] = {rr};
-  block_sum_to_part<1>(v, A.part, gridDim.x);
-#pragma unroll
-  for (int k = 0; k < PCG_MAXCW; ++k) {
-    const int c = hw + 16 * k;
-    if (16 * k < A.ell) {   // warp-uniform condition for the shuffles
-      double g = gacc[k];
-      g += __shfl_xor_sync(0xffffffffu, g, 8);
-      g += __shfl_xor_sync(0xffffffffu, g, 4);
-      g += __shfl_xor_sync(0xffffffffu, g, 2);
-      g += __shfl_xor_sync(0xffffffffu, g, 1);
-      if (hrow == 0 && c < A.ell) A.part[(size_t)(1 + c) * gridDim.x + blockIdx.x] = g;
-    }
-  }
-  if (last_block_arrive(A.counter)) {
-    __shared__ int conv;
-    if (warp == 0) {
-      const double rrt = warp_sum_array(A.part, gridDim.x);
-      if (tid == 0) {
-        A.sc[S_RR] = rrt;
-        double iters = A.sc[S_ITERS];
-        if (!A.init) iters += 1.0;
-        A.sc[S_ITERS] = iters;
-        const double tol = A.sc[S_TOL];
-        int cv = (sqrt(rrt) <= tol) ? 1 : 0;
-        if (!isfinite(rrt)) { A.sc[S_STATUS] = (double)NYS_EBREAKDOWN; cv = 1; }
-        if (cv || iters >= (double)A.max_iter) {
-          A.sc[S_DONE] = 1.0;
-          if (A.cond != 0ull) cudaGraphSetConditional(A.cond, 0u);
-        }
-        if (A.ell == 0 && !cv) {  // P = I: z = r, rz_new = rr
-          const double rzold = A.sc[S_RZ];
-          A.sc[S_BETA] = A.init ? 0.0 : rrt / rzold;
-          A.sc[S_RZ] = rrt;
-        }
-        conv = cv;
-        *A.counter = 0u;
-      }
-    }
-    __syncthreads();
-    if (!conv) {
-      for (int c = warp; c < A.ell; c += 8) {
-        const double gc = warp_sum_array(A.part + (size_t)(1 + c) * gridDim.x, gridDim.x);
-        if (lane == 0) A.h[c] = A.s[c] * gc;
-      }
-    }
+  __syncthreads();
+  for (int c = tid; c < ncol; c += 256) {
+    const double v = ((wred[0][c] + wred[1][c]) + (wred[2][c] + wred[3][c])) + ((wred[4][c] + wred[5][c]) + (wred[6][c] + wred[7][c]));
+    A.part[(size_t)c * gridDim.x + blockIdx.x] = v;
   }
 }
 
-// precond: z = r + U h  (= P^{-1} r, P:418 rewritten as v + U((lam_l+mu)/(Lam+mu) - 1) U^T v);
-//          rz = r^T z ; last block: beta = rz_new / rz_old
+// column c of the block partials -> rr (c = 0: convergence test, PCG bookkeeping) or h_{c-1}
+__global__ void __launch_bounds__(256) pcg_hred_kernel(const PcgUpdArgs A, int G) {
+  if (A.sc[S_DONE] != 0.0) return;
+  __shared__ double ws[8];
+  const int c = blockIdx.x, tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31;
+  const double* src = A.part + (size_t)c * G;
+  double acc = 0.0;
+  for (int k0 = tid; k0 < G; k0 += 1024) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = (k0 + 256 * u < G) ? __ldcg(src + k0 + 256 * u) : 0.0;
+    acc += (v[0] + v[1]) + (v[2] + v[3]);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) ws[warp] = acc;
+  __syncthreads();
+  if (tid != 0) return;
+  const double tot = ((ws[0] + ws[1]) + (ws[2] + ws[3])) + ((ws[4] + ws[5]) + (ws[6] + ws[7]));
+  if (c > 0) {
+    A.h[c - 1] = A.s[c - 1] * tot;
+    return;
+  }
+  const double rrt = tot;
+  A.sc[S_RR] = rrt;
+  double iters = A.sc[S_ITERS];
+  if (!A.init) iters += 1.0;
+  A.sc[S_ITERS] = iters;
+  const double tol = A.sc[S_TOL];
+  int cv = (sqrt(rrt) <= tol) ? 1 : 0;
+  if (!isfinite(rrt)) { A.sc[S_STATUS] = (double)NYS_EBREAKDOWN; cv = 1; }
+  if (cv || iters >= (double)A.max_iter) {
+    A.sc[S_DONE] = 1.0;
+    if (A.cond != 0ull) cudaGraphSetConditional(A.cond, 0u);
+  }
+  if (A.ell == 0 && !cv) {  // P = I: z = r, rz_new = rr
+    const double rzold = A.sc[S_RZ];
+    A.sc[S_BETA] = A.init ? 0.0 : rrt / rzold;
+    A.sc[S_RZ] = rrt;
+  }
+}
+
 struct PcgPrecArgs {
   int init;
   int64_t m;
@@ -486,31 +493,47 @@ struct PcgPrecArgs {
   int nsub;
 };
 
+// z = r + U h with U stored ROW-major (Ut[i][c], row stride ldu): one warp per row, lane L
+// covering columns L, L+32, ... (contiguous reads), 4 rows in flight per warp, a shuffle sum per
+// row; rz = r^T z partials, the last block finishes rz and beta.
 __global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
   if (A.sc[S_DONE] != 0.0) return;
   __shared__ double hsh[256];
-  __shared__ double red[PCG_RB][PCG_NG + 1];
-  const int tid = threadIdx.x;
-  for (int c = tid; c < A.ell; c += blockDim.x) hsh[c] = A.h[c];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int c = tid; c < A.ell; c += blockDim.x) hsh[c] = __ldcg(A.h + c);
   __syncthreads();
-  const int row = tid % PCG_RB, grp = tid / PCG_RB;
+  double hl[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) hl[k] = (lane + 32 * k < A.ell) ? hsh[lane + 32 * k] : 0.0;
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  const int64_t w0 = (int64_t)blockIdx.x * 8 + (tid >> 5);
   double rz = 0.0;
-  for (int sub = 0; sub < A.nsub; ++sub) {
-    const int64_t i0 = ((int64_t)blockIdx.x * A.nsub + sub) * PCG_RB;
-    if (i0 >= A.m) break;
-    const int64_t i = i0 + row;
-    double acc = 0.0;
-    if (i < A.m)
-      for (int c = grp; c < A.ell; c += PCG_NG) acc = fma(A.U[(size_t)c * A.ldu + i], hsh[c], acc);
-    red[row][grp] = acc;
-    __syncthreads();
-    if (tid < PCG_RB && i < A.m) {
-      const double ri = A.r[i];
-      const double zi = ri + sum16(red[row]);
-      A.z[i] = zi;
-      rz = fma(ri, zi, rz);
+  for (int64_t i0 = w0; i0 < A.m; i0 += 4 * nw) {
+    double acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = i0 + q * nw;
+      double a = 0.0;
+      if (i < A.m) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int c = lane + 32 * k;
+          if (c < A.ell) a = fma(A.U[(size_t)i * A.ldu + c], hl[k], a);
+        }
+      }
+      acc[q] = a;
     }
-    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = i0 + q * nw;
+      const double us = warp_sum(acc[q]);
+      if (lane == 0 && i < A.m) {
+        const double ri = A.r[i];
+        const double zi = ri + us;
+        A.z[i] = zi;
+        rz = fma(ri, zi, rz);
+      }
+    }
   }
   double v[1] = {rz};
   block_sum_to_part<1>(v, A.part, gridDim.x);
@@ -525,12 +548,30 @@ __global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
   }
 }
 
-static void pcg_grid(nys_ctx* ctx, int64_t m, int& grid, int& nsub) {
-  const int64_t chunks = (m + PCG_RB - 1) / PCG_RB;
-  nsub = (int)((chunks + ctx->num_sms - 1) / ctx->num_sms);
-  if (nsub < 1) nsub = 1;
-  grid = (int)((chunks + nsub - 1) / nsub);
-  if (grid < 1) grid = 1;
+// Ut[i][c] = U[c][i]  (m x ell column-major, ld ldu  ->  row-major, row stride ell), 32x32 tiles
+__global__ void transpose_u_kernel(int64_t m, int ell, const double* U, int64_t ldu, double* Ut) {
+  __shared__ double t[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows of 32
+  for (int cc = ty; cc < 32; cc += 8) {
+    const int c = c0 + cc;
+    const int64_t i = i0 + tx;
+    t[cc][tx] = (c < ell && i < m) ? U[(size_t)c * ldu + i] : 0.0;
+  }
+  __syncthreads();
+  for (int ii = ty; ii < 32; ii += 8) {
+    const int64_t i = i0 + ii;
+    const int c = c0 + tx;
+    if (i < m && c < ell) Ut[(size_t)i * ell + c] = t[tx][ii];
+  }
+}
+int launch_transpose_u(nys_ctx* ctx, int64_t m, int ell, const double* U, int64_t ldu, double* Ut) {
+  if (m <= 0 || ell <= 0) return NYS_OK;
+  dim3 grid((unsigned)((m + 31) / 32), (unsigned)((ell + 31) / 32));
+  transpose_u_kernel<<<grid, 256, 0, ctx->stream>>>(m, ell, U, ldu, Ut);
+  ctx->launches++;
+  return ctx->check_launch("transpose_u");
 }
 
 int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, const double* rhs, const double* p,
@@ -544,26 +585,33 @@ int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, c
   if (fp) { A.Wp = fp->Wp; A.wp_ld = fp->wp_ld; A.nparts = fp->nparts; A.pwp = fp->pwp; A.npw = fp->npw; }
   A.delta = delta; A.e = e;
   A.U = U; A.ldu = ldu; A.ell = ell; A.s = s; A.h = h; A.sc = ctx->sc; A.max_iter = max_iter;
-  int g, nsub;
-  pcg_grid(ctx, m, g, nsub);
-  A.nsub = nsub;
+  // one 256-row tile per block while that gives <= 8 blocks per SM, else 256-row tiles in a loop
+  int64_t rpb = 256;
+  if ((m + rpb - 1) / rpb > 8LL * ctx->num_sms) rpb = ((m + 8LL * ctx->num_sms - 1) / (8LL * ctx->num_sms) + 255) / 256 * 256;
+  int g = (int)((m + rpb - 1) / rpb);
+  if (g < 1) g = 1;
+  A.rows_per_block = rpb;
   A.part = ctx->wsd("pcg_upd_part", (size_t)(1 + ell) * g);
   A.counter = ctx->counters + 1;
   pcg_update_kernel<<<(unsigned)g, 256, 0, ctx->stream>>>(A);
   ctx->launches++;
-  return ctx->check_launch("pcg_update");
+  NYS_TRY(ctx->check_launch("pcg_update"));
+  pcg_hred_kernel<<<(unsigned)(1 + ell), 256, 0, ctx->stream>>>(A, g);
+  ctx->launches++;
+  return ctx->check_launch("pcg_hred");
 }
 
 int launch_pcg_precond(nys_ctx* ctx, int init, int64_t m, const double* r, double* z, const double* U, int64_t ldu,
                        int ell, const double* h) {
   PcgPrecArgs A{};
   A.init = init; A.m = m; A.r = r; A.z = z; A.U = U; A.ldu = ldu; A.ell = ell; A.h = h; A.sc = ctx->sc;
-  int g, nsub;
-  pcg_grid(ctx, m, g, nsub);
-  A.nsub = nsub;
+  int64_t g = (m + 31) / 32;  // 8 warps per block, 4 rows per warp
+  if (g > 4 * ctx->num_sms) g = 4 * ctx->num_sms;
+  if (g < 1) g = 1;
+  A.nsub = 0;
   A.part = ctx->wsd("pcg_prec_part", (size_t)g);
   A.counter = ctx->counters + 2;
-  pcg_precond_kernel<<<g, 256, 0, ctx->stream>>>(A);
+  pcg_precond_kernel<<<(unsigned)g, 256, 0, ctx->stream>>>(A);
   ctx->launches++;
   return ctx->check_launch("pcg_precond");
 }

@@ -17,6 +17,9 @@ int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, c
                       const double* w, const FusedPartials* fp, double delta, const double* e, const double* U,
                       int64_t ldu, int ell, const double* s, double* h, int max_iter,
                       unsigned long long cond = 0ull, bool delta_slot = false);
+// U (m x ell, column-major, ld ldu) -> Ut row-major (row stride ell): the layout the graph-path PCG
+// kernels read (contiguous rows)
+int launch_transpose_u(nys_ctx* ctx, int64_t m, int ell, const double* U, int64_t ldu, double* Ut);
 int launch_pcg_precond(nys_ctx* ctx, int init, int64_t m, const double* r, double* z, const double* U, int64_t ldu,
                        int ell, const double* h);
 int launch_prec_coef(nys_ctx* ctx, const double* lam, int ell, double mu, double* s);

@@ -341,10 +341,17 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
     ctx->matvecs += res.iters;
     return NYS_OK;
   }
+  // the non-persistent PCG kernels read U ROW-major (contiguous rows): transpose once per solve
+  if (ell > 0) {
+    double* Ut = ctx->wsd("pcg_Ut", (size_t)m * ell);
+    NYS_TRY(launch_transpose_u(ctx, m, ell, U, ldu, Ut));
+    U = Ut;
+    ldu = ell;
+  }
   NYS_TRY(launch_pcg_update(ctx, 1, m, x, r, rhs, nullptr, nullptr, nullptr, op.delta, op.e, U, ldu, ell, s, h,
                             max_iter));
   if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 1, m, r, z, U, ldu, ell, h));
-  if (ctx->world == 1) {
+  if (ctx->world == 1 && getenv("NYS_NO_GRAPH") == nullptr) {  // NYS_NO_GRAPH: eager loop (profiling)
     // iterations 0 and 1 eagerly (they size every workspace), then the rest of the loop as ONE
     // graph launch: a conditional WHILE node whose body is two iterations (p double-buffer
     // parity); pcg_update's last block clears the condition when PCG is done.
@@ -391,9 +398,10 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
     }
     NYS_CUDA_TRY(ctx, cudaGraphLaunch(exec, ctx->stream));
     NYS_TRY(read_slots(ctx));
-    // accounting: each body run is 2 iterations x (2 or 3) kernels (+ the matvec)
+    // accounting: each pcg_update run in the graph body stands for matvec + update + hred
+    // (+ precond) launches of that iteration
     const int64_t body_updates = (int64_t)ctx->h_sc[S_GITER];
-    ctx->launches += body_updates * (ell > 0 ? 3 : 2);
+    ctx->launches += body_updates * (ell > 0 ? 4 : 3);
     res.iters = (int)ctx->h_sc[S_ITERS];
     ctx->matvecs += res.iters > 2 ? res.iters - 2 : 0;
   } else {
