@@ -64,12 +64,10 @@ __device__ __forceinline__ void pcg_grid_barrier(unsigned int* bar, unsigned int
   if (threadIdx.x == 0) {
     ++epoch;
     const unsigned int target = epoch * nblocks;
-    __threadfence();
-    atomicAdd(bar, 1u);
-    volatile unsigned int* cnt = bar;
-    while (*cnt < target) {
+    red_add_release_gpu(bar, 1u);
+    while (ld_relaxed_gpu(bar) < target) {
     }
-    __threadfence();
+    fence_acquire_gpu();
   }
   named_bar_sync(9, nthreads);
 }
@@ -282,9 +280,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       named_bar_sync(9, T);  // this CTA's partial row is written
       if (tid == 0) {
         ++red_epoch;
-        __threadfence();
-        const unsigned int old = atomicAdd(P.rbar + grp, 1u);
-        __threadfence();
+        const unsigned int old = atom_add_acqrel_gpu(P.rbar + grp, 1u);
         s_role = (old + 1 == red_epoch * gsz) ? 1 : 0;
       }
       named_bar_sync(9, T);
@@ -302,9 +298,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
         }
         named_bar_sync(9, T);
         if (tid == 0) {
-          __threadfence();
-          const unsigned int old = atomicAdd(P.rbar + 64, 1u);
-          __threadfence();
+          const unsigned int old = atom_add_acqrel_gpu(P.rbar + 64, 1u);
           s_role = (old + 1 == red_epoch * ngr) ? 2 : 1;
         }
         named_bar_sync(9, T);
@@ -320,17 +314,13 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
             P.tot[c] = acc;
           }
           named_bar_sync(9, T);
-          if (tid == 0) {
-            __threadfence();
-            atomicExch(P.rbar + 65, red_epoch);
-          }
+          if (tid == 0) st_release_gpu(P.rbar + 65, red_epoch);
         }
       }
       if (tid == 0) {
-        volatile unsigned int* fl = P.rbar + 65;
-        while (*fl < red_epoch) {
+        while (ld_relaxed_gpu(P.rbar + 65) < red_epoch) {
         }
-        __threadfence();
+        fence_acquire_gpu();
       }
       named_bar_sync(9, T);
       for (int c = tid; c < ncol; c += T) {
