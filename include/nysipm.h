@@ -59,6 +59,15 @@ int nys_destroy(nys_ctx* ctx);
 /* Fill out128 (128 bytes) with a fresh ncclUniqueId (rank 0 calls this and broadcasts it
  * through the caller's own channel, e.g. torch.distributed).  dlopens libnccl.so.2. */
 int nys_nccl_unique_id(void* out128);
+
+/* In-process LOOPBACK communicator for `world` ranks on ONE device (validation of the multi-rank
+ * path where a single GPU is available).  Fills the 128-byte id that nys_create takes in place of
+ * an NCCL unique id; each rank is then driven by its own host thread.  All-reduces synchronise the
+ * rank's stream, meet at a host barrier and sum the ranks' device buffers in rank order (bitwise
+ * identical on every rank); no kernel waits on another rank.  Destroy after every context using it
+ * has been destroyed.  2 <= world <= 16.  Returns NYS_EINVAL on bad arguments. */
+int nys_loopback_comm_create(int world, void* out128);
+int nys_loopback_comm_destroy(void* id128);
 const char* nys_strerror(int code);
 /* Last detailed error message of this context (CUDA/NCCL string, offending index...). */
 const char* nys_last_error(nys_ctx* ctx);

@@ -71,7 +71,7 @@ class Report(C.Structure):
 
 EXPORTED = ["nys_create", "nys_destroy", "nys_nccl_unique_id", "nys_strerror", "nys_last_error", "nys_normal_matvec",
             "nys_check_scaling", "nys_sketch", "nys_sketch_apply", "nys_gaussian", "nys_pcg_solve", "nys_default_options",
-            "nys_ipppmm_solve", "nys_kernel_launches"]
+            "nys_ipppmm_solve", "nys_kernel_launches", "nys_loopback_comm_create", "nys_loopback_comm_destroy"]
 
 _lib = None
 
@@ -88,6 +88,8 @@ def load_library(path: str = LIB_PATH):
     lib.nys_create.argtypes = [C.POINTER(vp), i32, vp, vp, i32, i32]
     lib.nys_destroy.argtypes = [vp]
     lib.nys_nccl_unique_id.argtypes = [vp]
+    lib.nys_loopback_comm_create.argtypes = [C.c_int, vp]
+    lib.nys_loopback_comm_destroy.argtypes = [vp]
     lib.nys_strerror.argtypes = [i32]
     lib.nys_strerror.restype = C.c_char_p
     lib.nys_last_error.argtypes = [vp]
@@ -146,6 +148,26 @@ def nccl_unique_id() -> bytes:
     if rc != 0:
         raise NysError(rc, "ncclGetUniqueId failed")
     return buf.raw
+
+
+class LoopbackComm:
+    """In-process loopback communicator: `world` ranks on ONE device, each driven by its own host
+    thread (validation of the multi-rank path; production multi-GPU runs use NCCL).  `id` is passed
+    to Context(nccl_id=...) in place of an NCCL unique id."""
+
+    def __init__(self, world: int):
+        lib = load_library()
+        self._buf = C.create_string_buffer(128)
+        rc = lib.nys_loopback_comm_create(int(world), C.cast(self._buf, C.c_void_p))
+        if rc != 0:
+            raise NysError(rc, "nys_loopback_comm_create failed")
+        self.id = self._buf.raw
+        self.world = world
+
+    def close(self):
+        if self._buf is not None:
+            load_library().nys_loopback_comm_destroy(C.cast(self._buf, C.c_void_p))
+            self._buf = None
 
 
 class Context:

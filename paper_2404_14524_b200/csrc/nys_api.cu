@@ -9,6 +9,8 @@
 
 #include <chrono>
 #include <cstdlib>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -84,8 +86,66 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
+// ------------------------------------------------------------------------------------------
+// In-process loopback communicator: `world` contexts on ONE device, driven by `world` host
+// threads, exchange through host-side barriers.  The sum/min is a fixed-order reduction over the
+// ranks' device buffers (bitwise identical on every rank, as NCCL's), done only after every rank
+// has synchronised its stream and arrived: no kernel ever waits on another rank's kernel.  It
+// exists to run the multi-rank code path (sharding, replicated decisions, every all-reduce) where
+// only one GPU is available; production multi-GPU runs use NCCL.
+// ------------------------------------------------------------------------------------------
+struct LoopComm {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<double*> bufs;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+struct RankPtrs {
+  const double* p[16];
+};
+__global__ void loop_reduce_kernel(RankPtrs R, int world, size_t count, int is_min, double* out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    double v = R.p[0][i];
+    for (int r = 1; r < world; ++r) v = is_min ? fmin(v, R.p[r][i]) : v + R.p[r][i];
+    out[i] = v;
+  }
+}
+
+int loop_allreduce(nys_ctx* ctx, double* buf, size_t count, bool is_min) {
+  LoopComm* c = (LoopComm*)ctx->loop_comm;
+  NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  c->bufs[ctx->rank] = buf;
+  c->barrier();  // every rank's buffer is final
+  double* tmp = ctx->wsd("loop_tmp", count);
+  RankPtrs R{};
+  for (int r = 0; r < c->world; ++r) R.p[r] = c->bufs[r];
+  int g = (int)((count + 255) / 256);
+  if (g > 1024) g = 1024;
+  loop_reduce_kernel<<<g, 256, 0, ctx->stream>>>(R, c->world, count, is_min ? 1 : 0, tmp);
+  NYS_CUDA_TRY(ctx, cudaGetLastError());
+  NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  c->barrier();  // every rank has read every buffer
+  NYS_CUDA_TRY(ctx, cudaMemcpyAsync(buf, tmp, count * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  return NYS_OK;
+}
+
 int allreduce(nys_ctx* ctx, double* buf, size_t count, bool is_min = false) {
   if (ctx->world <= 1 || count == 0) return NYS_OK;
+  if (ctx->loop_comm) return loop_allreduce(ctx, buf, count, is_min);
   ncclResult_t r = g_nccl.allReduce(buf, buf, count, ncclFloat64, is_min ? ncclMin : ncclSum,
                                     (ncclComm_t)ctx->nccl_comm, ctx->stream);
   if (r != ncclSuccess) {
@@ -923,7 +983,13 @@ int nys_create(nys_ctx** out, int device, void* cuda_stream, const void* nccl_un
   if (cudaMallocHost(&ctx->h_sc, S_COUNT * sizeof(double)) != cudaSuccess) return fail(NYS_ENOMEM);
   cudaEventCreate(&ctx->ev0);
   cudaEventCreate(&ctx->ev1);
-  if (world > 1) {
+  if (world > 1 && std::memcmp(nccl_unique_id, "NYSLOOP", 8) == 0) {  // loopback (one device)
+    void* lc = nullptr;
+    std::memcpy(&lc, (const char*)nccl_unique_id + 8, sizeof(void*));
+    LoopComm* c = (LoopComm*)lc;
+    if (!c || c->world != world) { ctx->set_error("loopback communicator / world mismatch"); return fail(NYS_EINVAL); }
+    ctx->loop_comm = c;
+  } else if (world > 1) {
     std::string err;
     if (!g_nccl.load(err)) { ctx->set_error(err); return fail(NYS_ENCCL); }
     ncclUniqueId id;
@@ -935,6 +1001,25 @@ int nys_create(nys_ctx** out, int device, void* cuda_stream, const void* nccl_un
   }
   cudaDeviceSynchronize();
   *out = ctx;
+  return NYS_OK;
+}
+
+int nys_loopback_comm_create(int world, void* out128) {
+  if (world < 2 || world > 16 || !out128) return NYS_EINVAL;
+  LoopComm* c = new LoopComm();
+  c->world = world;
+  c->bufs.assign(world, nullptr);
+  std::memset(out128, 0, 128);
+  std::memcpy(out128, "NYSLOOP", 8);
+  std::memcpy((char*)out128 + 8, &c, sizeof(void*));
+  return NYS_OK;
+}
+
+int nys_loopback_comm_destroy(void* id128) {
+  if (!id128 || std::memcmp(id128, "NYSLOOP", 8) != 0) return NYS_EINVAL;
+  LoopComm* c = nullptr;
+  std::memcpy(&c, (const char*)id128 + 8, sizeof(void*));
+  delete c;
   return NYS_OK;
 }
 

@@ -52,6 +52,7 @@ struct nys_ctx {
   bool own_stream = false;
   int rank = 0, world = 1;
   void* nccl_comm = nullptr;
+  void* loop_comm = nullptr;      // in-process loopback communicator (nys_loopback_comm_create)
   int num_sms = 148;
   int64_t launches = 0;
   int64_t matvecs = 0;

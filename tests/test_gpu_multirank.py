@@ -1,0 +1,141 @@
+"""Multi-rank path (world = 2, 3) on ONE B200 through the library's in-process loopback communicator
+(nys_loopback_comm_create): each rank is a context with its own stream, driven by its own host
+thread, holding ITS column shard of A; every all-reduce meets at a host barrier and
+sums the ranks' buffers in rank order, so no kernel waits on another rank.  Checks: replicated
+results are bitwise identical on every rank; they match the single-rank GPU result and the CPU
+oracle at the §8 tolerances.
+"""
+import concurrent.futures as cf
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import ippmm, linops  # noqa: E402
+from synth import make_config  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+
+
+def _run_ranks(world, fn):
+    """fn(ctx, rank, stream) on `world` threads with loopback contexts; returns the per-rank results."""
+    from paper_2404_14524_b200 import Context, LoopbackComm
+    comm = LoopbackComm(world)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    ctxs = [Context(0, stream=streams[r], nccl_id=comm.id, rank=r, world=world) for r in range(world)]
+
+    def worker(r):
+        torch.cuda.set_device(0)
+        with torch.cuda.stream(streams[r]):
+            out = fn(ctxs[r], r, streams[r])
+        streams[r].synchronize()
+        return out
+
+    try:
+        with cf.ThreadPoolExecutor(max_workers=world) as ex:
+            res = list(ex.map(worker, range(world)))
+    finally:
+        for c in ctxs:
+            c.close()
+        comm.close()
+    return res
+
+
+def _shards(A, world):
+    from paper_2404_14524_b200 import colmajor_device
+    n = A.shape[1]
+    out = []
+    for r in range(world):
+        lo, hi = (n * r) // world, (n * (r + 1)) // world
+        Ad, lda = colmajor_device(np.asfortranarray(A[:, lo:hi]))
+        out.append((lo, hi, Ad, lda))
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multirank_normal_matvec_and_sketch(world):
+    inst = make_config(1, m=300, n=1201, ell=20)
+    m, ell = inst.m, inst.ell
+    rs = np.random.default_rng(3)
+    d = rs.uniform(0.01, 3.0, inst.n)
+    v = rs.standard_normal(m)
+    sh = _shards(inst.A, world)
+    torch.cuda.synchronize()
+
+    def fn(ctx, r, st):
+        lo, hi, Ad, lda = sh[r]
+        w = torch.empty(m, dtype=torch.float64, device="cuda")
+        ctx.nys_normal_matvec(Ad, lda, m, dev(d[lo:hi]), None, 0.25, dev(v), w)
+        Om = torch.empty((ell, m), dtype=torch.float64, device="cuda")
+        U = torch.empty((ell, m), dtype=torch.float64, device="cuda")
+        lam = torch.empty(ell, dtype=torch.float64, device="cuda")
+        ctx.nys_gaussian(m, ell, 7, 3, Om)
+        ctx.nys_sketch(Ad, lda, m, dev(d[lo:hi]), None, 1e-2, ell, Om, U, lam)
+        st.synchronize()
+        return w.cpu().numpy(), U.cpu().numpy(), lam.cpu().numpy()
+
+    res = _run_ranks(world, fn)
+    ref = linops.normal_matvec(inst.A, d, v, 0.25)
+    for w, U, lam in res:
+        assert np.linalg.norm(w - ref) <= 1e-12 * np.linalg.norm(ref)
+    for w, U, lam in res[1:]:  # replicated results are bitwise identical across ranks
+        assert np.array_equal(w, res[0][0]) and np.array_equal(U, res[0][1]) and np.array_equal(lam, res[0][2])
+    # the sharded Nystrom approximation equals the single-rank one (operator, A5)
+    from paper_2404_14524_b200 import Context, colmajor_device
+    c1 = Context(0)
+    Ad, lda = colmajor_device(inst.A)
+    Om = torch.empty((ell, m), dtype=torch.float64, device="cuda")
+    U1 = torch.empty((ell, m), dtype=torch.float64, device="cuda")
+    lam1 = torch.empty(ell, dtype=torch.float64, device="cuda")
+    c1.nys_gaussian(m, ell, 7, 3, Om)
+    c1.nys_sketch(Ad, lda, m, dev(d), None, 1e-2, ell, Om, U1, lam1)
+    torch.cuda.synchronize()
+    U1h, l1 = U1.cpu().numpy(), lam1.cpu().numpy()
+    Nh1 = (U1h.T * l1) @ U1h
+    Uh, lh = res[0][1], res[0][2]
+    Nh = (Uh.T * lh) @ Uh
+    assert np.linalg.norm(Nh - Nh1) <= 1e-10 * np.linalg.norm(Nh1)
+    c1.close()
+
+
+@pytest.mark.parametrize("cfg,kw,world", [(0, {}, 2), (1, dict(m=200, n=800, ell=20), 2), (4, dict(m=150, n=900, ell=20), 3)])
+def test_multirank_ipppmm_matches_oracle(cfg, kw, world):
+    inst = make_config(cfg, **kw)
+    m = inst.m
+    sh = _shards(inst.A, world)
+    torch.cuda.synchronize()
+
+    def fn(ctx, r, st):
+        lo, hi, Ad, lda = sh[r]
+        g = ctx.nys_ipppmm_solve(Ad, lda, m, dev(inst.q[lo:hi]), dev(inst.b), dev(inst.c[lo:hi]), ell=inst.ell)
+        st.synchronize()
+        return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in g.items() if k != "log"}
+
+    res = _run_ranks(world, fn)
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
+    assert ref.status == "optimal"
+    for g in res:
+        assert g["status"] == 0 and g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    for g in res[1:]:  # replicated decisions and iterates identical on every rank
+        assert g["outer"] == res[0]["outer"] and g["inner"] == res[0]["inner"]
+        assert np.array_equal(g["y"], res[0]["y"]) and g["obj"] == res[0]["obj"]
+    x = np.concatenate([g["x"] for g in res])
+    z = np.concatenate([g["z"] for g in res])
+    y = res[0]["y"]
+    assert x.min() > 0 and z.min() > 0
+    assert np.linalg.norm(inst.b - inst.A @ x) / (1 + np.linalg.norm(inst.b)) <= 1e-8
+    assert np.linalg.norm(inst.c + inst.q * x - inst.A.T @ y - z) / (1 + np.linalg.norm(inst.c)) <= 1e-8
+    f = 0.5 * x @ (inst.q * x) + inst.c @ x
+    assert abs(f - res[0]["obj"]) <= 1e-10 * max(1.0, abs(f))
+    # objective vs the oracle: within the two certified bands (A17')
+    band = lambda p, d, xx, yy, zz: abs(p - d) + np.linalg.norm(xx) * np.linalg.norm(  # noqa: E731
+        inst.c + inst.q * xx - inst.A.T @ yy - zz) + np.linalg.norm(yy) * np.linalg.norm(inst.b - inst.A @ xx)
+    tol = max(1e-7 * max(1.0, abs(ref.obj)),
+              band(res[0]["obj"], res[0]["dual_obj"], x, y, z) + band(ref.obj, ref.dual_obj, ref.x, ref.y, ref.z))
+    assert abs(res[0]["obj"] - ref.obj) <= tol
+    assert abs(res[0]["outer"] - ref.outer) <= 2
