@@ -202,6 +202,27 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     for (int k = 0; k < 16; ++k) gacc[k] = 0.0;
     for (int64_t i0 = r_lo; i0 < r_hi; i0 += 16) {
       const int64_t i = i0 + row16;
+      // everything that does not depend on the partial sums is loaded up front (one round trip
+      // overlapped with the partial-row reduction instead of two more after it)
+      double pre_p = 0.0, pre_e = 0.0, pre_x = 0.0, pre_r = 0.0;
+      if (tid < 16 && i < r_hi) {
+        if (init) {
+          pre_r = P.rhs[i];
+        } else {
+          pre_p = __ldcg(pnew + i);
+          pre_e = P.e ? P.e[i] : 0.0;
+          pre_x = P.x[i];
+          pre_r = P.r[i];
+        }
+      }
+      // (the 512-thread configurations keep the U loads after the barrier: register budget)
+      constexpr bool PRE_U = (T == 256);
+      double uval[PRE_U ? 16 : 1];
+#pragma unroll
+      for (int k = 0; k < (PRE_U ? 16 : 1); ++k) {
+        const int c = hw + 16 * k;
+        uval[k] = (PRE_U && warp < 8 && c < ell && i0 + hrow < r_hi) ? P.U[(size_t)c * P.ldu + i0 + hrow] : 0.0;
+      }
       if (!init && warp < 8) {
         double acc = 0.0;
         if (i < r_hi) {
@@ -222,16 +243,15 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
         double ri = 0.0;
         if (i < r_hi) {
           if (init) {
-            ri = P.rhs[i];
+            ri = pre_r;
             P.x[i] = 0.0;
           } else {
             const double* v = chunk_red[row16];
             const double wsum = (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
                                 (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
-            const double pi = __ldcg(pnew + i);
-            const double wi = wsum + (delta + (P.e ? P.e[i] : 0.0)) * pi;
-            P.x[i] = fma(alpha, pi, P.x[i]);
-            ri = fma(-alpha, wi, P.r[i]);
+            const double wi = wsum + (delta + pre_e) * pre_p;
+            P.x[i] = fma(alpha, pre_p, pre_x);
+            ri = fma(-alpha, wi, pre_r);
           }
           P.r[i] = ri;
         }
@@ -240,10 +260,16 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       }
       named_bar_sync(9, T);
       if (warp < 8) {
+        const double hr = hsh[hrow];
+        if constexpr (PRE_U) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int c = hw + 16 * k;
-          if (c < ell && i0 + hrow < r_hi) gacc[k] = fma(P.U[(size_t)c * P.ldu + i0 + hrow], hsh[hrow], gacc[k]);
+          for (int k = 0; k < 16; ++k) gacc[k] = fma(uval[k], hr, gacc[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int c = hw + 16 * k;
+            if (c < ell && i0 + hrow < r_hi) gacc[k] = fma(P.U[(size_t)c * P.ldu + i0 + hrow], hr, gacc[k]);
+          }
         }
       }
       named_bar_sync(9, T);
@@ -396,16 +422,21 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     double* pnew = (k & 1) ? P.P0 : P.P1;
     double vreg[RPT];
     double wacc[RPT];
+    // all loads first (z, p are written by other CTAs in this launch: read through L2), then the
+    // stores: interleaving them would serialise the loads behind possibly-aliasing stores
+    double zr[RPT], pr[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int64_t rl = lig + (int64_t)GT * i;
-      double v = 0.0;
-      if (rl < P.m) {
-        v = __ldcg(P.z + rl);  // written by other CTAs in this launch: read through L2
-        if (k > 0) v = fma(beta, __ldcg(pold + rl), v);
-        if (cid == 0 && g == 0) pnew[rl] = v;
-      }
-      vreg[i] = v;
+      zr[i] = (rl < P.m) ? __ldcg(P.z + rl) : 0.0;
+      pr[i] = (rl < P.m && k > 0) ? __ldcg(pold + rl) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int64_t rl = lig + (int64_t)GT * i;
+      const double v = (k > 0) ? fma(beta, pr[i], zr[i]) : zr[i];
+      if (rl < P.m && cid == 0 && g == 0) pnew[rl] = v;
+      vreg[i] = (rl < P.m) ? v : 0.0;
       wacc[i] = 0.0;
     }
     double pwacc = 0.0;
