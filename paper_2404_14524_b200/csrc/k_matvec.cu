@@ -271,16 +271,24 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
     // ------------------------------ consumers ----------------------------------------------
     if (MODE != MV_NONLY) {
       const double bval = (P.beta != nullptr) ? *P.beta : 0.0;
+      // every operand load first, then the p_out stores: a store that may alias z / p would
+      // otherwise serialise the following loads (one L2 round trip per row)
+      double zr[RPT], pr[RPT];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t rl = lig + (int64_t)GT * i;
+        const bool ok = rl < rs && rl < rows_valid;
+        zr[i] = ok ? P.z[r0 + rl] : 0.0;
+        pr[i] = (ok && P.p != nullptr) ? P.p[r0 + rl] : 0.0;
+      }
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const int64_t rl = lig + (int64_t)GT * i;
         if (rl < rs) {
           double v = 0.0;
           if (rl < rows_valid) {
-            const int64_t r = r0 + rl;
-            v = P.z[r];
-            if (P.p != nullptr) v += bval * P.p[r];
-            if (P.p_out != nullptr && cid == 0 && g == 0) P.p_out[r] = v;
+            v = (P.p != nullptr) ? zr[i] + bval * pr[i] : zr[i];
+            if (P.p_out != nullptr && cid == 0 && g == 0) P.p_out[r0 + rl] = v;
           }
           if (VS) { if (g == 0) vsm[rl] = v; } else vreg[i] = v;
         }
