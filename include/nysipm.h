@@ -191,6 +191,14 @@ typedef struct {
   double init_delta;     /* 10                                                     */
   double init_tol_rel;   /* 1e-8 (A14')                                                    */
   int    verbose;        /* 1: print one line per outer iteration to stderr                */
+  /* Preconditioner reuse (the paper's future work, "reusing the
+   * preconditioner between iterations").  The Nystrom factors (U, lambda) are rebuilt at outer
+   * iteration k when k - k_last >= prec_refresh, or (prec_growth > 0) when the previous outer
+   * iteration's PCG count (predictor + corrector) exceeded prec_growth x the count of the iteration
+   * that followed the last rebuild.  Between rebuilds only mu_prec = delta_k is updated.
+   * prec_refresh = 1, prec_growth = 0 is Alg. 3 as written (a fresh sketch every iteration).      */
+  int    prec_refresh;   /* 1                                                              */
+  double prec_growth;    /* 0 (off)                                                         */
 } nys_options;
 
 /* Fill *opt with the defaults above. */
@@ -203,6 +211,7 @@ typedef struct {
   int    pcg_pred, pcg_corr;
   double rho, delta;     /* parameters used in this iteration                              */
   double t_sketch_ms, t_pcg_ms, t_other_ms;
+  int    prec_built;     /* 1: the Nystrom preconditioner was (re)built this iteration     */
 } nys_iter_record;
 
 typedef struct {

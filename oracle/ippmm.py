@@ -55,6 +55,11 @@ class Options:
     init_delta: float = 10.0
     init_tol_rel: float = 1e-8         # A14'
     omega_fn: Optional[Callable[[int, int, int], np.ndarray]] = None  # (m, ell, stream) -> Omega
+    # preconditioner reuse ("reusing the preconditioner between iterations"):
+    # rebuild when k - k_last >= prec_refresh, or when the previous iteration's PCG count exceeded
+    # prec_growth x the count right after the last rebuild; (1, 0.0) = Alg. 3 as written
+    prec_refresh: int = 1
+    prec_growth: float = 0.0
 
 
 @dataclass
@@ -223,6 +228,8 @@ def solve(A, q, b, c, opts: Options = Options()) -> Result:
     log = []
     status = "max_outer"
     k = 0
+    U = lamh = None
+    last_build, base_its, last_its = -1, None, 0
     for k in range(opts.max_outer + 1):
         rel_p, rel_d = nrP / (1.0 + bnorm), nrD / (1.0 + cnorm)
         # ---- TC (A11) ----
@@ -237,10 +244,14 @@ def solve(A, q, b, c, opts: Options = Options()) -> Result:
         if opts.path == "direct":
             sol = _direct_solver(A, d, delta)
         else:
-            U = lamh = None
+            built = False
             if opts.ell > 0:
-                U, lamh, _ = build_preconditioner(A, d, opts.ell, omega_fn(m, opts.ell, omega_stream(k)))
-            sol = _krylov_solver(A, d, delta, U, lamh, max_iter)
+                rebuild = (last_build < 0 or k - last_build >= max(1, opts.prec_refresh) or
+                           (opts.prec_growth > 0 and base_its and last_its > opts.prec_growth * base_its))
+                if rebuild:
+                    U, lamh, _ = build_preconditioner(A, d, opts.ell, omega_fn(m, opts.ell, omega_stream(k)))
+                    last_build, base_its, built = k, None, True
+            sol = _krylov_solver(A, d, delta, U, lamh, max_iter)   # P^{-1} with mu = delta_k (A7)
 
         # ---- Alg. 5 predictor ----
         r_d = c + q * x - A.T @ y - z + rho * (x - zeta)
@@ -283,8 +294,12 @@ def solve(A, q, b, c, opts: Options = Options()) -> Result:
         rho = max(opts.reg_floor, peu_factor(d_imp, r) * rho)
         it_p, it_c = ip.get("iters", 0), ic.get("iters", 0)
         inner_total += it_p + it_c
+        last_its = it_p + it_c
+        if base_its is None:
+            base_its = last_its
         log.append({"k": k, "mu": mu, "rel_p": rel_p, "rel_d": rel_d, "alpha_p": ap, "alpha_d": ad,
                     "pcg_pred": it_p, "pcg_corr": it_c, "rho_next": rho, "delta_next": delta,
+                    "prec_built": bool(opts.path != "direct" and opts.ell > 0 and built),
                     "mu_next": mu_new})
         mu = mu_new
 

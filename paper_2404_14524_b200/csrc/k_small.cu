@@ -263,7 +263,7 @@ __device__ __forceinline__ void jacobi_rotation(double al, double be, double ga,
 
 template <int NMAX, bool SM>
 __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, int ldr, double* Vout, int ldv,
-                                                      double* sigma, double* gws, double* jsweeps) {
+                                                      double* sigma, double* gws, double* jsweeps, long long* jdbg) {
   constexpr int E = NMAX / 32;
   extern __shared__ double jsm[];
   double* X = SM ? jsm : gws;
@@ -326,30 +326,44 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
         }
         if (a >= n || b >= n) continue;         // the dummy column of odd n (warp-uniform)
         const int p = a < b ? a : b, q = a < b ? b : a;
-        double xp[E], xq[E];
+        // X and V columns loaded together up front (the V loads would otherwise wait behind the
+        // X stores of the rotation: same shared array, possible aliasing)
+        long long tj0 = 0, tj1 = 0, tj2 = 0, tj3 = 0;
+        const bool jtr = jdbg != nullptr && warp == 0 && lane == 0 && sweep == 1 && r < 8;
+        if (jtr) tj0 = clock64();
+        double xp[E], xq[E], vp[E], vq[E];
         double ga = 0.0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const int i = lane + 32 * e;
           xp[e] = (i < n) ? X[i + p * n] : 0.0;
           xq[e] = (i < n) ? X[i + q * n] : 0.0;
+          vp[e] = (i < n) ? V[i + p * n] : 0.0;
+          vq[e] = (i < n) ? V[i + q * n] : 0.0;
           ga = fma(xp[e], xq[e], ga);
         }
         ga = wsum(ga);
+        if (jtr) tj1 = clock64();
         const double al = nrm[p], be = nrm[q];
         if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {   // warp-uniform
           double c, sn, t;
           jacobi_rotation(al, be, ga, c, sn, t);
+          if (jtr) tj2 = clock64();
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int i = lane + 32 * e;
             if (i < n) {
               X[i + p * n] = c * xp[e] - sn * xq[e];
               X[i + q * n] = sn * xp[e] + c * xq[e];
-              const double vp = V[i + p * n], vq = V[i + q * n];
-              V[i + p * n] = c * vp - sn * vq;
-              V[i + q * n] = sn * vp + c * vq;
+              V[i + p * n] = c * vp[e] - sn * vq[e];
+              V[i + q * n] = sn * vp[e] + c * vq[e];
             }
+          }
+          if (jtr) {
+            tj3 = clock64();
+            jdbg[4 * r + 0] = tj1 - tj0;
+            jdbg[4 * r + 1] = tj2 - tj1;
+            jdbg[4 * r + 2] = tj3 - tj2;
           }
           if (lane == 0) {
             nrm[p] = fmax(al - t * ga, 0.0);
@@ -359,6 +373,12 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
         }
       }
       __syncthreads();
+      if (jdbg != nullptr && threadIdx.x == 0 && sweep == 1 && r < 8) {
+        __shared__ long long jt_prev;
+        const long long now = clock64();
+        if (r > 0) jdbg[4 * r + 3] = now - jt_prev;
+        jt_prev = now;
+      }
     }
     if (!rotated) break;
     __syncthreads();
@@ -397,10 +417,19 @@ static int launch_jacobi_t(nys_ctx* ctx, int ell, const double* R, int ldr, doub
   if (nthr > 1024) nthr = 1024;
   if (need <= 200 * 1024) {
     NYS_TRY(ensure_max_smem(ctx, (const void*)jacobi_kernel<NMAX, true>, 200 * 1024));
-    jacobi_kernel<NMAX, true><<<1, nthr, need, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, nullptr, ctx->sc + S_JSWEEPS);
+    long long* jdbg = getenv("NYS_JACOBI_TRACE") ? (long long*)ctx->ws("jac_dbg", 32 * 8) : nullptr;
+    jacobi_kernel<NMAX, true><<<1, nthr, need, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, nullptr, ctx->sc + S_JSWEEPS, jdbg);
+    if (jdbg) {
+      long long h[32];
+      cudaMemcpyAsync(h, jdbg, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+      for (int r = 1; r < 8; ++r)
+        fprintf(stderr, "[jactrace] ell=%d round=%d dot=%lld rot=%lld upd=%lld round_total=%lld cycles\n", ell, r, h[4 * r],
+                h[4 * r + 1], h[4 * r + 2], h[4 * r + 3]);
+    }
   } else {
     double* gws = ctx->wsd("jacobi_ws", 2 * (size_t)ell * ell);
-    jacobi_kernel<NMAX, false><<<1, nthr, 0, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, gws, ctx->sc + S_JSWEEPS);
+    jacobi_kernel<NMAX, false><<<1, nthr, 0, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, gws, ctx->sc + S_JSWEEPS, nullptr);
   }
   ctx->launches++;
   return ctx->check_launch("jacobi");

@@ -775,6 +775,8 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   double nrP_ref = nrP, nrD_ref = nrD;
   int status = NYS_EMAXITER;
   int k = 0;
+  int last_build = -1;          // outer iteration of the last preconditioner build (f3)
+  int64_t base_its = -1, last_its = 0;
   for (k = 0; k <= opt->max_outer; ++k) {
     const double rel_p = nrP / (1.0 + bnorm), rel_d = nrD / (1.0 + cnorm);
     if (rel_p <= opt->tol && rel_d <= opt->tol && mu <= opt->tol) { status = NYS_OK; break; }   // A11
@@ -788,8 +790,16 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(AO.normal_op(d, delta, op));
     if (ell > 0) {                                                    // P:759, Alg. 2
       auto ts = std::chrono::steady_clock::now();
-      NYS_TRY(gen_omega(ctx, m, ell, opt->seed, (uint64_t)k + 1, Om));
-      NYS_TRY(sketch_impl(ctx, m, op.n, op.A, op.lda, op.d, op.e, ell, Om, U, lamh, nullptr));
+      const int refresh = opt->prec_refresh > 0 ? opt->prec_refresh : 1;
+      const bool rebuild = last_build < 0 || k - last_build >= refresh ||
+                           (opt->prec_growth > 0.0 && base_its > 0 && last_its > opt->prec_growth * base_its);
+      if (rebuild) {                                                  // f3: reuse between rebuilds
+        NYS_TRY(gen_omega(ctx, m, ell, opt->seed, (uint64_t)k + 1, Om));
+        NYS_TRY(sketch_impl(ctx, m, op.n, op.A, op.lda, op.d, op.e, ell, Om, U, lamh, nullptr));
+        last_build = k;
+        base_its = -1;
+        rec.prec_built = 1;
+      }
       NYS_TRY(launch_prec_coef(ctx, lamh, ell, delta, scoef));        // mu_prec = delta_k (A7)
       NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
       rec.t_sketch_ms = ms_since(ts);
@@ -826,6 +836,8 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     rec.t_pcg_ms += ms_since(tp2);
     if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
     rec.pcg_corr = pr.iters;
+    last_its = (int64_t)rec.pcg_pred + rec.pcg_corr;
+    if (base_its < 0) base_its = last_its;
     NYS_TRY(AO.At_dx(dyc, nullptr, xiau, rxz, z, x, d, dxc, dzc));
     // ---- combine, stepsizes, update ----
     NYS_TRY(launch_ratio(ctx, n, x, dx, dxp, dxc, z, dz, dzp, dzc, 8));
@@ -951,6 +963,8 @@ void nys_default_options(nys_options* o) {
   o->init_delta = 10.0;
   o->init_tol_rel = 1e-8;
   o->verbose = 0;
+  o->prec_refresh = 1;
+  o->prec_growth = 0.0;
 }
 
 int nys_create(nys_ctx** out, int device, void* cuda_stream, const void* nccl_unique_id, int rank, int world) {

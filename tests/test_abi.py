@@ -45,8 +45,9 @@ def test_default_options_match_oracle(lib):
     lib.nys_default_options(C.byref(o))
     r = OO()
     assert (o.tol, o.rho0, o.delta0, o.reg_floor, o.pcg_c, o.pcg_floor, o.pcg_max_iter, o.init_delta,
-            o.init_tol_rel) == (r.tol, r.rho0, r.delta0, r.reg_floor, r.pcg_c, r.pcg_floor, r.pcg_max_iter,
-                                r.init_delta, r.init_tol_rel)
+            o.init_tol_rel, o.prec_refresh, o.prec_growth) == (r.tol, r.rho0, r.delta0, r.reg_floor, r.pcg_c,
+                                                                r.pcg_floor, r.pcg_max_iter, r.init_delta,
+                                                                r.init_tol_rel, r.prec_refresh, r.prec_growth)
 
 
 def test_product_package_does_not_import_oracle():

@@ -360,3 +360,22 @@ def test_ipppmm_config3_full(ctx):
     assert ref.status == "optimal" and g["status"] == 0
     assert obj_agree(g, ref, inst=inst)
     assert abs(g["outer"] - ref.outer) <= 2
+
+
+# ------------------------------------------------------------------------ f3: preconditioner reuse
+@pytest.mark.parametrize("cfg,kw,refresh,growth", [(0, {}, 3, 0.0), (1, dict(m=200, n=800, ell=20), 4, 0.0),
+                                                   (0, {}, 10 ** 6, 1.5)])
+def test_ipppmm_prec_reuse_parity(ctx, cfg, kw, refresh, growth):
+    inst = make_config(cfg, **kw)
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c,
+                      ippmm.Options(path="krylov", ell=inst.ell, prec_refresh=refresh, prec_growth=growth))
+    g = _solve_gpu(ctx, inst, inst.ell, prec_refresh=refresh, prec_growth=growth)
+    assert ref.status == "optimal" and g["status"] == 0
+    assert g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    assert obj_agree(g, ref, inst=inst)
+    assert abs(g["outer"] - ref.outer) <= 2
+    built = [r["k"] for r in g["log"] if r["prec_built"]]
+    if growth == 0.0:
+        assert built == list(range(0, g["outer"], refresh))        # the fixed schedule
+    else:
+        assert built[0] == 0 and len(built) < g["outer"]

@@ -460,3 +460,38 @@ def test_svm_tiny_qp_against_active_set():
     r = ippmm.solve(A, inst.q, inst.b, inst.c, ippmm.Options(path="direct"))
     assert r.status == "optimal"
     assert abs(r.obj - ref["obj"]) <= 1e-6 * max(1.0, abs(ref["obj"]))
+
+
+# ------------------------------------------------------------------ f3: preconditioner reuse
+def test_prec_reuse_schedule_and_kkt():
+    """prec_refresh = k rebuilds the Nystrom factors at outer iterations 0, k, 2k, ... (between
+    rebuilds only mu_prec = delta_k changes); the solve still reaches the paper's tolerance (the
+    Newton systems are solved to the same A8' tolerance whatever the preconditioner)."""
+    inst = make_config(0)
+    base = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(ell=inst.ell))
+    for k in (2, 3, 5):
+        r = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(ell=inst.ell, prec_refresh=k))
+        assert r.status == "optimal" and r.rel_p <= 1e-8 and r.rel_d <= 1e-8 and r.mu <= 1e-8
+        built = [l["k"] for l in r.log if l["prec_built"]]
+        assert built == list(range(0, len(r.log), k))
+        assert abs(r.obj - base.obj) <= abs(r.obj - r.dual_obj) + abs(base.obj - base.dual_obj) + 1e-7
+    r1 = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(ell=inst.ell, prec_refresh=1))
+    assert r1.obj == base.obj and r1.inner_total == base.inner_total and all(l["prec_built"] for l in r1.log)
+
+
+def test_prec_reuse_growth_trigger():
+    """prec_growth: with an unbounded refresh period, rebuilds happen exactly when the previous
+    iteration's PCG count exceeds growth x the count right after the last rebuild."""
+    inst = make_config(0)
+    g = 1.5
+    r = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(ell=inst.ell, prec_refresh=10 ** 6, prec_growth=g))
+    assert r.status == "optimal"
+    base = None
+    for i, l in enumerate(r.log):
+        if i == 0:
+            assert l["prec_built"]
+        else:
+            prev = r.log[i - 1]["pcg_pred"] + r.log[i - 1]["pcg_corr"]
+            assert l["prec_built"] == (prev > g * base)
+        if l["prec_built"]:
+            base = l["pcg_pred"] + l["pcg_corr"]
