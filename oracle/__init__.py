@@ -20,5 +20,6 @@ Modules
   pcg       textbook preconditioned CG
   ippmm     Alg. 3 / 4 / 5 Nys-IP-PMM for x >= 0 (App. B)
   rng       Philox4x32-10 + Box-Muller Gaussian test matrix Omega_k
+  partial_chol  partial Cholesky preconditioner of Chol-IP-PMM
   active_set brute-force active-set enumeration for tiny QPs
 """

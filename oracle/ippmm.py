@@ -35,6 +35,7 @@ import scipy.linalg as sla
 
 from .linops import normal_matvec, scaling_d, sketch, dense_normal_matrix
 from .nystrom import nystrom_from_sketch, precond_inv_apply
+from .partial_chol import partial_cholesky, chol_precond_inv_apply
 from .pcg import pcg
 from .rng import gaussian_omega, omega_stream
 
@@ -60,6 +61,9 @@ class Options:
     # prec_growth x the count right after the last rebuild; (1, 0.0) = Alg. 3 as written
     prec_refresh: int = 1
     prec_growth: float = 0.0
+    # "nystrom" (Nys-IP-PMM) or "chol": the partial Cholesky preconditioner of rank ell (Chol-IP-PMM,
+    # the paper's comparison arm), rebuilt every outer iteration
+    precond: str = "nystrom"
 
 
 @dataclass
@@ -165,9 +169,11 @@ def _direct_solver(A, d, delta):
     return solve
 
 
-def _krylov_solver(A, d, delta, U, lam, max_iter):
+def _krylov_solver(A, d, delta, U, lam, max_iter, chol=None):
     apply_op = lambda v: normal_matvec(A, d, v, delta)  # noqa: E731
-    if U is None:
+    if chol is not None:
+        pinv = lambda v: chol_precond_inv_apply(chol, v)  # noqa: E731
+    elif U is None:
         pinv = None
     else:
         pinv = lambda v: precond_inv_apply(U, lam, delta, v)  # noqa: E731 (mu_prec = delta, A7)
@@ -209,10 +215,12 @@ def solve(A, q, b, c, opts: Options = Options()) -> Result:
         sol0 = _direct_solver(A, ones, opts.init_delta)
         solve_aat = lambda r: sol0(r)  # noqa: E731
     else:
-        U0 = lam0 = None
-        if opts.ell > 0:
+        U0 = lam0 = F0 = None
+        if opts.ell > 0 and opts.precond == "chol":
+            F0 = partial_cholesky(A, ones, opts.init_delta, opts.ell)
+        elif opts.ell > 0:
             U0, lam0, _ = build_preconditioner(A, ones, opts.ell, omega_fn(m, opts.ell, omega_stream(-1)))
-        sol0 = _krylov_solver(A, ones, opts.init_delta, U0, lam0, max_iter)
+        sol0 = _krylov_solver(A, ones, opts.init_delta, U0, lam0, max_iter, F0)
         solve_aat = lambda r: sol0(r, opts.init_tol_rel * float(np.linalg.norm(r)))  # noqa: E731
     x, y, z, info0 = initial_point(A, q, b, c, solve_aat)
     inner_total = info0["pcg_iters"]
@@ -245,13 +253,17 @@ def solve(A, q, b, c, opts: Options = Options()) -> Result:
             sol = _direct_solver(A, d, delta)
         else:
             built = False
-            if opts.ell > 0:
+            F = None
+            if opts.ell > 0 and opts.precond == "chol":
+                F = partial_cholesky(A, d, delta, opts.ell)               # P:250-349, every iteration
+                built = True
+            elif opts.ell > 0:
                 rebuild = (last_build < 0 or k - last_build >= max(1, opts.prec_refresh) or
                            (opts.prec_growth > 0 and base_its and last_its > opts.prec_growth * base_its))
                 if rebuild:
                     U, lamh, _ = build_preconditioner(A, d, opts.ell, omega_fn(m, opts.ell, omega_stream(k)))
                     last_build, base_its, built = k, None, True
-            sol = _krylov_solver(A, d, delta, U, lamh, max_iter)   # P^{-1} with mu = delta_k (A7)
+            sol = _krylov_solver(A, d, delta, U, lamh, max_iter, F)   # Nystrom: mu_prec = delta_k (A7)
 
         # ---- Alg. 5 predictor ----
         r_d = c + q * x - A.T @ y - z + rho * (x - zeta)

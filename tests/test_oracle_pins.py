@@ -495,3 +495,80 @@ def test_prec_reuse_growth_trigger():
             assert l["prec_built"] == (prev > g * base)
         if l["prec_built"]:
             base = l["pcg_pred"] + l["pcg_corr"]
+
+
+# ------------------------------------------------------------------ f2: partial Cholesky
+def _chol_case(seed=0, m=12, n=40, delta=0.3):
+    rs = np.random.default_rng(seed)
+    A = rs.standard_normal((m, n))
+    d = rs.uniform(0.05, 3.0, n)
+    Nd = linops.dense_normal_matrix(A, d, delta)
+    return A, d, delta, Nd
+
+
+def test_partial_chol_diag_is_the_normal_diagonal():
+    from oracle import partial_chol as pc
+    A, d, delta, Nd = _chol_case()
+    np.testing.assert_allclose(pc.diag_normal(A, d, delta), np.diag(Nd), rtol=1e-13)
+    # pivots: the ell largest diagonal entries, ties -> smaller index (reading C1)
+    assert list(pc.pivots(np.array([1.0, 3.0, 2.0, 3.0]), 2)) == [1, 3]
+
+
+def test_partial_chol_full_rank_is_exact_and_zero_rank_is_jacobi():
+    """ell = m: P_Chol = N_delta (S is empty); ell = 0: P_Chol = diag(N_delta) (eq. P:293-306)."""
+    from oracle import partial_chol as pc
+    A, d, delta, Nd = _chol_case(1)
+    m = Nd.shape[0]
+    F = pc.partial_cholesky(A, d, delta, m)
+    np.testing.assert_allclose(pc.chol_precond_dense(F, m), Nd, rtol=1e-12, atol=1e-12 * np.abs(Nd).max())
+    F0 = pc.partial_cholesky(A, d, delta, 0)
+    np.testing.assert_allclose(pc.chol_precond_dense(F0, m), np.diag(np.diag(Nd)), rtol=1e-13)
+
+
+def test_partial_chol_block_structure_schur_diagonal_and_inverse():
+    """P_Chol equals N_delta on the pivot rows/columns, its complement block is L21 L21^T + diag(S),
+    diag(S) is the diagonal of the exact Schur complement, and the closed-form inverse
+    inverts it."""
+    from oracle import partial_chol as pc
+    A, d, delta, Nd = _chol_case(2, m=15, n=50)
+    m, ell = Nd.shape[0], 5
+    F = pc.partial_cholesky(A, d, delta, ell)
+    Pm = pc.chol_precond_dense(F, m)
+    P, Q = F["P"], F["Q"]
+    np.testing.assert_allclose(Pm[P, :], Nd[P, :], rtol=1e-12, atol=1e-12 * np.abs(Nd).max())
+    S = Nd[np.ix_(Q, Q)] - Nd[np.ix_(Q, P)] @ np.linalg.solve(Nd[np.ix_(P, P)], Nd[np.ix_(P, Q)])
+    np.testing.assert_allclose(F["dS"], np.diag(S), rtol=1e-11)
+    assert np.all(np.diag(Nd)[P].min() >= np.diag(Nd)[Q].max())     # the ell largest diagonal entries
+    rs = np.random.default_rng(3)
+    for _ in range(3):
+        v = rs.standard_normal(m)
+        np.testing.assert_allclose(Pm @ pc.chol_precond_inv_apply(F, v), v, rtol=1e-10, atol=1e-10)
+
+
+def test_partial_chol_pcg_full_rank_one_iteration():
+    from oracle import partial_chol as pc
+    A, d, delta, Nd = _chol_case(4)
+    m = Nd.shape[0]
+    F = pc.partial_cholesky(A, d, delta, m)
+    b = np.random.default_rng(5).standard_normal(m)
+    x, info = pcgmod.pcg(lambda v: Nd @ v, b, lambda v: pc.chol_precond_inv_apply(F, v), tol_abs=1e-10 * np.linalg.norm(b))
+    assert info["iters"] <= 1
+    np.testing.assert_allclose(Nd @ x, b, rtol=1e-9, atol=1e-9)
+
+
+def test_chol_ippmm_tiny_qps_match_brute_force():
+    """Chol-IP-PMM (precond="chol") reaches the brute-force active-set optimum of tiny QPs."""
+    rs = np.random.default_rng(11)
+    for t in range(3):
+        m, n = 3, 9
+        A = rs.standard_normal((m, n))
+        x0 = rs.uniform(0.5, 1.5, n)
+        q = rs.uniform(0.1, 1.0, n)
+        b = A @ x0
+        c = A.T @ rs.standard_normal(m) + rs.uniform(-0.5, 1.5, n) - q * x0
+        bf = enumerate_active_sets(A, q, b, c)
+        f_bf, x_bf = bf["obj"], bf["x"]
+        r = ippmm.solve(A, q, b, c, ippmm.Options(ell=2, precond="chol"))
+        assert r.status == "optimal"
+        assert abs(r.obj - f_bf) <= 1e-6 * max(1.0, abs(f_bf))
+        assert np.abs(r.x - x_bf).max() <= 1e-5
