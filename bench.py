@@ -248,6 +248,8 @@ def main():
     ap.add_argument("--n-per-gpu", type=int, default=50000, help="config 4: columns of A per rank")
     ap.add_argument("--prec-refresh", type=int, default=1,
                     help="SURVEY §8(f) f3: rebuild the Nystrom preconditioner every K outer iterations (1 = Alg. 3)")
+    ap.add_argument("--precond", default="nystrom", choices=["nystrom", "chol"],
+                    help="nystrom: Nys-IP-PMM (default); chol: Chol-IP-PMM, partial Cholesky of rank ell (f2)")
     ap.add_argument("--prec-growth", type=float, default=0.0,
                     help="f3: also rebuild when PCG counts grow by this factor since the last rebuild (0 = off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -290,7 +292,8 @@ def main():
     def one_solve():
         with torch.cuda.stream(stream):
             return ctx.nys_ipppmm_solve(wl.At, lda, m, wl.q, wl.b, wl.c, ell=wl.ell, structure=wl.structure,
-                                        prec_refresh=args.prec_refresh, prec_growth=args.prec_growth)
+                                        prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
+                                        precond=1 if args.precond == "chol" else 0)
 
     # ---- warm-up ------------------------------------------------------------------------------
     W = max(args.warmup, 3)
@@ -473,7 +476,7 @@ def main():
             "warmup": W, "ms_per_step": sec_per_solve * 1e3, "higher_is_better": False,
             "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl.name, "m": m, "n": wl.n, "ell": wl.ell, "tol": 1e-8,
-                       "prec_refresh": args.prec_refresh, "prec_growth": args.prec_growth,
+                       "prec_refresh": args.prec_refresh, "prec_growth": args.prec_growth, "precond": args.precond,
                        "parallelism": f"column-shard x{world}",
                        "l2": ("A = %.0f MB vs 126 MB L2: roofline launches L2-flushed (256 MB read) before each"
                               % (wl.a_bytes() * world / 1e6)) if small else

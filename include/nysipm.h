@@ -60,6 +60,22 @@ int nys_destroy(nys_ctx* ctx);
  * through the caller's own channel, e.g. torch.distributed).  dlopens libnccl.so.2. */
 int nys_nccl_unique_id(void* out128);
 
+/* ---------------------------------------------------------------------------------------
+ * nys_partial_cholesky — the partial Cholesky preconditioner of Chol-IP-PMM (SURVEY
+ * §8(f) f2) for N_delta = A diag(d) A^T + diag(e) + delta I (summed over ranks), rank ell:
+ *   piv (device, ell int64, may be NULL): the pivots = indices of the ell largest diagonal entries of
+ *       N_delta (reading C1: original diagonal, ties -> smaller index), value-descending;
+ *   L   (device, m x ell column-major, ld m, may be NULL): rows piv = L11 (lower Cholesky factor of
+ *       N_delta[piv, piv], pivot order), other rows = L21 = N_delta[Q, piv] L11^{-T};
+ *   dS  (device, m, may be NULL): diag(S) of the Schur complement on the non-pivot rows, 0 on piv.
+ * The factors are also kept in the context for nys_chol_precond_apply.  NYS_ECHOL if N_delta[piv,piv]
+ * is not positive definite.  Synchronises the stream. */
+int nys_partial_cholesky(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                         const double* e, double delta, int ell, int64_t* piv, double* L, double* dS);
+/* out = P_Chol^{-1} v (eq. P:309-322) with the factors of the last nys_partial_cholesky call on this
+ * context (m must match).  v, out: device m-vectors. */
+int nys_chol_precond_apply(nys_ctx* ctx, int64_t m, const double* v, double* out);
+
 /* In-process LOOPBACK communicator for `world` ranks on ONE device (validation of the multi-rank
  * path where a single GPU is available).  Fills the 128-byte id that nys_create takes in place of
  * an NCCL unique id; each rank is then driven by its own host thread.  All-reduces synchronise the
@@ -199,6 +215,10 @@ typedef struct {
    * prec_refresh = 1, prec_growth = 0 is Alg. 3 as written (a fresh sketch every iteration).      */
   int    prec_refresh;   /* 1                                                              */
   double prec_growth;    /* 0 (off)                                                         */
+  /* 0: randomized Nystrom P^{-1} (Nys-IP-PMM).  1: the partial Cholesky preconditioner of rank
+   * ell (Chol-IP-PMM, the paper's comparison arm), built every outer
+   * iteration from diag(N_delta): pivots = the ell largest diagonal entries (reading C1).       */
+  int    precond;        /* 0                                                              */
 } nys_options;
 
 /* Fill *opt with the defaults above. */

@@ -47,7 +47,7 @@ class Options(C.Structure):
                 ("pcg_max_iter", C.c_int), ("rho0", C.c_double), ("delta0", C.c_double),
                 ("reg_floor", C.c_double), ("pcg_c", C.c_double), ("pcg_floor", C.c_double),
                 ("init_delta", C.c_double), ("init_tol_rel", C.c_double), ("verbose", C.c_int),
-                ("prec_refresh", C.c_int), ("prec_growth", C.c_double)]
+                ("prec_refresh", C.c_int), ("prec_growth", C.c_double), ("precond", C.c_int)]
 
 
 class IterRecord(C.Structure):
@@ -72,7 +72,8 @@ class Report(C.Structure):
 
 EXPORTED = ["nys_create", "nys_destroy", "nys_nccl_unique_id", "nys_strerror", "nys_last_error", "nys_normal_matvec",
             "nys_check_scaling", "nys_sketch", "nys_sketch_apply", "nys_gaussian", "nys_pcg_solve", "nys_default_options",
-            "nys_ipppmm_solve", "nys_kernel_launches", "nys_loopback_comm_create", "nys_loopback_comm_destroy"]
+            "nys_ipppmm_solve", "nys_kernel_launches", "nys_loopback_comm_create", "nys_loopback_comm_destroy",
+            "nys_partial_cholesky", "nys_chol_precond_apply"]
 
 _lib = None
 
@@ -90,6 +91,8 @@ def load_library(path: str = LIB_PATH):
     lib.nys_destroy.argtypes = [vp]
     lib.nys_nccl_unique_id.argtypes = [vp]
     lib.nys_loopback_comm_create.argtypes = [C.c_int, vp]
+    lib.nys_partial_cholesky.argtypes = [vp, i64, i64, vp, i64, vp, vp, C.c_double, C.c_int, vp, vp, vp]
+    lib.nys_chol_precond_apply.argtypes = [vp, i64, vp, vp]
     lib.nys_loopback_comm_destroy.argtypes = [vp]
     lib.nys_strerror.argtypes = [i32]
     lib.nys_strerror.restype = C.c_char_p
@@ -237,6 +240,17 @@ class Context:
         _check_cuda(A, d, e, Omega, Y)
         return self._rc(self.lib.nys_sketch_apply(self.h, m, A.shape[0], _ptr(A), lda, _ptr(d), _ptr(e), ell,
                                                   _ptr(Omega), _ptr(Y)))
+
+    def nys_partial_cholesky(self, A, lda: int, m: int, d, e, delta: float, ell: int, piv=None, L=None, dS=None):
+        _check_cuda(A, d, e, L, dS)
+        if piv is not None and (not piv.is_cuda or piv.dtype.__repr__() != "torch.int64"):
+            raise TypeError("piv must be a cuda int64 tensor")
+        return self._rc(self.lib.nys_partial_cholesky(self.h, m, A.shape[0], _ptr(A), lda, _ptr(d), _ptr(e),
+                                                      float(delta), int(ell), _ptr(piv), _ptr(L), _ptr(dS)))
+
+    def nys_chol_precond_apply(self, m: int, v, out):
+        _check_cuda(v, out)
+        return self._rc(self.lib.nys_chol_precond_apply(self.h, m, _ptr(v), _ptr(out)))
 
     def nys_pcg_solve(self, A, lda: int, m: int, d, e, delta: float, ell: int, U, lam, mu_prec: float, rhs, x,
                       tol_abs: float, max_iter: int) -> PcgInfo:

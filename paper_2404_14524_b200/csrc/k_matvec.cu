@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
     }
   } else {
     // ------------------------------ consumers ----------------------------------------------
-    if (MODE != MV_NONLY) {
+    if (MODE != MV_NONLY && MODE != MV_DIAG) {
       const double bval = (P.beta != nullptr) ? *P.beta : 0.0;
       // every operand load first, then the p_out stores: a store that may alias z / p would
       // otherwise serialise the following loads (one L2 round trip per row)
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
     }
     if (VS) named_bar_sync(1, T);  // vsm complete (NG == 1 for VS)
 
-    if (CLU && MODE != MV_NONLY) {
+    if (CLU && MODE != MV_NONLY && MODE != MV_DIAG) {
       // ---- cluster path (rows split over cl CTAs; NG == 1; v in registers).  Lag-1 software
       // pipeline: the CTA partial dots of panel `it` are pushed to every peer with st.async
       // (completing bytes on the peer's dotbar), and the rank-CPG update of panel it-1 runs
@@ -437,9 +437,10 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
 
       double dpre[CPG];  // scaling of this group's columns, loaded before the dot (hides L2 latency)
 #pragma unroll
-      for (int c = 0; c < CPG; ++c) dpre[c] = (MODE == MV_FUSED && col0 + c < P.n) ? __ldg(P.d + col0 + c) : 0.0;
+      for (int c = 0; c < CPG; ++c)
+        dpre[c] = ((MODE == MV_FUSED || MODE == MV_DIAG) && col0 + c < P.n) ? __ldg(P.d + col0 + c) : 0.0;
       double t[CPG];
-      if (MODE != MV_NONLY) {
+      if (MODE != MV_NONLY && MODE != MV_DIAG) {
         double pd[CPG];
 #pragma unroll
         for (int c = 0; c < CPG; ++c) {
@@ -481,6 +482,9 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
               if (lig == c && col0 + c < P.n) P.tbuf[col0 + c] = pd[c];
           }
         }
+      } else if (MODE == MV_DIAG) {
+#pragma unroll
+        for (int c = 0; c < CPG; ++c) t[c] = dpre[c];
       } else {
 #pragma unroll
         for (int c = 0; c < CPG; ++c) t[c] = (col0 + c < P.n) ? P.u[col0 + c] : 0.0;
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
         for (int i = 0; i < RPT; ++i) {
           double acc = wacc[i];
 #pragma unroll
-          for (int c = 0; c < CPG; ++c) acc = fma(a[c][i], t[c], acc);
+          for (int c = 0; c < CPG; ++c) acc = fma(MODE == MV_DIAG ? a[c][i] * a[c][i] : a[c][i], t[c], acc);
           wacc[i] = acc;
         }
       }
@@ -718,7 +722,8 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, 
     if (st < 2) st = 2;
     G.rs = rs_; G.c = c_; G.stages = st;
     G.smem = mv_smem_bytes(c_, rs_, st, cl_, clu_);
-    G.k = (mode == MV_FUSED) ? kernel_for<MV_FUSED>(c_, clu_) : (mode == MV_TONLY) ? kernel_for<MV_TONLY>(c_, clu_) : kernel_for<MV_NONLY>(c_, clu_);
+    G.k = (mode == MV_FUSED) ? kernel_for<MV_FUSED>(c_, clu_) : (mode == MV_TONLY) ? kernel_for<MV_TONLY>(c_, clu_)
+          : (mode == MV_NONLY) ? kernel_for<MV_NONLY>(c_, clu_) : kernel_for<MV_DIAG>(c_, clu_);
     NYS_TRY(ensure_max_smem(ctx, (const void*)G.k, G.smem));
     if (cl_ > 8) NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(G.k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     return NYS_OK;
@@ -906,7 +911,9 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
     P.fuse_fin = fuse ? 1 : 0;
     P.fin = F;
     P.gbar = gbar;
-    MvKernel k = (c.mode == MV_FUSED) ? kernel_for<MV_FUSED>(pl.cfg, pl.cl > 1) : (c.mode == MV_TONLY) ? kernel_for<MV_TONLY>(pl.cfg, pl.cl > 1) : kernel_for<MV_NONLY>(pl.cfg, pl.cl > 1);
+    MvKernel k = (c.mode == MV_FUSED) ? kernel_for<MV_FUSED>(pl.cfg, pl.cl > 1)
+                 : (c.mode == MV_TONLY) ? kernel_for<MV_TONLY>(pl.cfg, pl.cl > 1)
+                 : (c.mode == MV_NONLY) ? kernel_for<MV_NONLY>(pl.cfg, pl.cl > 1) : kernel_for<MV_DIAG>(pl.cfg, pl.cl > 1);
     if (c.n > 0) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)pl.grid);

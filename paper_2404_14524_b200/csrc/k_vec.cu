@@ -52,45 +52,6 @@ int launch_gaussian(nys_ctx* ctx, double* O, int64_t total, uint64_t seed, uint6
 }
 
 // ------------------------------------------------------------------------------------------
-// generic deterministic block reduction helpers
-// ------------------------------------------------------------------------------------------
-template <int NV>
-__device__ __forceinline__ void block_sum_to_part(double (&v)[NV], double* part, int stride) {
-  __shared__ double sh[NV][32];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) sh[k][w] = v[k];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int nw = blockDim.x >> 5;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      double s = 0.0;
-      for (int i = 0; i < nw; ++i) s += sh[k][i];
-      part[(size_t)k * stride + blockIdx.x] = s;
-    }
-  }
-}
-
-__device__ __forceinline__ bool last_block_arrive(unsigned int* counter) {
-  __shared__ bool last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(counter, 1u);
-    last = (prev == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last) __threadfence();
-  return last;
-}
-
-
-// ------------------------------------------------------------------------------------------
 // dots: out_slot[k] = sum_i a_k[i] * b_k[i]   (b_k == nullptr -> a_k[i]^2), k < 4
 // optional affine pre-map: a_k[i] + alpha_k * da_k[i]  (for mu_aff)
 // ------------------------------------------------------------------------------------------
@@ -317,6 +278,7 @@ struct PcgUpdArgs {
   unsigned int* counter;
   int max_iter;
   int64_t rows_per_block;
+  int ext_prec;         // 1: an external preconditioner (partial Cholesky) sets rz / beta
 };
 
 // Row-parallel update: a block owns `rows_per_block` consecutive rows, one row per thread per
@@ -471,7 +433,7 @@ __global__ void __launch_bounds__(256) pcg_hred_kernel(const PcgUpdArgs A, int G
     A.sc[S_DONE] = 1.0;
     if (A.cond != 0ull) cudaGraphSetConditional(A.cond, 0u);
   }
-  if (A.ell == 0 && !cv) {  // P = I: z = r, rz_new = rr
+  if (A.ell == 0 && !A.ext_prec && !cv) {  // P = I: z = r, rz_new = rr
     const double rzold = A.sc[S_RZ];
     A.sc[S_BETA] = A.init ? 0.0 : rrt / rzold;
     A.sc[S_RZ] = rrt;
@@ -577,8 +539,9 @@ int launch_transpose_u(nys_ctx* ctx, int64_t m, int ell, const double* U, int64_
 int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, const double* rhs, const double* p,
                       const double* w, const FusedPartials* fp, double delta, const double* e, const double* U,
                       int64_t ldu, int ell, const double* s, double* h, int max_iter, unsigned long long cond,
-                      bool delta_slot) {
+                      bool delta_slot, bool ext_prec) {
   PcgUpdArgs A{};
+  A.ext_prec = ext_prec ? 1 : 0;
   A.cond = cond;
   A.delta_slot = delta_slot ? 1 : 0;
   A.init = init; A.m = m; A.x = x; A.r = r; A.rhs = rhs; A.p = p; A.w = w;

@@ -3,6 +3,47 @@
 #include "nys_common.cuh"
 
 namespace nys {
+
+// ------------------------------------------------------------------------------------------
+// generic deterministic block reduction helpers
+// ------------------------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void block_sum_to_part(double (&v)[NV], double* part, int stride) {
+  __shared__ double sh[NV][32];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sh[k][w] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = 0.0;
+      for (int i = 0; i < nw; ++i) s += sh[k][i];
+      part[(size_t)k * stride + blockIdx.x] = s;
+    }
+  }
+}
+
+__device__ __forceinline__ bool last_block_arrive(unsigned int* counter) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(counter, 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+
+
 // k_vec.cu
 int launch_gaussian(nys_ctx* ctx, double* O, int64_t total, uint64_t seed, uint64_t stream);
 int launch_dots(nys_ctx* ctx, int64_t n, int nv, const double* const* a, const double* const* b, const int* out,
@@ -16,10 +57,27 @@ int launch_steps_post(nys_ctx* ctx);
 int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, const double* rhs, const double* p,
                       const double* w, const FusedPartials* fp, double delta, const double* e, const double* U,
                       int64_t ldu, int ell, const double* s, double* h, int max_iter,
-                      unsigned long long cond = 0ull, bool delta_slot = false);
+                      unsigned long long cond = 0ull, bool delta_slot = false, bool ext_prec = false);
 // U (m x ell, column-major, ld ldu) -> Ut row-major (row stride ell): the layout the graph-path PCG
 // kernels read (contiguous rows)
 int launch_transpose_u(nys_ctx* ctx, int64_t m, int ell, const double* U, int64_t ldu, double* Ut);
+// k_chol.cu — partial Cholesky preconditioner (Chol-IP-PMM)
+struct CholFactors {
+  int64_t m = 0;
+  int ell = 0;
+  int64_t* piv = nullptr;   // ell pivots, value-descending
+  int* pivpos = nullptr;    // m: position in piv, -1 off the pivots
+  double* Rinv = nullptr;   // ell x ell upper, ld ldr: R^{-1} with R^T R = N11
+  int ldr = 0;
+  double* Zt = nullptr;     // m x ell ROW-major: rows P = L11 = R^T, rows Q = L21
+  double* dS = nullptr;     // m: diag(S) on Q, 0 on P
+  double* diag = nullptr;   // m: diag(N_delta)
+};
+int launch_topl_select(nys_ctx* ctx, const double* v, int64_t m, int ell, int64_t* piv, int* pivpos);
+int launch_selection(nys_ctx* ctx, int64_t m, int ell, const int64_t* piv, double* Om, int64_t ldo);
+int launch_pivot_block(nys_ctx* ctx, double* Y, int64_t ldy, const int64_t* piv, int ell, double delta, double* N11);
+int launch_chol_ds(nys_ctx* ctx, int64_t m, int ell, const double* Zt, const double* dg, const int* pivpos, double* dS);
+int launch_chol_apply(nys_ctx* ctx, const CholFactors& F, const double* v, double* out, int pcg, int init);
 int launch_pcg_precond(nys_ctx* ctx, int init, int64_t m, const double* r, double* z, const double* U, int64_t ldu,
                        int ell, const double* h);
 int launch_prec_coef(nys_ctx* ctx, const double* lam, int ell, double mu, double* s);

@@ -349,6 +349,58 @@ int sketch_impl(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda
 }
 
 // ------------------------------------------------------------------------------------------
+// Partial Cholesky preconditioner of rank ell for N_delta = N + delta I (f2)
+// ------------------------------------------------------------------------------------------
+int chol_build(nys_ctx* ctx, const NormalOp& op, int ell, CholFactors& F) {
+  const int64_t m = op.m, mp = even(m);
+  F.m = m;
+  F.ell = ell;
+  F.diag = ctx->wsd("ch_diag", (size_t)mp);
+  double* ones = ctx->wsd("ch_ones", (size_t)mp);
+  NYS_CUDA_TRY(ctx, cudaMemsetAsync(ones, 0, (size_t)mp * sizeof(double), ctx->stream));
+  NYS_TRY(launch_shift(ctx, m, ones, 1.0));
+  {  // diag(N_delta) = sum_j d_j A_ij^2 + e_i + delta
+    MatvecCall c;
+    c.mode = MV_DIAG; c.m = m; c.n = op.n; c.lda = op.lda; c.A = op.A; c.d = op.d; c.z = ones;
+    c.out = F.diag;
+    if (ctx->world == 1) {
+      c.use_delta = true; c.delta = op.delta; c.e = op.e;
+      NYS_TRY(launch_matvec(ctx, c));
+    } else {
+      NYS_TRY(launch_matvec(ctx, c));
+      NYS_TRY(allreduce(ctx, F.diag, (size_t)m));
+      NYS_TRY(launch_finalize_terms(ctx, m, F.diag, ones, op.delta, op.e, false, nullptr));
+    }
+  }
+  F.piv = (int64_t*)ctx->ws("ch_piv", (size_t)(ell > 0 ? ell : 1) * sizeof(int64_t));
+  F.pivpos = (int*)ctx->ws("ch_pivpos", (size_t)mp * sizeof(int));
+  NYS_TRY(launch_topl_select(ctx, F.diag, m, ell, F.piv, F.pivpos));
+  F.dS = ctx->wsd("ch_dS", (size_t)mp);
+  F.ldr = ell > 0 ? ell : 1;
+  F.Rinv = ctx->wsd("ch_Rinv", (size_t)F.ldr * F.ldr);
+  F.Zt = ctx->wsd("ch_Zt", (size_t)m * (ell > 0 ? ell : 1));
+  if (ell > 0) {
+    double* Om = ctx->wsd("ch_Om", (size_t)mp * ell);
+    double* Y = ctx->wsd("ch_Y", (size_t)mp * ell);
+    double* N11 = ctx->wsd("ch_N11", (size_t)ell * ell);
+    double* Z = ctx->wsd("ch_Z", (size_t)mp * ell);
+    NYS_TRY(launch_selection(ctx, m, ell, F.piv, Om, mp));
+    NYS_TRY(sketch_Y(ctx, m, op.n, op.A, op.lda, op.d, op.e, ell, Om, Y));   // N E_P (+ e)
+    NYS_TRY(launch_pivot_block(ctx, Y, mp, F.piv, ell, op.delta, N11));     // + delta; N11 = Y[P, :]
+    NYS_TRY(launch_set_slots(ctx, S_CHOLFAIL, 0.0));
+    NYS_TRY(launch_chol_inv(ctx, ell, N11, ell, F.Rinv, ell, 0));          // N11 = R^T R, R^{-1}
+    NYS_TRY(read_slots(ctx));
+    if (ctx->h_sc[S_CHOLFAIL] != 0.0) { ctx->set_error("partial Cholesky: N11 not positive definite"); return NYS_ECHOL; }
+    GemmCall gz;  // Z = Y R^{-1}: rows P = L11 = R^T, rows Q = L21 = N21 L11^{-T}
+    gz.M = m; gz.N = ell; gz.K = ell; gz.A = Y; gz.lda = mp; gz.a_kmajor = false; gz.B = F.Rinv; gz.ldb = ell;
+    gz.C = Z; gz.ldc = mp;
+    NYS_TRY(launch_gemm(ctx, gz));
+    NYS_TRY(launch_transpose_u(ctx, m, ell, Z, mp, F.Zt));
+  }
+  return launch_chol_ds(ctx, m, ell, F.Zt, F.diag, F.pivpos, F.dS);
+}
+
+// ------------------------------------------------------------------------------------------
 // PCG with device scalars (tolerance already in S_TOL via launch_pcg_setup)
 // ------------------------------------------------------------------------------------------
 struct PcgResult {
@@ -360,7 +412,7 @@ struct PcgResult {
 // One PCG iteration (it) of the fused single-GPU path: K1 -> update -> precond.
 int pcg_iteration(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t ldu, const double* s,
                   double* x, double* r, double* z, double* const* Pp, double* h, int it, int max_iter,
-                  unsigned long long cond) {
+                  unsigned long long cond, const CholFactors* chol = nullptr) {
   const double* done = ctx->sc + S_DONE;
   const double* pold = (it == 0) ? nullptr : Pp[it & 1];
   double* pnew = Pp[(it + 1) & 1];
@@ -372,6 +424,11 @@ int pcg_iteration(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, in
   FusedPartials fp;
   c.fused_out = &fp;
   NYS_TRY(launch_matvec(ctx, c));
+  if (chol) {  // partial Cholesky P^{-1} (Chol-IP-PMM): update computes rr only
+    NYS_TRY(launch_pcg_update(ctx, 0, op.m, x, r, nullptr, pnew, nullptr, &fp, op.delta, op.e, nullptr, 0, 0, nullptr,
+                              h, max_iter, cond, true, true));
+    return launch_chol_apply(ctx, *chol, r, z, 1, 0);
+  }
   NYS_TRY(launch_pcg_update(ctx, 0, op.m, x, r, nullptr, pnew, nullptr, &fp, op.delta, op.e, U, ldu, ell, s, h,
                             max_iter, cond, true));
   if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 0, op.m, r, z, U, ldu, ell, h));
@@ -379,11 +436,12 @@ int pcg_iteration(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, in
 }
 
 int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t ldu, const double* s,
-             const double* rhs, double* x, int max_iter, PcgResult& res) {
+             const double* rhs, double* x, int max_iter, PcgResult& res, const CholFactors* chol = nullptr) {
   const int64_t m = op.m;
   const int64_t mp = even(m);
+  if (chol) ell = 0;  // no Nystrom factors on the partial-Cholesky path
   double* r = ctx->wsd("pcg_r", (size_t)mp);
-  double* z = ell > 0 ? ctx->wsd("pcg_z", (size_t)mp) : r;
+  double* z = (ell > 0 || chol) ? ctx->wsd("pcg_z", (size_t)mp) : r;
   double* P0 = ctx->wsd("pcg_p0", (size_t)mp);
   double* P1 = ctx->wsd("pcg_p1", (size_t)mp);
   double* w = ctx->wsd("pcg_w", (size_t)mp);
@@ -391,7 +449,7 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
   double* Pp[2] = {P0, P1};
   const double* done = ctx->sc + S_DONE;
   NYS_TRY(launch_set_slots(ctx, S_DELTA, op.delta, S_GITER, 0.0));
-  if (pcg_persistent_supported(ctx, m, op.n, ell)) {
+  if (!chol && pcg_persistent_supported(ctx, m, op.n, ell)) {
     // the whole solve is ONE cooperative launch (k_pcg.cu)
     NYS_TRY(launch_pcg_persistent(ctx, m, op.n, op.A, op.lda, op.d, op.e, U, ldu, ell, s, rhs, x, max_iter));
     NYS_TRY(read_slots(ctx));
@@ -409,15 +467,16 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
     ldu = ell;
   }
   NYS_TRY(launch_pcg_update(ctx, 1, m, x, r, rhs, nullptr, nullptr, nullptr, op.delta, op.e, U, ldu, ell, s, h,
-                            max_iter));
-  if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 1, m, r, z, U, ldu, ell, h));
+                            max_iter, 0ull, false, chol != nullptr));
+  if (chol) NYS_TRY(launch_chol_apply(ctx, *chol, r, z, 1, 1));
+  else if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 1, m, r, z, U, ldu, ell, h));
   if (ctx->world == 1 && getenv("NYS_NO_GRAPH") == nullptr) {  // NYS_NO_GRAPH: eager loop (profiling)
     // iterations 0 and 1 eagerly (they size every workspace), then the rest of the loop as ONE
     // graph launch: a conditional WHILE node whose body is two iterations (p double-buffer
     // parity); pcg_update's last block clears the condition when PCG is done.
-    for (int it = 0; it < 2; ++it) NYS_TRY(pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, it, max_iter, 0ull));
+    for (int it = 0; it < 2; ++it) NYS_TRY(pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, it, max_iter, 0ull, chol));
     char key[512];
-    snprintf(key, sizeof(key), "pcg:%lld:%lld:%lld:%p:%p:%p:%p:%lld:%p:%d:%p:%d:%lld", (long long)m, (long long)op.n,
+    snprintf(key, sizeof(key), "pcg%s:%lld:%lld:%lld:%p:%p:%p:%p:%lld:%p:%d:%p:%d:%lld", chol ? "C" : "N", (long long)m, (long long)op.n,
              (long long)op.lda, (const void*)op.A, (const void*)op.d, (const void*)op.e, (const void*)U,
              (long long)ldu, (const void*)s, ell, (const void*)x, max_iter, (long long)ctx->ws_epoch);
     auto itg = ctx->graphs.find(key);
@@ -446,8 +505,8 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
       cudaGraph_t body = gp.conditional.phGraph_out[0];
       const int64_t l0 = ctx->launches, mv0 = ctx->matvecs;
       NYS_CUDA_TRY(ctx, cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-      int rc1 = pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, 2, max_iter, (unsigned long long)hcond);
-      int rc2 = rc1 == NYS_OK ? pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, 3, max_iter, (unsigned long long)hcond) : rc1;
+      int rc1 = pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, 2, max_iter, (unsigned long long)hcond, chol);
+      int rc2 = rc1 == NYS_OK ? pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, 3, max_iter, (unsigned long long)hcond, chol) : rc1;
       cudaGraph_t body_out = body;
       cudaError_t ec = cudaStreamEndCapture(ctx->stream, &body_out);
       ctx->launches = l0; ctx->matvecs = mv0;
@@ -461,7 +520,7 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
     // accounting: each pcg_update run in the graph body stands for matvec + update + hred
     // (+ precond) launches of that iteration
     const int64_t body_updates = (int64_t)ctx->h_sc[S_GITER];
-    ctx->launches += body_updates * (ell > 0 ? 4 : 3);
+    ctx->launches += body_updates * (chol ? 7 : (ell > 0 ? 4 : 3));
     res.iters = (int)ctx->h_sc[S_ITERS];
     ctx->matvecs += res.iters > 2 ? res.iters - 2 : 0;
   } else {
@@ -473,8 +532,9 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
         double* pnew = Pp[(it + 1) & 1];
         NYS_TRY(apply_normal_full(ctx, op, z, pold, ctx->sc + S_BETA, pnew, w, true, done));
         NYS_TRY(launch_pcg_update(ctx, 0, m, x, r, nullptr, pnew, w, nullptr, op.delta, op.e, U, ldu, ell, s, h,
-                                  max_iter));
-        if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 0, m, r, z, U, ldu, ell, h));
+                                  max_iter, 0ull, false, chol != nullptr));
+        if (chol) NYS_TRY(launch_chol_apply(ctx, *chol, r, z, 1, 0));
+        else if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 0, m, r, z, U, ldu, ell, h));
       }
       NYS_TRY(read_slots(ctx));
       if (ctx->h_sc[S_DONE] != 0.0) break;
@@ -705,25 +765,32 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   NYS_TRY(launch_shift(ctx, n, ones, 1.0));
   NormalOp op0;
   NYS_TRY(AO.normal_op(ones, opt->init_delta, op0));
-  if (ell > 0) {
+  const bool use_chol = opt->precond == 1;                            // Chol-IP-PMM (f2)
+  CholFactors CF;
+  if (ell > 0 || use_chol) {
     auto ts = std::chrono::steady_clock::now();
-    NYS_TRY(gen_omega(ctx, m, ell, opt->seed, 0, Om));                 // stream 0
-    NYS_TRY(sketch_impl(ctx, m, op0.n, op0.A, op0.lda, op0.d, op0.e, ell, Om, U, lamh, nullptr));
-    NYS_TRY(launch_prec_coef(ctx, lamh, ell, opt->init_delta, scoef));
+    if (use_chol) {
+      NYS_TRY(chol_build(ctx, op0, ell, CF));
+    } else {
+      NYS_TRY(gen_omega(ctx, m, ell, opt->seed, 0, Om));               // stream 0
+      NYS_TRY(sketch_impl(ctx, m, op0.n, op0.A, op0.lda, op0.d, op0.e, ell, Om, U, lamh, nullptr));
+      NYS_TRY(launch_prec_coef(ctx, lamh, ell, opt->init_delta, scoef));
+    }
     t_sketch += ms_since(ts);
   }
+  const CholFactors* cfp = use_chol ? &CF : nullptr;
   auto tp = std::chrono::steady_clock::now();
   PcgResult pr;
   NYS_TRY(D.dot(m, b, b, S_XINORM));
   NYS_TRY(launch_pcg_setup(ctx, 2, 0, 0, 0, S_XINORM, 0, 0, opt->init_tol_rel));
-  NYS_TRY(pcg_impl(ctx, op0, ell, U, mp, scoef, b, u1, opt->pcg_max_iter, pr));
+  NYS_TRY(pcg_impl(ctx, op0, ell, U, mp, scoef, b, u1, opt->pcg_max_iter, pr, cfp));
   total_inner += pr.iters;
   NYS_TRY(AO.At_plain(u1, x));                                       // x~ = A^T u1
   NYS_TRY(launch_cpqx(ctx, n, c, q, x, t));                          // c + Q x~
   NYS_TRY(AO.Ax(t, xi, nullptr));                                    // A (c + Q x~)
   NYS_TRY(D.dot(m, xi, xi, S_XINORM));
   NYS_TRY(launch_pcg_setup(ctx, 2, 0, 0, 0, S_XINORM, 0, 0, opt->init_tol_rel));
-  NYS_TRY(pcg_impl(ctx, op0, ell, U, mp, scoef, xi, y, opt->pcg_max_iter, pr));
+  NYS_TRY(pcg_impl(ctx, op0, ell, U, mp, scoef, xi, y, opt->pcg_max_iter, pr, cfp));
   total_inner += pr.iters;
   t_pcg += ms_since(tp);
   NYS_TRY(AO.At_rd(y, c, q, x, nullptr, z));                         // z~ = c - A^T y~ + Q x~
@@ -788,7 +855,14 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(launch_scaling(ctx, n, q, x, z, rho, d));
     NormalOp op;
     NYS_TRY(AO.normal_op(d, delta, op));
-    if (ell > 0) {                                                    // P:759, Alg. 2
+    if (use_chol) {                                                   // P:250-349, every iteration
+      auto ts = std::chrono::steady_clock::now();
+      NYS_TRY(chol_build(ctx, op, ell, CF));
+      NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      rec.prec_built = 1;
+      rec.t_sketch_ms = ms_since(ts);
+      t_sketch += rec.t_sketch_ms;
+    } else if (ell > 0) {                                             // P:759, Alg. 2
       auto ts = std::chrono::steady_clock::now();
       const int refresh = opt->prec_refresh > 0 ? opt->prec_refresh : 1;
       const bool rebuild = last_build < 0 || k - last_build >= refresh ||
@@ -813,7 +887,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
     NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
     auto tp1 = std::chrono::steady_clock::now();
-    NYS_TRY(pcg_impl(ctx, op, ell, U, mp, scoef, xi, dyp, opt->pcg_max_iter, pr));
+    NYS_TRY(pcg_impl(ctx, op, ell, U, mp, scoef, xi, dyp, opt->pcg_max_iter, pr, cfp));
     rec.t_pcg_ms += ms_since(tp1);
     if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
     rec.pcg_pred = pr.iters;
@@ -832,7 +906,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
     NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
     auto tp2 = std::chrono::steady_clock::now();
-    NYS_TRY(pcg_impl(ctx, op, ell, U, mp, scoef, xi, dyc, opt->pcg_max_iter, pr));
+    NYS_TRY(pcg_impl(ctx, op, ell, U, mp, scoef, xi, dyc, opt->pcg_max_iter, pr, cfp));
     rec.t_pcg_ms += ms_since(tp2);
     if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
     rec.pcg_corr = pr.iters;
@@ -965,6 +1039,7 @@ void nys_default_options(nys_options* o) {
   o->verbose = 0;
   o->prec_refresh = 1;
   o->prec_growth = 0.0;
+  o->precond = 0;
 }
 
 int nys_create(nys_ctx** out, int device, void* cuda_stream, const void* nccl_unique_id, int rank, int world) {
@@ -1018,6 +1093,8 @@ int nys_create(nys_ctx** out, int device, void* cuda_stream, const void* nccl_un
   return NYS_OK;
 }
 
+static std::map<nys_ctx*, nys::CholFactors> g_chol;  // last nys_partial_cholesky per context
+
 int nys_loopback_comm_create(int world, void* out128) {
   if (world < 2 || world > 16 || !out128) return NYS_EINVAL;
   LoopComm* c = new LoopComm();
@@ -1049,6 +1126,7 @@ int nys_nccl_unique_id(void* out128) {
 
 int nys_destroy(nys_ctx* ctx) {
   if (!ctx) return NYS_OK;
+  g_chol.erase(ctx);
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
@@ -1164,6 +1242,42 @@ int nys_sketch_apply(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_
   NYS_TRY(sketch_Y(ctx, m, n, A, lda, d, e, ell, Om, Yo));
   if (Yo != Y)
     NYS_CUDA_TRY(ctx, cudaMemcpy2DAsync(Y, m * 8, Yo, mp * 8, m * 8, ell, cudaMemcpyDeviceToDevice, ctx->stream));
+  return NYS_OK;
+  NYS_GUARD_END
+}
+
+int nys_partial_cholesky(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                         const double* e, double delta, int ell, int64_t* piv, double* L, double* dS) {
+  NYS_GUARD_BEGIN
+  NYS_TRY(check_A(ctx, m, n, A, lda));
+  if (ell < 0 || ell > m || ell > 256 || !(delta > 0) || (n > 0 && !d)) {
+    ctx->set_error("nys_partial_cholesky: bad arguments");
+    return NYS_EINVAL;
+  }
+  cudaSetDevice(ctx->device);
+  NormalOp op{m, n, lda, A, d, e, delta};
+  CholFactors F;
+  NYS_TRY(chol_build(ctx, op, ell, F));
+  g_chol[ctx] = F;
+  if (piv && ell > 0)
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(piv, F.piv, sizeof(int64_t) * ell, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (L && ell > 0) NYS_TRY(launch_transpose_u(ctx, ell, (int)m, F.Zt, ell, L));   // row-major -> column-major
+  if (dS) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(dS, F.dS, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+  NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return NYS_OK;
+  NYS_GUARD_END
+}
+
+int nys_chol_precond_apply(nys_ctx* ctx, int64_t m, const double* v, double* out) {
+  NYS_GUARD_BEGIN
+  if (!ctx || !v || !out) return NYS_EINVAL;
+  auto it = g_chol.find(ctx);
+  if (it == g_chol.end() || it->second.m != m) {
+    ctx->set_error("nys_chol_precond_apply: no partial Cholesky factors of this size on the context");
+    return NYS_EINVAL;
+  }
+  cudaSetDevice(ctx->device);
+  NYS_TRY(launch_chol_apply(ctx, it->second, v, out, 0, 0));
   return NYS_OK;
   NYS_GUARD_END
 }

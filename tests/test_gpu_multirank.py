@@ -139,3 +139,32 @@ def test_multirank_ipppmm_matches_oracle(cfg, kw, world):
               band(res[0]["obj"], res[0]["dual_obj"], x, y, z) + band(ref.obj, ref.dual_obj, ref.x, ref.y, ref.z))
     assert abs(res[0]["obj"] - ref.obj) <= tol
     assert abs(res[0]["outer"] - ref.outer) <= 2
+
+
+def test_multirank_chol_ipppmm_matches_oracle():
+    """Chol-IP-PMM (f2) on 2 loopback ranks: the diagonal and the pivot columns are all-reduced."""
+    inst = make_config(1, m=200, n=800, ell=20)
+    world, m = 2, inst.m
+    sh = _shards(inst.A, world)
+    torch.cuda.synchronize()
+
+    def fn(ctx, r, st):
+        lo, hi, Ad, lda = sh[r]
+        g = ctx.nys_ipppmm_solve(Ad, lda, m, dev(inst.q[lo:hi]), dev(inst.b), dev(inst.c[lo:hi]), ell=inst.ell,
+                                 precond=1)
+        st.synchronize()
+        return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in g.items() if k != "log"}
+
+    res = _run_ranks(world, fn)
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell, precond="chol"))
+    for g in res:
+        assert g["status"] == 0 and g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    assert np.array_equal(res[0]["y"], res[1]["y"]) and res[0]["inner"] == res[1]["inner"]
+    x = np.concatenate([g["x"] for g in res])
+    z = np.concatenate([g["z"] for g in res])
+    y = res[0]["y"]
+    band = lambda p, d, xx, yy, zz: abs(p - d) + np.linalg.norm(xx) * np.linalg.norm(  # noqa: E731
+        inst.c + inst.q * xx - inst.A.T @ yy - zz) + np.linalg.norm(yy) * np.linalg.norm(inst.b - inst.A @ xx)
+    tol = max(1e-7 * max(1.0, abs(ref.obj)),
+              band(res[0]["obj"], res[0]["dual_obj"], x, y, z) + band(ref.obj, ref.dual_obj, ref.x, ref.y, ref.z))
+    assert abs(res[0]["obj"] - ref.obj) <= tol

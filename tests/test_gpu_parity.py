@@ -379,3 +379,74 @@ def test_ipppmm_prec_reuse_parity(ctx, cfg, kw, refresh, growth):
         assert built == list(range(0, g["outer"], refresh))        # the fixed schedule
     else:
         assert built[0] == 0 and len(built) < g["outer"]
+
+
+# ------------------------------------------------------------------------ f2: partial Cholesky
+@pytest.mark.parametrize("m,n,ell", [(60, 300, 10), (301, 900, 40), (2000, 3000, 50), (9001, 700, 64)])
+def test_partial_cholesky_factors_parity(ctx, m, n, ell):
+    from oracle import partial_chol as pc
+    from paper_2404_14524_b200 import colmajor_device
+    rs = np.random.default_rng(m + ell)
+    A = rs.standard_normal((m, n))
+    d = rs.uniform(0.01, 3.0, n)
+    delta = 1e-2
+    F = pc.partial_cholesky(A, d, delta, ell)
+    Ad, lda = colmajor_device(A)
+    piv = torch.empty(ell, dtype=torch.int64, device="cuda")
+    L = torch.empty((ell, m), dtype=torch.float64, device="cuda")
+    dS = torch.empty(m, dtype=torch.float64, device="cuda")
+    ctx.nys_partial_cholesky(Ad, lda, m, dev(d), None, delta, ell, piv, L, dS)
+    torch.cuda.synchronize()
+    assert np.array_equal(piv.cpu().numpy(), F["P"])                    # pivots: bit-exact
+    Lh = L.cpu().numpy().T                                               # m x ell
+    np.testing.assert_allclose(Lh[F["P"]], F["L11"], rtol=0, atol=1e-12 * np.abs(F["L11"]).max())
+    np.testing.assert_allclose(Lh[F["Q"]], F["L21"], rtol=0, atol=1e-11 * np.abs(F["L21"]).max())
+    dSh = dS.cpu().numpy()
+    assert np.all(dSh[F["P"]] == 0.0)
+    np.testing.assert_allclose(dSh[F["Q"]], F["dS"], rtol=1e-10)
+    # P^{-1} v (eq. P:309-322) on random vectors
+    for k in range(3):
+        v = rs.standard_normal(m)
+        out = torch.empty(m, dtype=torch.float64, device="cuda")
+        ctx.nys_chol_precond_apply(m, dev(v), out)
+        torch.cuda.synchronize()
+        ref = pc.chol_precond_inv_apply(F, v)
+        assert rel(out.cpu().numpy(), ref) <= 1e-10
+
+
+def test_partial_cholesky_ties_and_full_rank(ctx):
+    """Equal diagonal entries pick the smaller indices (reading C1); ell = m is exact."""
+    from oracle import partial_chol as pc
+    from paper_2404_14524_b200 import colmajor_device
+    m, n = 40, 40
+    A = np.eye(m, n) * 2.0
+    A[5, 5] = A[17, 17] = 3.0
+    d = np.ones(n)
+    Ad, lda = colmajor_device(A)
+    piv = torch.empty(6, dtype=torch.int64, device="cuda")
+    ctx.nys_partial_cholesky(Ad, lda, m, dev(d), None, 0.5, 6, piv, None, None)
+    torch.cuda.synchronize()
+    assert list(piv.cpu().numpy()) == [5, 17, 0, 1, 2, 3] == list(pc.pivots(pc.diag_normal(A, d, 0.5), 6))
+    rs = np.random.default_rng(1)
+    B = rs.standard_normal((30, 60))
+    Bd, ldb = colmajor_device(B)
+    dd = rs.uniform(0.1, 2.0, 60)
+    ctx.nys_partial_cholesky(Bd, ldb, 30, dev(dd), None, 0.1, 30, None, None, None)
+    v = rs.standard_normal(30)
+    out = torch.empty(30, dtype=torch.float64, device="cuda")
+    ctx.nys_chol_precond_apply(30, dev(v), out)
+    torch.cuda.synchronize()
+    Nd = linops.dense_normal_matrix(B, dd, 0.1)
+    assert rel(Nd @ out.cpu().numpy(), v) <= 1e-10                      # P = N_delta exactly
+
+
+@pytest.mark.parametrize("cfg,kw", [(0, {}), (1, dict(m=200, n=800, ell=20)), (3, dict(m=16, n=2000, ell=8))])
+def test_chol_ipppmm_parity(ctx, cfg, kw):
+    """Chol-IP-PMM (precond = 1) against the oracle's precond='chol' path."""
+    inst = make_config(cfg, **kw)
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell, precond="chol"))
+    g = _solve_gpu(ctx, inst, inst.ell, precond=1)
+    assert ref.status == "optimal" and g["status"] == 0
+    assert g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    assert obj_agree(g, ref, inst=inst)
+    assert abs(g["outer"] - ref.outer) <= 2
