@@ -424,14 +424,25 @@ def main():
         except Exception:
             avail = float("inf")
         if need < 0.6 * avail:
-            A_host = wl.At.cpu().numpy()
-            qh, bh, ch = wl.q.cpu().numpy(), wl.b.cpu().numpy(), wl.c.cpu().numpy()
+            # inputs in PINNED host memory (the contract's H2D leg), copied in by the library each step
+            def pinned(t):
+                h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                h.copy_(t)
+                return h
+            A_pin, q_pin, b_pin, c_pin = pinned(wl.At), pinned(wl.q), pinned(wl.b), pinned(wl.c)
+            A_host, qh, bh, ch = A_pin.numpy(), q_pin.numpy(), b_pin.numpy(), c_pin.numpy()
+            with torch.cuda.stream(stream):  # one untimed e2e solve: workspace for the host path, graphs
+                ctx.nys_ipppmm_solve(A_host, lda, m, qh, bh, ch, ell=wl.ell, host=True, structure=wl.structure,
+                                     prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
+                                     precond=1 if args.precond == "chol" else 0)
             barrier()
             t0 = time.perf_counter()
             E_STEPS = max(1, min(args.steps, 3))
             for _ in range(E_STEPS):
                 with torch.cuda.stream(stream):
-                    ctx.nys_ipppmm_solve(A_host, lda, m, qh, bh, ch, ell=wl.ell, host=True, structure=wl.structure)
+                    ctx.nys_ipppmm_solve(A_host, lda, m, qh, bh, ch, ell=wl.ell, host=True, structure=wl.structure,
+                                         prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
+                                         precond=1 if args.precond == "chol" else 0)
             barrier()
             t_e2e = (time.perf_counter() - t0) / E_STEPS
             if world > 1:
@@ -440,8 +451,8 @@ def main():
                 t_e2e = float(tt.item())
             nq = qh.shape[0]
             e2e = {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": int(A_host.nbytes + 8 * (2 * nq + m)),
-                   "d2h_bytes_per_step": int(8 * (2 * nq + m))}
-            del A_host
+                   "d2h_bytes_per_step": int(8 * (2 * nq + m)), "host_buffers": "pinned"}
+            del A_host, A_pin
         else:
             e2e = {"value": None, "unit": "s", "skipped": f"host RAM: need {need / 1e9:.0f} GB pinned-able, "
                                                           f"{avail / 1e9:.0f} GB available per rank"}

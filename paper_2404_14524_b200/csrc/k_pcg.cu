@@ -595,6 +595,7 @@ static PcgKernel pcg_kernel_for(const PcgCfg& c) {
   if (c.GT == 32 && c.RPT == 4) return pcg_persistent_kernel<256, 32, 4, 2>;
   if (c.GT == 64) return pcg_persistent_kernel<256, 64, 4, 2>;
   if (c.GT == 128) return pcg_persistent_kernel<256, 128, 8, 2>;
+  if (c.GT == 256 && c.CPG == 2) return pcg_persistent_kernel<256, 256, 8, 2>;
   if (c.GT == 256) return pcg_persistent_kernel<256, 256, 8, 4>;
   if (c.RPT == 8) return pcg_persistent_kernel<512, 512, 8, 2>;
   return pcg_persistent_kernel<512, 512, 16, 1>;
@@ -608,7 +609,11 @@ bool pcg_persistent_supported(nys_ctx* ctx, int64_t m, int64_t n, int ell) {
 int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
                           const double* e, const double* U, int64_t ldu, int ell, const double* s, const double* rhs,
                           double* x, int max_iter) {
-  const PcgCfg c = pcg_pick(m);
+  PcgCfg c = pcg_pick(m);
+  if (const char* ov = getenv("NYS_PCG_CFG")) {  // tuning override "T,GT,RPT,CPG" (must be instantiated)
+    PcgCfg o;
+    if (sscanf(ov, "%d,%d,%d,%d", &o.T, &o.GT, &o.RPT, &o.CPG) == 4 && (int64_t)o.GT * o.RPT >= m) c = o;
+  }
   const int NG = c.T / c.GT, WPG = c.GT / 32, BN = NG * c.CPG;
   const int64_t mp = (m + 1) & ~int64_t(1);
   const size_t stage_bytes = (size_t)BN * mp * 8;
