@@ -572,3 +572,69 @@ def test_chol_ippmm_tiny_qps_match_brute_force():
         assert r.status == "optimal"
         assert abs(r.obj - f_bf) <= 1e-6 * max(1.0, abs(f_bf))
         assert np.abs(r.x - x_bf).max() <= 1e-5
+
+
+# ------------------------------------------------------------------ f1: free and box variables
+def _gen_qp(rs, m, n, vtype, ub_scale=1.0):
+    A = rs.standard_normal((m, n))
+    vt = np.asarray(vtype)
+    x0 = rs.uniform(0.2, 0.8, n) * ub_scale
+    x0[vt == 1] = rs.standard_normal(int((vt == 1).sum()))
+    u = np.where(vt == 2, ub_scale, 0.0)
+    q = rs.uniform(0.1, 1.0, n)
+    b = A @ x0
+    c = rs.standard_normal(n)
+    return A, q, b, c, u
+
+
+def test_general_form_all_nonnegative_reduces_to_standard():
+    """vtype = all I (u = 0, w = s = 0): the general-form iteration is the standard one."""
+    from oracle import ippmm_gen
+    inst = make_config(0)
+    r0 = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(ell=inst.ell))
+    rg = ippmm_gen.solve_general(inst.A, inst.q, inst.b, inst.c, np.zeros(inst.n, dtype=int), np.zeros(inst.n),
+                                 ippmm.Options(ell=inst.ell))
+    # identical formulas; only the rounding of the residual norms (sqrt of sums vs np.linalg.norm)
+    # differs, which moves the PCG stopping points by a few iterations
+    assert rg.status == "optimal" and rg.outer == r0.outer
+    assert abs(rg.inner_total - r0.inner_total) <= 0.01 * r0.inner_total
+    assert abs(rg.obj - r0.obj) <= 1e-9 * abs(r0.obj)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_general_form_tiny_qps_match_brute_force(seed):
+    """Free / non-negative / box variables mixed: the solve reaches the brute-force optimum."""
+    from oracle import ippmm_gen
+    from oracle.active_set import enumerate_active_sets_general
+    rs = np.random.default_rng(100 + seed)
+    vtype = [0, 0, 1, 2, 2, 2, 0, 2]
+    A, q, b, c, u = _gen_qp(rs, 3, len(vtype), vtype)
+    bf = enumerate_active_sets_general(A, q, b, c, np.array(vtype), u)
+    for path in ("direct", "krylov"):
+        r = ippmm_gen.solve_general(A, q, b, c, vtype, u, ippmm.Options(path=path, ell=2))
+        assert r.status == "optimal"
+        assert abs(r.obj - bf["obj"]) <= 1e-6 * max(1.0, abs(bf["obj"]))
+        assert np.abs(r.x - bf["x"]).max() <= 1e-5
+        vt = np.array(vtype)
+        assert np.all(r.x[vt != 1] > 0) and np.all(r.x[vt == 2] < u[vt == 2])       # strictly interior iterates
+        assert np.allclose(r.w[vt == 2], u[vt == 2] - r.x[vt == 2], atol=1e-7)
+
+
+def test_free_variables_equal_the_split_formulation():
+    """x_F free is equivalent to x_F = x+ - x- with x+, x- >= 0: same optimal objective."""
+    from oracle import ippmm_gen
+    rs = np.random.default_rng(7)
+    m, n = 4, 10
+    vtype = np.array([1, 1, 0, 0, 0, 0, 0, 0, 1, 0])
+    A, q, b, c, u = _gen_qp(rs, m, n, vtype)
+    q[vtype == 1] = 0.5
+    rg = ippmm_gen.solve_general(A, q, b, c, vtype, u, ippmm.Options(path="direct"))
+    F = np.where(vtype == 1)[0]
+    As = np.hstack([A, -A[:, F]])
+    qs = np.concatenate([q, q[F]])
+    cs = np.concatenate([c, -c[F]])
+    # with Q: 1/2 q (x+ - x-)^2 != 1/2 q (x+^2 + x-^2) in general -> compare on q_F -> the split optimum
+    # has x+ x- = 0, where both coincide
+    rs_ = ippmm.solve(As, qs, b, cs, ippmm.Options(path="direct"))
+    assert rg.status == "optimal" and rs_.status == "optimal"
+    assert abs(rg.obj - rs_.obj) <= 1e-6 * max(1.0, abs(rs_.obj))
