@@ -192,6 +192,13 @@ typedef struct {
                             [w+, w-, xi, s].  The identity blocks are never materialised: they
                             contribute the diagonal term e = d_xi + d_s of the normal operator.   */
   int64_t nd;            /* structure 1: number of dense columns (features) d              */
+  /* Free and box-constrained variables, problem (P~)/(D~) (Alg. 5; SURVEY
+   * §8(f) f1).  vtype == NULL: every variable is in I (x >= 0), the form (P)/(D).  Otherwise
+   * vtype[j] (n local entries, int8) is 0 for j in I (x_j >= 0), 1 for j in F (free), 2 for j in J
+   * (0 <= x_j <= ub[j]); ub (n local doubles) is read on J only and may be NULL when no entry is 2.
+   * Same memory space as A (host_ptrs).  Not combined with structure 1 (NYS_EINVAL).            */
+  const int8_t* vtype;
+  const double* ub;
 } nys_qp;
 
 typedef struct {
@@ -239,7 +246,9 @@ typedef struct {
   double* y;             /* m out                                                          */
   double* z;             /* n (local) out                                                  */
   double obj;            /* 1/2 x^T Q x + c^T x  (summed over ranks)                       */
-  double dual_obj;       /* b^T y - 1/2 x^T Q x                                            */
+  double dual_obj;       /* b^T y - 1/2 x^T Q x  (- u_J^T s_J with box variables)           */
+  double* w;             /* n (local) out or NULL: the upper-bound slack (0 off J)          */
+  double* s;             /* n (local) out or NULL: the upper-bound dual (0 off J)           */
 } nys_solution;
 
 typedef struct {

@@ -39,7 +39,7 @@ class PcgInfo(C.Structure):
 class QP(C.Structure):
     _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("A", C.c_void_p), ("lda", C.c_int64), ("q", C.c_void_p),
                 ("b", C.c_void_p), ("c", C.c_void_p), ("host_ptrs", C.c_int), ("structure", C.c_int),
-                ("nd", C.c_int64)]
+                ("nd", C.c_int64), ("vtype", C.c_void_p), ("ub", C.c_void_p)]
 
 
 class Options(C.Structure):
@@ -59,7 +59,7 @@ class IterRecord(C.Structure):
 
 class Solution(C.Structure):
     _fields_ = [("x", C.c_void_p), ("y", C.c_void_p), ("z", C.c_void_p), ("obj", C.c_double),
-                ("dual_obj", C.c_double)]
+                ("dual_obj", C.c_double), ("w", C.c_void_p), ("s", C.c_void_p)]
 
 
 class Report(C.Structure):
@@ -263,9 +263,10 @@ class Context:
 
     def nys_ipppmm_solve(self, A, lda: int, m: int, q, b, c, ell: int = 0, tol: float = 1e-8, seed: int = 0,
                          max_outer: int = 100, host: bool = False, max_records: int = 256, verbose: bool = False,
-                         structure: int = 0, **opt_overrides):
+                         structure: int = 0, vtype=None, ub=None, **opt_overrides):
         """A: device tensor (ncols, lda) [or host numpy when host=True]; q, c: n; b: m.
-        structure=1: A holds the dense block Xt (nd columns) of A = [Xt, -Xt, I, -I]; n = 2 nd + 2 m."""
+        structure=1: A holds the dense block Xt (nd columns) of A = [Xt, -Xt, I, -I]; n = 2 nd + 2 m.
+        vtype (int8, n; 0 = I, 1 = F free, 2 = J box) and ub (n, read on J): problem (P~)/(D~), f1."""
         import torch
         nd = A.shape[0]
         n = q.shape[0]
@@ -277,25 +278,32 @@ class Context:
         if host:
             arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (A, q, b, c)]
             A, q, b, c = arrs
-            x = np.zeros(n)
-            y = np.zeros(m)
-            z = np.zeros(n)
+            if vtype is not None:
+                vtype = np.ascontiguousarray(vtype, dtype=np.int8)
+            if ub is not None:
+                ub = np.ascontiguousarray(ub, dtype=np.float64)
+            x, y, z, w, s = np.zeros(n), np.zeros(m), np.zeros(n), np.zeros(n), np.zeros(n)
         else:
             _check_cuda(A, q, b, c)
-            x = torch.zeros(n, dtype=torch.float64, device=A.device)
-            y = torch.zeros(m, dtype=torch.float64, device=A.device)
-            z = torch.zeros(n, dtype=torch.float64, device=A.device)
-        qp = QP(m, n, _ptr(A), lda, _ptr(q), _ptr(b), _ptr(c), 1 if host else 0, structure, nd if structure else 0)
+            if vtype is not None and (not isinstance(vtype, torch.Tensor) or vtype.dtype != torch.int8
+                                      or not vtype.is_cuda or not vtype.is_contiguous()):
+                raise TypeError("vtype must be a contiguous int8 CUDA tensor")
+            if ub is not None:
+                _check_cuda(ub)
+            mk = lambda k: torch.zeros(k, dtype=torch.float64, device=A.device)  # noqa: E731
+            x, y, z, w, s = mk(n), mk(m), mk(n), mk(n), mk(n)
+        qp = QP(m, n, _ptr(A), lda, _ptr(q), _ptr(b), _ptr(c), 1 if host else 0, structure, nd if structure else 0,
+                _ptr(vtype) if vtype is not None else None, _ptr(ub) if ub is not None else None)
         recs = (IterRecord * max_records)()
         rep = Report()
         rep.max_records = max_records
         rep.records = C.cast(recs, C.POINTER(IterRecord))
-        sol = Solution(_ptr(x), _ptr(y), _ptr(z), 0.0, 0.0)
+        sol = Solution(_ptr(x), _ptr(y), _ptr(z), 0.0, 0.0, _ptr(w), _ptr(s))
         rc = self.lib.nys_ipppmm_solve(self.h, C.byref(qp), C.byref(opts), C.byref(sol), C.byref(rep))
         if rc not in (0, -5):
             raise NysError(rc, self.lib.nys_last_error(self.h).decode())
         log = [{f: getattr(recs[i], f) for f, _ in IterRecord._fields_} for i in range(rep.n_records)]
-        return {"x": x, "y": y, "z": z, "obj": sol.obj, "dual_obj": sol.dual_obj, "status": rep.status,
+        return {"x": x, "y": y, "z": z, "w": w, "s": s, "obj": sol.obj, "dual_obj": sol.dual_obj, "status": rep.status,
                 "outer": rep.outer_iters, "inner": rep.inner_iters, "rel_p": rep.rel_p, "rel_d": rep.rel_d,
                 "mu": rep.mu, "t_total_ms": rep.t_total_ms, "t_sketch_ms": rep.t_sketch_ms,
                 "t_pcg_ms": rep.t_pcg_ms, "t_other_ms": rep.t_other_ms, "matvecs": rep.matvecs,

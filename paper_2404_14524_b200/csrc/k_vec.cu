@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256) dots_kernel(const DotArgs D) {
     *D.counter = 0u;
     if (D.post == DP_MUAFF) {
       // mu_aff = (x + ap dx)^T (z + ad dz) / n_total ; mu~ = mu_aff^3 / mu^2
-      const double muaff = D.sc[D.out[0]] / D.post_a;
+      const double muaff = D.post_a > 0 ? (D.sc[D.out[0]] + (D.nv > 1 ? D.sc[D.out[1]] : 0.0)) / D.post_a : 0.0;
       const double mu = D.sc[S_MUCUR];
       D.sc[S_MUAFF] = muaff;
       D.sc[S_MUT] = muaff * muaff * muaff / (mu * mu);
@@ -140,13 +140,19 @@ int launch_dots(nys_ctx* ctx, int64_t n, int nv, const double* const* a, const d
 }
 
 int launch_muaff(nys_ctx* ctx, int64_t n, const double* x, const double* dx, const double* z, const double* dz,
-                 double n_total, int counter_slot) {
+                 double n_total, int counter_slot, const double* w, const double* dw, const double* s,
+                 const double* ds) {
   DotArgs D{};
-  D.nv = 1; D.n = n;
+  D.nv = w ? 2 : 1; D.n = n;
   for (int k = 0; k < 4; ++k) { D.sa[k] = -1; D.sb[k] = -1; }
   D.a[0] = x; D.da[0] = dx; D.sa[0] = S_AP;
   D.b[0] = z; D.db[0] = dz; D.sb[0] = S_AD;
   D.out[0] = S_TMP7;
+  if (w) {  // general form (f1): + (w + ap dw)^T (s + ad ds) on J (w, s, dw, ds are 0 off J)
+    D.a[1] = w; D.da[1] = dw; D.sa[1] = S_AP;
+    D.b[1] = s; D.db[1] = ds; D.sb[1] = S_AD;
+    D.out[1] = S_TMP6;
+  }
   D.sc = ctx->sc;
   const int g = reduce_grid(ctx, n);
   D.part = ctx->wsd("dot_part", (size_t)4 * g);
@@ -158,14 +164,14 @@ int launch_muaff(nys_ctx* ctx, int64_t n, const double* x, const double* dx, con
   return ctx->check_launch("muaff");
 }
 
-__global__ void muaff_post_kernel(double* sc, double n_total) {
-  const double muaff = sc[S_TMP7] / n_total;
+__global__ void muaff_post_kernel(double* sc, double n_total, int gen) {
+  const double muaff = n_total > 0 ? (sc[S_TMP7] + (gen ? sc[S_TMP6] : 0.0)) / n_total : 0.0;
   const double mu = sc[S_MUCUR];
   sc[S_MUAFF] = muaff;
   sc[S_MUT] = muaff * muaff * muaff / (mu * mu);
 }
-int launch_muaff_post(nys_ctx* ctx, double n_total) {
-  muaff_post_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc, n_total);
+int launch_muaff_post(nys_ctx* ctx, double n_total, int gen) {
+  muaff_post_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc, n_total, gen);
   ctx->launches++;
   return ctx->check_launch("muaff_post");
 }

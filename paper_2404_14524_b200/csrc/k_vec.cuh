@@ -49,11 +49,36 @@ int launch_gaussian(nys_ctx* ctx, double* O, int64_t total, uint64_t seed, uint6
 int launch_dots(nys_ctx* ctx, int64_t n, int nv, const double* const* a, const double* const* b, const int* out,
                 int counter_slot);
 int launch_muaff(nys_ctx* ctx, int64_t n, const double* x, const double* dx, const double* z, const double* dz,
-                 double n_total, int counter_slot);
-int launch_muaff_post(nys_ctx* ctx, double n_total);
+                 double n_total, int counter_slot, const double* w = nullptr, const double* dw = nullptr,
+                 const double* s = nullptr, const double* ds = nullptr);
+int launch_muaff_post(nys_ctx* ctx, double n_total, int gen = 0);
 int launch_ratio(nys_ctx* ctx, int64_t n, const double* x, double* dx, const double* dx1, const double* dx2,
                  const double* z, double* dz, const double* dz1, const double* dz2, int counter_slot);
 int launch_steps_post(nys_ctx* ctx);
+// general form (f1, k_gen.cu): vt[j] 0 = I, 1 = F, 2 = J
+int launch_gen_scaling(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* q, const double* x, const double* z,
+                       const double* w, const double* s, double rho, double* d);
+int launch_gen_pred_rhs(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* ub, const double* x, const double* z,
+                        const double* w, const double* s, const double* zeta, const double* rD, double rho,
+                        const double* d, double* rd, double* rxz, double* ru, double* rws, double* xiau, double* t);
+int launch_gen_corr_rhs(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* x, const double* w, const double* dxp,
+                        const double* dzp, const double* dwp, const double* dsp, const double* d, double* rxz,
+                        double* ru, double* rws, double* xiau, double* t);
+int launch_gen_recover(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* x, const double* z, const double* w,
+                       const double* s, const double* dx, const double* rxz, const double* ru, const double* rws,
+                       double* dz, double* dw, double* ds);
+int launch_gen_ratio(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* x, const double* z, const double* w,
+                     const double* s, double* dx, double* dz, double* dw, double* ds, const double* dx1,
+                     const double* dx2, const double* dz1, const double* dz2, const double* dw1, const double* dw2,
+                     const double* ds1, const double* ds2, int counter_slot);
+int launch_gen_ru(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* ub, const double* x, const double* w,
+                  double* ru);
+int launch_gen_init_stats(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* ub, double* x, double* z, double* w,
+                          double* s, double* st);
+int launch_gen_init_apply(nys_ctx* ctx, int64_t n, const int8_t* vt, double* x, double* z, double* w, double* s,
+                          double dpt, double ddt);
+int launch_gen_half_u(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* ub, double scale, double* v);
+int launch_gen_check(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* ub, unsigned long long* bad);
 int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, const double* rhs, const double* p,
                       const double* w, const FusedPartials* fp, double delta, const double* e, const double* U,
                       int64_t ldu, int ell, const double* s, double* h, int max_iter,

@@ -714,6 +714,33 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_CUDA_TRY(ctx, cudaMemcpyAsync(bd, qp_in->b, m * 8, cudaMemcpyHostToDevice, ctx->stream));
     A = Ad; lda = ldd; q = qd; b = bd; c = cd;
   }
+  // ---- free / box variables (f1, (P~)/(D~)) ---------------------------------------
+  const bool gen = qp_in->vtype != nullptr;
+  const int8_t* vt = qp_in->vtype;
+  const double* ub = qp_in->ub;
+  if (gen && qp_in->host_ptrs && n > 0) {
+    int8_t* vtd = (int8_t*)ctx->ws("ipm_vt", (size_t)np_ + 16);
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(vtd, qp_in->vtype, n, cudaMemcpyHostToDevice, ctx->stream));
+    vt = vtd;
+    if (qp_in->ub) {
+      double* ubd = ctx->wsd("ipm_ub", (size_t)np_ + 2);
+      NYS_CUDA_TRY(ctx, cudaMemcpyAsync(ubd, qp_in->ub, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+      ub = ubd;
+    }
+  }
+  if (gen) {
+    unsigned long long* bad = (unsigned long long*)ctx->ws("chk_bad", 8);
+    unsigned long long hv = 0;
+    NYS_CUDA_TRY(ctx, cudaMemsetAsync(bad, 0, 8, ctx->stream));
+    NYS_TRY(launch_gen_check(ctx, n, vt, ub, bad));
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(&hv, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (hv != 0) {
+      ctx->set_error("nys_ipppmm_solve: vtype not in {0,1,2} or ub_J not finite and > 0 (" + std::to_string(hv) +
+                     " entries)");
+      return NYS_EINVAL;
+    }
+  }
   // ---- iterate and work vectors ------------------------------------------------------------
   const size_t nn = (size_t)np_ + 2, mm = (size_t)mp;
   double *x = ctx->wsd("ipm_x", nn), *z = ctx->wsd("ipm_z", nn), *zeta = ctx->wsd("ipm_zeta", nn);
@@ -722,6 +749,15 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   double *dxp = ctx->wsd("ipm_dxp", nn), *dzp = ctx->wsd("ipm_dzp", nn), *dxc = ctx->wsd("ipm_dxc", nn);
   double *dzc = ctx->wsd("ipm_dzc", nn), *dx = ctx->wsd("ipm_dx", nn), *dz = ctx->wsd("ipm_dz", nn);
   double *ones = ctx->wsd("ipm_ones", nn);
+  // general form: w, s, r_u, r_ws and the w / s directions (0 off J)
+  double *w = nullptr, *sv = nullptr, *ru = nullptr, *rws = nullptr, *dwp = nullptr, *dsp = nullptr;
+  double *dwc = nullptr, *dsc = nullptr, *dw = nullptr, *ds = nullptr;
+  if (gen) {
+    w = ctx->wsd("ipm_w", nn); sv = ctx->wsd("ipm_sv", nn); ru = ctx->wsd("ipm_ru", nn);
+    rws = ctx->wsd("ipm_rws", nn); dwp = ctx->wsd("ipm_dwp", nn); dsp = ctx->wsd("ipm_dsp", nn);
+    dwc = ctx->wsd("ipm_dwc", nn); dsc = ctx->wsd("ipm_dsc", nn); dw = ctx->wsd("ipm_dw", nn);
+    ds = ctx->wsd("ipm_ds", nn);
+  }
   double *y = ctx->wsd("ipm_y", mm), *lam = ctx->wsd("ipm_lam", mm), *ax = ctx->wsd("ipm_ax", mm);
   double *rP = ctx->wsd("ipm_rP", mm), *rp = ctx->wsd("ipm_rp", mm), *xi = ctx->wsd("ipm_xi", mm);
   double *dyp = ctx->wsd("ipm_dyp", mm), *dyc = ctx->wsd("ipm_dyc", mm), *u1 = ctx->wsd("ipm_u1", mm);
@@ -754,9 +790,16 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   // ---- norms of b and c ------------------------------------------------------------------
   NYS_TRY(D.dot(m, b, b, S_BNORM));
   NYS_TRY(D.dot(n, c, c, S_TMP4));
-  NYS_TRY(allreduce_slots(ctx, S_TMP4, 1));
+  if (gen) {                                                         // t = -u_J / 2 ; ||u_J||^2 = 4 ||t||^2 (G1)
+    NYS_TRY(launch_gen_half_u(ctx, n, vt, ub, -0.5, t));
+    NYS_TRY(D.dot(n, t, t, S_TMP5));
+  } else {
+    NYS_TRY(launch_set_slots(ctx, S_TMP5, 0.0));
+  }
+  NYS_TRY(allreduce_slots(ctx, S_TMP4, 2));
   NYS_TRY(read_slots(ctx));
-  const double bnorm = std::sqrt(ctx->h_sc[S_BNORM]);
+  const double bnorm = std::sqrt(ctx->h_sc[S_BNORM] + 4.0 * ctx->h_sc[S_TMP5]);
+  if (gen) NYS_TRY(launch_set_slots(ctx, S_BNORM, bnorm * bnorm));  // ||[b; u_J]||^2 for the PCG tolerance (G1)
   const double cnorm = std::sqrt(ctx->h_sc[S_TMP4]);
   int total_inner = 0;
 
@@ -781,11 +824,17 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   const CholFactors* cfp = use_chol ? &CF : nullptr;
   auto tp = std::chrono::steady_clock::now();
   PcgResult pr;
-  NYS_TRY(D.dot(m, b, b, S_XINORM));
+  const double* rhs0 = b;
+  if (gen) {                                                         // App. B.2: rhs = b - A u / 2
+    NYS_TRY(AO.Ax(t, xi, b));
+    rhs0 = xi;
+  }
+  NYS_TRY(D.dot(m, rhs0, rhs0, S_XINORM));
   NYS_TRY(launch_pcg_setup(ctx, 2, 0, 0, 0, S_XINORM, 0, 0, opt->init_tol_rel));
-  NYS_TRY(pcg_impl(ctx, op0, ell, U, mp, scoef, b, u1, opt->pcg_max_iter, pr, cfp));
+  NYS_TRY(pcg_impl(ctx, op0, ell, U, mp, scoef, rhs0, u1, opt->pcg_max_iter, pr, cfp));
   total_inner += pr.iters;
-  NYS_TRY(AO.At_plain(u1, x));                                       // x~ = A^T u1
+  NYS_TRY(AO.At_plain(u1, x));                                       // x~ = A^T u1 (+ u/2)
+  if (gen) NYS_TRY(launch_axpby(ctx, n, 1.0, x, -1.0, t, x));
   NYS_TRY(launch_cpqx(ctx, n, c, q, x, t));                          // c + Q x~
   NYS_TRY(AO.Ax(t, xi, nullptr));                                    // A (c + Q x~)
   NYS_TRY(D.dot(m, xi, xi, S_XINORM));
@@ -794,6 +843,23 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   total_inner += pr.iters;
   t_pcg += ms_since(tp);
   NYS_TRY(AO.At_rd(y, c, q, x, nullptr, z));                         // z~ = c - A^T y~ + Q x~
+  if (gen) {                                                         // App. B.2 with w, s (G2, G3)
+    NYS_TRY(launch_gen_init_stats(ctx, n, vt, ub, x, z, w, sv, ctx->sc + S_G0));
+    NYS_TRY(allreduce_slots(ctx, S_G0, 4, true));
+    NYS_TRY(allreduce_slots(ctx, S_G4, 8));
+    NYS_TRY(read_slots(ctx));
+    const double* G = ctx->h_sc + S_G0;
+    const double mx = G[0], mw = G[1], mz = G[2], ms = G[3], sx = G[4], sw = G[5], sz = G[6], ss = G[7];
+    const double xz = G[8], ws = G[9], nij = G[10], nj = G[11];
+    const double dp = std::max(-1.5 * std::min(mx, mw), 0.0);       // P:1468 over x~_IJ and w~_J
+    const double dd = std::max(-1.5 * std::min(mz, ms), 0.0);       // P:1469 over z~_IJ and s~_J
+    const double gam = xz + dd * sx + dp * sz + nij * dp * dd + ws + dd * sw + dp * ss + nj * dp * dd;
+    const double den_p = sz + nij * dd + ss + nj * dd, den_d = sx + nij * dp + sw + nj * dp;   // G2
+    const double dpt = dp + (den_p > 0 ? 0.5 * gam / den_p : 0.0);
+    const double ddt = dd + (den_d > 0 ? 0.5 * gam / den_d : 0.0);
+    NYS_TRY(launch_gen_init_apply(ctx, n, vt, x, z, w, sv, dpt, ddt));
+    n_total = nij + nj;                                               // mu = (x^T z + w^T s) / (|IJ| + |J|)
+  } else {
   NYS_TRY(launch_minsum(ctx, n, x, 0.0, S_TMP0, S_TMP1, 6));
   NYS_TRY(launch_minsum(ctx, n, z, 0.0, S_TMP2, S_TMP3, 7));
   NYS_TRY(D.dot(n, x, z, S_TMP4));
@@ -819,6 +885,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(launch_shift(ctx, n, x, dpt));
     NYS_TRY(launch_shift(ctx, n, z, ddt));
   }
+  }
   // ---- PMM parameters --------------------------------------------------------------
   NYS_CUDA_TRY(ctx, cudaMemcpyAsync(lam, y, m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   if (n > 0) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(zeta, x, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -829,16 +896,26 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(AO.Ax(x, ax, nullptr));
     NYS_TRY(launch_axpby(ctx, m, 1.0, b, -1.0, ax, rP));
     NYS_TRY(AO.At_rd(y, c, q, x, z, rD));
+    if (gen) {                                                        // G1: r_D += s ; r_U = u - x - w on J
+      NYS_TRY(launch_axpby(ctx, n, 1.0, rD, 1.0, sv, rD));
+      NYS_TRY(launch_gen_ru(ctx, n, vt, ub, x, w, ru));
+      NYS_TRY(D.dot(n, ru, ru, S_TMP3));
+      NYS_TRY(D.dot(n, w, sv, S_TMP4));
+    } else {
+      NYS_TRY(launch_set_slots(ctx, S_TMP3, 0.0, S_TMP4, 0.0));
+    }
     NYS_TRY(D.dot(m, rP, rP, S_TMP0));
     NYS_TRY(D.dot(n, rD, rD, S_TMP1));
     NYS_TRY(D.dot(n, x, z, S_TMP2));
-    NYS_TRY(allreduce_slots(ctx, S_TMP1, 2));
+    NYS_TRY(allreduce_slots(ctx, S_TMP1, gen ? 4 : 2));
     NYS_TRY(read_slots(ctx));
+    ctx->h_sc[S_TMP0] += ctx->h_sc[S_TMP3];                           // ||[r_P; r_U]||^2
+    ctx->h_sc[S_TMP2] += ctx->h_sc[S_TMP4];                           // x^T z + w^T s
     return NYS_OK;
   };
   NYS_TRY(residuals());
   double nrP = std::sqrt(ctx->h_sc[S_TMP0]), nrD = std::sqrt(ctx->h_sc[S_TMP1]);
-  double mu = ctx->h_sc[S_TMP2] / n_total;
+  double mu = n_total > 0 ? ctx->h_sc[S_TMP2] / n_total : 0.0;
   double nrP_ref = nrP, nrD_ref = nrD;
   int status = NYS_EMAXITER;
   int k = 0;
@@ -852,7 +929,8 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     nys_iter_record rec{};
     rec.k = k; rec.mu = mu; rec.rel_p = rel_p; rec.rel_d = rel_d; rec.rho = rho; rec.delta = delta;
     auto t_it = std::chrono::steady_clock::now();
-    NYS_TRY(launch_scaling(ctx, n, q, x, z, rho, d));
+    if (gen) NYS_TRY(launch_gen_scaling(ctx, n, vt, q, x, z, w, sv, rho, d));
+    else NYS_TRY(launch_scaling(ctx, n, q, x, z, rho, d));
     NormalOp op;
     NYS_TRY(AO.normal_op(d, delta, op));
     if (use_chol) {                                                   // P:250-349, every iteration
@@ -881,7 +959,8 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     }
     NYS_TRY(launch_set_slots(ctx, S_MUCUR, mu));
     // ---- predictor ----
-    NYS_TRY(launch_pred_rhs_n(ctx, n, x, z, zeta, rD, rho, d, rd, rxz, xiau, t));
+    if (gen) NYS_TRY(launch_gen_pred_rhs(ctx, n, vt, ub, x, z, w, sv, zeta, rD, rho, d, rd, rxz, ru, rws, xiau, t));
+    else NYS_TRY(launch_pred_rhs_n(ctx, n, x, z, zeta, rD, rho, d, rd, rxz, xiau, t));
     NYS_TRY(launch_pred_rhs_m(ctx, m, b, ax, y, lam, delta, rp));
     NYS_TRY(AO.Ax(t, xi, rp));                                        // xi = r_p + A d (r_d + xi_au)
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
@@ -892,16 +971,24 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
     rec.pcg_pred = pr.iters;
     NYS_TRY(AO.At_dx(dyp, rd, xiau, rxz, z, x, d, dxp, dzp));        // dx, dz (A15)
-    NYS_TRY(launch_ratio(ctx, n, x, dxp, nullptr, nullptr, z, dzp, nullptr, nullptr, 8));
+    if (gen) {
+      NYS_TRY(launch_gen_recover(ctx, n, vt, x, z, w, sv, dxp, rxz, ru, rws, dzp, dwp, dsp));   // Alg. 4 line 3
+      NYS_TRY(launch_gen_ratio(ctx, n, vt, x, z, w, sv, dxp, dzp, dwp, dsp, nullptr, nullptr, nullptr, nullptr,
+                               nullptr, nullptr, nullptr, nullptr, 8));
+    } else {
+      NYS_TRY(launch_ratio(ctx, n, x, dxp, nullptr, nullptr, z, dzp, nullptr, nullptr, 8));
+    }
     NYS_TRY(allreduce_slots(ctx, S_TMP0, 2, true));
     NYS_TRY(launch_steps_post(ctx));
-    NYS_TRY(launch_muaff(ctx, n, x, dxp, z, dzp, n_total, 9));
+    NYS_TRY(launch_muaff(ctx, n, x, dxp, z, dzp, n_total, 9, w, dwp, sv, dsp));
     if (ctx->world > 1) {
-      NYS_TRY(allreduce_slots(ctx, S_TMP7, 1));
-      NYS_TRY(launch_muaff_post(ctx, n_total));
+      if (gen) NYS_TRY(allreduce_slots(ctx, S_TMP6, 2));
+      else NYS_TRY(allreduce_slots(ctx, S_TMP7, 1));
+      NYS_TRY(launch_muaff_post(ctx, n_total, gen ? 1 : 0));
     }
     // ---- corrector ----
-    NYS_TRY(launch_corr_rhs(ctx, n, x, dxp, dzp, d, rxz, xiau, t));
+    if (gen) NYS_TRY(launch_gen_corr_rhs(ctx, n, vt, x, w, dxp, dzp, dwp, dsp, d, rxz, ru, rws, xiau, t));
+    else NYS_TRY(launch_corr_rhs(ctx, n, x, dxp, dzp, d, rxz, xiau, t));
     NYS_TRY(AO.Ax(t, xi, nullptr));
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
     NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
@@ -914,15 +1001,21 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     if (base_its < 0) base_its = last_its;
     NYS_TRY(AO.At_dx(dyc, nullptr, xiau, rxz, z, x, d, dxc, dzc));
     // ---- combine, stepsizes, update ----
-    NYS_TRY(launch_ratio(ctx, n, x, dx, dxp, dxc, z, dz, dzp, dzc, 8));
+    if (gen) {
+      NYS_TRY(launch_gen_recover(ctx, n, vt, x, z, w, sv, dxc, rxz, ru, rws, dzc, dwc, dsc));
+      NYS_TRY(launch_gen_ratio(ctx, n, vt, x, z, w, sv, dx, dz, dw, ds, dxp, dxc, dzp, dzc, dwp, dwc, dsp, dsc, 8));
+    } else {
+      NYS_TRY(launch_ratio(ctx, n, x, dx, dxp, dxc, z, dz, dzp, dzc, 8));
+    }
     NYS_TRY(allreduce_slots(ctx, S_TMP0, 2, true));
     NYS_TRY(launch_steps_post(ctx));
     NYS_TRY(launch_update_n(ctx, n, x, dx, z, dz));
+    if (gen) NYS_TRY(launch_update_n(ctx, n, w, dw, sv, ds));         // w += ap dw ; s += ad ds
     NYS_TRY(launch_update_m(ctx, m, y, dyp, dyc));
     NYS_TRY(residuals());
     rec.alpha_p = ctx->h_sc[S_AP];
     rec.alpha_d = ctx->h_sc[S_AD];
-    const double mu_new = ctx->h_sc[S_TMP2] / n_total;
+    const double mu_new = n_total > 0 ? ctx->h_sc[S_TMP2] / n_total : 0.0;
     nrP = std::sqrt(ctx->h_sc[S_TMP0]);
     nrD = std::sqrt(ctx->h_sc[S_TMP1]);
     // ---- PEU (A12) ----
@@ -955,16 +1048,30 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(D.dot(n, x, qx, S_TMP3));
     NYS_TRY(D.dot(n, c, x, S_TMP4));
     NYS_TRY(D.dot(m, b, y, S_TMP5));
+    if (gen) {                                                        // u_J^T s_J
+      NYS_TRY(launch_gen_half_u(ctx, n, vt, ub, 1.0, xiau));
+      NYS_TRY(D.dot(n, xiau, sv, S_TMP6));
+      NYS_TRY(allreduce_slots(ctx, S_TMP6, 1));
+    } else {
+      NYS_TRY(launch_set_slots(ctx, S_TMP6, 0.0));
+    }
     NYS_TRY(allreduce_slots(ctx, S_TMP3, 2));
     NYS_TRY(read_slots(ctx));
-    const double xqx = ctx->h_sc[S_TMP3], cx = ctx->h_sc[S_TMP4], by = ctx->h_sc[S_TMP5];
+    const double xqx = ctx->h_sc[S_TMP3], cx = ctx->h_sc[S_TMP4], by = ctx->h_sc[S_TMP5], us = ctx->h_sc[S_TMP6];
     if (sol) {
       sol->obj = 0.5 * xqx + cx;
-      sol->dual_obj = by - 0.5 * xqx;
+      sol->dual_obj = by - 0.5 * xqx - us;
       const cudaMemcpyKind kind = qp_in->host_ptrs ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
       if (sol->x && n > 0) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(sol->x, x, n * 8, kind, ctx->stream));
       if (sol->z && n > 0) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(sol->z, z, n * 8, kind, ctx->stream));
       if (sol->y) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(sol->y, y, m * 8, kind, ctx->stream));
+      for (int k2 = 0; k2 < 2; ++k2) {                                // w, s (0 for the all-I form)
+        double* dst = k2 == 0 ? sol->w : sol->s;
+        if (!dst || n <= 0) continue;
+        if (gen) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(dst, k2 == 0 ? w : sv, n * 8, kind, ctx->stream));
+        else if (qp_in->host_ptrs) memset(dst, 0, n * 8);
+        else NYS_CUDA_TRY(ctx, cudaMemsetAsync(dst, 0, n * 8, ctx->stream));
+      }
       NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     }
   }
@@ -1343,6 +1450,10 @@ int nys_ipppmm_solve(nys_ctx* ctx, const nys_qp* qp, const nys_options* opt, nys
   }
   if (qp->structure != 0 && (qp->structure != 1 || qp->nd < 0 || qp->n != 2 * qp->nd + 2 * qp->m)) {
     ctx->set_error("nys_ipppmm_solve: structure 1 needs n = 2 nd + 2 m");
+    return NYS_EINVAL;
+  }
+  if (qp->vtype && qp->structure != 0) {
+    ctx->set_error("nys_ipppmm_solve: vtype (free / box variables) needs structure 0");
     return NYS_EINVAL;
   }
   if (!qp->host_ptrs) NYS_TRY(check_A(ctx, qp->m, qp->structure == 1 ? qp->nd : qp->n, qp->A, qp->lda));

@@ -38,6 +38,8 @@ enum Slot : int {
   S_TMP0, S_TMP1, S_TMP2, S_TMP3, S_TMP4, S_TMP5, S_TMP6, S_TMP7,
   S_AP, S_AD, S_MUAFF, S_MUT, S_MUCUR, S_XINORM, S_BNORM,
   S_NU, S_SHIFT, S_CHOLFAIL, S_FRO, S_JSWEEPS, S_DELTA, S_GITER,
+  // general-form initial point statistics (f1, gen_init_stats): 4 minima then 8 sums
+  S_G0, S_G1, S_G2, S_G3, S_G4, S_G5, S_G6, S_G7, S_G8, S_G9, S_G10, S_G11,
   S_COUNT = 64
 };
 constexpr int kMaxCounters = 64;

@@ -153,6 +153,35 @@ def make_config(idx: int, m: Optional[int] = None, n: Optional[int] = None,
     raise ValueError(f"unknown config {idx}")
 
 
+def make_general(m: int, n: int, frac_free: float = 0.2, frac_box: float = 0.3, ell: int = 20,
+                 seed: int = 10) -> QPInstance:
+    """Problem (P~)/(D~) with mixed variable types, SURVEY §8(f) f1 (the paper gives no
+    workload; config 0's recipe extended).  vtype: 0 = I, 1 = F, 2 = J; A_ij ~ N(0, 1/n); q ~ U(0, 1);
+    strictly feasible primal x0 (I: U(0.5,1.5), F: N(0,1), J: u U(0.2,0.8) with u ~ U(1,3)) and dual
+    (y0 ~ N(0,1), z0_IJ ~ U(0.5,1.5), s0_J ~ U(0.5,1.5)), b = A x0, c = A^T y0 + z0 - s0 - q x0.
+    Draw order: A, vtype-permutation, q, u, x0 parts, y0, z0, s0.  extra = {"vtype", "ub"}."""
+    rng = np.random.default_rng(seed)
+    A = gaussian_matrix(rng, m, n, 1.0 / np.sqrt(n))
+    nf, nb = int(round(frac_free * n)), int(round(frac_box * n))
+    perm = rng.permutation(n)
+    vtype = np.zeros(n, dtype=np.int8)
+    vtype[perm[:nf]] = 1
+    vtype[perm[nf:nf + nb]] = 2
+    F, J = vtype == 1, vtype == 2
+    q = rng.uniform(0.0, 1.0, n)
+    ub = np.where(J, rng.uniform(1.0, 3.0, n), 0.0)
+    x0 = rng.uniform(0.5, 1.5, n)
+    x0[F] = rng.standard_normal(int(F.sum()))
+    x0[J] = ub[J] * rng.uniform(0.2, 0.8, int(J.sum()))
+    y0 = rng.standard_normal(m)
+    z0 = np.where(F, 0.0, rng.uniform(0.5, 1.5, n))
+    s0 = np.where(J, rng.uniform(0.5, 1.5, n), 0.0)
+    b = A @ x0
+    c = A.T @ y0 + z0 - s0 - q * x0
+    return QPInstance(f"gen_m{m}_n{n}_f{nf}_j{nb}", -1, A, q, b, c, ell, x0, y0, z0,
+                      extra={"vtype": vtype, "ub": ub, "s0": s0})
+
+
 def svm_dense_A(inst: QPInstance) -> np.ndarray:
     """Materialise A = [Xt, -Xt, I, -I] for SMALL SVM instances only (tests)."""
     Xt = inst.extra["Xt"]

@@ -68,3 +68,19 @@ def test_config4_slice_is_restriction_of_the_generator():
     sl = large.generate_shard(m, n, 0, n, n_gen=n_gen)
     assert torch.equal(sl.At, full.At[:n])
     assert torch.equal(sl.q, full.q[:n]) and torch.equal(sl.x0, full.x0[:n]) and torch.equal(sl.y0, full.y0)
+
+
+def test_make_general_is_strictly_feasible():
+    """f1 generator: x0 interior on I and J, z0_F = 0, and (x0, y0, z0, s0) satisfy (P~)/(D~) exactly."""
+    from synth import make_general
+    inst = make_general(30, 90, 0.2, 0.3, ell=4, seed=3)
+    vt, u = inst.extra["vtype"], inst.extra["ub"]
+    I, F, J = vt == 0, vt == 1, vt == 2
+    assert vt.dtype == np.int8 and F.sum() == 18 and J.sum() == 27
+    assert np.all(inst.x0[I] > 0) and np.all(inst.x0[J] > 0) and np.all(inst.x0[J] < u[J])
+    assert np.all(inst.z0[F] == 0) and np.all(inst.z0[~F] > 0) and np.all(u[~J] == 0)
+    s0 = inst.extra["s0"]
+    assert np.allclose(inst.A @ inst.x0, inst.b, atol=1e-12)
+    assert np.allclose(inst.c + inst.q * inst.x0 - inst.A.T @ inst.y0 - inst.z0 + s0, 0, atol=1e-12)
+    again = make_general(30, 90, 0.2, 0.3, ell=4, seed=3)
+    assert np.array_equal(again.A, inst.A) and np.array_equal(again.extra["vtype"], vt)
