@@ -178,6 +178,12 @@ int nys_pcg_solve(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t l
  *   A11-A12.  The preconditioner is rebuilt every outer iteration from a fresh
  *   Omega_k (Philox, stream k+1; the initial point uses stream 0).
  * ------------------------------------------------------------------------------------- */
+typedef struct nys_unit_block {
+  int64_t row0;          /* row of the block's first column                                 */
+  int64_t count;         /* columns in the block (rows row0 .. row0 + count - 1)           */
+  double  scale;         /* nonzero entry of every column (e.g. +1, -1)                     */
+} nys_unit_block;
+
 typedef struct {
   int64_t m, n;          /* rows; LOCAL column count on this rank                          */
   const double* A;       /* m x n column-major, lda (see conventions)                      */
@@ -190,15 +196,27 @@ typedef struct {
                             A23): A = [Xt, -Xt, I_m, -I_m] with the dense block Xt (m x nd,
                             column-major, lda) passed in `A`; n = 2 nd + 2 m variables ordered
                             [w+, w-, xi, s].  The identity blocks are never materialised: they
-                            contribute the diagonal term e = d_xi + d_s of the normal operator.   */
-  int64_t nd;            /* structure 1: number of dense columns (features) d              */
+                            contribute the diagonal term e = d_xi + d_s of the normal operator.
+                            Single rank.  2: dense block + scaled identity blocks (below).         */
+  int64_t nd;            /* structure 1 / 2: number of dense columns stored in `A`          */
   /* Free and box-constrained variables, problem (P~)/(D~) (Alg. 5; SURVEY
    * §8(f) f1).  vtype == NULL: every variable is in I (x >= 0), the form (P)/(D).  Otherwise
    * vtype[j] (n local entries, int8) is 0 for j in I (x_j >= 0), 1 for j in F (free), 2 for j in J
    * (0 <= x_j <= ub[j]); ub (n local doubles) is read on J only and may be NULL when no entry is 2.
-   * Same memory space as A (host_ptrs).  Not combined with structure 1 (NYS_EINVAL).            */
+   * Same memory space as A (host_ptrs).  Works with every `structure`.                         */
   const int8_t* vtype;
   const double* ub;
+  /* structure 2: A = [B, S_0, ..., S_{K-1}] with the dense block B (m x nd, column-major, lda) in
+   * `A` and K <= 8 scaled identity blocks S_k = scale_k [e_{row0_k}, ..., e_{row0_k + count_k - 1}]
+   * (never materialised); variables ordered [B columns, S_0 columns, S_1 columns, ...], so
+   * n = nd + sum_k count_k (this rank's local columns; each rank passes its own blocks).  The blocks
+   * contribute the diagonal term e_i = sum_k scale_k^2 d_j of the normal operator and the
+   * elementwise parts of A u and A^T y.  This is the shape of the paper's own QP formulations:
+   * dual SVM A = [I_d, -X diag(y); 0, y^T] (App. C.2: dense block [-X diag(y); y^T],
+   * one identity block) and the factor-model portfolio (App. C.1: identity blocks for
+   * the free factor variables and the slacks).  unit_blocks is a HOST array.                    */
+  int n_unit_blocks;
+  const struct nys_unit_block* unit_blocks;
 } nys_qp;
 
 typedef struct {

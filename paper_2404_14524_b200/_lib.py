@@ -36,10 +36,15 @@ class PcgInfo(C.Structure):
                 ("true_res_norm", C.c_double), ("t_ms", C.c_double)]
 
 
+class UnitBlock(C.Structure):
+    _fields_ = [("row0", C.c_int64), ("count", C.c_int64), ("scale", C.c_double)]
+
+
 class QP(C.Structure):
     _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("A", C.c_void_p), ("lda", C.c_int64), ("q", C.c_void_p),
                 ("b", C.c_void_p), ("c", C.c_void_p), ("host_ptrs", C.c_int), ("structure", C.c_int),
-                ("nd", C.c_int64), ("vtype", C.c_void_p), ("ub", C.c_void_p)]
+                ("nd", C.c_int64), ("vtype", C.c_void_p), ("ub", C.c_void_p), ("n_unit_blocks", C.c_int),
+                ("unit_blocks", C.POINTER(UnitBlock))]
 
 
 class Options(C.Structure):
@@ -263,10 +268,12 @@ class Context:
 
     def nys_ipppmm_solve(self, A, lda: int, m: int, q, b, c, ell: int = 0, tol: float = 1e-8, seed: int = 0,
                          max_outer: int = 100, host: bool = False, max_records: int = 256, verbose: bool = False,
-                         structure: int = 0, vtype=None, ub=None, **opt_overrides):
+                         structure: int = 0, vtype=None, ub=None, unit_blocks=None, **opt_overrides):
         """A: device tensor (ncols, lda) [or host numpy when host=True]; q, c: n; b: m.
         structure=1: A holds the dense block Xt (nd columns) of A = [Xt, -Xt, I, -I]; n = 2 nd + 2 m.
-        vtype (int8, n; 0 = I, 1 = F free, 2 = J box) and ub (n, read on J): problem (P~)/(D~), f1."""
+        vtype (int8, n; 0 = I, 1 = F free, 2 = J box) and ub (n, read on J): problem (P~)/(D~), f1.
+        structure=2: A holds the dense block B (nd columns) of A = [B, S_0, ...], unit_blocks =
+        [(row0, count, scale), ...] the scaled identity blocks S_k (nys_unit_block)."""
         import torch
         nd = A.shape[0]
         n = q.shape[0]
@@ -292,8 +299,11 @@ class Context:
                 _check_cuda(ub)
             mk = lambda k: torch.zeros(k, dtype=torch.float64, device=A.device)  # noqa: E731
             x, y, z, w, s = mk(n), mk(m), mk(n), mk(n), mk(n)
+        blocks = list(unit_blocks or [])
+        ub_arr = (UnitBlock * max(1, len(blocks)))(*[UnitBlock(int(r), int(k), float(sc)) for r, k, sc in blocks])
         qp = QP(m, n, _ptr(A), lda, _ptr(q), _ptr(b), _ptr(c), 1 if host else 0, structure, nd if structure else 0,
-                _ptr(vtype) if vtype is not None else None, _ptr(ub) if ub is not None else None)
+                _ptr(vtype) if vtype is not None else None, _ptr(ub) if ub is not None else None, len(blocks),
+                C.cast(ub_arr, C.POINTER(UnitBlock)))
         recs = (IterRecord * max_records)()
         rep = Report()
         rep.max_records = max_records

@@ -259,6 +259,35 @@ __global__ void gen_check_kernel(int64_t n, const int8_t* vt, const double* ub, 
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// structure 2: A = [B, S_0, ..., S_{K-1}], S_k = scale_k [e_{row0_k} ... e_{row0_k + count_k - 1}]
+// (never materialised).  u_unit / d_unit / atv_unit point at the unit part of the n-vectors.
+// ------------------------------------------------------------------------------------------
+// atv_unit[j] = scale_k y[row0_k + j - off_k]  (A^T y on the unit columns)
+__global__ void unit_expand_kernel(UnitBlocks U, const double* y, double* atv_unit) {
+  GRID_STRIDE(j, U.total) {
+    int k = 0;
+    while (k + 1 < U.nb && j >= U.off[k + 1]) ++k;
+    atv_unit[j] = U.scale[k] * y[U.row0[k] + (j - U.off[k])];
+  }
+}
+// out_i = add_i + sum_k [i in block k] scale_k u_unit[off_k + i - row0_k]   (fixed block order)
+// diag mode: out_i = sum_k [i in block k] scale_k^2 d_unit[...]             (the e term)
+__global__ void unit_fold_kernel(UnitBlocks U, int64_t m, const double* u_unit, const double* add, int diag,
+                                 double* out) {
+  GRID_STRIDE(i, m) {
+    double s = add ? add[i] : 0.0;
+    for (int k = 0; k < U.nb; ++k) {
+      const int64_t r = i - U.row0[k];
+      if (r >= 0 && r < U.count[k]) {
+        const double v = u_unit[U.off[k] + r];
+        s += diag ? U.scale[k] * U.scale[k] * v : U.scale[k] * v;
+      }
+    }
+    out[i] = s;
+  }
+}
+
 static int ggrid(nys_ctx* ctx, int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 4 * ctx->num_sms) g = 4 * ctx->num_sms;
@@ -340,6 +369,18 @@ int launch_gen_half_u(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* u
   gen_half_u_kernel<<<ggrid(ctx, n), 256, 0, ctx->stream>>>(n, vt, ub, scale, v);
   ctx->launches++;
   return ctx->check_launch("gen_half_u");
+}
+int launch_unit_expand(nys_ctx* ctx, const UnitBlocks& U, const double* y, double* atv_unit) {
+  if (U.total <= 0) return NYS_OK;
+  unit_expand_kernel<<<ggrid(ctx, U.total), 256, 0, ctx->stream>>>(U, y, atv_unit);
+  ctx->launches++;
+  return ctx->check_launch("unit_expand");
+}
+int launch_unit_fold(nys_ctx* ctx, const UnitBlocks& U, int64_t m, const double* u_unit, const double* add, int diag,
+                     double* out) {
+  unit_fold_kernel<<<ggrid(ctx, m), 256, 0, ctx->stream>>>(U, m, u_unit, add, diag, out);
+  ctx->launches++;
+  return ctx->check_launch("unit_fold");
 }
 int launch_gen_check(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* ub, unsigned long long* bad) {
   if (n <= 0) return NYS_OK;

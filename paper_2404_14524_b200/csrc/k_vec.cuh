@@ -55,6 +55,16 @@ int launch_muaff_post(nys_ctx* ctx, double n_total, int gen = 0);
 int launch_ratio(nys_ctx* ctx, int64_t n, const double* x, double* dx, const double* dx1, const double* dx2,
                  const double* z, double* dz, const double* dz1, const double* dz2, int counter_slot);
 int launch_steps_post(nys_ctx* ctx);
+// structure 2 (k_gen.cu): scaled identity blocks of A (nys_unit_block); off = column offsets in the unit part
+struct UnitBlocks {
+  int nb = 0;
+  int64_t total = 0;
+  int64_t row0[8], count[8], off[8];
+  double scale[8];
+};
+int launch_unit_expand(nys_ctx* ctx, const UnitBlocks& U, const double* y, double* atv_unit);
+int launch_unit_fold(nys_ctx* ctx, const UnitBlocks& U, int64_t m, const double* u_unit, const double* add, int diag,
+                     double* out);
 // general form (f1, k_gen.cu): vt[j] 0 = I, 1 = F, 2 = J
 int launch_gen_scaling(nys_ctx* ctx, int64_t n, const int8_t* vt, const double* q, const double* x, const double* z,
                        const double* w, const double* s, double rho, double* d);

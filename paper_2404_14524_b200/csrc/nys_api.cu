@@ -633,10 +633,17 @@ struct AOps {
   int64_t m, n, nd;        // n = variables; nd = columns of the dense block (n for structure 0)
   const double* A;         // dense block, column-major, lda
   int64_t lda;
-  double *g, *atv, *uw, *addm, *dw, *e;  // structure-1 work vectors
+  double *g, *atv, *uw, *addm, *dw, *e;  // structure-1/2 work vectors
+  UnitBlocks UB;                          // structure 2
   // normal operator for the scaling d (n): dense -> (A, d); structured -> (Xt, d_w+ + d_w-, e)
   int normal_op(const double* d, double delta, NormalOp& op) {
     if (structure == 0) { op = NormalOp{m, n, lda, A, d, nullptr, delta}; return NYS_OK; }
+    if (structure == 2) {                 // e = sum_k scale_k^2 d_unit (global: a replicated term)
+      NYS_TRY(launch_unit_fold(ctx, UB, m, d + nd, nullptr, 1, e));
+      if (ctx->world > 1) NYS_TRY(allreduce(ctx, e, (size_t)m));
+      op = NormalOp{m, nd, lda, A, d, e, delta};
+      return NYS_OK;
+    }
     NYS_TRY(launch_svm_scaling_fold(ctx, nd, m, d, dw, e));
     op = NormalOp{m, nd, lda, A, dw, e, delta};
     return NYS_OK;
@@ -644,14 +651,29 @@ struct AOps {
   // out = A u (+ add)
   int Ax(const double* u, double* out, const double* add) {
     if (structure == 0) return apply_A(ctx, m, n, A, lda, u, out, 1.0, add);
+    if (structure == 2) {
+      if (ctx->world == 1) {              // unit part + add folded into the matvec's add vector
+        NYS_TRY(launch_unit_fold(ctx, UB, m, u + nd, add, 0, addm));
+        return apply_A(ctx, m, nd, A, lda, u, out, 1.0, addm);
+      }
+      NYS_TRY(launch_unit_fold(ctx, UB, m, u + nd, nullptr, 0, addm));   // local partial: before the all-reduce
+      MatvecCall c;
+      c.mode = MV_NONLY; c.m = m; c.n = nd; c.lda = lda; c.A = A; c.u = u; c.out = out; c.sgn = 1.0; c.add = addm;
+      NYS_TRY(launch_matvec(ctx, c));
+      NYS_TRY(allreduce(ctx, out, (size_t)m));
+      if (add) NYS_TRY(launch_axpby(ctx, m, 1.0, out, 1.0, add, out));
+      return NYS_OK;
+    }
     NYS_TRY(launch_svm_fold(ctx, nd, m, u, add, uw, addm));
     return apply_A(ctx, m, nd, A, lda, uw, out, 1.0, addm);
   }
   // structured: atv = A^T y (n-vector)
   int At_vec(const double* y) {
     MatvecCall mc;
-    mc.mode = MV_TONLY; mc.m = m; mc.n = nd; mc.lda = lda; mc.A = A; mc.z = y; mc.tep = TE_PLAIN; mc.t1 = g;
+    mc.mode = MV_TONLY; mc.m = m; mc.n = nd; mc.lda = lda; mc.A = A; mc.z = y; mc.tep = TE_PLAIN;
+    mc.t1 = structure == 2 ? atv : g;
     NYS_TRY(apply_At(ctx, mc));
+    if (structure == 2) return launch_unit_expand(ctx, UB, y, atv + nd);
     return launch_svm_expand(ctx, nd, m, g, y, atv);
   }
   int At_plain(const double* y, double* out) {
@@ -698,7 +720,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   // ---- problem data on the device --------------------------------------------------------
   const double *A = qp_in->A, *q = qp_in->q, *b = qp_in->b, *c = qp_in->c;
   int64_t lda = qp_in->lda;
-  const int64_t ncolA = qp_in->structure == 1 ? qp_in->nd : n;  // dense columns stored
+  const int64_t ncolA = qp_in->structure >= 1 ? qp_in->nd : n;  // dense columns stored
   if (qp_in->host_ptrs) {
     const int64_t ldd = even(m);
     double* Ad = ctx->wsd("ipm_A", (size_t)ldd * (ncolA > 0 ? ncolA : 1));
@@ -766,6 +788,21 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   double *lamh = ctx->wsd("ipm_lamh", (size_t)le), *scoef = ctx->wsd("ipm_s", (size_t)le);
   Dots D{ctx};
   AOps AO{ctx, qp_in->structure, m, n, ncolA, A, lda, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (AO.structure == 2) {
+    AO.atv = ctx->wsd("svm_atv", nn);
+    AO.addm = ctx->wsd("svm_addm", mm);
+    AO.e = ctx->wsd("svm_e", mm);
+    int64_t off = 0;
+    AO.UB.nb = qp_in->n_unit_blocks;
+    for (int k = 0; k < AO.UB.nb; ++k) {
+      AO.UB.row0[k] = qp_in->unit_blocks[k].row0;
+      AO.UB.count[k] = qp_in->unit_blocks[k].count;
+      AO.UB.scale[k] = qp_in->unit_blocks[k].scale;
+      AO.UB.off[k] = off;
+      off += AO.UB.count[k];
+    }
+    AO.UB.total = off;
+  }
   if (AO.structure == 1) {
     AO.g = ctx->wsd("svm_g", (size_t)even(ncolA) + 2);
     AO.atv = ctx->wsd("svm_atv", nn);
@@ -1448,15 +1485,30 @@ int nys_ipppmm_solve(nys_ctx* ctx, const nys_qp* qp, const nys_options* opt, nys
     ctx->set_error("nys_ipppmm_solve: bad problem");
     return NYS_EINVAL;
   }
-  if (qp->structure != 0 && (qp->structure != 1 || qp->nd < 0 || qp->n != 2 * qp->nd + 2 * qp->m)) {
-    ctx->set_error("nys_ipppmm_solve: structure 1 needs n = 2 nd + 2 m");
+  if (qp->structure == 1 && (qp->nd < 0 || qp->n != 2 * qp->nd + 2 * qp->m || ctx->world != 1)) {
+    ctx->set_error("nys_ipppmm_solve: structure 1 needs n = 2 nd + 2 m and one rank");
     return NYS_EINVAL;
   }
-  if (qp->vtype && qp->structure != 0) {
-    ctx->set_error("nys_ipppmm_solve: vtype (free / box variables) needs structure 0");
+  if (qp->structure == 2) {
+    bool ok = qp->nd >= 1 && qp->n_unit_blocks >= 0 && qp->n_unit_blocks <= 8 &&
+              (qp->n_unit_blocks == 0 || qp->unit_blocks != nullptr);
+    int64_t tot = qp->nd;
+    for (int k = 0; ok && k < qp->n_unit_blocks; ++k) {
+      const nys_unit_block& u = qp->unit_blocks[k];
+      ok = u.row0 >= 0 && u.count >= 0 && u.row0 + u.count <= qp->m && std::isfinite(u.scale) && u.scale != 0.0;
+      tot += u.count;
+    }
+    if (!ok || tot != qp->n) {
+      ctx->set_error("nys_ipppmm_solve: structure 2 needs nd >= 1, <= 8 unit blocks inside [0, m) with nonzero "
+                     "scale, and n = nd + sum(count)");
+      return NYS_EINVAL;
+    }
+  }
+  if (qp->structure < 0 || qp->structure > 2) {
+    ctx->set_error("nys_ipppmm_solve: unknown structure");
     return NYS_EINVAL;
   }
-  if (!qp->host_ptrs) NYS_TRY(check_A(ctx, qp->m, qp->structure == 1 ? qp->nd : qp->n, qp->A, qp->lda));
+  if (!qp->host_ptrs) NYS_TRY(check_A(ctx, qp->m, qp->structure >= 1 ? qp->nd : qp->n, qp->A, qp->lda));
   if (opt->ell < 0 || opt->ell > qp->m || opt->ell > 256 || !(opt->tol > 0)) {
     ctx->set_error("nys_ipppmm_solve: bad options");
     return NYS_EINVAL;

@@ -6,4 +6,5 @@ BASELINE.json config recipes prescribe).  It holds none of the method's arithmet
 no normal-equation operator, no sketch, no PCG, no IP-PMM step.  Neither `oracle/` nor
 the CUDA path is imported from here.
 """
-from .configs import QPInstance, make_config, make_general, CONFIG_NAMES, gaussian_matrix  # noqa: F401
+from .configs import (QPInstance, make_config, make_general, make_svm_dual, make_portfolio,  # noqa: F401
+                      structured_dense_A, CONFIG_NAMES, gaussian_matrix)

@@ -182,6 +182,74 @@ def make_general(m: int, n: int, frac_free: float = 0.2, frac_box: float = 0.3, 
                       extra={"vtype": vtype, "ub": ub, "s0": s0})
 
 
+def make_svm_dual(n_samples: int, d: int, tau: float = 1.0, ell: int = 20, seed: int = 20) -> QPInstance:
+    """The paper's own SVM formulation (App. C.2): dual linear SVM
+        min 1/2 v^T v - 1^T p   s.t.  v - X diag(y) p = 0,  y^T p = 0,  v free,  0 <= p <= tau,
+    X (d x n_samples) a two-class Gaussian mixture, column i = (0.5 y_i 1_d + g_i) / sqrt(d) (the
+    stand-in for the paper's datasets, Table 4; no dataset item is reproduced).  Variables are
+    ordered [p; v] (structure 2: the dense block first): A = [-X diag(y), I_d; y^T, 0] (m = d + 1),
+    dense block B = [-X diag(y); y^T], one unit block (row0 = 0, count = d, scale = +1).
+    q = [0; 1_d]; c = [-1_n; 0] (reading G4: the paper prints c = [0; 1], which contradicts its
+    objective -sum p_i); b = 0; vtype = [2 (J, u = tau); 1 (F)].
+    Draw order: labels, G.  extra = {B, unit_blocks, vtype, ub, labels}."""
+    rng = np.random.default_rng(seed)
+    yl = np.where(rng.uniform(size=n_samples) < 0.5, -1.0, 1.0)
+    X = gaussian_matrix(rng, d, n_samples)
+    X += 0.5 * yl[None, :]
+    X /= np.sqrt(d)
+    B = np.asfortranarray(np.vstack([-X * yl[None, :], yl[None, :]]))
+    m = d + 1
+    n = n_samples + d
+    q = np.concatenate([np.zeros(n_samples), np.ones(d)])
+    c = np.concatenate([-np.ones(n_samples), np.zeros(d)])
+    b = np.zeros(m)
+    vtype = np.concatenate([np.full(n_samples, 2, np.int8), np.full(d, 1, np.int8)])
+    ub = np.concatenate([np.full(n_samples, float(tau)), np.zeros(d)])
+    return QPInstance(f"svmdual_n{n_samples}_d{d}", -2, None, q, b, c, ell,
+                      extra={"B": B, "unit_blocks": [(0, d, 1.0)], "vtype": vtype, "ub": ub, "labels": yl})
+
+
+def make_portfolio(n_assets: int, d: int, s: int, ell: int = 20, gamma: float = 1.0, seed: int = 30) -> QPInstance:
+    """The paper's portfolio formulation (Sec. 5.1, App. C.1) with a factor
+    model Sigma = F F^T + D:
+        min -gamma^{-1} r^T x + x^T D x + y^T y  s.t.  y = F^T x,  M x <= u,  1^T x = 1,  x >= 0,  y free.
+    Slacks t = u - M x >= 0 make it (P~): variables [x (n, I); y (s, F); t (d, I)], rows
+    [y - F^T x = 0 (s); M x + t = u (d); 1^T x = 1 (1)], so m = s + d + 1 (50101 at the paper's
+    n = 80000, d = 50000, s = 100).  Structure 2: dense block B = [-F^T; M; 1^T] (the x columns),
+    unit blocks (0, s, +1) for y and (s, d, +1) for t.  q = [2 diag(D); 2 1_s; 0_d], c = [-r/gamma; 0; 0].
+    Synthetic stand-in: F = V diag(sqrt(sigma)) with V an orthonormalised Gaussian
+    n x s and sigma_i = 10^{-3 (i-1)/s} (rapid decay); diag(D) = 1e-3 U(0.5, 1.5) (the slow tail);
+    M ~ N(0, 1); r ~ N(0, 1); u ~ U(0.1, 1) (x = 1/n is strictly feasible w.h.p.).
+    Draw order: V, D, M, r, u.  extra = {B, unit_blocks, vtype, ub}."""
+    rng = np.random.default_rng(seed)
+    V, _ = np.linalg.qr(rng.standard_normal((n_assets, s)))
+    sigma = 10.0 ** (-3.0 * np.arange(s) / max(s, 1))
+    F = V * np.sqrt(sigma)[None, :]
+    Dd = 1e-3 * rng.uniform(0.5, 1.5, n_assets)
+    M = gaussian_matrix(rng, d, n_assets)
+    r = rng.standard_normal(n_assets)
+    u = rng.uniform(0.1, 1.0, d)
+    B = np.asfortranarray(np.vstack([-F.T, M, np.ones((1, n_assets))]))
+    m = s + d + 1
+    q = np.concatenate([2.0 * Dd, 2.0 * np.ones(s), np.zeros(d)])
+    c = np.concatenate([-r / gamma, np.zeros(s), np.zeros(d)])
+    b = np.concatenate([np.zeros(s), u, [1.0]])
+    vtype = np.concatenate([np.zeros(n_assets, np.int8), np.ones(s, np.int8), np.zeros(d, np.int8)])
+    return QPInstance(f"portfolio_n{n_assets}_d{d}_s{s}", -3, None, q, b, c, ell,
+                      extra={"B": B, "unit_blocks": [(0, s, 1.0), (s, d, 1.0)], "vtype": vtype,
+                             "ub": np.zeros(n_assets + s + d)})
+
+
+def structured_dense_A(B: np.ndarray, unit_blocks, m: int) -> np.ndarray:
+    """Materialise A = [B, S_0, S_1, ...] (structure 2) for SMALL instances only (tests)."""
+    cols = [np.asarray(B)]
+    for row0, count, scale in unit_blocks:
+        S = np.zeros((m, count))
+        S[row0 + np.arange(count), np.arange(count)] = scale
+        cols.append(S)
+    return np.asfortranarray(np.hstack(cols))
+
+
 def svm_dense_A(inst: QPInstance) -> np.ndarray:
     """Materialise A = [Xt, -Xt, I, -I] for SMALL SVM instances only (tests)."""
     Xt = inst.extra["Xt"]

@@ -1,0 +1,191 @@
+"""GPU parity for structure 2 (dense block + scaled identity blocks, nys_qp.unit_blocks) on the paper's
+own QP formulations — dual SVM (App. C.2) and the factor-model portfolio (App. C.1,
+P:1500-1520) — which need free and box variables (f1).  The CUDA path never materialises the
+identity blocks; the oracle (oracle.ippmm_gen.solve_general) gets the dense A."""
+import concurrent.futures as cf
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import ippmm, ippmm_gen  # noqa: E402
+from synth import make_portfolio, make_svm_dual, structured_dense_A  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a, dtype=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dtype).cuda()
+
+
+def _h(t):
+    return t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)
+
+
+def band_general(A, inst, x, y, z, s, p, d, w=None):
+    """A17'': |p - d| + ||x|| ||r_D|| + ||y|| ||r_P|| + ||s|| ||r_U||."""
+    vt, u = inst.extra["vtype"], inst.extra["ub"]
+    J = vt == 2
+    rP = inst.b - A @ x
+    rD = inst.c + inst.q * x - A.T @ y - z + s
+    rU = np.where(J, u - x - (w if w is not None else np.where(J, u - x, 0.0)), 0.0)
+    return (abs(p - d) + np.linalg.norm(x) * np.linalg.norm(rD) + np.linalg.norm(y) * np.linalg.norm(rP)
+            + np.linalg.norm(s) * np.linalg.norm(rU))
+
+
+def _solve_structured(ctx, inst, **kw):
+    from paper_2404_14524_b200 import colmajor_device
+    Bd, lda = colmajor_device(inst.extra["B"])
+    return ctx.nys_ipppmm_solve(Bd, lda, inst.m, dev(inst.q), dev(inst.b), dev(inst.c), ell=inst.ell, structure=2,
+                                unit_blocks=inst.extra["unit_blocks"], vtype=dev(inst.extra["vtype"], torch.int8),
+                                ub=dev(inst.extra["ub"]), **kw)
+
+
+CASES = [("svm", dict(n_samples=200, d=60, ell=20)), ("svm", dict(n_samples=60, d=300, ell=20)),
+         ("svm", dict(n_samples=150, d=97, ell=0)), ("portfolio", dict(n_assets=300, d=40, s=5, ell=10)),
+         ("portfolio", dict(n_assets=800, d=120, s=10, ell=20))]
+
+
+def _make(kind, kw):
+    return make_svm_dual(**kw) if kind == "svm" else make_portfolio(**kw)
+
+
+@pytest.mark.parametrize("kind,kw", CASES)
+def test_structured_paper_formulations_match_oracle(kind, kw):
+    from paper_2404_14524_b200 import Context
+    inst = _make(kind, kw)
+    A = structured_dense_A(inst.extra["B"], inst.extra["unit_blocks"], inst.m)
+    vt, u = inst.extra["vtype"], inst.extra["ub"]
+    ref = ippmm_gen.solve_general(A, inst.q, inst.b, inst.c, vt, u, ippmm.Options(path="krylov", ell=inst.ell))
+    assert ref.status == "optimal"
+    ctx = Context(0)
+    g = _solve_structured(ctx, inst)
+    torch.cuda.synchronize()
+    x, y, z, s = (_h(g[k]) for k in ("x", "y", "z", "s"))
+    assert g["status"] == 0 and g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    J = vt == 2
+    bn = np.sqrt(inst.b @ inst.b + u[J] @ u[J])
+    w = _h(g["w"])
+    rP = np.concatenate([inst.b - A @ x, (u - x - w)[J]])
+    assert np.linalg.norm(rP) / (1 + bn) <= 1.01e-8                   # A u computed without the identity blocks
+    assert np.linalg.norm(inst.c + inst.q * x - A.T @ y - z + s) / (1 + np.linalg.norm(inst.c)) <= 1.01e-8
+    tol = max(1e-7 * max(1.0, abs(ref.obj)),
+              band_general(A, inst, x, y, z, s, g["obj"], g["dual_obj"], w) +
+              band_general(A, inst, ref.x, ref.y, ref.z, ref.s, ref.obj, ref.dual_obj, ref.w))
+    print(f"{inst.name}: gpu {g['obj']!r} ref {ref.obj!r} outer {g['outer']}/{ref.outer} "
+          f"inner {g['inner']}/{ref.inner_total}")
+    assert abs(g["obj"] - ref.obj) <= tol
+    assert abs(g["outer"] - ref.outer) <= 2
+    for k in range(min(2, len(g["log"]), len(ref.log))):                # same trajectory at the start
+        assert abs(g["log"][k]["mu"] - ref.log[k]["mu"]) <= 1e-6 * ref.log[k]["mu"]
+        assert abs(g["log"][k]["alpha_p"] - ref.log[k]["alpha_p"]) <= 1e-6
+    ctx.close()
+
+
+def test_structured_equals_dense_materialised():
+    """structure 2 and the materialised dense A (structure 0) give the same solve (same operator)."""
+    from paper_2404_14524_b200 import Context, colmajor_device
+    inst = make_portfolio(400, 50, 6, ell=12, seed=31)
+    A = structured_dense_A(inst.extra["B"], inst.extra["unit_blocks"], inst.m)
+    ctx = Context(0)
+    g2 = _solve_structured(ctx, inst)
+    Ad, lda = colmajor_device(A)
+    g0 = ctx.nys_ipppmm_solve(Ad, lda, inst.m, dev(inst.q), dev(inst.b), dev(inst.c), ell=inst.ell,
+                              vtype=dev(inst.extra["vtype"], torch.int8), ub=dev(inst.extra["ub"]))
+    torch.cuda.synchronize()
+    assert g0["status"] == 0 and g2["status"] == 0
+    assert abs(g0["outer"] - g2["outer"]) <= 1
+    for k in range(min(3, len(g0["log"]), len(g2["log"]))):
+        assert abs(g0["log"][k]["mu"] - g2["log"][k]["mu"]) <= 1e-9 * g0["log"][k]["mu"]
+    assert abs(g0["obj"] - g2["obj"]) <= 1e-7 * max(1.0, abs(g0["obj"]))
+    ctx.close()
+
+
+def test_structured_chol_preconditioner():
+    """Chol-IP-PMM (f2) on structure 2: diag(N) includes the identity blocks' e term."""
+    from paper_2404_14524_b200 import Context
+    inst = make_svm_dual(120, 80, ell=16, seed=21)
+    A = structured_dense_A(inst.extra["B"], inst.extra["unit_blocks"], inst.m)
+    vt, u = inst.extra["vtype"], inst.extra["ub"]
+    ref = ippmm_gen.solve_general(A, inst.q, inst.b, inst.c, vt, u, ippmm.Options(path="direct"))
+    ctx = Context(0)
+    g = _solve_structured(ctx, inst, precond=1)
+    torch.cuda.synchronize()
+    assert g["status"] == 0 and ref.status == "optimal"
+    x, y, z, s = (_h(g[k]) for k in ("x", "y", "z", "s"))
+    tol = max(1e-7 * max(1.0, abs(ref.obj)),
+              band_general(A, inst, x, y, z, s, g["obj"], g["dual_obj"]) +
+              band_general(A, inst, ref.x, ref.y, ref.z, ref.s, ref.obj, ref.dual_obj))
+    assert abs(g["obj"] - ref.obj) <= tol
+    ctx.close()
+
+
+def test_structured_rejects_bad_blocks():
+    from paper_2404_14524_b200 import Context, NysError, colmajor_device
+    inst = make_svm_dual(50, 20, ell=4)
+    ctx = Context(0)
+    Bd, lda = colmajor_device(inst.extra["B"])
+    args = (Bd, lda, inst.m, dev(inst.q), dev(inst.b), dev(inst.c))
+    for blocks in ([(0, 19, 1.0)], [(2, 20, 1.0)], [(0, 20, 0.0)]):      # wrong n, outside [0, m), zero scale
+        with pytest.raises(NysError):
+            ctx.nys_ipppmm_solve(*args, ell=4, structure=2, unit_blocks=blocks)
+    ctx.close()
+
+
+def test_structured_multirank_loopback():
+    """structure 2 on 2 loopback ranks: rank 0 = first half of B + the y block, rank 1 = second half of
+    B + the slack block (each rank passes its own unit blocks; e and A u partials are all-reduced)."""
+    from paper_2404_14524_b200 import Context, LoopbackComm, colmajor_device
+    inst = make_portfolio(500, 60, 8, ell=16, seed=32)
+    B, (blk_y, blk_t) = inst.extra["B"], inst.extra["unit_blocks"]
+    na, s_, d_ = B.shape[1], blk_y[1], blk_t[1]
+    vt, u = inst.extra["vtype"], inst.extra["ub"]
+    h = na // 2
+    # global variable index lists per rank: [dense cols, unit cols]
+    idx = [np.concatenate([np.arange(0, h), na + np.arange(s_)]),
+           np.concatenate([np.arange(h, na), na + s_ + np.arange(d_)])]
+    blocks = [[blk_y], [blk_t]]
+    dense = [B[:, :h], B[:, h:]]
+    world, m = 2, inst.m
+    comm = LoopbackComm(world)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    ctxs = [Context(0, stream=streams[r], nccl_id=comm.id, rank=r, world=world) for r in range(world)]
+    data = []
+    for r in range(world):
+        Bd, lda = colmajor_device(np.asfortranarray(dense[r]))
+        ii = idx[r]
+        data.append((Bd, lda, dev(inst.q[ii]), dev(inst.b), dev(inst.c[ii]), dev(vt[ii], torch.int8), dev(u[ii])))
+    torch.cuda.synchronize()
+
+    def worker(r):
+        torch.cuda.set_device(0)
+        Bd, lda, q, b, c, v, uu = data[r]
+        with torch.cuda.stream(streams[r]):
+            g = ctxs[r].nys_ipppmm_solve(Bd, lda, m, q, b, c, ell=inst.ell, structure=2, unit_blocks=blocks[r],
+                                         vtype=v, ub=uu)
+        streams[r].synchronize()
+        return {k: _h(val) if hasattr(val, "cpu") else val for k, val in g.items() if k != "log"}
+
+    try:
+        with cf.ThreadPoolExecutor(max_workers=world) as ex:
+            res = list(ex.map(worker, range(world)))
+    finally:
+        for cx in ctxs:
+            cx.close()
+        comm.close()
+    A = structured_dense_A(B, inst.extra["unit_blocks"], m)
+    ref = ippmm_gen.solve_general(A, inst.q, inst.b, inst.c, vt, u, ippmm.Options(path="krylov", ell=inst.ell))
+    for g in res:
+        assert g["status"] == 0 and g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    assert np.array_equal(res[0]["y"], res[1]["y"]) and res[0]["inner"] == res[1]["inner"]
+    perm = np.concatenate(idx)
+    x, z, s = (np.empty(A.shape[1]) for _ in range(3))
+    x[perm] = np.concatenate([g["x"] for g in res])
+    z[perm] = np.concatenate([g["z"] for g in res])
+    s[perm] = np.concatenate([g["s"] for g in res])
+    tol = max(1e-7 * max(1.0, abs(ref.obj)),
+              band_general(A, inst, x, res[0]["y"], z, s, res[0]["obj"], res[0]["dual_obj"]) +
+              band_general(A, inst, ref.x, ref.y, ref.z, ref.s, ref.obj, ref.dual_obj))
+    assert abs(res[0]["obj"] - ref.obj) <= tol
+    assert abs(res[0]["outer"] - ref.outer) <= 2

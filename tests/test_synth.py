@@ -84,3 +84,24 @@ def test_make_general_is_strictly_feasible():
     assert np.allclose(inst.c + inst.q * inst.x0 - inst.A.T @ inst.y0 - inst.z0 + s0, 0, atol=1e-12)
     again = make_general(30, 90, 0.2, 0.3, ell=4, seed=3)
     assert np.array_equal(again.A, inst.A) and np.array_equal(again.extra["vtype"], vt)
+
+
+def test_paper_formulation_generators():
+    """App. C.2 dual SVM and App. C.1 portfolio in structure-2 form: shapes, identity blocks, and a
+    strictly feasible primal point of the portfolio (x = 1/n, y = F^T x, t = u - M x > 0)."""
+    from synth import make_portfolio, make_svm_dual, structured_dense_A
+    sv = make_svm_dual(40, 12, tau=2.0)
+    A = structured_dense_A(sv.extra["B"], sv.extra["unit_blocks"], sv.m)
+    assert A.shape == (13, 52) and np.array_equal(A[:12, 40:], np.eye(12)) and np.all(A[12, 40:] == 0)
+    yl = sv.extra["labels"]
+    assert np.array_equal(A[12, :40], yl) and np.all(sv.c[:40] == -1) and np.all(sv.q[40:] == 1)
+    assert np.all(sv.extra["ub"][:40] == 2.0) and np.all(sv.extra["vtype"][40:] == 1)
+    pf = make_portfolio(50, 7, 3)
+    A = structured_dense_A(pf.extra["B"], pf.extra["unit_blocks"], pf.m)
+    assert A.shape == (11, 60)
+    x = np.full(50, 1 / 50)
+    FT = -pf.extra["B"][:3]
+    y = FT @ x
+    t = pf.b[3:10] - pf.extra["B"][3:10] @ x
+    assert np.all(t > 0)
+    assert np.allclose(A @ np.concatenate([x, y, t]), pf.b, atol=1e-14)
