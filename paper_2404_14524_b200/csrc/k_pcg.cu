@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   uint64_t* empty = full + S;
   double* red = reinterpret_cast<double*>(empty + S);  // 2 * NG * WPG * CPG
   __shared__ double hsh[256];
+  __shared__ double gsh[256];
   __shared__ int s_role;
   __shared__ double chunk_red[16][17];
   __shared__ double s_scal[8];
@@ -99,7 +100,10 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31;
   const unsigned int G = gridDim.x;
   const unsigned int cid = blockIdx.x;
-  const int64_t niter = (cid < P.npanels) ? (P.npanels - cid + G - 1) / G : 0;
+  // this CTA's contiguous column range [c_lo, c_hi) (balanced to one column), streamed in panels of
+  // BN columns with a ragged last panel
+  const int64_t c_lo = (P.n * (int64_t)cid) / G, c_hi = (P.n * ((int64_t)cid + 1)) / G;
+  const int64_t niter = (c_hi - c_lo + BN - 1) / BN;
   const uint32_t copy_bytes = (uint32_t)(((P.m + 1) & ~int64_t(1)) * 8);
   const int64_t r_lo = (int64_t)cid * P.rows_per_cta;
   int64_t r_hi = r_lo + P.rows_per_cta;
@@ -134,8 +138,8 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
         const int s = (int)(q % S);
         for (; pf < q + S + PF; ++pf) {
           const int64_t itp = pf % niter;
-          const int64_t c0 = (int64_t)(cid + itp * G) * BN;
-          int64_t nc = P.n - c0;
+          const int64_t c0 = c_lo + itp * BN;
+          int64_t nc = c_hi - c0;
           nc = nc > BN ? BN : nc;
           if (pf >= q + S) bulk_prefetch_l2(P.A + c0 * P.lda, (uint32_t)(((nc - 1) * P.lda) * 8) + copy_bytes);
         }
@@ -156,8 +160,8 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
         }
         if (s_stop) break;
         const int64_t it = q % niter;
-        const int64_t col0 = (int64_t)(cid + it * G) * BN;
-        int64_t ncols = P.n - col0;
+        const int64_t col0 = c_lo + it * BN;
+        int64_t ncols = c_hi - col0;
         ncols = ncols > BN ? BN : ncols;
         mbar_arrive_expect_tx(&full[s], (uint32_t)ncols * copy_bytes);
         for (int c = 0; c < ncols; ++c)
@@ -293,8 +297,9 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     }
   };
 
-  // P3: converged? then h and z = r + U h, r^T z partial
-  auto phase_prec = [&](bool init) -> bool {
+  // P3: converged? then h = s o (U^T r), r^T z = r^T r + (U^T r)^T h (no extra reduction), beta, and
+  // own rows: z = r + U h, p_next = z + beta p_cur
+  auto phase_prec = [&](bool init, const double* pcur, double* pnext) -> bool {
     // all 1 + ell sums of the CTA partial rows part1[cid][.] (||r||^2, U^T r): two-level "last
     // arriver reduces" (groups of RG CTAs, then the groups), fixed order -> deterministic; every CTA
     // then reads the ncol totals.  Replaces a grid barrier + every CTA re-reading all G partials.
@@ -352,7 +357,17 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       for (int c = tid; c < ncol; c += T) {
         const double sum = __ldcg(P.tot + c);
         if (c == 0) s_scal[0] = sum;
-        else hsh[c - 1] = P.s[c - 1] * sum;
+        else {
+          gsh[c - 1] = sum;
+          hsh[c - 1] = P.s[c - 1] * sum;
+        }
+      }
+      named_bar_sync(9, T);
+      if (warp == 0 && ell > 0) {  // r^T z = r^T r + sum_c g_c h_c : the same fixed order in every CTA
+        double acc = 0.0;
+        for (int c = lane; c < ell; c += 32) acc = fma(gsh[c], hsh[c], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) s_scal[1] = s_scal[0] + acc;
       }
       named_bar_sync(9, T);
     }
@@ -368,9 +383,17 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       return true;
     }
     if (ell > 0) {
-      double rzp = 0.0;
+      const double rzn = s_scal[1];
+      if (!(rzn > 0.0) || !isfinite(rzn)) { status = NYS_EBREAKDOWN; return true; }
+      beta = init ? 0.0 : rzn / rz;
+      rz = rzn;
       for (int64_t i0 = r_lo; i0 < r_hi; i0 += 16) {
         const int64_t i = i0 + row16;
+        double pre_r = 0.0, pre_p = 0.0;
+        if (tid < 16 && i < r_hi) {
+          pre_r = P.r[i];
+          pre_p = init ? 0.0 : __ldcg(pcur + i);
+        }
         if (warp < 8) {
           double acc = 0.0;
           if (i < r_hi)
@@ -382,26 +405,14 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
           const double* v = chunk_red[row16];
           const double us = (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
                             (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
-          const double ri = P.r[i];
-          const double zi = ri + us;
+          const double zi = pre_r + us;
           P.z[i] = zi;
-          rzp = fma(ri, zi, rzp);
+          pnext[i] = init ? zi : fma(beta, pre_p, zi);
         }
         named_bar_sync(9, T);
       }
-      rzp = warp_sum(rzp);
-      if (tid == 0) P.part2[cid] = rzp;
       if (!init) stamp(7);
-      pcg_grid_barrier(P.bar, G, T, bar_epoch);
-      if (warp == 0) {
-        const double rzn = warp_sum_array(P.part2, G);
-        if (lane == 0) s_scal[1] = rzn;
-      }
-      named_bar_sync(9, T);
-      const double rzn = s_scal[1];
-      if (!(rzn > 0.0) || !isfinite(rzn)) { status = NYS_EBREAKDOWN; return true; }
-      beta = init ? 0.0 : rzn / rz;
-      rz = rzn;
+      pcg_grid_barrier(P.bar, G, T, bar_epoch);   // p_next complete on every row
     } else {
       beta = init ? 0.0 : rrt / rz;
       rz = rrt;
@@ -411,40 +422,49 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
 
   const double delta = P.sc[S_DELTA];
   rows_phase_rr_ut(true, 0.0, nullptr, nullptr, delta);
-  bool stop = phase_prec(true);
+  bool stop = phase_prec(true, nullptr, P.P1);   // p_0 -> the buffer iteration 0 reads (pnew of k = 0)
 
   int k = 0;
   while (!stop) {
     trace_k = k;
     stamp(0);
     // ---- P1: v = z + beta p ; fused matvec over this CTA's panels ----------------------------
-    const double* pold = (k & 1) ? P.P1 : P.P0;
+    double* pold = (k & 1) ? P.P1 : P.P0;
     double* pnew = (k & 1) ? P.P0 : P.P1;
     double vreg[RPT];
     double wacc[RPT];
     // all loads first (z, p are written by other CTAs in this launch: read through L2), then the
     // stores: interleaving them would serialise the loads behind possibly-aliasing stores
-    double zr[RPT], pr[RPT];
+    if (ell > 0) {  // p_k was formed row-wise at the end of the previous phase_prec
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int64_t rl = lig + (int64_t)GT * i;
-      zr[i] = (rl < P.m) ? __ldcg(P.z + rl) : 0.0;
-      pr[i] = (rl < P.m && k > 0) ? __ldcg(pold + rl) : 0.0;
-    }
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t rl = lig + (int64_t)GT * i;
+        vreg[i] = (rl < P.m) ? __ldcg(pnew + rl) : 0.0;
+        wacc[i] = 0.0;
+      }
+    } else {
+      double zr[RPT], pr[RPT];
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int64_t rl = lig + (int64_t)GT * i;
-      const double v = (k > 0) ? fma(beta, pr[i], zr[i]) : zr[i];
-      if (rl < P.m && cid == 0 && g == 0) pnew[rl] = v;
-      vreg[i] = (rl < P.m) ? v : 0.0;
-      wacc[i] = 0.0;
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t rl = lig + (int64_t)GT * i;
+        zr[i] = (rl < P.m) ? __ldcg(P.z + rl) : 0.0;
+        pr[i] = (rl < P.m && k > 0) ? __ldcg(pold + rl) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t rl = lig + (int64_t)GT * i;
+        const double v = (k > 0) ? fma(beta, pr[i], zr[i]) : zr[i];
+        if (rl < P.m && cid == 0 && g == 0) pnew[rl] = v;
+        vreg[i] = (rl < P.m) ? v : 0.0;
+        wacc[i] = 0.0;
+      }
     }
     double pwacc = 0.0;
     stamp(8);
     for (int64_t it = 0; it < niter; ++it, ++qc) {
       const int s = (int)(qc % S);
       const uint32_t par = (uint32_t)((qc / S) & 1);
-      const int64_t col0 = (int64_t)(cid + it * G) * BN + (int64_t)g * CPG;
+      const int64_t col0 = c_lo + it * BN + (int64_t)g * CPG;
       mbar_wait(&full[s], par);
       if (it == 0) stamp(9);
       if (it == niter / 2) stamp(10);
@@ -453,7 +473,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       const double* sb = stage + ((size_t)s * BN + (size_t)g * CPG) * rs;
 #pragma unroll
       for (int c = 0; c < CPG; ++c) {
-        const bool cv = (col0 + c) < P.n;
+        const bool cv = (col0 + c) < c_hi;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
           const int64_t rl = lig + (int64_t)GT * i;
@@ -464,7 +484,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       if (lane == 0) mbar_arrive(&empty[s]);
       double dpre[CPG];
 #pragma unroll
-      for (int c = 0; c < CPG; ++c) dpre[c] = (col0 + c < P.n) ? __ldg(P.d + col0 + c) : 0.0;
+      for (int c = 0; c < CPG; ++c) dpre[c] = (col0 + c < c_hi) ? __ldg(P.d + col0 + c) : 0.0;
       double pd[CPG];
 #pragma unroll
       for (int c = 0; c < CPG; ++c) {
@@ -558,7 +578,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     stamp(3);
     stamp(4);
     // ---- P3 / P4 -------------------------------------------------------------------------------
-    stop = phase_prec(false);
+    stop = phase_prec(false, pnew, pold);   // p_{k+1} goes to the buffer iteration k + 1 reads
     stamp(5);
     ++k;
   }
