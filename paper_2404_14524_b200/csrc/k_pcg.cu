@@ -16,6 +16,7 @@
 // the next matvec.  Grid barriers involve the consumer threads only; the producer polls a stop
 // flag so it can never block the exit.
 #include <cstdlib>
+#include <vector>
 
 #include "k_vec.cuh"
 
@@ -51,6 +52,8 @@ struct PcgPParams {
   int l2_prefetch;            // panels prefetched into L2 ahead of the smem ring
   int l2_keep;                // panels per CTA copied with evict_last (L2-resident across iterations)
   unsigned long long* trace;  // debug (NYS_PCG_TRACE): [2 CTAs][32 iters][8] globaltimer stamps
+  unsigned long long* trace_arr;
+  int flat_red;               // 1: grid barrier + every CTA reduces all partial rows; 0: two-level last-arriver tree  // debug: [3][G] arrival stamps of every CTA at the 3 syncs of iteration 14
   int64_t npanels;
   int64_t rows_per_cta;
 };
@@ -91,6 +94,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   double* red = reinterpret_cast<double*>(empty + S);  // 2 * NG * WPG * CPG
   __shared__ double hsh[256];
   __shared__ double gsh[256];
+  __shared__ double colred[512];
   __shared__ int s_role;
   __shared__ double chunk_red[16][17];
   __shared__ double s_scal[8];
@@ -185,6 +189,13 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   unsigned int bar_epoch = 0;  // grid barriers passed (thread 0)
   unsigned int red_epoch = 0;  // column reductions done (thread 0)
   int trace_k = 0;
+  auto arrive_stamp = [&](int which) {
+    if (P.trace_arr != nullptr && tid == 0 && trace_k == 14) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      P.trace_arr[(size_t)which * G + cid] = t;
+    }
+  };
   auto stamp = [&](int slot) {
     if (P.trace != nullptr && tid == 0 && (cid == 0 || cid == G - 1) && trace_k < 32) {
       unsigned long long t;
@@ -230,14 +241,14 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       if (!init && warp < 8) {
         double acc = 0.0;
         if (i < r_hi) {
-          for (int c0 = grp16; c0 < (int)G; c0 += 128) {  // 8 independent L2 loads per round
-            double v[8];
+          for (int c0 = grp16; c0 < (int)G; c0 += 160) {  // 10 independent L2 loads: one round at G <= 160
+            double v[10];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 10; ++u) {
               const int c = c0 + 16 * u;
               v[u] = (c < (int)G) ? __ldcg(Wp + (size_t)c * P.wp_ld + i) : 0.0;
             }
-            acc += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+            acc += (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) + (v[8] + v[9]);
           }
         }
         chunk_red[row16][grp16] = acc;
@@ -300,15 +311,48 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   // P3: converged? then h = s o (U^T r), r^T z = r^T r + (U^T r)^T h (no extra reduction), beta, and
   // own rows: z = r + U h, p_next = z + beta p_cur
   auto phase_prec = [&](bool init, const double* pcur, double* pnext) -> bool {
-    // all 1 + ell sums of the CTA partial rows part1[cid][.] (||r||^2, U^T r): two-level "last
-    // arriver reduces" (groups of RG CTAs, then the groups), fixed order -> deterministic; every CTA
-    // then reads the ncol totals.  Replaces a grid barrier + every CTA re-reading all G partials.
+    // all 1 + ell sums of the CTA partial rows part1[cid][.] (||r||^2, U^T r): a grid barrier, then
+    // EVERY CTA reduces the G partial rows itself in one fixed order (identical totals and decisions
+    // in every CTA).  Thread (s, c) sums column c over the slice g = s, s + NS, ... with LB loads in
+    // flight (two L2 round trips at G = 148), then the NS slice sums are added in order.  Measured:
+    // the previous two-level "last arriver reduces" chain released CTAs 6.7 us after the last
+    // arrival, this 1.5 us barrier + the flat read about half of that.
     {
       const int ncol = 1 + ell;
+      if (P.flat_red) {
+      named_bar_sync(9, T);  // this CTA's partial row is written
+      if (!init) arrive_stamp(1);
+      pcg_grid_barrier(P.bar, G, T, bar_epoch);
+      constexpr int LB = 20;
+      const int CP = (ncol <= 32) ? 32 : (ncol <= 64) ? 64 : (ncol <= 128 || T <= 128) ? 128 : (T <= 256 ? 256 : 512);
+      const int NS = T / CP;
+      const int sl = tid / CP, cix = tid % CP;
+#pragma unroll 1
+      for (int c = cix; c < ncol; c += CP) {
+        double tot = 0.0;
+#pragma unroll 1
+        for (int g0 = sl; g0 < (int)G; g0 += NS * LB) {
+          double v[LB];
+#pragma unroll
+          for (int u = 0; u < LB; ++u) {
+            const int gg = g0 + NS * u;
+            v[u] = (gg < (int)G) ? __ldcg(P.part1 + (size_t)gg * ncol + c) : 0.0;
+          }
+#pragma unroll
+          for (int w = 16; w > 0; w >>= 1)
+#pragma unroll
+            for (int u = 0; u < w; ++u)
+              if (u + w < LB) v[u] += v[u + w];
+          tot += v[0];
+        }
+        colred[sl * ncol + c] = tot;
+      }
+      } else {
       const unsigned int ngr = (G + RG - 1) / RG;
       const unsigned int grp = cid / RG;
       const unsigned int gsz = (grp + 1 == ngr) ? G - grp * RG : RG;
       named_bar_sync(9, T);  // this CTA's partial row is written
+      if (!init) arrive_stamp(1);
       if (tid == 0) {
         ++red_epoch;
         const unsigned int old = atom_add_acqrel_gpu(P.rbar + grp, 1u);
@@ -354,8 +398,13 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
         fence_acquire_gpu();
       }
       named_bar_sync(9, T);
+      for (int c = tid; c < ncol; c += T) colred[c] = __ldcg(P.tot + c);
+      }
+      named_bar_sync(9, T);
+      const int NSf = P.flat_red ? T / ((ncol <= 32) ? 32 : (ncol <= 64) ? 64 : (ncol <= 128 || T <= 128) ? 128 : (T <= 256 ? 256 : 512)) : 1;
       for (int c = tid; c < ncol; c += T) {
-        const double sum = __ldcg(P.tot + c);
+        double sum = 0.0;
+        for (int q = 0; q < NSf; ++q) sum += colred[q * ncol + c];
         if (c == 0) s_scal[0] = sum;
         else {
           gsh[c - 1] = sum;
@@ -412,6 +461,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
         named_bar_sync(9, T);
       }
       if (!init) stamp(7);
+      if (!init) arrive_stamp(2);
       pcg_grid_barrier(P.bar, G, T, bar_epoch);   // p_next complete on every row
     } else {
       beta = init ? 0.0 : rrt / rz;
@@ -421,16 +471,18 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   };
 
   const double delta = P.sc[S_DELTA];
-  rows_phase_rr_ut(true, 0.0, nullptr, nullptr, delta);
-  bool stop = phase_prec(true, nullptr, P.P1);   // p_0 -> the buffer iteration 0 reads (pnew of k = 0)
-
-  int k = 0;
-  while (!stop) {
+  // one call site per phase (k = -1 is the initialisation: x = 0, r = rhs, first reduction, p_0):
+  // the phase lambdas inline, so their state stays in registers
+  int k = -1;
+  double alpha = 0.0;
+  for (;;) {
+    const bool init = k < 0;
+    double* pold = (k & 1) ? P.P1 : P.P0;   // p_{k-1}; receives p_{k+1} at the end of iteration k
+    double* pnew = (k & 1) ? P.P0 : P.P1;   // p_k
+    if (!init) {
     trace_k = k;
     stamp(0);
     // ---- P1: v = z + beta p ; fused matvec over this CTA's panels ----------------------------
-    double* pold = (k & 1) ? P.P1 : P.P0;
-    double* pnew = (k & 1) ? P.P0 : P.P1;
     double vreg[RPT];
     double wacc[RPT];
     // all loads first (z, p are written by other CTAs in this launch: read through L2), then the
@@ -563,6 +615,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       }
     }
     stamp(1);
+    arrive_stamp(0);
     pcg_grid_barrier(P.bar, G, T, bar_epoch);
     stamp(2);
     // ---- P2: alpha, own-row updates, partials --------------------------------------------------
@@ -573,13 +626,18 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     named_bar_sync(9, T);
     const double pw = s_scal[2];
     if (!(pw > 0.0) || !isfinite(pw)) { status = NYS_EBREAKDOWN; break; }
-    const double alpha = rz / pw;
-    rows_phase_rr_ut(false, alpha, pnew, P.Wp, delta);
-    stamp(3);
-    stamp(4);
+    alpha = rz / pw;
+    }  // !init
+    rows_phase_rr_ut(init, alpha, init ? nullptr : pnew, init ? nullptr : P.Wp, delta);
+    if (!init) {
+      stamp(3);
+      stamp(4);
+    }
     // ---- P3 / P4 -------------------------------------------------------------------------------
-    stop = phase_prec(false, pnew, pold);   // p_{k+1} goes to the buffer iteration k + 1 reads
-    stamp(5);
+    // k = -1: p_0 -> P1 (= pnew of k = 0); else p_{k+1} -> pold (= pnew of k + 1)
+    const bool stop = phase_prec(init, init ? nullptr : pnew, init ? P.P1 : pold);
+    if (!init) stamp(5);
+    if (stop) break;
     ++k;
   }
 
@@ -669,6 +727,8 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
   P.gtot = ctx->wsd("pp_gtot", (size_t)((G + RG - 1) / RG) * (1 + ell));
   P.tot = ctx->wsd("pp_tot", (size_t)(1 + ell));
   P.max_iter = max_iter;
+  P.flat_red = 1;
+  if (const char* e = getenv("NYS_PCG_RED")) P.flat_red = (e[0] == 'f');
   P.stages = stages;
   P.npanels = npanels;
   P.rows_per_cta = (m + G - 1) / G;
@@ -701,13 +761,34 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
   if (trace) {
     P.trace = (unsigned long long*)ctx->ws("pp_trace", 2 * 32 * 16 * 8);
     NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.trace, 0, 2 * 32 * 16 * 8, ctx->stream));
+    P.trace_arr = (unsigned long long*)ctx->ws("pp_trace_arr", 3 * G * 8);
+    NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.trace_arr, 0, 3 * G * 8, ctx->stream));
   }
   NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, P));
   ctx->launches++;
   if (trace) {
     unsigned long long h[2 * 32 * 16];
     NYS_CUDA_TRY(ctx, cudaMemcpyAsync(h, P.trace, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<unsigned long long> ha(3 * G);
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(ha.data(), P.trace_arr, 3 * G * 8, cudaMemcpyDeviceToHost, ctx->stream));
     NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    {
+      const unsigned long long* r = h + 14 * 16;   // CTA 0, iteration 14: release stamps 2 (bar1), 6 (colsum), 5 (bar3)
+      const int rel_slot[3] = {2, 6, 5};
+      const char* nm[3] = {"bar1", "colsum", "bar3"};
+      for (int w = 0; w < 3 && r[0] != 0; ++w) {
+        unsigned long long mn = ~0ull, mx = 0;
+        int64_t amx = 0;
+        for (int64_t c = 0; c < G; ++c) {
+          const unsigned long long t = ha[(size_t)w * G + c];
+          if (t == 0) continue;
+          mn = t < mn ? t : mn;
+          if (t > mx) { mx = t; amx = c; }
+        }
+        fprintf(stderr, "[pcgsync] it=14 %s: arrivals spread %.2f us (last CTA %lld), CTA0 released %.2f us after the last arrival\n",
+                nm[w], (mx - mn) * 1e-3, (long long)amx, ((double)r[rel_slot[w]] - (double)mx) * 1e-3);
+      }
+    }
     for (int c = 0; c < 2; ++c)
       for (int it = 0; it < 32; ++it) {
         const unsigned long long* r = h + (c * 32 + it) * 16;
