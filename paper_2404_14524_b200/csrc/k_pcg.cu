@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     // all 1 + ell sums of the CTA partial rows part1[cid][.] (||r||^2, U^T r): a grid barrier, then
     // EVERY CTA reduces the G partial rows itself in one fixed order (identical totals and decisions
     // in every CTA).  Thread (s, c) sums column c over the slice g = s, s + NS, ... with LB loads in
-    // flight (two L2 round trips at G = 148), then the NS slice sums are added in order.  Measured:
+    // flight (one L2 round trip at G = 148), then the NS slice sums are added in order.  Measured:
     // the previous two-level "last arriver reduces" chain released CTAs 6.7 us after the last
     // arrival, this 1.5 us barrier + the flat read about half of that.
     {
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       named_bar_sync(9, T);  // this CTA's partial row is written
       if (!init) arrive_stamp(1);
       pcg_grid_barrier(P.bar, G, T, bar_epoch);
-      constexpr int LB = 20;
+      constexpr int LB = 38;
       const int CP = (ncol <= 32) ? 32 : (ncol <= 64) ? 64 : (ncol <= 128 || T <= 128) ? 128 : (T <= 256 ? 256 : 512);
       const int NS = T / CP;
       const int sl = tid / CP, cix = tid % CP;
