@@ -3,7 +3,11 @@
 // of B = Y_nu C^{-1} finished on the ell x ell triangular factor by one-sided Jacobi.
 // All ell x ell routines run in ONE CTA (1024 threads) with the matrices in shared memory
 // when they fit, else in an L2-resident global workspace.
+#include <cooperative_groups.h>
+
 #include "k_vec.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace nys {
 
@@ -116,6 +120,7 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(int ell, double* G, int l
   double* W = SM ? csm : gws;             // n x n, ld n : the factor
   double* X = W + (size_t)n * n;          // n x n, ld lx : R^{-1}
   __shared__ double rsq[256];
+  __shared__ double rowk[256];  // row k gathered once per step (a strided, bank-conflicted read otherwise)
   __shared__ double shift;
   const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31, nw = blockDim.x >> 5;
   for (int e = tid; e < n * n; e += blockDim.x) {
@@ -146,10 +151,12 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(int ell, double* G, int l
       if (tid == 0) sc[S_CHOLFAIL] = 1.0;
       return;
     }
+    for (int i = k + 1 + tid; i < n; i += blockDim.x) rowk[i] = W[k + i * n];
+    __syncthreads();
     const double inv = 1.0 / piv;
     for (int j = k + 1 + warp; j < n; j += nw) {
-      const double akj = W[k + j * n] * inv;
-      for (int i = k + 1 + lane; i <= j; i += 32) W[i + j * n] = fma(-W[k + i * n], akj, W[i + j * n]);
+      const double akj = rowk[j] * inv;
+      for (int i = k + 1 + lane; i <= j; i += 32) W[i + j * n] = fma(-rowk[i], akj, W[i + j * n]);
     }
     __syncthreads();
   }
@@ -182,9 +189,103 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(int ell, double* G, int l
   }
 }
 
+// Same contract as chol_inv_kernel for ell up to 226 in ONE CTA: the upper triangle is held PACKED
+// in shared memory (column-major upper packing, idx(i, j) = j (j + 1) / 2 + i, ell (ell + 1) / 2
+// doubles = 205 KB at ell = 226) and R is inverted IN PLACE (the column-oriented upper-triangular
+// inverse: column j of R^{-1} = -R^{-1}_jj T_{0:j,0:j} R_{0:j,j} with T the already inverted block),
+// instead of the ell^2 + ell^2 layout the unpacked kernel needs (which fits only ell <= 113).
+__device__ __forceinline__ int pidx(int i, int j) { return j * (j + 1) / 2 + i; }
+__global__ void __launch_bounds__(1024) chol_inv_packed_kernel(int ell, double* G, int ldg, double* Rinv, int ldr,
+                                                              int shift_mode, double* sc) {
+  extern __shared__ double pk[];
+  const int n = ell;
+  __shared__ double rsq[256];
+  __shared__ double tmp[256];
+  __shared__ double row[256];   // row k / row i of the packed matrix (a strided gather done once per step)
+  __shared__ double shift;
+  const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31, nw = blockDim.x >> 5;
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i <= j; i += 32) pk[pidx(i, j)] = 0.5 * (G[i + (size_t)j * ldg] + G[j + (size_t)i * ldg]);
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    if (shift_mode == 1) {
+      double tr = 0.0;
+      for (int i = 0; i < n; ++i) tr += pk[pidx(i, i)];
+      s = 11.0 * (sc[S_SHIFT] * n + (double)n * (n + 1)) * 0x1p-53 * tr;
+    }
+    shift = s;
+  }
+  __syncthreads();
+  if (shift_mode == 1) {
+    for (int i = tid; i < n; i += blockDim.x) pk[pidx(i, i)] += shift;
+    __syncthreads();
+  }
+  for (int k = 0; k < n; ++k) {  // right-looking, unscaled row k (as chol_inv_kernel)
+    const double piv = pk[pidx(k, k)];
+    if (!(piv > 0.0) || !isfinite(piv)) {
+      if (tid == 0) sc[S_CHOLFAIL] = 1.0;
+      return;
+    }
+    for (int i = k + 1 + tid; i < n; i += blockDim.x) row[i] = pk[pidx(k, i)];
+    __syncthreads();
+    const double inv = 1.0 / piv;
+    for (int j = k + 1 + warp; j < n; j += nw) {
+      const double akj = row[j] * inv;
+      double* colj = pk + pidx(0, j);
+      for (int i = k + 1 + lane; i <= j; i += 32) colj[i] = fma(-row[i], akj, colj[i]);
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += blockDim.x) rsq[i] = 1.0 / sqrt(pk[pidx(i, i)]);
+  __syncthreads();
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i <= j; i += 32) pk[pidx(i, j)] *= rsq[i];
+  __syncthreads();
+  for (int e = tid; e < n * n; e += blockDim.x) {  // R out (lower zeroed)
+    const int i = e % n, j = e / n;
+    G[i + (size_t)j * ldg] = (i <= j) ? pk[pidx(i, j)] : 0.0;
+  }
+  __syncthreads();
+  // in-place inverse, right to left (every (k, j) update of a step in parallel): at step i the
+  // column above the diagonal still holds R(0:i, i) -> tmp; row i (holding the accumulated X(i, j > i))
+  // is scaled by 1 / R(i, i); then X(k < i, j >= i) -= R(k, i) X(i, j) with X(k, i) starting at 0.
+  for (int i = n - 1; i >= 0; --i) {
+    for (int k = tid; k < i; k += blockDim.x) tmp[k] = pk[pidx(k, i)];
+    const double inv = 1.0 / pk[pidx(i, i)];
+    __syncthreads();
+    for (int j = i + 1 + tid; j < n; j += blockDim.x) {
+      const double x = pk[pidx(i, j)] * inv;
+      pk[pidx(i, j)] = x;
+      row[j] = x;
+    }
+    if (tid == 0) {
+      pk[pidx(i, i)] = inv;
+      row[i] = inv;
+    }
+    __syncthreads();
+    const int cols = n - i;
+    for (int e = tid; e < i * cols; e += blockDim.x) {
+      const int k = e % i, j = i + e / i;
+      const double xij = row[j];
+      double* cj = pk + pidx(0, j);
+      cj[k] = (j == i) ? -tmp[k] * xij : fma(-tmp[k], xij, cj[k]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    Rinv[i + (size_t)j * ldr] = (i <= j) ? pk[pidx(i, j)] : 0.0;
+  }
+}
+
 int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int ldr, int shift_mode) {
   const size_t need = ((size_t)ell * ell + (size_t)ell * (ell | 1)) * sizeof(double);
-  if (need <= 200 * 1024) {
+  const size_t need_packed = (size_t)ell * (ell + 1) / 2 * sizeof(double);
+  if (need > 200 * 1024 && need_packed <= 208 * 1024) {
+    NYS_TRY(ensure_max_smem(ctx, (const void*)chol_inv_packed_kernel, 208 * 1024));
+    chol_inv_packed_kernel<<<1, 1024, need_packed, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);
+  } else if (need <= 200 * 1024) {
     static bool set = false;
     if (!set) {
       NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -409,6 +510,173 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
   }
 }
 
+// The same one-sided Jacobi for ell > 113 (X and V no longer fit one CTA's shared memory): a
+// thread-block CLUSTER of C CTAs holds the columns cyclically (column j in CTA j % C, slot j / C) and
+// every pair reads / writes its four columns and two norms through distributed shared memory; a
+// cluster barrier separates the rounds.  Same ordering, rotation, convergence test and output.
+template <int NMAX, int C>
+__global__ void __launch_bounds__(1024) jacobi_cluster_kernel(int n, const double* R, int ldr, double* Vout, int ldv,
+                                                              double* sigma, double* jsweeps) {
+  constexpr int E = NMAX / 32;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  extern __shared__ double jsm[];
+  const int ncl = (n + C - 1) / C;
+  double* Xl = jsm;                       // local slot t = global column rank + C t, ld n
+  double* Vl = jsm + (size_t)ncl * n;
+  __shared__ double nrm_l[NMAX / C + 1];
+  __shared__ double flag_l[2];            // [0] max column norm^2 of this CTA, [1] rotated in this sweep
+  __shared__ double sv_all[NMAX];
+  __shared__ int order[NMAX];
+  auto xcol = [&](int j) { return cl.map_shared_rank(Xl + (size_t)(j / C) * n, j % C); };
+  auto vcol = [&](int j) { return cl.map_shared_rank(Vl + (size_t)(j / C) * n, j % C); };
+  auto nrmp = [&](int j) { return cl.map_shared_rank(nrm_l + j / C, j % C); };
+  for (int e = threadIdx.x; e < ncl * n; e += blockDim.x) {
+    const int t = e / n, i = e % n, j = rank + C * t;
+    Xl[e] = (j < n) ? R[j + (size_t)i * ldr] : 0.0;  // X = R^T
+    Vl[e] = (j < n && i == j) ? 1.0 : 0.0;
+  }
+  const int P = (n % 2 == 0) ? n : n + 1;
+  const int nwarp = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double tol = fmax(1e-15, (double)n * 0x1p-53);
+  const double tol2 = tol * tol;
+  auto wsum = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  __syncthreads();
+  int sweep = 0;
+  for (; sweep < 30; ++sweep) {
+    for (int t = warp; t < ncl; t += nwarp) {  // exact norms of the local columns
+      double a = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = lane + 32 * e;
+        if (i < n) a = fma(Xl[i + (size_t)t * n], Xl[i + (size_t)t * n], a);
+      }
+      a = wsum(a);
+      if (lane == 0) nrm_l[t] = (rank + C * t < n) ? a : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mx = 0.0;
+      for (int t = 0; t < ncl; ++t) mx = fmax(mx, nrm_l[t]);
+      flag_l[0] = mx;
+      flag_l[1] = 0.0;
+    }
+    cl.sync();
+    double mxall = 0.0;
+    for (int r = 0; r < C; ++r) mxall = fmax(mxall, *cl.map_shared_rank(&flag_l[0], r));
+    const double floor_g = 1e-2 * 0x1p-52 * mxall;   // as jacobi_kernel
+    for (int r = 0; r < P - 1; ++r) {
+      for (int pi = rank + C * warp; pi < P / 2; pi += C * nwarp) {
+        int a, b;
+        if (pi == 0) { a = r; b = P - 1; }
+        else {
+          a = r + pi; if (a >= P - 1) a -= P - 1;
+          b = r - pi; if (b < 0) b += P - 1;
+        }
+        if (a >= n || b >= n) continue;
+        const int p = a < b ? a : b, q = a < b ? b : a;
+        double* Xp = xcol(p);
+        double* Xq = xcol(q);
+        double* Vp = vcol(p);
+        double* Vq = vcol(q);
+        double xp[E], xq[E], vp[E], vq[E];
+        double ga = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = lane + 32 * e;
+          xp[e] = (i < n) ? Xp[i] : 0.0;
+          xq[e] = (i < n) ? Xq[i] : 0.0;
+          vp[e] = (i < n) ? Vp[i] : 0.0;
+          vq[e] = (i < n) ? Vq[i] : 0.0;
+          ga = fma(xp[e], xq[e], ga);
+        }
+        ga = wsum(ga);
+        double* np_ = nrmp(p);
+        double* nq_ = nrmp(q);
+        const double al = *np_, be = *nq_;
+        if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {
+          double c, sn, t;
+          jacobi_rotation(al, be, ga, c, sn, t);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int i = lane + 32 * e;
+            if (i < n) {
+              Xp[i] = c * xp[e] - sn * xq[e];
+              Xq[i] = sn * xp[e] + c * xq[e];
+              Vp[i] = c * vp[e] - sn * vq[e];
+              Vq[i] = sn * vp[e] + c * vq[e];
+            }
+          }
+          if (lane == 0) {
+            *np_ = fmax(al - t * ga, 0.0);
+            *nq_ = be + t * ga;
+            flag_l[1] = 1.0;
+          }
+        }
+      }
+      cl.sync();
+    }
+    bool any = false;
+    for (int r = 0; r < C; ++r) any = any || (*cl.map_shared_rank(&flag_l[1], r) != 0.0);
+    cl.sync();  // every CTA has read the flags before the next sweep resets them
+    if (!any) break;
+  }
+  if (rank == 0 && threadIdx.x == 0) jsweeps[0] = (double)(sweep + 1);
+  for (int t = warp; t < ncl; t += nwarp) {  // sigma of the local columns
+    double a = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = lane + 32 * e;
+      if (i < n) a = fma(Xl[i + (size_t)t * n], Xl[i + (size_t)t * n], a);
+    }
+    a = wsum(a);
+    if (lane == 0) nrm_l[t] = sqrt(a);
+  }
+  cl.sync();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) sv_all[j] = *nrmp(j);
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {  // rank sort, ties by index (every CTA the same)
+    int rk = 0;
+    for (int k = 0; k < n; ++k) rk += (sv_all[k] > sv_all[j]) || (sv_all[k] == sv_all[j] && k < j);
+    order[rk] = j;
+  }
+  __syncthreads();
+  for (int jo = rank; jo < n; jo += C) {
+    const double* src = vcol(order[jo]);
+    if (threadIdx.x == 0) sigma[jo] = sv_all[order[jo]];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) Vout[i + (size_t)jo * ldv] = src[i];
+  }
+  cl.sync();  // no CTA leaves while a peer still reads its shared memory
+}
+
+template <int C>
+static int launch_jacobi_cluster(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma,
+                                 size_t smem) {
+  auto k = jacobi_cluster_kernel<256, C>;
+  NYS_TRY(ensure_max_smem(ctx, (const void*)k, smem));
+  int warps = ((ell + 1) / 2 + C - 1) / C;
+  if (warps > 32) warps = 32;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(32 * warps);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, ell, R, ldr, V, ldv, sigma, ctx->sc + S_JSWEEPS));
+  return NYS_OK;
+}
+
 template <int NMAX>
 static int launch_jacobi_t(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
   const size_t need = 2 * (size_t)ell * ell * sizeof(double);
@@ -428,8 +696,18 @@ static int launch_jacobi_t(nys_ctx* ctx, int ell, const double* R, int ldr, doub
                 h[4 * r + 1], h[4 * r + 2], h[4 * r + 3]);
     }
   } else {
-    double* gws = ctx->wsd("jacobi_ws", 2 * (size_t)ell * ell);
-    jacobi_kernel<NMAX, false><<<1, nthr, 0, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, gws, ctx->sc + S_JSWEEPS, nullptr);
+    // cluster of C CTAs: the smallest C whose per-CTA share of X and V fits 208 KB
+    int C = 2;
+    while (C < 8 && 2 * (size_t)((ell + C - 1) / C) * ell * sizeof(double) > 208 * 1024) C *= 2;
+    const size_t smem = 2 * (size_t)((ell + C - 1) / C) * ell * sizeof(double);
+    if (NMAX == 256 && smem <= 208 * 1024 && getenv("NYS_JACOBI_GLOBAL") == nullptr) {
+      if (C == 2) NYS_TRY(launch_jacobi_cluster<2>(ctx, ell, R, ldr, V, ldv, sigma, smem));
+      else if (C == 4) NYS_TRY(launch_jacobi_cluster<4>(ctx, ell, R, ldr, V, ldv, sigma, smem));
+      else NYS_TRY(launch_jacobi_cluster<8>(ctx, ell, R, ldr, V, ldv, sigma, smem));
+    } else {
+      double* gws = ctx->wsd("jacobi_ws", 2 * (size_t)ell * ell);
+      jacobi_kernel<NMAX, false><<<1, nthr, 0, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, gws, ctx->sc + S_JSWEEPS, nullptr);
+    }
   }
   ctx->launches++;
   return ctx->check_launch("jacobi");
@@ -437,7 +715,7 @@ static int launch_jacobi_t(nys_ctx* ctx, int ell, const double* R, int ldr, doub
 
 int launch_jacobi_svd(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
   if (ell <= 64) return launch_jacobi_t<64>(ctx, ell, R, ldr, V, ldv, sigma);
-  if (ell <= 128) return launch_jacobi_t<128>(ctx, ell, R, ldr, V, ldv, sigma);
+  if (ell <= 112) return launch_jacobi_t<128>(ctx, ell, R, ldr, V, ldv, sigma);   // above: cluster path
   return launch_jacobi_t<256>(ctx, ell, R, ldr, V, ldv, sigma);
 }
 
