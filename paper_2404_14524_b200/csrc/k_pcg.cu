@@ -338,8 +338,9 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
             const int gg = g0 + NS * u;
             v[u] = (gg < (int)G) ? __ldcg(P.part1 + (size_t)gg * ncol + c) : 0.0;
           }
+          static_assert(LB <= 64, "pairwise tree below covers 64 terms");
 #pragma unroll
-          for (int w = 16; w > 0; w >>= 1)
+          for (int w = 32; w > 0; w >>= 1)
 #pragma unroll
             for (int u = 0; u < w; ++u)
               if (u + w < LB) v[u] += v[u + w];

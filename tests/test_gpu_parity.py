@@ -179,7 +179,8 @@ def test_nystrom_exact_recovery_lowrank(ctx):
 
 
 # ------------------------------------------------------------------------ PCG
-@pytest.mark.parametrize("cfg,kw", [(0, {}), (1, dict(m=300, n=1200, ell=30)), (3, dict(m=16, n=4000, ell=8))])
+@pytest.mark.parametrize("cfg,kw", [(0, {}), (1, dict(m=300, n=1200, ell=30)), (3, dict(m=16, n=4000, ell=8)),
+                                    (1, {})])   # full config 1: the persistent kernel with G = 148 CTAs
 @pytest.mark.parametrize("use_prec", [True, False])
 def test_pcg_parity(ctx, cfg, kw, use_prec):
     from paper_2404_14524_b200 import colmajor_device
@@ -208,6 +209,29 @@ def test_pcg_parity(ctx, cfg, kw, use_prec):
     assert abs(info.iters - io["iters"]) <= slack
     assert np.linalg.norm(xg - xo) <= 2 * tol / delta
     assert info.true_res_norm <= max(1.5 * tol, 1.5 * io["true_res"])  # recursive-residual drift as the oracle
+
+
+@pytest.mark.parametrize("cfg,kw,iters", [(1, {}, 25), (1, dict(m=300, n=1200, ell=30), 15), (0, {}, 40)])
+def test_pcg_fixed_iterations_match_oracle(ctx, cfg, kw, iters):
+    """Exactly `iters` PCG iterations (tol = 0) on the GPU and in the oracle: the iterates agree to
+    rounding (every reduction of the persistent kernel — p^T N p, ||r||^2, U^T r, r^T z — enters x)."""
+    from paper_2404_14524_b200 import colmajor_device
+    inst = make_config(cfg, **kw)
+    A, m, n, ell = inst.A, inst.m, inst.n, inst.ell
+    rs = np.random.default_rng(7)
+    d = linops.scaling_d(inst.q, rs.uniform(0.01, 2.0, n), rs.uniform(0.01, 2.0, n), 1e-2)
+    delta = 1e-3
+    rhs = rs.standard_normal(m)
+    Om = orng.gaussian_omega(m, ell, 0, 1)
+    Uo, lamo, _ = nystrom.nystrom_from_sketch(linops.sketch(A, d, Om), Om)
+    pinv = lambda v: nystrom.precond_inv_apply(Uo, lamo, delta, v)  # noqa: E731
+    xo, io = oracle_pcg(lambda v: linops.normal_matvec(A, d, v, delta), rhs, pinv, tol_abs=0.0, max_iter=iters)
+    Ad, lda = colmajor_device(A)
+    xg = torch.empty(m, dtype=torch.float64, device="cuda")
+    info = ctx.nys_pcg_solve(Ad, lda, m, dev(d), None, delta, ell, dev_cm(Uo), dev(lamo), delta, dev(rhs), xg, 0.0,
+                             iters)
+    assert info.iters == iters == io["iters"]
+    assert rel(xg.cpu().numpy(), xo) <= 1e-8
 
 
 def test_pcg_zero_rhs_and_maxiter(ctx):
