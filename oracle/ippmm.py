@@ -64,6 +64,12 @@ class Options:
     # "nystrom" (Nys-IP-PMM) or "chol": the partial Cholesky preconditioner of rank ell (Chol-IP-PMM,
     # the paper's comparison arm), rebuilt every outer iteration
     precond: str = "nystrom"
+    # adaptive rank (the paper's future work "tuning the rank"; reading F1 in
+    # DESIGN.md): when ell_max > ell, after a Nystrom build with rank ell_k whose estimate
+    # lam_hat_ell exceeds ell_tau * mu_prec (mu_prec = delta_k, A7), the next build uses
+    # min(2 ell_k, ell_max) (a rebuild is forced at the next iteration); the rank never shrinks
+    ell_max: int = 0
+    ell_tau: float = 10.0
 
 
 @dataclass
@@ -238,6 +244,8 @@ def solve(A, q, b, c, opts: Options = Options()) -> Result:
     k = 0
     U = lamh = None
     last_build, base_its, last_its = -1, None, 0
+    ell_k = opts.ell                       # rank of the next Nystrom build (F1)
+    ell_built = opts.ell                   # rank of the factors in use
     for k in range(opts.max_outer + 1):
         rel_p, rel_d = nrP / (1.0 + bnorm), nrD / (1.0 + cnorm)
         # ---- TC (A11) ----
@@ -248,6 +256,7 @@ def solve(A, q, b, c, opts: Options = Options()) -> Result:
             break
         # ---- N_k as an operator ----
         d = scaling_d(q, x, z, rho)
+        delta_used = delta
         # ---- P_k^{-1} ----
         if opts.path == "direct":
             sol = _direct_solver(A, d, delta)
@@ -259,10 +268,14 @@ def solve(A, q, b, c, opts: Options = Options()) -> Result:
                 built = True
             elif opts.ell > 0:
                 rebuild = (last_build < 0 or k - last_build >= max(1, opts.prec_refresh) or
-                           (opts.prec_growth > 0 and base_its and last_its > opts.prec_growth * base_its))
+                           (opts.prec_growth > 0 and base_its and last_its > opts.prec_growth * base_its) or
+                           ell_k != ell_built)
                 if rebuild:
-                    U, lamh, _ = build_preconditioner(A, d, opts.ell, omega_fn(m, opts.ell, omega_stream(k)))
-                    last_build, base_its, built = k, None, True
+                    U, lamh, _ = build_preconditioner(A, d, ell_k, omega_fn(m, ell_k, omega_stream(k)))
+                    last_build, base_its, built, ell_built = k, None, True, ell_k
+                    cap = min(opts.ell_max, m, 256)
+                    if cap > ell_k and lamh[ell_k - 1] > opts.ell_tau * delta:      # F1
+                        ell_k = min(2 * ell_k, cap)
             sol = _krylov_solver(A, d, delta, U, lamh, max_iter, F)   # Nystrom: mu_prec = delta_k (A7)
 
         # ---- Alg. 5 predictor ----
@@ -312,6 +325,8 @@ def solve(A, q, b, c, opts: Options = Options()) -> Result:
         log.append({"k": k, "mu": mu, "rel_p": rel_p, "rel_d": rel_d, "alpha_p": ap, "alpha_d": ad,
                     "pcg_pred": it_p, "pcg_corr": it_c, "rho_next": rho, "delta_next": delta,
                     "prec_built": bool(opts.path != "direct" and opts.ell > 0 and built),
+                    "ell": ell_built if (opts.path != "direct" and opts.ell > 0 and opts.precond != "chol") else opts.ell,
+                    "lam_ell": float(lamh[-1]) if lamh is not None else 0.0, "delta": delta_used,
                     "mu_next": mu_new})
         mu = mu_new
 

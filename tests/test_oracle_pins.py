@@ -638,3 +638,30 @@ def test_free_variables_equal_the_split_formulation():
     rs_ = ippmm.solve(As, qs, b, cs, ippmm.Options(path="direct"))
     assert rg.status == "optimal" and rs_.status == "optimal"
     assert abs(rg.obj - rs_.obj) <= 1e-6 * max(1.0, abs(rs_.obj))
+
+
+# ------------------------------------------------------------------ f3: adaptive rank (reading F1)
+def test_adaptive_rank_off_is_the_fixed_rank_solve():
+    inst = make_config(1, m=120, n=480, ell=8)
+    r0 = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(ell=8))
+    r1 = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(ell=8, ell_max=8))
+    assert r0.outer == r1.outer and r0.inner_total == r1.inner_total and r0.obj == r1.obj
+    assert all(l["ell"] == 8 for l in r1.log)
+
+
+def test_adaptive_rank_follows_the_doubling_rule():
+    """F1: the rank doubles (capped) for the next build exactly when lam_hat_ell > tau * delta_k after a
+    build; never shrinks; the rank-40 spike of config 1 is captured and PCG work drops."""
+    inst = make_config(1, m=200, n=800, ell=10)
+    tau, cap = 10.0, 80
+    r = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(ell=10, ell_max=cap, ell_tau=tau))
+    rf = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(ell=10))
+    assert r.status == "optimal" and rf.status == "optimal"
+    ells = [l["ell"] for l in r.log]
+    assert ells[0] == 10 and all(b >= a for a, b in zip(ells, ells[1:]))
+    for a, b in zip(r.log, r.log[1:]):
+        grow = a["prec_built"] and a["lam_ell"] > tau * a["delta"] and a["ell"] < cap
+        assert b["ell"] == (min(2 * a["ell"], cap) if grow else a["ell"])
+    assert max(ells) == cap                                   # the spike (rank 40) needs > 40
+    assert r.inner_total < 0.5 * rf.inner_total
+    assert abs(r.obj - rf.obj) <= 1e-6 * abs(rf.obj)
