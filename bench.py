@@ -252,6 +252,8 @@ def main():
                     help="nystrom: Nys-IP-PMM (default); chol: Chol-IP-PMM, partial Cholesky of rank ell (f2)")
     ap.add_argument("--prec-growth", type=float, default=0.0,
                     help="f3: also rebuild when PCG counts grow by this factor since the last rebuild (0 = off)")
+    ap.add_argument("--ell-max", type=int, default=0,
+                    help="f3 adaptive rank (reading F1): double ell up to this cap while lam_hat_ell > 10 delta (0 = off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--matvec-reps", type=int, default=50)
@@ -293,7 +295,7 @@ def main():
         with torch.cuda.stream(stream):
             return ctx.nys_ipppmm_solve(wl.At, lda, m, wl.q, wl.b, wl.c, ell=wl.ell, structure=wl.structure,
                                         prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
-                                        precond=1 if args.precond == "chol" else 0)
+                                        precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max)
 
     # ---- warm-up ------------------------------------------------------------------------------
     W = max(args.warmup, 3)
@@ -434,7 +436,7 @@ def main():
             with torch.cuda.stream(stream):  # one untimed e2e solve: workspace for the host path, graphs
                 ctx.nys_ipppmm_solve(A_host, lda, m, qh, bh, ch, ell=wl.ell, host=True, structure=wl.structure,
                                      prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
-                                     precond=1 if args.precond == "chol" else 0)
+                                     precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max)
             barrier()
             t0 = time.perf_counter()
             E_STEPS = max(1, min(args.steps, 3))
@@ -442,7 +444,7 @@ def main():
                 with torch.cuda.stream(stream):
                     ctx.nys_ipppmm_solve(A_host, lda, m, qh, bh, ch, ell=wl.ell, host=True, structure=wl.structure,
                                          prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
-                                         precond=1 if args.precond == "chol" else 0)
+                                         precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max)
             barrier()
             t_e2e = (time.perf_counter() - t0) / E_STEPS
             if world > 1:
@@ -488,6 +490,7 @@ def main():
             "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl.name, "m": m, "n": wl.n, "ell": wl.ell, "tol": 1e-8,
                        "prec_refresh": args.prec_refresh, "prec_growth": args.prec_growth, "precond": args.precond,
+                       "ell_max": args.ell_max,
                        "parallelism": f"column-shard x{world}",
                        "l2": ("A = %.0f MB vs 126 MB L2: roofline launches L2-flushed (256 MB read) before each"
                               % (wl.a_bytes() * world / 1e6)) if small else

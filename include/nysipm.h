@@ -244,6 +244,12 @@ typedef struct {
    * ell (Chol-IP-PMM, the paper's comparison arm), built every outer
    * iteration from diag(N_delta): pivots = the ell largest diagonal entries (reading C1).       */
   int    precond;        /* 0                                                              */
+  /* Adaptive Nystrom rank (the paper's future work "tuning the rank", P:1102;
+   * reading F1): when ell_max > ell, after a build with rank ell_k whose lambda_hat_ell exceeds
+   * ell_tau * delta_k (mu_prec, A7) the next build (forced at the next outer iteration) uses
+   * min(2 ell_k, ell_max, m, 256).  The rank never shrinks.  0 = fixed rank.                    */
+  int    ell_max;        /* 0                                                              */
+  double ell_tau;        /* 10                                                             */
 } nys_options;
 
 /* Fill *opt with the defaults above. */
@@ -257,6 +263,8 @@ typedef struct {
   double rho, delta;     /* parameters used in this iteration                              */
   double t_sketch_ms, t_pcg_ms, t_other_ms;
   int    prec_built;     /* 1: the Nystrom preconditioner was (re)built this iteration     */
+  int    ell;            /* rank of the preconditioner used in this iteration              */
+  double lam_ell;        /* its lambda_hat_ell (0 when ell = 0 or partial Cholesky)         */
 } nys_iter_record;
 
 typedef struct {

@@ -52,14 +52,16 @@ class Options(C.Structure):
                 ("pcg_max_iter", C.c_int), ("rho0", C.c_double), ("delta0", C.c_double),
                 ("reg_floor", C.c_double), ("pcg_c", C.c_double), ("pcg_floor", C.c_double),
                 ("init_delta", C.c_double), ("init_tol_rel", C.c_double), ("verbose", C.c_int),
-                ("prec_refresh", C.c_int), ("prec_growth", C.c_double), ("precond", C.c_int)]
+                ("prec_refresh", C.c_int), ("prec_growth", C.c_double), ("precond", C.c_int),
+                ("ell_max", C.c_int), ("ell_tau", C.c_double)]
 
 
 class IterRecord(C.Structure):
     _fields_ = [("k", C.c_int), ("mu", C.c_double), ("rel_p", C.c_double), ("rel_d", C.c_double),
                 ("alpha_p", C.c_double), ("alpha_d", C.c_double), ("pcg_pred", C.c_int), ("pcg_corr", C.c_int),
                 ("rho", C.c_double), ("delta", C.c_double), ("t_sketch_ms", C.c_double),
-                ("t_pcg_ms", C.c_double), ("t_other_ms", C.c_double), ("prec_built", C.c_int)]
+                ("t_pcg_ms", C.c_double), ("t_other_ms", C.c_double), ("prec_built", C.c_int), ("ell", C.c_int),
+                ("lam_ell", C.c_double)]
 
 
 class Solution(C.Structure):

@@ -19,6 +19,7 @@
 // The same kernel also provides the T-only pass (A^T v with IPM epilogues) and the N-only
 // pass (A u) that Alg. 4 needs.
 #include <cstdlib>
+#include <mutex>
 
 #include "nys_common.cuh"
 
@@ -686,12 +687,18 @@ static size_t mv_smem_bytes(const MvCfg& c, int64_t rs, int stages, int cl, bool
   return b;
 }
 
+// process-wide caches, shared by every context: contexts may be driven from several host threads
+// at once (the loopback ranks of one process), so every access holds the lock
 static std::map<std::tuple<int, int, int64_t, int64_t, int64_t>, MvPlan> g_plans;
+static std::mutex g_plans_mu;
 
 static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, MvPlan& pl) {
   auto key = std::make_tuple(ctx->device, mode, m, n, lda);
-  auto itp = g_plans.find(key);
-  if (itp != g_plans.end()) { pl = itp->second; return NYS_OK; }
+  {
+    std::lock_guard<std::mutex> lk(g_plans_mu);
+    auto itp = g_plans.find(key);
+    if (itp != g_plans.end()) { pl = itp->second; return NYS_OK; }
+  }
   // Geometry for a cluster split cl: rows per CTA rs, thread config, stages, smem, kernel.
   struct Geo {
     int64_t rs;
@@ -848,7 +855,10 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, 
   if (grid < cl) grid = cl;
   pl.cfg = c; pl.cl = cl; pl.rs = rs; pl.stages = stages; pl.smem = smem; pl.npanels = npanels;
   pl.grid = grid; pl.rc = rc; pl.cdim = cl > 1 ? cl : rc; pl.nparts = grid / pl.cdim;
-  g_plans[key] = pl;
+  {
+    std::lock_guard<std::mutex> lk(g_plans_mu);
+    g_plans[key] = pl;
+  }
   if (getenv("NYS_DEBUG"))
     fprintf(stderr, "[nys] matvec plan mode=%d m=%lld n=%lld: T=%d GT=%d RPT=%d CPG=%d cl=%d rc=%d rs=%lld stages=%d smem=%zu grid=%d nparts=%d npanels=%lld\n",
             mode, (long long)m, (long long)n, c.T, c.GT, c.RPT, c.CPG, cl, rc, (long long)rs, stages, smem, grid, pl.nparts,
@@ -858,6 +868,8 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, 
 
 int ensure_max_smem(nys_ctx* ctx, const void* fn, size_t bytes) {
   static std::map<std::pair<int, const void*>, size_t> set;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
   auto key = std::make_pair(ctx->device, fn);
   auto it = set.find(key);
   if (it != set.end() && it->second >= bytes) return NYS_OK;

@@ -286,11 +286,7 @@ int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int
     NYS_TRY(ensure_max_smem(ctx, (const void*)chol_inv_packed_kernel, 208 * 1024));
     chol_inv_packed_kernel<<<1, 1024, need_packed, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);
   } else if (need <= 200 * 1024) {
-    static bool set = false;
-    if (!set) {
-      NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      set = true;
-    }
+    NYS_TRY(ensure_max_smem(ctx, (const void*)chol_inv_kernel<true>, 200 * 1024));
     chol_inv_kernel<true><<<1, 256, need, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc, nullptr);
   } else {
     double* gws = ctx->wsd("chol_ws", (size_t)ell * ell + (size_t)ell * (ell | 1));

@@ -783,7 +783,16 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   double *y = ctx->wsd("ipm_y", mm), *lam = ctx->wsd("ipm_lam", mm), *ax = ctx->wsd("ipm_ax", mm);
   double *rP = ctx->wsd("ipm_rP", mm), *rp = ctx->wsd("ipm_rp", mm), *xi = ctx->wsd("ipm_xi", mm);
   double *dyp = ctx->wsd("ipm_dyp", mm), *dyc = ctx->wsd("ipm_dyc", mm), *u1 = ctx->wsd("ipm_u1", mm);
-  const int le = ell > 0 ? ell : 1;
+  // adaptive rank (f3, reading F1): workspace for the largest rank the run may reach
+  int ell_cap = ell;
+  if (ell > 0 && opt->precond != 1 && opt->ell_max > ell) {
+    ell_cap = opt->ell_max;
+    if (ell_cap > m) ell_cap = (int)m;
+    if (ell_cap > 256) ell_cap = 256;
+  }
+  int ell_k = ell, ell_built = ell;      // rank of the next build / of the factors in use
+  double lam_ell_cur = 0.0;
+  const int le = ell_cap > 0 ? ell_cap : 1;
   double *Om = ctx->wsd("ipm_Om", (size_t)mp * le), *U = ctx->wsd("ipm_U", (size_t)mp * le);
   double *lamh = ctx->wsd("ipm_lamh", (size_t)le), *scoef = ctx->wsd("ipm_s", (size_t)le);
   Dots D{ctx};
@@ -981,15 +990,21 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
       auto ts = std::chrono::steady_clock::now();
       const int refresh = opt->prec_refresh > 0 ? opt->prec_refresh : 1;
       const bool rebuild = last_build < 0 || k - last_build >= refresh ||
-                           (opt->prec_growth > 0.0 && base_its > 0 && last_its > opt->prec_growth * base_its);
+                           (opt->prec_growth > 0.0 && base_its > 0 && last_its > opt->prec_growth * base_its) ||
+                           ell_k != ell_built;
       if (rebuild) {                                                  // f3: reuse between rebuilds
-        NYS_TRY(gen_omega(ctx, m, ell, opt->seed, (uint64_t)k + 1, Om));
-        NYS_TRY(sketch_impl(ctx, m, op.n, op.A, op.lda, op.d, op.e, ell, Om, U, lamh, nullptr));
+        NYS_TRY(gen_omega(ctx, m, ell_k, opt->seed, (uint64_t)k + 1, Om));
+        NYS_TRY(sketch_impl(ctx, m, op.n, op.A, op.lda, op.d, op.e, ell_k, Om, U, lamh, nullptr));
         last_build = k;
         base_its = -1;
         rec.prec_built = 1;
+        ell_built = ell_k;
+        NYS_CUDA_TRY(ctx, cudaMemcpyAsync(&lam_ell_cur, lamh + ell_built - 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        if (ell_cap > ell_k && lam_ell_cur > opt->ell_tau * delta)    // F1: grow for the next build
+          ell_k = std::min(2 * ell_k, ell_cap);
       }
-      NYS_TRY(launch_prec_coef(ctx, lamh, ell, delta, scoef));        // mu_prec = delta_k (A7)
+      NYS_TRY(launch_prec_coef(ctx, lamh, ell_built, delta, scoef));  // mu_prec = delta_k (A7)
       NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
       rec.t_sketch_ms = ms_since(ts);
       t_sketch += rec.t_sketch_ms;
@@ -1003,7 +1018,9 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
     NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
     auto tp1 = std::chrono::steady_clock::now();
-    NYS_TRY(pcg_impl(ctx, op, ell, U, mp, scoef, xi, dyp, opt->pcg_max_iter, pr, cfp));
+    rec.ell = use_chol ? ell : ell_built;
+    rec.lam_ell = use_chol ? 0.0 : lam_ell_cur;
+    NYS_TRY(pcg_impl(ctx, op, use_chol ? ell : ell_built, U, mp, scoef, xi, dyp, opt->pcg_max_iter, pr, cfp));
     rec.t_pcg_ms += ms_since(tp1);
     if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
     rec.pcg_pred = pr.iters;
@@ -1030,7 +1047,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
     NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
     auto tp2 = std::chrono::steady_clock::now();
-    NYS_TRY(pcg_impl(ctx, op, ell, U, mp, scoef, xi, dyc, opt->pcg_max_iter, pr, cfp));
+    NYS_TRY(pcg_impl(ctx, op, use_chol ? ell : ell_built, U, mp, scoef, xi, dyc, opt->pcg_max_iter, pr, cfp));
     rec.t_pcg_ms += ms_since(tp2);
     if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
     rec.pcg_corr = pr.iters;
@@ -1184,6 +1201,8 @@ void nys_default_options(nys_options* o) {
   o->prec_refresh = 1;
   o->prec_growth = 0.0;
   o->precond = 0;
+  o->ell_max = 0;
+  o->ell_tau = 10.0;
 }
 
 int nys_create(nys_ctx** out, int device, void* cuda_stream, const void* nccl_unique_id, int rank, int world) {
@@ -1238,6 +1257,7 @@ int nys_create(nys_ctx** out, int device, void* cuda_stream, const void* nccl_un
 }
 
 static std::map<nys_ctx*, nys::CholFactors> g_chol;  // last nys_partial_cholesky per context
+static std::mutex g_chol_mu;
 
 int nys_loopback_comm_create(int world, void* out128) {
   if (world < 2 || world > 16 || !out128) return NYS_EINVAL;
@@ -1270,7 +1290,10 @@ int nys_nccl_unique_id(void* out128) {
 
 int nys_destroy(nys_ctx* ctx) {
   if (!ctx) return NYS_OK;
-  g_chol.erase(ctx);
+  {
+    std::lock_guard<std::mutex> lk(g_chol_mu);
+    g_chol.erase(ctx);
+  }
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
@@ -1402,7 +1425,10 @@ int nys_partial_cholesky(nys_ctx* ctx, int64_t m, int64_t n, const double* A, in
   NormalOp op{m, n, lda, A, d, e, delta};
   CholFactors F;
   NYS_TRY(chol_build(ctx, op, ell, F));
-  g_chol[ctx] = F;
+  {
+    std::lock_guard<std::mutex> lk(g_chol_mu);
+    g_chol[ctx] = F;
+  }
   if (piv && ell > 0)
     NYS_CUDA_TRY(ctx, cudaMemcpyAsync(piv, F.piv, sizeof(int64_t) * ell, cudaMemcpyDeviceToDevice, ctx->stream));
   if (L && ell > 0) NYS_TRY(launch_transpose_u(ctx, ell, (int)m, F.Zt, ell, L));   // row-major -> column-major
@@ -1415,13 +1441,18 @@ int nys_partial_cholesky(nys_ctx* ctx, int64_t m, int64_t n, const double* A, in
 int nys_chol_precond_apply(nys_ctx* ctx, int64_t m, const double* v, double* out) {
   NYS_GUARD_BEGIN
   if (!ctx || !v || !out) return NYS_EINVAL;
-  auto it = g_chol.find(ctx);
-  if (it == g_chol.end() || it->second.m != m) {
-    ctx->set_error("nys_chol_precond_apply: no partial Cholesky factors of this size on the context");
-    return NYS_EINVAL;
+  CholFactors F;
+  {
+    std::lock_guard<std::mutex> lk(g_chol_mu);
+    auto it = g_chol.find(ctx);
+    if (it == g_chol.end() || it->second.m != m) {
+      ctx->set_error("nys_chol_precond_apply: no partial Cholesky factors of this size on the context");
+      return NYS_EINVAL;
+    }
+    F = it->second;
   }
   cudaSetDevice(ctx->device);
-  NYS_TRY(launch_chol_apply(ctx, it->second, v, out, 0, 0));
+  NYS_TRY(launch_chol_apply(ctx, F, v, out, 0, 0));
   return NYS_OK;
   NYS_GUARD_END
 }

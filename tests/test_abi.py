@@ -48,6 +48,7 @@ def test_default_options_match_oracle(lib):
             o.init_tol_rel, o.prec_refresh, o.prec_growth) == (r.tol, r.rho0, r.delta0, r.reg_floor, r.pcg_c,
                                                                 r.pcg_floor, r.pcg_max_iter, r.init_delta,
                                                                 r.init_tol_rel, r.prec_refresh, r.prec_growth)
+    assert (o.ell_max, o.ell_tau, o.precond) == (r.ell_max, r.ell_tau, 0)
 
 
 def test_product_package_does_not_import_oracle():

@@ -480,3 +480,21 @@ def test_chol_ipppmm_parity(ctx, cfg, kw):
     assert g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
     assert obj_agree(g, ref, inst=inst)
     assert abs(g["outer"] - ref.outer) <= 2
+
+
+# ------------------------------------------------------------------------ f3: adaptive rank (F1)
+def test_adaptive_rank_matches_oracle(ctx):
+    """The rank sequence (doubling while lam_hat_ell > tau delta_k, capped) and lam_hat_ell agree with
+    the oracle; the solve reaches the oracle's optimum."""
+    inst = make_config(1, m=200, n=800, ell=10)
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=10, ell_max=80, ell_tau=10.0))
+    g = _solve_gpu(ctx, inst, 10, ell_max=80, ell_tau=10.0)
+    assert g["status"] == 0 and ref.status == "optimal"
+    n_cmp = min(len(g["log"]), len(ref.log), 6)
+    assert [r["ell"] for r in g["log"][:n_cmp]] == [r["ell"] for r in ref.log[:n_cmp]]
+    for a, b in zip(g["log"][:n_cmp], ref.log[:n_cmp]):
+        # lam_hat_ell is the smallest captured eigenvalue: absolute accuracy ~ eps lam_hat_1, so relative 1e-6
+        assert abs(a["lam_ell"] - b["lam_ell"]) <= 1e-6 * abs(b["lam_ell"])
+    assert max(r["ell"] for r in g["log"]) == 80
+    assert obj_agree(g, ref, inst=inst)
+    assert abs(g["outer"] - ref.outer) <= 2
