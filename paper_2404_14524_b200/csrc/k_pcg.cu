@@ -56,6 +56,7 @@ struct PcgPParams {
   int flat_red;               // 1: grid barrier + every CTA reduces all partial rows; 0: two-level last-arriver tree  // debug: [3][G] arrival stamps of every CTA at the 3 syncs of iteration 14
   int64_t npanels;
   int64_t rows_per_cta;
+  int64_t ss;                 // stage row stride (lda when near-tight, else even(m))
 };
 
 // Grid barrier on a monotonically increasing arrival counter (zeroed before the launch): each CTA
@@ -87,7 +88,10 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   constexpr int BN = NG * CPG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int S = P.stages;
-  const int64_t rs = (P.m + 1) & ~int64_t(1);  // full column height (cl == 1), even for 16-B copies
+  // stage row stride: lda when it is near-tight (a panel of BN consecutive columns is then ONE bulk
+  // copy; the padding rows are read but masked off), else the even column height with one copy per column
+  const int64_t rs = P.ss;
+  const bool contig = (P.ss == P.lda);
   double* stage = reinterpret_cast<double*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(stage + (size_t)S * BN * rs);
   uint64_t* empty = full + S;
@@ -167,10 +171,17 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
         const int64_t col0 = c_lo + it * BN;
         int64_t ncols = c_hi - col0;
         ncols = ncols > BN ? BN : ncols;
-        mbar_arrive_expect_tx(&full[s], (uint32_t)ncols * copy_bytes);
-        for (int c = 0; c < ncols; ++c)
-          bulk_g2s(stage + ((size_t)s * BN + c) * rs, P.A + (col0 + c) * P.lda, copy_bytes, &full[s],
+        if (contig) {
+          const uint32_t bytes = (uint32_t)((ncols - 1) * rs * 8) + copy_bytes;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          bulk_g2s(stage + (size_t)s * BN * rs, P.A + col0 * P.lda, bytes, &full[s],
                    it < P.l2_keep ? pol_keep : pol_stream);
+        } else {
+          mbar_arrive_expect_tx(&full[s], (uint32_t)ncols * copy_bytes);
+          for (int c = 0; c < ncols; ++c)
+            bulk_g2s(stage + ((size_t)s * BN + c) * rs, P.A + (col0 + c) * P.lda, copy_bytes, &full[s],
+                     it < P.l2_keep ? pol_keep : pol_stream);
+        }
         ++q;
       }
       s_issued = q;
@@ -514,10 +525,25 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     }
     double pwacc = 0.0;
     stamp(8);
+    // d of the next panel is loaded one panel ahead (its L2 latency would otherwise sit on every
+    // panel's critical path: short columns make that dominant)
+    double dnext[CPG];
+#pragma unroll
+    for (int c = 0; c < CPG; ++c) {
+      const int64_t col = c_lo + (int64_t)g * CPG + c;
+      dnext[c] = (niter > 0 && col < c_hi) ? __ldg(P.d + col) : 0.0;
+    }
     for (int64_t it = 0; it < niter; ++it, ++qc) {
       const int s = (int)(qc % S);
       const uint32_t par = (uint32_t)((qc / S) & 1);
       const int64_t col0 = c_lo + it * BN + (int64_t)g * CPG;
+      double dpre[CPG];
+#pragma unroll
+      for (int c = 0; c < CPG; ++c) {
+        dpre[c] = dnext[c];
+        const int64_t coln = col0 + BN + c;
+        dnext[c] = (it + 1 < niter && coln < c_hi) ? __ldg(P.d + coln) : 0.0;
+      }
       mbar_wait(&full[s], par);
       if (it == 0) stamp(9);
       if (it == niter / 2) stamp(10);
@@ -535,9 +561,6 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      double dpre[CPG];
-#pragma unroll
-      for (int c = 0; c < CPG; ++c) dpre[c] = (col0 + c < c_hi) ? __ldg(P.d + col0 + c) : 0.0;
       double pd[CPG];
 #pragma unroll
       for (int c = 0; c < CPG; ++c) {
@@ -665,7 +688,7 @@ static PcgCfg pcg_pick(int64_t m) {
   if (m <= 256) return {256, 64, 4, 2};
   if (m <= 1024) return {256, 128, 8, 2};
   if (m <= 2048) return {256, 256, 8, 4};
-  if (m <= 4096) return {512, 512, 8, 2};
+  if (m <= 4096) return getenv("NYS_PCG_T512") ? PcgCfg{512, 512, 8, 2} : PcgCfg{256, 256, 16, 2};
   return {512, 512, 16, 1};
 }
 typedef void (*PcgKernel)(const PcgPParams);
@@ -674,6 +697,7 @@ static PcgKernel pcg_kernel_for(const PcgCfg& c) {
   if (c.GT == 32 && c.RPT == 4) return pcg_persistent_kernel<256, 32, 4, 2>;
   if (c.GT == 64) return pcg_persistent_kernel<256, 64, 4, 2>;
   if (c.GT == 128) return pcg_persistent_kernel<256, 128, 8, 2>;
+  if (c.GT == 256 && c.RPT == 16) return pcg_persistent_kernel<256, 256, 16, 2>;
   if (c.GT == 256 && c.CPG == 2) return pcg_persistent_kernel<256, 256, 8, 2>;
   if (c.GT == 256) return pcg_persistent_kernel<256, 256, 8, 4>;
   if (c.RPT == 8) return pcg_persistent_kernel<512, 512, 8, 2>;
@@ -695,7 +719,8 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
   }
   const int NG = c.T / c.GT, WPG = c.GT / 32, BN = NG * c.CPG;
   const int64_t mp = (m + 1) & ~int64_t(1);
-  const size_t stage_bytes = (size_t)BN * mp * 8;
+  const int64_t ss = (lda >= mp && lda <= mp + 32) ? lda : mp;
+  const size_t stage_bytes = (size_t)BN * ss * 8;
   const size_t budget = (mp <= 1024) ? 96 * 1024 : 196 * 1024;
   int stages = (int)(budget / stage_bytes);
   if (stages > 8) stages = 8;
@@ -732,6 +757,7 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
   if (const char* e = getenv("NYS_PCG_RED")) P.flat_red = (e[0] == 'f');
   P.stages = stages;
   P.npanels = npanels;
+  P.ss = ss;
   P.rows_per_cta = (m + G - 1) / G;
   {
     // prefetch depth: keep about half of L2 (~60 MB) of A in flight ahead of the ring
