@@ -650,6 +650,238 @@ __global__ void __launch_bounds__(1024) jacobi_cluster_kernel(int n, const doubl
   cl.sync();  // no CTA leaves while a peer still reads its shared memory
 }
 
+// Block one-sided Jacobi over a cluster of C CTAs (ell > 112): the columns form 2C blocks of
+// bs = ceil(ell / 2C); each CTA holds two blocks (a "top" and a "bottom" slot, plus a spare) in its
+// OWN shared memory and processes their column pairs locally (one warp per pair, a CTA barrier per
+// local round); between block rounds the blocks move one position along the round-robin ring
+// (t_1 .. t_{C-1}, b_{C-1} .. b_0; t_0 fixed) through two DSMEM pushes into free slots.  Block round 0
+// of a sweep pairs every column of the two blocks (the within-block pairs), the other 2C - 2 rounds
+// the cross pairs only, so each pair of columns meets once per sweep (a cyclic ordering).  Same
+// rotation, incremental norms, convergence test and output as jacobi_kernel.  Shared memory is read
+// remotely only by the block moves, never per pair (per-pair DSMEM traffic made the column-cyclic
+// cluster kernel ~11 us per round).
+template <int NMAX, int C>
+__global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const double* R, int ldr, double* Vout,
+                                                            int ldv, double* sigma, double* jsweeps) {
+  constexpr int E = NMAX / 32;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  extern __shared__ double jsm[];
+  // slot layout: X (bs columns x n), V (bs x n), nrm (bs), block id (1), pad
+  const size_t slot = ((size_t)2 * bs * n + bs + 2 + 1) & ~(size_t)1;   // even: 16-byte aligned slots
+  double* sl[3] = {jsm, jsm + slot, jsm + 2 * slot};
+  __shared__ int smap[3];             // this CTA's slot indices of (top, bottom, spare); read by peers
+  __shared__ double flag_l[2];
+  __shared__ double sv_all[NMAX];
+  __shared__ int order[NMAX];
+  if (threadIdx.x == 0) { smap[0] = 0; smap[1] = 1; smap[2] = 2; }
+  int top = 0, bot = 1, spare = 2;
+  const int nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto Xc = [&](double* s, int j) { return s + (size_t)j * n; };
+  auto Vc = [&](double* s, int j) { return s + (size_t)bs * n + (size_t)j * n; };
+  auto Nr = [&](double* s) { return s + (size_t)2 * bs * n; };
+  auto Bid = [&](double* s) { return s + (size_t)2 * bs * n + bs; };
+  auto cnt = [&](int b) { const int c0 = b * bs; return c0 >= n ? 0 : (n - c0 < bs ? n - c0 : bs); };
+  // initial blocks: t_c = block c, b_c = block 2C - 1 - c
+  for (int w = 0; w < 2; ++w) {
+    double* S = sl[w];
+    const int b = (w == 0) ? rank : 2 * C - 1 - rank;
+    for (int e = threadIdx.x; e < bs * n; e += blockDim.x) {
+      const int j = e / n, i = e % n, gj = b * bs + j;
+      Xc(S, j)[i] = (j < cnt(b)) ? R[gj + (size_t)i * ldr] : 0.0;   // X = R^T
+      Vc(S, j)[i] = (j < cnt(b) && i == gj) ? 1.0 : 0.0;
+    }
+    if (threadIdx.x == 0) Bid(S)[0] = (double)b;
+  }
+  const double tol = fmax(1e-15, (double)n * 0x1p-53);
+  const double tol2 = tol * tol;
+  auto wsum = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  __syncthreads();
+  // one pair (p, q) of LOCAL columns: p, q in [0, 2 bs) (< bs: top slot, else bottom slot)
+  auto do_pair = [&](int p, int q, double floor_g) {
+    double* Sp = sl[p < bs ? top : bot];
+    double* Sq = sl[q < bs ? top : bot];
+    const int jp = p < bs ? p : p - bs, jq = q < bs ? q : q - bs;
+    const int bp = (int)Bid(Sp)[0], bq = (int)Bid(Sq)[0];
+    if (jp >= cnt(bp) || jq >= cnt(bq)) return;
+    double* Xp = Xc(Sp, jp);
+    double* Xq = Xc(Sq, jq);
+    double* Vp = Vc(Sp, jp);
+    double* Vq = Vc(Sq, jq);
+    double xp[E], xq[E], vp[E], vq[E];
+    double ga = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = lane + 32 * e;
+      xp[e] = (i < n) ? Xp[i] : 0.0;
+      xq[e] = (i < n) ? Xq[i] : 0.0;
+      vp[e] = (i < n) ? Vp[i] : 0.0;
+      vq[e] = (i < n) ? Vq[i] : 0.0;
+      ga = fma(xp[e], xq[e], ga);
+    }
+    ga = wsum(ga);
+    // the global column with the smaller index plays "p" (as in the column-cyclic kernels)
+    const bool swp = (bp * bs + jp) > (bq * bs + jq);
+    double* np_ = Nr(Sp) + jp;
+    double* nq_ = Nr(Sq) + jq;
+    const double al = swp ? *nq_ : *np_, be = swp ? *np_ : *nq_;
+    if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {
+      double c, sn, t;
+      jacobi_rotation(al, be, ga, c, sn, t);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = lane + 32 * e;
+        if (i < n) {
+          const double a0 = swp ? xq[e] : xp[e], a1 = swp ? xp[e] : xq[e];
+          const double w0 = swp ? vq[e] : vp[e], w1 = swp ? vp[e] : vq[e];
+          double* X0 = swp ? Xq : Xp;
+          double* X1 = swp ? Xp : Xq;
+          double* V0 = swp ? Vq : Vp;
+          double* V1 = swp ? Vp : Vq;
+          X0[i] = c * a0 - sn * a1;
+          X1[i] = sn * a0 + c * a1;
+          V0[i] = c * w0 - sn * w1;
+          V1[i] = sn * w0 + c * w1;
+        }
+      }
+      if (lane == 0) {
+        double* n0 = swp ? nq_ : np_;
+        double* n1 = swp ? np_ : nq_;
+        *n0 = fmax(al - t * ga, 0.0);
+        *n1 = be + t * ga;
+        flag_l[1] = 1.0;
+      }
+    }
+  };
+  // move a slot's contents (X, V, nrm, id) into a peer's slot (DSMEM, 16-byte stores)
+  auto push = [&](double* src, int dst_rank, int dst_slot_idx) {
+    double* dst = cl.map_shared_rank(sl[dst_slot_idx], dst_rank);
+    const size_t nv = slot / 2;
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    for (size_t e = threadIdx.x; e < nv; e += blockDim.x) d2[e] = s2[e];
+  };
+  int sweep = 0;
+  for (; sweep < 30; ++sweep) {
+    for (int w = 0; w < 2; ++w) {  // exact norms of the local columns
+      double* S = w == 0 ? sl[top] : sl[bot];
+      for (int j = warp; j < bs; j += nwarp) {
+        double a = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = lane + 32 * e;
+          if (i < n) a = fma(Xc(S, j)[i], Xc(S, j)[i], a);
+        }
+        a = wsum(a);
+        if (lane == 0) Nr(S)[j] = a;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mx = 0.0;
+      for (int j = 0; j < bs; ++j) mx = fmax(mx, fmax(Nr(sl[top])[j], Nr(sl[bot])[j]));
+      flag_l[0] = mx;
+      flag_l[1] = 0.0;
+    }
+    cl.sync();
+    double mxall = 0.0;
+    for (int r = 0; r < C; ++r) mxall = fmax(mxall, *cl.map_shared_rank(&flag_l[0], r));
+    const double floor_g = 1e-2 * 0x1p-52 * mxall;
+    for (int br = 0; br < 2 * C - 1; ++br) {
+      if (br == 0) {                                   // all pairs of the 2 bs local columns
+        const int P2 = 2 * bs;                         // even
+        for (int r = 0; r < P2 - 1; ++r) {
+          for (int pi = warp; pi < P2 / 2; pi += nwarp) {
+            int a, b;
+            if (pi == 0) { a = r; b = P2 - 1; }
+            else {
+              a = r + pi; if (a >= P2 - 1) a -= P2 - 1;
+              b = r - pi; if (b < 0) b += P2 - 1;
+            }
+            do_pair(a < b ? a : b, a < b ? b : a, floor_g);
+          }
+          __syncthreads();
+        }
+      } else {                                         // cross pairs (top i, bottom (i + r) mod bs)
+        for (int r = 0; r < bs; ++r) {
+          for (int i = warp; i < bs; i += nwarp) do_pair(i, bs + (i + r) % bs, floor_g);
+          __syncthreads();
+        }
+      }
+      // ---- move the blocks one position along the ring -----------------------------------------
+      cl.sync();                                       // every CTA finished with its blocks
+      // phase A: t_c -> t_{c+1} (c = 1 .. C-2), b_0 -> t_1; t_{C-1} becomes b_{C-1} locally (below)
+      if (rank >= 1 && rank <= C - 2) push(sl[top], rank + 1, *cl.map_shared_rank(&smap[2], rank + 1));
+      if (rank == 0) push(sl[bot], 1, *cl.map_shared_rank(&smap[2], 1));
+      cl.sync();
+      // phase B: b_c -> b_{c-1} (c = 1 .. C-1) into the slot freed in phase A
+      //   (CTA c - 1 >= 1: its old top slot; CTA 0: its old bottom slot)
+      if (rank >= 1) push(sl[bot], rank - 1, *cl.map_shared_rank(&smap[rank - 1 >= 1 ? 0 : 1], rank - 1));
+      cl.sync();
+      // slot renaming: CTA 0 keeps its slots (its bottom slot was refilled in phase B); the others take
+      // the spare (filled in phase A) as top, the old top (refilled in B, or relabelled at C - 1) as
+      // bottom, and the old bottom (sent in B) as spare
+      if (rank != 0) {
+        const int nt = spare, nb = top, ns = bot;
+        top = nt; bot = nb; spare = ns;
+      }
+      if (threadIdx.x == 0) { smap[0] = top; smap[1] = bot; smap[2] = spare; }
+      cl.sync();                                       // peers read smap only after this
+    }
+    bool any = false;
+    for (int r = 0; r < C; ++r) any = any || (*cl.map_shared_rank(&flag_l[1], r) != 0.0);
+    cl.sync();
+    if (!any) break;
+  }
+  if (rank == 0 && threadIdx.x == 0) jsweeps[0] = (double)(sweep + 1);
+  // sigma of the local columns
+  for (int w = 0; w < 2; ++w) {
+    double* S = w == 0 ? sl[top] : sl[bot];
+    for (int j = warp; j < bs; j += nwarp) {
+      double a = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = lane + 32 * e;
+        if (i < n) a = fma(Xc(S, j)[i], Xc(S, j)[i], a);
+      }
+      a = wsum(a);
+      if (lane == 0) Nr(S)[j] = sqrt(a);
+    }
+  }
+  __syncthreads();
+  // every CTA publishes (global index -> sigma) of its two live blocks into sv_all of every peer
+  for (int w = 0; w < 2; ++w) {
+    double* S = w == 0 ? sl[top] : sl[bot];
+    const int b = (int)Bid(S)[0];
+    for (int j = threadIdx.x; j < cnt(b); j += blockDim.x)
+      for (int r = 0; r < C; ++r) *cl.map_shared_rank(&sv_all[b * bs + j], r) = Nr(S)[j];
+  }
+  cl.sync();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {  // rank sort, ties by index (the same in every CTA)
+    int rk = 0;
+    for (int k = 0; k < n; ++k) rk += (sv_all[k] > sv_all[j]) || (sv_all[k] == sv_all[j] && k < j);
+    order[rk] = j;
+  }
+  __syncthreads();
+  // each CTA writes the output columns whose source column it holds
+  for (int w = 0; w < 2; ++w) {
+    double* S = w == 0 ? sl[top] : sl[bot];
+    const int b = (int)Bid(S)[0];
+    for (int jo = 0; jo < n; ++jo) {
+      const int src = order[jo];
+      if (src / bs != b || src - b * bs >= cnt(b)) continue;
+      const double* vcol = Vc(S, src - b * bs);
+      if (threadIdx.x == 0) sigma[jo] = sv_all[src];
+      for (int i = threadIdx.x; i < n; i += blockDim.x) Vout[i + (size_t)jo * ldv] = vcol[i];
+    }
+  }
+  cl.sync();
+}
+
 template <int C>
 static int launch_jacobi_cluster(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma,
                                  size_t smem) {
@@ -670,6 +902,29 @@ static int launch_jacobi_cluster(nys_ctx* ctx, int ell, const double* R, int ldr
   cfg.attrs = at;
   cfg.numAttrs = 1;
   NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, ell, R, ldr, V, ldv, sigma, ctx->sc + S_JSWEEPS));
+  return NYS_OK;
+}
+
+static int launch_jacobi_block(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+  constexpr int C = 8;
+  const int bs = (ell + 2 * C - 1) / (2 * C);
+  const size_t slot = ((size_t)2 * bs * ell + bs + 2 + 1) & ~(size_t)1;
+  const size_t smem = 3 * slot * sizeof(double);
+  auto k = jacobi_block_kernel<256, C>;
+  NYS_TRY(ensure_max_smem(ctx, (const void*)k, smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(32 * (bs < 1 ? 1 : bs));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, ell, bs, R, ldr, V, ldv, sigma, ctx->sc + S_JSWEEPS));
   return NYS_OK;
 }
 
@@ -696,7 +951,9 @@ static int launch_jacobi_t(nys_ctx* ctx, int ell, const double* R, int ldr, doub
     int C = 2;
     while (C < 8 && 2 * (size_t)((ell + C - 1) / C) * ell * sizeof(double) > 208 * 1024) C *= 2;
     const size_t smem = 2 * (size_t)((ell + C - 1) / C) * ell * sizeof(double);
-    if (NMAX == 256 && smem <= 208 * 1024 && getenv("NYS_JACOBI_GLOBAL") == nullptr) {
+    if (NMAX == 256 && getenv("NYS_JACOBI_CYCLIC") == nullptr && getenv("NYS_JACOBI_GLOBAL") == nullptr) {
+      NYS_TRY(launch_jacobi_block(ctx, ell, R, ldr, V, ldv, sigma));   // block Jacobi over 8 CTAs
+    } else if (NMAX == 256 && smem <= 208 * 1024 && getenv("NYS_JACOBI_GLOBAL") == nullptr) {
       if (C == 2) NYS_TRY(launch_jacobi_cluster<2>(ctx, ell, R, ldr, V, ldv, sigma, smem));
       else if (C == 4) NYS_TRY(launch_jacobi_cluster<4>(ctx, ell, R, ldr, V, ldv, sigma, smem));
       else NYS_TRY(launch_jacobi_cluster<8>(ctx, ell, R, ldr, V, ldv, sigma, smem));
@@ -710,6 +967,14 @@ static int launch_jacobi_t(nys_ctx* ctx, int ell, const double* R, int ldr, doub
 }
 
 int launch_jacobi_svd(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+  // block Jacobi over an 8-CTA cluster from ell = block_min on (tuning override NYS_JACOBI_BLOCK_MIN)
+  int block_min = 72;   // measured crossover (sketch at m = 20532): 64 equal, 80 2.65 vs 3.59 ms, 112 3.99 vs 6.21 ms
+  if (const char* e = getenv("NYS_JACOBI_BLOCK_MIN")) block_min = atoi(e);
+  if (ell >= block_min && ell >= 16 && ell <= 256 && getenv("NYS_JACOBI_CYCLIC") == nullptr) {
+    NYS_TRY(launch_jacobi_block(ctx, ell, R, ldr, V, ldv, sigma));
+    ctx->launches++;
+    return ctx->check_launch("jacobi_block");
+  }
   if (ell <= 64) return launch_jacobi_t<64>(ctx, ell, R, ldr, V, ldv, sigma);
   if (ell <= 112) return launch_jacobi_t<128>(ctx, ell, R, ldr, V, ldv, sigma);   // above: cluster path
   return launch_jacobi_t<256>(ctx, ell, R, ldr, V, ldv, sigma);
