@@ -905,11 +905,12 @@ static int launch_jacobi_cluster(nys_ctx* ctx, int ell, const double* R, int ldr
   return NYS_OK;
 }
 
-static int launch_jacobi_block(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
-  constexpr int C = 8;
+template <int C>
+static int launch_jacobi_block_c(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
   const int bs = (ell + 2 * C - 1) / (2 * C);
   const size_t slot = ((size_t)2 * bs * ell + bs + 2 + 1) & ~(size_t)1;
   const size_t smem = 3 * slot * sizeof(double);
+  if (smem > 220 * 1024) { ctx->set_error("jacobi_block: blocks do not fit shared memory"); return NYS_EINVAL; }
   auto k = jacobi_block_kernel<256, C>;
   NYS_TRY(ensure_max_smem(ctx, (const void*)k, smem));
   cudaLaunchConfig_t cfg = {};
@@ -926,6 +927,16 @@ static int launch_jacobi_block(nys_ctx* ctx, int ell, const double* R, int ldr, 
   cfg.numAttrs = 1;
   NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, ell, bs, R, ldr, V, ldv, sigma, ctx->sc + S_JSWEEPS));
   return NYS_OK;
+}
+// cluster size 8 (measured best or equal from ell = 64 to 200 against clusters of 2 and 4); the
+// override must keep bs = ceil(ell / 2C) <= 16 (one warp per pair, 512 threads)
+static int launch_jacobi_block(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+  int C = 8;
+  if (const char* e = getenv("NYS_JACOBI_C")) C = atoi(e);
+  if ((ell + 2 * C - 1) / (2 * C) > 16) C = 8;
+  if (C == 2) return launch_jacobi_block_c<2>(ctx, ell, R, ldr, V, ldv, sigma);
+  if (C == 4) return launch_jacobi_block_c<4>(ctx, ell, R, ldr, V, ldv, sigma);
+  return launch_jacobi_block_c<8>(ctx, ell, R, ldr, V, ldv, sigma);
 }
 
 template <int NMAX>
