@@ -15,6 +15,7 @@
 // iterations (A does not depend on the iterate), so the barrier phases overlap the HBM stream of
 // the next matvec.  Grid barriers involve the consumer threads only; the producer polls a stop
 // flag so it can never block the exit.
+#include <chrono>
 #include <cstdlib>
 #include <vector>
 
@@ -712,6 +713,7 @@ bool pcg_persistent_supported(nys_ctx* ctx, int64_t m, int64_t n, int ell) {
 int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
                           const double* e, const double* U, int64_t ldu, int ell, const double* s, const double* rhs,
                           double* x, int max_iter) {
+  const auto hp0 = std::chrono::steady_clock::now();
   PcgCfg c = pcg_pick(m);
   if (const char* ov = getenv("NYS_PCG_CFG")) {  // tuning override "T,GT,RPT,CPG" (must be instantiated)
     PcgCfg o;
@@ -793,8 +795,15 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
     P.trace_arr = (unsigned long long*)ctx->ws("pp_trace_arr", 3 * G * 8);
     NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.trace_arr, 0, 3 * G * 8, ctx->stream));
   }
+  const auto hp1 = std::chrono::steady_clock::now();
   NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, P));
   ctx->launches++;
+  if (getenv("NYS_PCG_HOSTPROF")) {
+    const auto hp2 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pcghost] prep %.1f us, launch call %.1f us\n",
+            std::chrono::duration<double, std::micro>(hp1 - hp0).count(),
+            std::chrono::duration<double, std::micro>(hp2 - hp1).count());
+  }
   if (trace) {
     unsigned long long h[2 * 32 * 16];
     NYS_CUDA_TRY(ctx, cudaMemcpyAsync(h, P.trace, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
