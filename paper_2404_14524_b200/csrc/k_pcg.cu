@@ -42,7 +42,6 @@ struct PcgPParams {
   int64_t wp_ld;
   double* pwp;           // [G]
   double* part1;         // [G][(1 + ell)]   (rr, U^T r) partial row per CTA
-  double* part2;         // [G]              r^T z partials
   double* gtot;          // [ceil(G/RG)][1 + ell] group totals of part1
   double* tot;           // [1 + ell] grand totals
   unsigned int* rbar;    // [66]: group arrival counters [0, 64), top counter [64], publish flag [65]
@@ -79,8 +78,6 @@ __device__ __forceinline__ void pcg_grid_barrier(unsigned int* bar, unsigned int
 
 constexpr int RG = 16;  // CTAs per first-level reduction group (G <= 64 * RG)
 
-// deterministic sum over G partials of column j (one warp)
-__device__ __forceinline__ double col_sum(const double* part, int j, int G) { return warp_sum_array(part + (size_t)j * G, G); }
 
 template <int T, int GT, int RPT, int CPG>
 __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPParams P) {
@@ -748,7 +745,6 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
   P.Wp = ctx->wsd("pp_Wp", (size_t)G * mp);
   P.pwp = ctx->wsd("pp_pwp", (size_t)G);
   P.part1 = ctx->wsd("pp_part1", (size_t)(1 + ell) * G);
-  P.part2 = ctx->wsd("pp_part2", (size_t)G);
   P.sc = ctx->sc;
   P.bar = (unsigned int*)ctx->ws("pp_bar", 64 + 66 * 4);
   P.rbar = P.bar + 16;
