@@ -2,19 +2,19 @@
 // — ONE cooperative launch for the whole solve (single GPU, m <= 8192 so that a CTA
 // holds the full column height).
 //
-// Every CTA owns a fixed set of column panels of A (as in the fused matvec, k_matvec.cu) and a
-// fixed chunk of rows of the m-space vectors.  Per iteration:
-//   P1  v = z + beta p  (all rows, registers);   w_partial = A_panels (d o (A_panels^T v)),
-//       p^T N p partial                                                   -> grid barrier
-//   P2  alpha = rz / p^T w; own rows: w = sum partials + (delta + e) p; x += alpha p;
-//       r -= alpha w; ||r||^2 and U^T r partials                           -> grid barrier
-//   P3  every CTA sums the same partials in the same order (identical decisions):
-//       converged? h = s o (U^T r); own rows: z = r + U h; r^T z partial  -> grid barrier
-//   P4  beta = rz_new / rz
+// Every CTA owns a contiguous, balanced range of columns of A (streamed in panels, as in the fused
+// matvec, k_matvec.cu) and a fixed chunk of rows of the m-space vectors.  Per iteration k:
+//   P1  load p_k (all rows); w_partial = A_cols (d o (A_cols^T p_k)), p^T N p partial
+//                                                                          -> grid barrier
+//   P2  alpha = rz / p^T N p; own rows: w = sum of the partials + (delta + e) p; x += alpha p;
+//       r -= alpha w; ||r||^2 and U^T r partial rows                       -> grid barrier
+//   P3  every CTA sums all partial rows itself in one fixed order (identical decisions):
+//       converged? h = s o (U^T r); r^T z = ||r||^2 + (U^T r)^T h (no extra reduction);
+//       beta; own rows: z = r + U h, p_{k+1} = z + beta p_k              -> grid barrier
 // The producer warp streams A panels through the S-stage cp.async.bulk ring CONTINUOUSLY across
-// iterations (A does not depend on the iterate), so the barrier phases overlap the HBM stream of
-// the next matvec.  Grid barriers involve the consumer threads only; the producer polls a stop
-// flag so it can never block the exit.
+// iterations (A does not depend on the iterate) and prefetches further panels into L2, so HBM keeps
+// streaming through the barrier phases.  Grid barriers involve the consumer threads only; the
+// producer polls a stop flag so it can never block the exit.
 #include <chrono>
 #include <cstdlib>
 #include <vector>
