@@ -392,6 +392,40 @@ def test_ipppmm_svm_structured_parity(ctx, N, d, ell):
     assert np.linalg.norm(inst.c + inst.q * x - A.T @ y - z) / (1 + np.linalg.norm(inst.c)) <= 1e-8
 
 
+def test_ipppmm_config2_full_kkt(ctx):
+    """BASELINE configs[2] at full size (N = 50000 samples, d = 1000, the SVM operator, the bench's
+    launch configuration): the oracle cannot run it (A would be 40 GB dense), so the solve is checked
+    by properties that hold at any size — the KKT residuals recomputed here in fp64 with the
+    structured operator, x, z >= 0, and the reported duality gap equal to its algebraic identity."""
+    from paper_2404_14524_b200 import colmajor_device
+    inst = make_config(2)
+    Xt = inst.extra["Xt"]
+    N, dd = Xt.shape
+    Xd, lda = colmajor_device(Xt)
+    g = ctx.nys_ipppmm_solve(Xd, lda, N, dev(inst.q), dev(inst.b), dev(inst.c), ell=inst.ell, structure=1)
+    torch.cuda.synchronize()
+    assert g["status"] == 0 and g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    x, y, z = g["x"].cpu().numpy(), g["y"].cpu().numpy(), g["z"].cpu().numpy()
+    wp, wm, xi, sl = x[:dd], x[dd:2 * dd], x[2 * dd:2 * dd + N], x[2 * dd + N:]
+    Ax = Xt @ (wp - wm) + xi - sl                                      # A = [Xt, -Xt, I, -I]
+    g_ = Xt.T @ y
+    Aty = np.concatenate([g_, -g_, y, -y])
+    rP = inst.b - Ax
+    rD = inst.c + inst.q * x - Aty - z
+    assert np.linalg.norm(rP) / (1 + np.linalg.norm(inst.b)) <= 1.01e-8
+    assert np.linalg.norm(rD) / (1 + np.linalg.norm(inst.c)) <= 1.01e-8
+    assert x.min() > 0 and z.min() > 0
+    f = 0.5 * x @ (inst.q * x) + inst.c @ x
+    assert abs(f - g["obj"]) <= 1e-10 * abs(f)
+    # the reported gap is the algebraic identity p - d = x^T r_D + x^T z - y^T r_P of this iterate
+    gap = g["obj"] - g["dual_obj"]
+    ident = x @ rD + x @ z - y @ rP
+    scale = abs(x) @ abs(inst.c + inst.q * x) + abs(y) @ abs(inst.b) + abs(x) @ z + 1.0
+    assert abs(gap - ident) <= 1e-10 * scale
+    band = abs(gap) + np.linalg.norm(x) * np.linalg.norm(rD) + np.linalg.norm(y) * np.linalg.norm(rP)
+    print(f"config 2: f = {f!r}, certified band of f* = {band:.3e} (A17')")
+
+
 def test_ipppmm_config3_full(ctx):
     """BASELINE configs[3] at full size (m=64, n=200000, l=64 = m: the Nystrom P^{-1} is exact)."""
     inst = make_config(3)
