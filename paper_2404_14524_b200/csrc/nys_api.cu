@@ -792,6 +792,14 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   }
   int ell_k = ell, ell_built = ell;      // rank of the next build / of the factors in use
   double lam_ell_cur = 0.0;
+  // per-iteration phase timing with CUDA events (no stream synchronisation of its own: the events
+  // are read after the iteration's residual read-back, which synchronises anyway)
+  struct PhaseEvents {
+    cudaEvent_t e[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    PhaseEvents() { for (auto& v : e) cudaEventCreate(&v); }
+    ~PhaseEvents() { for (auto& v : e) if (v) cudaEventDestroy(v); }
+    float ms(int a, int b) const { float t = 0.f; cudaEventElapsedTime(&t, e[a], e[b]); return t; }
+  } pev;
   const int le = ell_cap > 0 ? ell_cap : 1;
   double *Om = ctx->wsd("ipm_Om", (size_t)mp * le), *U = ctx->wsd("ipm_U", (size_t)mp * le);
   double *lamh = ctx->wsd("ipm_lamh", (size_t)le), *scoef = ctx->wsd("ipm_s", (size_t)le);
@@ -979,15 +987,13 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     else NYS_TRY(launch_scaling(ctx, n, q, x, z, rho, d));
     NormalOp op;
     NYS_TRY(AO.normal_op(d, delta, op));
+    NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[0], ctx->stream));
+    bool built_now = false;
+    const double delta_build = delta;
     if (use_chol) {                                                   // P:250-349, every iteration
-      auto ts = std::chrono::steady_clock::now();
       NYS_TRY(chol_build(ctx, op, ell, CF));
-      NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
       rec.prec_built = 1;
-      rec.t_sketch_ms = ms_since(ts);
-      t_sketch += rec.t_sketch_ms;
     } else if (ell > 0) {                                             // P:759, Alg. 2
-      auto ts = std::chrono::steady_clock::now();
       const int refresh = opt->prec_refresh > 0 ? opt->prec_refresh : 1;
       const bool rebuild = last_build < 0 || k - last_build >= refresh ||
                            (opt->prec_growth > 0.0 && base_its > 0 && last_its > opt->prec_growth * base_its) ||
@@ -999,16 +1005,14 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
         base_its = -1;
         rec.prec_built = 1;
         ell_built = ell_k;
-        NYS_CUDA_TRY(ctx, cudaMemcpyAsync(&lam_ell_cur, lamh + ell_built - 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
-        NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-        if (ell_cap > ell_k && lam_ell_cur > opt->ell_tau * delta)    // F1: grow for the next build
-          ell_k = std::min(2 * ell_k, ell_cap);
+        built_now = true;
+        // lambda_hat_ell into a device scalar slot: read with the iteration's residuals (F1 below)
+        NYS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->sc + S_LAML, lamh + ell_built - 1, 8, cudaMemcpyDeviceToDevice,
+                                          ctx->stream));
       }
       NYS_TRY(launch_prec_coef(ctx, lamh, ell_built, delta, scoef));  // mu_prec = delta_k (A7)
-      NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-      rec.t_sketch_ms = ms_since(ts);
-      t_sketch += rec.t_sketch_ms;
     }
+    NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[1], ctx->stream));
     NYS_TRY(launch_set_slots(ctx, S_MUCUR, mu));
     // ---- predictor ----
     if (gen) NYS_TRY(launch_gen_pred_rhs(ctx, n, vt, ub, x, z, w, sv, zeta, rD, rho, d, rd, rxz, ru, rws, xiau, t));
@@ -1017,11 +1021,10 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(AO.Ax(t, xi, rp));                                        // xi = r_p + A d (r_d + xi_au)
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
     NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
-    auto tp1 = std::chrono::steady_clock::now();
     rec.ell = use_chol ? ell : ell_built;
-    rec.lam_ell = use_chol ? 0.0 : lam_ell_cur;
+    NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[2], ctx->stream));
     NYS_TRY(pcg_impl(ctx, op, use_chol ? ell : ell_built, U, mp, scoef, xi, dyp, opt->pcg_max_iter, pr, cfp));
-    rec.t_pcg_ms += ms_since(tp1);
+    NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[3], ctx->stream));
     if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
     rec.pcg_pred = pr.iters;
     NYS_TRY(AO.At_dx(dyp, rd, xiau, rxz, z, x, d, dxp, dzp));        // dx, dz (A15)
@@ -1046,9 +1049,9 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(AO.Ax(t, xi, nullptr));
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
     NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
-    auto tp2 = std::chrono::steady_clock::now();
+    NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[4], ctx->stream));
     NYS_TRY(pcg_impl(ctx, op, use_chol ? ell : ell_built, U, mp, scoef, xi, dyc, opt->pcg_max_iter, pr, cfp));
-    rec.t_pcg_ms += ms_since(tp2);
+    NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[5], ctx->stream));
     if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
     rec.pcg_corr = pr.iters;
     last_its = (int64_t)rec.pcg_pred + rec.pcg_corr;
@@ -1066,7 +1069,16 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(launch_update_n(ctx, n, x, dx, z, dz));
     if (gen) NYS_TRY(launch_update_n(ctx, n, w, dw, sv, ds));         // w += ap dw ; s += ad ds
     NYS_TRY(launch_update_m(ctx, m, y, dyp, dyc));
-    NYS_TRY(residuals());
+    NYS_TRY(residuals());                                             // synchronises: events complete
+    rec.t_sketch_ms = pev.ms(0, 1);
+    rec.t_pcg_ms = pev.ms(2, 3) + pev.ms(4, 5);
+    t_sketch += rec.t_sketch_ms;
+    if (built_now) {
+      lam_ell_cur = ctx->h_sc[S_LAML];
+      if (ell_cap > ell_k && lam_ell_cur > opt->ell_tau * delta_build)   // F1: grow for the next build
+        ell_k = std::min(2 * ell_k, ell_cap);
+    }
+    rec.lam_ell = use_chol ? 0.0 : lam_ell_cur;
     rec.alpha_p = ctx->h_sc[S_AP];
     rec.alpha_d = ctx->h_sc[S_AD];
     const double mu_new = n_total > 0 ? ctx->h_sc[S_TMP2] / n_total : 0.0;
