@@ -733,6 +733,8 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
   const int64_t npanels = (n + BN - 1) / BN;
   int64_t G = (int64_t)ctx->num_sms * occ;
   if (G > npanels) G = npanels;
+  if (const char* e = getenv("NYS_PCG_GRID")) G = atoi(e);   // tuning override (grid size)
+  if (G > npanels) G = npanels;
   if (G < 1) G = 1;
   PcgPParams P{};
   P.A = A; P.lda = lda; P.m = m; P.n = n; P.d = d; P.e = e; P.U = U; P.ldu = ldu; P.ell = ell; P.s = s;
