@@ -105,3 +105,13 @@ def test_paper_formulation_generators():
     t = pf.b[3:10] - pf.extra["B"][3:10] @ x
     assert np.all(t > 0)
     assert np.allclose(A @ np.concatenate([x, y, t]), pf.b, atol=1e-14)
+
+
+def test_studies_scripts_are_importable():
+    """The f4 / Table 3 study scripts import without a GPU (they only touch CUDA inside main())."""
+    import importlib
+    for name in ("studies.f4_condition", "studies.f4_rank_time", "studies.table3_shapes"):
+        mod = importlib.import_module(name)
+        assert callable(mod.main)
+    from studies.table3_shapes import TABLE3
+    assert set(TABLE3) == {"SensIT", "CIFAR10", "RNASeq", "STL-10", "Arcene"}
