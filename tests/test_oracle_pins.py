@@ -665,3 +665,56 @@ def test_adaptive_rank_follows_the_doubling_rule():
     assert max(ells) == cap                                   # the spike (rank 40) needs > 40
     assert r.inner_total < 0.5 * rf.inner_total
     assert abs(r.obj - rf.obj) <= 1e-6 * abs(rf.obj)
+
+
+def test_general_form_elementwise_pieces_by_hand():
+    """Theta^{-1}, mu and the two-set step length of (P~)/(D~) on a hand-worked 3-variable example
+    (one variable in each of I, F, J; P:1431 elimination)."""
+    from oracle import ippmm_gen
+    vt = np.array([0, 1, 2])
+    x = np.array([2.0, -3.0, 0.5])
+    z = np.array([4.0, 0.0, 1.0])
+    w = np.array([0.0, 0.0, 1.5])
+    s = np.array([0.0, 0.0, 3.0])
+    th = ippmm_gen.theta_inv(x, z, w, s, vt)
+    assert np.allclose(th, [4.0 / 2.0, 0.0, 1.0 / 0.5 + 3.0 / 1.5])
+    # mu = (x_IJ^T z_IJ + w_J^T s_J) / (|IJ| + |J|) = (8 + 0.5 + 4.5) / 3
+    assert abs(ippmm_gen.mu_general(x, z, w, s, vt) - 13.0 / 3.0) < 1e-15
+    # step: x_I blocks at 2/4 = 0.5, x_J at 0.5/1 = 0.5, w_J at 1.5/0.5 = 3; the free x is ignored
+    dx = np.array([-4.0, -100.0, -1.0])
+    dw = np.array([0.0, 0.0, -0.5])
+    assert abs(ippmm_gen.stepsize_general(x, dx, w, dw, vt) - 0.995 * 0.5) < 1e-15
+    dw2 = np.array([0.0, 0.0, -6.0])    # now w blocks first: 1.5 / 6 = 0.25
+    assert abs(ippmm_gen.stepsize_general(x, dx, w, dw2, vt) - 0.995 * 0.25) < 1e-15
+
+
+def test_general_newton_direction_solves_the_linearised_system():
+    """With an exact normal-equation solve, Alg. 4's direction satisfies every block row of the
+    Newton system P:1431 (the 5 x 5 block system in dx, dy, dw, dz, ds) to rounding."""
+    from oracle import ippmm_gen
+    rs = np.random.default_rng(5)
+    m, n = 4, 9
+    vt = np.array([0, 1, 2, 0, 2, 1, 0, 2, 2])
+    I, F, J, IJ = ippmm_gen.masks(vt)
+    A = rs.standard_normal((m, n))
+    q = rs.uniform(0.1, 1.0, n)
+    x = np.where(F, rs.standard_normal(n), rs.uniform(0.2, 1.0, n))
+    z = np.where(F, 0.0, rs.uniform(0.2, 1.0, n))
+    w = np.where(J, rs.uniform(0.2, 1.0, n), 0.0)
+    s = np.where(J, rs.uniform(0.2, 1.0, n), 0.0)
+    rho, delta = 0.3, 0.2
+    d = 1.0 / (q + ippmm_gen.theta_inv(x, z, w, s, vt) + rho)
+    r_d, r_p = rs.standard_normal(n), rs.standard_normal(m)
+    r_u = np.where(J, rs.standard_normal(n), 0.0)
+    r_xz = np.where(IJ, rs.standard_normal(n), 0.0)
+    r_ws = np.where(J, rs.standard_normal(n), 0.0)
+    N = (A * d) @ A.T + delta * np.eye(m)
+    solve = lambda xi: (np.linalg.solve(N, xi), {})  # noqa: E731
+    dx, dy, dz, dw, ds, _ = ippmm_gen.newton_direction_general(A, d, x, z, w, s, vt, r_d, r_p, r_u, r_xz, r_ws, solve)
+    # row 1: -(Q + rho I) dx + A^T dy + dz - ds = r_d   (sign convention of Alg. 4 / reading G0)
+    assert np.allclose(-(q + rho) * dx + A.T @ dy + dz - ds, r_d, atol=1e-10)
+    assert np.allclose(A @ dx + delta * dy, r_p, atol=1e-10)                           # row 2
+    assert np.allclose((dx + dw)[J], r_u[J], atol=1e-12)                                 # row 3
+    assert np.allclose((z * dx + x * dz)[IJ], r_xz[IJ], atol=1e-12)                      # row 4
+    assert np.allclose((s * dw + w * ds)[J], r_ws[J], atol=1e-12)                        # row 5
+    assert np.all(dz[F] == 0) and np.all(dw[~J] == 0) and np.all(ds[~J] == 0)
