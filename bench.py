@@ -254,6 +254,9 @@ def main():
                     help="f3: also rebuild when PCG counts grow by this factor since the last rebuild (0 = off)")
     ap.add_argument("--ell-max", type=int, default=0,
                     help="f3 adaptive rank (reading F1): double ell up to this cap while lam_hat_ell > 10 delta (0 = off)")
+    ap.add_argument("--max-outer", type=int, default=100,
+                    help="cap on IP-PMM outer iterations; below 100 the step is 'max-outer iterations', not "
+                         "time-to-1e-8 (config 4's one-GPU slice is ill-conditioned: DESIGN.md §2, A25)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--matvec-reps", type=int, default=50)
@@ -295,13 +298,14 @@ def main():
         with torch.cuda.stream(stream):
             return ctx.nys_ipppmm_solve(wl.At, lda, m, wl.q, wl.b, wl.c, ell=wl.ell, structure=wl.structure,
                                         prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
-                                        precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max)
+                                        precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max,
+                                        max_outer=args.max_outer)
 
     # ---- warm-up ------------------------------------------------------------------------------
     W = max(args.warmup, 3)
     for _ in range(W):
         g = one_solve()
-    assert g["status"] == 0, f"solve status {g['status']}"
+    assert g["status"] == 0 or (args.max_outer < 100 and g["status"] == -5), f"solve status {g['status']}"
     # ---- timed region: K complete solves, CUDA events on the library's stream ------------------
     barrier()
     launches0 = ctx.kernel_launches
@@ -436,7 +440,8 @@ def main():
             with torch.cuda.stream(stream):  # one untimed e2e solve: workspace for the host path, graphs
                 ctx.nys_ipppmm_solve(A_host, lda, m, qh, bh, ch, ell=wl.ell, host=True, structure=wl.structure,
                                      prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
-                                     precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max)
+                                     precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max,
+                                        max_outer=args.max_outer)
             barrier()
             t0 = time.perf_counter()
             E_STEPS = max(1, min(args.steps, 3))
@@ -444,7 +449,8 @@ def main():
                 with torch.cuda.stream(stream):
                     ctx.nys_ipppmm_solve(A_host, lda, m, qh, bh, ch, ell=wl.ell, host=True, structure=wl.structure,
                                          prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
-                                         precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max)
+                                         precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max,
+                                        max_outer=args.max_outer)
             barrier()
             t_e2e = (time.perf_counter() - t0) / E_STEPS
             if world > 1:
@@ -490,7 +496,8 @@ def main():
             "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl.name, "m": m, "n": wl.n, "ell": wl.ell, "tol": 1e-8,
                        "prec_refresh": args.prec_refresh, "prec_growth": args.prec_growth, "precond": args.precond,
-                       "ell_max": args.ell_max,
+                       "ell_max": args.ell_max, "max_outer": args.max_outer,
+                       "step": "solve to 1e-8" if args.max_outer >= 100 else f"{args.max_outer} outer iterations",
                        "parallelism": f"column-shard x{world}",
                        "l2": ("A = %.0f MB vs 126 MB L2: roofline launches L2-flushed (256 MB read) before each"
                               % (wl.a_bytes() * world / 1e6)) if small else
