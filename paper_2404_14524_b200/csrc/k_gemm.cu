@@ -372,7 +372,12 @@ int launch_gemm(nys_ctx* ctx, const GemmCall& g) {
   if (g.M <= 0 || g.N <= 0) return NYS_OK;
   // the 128-row kernel pays off on tall products (the sketch at large n or m); short-M products
   // (split-K Gram / Y = A T at small m) keep the 64 x 64 kernel (measured on B200)
-  if (g.M < 16384 || g.K < 4096 || getenv("NYS_GEMM_OLD")) return launch_gemm_old(ctx, g);
+  int64_t min_m = 16384, min_k = 4096;   // tuning overrides: NYS_GEMM_NT_MIN="M,K"
+  if (const char* e = getenv("NYS_GEMM_NT_MIN")) {
+    long long a = 0, b = 0;
+    if (sscanf(e, "%lld,%lld", &a, &b) == 2) { min_m = a; min_k = b; }
+  }
+  if (g.M < min_m || g.K < min_k || getenv("NYS_GEMM_OLD")) return launch_gemm_old(ctx, g);
   const int NT = pick_nt(g.N);
   const int BN = 8 * NT;
   const size_t smem = (size_t)HST * (HA_STAGE + BN * HLD_K) * sizeof(double);
