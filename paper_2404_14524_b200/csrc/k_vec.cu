@@ -117,7 +117,10 @@ __global__ void __launch_bounds__(256) dots_kernel(const DotArgs D) {
 }
 
 static int reduce_grid(nys_ctx* ctx, int64_t n) {
-  int g = (int)((n + 1023) / 1024);
+  // one 256-row tile per block while that stays under two blocks per SM (the reductions are
+  // latency-bound at the IPM's n: more blocks in flight, one element per thread)
+  int g = (int)((n + 255) / 256);
+  if (const char* e = getenv("NYS_REDUCE_ROWS")) g = (int)((n + atoi(e) - 1) / atoi(e));
   if (g < 1) g = 1;
   if (g > 2 * ctx->num_sms) g = 2 * ctx->num_sms;
   return g;
