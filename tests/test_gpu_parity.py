@@ -543,3 +543,26 @@ def test_adaptive_rank_matches_oracle(ctx):
     assert max(r["ell"] for r in g["log"]) == 80
     assert obj_agree(g, ref, inst=inst)
     assert abs(g["outer"] - ref.outer) <= 2
+
+
+@pytest.mark.parametrize("m,n", [(1, 3), (5, 3), (3, 3), (2, 1)])
+def test_ipppmm_degenerate_shapes(ctx, m, n):
+    """Degenerate shapes: one constraint, more constraints than variables (A A^T singular: the
+    proximal delta keeps N_delta positive definite), square A, a single variable."""
+    from paper_2404_14524_b200 import colmajor_device
+    rs = np.random.default_rng(m * 10 + n)
+    A = rs.standard_normal((m, n))
+    x0 = rs.uniform(0.5, 1.5, n)
+    q = rs.uniform(0.0, 1.0, n)
+    b = A @ x0
+    y0 = rs.standard_normal(m)
+    z0 = rs.uniform(0.5, 1.5, n)
+    c = A.T @ y0 + z0 - q * x0
+    ell = min(m, 2)
+    ref = ippmm.solve(A, q, b, c, ippmm.Options(path="krylov", ell=ell))
+    Ad, lda = colmajor_device(A)
+    g = ctx.nys_ipppmm_solve(Ad, lda, m, dev(q), dev(b), dev(c), ell=ell)
+    assert ref.status == "optimal" and g["status"] == 0
+    x = g["x"].cpu().numpy()
+    assert np.linalg.norm(b - A @ x) / (1 + np.linalg.norm(b)) <= 1.01e-8
+    assert abs(g["obj"] - ref.obj) <= 1e-6 * max(1.0, abs(ref.obj))
