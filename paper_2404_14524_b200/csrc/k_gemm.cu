@@ -368,8 +368,25 @@ __global__ void gemm_reduce_kernel(int64_t M, int64_t N, int splits, const doubl
 
 static int launch_gemm_old(nys_ctx* ctx, const GemmCall& g);
 
+// K = 0 (a rank with no columns): C = the epilogue's additive term only (addv o addm, else 0)
+__global__ void gemm_k0_kernel(int64_t M, int64_t N, double* C, int64_t ldc, const double* addv, const double* addm,
+                               int64_t ldadd) {
+  const int64_t total = M * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e % M, col = e / M;
+    C[row + col * ldc] = addv ? addv[row] * addm[row + col * ldadd] : 0.0;
+  }
+}
+
 int launch_gemm(nys_ctx* ctx, const GemmCall& g) {
   if (g.M <= 0 || g.N <= 0) return NYS_OK;
+  if (g.K <= 0) {
+    int64_t blocks = (g.M * g.N + 255) / 256;
+    if (blocks > 4 * ctx->num_sms) blocks = 4 * ctx->num_sms;
+    gemm_k0_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(g.M, g.N, g.C, g.ldc, g.addv, g.addm, g.ldadd);
+    ctx->launches++;
+    return ctx->check_launch("gemm_k0");
+  }
   // the 128-row kernel pays off on tall products (the sketch at large n or m); short-M products
   // (split-K Gram / Y = A T at small m) keep the 64 x 64 kernel (measured on B200)
   int64_t min_m = 16384, min_k = 4096;   // tuning overrides: NYS_GEMM_NT_MIN="M,K"

@@ -866,6 +866,15 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, 
   return NYS_OK;
 }
 
+// a rank with no columns still forms the PCG direction p = z + beta p (replicated m-space state)
+__global__ void empty_shard_prologue_kernel(int64_t m, const double* z, const double* p, const double* beta,
+                                            double* p_out, const double* done) {
+  if (done != nullptr && *done != 0.0) return;
+  const double b = (beta != nullptr) ? *beta : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    p_out[i] = (p != nullptr) ? z[i] + b * p[i] : z[i];
+}
+
 int ensure_max_smem(nys_ctx* ctx, const void* fn, size_t bytes) {
   static std::map<std::pair<int, const void*>, size_t> set;
   static std::mutex mu;
@@ -950,8 +959,15 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
     }
   }
   if (c.mode == MV_TONLY) return NYS_OK;
-  if (c.n <= 0) {  // empty shard: zero partial
+  if (c.n <= 0) {  // empty shard: zero partials, and the operand prologue the kernel would have done
     NYS_CUDA_TRY(ctx, cudaMemsetAsync(Wp, 0, sizeof(double) * (size_t)pl.nparts * wp_ld, ctx->stream));
+    if (pwp) NYS_CUDA_TRY(ctx, cudaMemsetAsync(pwp, 0, sizeof(double) * (size_t)pl.grid, ctx->stream));
+    if (c.mode == MV_FUSED && c.p_out != nullptr) {   // v = z + beta p is still this rank's p (PCG)
+      empty_shard_prologue_kernel<<<(unsigned)((c.m + 255) / 256), 256, 0, ctx->stream>>>(c.m, c.z, c.p, c.beta,
+                                                                                          c.p_out, c.done);
+      ctx->launches++;
+      NYS_TRY(ctx->check_launch("empty_shard_prologue"));
+    }
   }
   if (c.pcg_fused) {  // the PCG update kernel consumes the partials directly (no finalize)
     if (c.fused_out) {

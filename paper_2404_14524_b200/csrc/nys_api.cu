@@ -100,19 +100,33 @@ struct LoopComm {
   std::condition_variable cv;
   int arrived = 0;
   uint64_t gen = 0;
+  bool aborted = false;   // a rank's call failed: its peers leave their collectives with an error
   std::vector<double*> bufs;
-  void barrier() {
+  bool barrier() {
     std::unique_lock<std::mutex> lk(mu);
+    if (aborted) return false;
     const uint64_t g = gen;
     if (++arrived == world) {
       arrived = 0;
       ++gen;
       cv.notify_all();
     } else {
-      cv.wait(lk, [&] { return gen != g; });
+      cv.wait(lk, [&] { return gen != g || aborted; });
     }
+    return !aborted;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
   }
 };
+// a failed collective call on one loopback rank must not leave its peers waiting forever
+int loop_abort_on_error(nys_ctx* ctx, int rc) {
+  if (rc != NYS_OK && rc != NYS_EMAXITER && rc != NYS_NOTCONV && ctx && ctx->loop_comm)
+    static_cast<LoopComm*>(ctx->loop_comm)->abort();
+  return rc;
+}
 
 struct RankPtrs {
   const double* p[16];
@@ -129,7 +143,7 @@ int loop_allreduce(nys_ctx* ctx, double* buf, size_t count, bool is_min) {
   LoopComm* c = (LoopComm*)ctx->loop_comm;
   NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   c->bufs[ctx->rank] = buf;
-  c->barrier();  // every rank's buffer is final
+  if (!c->barrier()) { ctx->set_error("loopback all-reduce: a peer rank failed"); return NYS_ECUDA; }  // buffers final
   double* tmp = ctx->wsd("loop_tmp", count);
   RankPtrs R{};
   for (int r = 0; r < c->world; ++r) R.p[r] = c->bufs[r];
@@ -138,7 +152,7 @@ int loop_allreduce(nys_ctx* ctx, double* buf, size_t count, bool is_min) {
   loop_reduce_kernel<<<g, 256, 0, ctx->stream>>>(R, c->world, count, is_min ? 1 : 0, tmp);
   NYS_CUDA_TRY(ctx, cudaGetLastError());
   NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  c->barrier();  // every rank has read every buffer
+  if (!c->barrier()) { ctx->set_error("loopback all-reduce: a peer rank failed"); return NYS_ECUDA; }  // all read
   NYS_CUDA_TRY(ctx, cudaMemcpyAsync(buf, tmp, count * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   return NYS_OK;
 }
@@ -1331,8 +1345,8 @@ static int check_A(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t 
   return NYS_OK;
 }
 
-int nys_normal_matvec(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
-                      const double* e, double delta, const double* v, double* w) {
+static int nys_normal_matvec_body(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                             const double* e, double delta, const double* v, double* w) {
   NYS_GUARD_BEGIN
   NYS_TRY(check_A(ctx, m, n, A, lda));
   if (!v || !w || (n > 0 && !d) || delta < 0 || v == w) { ctx->set_error("bad vector arguments"); return NYS_EINVAL; }
@@ -1341,6 +1355,12 @@ int nys_normal_matvec(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64
   NYS_TRY(apply_normal_full(ctx, op, v, nullptr, nullptr, nullptr, w, false, nullptr));
   return NYS_OK;
   NYS_GUARD_END
+}
+
+// a failing call on one loopback rank releases its peers (LoopComm::abort)
+int nys_normal_matvec(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                      const double* e, double delta, const double* v, double* w) {
+  return loop_abort_on_error(ctx, nys_normal_matvec_body(ctx, m, n, A, lda, d, e, delta, v, w));
 }
 
 int nys_check_scaling(nys_ctx* ctx, int64_t n, const double* d, int64_t* bad_index) {
@@ -1370,8 +1390,8 @@ int nys_gaussian(nys_ctx* ctx, int64_t m, int ell, uint64_t seed, uint64_t strea
   NYS_GUARD_END
 }
 
-int nys_sketch(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
-               double delta, int ell, const double* Omega, double* U, double* lambda, nys_sketch_info* info) {
+static int nys_sketch_body(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
+                      double delta, int ell, const double* Omega, double* U, double* lambda, nys_sketch_info* info) {
   NYS_GUARD_BEGIN
   NYS_TRY(check_A(ctx, m, n, A, lda));
   if (ell < 1 || ell > m || ell > 256 || !(delta > 0) || !Omega || !U || !lambda || (n > 0 && !d)) {
@@ -1403,8 +1423,14 @@ int nys_sketch(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda,
   NYS_GUARD_END
 }
 
-int nys_sketch_apply(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
-                     const double* e, int ell, const double* Omega, double* Y) {
+// a failing call on one loopback rank releases its peers (LoopComm::abort)
+int nys_sketch(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
+               double delta, int ell, const double* Omega, double* U, double* lambda, nys_sketch_info* info) {
+  return loop_abort_on_error(ctx, nys_sketch_body(ctx, m, n, A, lda, d, e, delta, ell, Omega, U, lambda, info));
+}
+
+static int nys_sketch_apply_body(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                            const double* e, int ell, const double* Omega, double* Y) {
   NYS_GUARD_BEGIN
   NYS_TRY(check_A(ctx, m, n, A, lda));
   if (ell < 1 || !Omega || !Y || (n > 0 && !d)) { ctx->set_error("nys_sketch_apply: bad arguments"); return NYS_EINVAL; }
@@ -1425,8 +1451,14 @@ int nys_sketch_apply(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_
   NYS_GUARD_END
 }
 
-int nys_partial_cholesky(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
-                         const double* e, double delta, int ell, int64_t* piv, double* L, double* dS) {
+// a failing call on one loopback rank releases its peers (LoopComm::abort)
+int nys_sketch_apply(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                     const double* e, int ell, const double* Omega, double* Y) {
+  return loop_abort_on_error(ctx, nys_sketch_apply_body(ctx, m, n, A, lda, d, e, ell, Omega, Y));
+}
+
+static int nys_partial_cholesky_body(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                                const double* e, double delta, int ell, int64_t* piv, double* L, double* dS) {
   NYS_GUARD_BEGIN
   NYS_TRY(check_A(ctx, m, n, A, lda));
   if (ell < 0 || ell > m || ell > 256 || !(delta > 0) || (n > 0 && !d)) {
@@ -1450,6 +1482,12 @@ int nys_partial_cholesky(nys_ctx* ctx, int64_t m, int64_t n, const double* A, in
   NYS_GUARD_END
 }
 
+// a failing call on one loopback rank releases its peers (LoopComm::abort)
+int nys_partial_cholesky(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                         const double* e, double delta, int ell, int64_t* piv, double* L, double* dS) {
+  return loop_abort_on_error(ctx, nys_partial_cholesky_body(ctx, m, n, A, lda, d, e, delta, ell, piv, L, dS));
+}
+
 int nys_chol_precond_apply(nys_ctx* ctx, int64_t m, const double* v, double* out) {
   NYS_GUARD_BEGIN
   if (!ctx || !v || !out) return NYS_EINVAL;
@@ -1469,9 +1507,9 @@ int nys_chol_precond_apply(nys_ctx* ctx, int64_t m, const double* v, double* out
   NYS_GUARD_END
 }
 
-int nys_pcg_solve(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
-                  double delta, int ell, const double* U, const double* lambda, double mu_prec, const double* rhs,
-                  double* x, double tol_abs, int max_iter, nys_pcg_info* info) {
+static int nys_pcg_solve_body(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
+                         double delta, int ell, const double* U, const double* lambda, double mu_prec, const double* rhs,
+                         double* x, double tol_abs, int max_iter, nys_pcg_info* info) {
   NYS_GUARD_BEGIN
   NYS_TRY(check_A(ctx, m, n, A, lda));
   if (ell < 0 || ell > m || ell > 256 || (ell > 0 && (!U || !lambda)) || !rhs || !x || max_iter < 0 || delta < 0 ||
@@ -1521,7 +1559,14 @@ int nys_pcg_solve(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t l
   NYS_GUARD_END
 }
 
-int nys_ipppmm_solve(nys_ctx* ctx, const nys_qp* qp, const nys_options* opt, nys_solution* sol, nys_report* rep) {
+// a failing call on one loopback rank releases its peers (LoopComm::abort)
+int nys_pcg_solve(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
+                  double delta, int ell, const double* U, const double* lambda, double mu_prec, const double* rhs,
+                  double* x, double tol_abs, int max_iter, nys_pcg_info* info) {
+  return loop_abort_on_error(ctx, nys_pcg_solve_body(ctx, m, n, A, lda, d, e, delta, ell, U, lambda, mu_prec, rhs, x, tol_abs, max_iter, info));
+}
+
+static int nys_ipppmm_solve_body(nys_ctx* ctx, const nys_qp* qp, const nys_options* opt, nys_solution* sol, nys_report* rep) {
   NYS_GUARD_BEGIN
   if (!ctx || !qp || !opt) return NYS_EINVAL;
   if (qp->m < 1 || qp->n < 0 || qp->lda < qp->m || !qp->b || (qp->n > 0 && (!qp->A || !qp->q || !qp->c))) {
@@ -1559,6 +1604,11 @@ int nys_ipppmm_solve(nys_ctx* ctx, const nys_qp* qp, const nys_options* opt, nys
   cudaSetDevice(ctx->device);
   return ipm_impl(ctx, qp, opt, sol, rep);
   NYS_GUARD_END
+}
+
+// a failing call on one loopback rank releases its peers (LoopComm::abort)
+int nys_ipppmm_solve(nys_ctx* ctx, const nys_qp* qp, const nys_options* opt, nys_solution* sol, nys_report* rep) {
+  return loop_abort_on_error(ctx, nys_ipppmm_solve_body(ctx, qp, opt, sol, rep));
 }
 
 }  // extern "C"

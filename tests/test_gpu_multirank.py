@@ -168,3 +168,65 @@ def test_multirank_chol_ipppmm_matches_oracle():
     tol = max(1e-7 * max(1.0, abs(ref.obj)),
               band(res[0]["obj"], res[0]["dual_obj"], x, y, z) + band(ref.obj, ref.dual_obj, ref.x, ref.y, ref.z))
     assert abs(res[0]["obj"] - ref.obj) <= tol
+
+
+def test_multirank_rank_without_columns():
+    """A rank whose column shard is empty (world 3, n = 2): its contributions are zero partials and
+    it still takes part in every all-reduce (SURVEY §8(e) column sharding)."""
+    rs = np.random.default_rng(4)
+    m, n, world = 3, 2, 3
+    A = rs.standard_normal((m, n))
+    x0 = rs.uniform(0.5, 1.5, n)
+    q = rs.uniform(0.1, 1.0, n)
+    b = A @ x0
+    c = A.T @ rs.standard_normal(m) + rs.uniform(0.5, 1.5, n) - q * x0
+    from paper_2404_14524_b200 import colmajor_device
+    bounds = [(0, 1), (1, 2), (2, 2)]
+    data = []
+    for lo, hi in bounds:
+        if hi > lo:
+            Ad, lda = colmajor_device(np.asfortranarray(A[:, lo:hi]))
+        else:
+            Ad, lda = torch.zeros((0, 32), dtype=torch.float64, device="cuda"), 32
+        data.append((lo, hi, Ad, lda))
+    torch.cuda.synchronize()
+
+    def fn(ctx, r, st):
+        lo, hi, Ad, lda = data[r]
+        g = ctx.nys_ipppmm_solve(Ad, lda, m, dev(q[lo:hi]) if hi > lo else torch.zeros(0, dtype=torch.float64, device="cuda"),
+                                 dev(b), dev(c[lo:hi]) if hi > lo else torch.zeros(0, dtype=torch.float64, device="cuda"),
+                                 ell=1)
+        st.synchronize()
+        return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in g.items() if k != "log"}
+
+    res = _run_ranks(world, fn)
+    ref = ippmm.solve(A, q, b, c, ippmm.Options(path="krylov", ell=1))
+    for g in res:
+        assert g["status"] == 0
+    assert res[2]["x"].size == 0
+    x = np.concatenate([g["x"] for g in res])
+    assert np.linalg.norm(b - A @ x) / (1 + np.linalg.norm(b)) <= 1.01e-8
+    assert abs(res[0]["obj"] - ref.obj) <= 1e-6 * max(1.0, abs(ref.obj))
+
+
+def test_multirank_failing_rank_releases_its_peers():
+    """One loopback rank fails argument validation: its peers leave their collectives with an error
+    instead of waiting forever (LoopComm::abort)."""
+    from paper_2404_14524_b200 import NysError
+    inst = make_config(1, m=120, n=360, ell=8)
+    m = inst.m
+    sh = _shards(inst.A, 2)
+    torch.cuda.synchronize()
+
+    def fn(ctx, r, st):
+        lo, hi, Ad, lda = sh[r]
+        try:
+            ctx.nys_ipppmm_solve(Ad, lda if r == 0 else lda + 1, m, dev(inst.q[lo:hi]), dev(inst.b),  # rank 1: odd lda
+                                 dev(inst.c[lo:hi]), ell=inst.ell)
+            return "ok"
+        except NysError as ex:
+            return str(ex)
+
+    res = _run_ranks(2, fn)
+    assert all(r != "ok" for r in res)
+    assert "peer rank failed" in res[0]
