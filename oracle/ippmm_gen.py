@@ -17,6 +17,9 @@ Readings where the paper is silent:
      (1 + ||c||), mu (P:888 general) <= tol; the PEU "primal improved" test uses the same primal norm.
   G2 initial point: the delta~_d denominator read as sum(x~_IJ + delta_p) + sum(w~_J + delta_p) (A13).
   G3 the initial-point systems use (A A^T + 10 I) as in App. B.2; x~_F is not shifted.
+  G5 with no inequality at all (every variable free) the duality measure and the corrector's target
+     are 0 (the sums in P:882 / P:888 are empty): the iteration is the proximal method of multipliers
+     on the equality-constrained QP.
 """
 from __future__ import annotations
 
@@ -95,8 +98,8 @@ def initial_point_general(A, q, b, c, vtype, u, solve_aat):
     wt = np.where(J, uu - xt, 0.0)
     cand_p = [xt[IJ]] + ([wt[J]] if J.any() else [])
     cand_d = [zt[IJ]] + ([st[J]] if J.any() else [])
-    dp = max(max(-1.5 * float(np.min(v)) for v in cand_p if v.size), 0.0)      # P:1468 general
-    dd = max(max(-1.5 * float(np.min(v)) for v in cand_d if v.size), 0.0)
+    dp = max([-1.5 * float(np.min(v)) for v in cand_p if v.size] + [0.0])      # P:1468 general (G5: none)
+    dd = max([-1.5 * float(np.min(v)) for v in cand_d if v.size] + [0.0])
     gxz = float((xt[IJ] + dp) @ (zt[IJ] + dd))
     gws = float((wt[J] + dp) @ (st[J] + dd))
     den_p = float(np.sum(zt[IJ] + dd) + np.sum(st[J] + dd))
@@ -178,9 +181,12 @@ def solve_general(A, q, b, c, vtype, u, opts: Options = Options()) -> Result:
         ap = stepsize_general(x, dxp, w, dwp, vtype)
         ad = stepsize_general(z, dzp, s, dsp, vtype)
         den = int(IJ.sum() + J.sum())
-        mu_aff = float((x[IJ] + ap * dxp[IJ]) @ (z[IJ] + ad * dzp[IJ]) +
-                       (w[J] + ap * dwp[J]) @ (s[J] + ad * dsp[J])) / den                  # eq. P:882
-        mu_t = mu_aff ** 3 / mu ** 2
+        if den == 0:             # G5: no inequality (all variables free): mu = mu_aff = mu~ = 0
+            mu_aff = mu_t = 0.0
+        else:
+            mu_aff = float((x[IJ] + ap * dxp[IJ]) @ (z[IJ] + ad * dzp[IJ]) +
+                           (w[J] + ap * dwp[J]) @ (s[J] + ad * dsp[J])) / den              # eq. P:882
+            mu_t = mu_aff ** 3 / mu ** 2
         # corrector (eq. P:894-897)
         zn, zm = np.zeros(n), np.zeros(m)
         r_xz_c = np.where(IJ, mu_t - dxp * dzp, 0.0)
@@ -194,7 +200,8 @@ def solve_general(A, q, b, c, vtype, u, opts: Options = Options()) -> Result:
         y, z, s = y + ad * dy, z + ad * dz, s + ad * ds
         mu_new = mu_general(x, z, w, s, vtype)
         nrP, nrD = residuals(x, y, z, w, s)
-        r = min(max(1.0 - mu_new / mu, 0.0), 1.0) if mu > 0 else 0.0
+        # G5: mu = 0 (no inequality) -> the reduction is complete, r = 1
+        r = min(max(1.0 - mu_new / mu, 0.0), 1.0) if mu > 0 else (1.0 if den == 0 else 0.0)
         p_imp, d_imp = nrP <= 0.95 * nrP_ref, nrD <= 0.95 * nrD_ref
         if p_imp:
             lam_est, nrP_ref = y.copy(), nrP

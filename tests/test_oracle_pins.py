@@ -718,3 +718,24 @@ def test_general_newton_direction_solves_the_linearised_system():
     assert np.allclose((z * dx + x * dz)[IJ], r_xz[IJ], atol=1e-12)                      # row 4
     assert np.allclose((s * dw + w * ds)[J], r_ws[J], atol=1e-12)                        # row 5
     assert np.all(dz[F] == 0) and np.all(dw[~J] == 0) and np.all(ds[~J] == 0)
+
+
+def test_general_form_all_free_is_the_kkt_solution():
+    """Every variable free (reading G5): min 1/2 x^T Q x + c^T x s.t. A x = b has the closed-form KKT
+    solution [Q A^T; A 0] [x; -y] = [-c; b]; the general-form solve reaches it (both paths)."""
+    from oracle import ippmm_gen
+    rs = np.random.default_rng(9)
+    m, n = 3, 7
+    A = rs.standard_normal((m, n))
+    q = rs.uniform(0.5, 2.0, n)
+    b = rs.standard_normal(m)
+    c = rs.standard_normal(n)
+    K = np.block([[np.diag(q), A.T], [A, np.zeros((m, m))]])
+    sol = np.linalg.solve(K, np.concatenate([-c, b]))
+    x_kkt, y_kkt = sol[:n], -sol[n:]
+    vt = np.ones(n, dtype=int)
+    for path in ("direct", "krylov"):
+        r = ippmm_gen.solve_general(A, q, b, c, vt, np.zeros(n), ippmm.Options(path=path, ell=2))
+        assert r.status == "optimal"
+        assert np.abs(r.x - x_kkt).max() <= 1e-7 and np.abs(r.y - y_kkt).max() <= 1e-7
+        assert np.all(r.z == 0)
