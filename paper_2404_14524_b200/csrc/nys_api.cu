@@ -1099,7 +1099,8 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     nrP = std::sqrt(ctx->h_sc[S_TMP0]);
     nrD = std::sqrt(ctx->h_sc[S_TMP1]);
     // ---- PEU (A12) ----
-    double r = (mu > 0) ? std::min(std::max(1.0 - mu_new / mu, 0.0), 1.0) : 0.0;
+    // G5: no inequality at all (every variable free): mu = 0 and the reduction is complete (r = 1)
+    double r = (mu > 0) ? std::min(std::max(1.0 - mu_new / mu, 0.0), 1.0) : (n_total > 0 ? 0.0 : 1.0);
     const bool p_imp = nrP <= 0.95 * nrP_ref;
     const bool d_imp = nrD <= 0.95 * nrD_ref;
     if (p_imp) {

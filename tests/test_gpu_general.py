@@ -191,3 +191,26 @@ def test_general_multirank_loopback():
               band_general(inst, ref.x, ref.y, ref.z, ref.s, ref.obj, ref.dual_obj))
     assert abs(res[0]["obj"] - ref.obj) <= tol
     assert abs(res[0]["outer"] - ref.outer) <= 2
+
+
+def test_general_all_free_is_the_kkt_solution():
+    """Reading G5 on the GPU: every variable free -> the equality-constrained QP's KKT solution."""
+    rs = np.random.default_rng(9)
+    m, n = 30, 70
+    A = rs.standard_normal((m, n))
+    q = rs.uniform(0.5, 2.0, n)
+    b = rs.standard_normal(m)
+    c = rs.standard_normal(n)
+    K = np.block([[np.diag(q), A.T], [A, np.zeros((m, m))]])
+    sol = np.linalg.solve(K, np.concatenate([-c, b]))
+    x_kkt, y_kkt = sol[:n], -sol[n:]
+    from paper_2404_14524_b200 import colmajor_device
+    ctx = _ctx()
+    Ad, lda = colmajor_device(A)
+    g = ctx.nys_ipppmm_solve(Ad, lda, m, dev(q), dev(b), dev(c), ell=8,
+                             vtype=torch.ones(n, dtype=torch.int8, device="cuda"), ub=dev(np.zeros(n)))
+    torch.cuda.synchronize()
+    assert g["status"] == 0
+    assert np.abs(_h(g["x"]) - x_kkt).max() <= 1e-7 and np.abs(_h(g["y"]) - y_kkt).max() <= 1e-7
+    assert np.all(_h(g["z"]) == 0)
+    ctx.close()
