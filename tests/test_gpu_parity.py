@@ -566,3 +566,26 @@ def test_ipppmm_degenerate_shapes(ctx, m, n):
     x = g["x"].cpu().numpy()
     assert np.linalg.norm(b - A @ x) / (1 + np.linalg.norm(b)) <= 1.01e-8
     assert abs(g["obj"] - ref.obj) <= 1e-6 * max(1.0, abs(ref.obj))
+
+
+@pytest.mark.parametrize("lda_multiple", [2, 128, 512])
+def test_pcg_leading_dimension_layouts(ctx, lda_multiple):
+    """The persistent PCG's two staging layouts: a near-tight lda (one bulk copy per panel) and a
+    padded lda (one copy per column) give the same iterates as the oracle."""
+    from paper_2404_14524_b200 import colmajor_device
+    inst = make_config(1, m=700, n=2400, ell=20)
+    A, m, n, ell = inst.A, inst.m, inst.n, inst.ell
+    rs = np.random.default_rng(11)
+    d = linops.scaling_d(inst.q, rs.uniform(0.01, 2.0, n), rs.uniform(0.01, 2.0, n), 1e-2)
+    delta, iters = 1e-3, 12
+    rhs = rs.standard_normal(m)
+    Om = orng.gaussian_omega(m, ell, 0, 1)
+    Uo, lamo, _ = nystrom.nystrom_from_sketch(linops.sketch(A, d, Om), Om)
+    pinv = lambda v: nystrom.precond_inv_apply(Uo, lamo, delta, v)  # noqa: E731
+    xo, _ = oracle_pcg(lambda v: linops.normal_matvec(A, d, v, delta), rhs, pinv, tol_abs=0.0, max_iter=iters)
+    Ad, lda = colmajor_device(A, lda_multiple=lda_multiple)
+    xg = torch.empty(m, dtype=torch.float64, device="cuda")
+    info = ctx.nys_pcg_solve(Ad, lda, m, dev(d), None, delta, ell, dev_cm(Uo), dev(lamo), delta, dev(rhs), xg, 0.0,
+                             iters)
+    assert info.iters == iters
+    assert rel(xg.cpu().numpy(), xo) <= 1e-9
