@@ -214,3 +214,26 @@ def test_general_all_free_is_the_kkt_solution():
     assert np.abs(_h(g["x"]) - x_kkt).max() <= 1e-7 and np.abs(_h(g["y"]) - y_kkt).max() <= 1e-7
     assert np.all(_h(g["z"]) == 0)
     ctx.close()
+
+
+@pytest.mark.parametrize("kw", [dict(prec_refresh=3), dict(ell_max=64), dict(precond=1)])
+def test_general_form_with_reuse_adaptive_and_chol(kw):
+    """f1 combined with f3 (reuse, adaptive rank) and f2 (partial Cholesky): the same optimum (KKT of
+    (P~)/(D~) at 1e-8 and the objective within the certified bands of the plain solve)."""
+    inst = make_general(150, 600, 0.2, 0.3, ell=16, seed=14)
+    vt, u = inst.extra["vtype"], inst.extra["ub"]
+    J = vt == 2
+    ctx = _ctx()
+    g0 = _solve(ctx, inst)
+    g = _solve(ctx, inst, **kw)
+    torch.cuda.synchronize()
+    assert g0["status"] == 0 and g["status"] == 0
+    x, y, z, w, s = (_h(g[k]) for k in ("x", "y", "z", "w", "s"))
+    bn = np.sqrt(inst.b @ inst.b + u[J] @ u[J])
+    rP = np.concatenate([inst.b - inst.A @ x, (u - x - w)[J]])
+    assert np.linalg.norm(rP) / (1 + bn) <= 1.01e-8
+    assert np.linalg.norm(inst.c + inst.q * x - inst.A.T @ y - z + s) / (1 + np.linalg.norm(inst.c)) <= 1.01e-8
+    tol = band_general(inst, x, y, z, s, g["obj"], g["dual_obj"]) + \
+        band_general(inst, _h(g0["x"]), _h(g0["y"]), _h(g0["z"]), _h(g0["s"]), g0["obj"], g0["dual_obj"])
+    assert abs(g["obj"] - g0["obj"]) <= max(tol, 1e-9 * abs(g0["obj"]))
+    ctx.close()
