@@ -230,3 +230,24 @@ def test_multirank_failing_rank_releases_its_peers():
     res = _run_ranks(2, fn)
     assert all(r != "ok" for r in res)
     assert "peer rank failed" in res[0]
+
+
+def test_multirank_adaptive_rank_and_reuse_agree():
+    """f3 decisions (adaptive rank, reuse) are taken from replicated values: identical on every rank."""
+    inst = make_config(1, m=200, n=800, ell=10)
+    m = inst.m
+    sh = _shards(inst.A, 2)
+    torch.cuda.synchronize()
+
+    def fn(ctx, r, st):
+        lo, hi, Ad, lda = sh[r]
+        g = ctx.nys_ipppmm_solve(Ad, lda, m, dev(inst.q[lo:hi]), dev(inst.b), dev(inst.c[lo:hi]), ell=inst.ell,
+                                 ell_max=80, prec_refresh=2)
+        st.synchronize()
+        return {"status": g["status"], "y": g["y"].cpu().numpy(), "ells": [rec["ell"] for rec in g["log"]],
+                "built": [rec["prec_built"] for rec in g["log"]], "inner": g["inner"]}
+
+    res = _run_ranks(2, fn)
+    assert res[0]["status"] == 0 and res[1]["status"] == 0
+    assert res[0]["ells"] == res[1]["ells"] and res[0]["built"] == res[1]["built"]
+    assert max(res[0]["ells"]) > 10 and np.array_equal(res[0]["y"], res[1]["y"])
