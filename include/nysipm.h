@@ -203,7 +203,9 @@ typedef struct {
    * §8(f) f1).  vtype == NULL: every variable is in I (x >= 0), the form (P)/(D).  Otherwise
    * vtype[j] (n local entries, int8) is 0 for j in I (x_j >= 0), 1 for j in F (free), 2 for j in J
    * (0 <= x_j <= ub[j]); ub (n local doubles) is read on J only and may be NULL when no entry is 2.
-   * Same memory space as A (host_ptrs).  Works with every `structure`.                         */
+   * Same memory space as A (host_ptrs).  Works with every `structure`.  With every variable free
+   * the duality measure is identically 0 and the method reduces to the proximal method of
+   * multipliers on the equality-constrained QP (reading G5).                          */
   const int8_t* vtype;
   const double* ub;
   /* structure 2: A = [B, S_0, ..., S_{K-1}] with the dense block B (m x nd, column-major, lda) in
