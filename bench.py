@@ -35,7 +35,7 @@ METRIC = "fp64 A·D·Aᵀv matvec GB/s (% HBM peak) and Nys-IP-PMM time-to-1e-8 
 TRAFFIC = {1: 134.6e6}
 # persistent PCG kernel, dram__bytes_read.sum + dram__bytes_write.sum per ITERATION (ncu --set full of
 # a 20-iteration launch, config 1: 2.535 GB + 20.9 MB; profiles/r01_pcg_persistent_cfg1_20it_full.ncu-rep)
-PCG_TRAFFIC_PER_IT = {1: 126.7e6}   # ncu --set full, profiles/r01_pcg_persistent_cfg1_20it_s6_full.ncu-rep
+PCG_TRAFFIC_PER_IT = {1: 85.6e6}   # ncu --set full, profiles/r01_pcg_persistent_cfg1_20it_final_full.ncu-rep
 
 
 def _peaks():
