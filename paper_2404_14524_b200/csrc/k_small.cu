@@ -279,10 +279,92 @@ __global__ void __launch_bounds__(1024) chol_inv_packed_kernel(int ell, double* 
   }
 }
 
+// Same contract for ell <= 64 (the paper's ranks up to 50 and CholeskyQR3 passes at them) with one
+// block barrier per elimination step instead of two: the lane that updates row k+1 of a trailing
+// column also publishes it into a double-buffered row, which is step k+1's pivot row.  R^{-1} is then
+// formed one column per warp with no block barrier at all: x = e_j; for i = j..0:
+// x_i /= R_ii, x_{0:i} -= R_{0:i,i} x_i (x held two elements per lane, x_i broadcast by a shuffle).
+__global__ void __launch_bounds__(1024) chol_inv_small_kernel(int ell, double* G, int ldg, double* Rinv, int ldr,
+                                                             int shift_mode, double* sc) {
+  __shared__ double W[64 * 64];
+  __shared__ double rowb[2][64];
+  __shared__ double rsq[64];
+  __shared__ double shift;
+  const int n = ell, tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31, nw = blockDim.x >> 5;
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    W[i + j * n] = 0.5 * (G[i + (size_t)j * ldg] + G[j + (size_t)i * ldg]);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    if (shift_mode == 1) {
+      double tr = 0.0;
+      for (int i = 0; i < n; ++i) tr += W[i + i * n];
+      s = 11.0 * (sc[S_SHIFT] * n + (double)n * (n + 1)) * 0x1p-53 * tr;
+    }
+    shift = s;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) W[i + i * n] += shift;
+  __syncthreads();
+  for (int j = tid; j < n; j += blockDim.x) rowb[0][j] = W[j * n];
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {  // right-looking, unscaled row k (as chol_inv_kernel)
+    const double* rk = rowb[k & 1];
+    double* rn = rowb[(k + 1) & 1];
+    const double piv = rk[k];
+    if (!(piv > 0.0) || !isfinite(piv)) {  // uniform
+      if (tid == 0) sc[S_CHOLFAIL] = 1.0;
+      return;
+    }
+    const double inv = 1.0 / piv;
+    for (int j = k + 1 + warp; j < n; j += nw) {
+      const double akj = rk[j] * inv;
+      for (int i = k + 1 + lane; i <= j; i += 32) {
+        const double v = fma(-rk[i], akj, W[i + j * n]);
+        W[i + j * n] = v;
+        if (i == k + 1) rn[j] = v;
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += blockDim.x) rsq[i] = 1.0 / sqrt(W[i + i * n]);
+  __syncthreads();
+  for (int e = tid; e < n * n; e += blockDim.x) {  // R = diag(rsq) W (upper), out to G
+    const int i = e % n, j = e / n;
+    const double r = (i <= j) ? W[e] * rsq[i] : 0.0;
+    W[e] = r;
+    G[i + (size_t)j * ldg] = r;
+  }
+  __syncthreads();
+  for (int j = warp; j < n; j += nw) {
+    double x0 = (lane == j) ? 1.0 : 0.0, x1 = (lane + 32 == j) ? 1.0 : 0.0;
+    for (int i = j; i >= 0; --i) {
+      const double wk0 = (lane < i) ? W[lane + i * n] : 0.0;
+      const double wk1 = (lane + 32 < i) ? W[lane + 32 + i * n] : 0.0;
+      const double xi = __shfl_sync(0xffffffffu, i < 32 ? x0 : x1, i & 31) * rsq[i];   // x_i / R_ii
+      if (lane == (i & 31)) {
+        if (i < 32) x0 = xi; else x1 = xi;
+      }
+      x0 = fma(-wk0, xi, x0);
+      x1 = fma(-wk1, xi, x1);
+    }
+    if (lane < n) Rinv[lane + (size_t)j * ldr] = x0;
+    if (lane + 32 < n) Rinv[lane + 32 + (size_t)j * ldr] = x1;
+  }
+}
+
 int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int ldr, int shift_mode) {
   const size_t need = ((size_t)ell * ell + (size_t)ell * (ell | 1)) * sizeof(double);
   const size_t need_packed = (size_t)ell * (ell + 1) / 2 * sizeof(double);
-  if (need > 200 * 1024 && need_packed <= 208 * 1024) {
+  static const int small_max = [] {
+    const char* s = getenv("NYS_CHOL_SMALL_MAX");  // tuning / A-B override (default 64; 0 disables)
+    return s ? atoi(s) : 64;
+  }();
+  if (ell <= small_max && ell <= 64) {
+    chol_inv_small_kernel<<<1, 1024, 0, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);
+  } else if (need > 200 * 1024 && need_packed <= 208 * 1024) {
     NYS_TRY(ensure_max_smem(ctx, (const void*)chol_inv_packed_kernel, 208 * 1024));
     chol_inv_packed_kernel<<<1, 1024, need_packed, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);
   } else if (need <= 200 * 1024) {
@@ -323,38 +405,38 @@ int launch_trmm_upper(nys_ctx* ctx, int ell, int ld, const double* R1, const dou
 // accuracy (c^2 + s^2 = 1 keeps V orthogonal); t only steers convergence.
 // Output: V (ell x ell, ld ldv) and sigma sorted descending (columns of V permuted to match).
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ double fast_rcp(double x) {
-  const double ax = fabs(x);
-  if (!(ax > 1e-30 && ax < 1e30)) return 1.0 / x;
-  double r = (double)__frcp_rn((float)x);
-  r = r * fma(-x, r, 2.0);
-  r = r * fma(-x, r, 2.0);
-  return r;
-}
-__device__ __forceinline__ double fast_rsqrt(double y) {  // y in [1, 1e30)
-  double r = (double)rsqrtf((float)y);
-  r = r * fma(-0.5 * y * r, r, 1.5);
-  r = r * fma(-0.5 * y * r, r, 1.5);
-  r = r * fma(-0.5 * y * r, r, 1.5);
-  return r;
-}
-
 // One warp per column pair (E = NMAX / 32 elements per lane, fully unrolled and predicated): a
 // round costs one dot product (5 shuffle levels), one rotation and the two column updates.
 // Rotation (symmetric Schur, fp64): zeta = (beta - alpha) / (2 gamma),
 // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), c = (1 + t^2)^{-1/2}, s = c t; the reciprocal and
-// rsqrt come from fp32 seeds refined by Newton steps to fp64 (t must be accurate: the column norms
-// are updated incrementally as alpha - t gamma, beta + t gamma).
+// rsqrt come from fp32 seeds refined by Newton steps.  Only c needs full fp64 accuracy given t
+// (c^2 (1 + t^2) = 1 keeps V orthogonal whatever t is): the rsqrts take two Newton steps from the
+// ~2^-22 fp32 seed (error ~2^-44 -> below 2^-53).  zeta and t steer the rotation and the incremental
+// norm update alpha - t gamma, beta + t gamma (norms are recomputed exactly every sweep): one step
+// each (relative error ~2^-44, a residual coupling ~1e-13 gamma that the next sweep removes).
+__device__ __forceinline__ double fast_rcp1(double x) {
+  const double ax = fabs(x);
+  if (!(ax > 1e-30 && ax < 1e30)) return 1.0 / x;
+  const double r = (double)__frcp_rn((float)x);
+  return r * fma(-x, r, 2.0);
+}
+__device__ __forceinline__ double fast_rsqrt2(double y) {  // y in [1, 1e30)
+  double r = (double)rsqrtf((float)y);
+  const double hy = -0.5 * y;
+  r = r * fma(hy * r, r, 1.5);
+  r = r * fma(hy * r, r, 1.5);
+  return r;
+}
 __device__ __forceinline__ void jacobi_rotation(double al, double be, double ga, double& c, double& s, double& t) {
-  const double zeta = (be - al) * 0.5 * fast_rcp(ga);
+  const double zeta = (be - al) * 0.5 * fast_rcp1(ga);
   const double az = fabs(zeta);
   if (az > 1e8) {
-    t = 0.5 * fast_rcp(zeta);
+    t = 0.5 * fast_rcp1(zeta);
   } else {
     const double y = fma(zeta, zeta, 1.0);
-    t = copysign(fast_rcp(az + y * fast_rsqrt(y)), zeta);
+    t = copysign(fast_rcp1(az + y * fast_rsqrt2(y)), zeta);
   }
-  c = fast_rsqrt(fma(t, t, 1.0));
+  c = fast_rsqrt2(fma(t, t, 1.0));
   s = c * t;
 }
 
