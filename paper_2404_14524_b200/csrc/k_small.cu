@@ -279,16 +279,18 @@ __global__ void __launch_bounds__(1024) chol_inv_packed_kernel(int ell, double* 
   }
 }
 
-// Same contract for ell <= 64 (the paper's ranks up to 50 and CholeskyQR3 passes at them) with one
-// block barrier per elimination step instead of two: the lane that updates row k+1 of a trailing
-// column also publishes it into a double-buffered row, which is step k+1's pivot row.  R^{-1} is then
-// formed one column per warp with no block barrier at all: x = e_j; for i = j..0:
-// x_i /= R_ii, x_{0:i} -= R_{0:i,i} x_i (x held two elements per lane, x_i broadcast by a shuffle).
+// Same contract for ell <= 128 (E = ceil(ell / 32) elements per lane; the paper's ranks up to 100 and
+// CholeskyQR3 passes at them) with one block barrier per elimination step instead of two: the lane
+// that updates row k+1 of a trailing column also publishes it into a double-buffered row, which is
+// step k+1's pivot row.  R^{-1} is then formed one column per warp with no block barrier at all:
+// x = e_j; for i = j..0: x_i /= R_ii, x_{0:i} -= R_{0:i,i} x_i (x held E elements per lane, x_i
+// broadcast by a shuffle).  W (ell x ell, ld ell) in dynamic shared memory (128 KB at ell = 128).
+template <int E>
 __global__ void __launch_bounds__(1024) chol_inv_small_kernel(int ell, double* G, int ldg, double* Rinv, int ldr,
                                                              int shift_mode, double* sc) {
-  __shared__ double W[64 * 64];
-  __shared__ double rowb[2][64];
-  __shared__ double rsq[64];
+  extern __shared__ double W[];
+  __shared__ double rowb[2][32 * E];
+  __shared__ double rsq[32 * E];
   __shared__ double shift;
   const int n = ell, tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31, nw = blockDim.x >> 5;
   for (int e = tid; e < n * n; e += blockDim.x) {
@@ -339,19 +341,27 @@ __global__ void __launch_bounds__(1024) chol_inv_small_kernel(int ell, double* G
   }
   __syncthreads();
   for (int j = warp; j < n; j += nw) {
-    double x0 = (lane == j) ? 1.0 : 0.0, x1 = (lane + 32 == j) ? 1.0 : 0.0;
+    double x[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) x[q] = (lane + 32 * q == j) ? 1.0 : 0.0;
     for (int i = j; i >= 0; --i) {
-      const double wk0 = (lane < i) ? W[lane + i * n] : 0.0;
-      const double wk1 = (lane + 32 < i) ? W[lane + 32 + i * n] : 0.0;
-      const double xi = __shfl_sync(0xffffffffu, i < 32 ? x0 : x1, i & 31) * rsq[i];   // x_i / R_ii
-      if (lane == (i & 31)) {
-        if (i < 32) x0 = xi; else x1 = xi;
+      double wk[E];
+#pragma unroll
+      for (int q = 0; q < E; ++q) wk[q] = (lane + 32 * q < i) ? W[lane + 32 * q + i * n] : 0.0;
+      const int qi = i >> 5;      // warp-uniform
+      double xo = x[0];
+#pragma unroll
+      for (int q = 1; q < E; ++q) if (qi == q) xo = x[q];
+      const double xi = __shfl_sync(0xffffffffu, xo, i & 31) * rsq[i];   // x_i / R_ii
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        if (q == qi && lane == (i & 31)) x[q] = xi;
+        x[q] = fma(-wk[q], xi, x[q]);
       }
-      x0 = fma(-wk0, xi, x0);
-      x1 = fma(-wk1, xi, x1);
     }
-    if (lane < n) Rinv[lane + (size_t)j * ldr] = x0;
-    if (lane + 32 < n) Rinv[lane + 32 + (size_t)j * ldr] = x1;
+#pragma unroll
+    for (int q = 0; q < E; ++q)
+      if (lane + 32 * q < n) Rinv[lane + 32 * q + (size_t)j * ldr] = x[q];
   }
 }
 
@@ -359,11 +369,17 @@ int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int
   const size_t need = ((size_t)ell * ell + (size_t)ell * (ell | 1)) * sizeof(double);
   const size_t need_packed = (size_t)ell * (ell + 1) / 2 * sizeof(double);
   static const int small_max = [] {
-    const char* s = getenv("NYS_CHOL_SMALL_MAX");  // tuning / A-B override (default 64; 0 disables)
-    return s ? atoi(s) : 64;
+    const char* s = getenv("NYS_CHOL_SMALL_MAX");  // tuning / A-B override (default 128; 0 disables)
+    return s ? atoi(s) : 128;
   }();
-  if (ell <= small_max && ell <= 64) {
-    chol_inv_small_kernel<<<1, 1024, 0, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);
+  if (ell <= small_max && ell <= 128) {
+    const size_t sm = (size_t)ell * ell * sizeof(double);
+    if (ell <= 64) {
+      chol_inv_small_kernel<2><<<1, 1024, sm, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);
+    } else {
+      NYS_TRY(ensure_max_smem(ctx, (const void*)chol_inv_small_kernel<4>, 128 * 1024));
+      chol_inv_small_kernel<4><<<1, 1024, sm, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);
+    }
   } else if (need > 200 * 1024 && need_packed <= 208 * 1024) {
     NYS_TRY(ensure_max_smem(ctx, (const void*)chol_inv_packed_kernel, 208 * 1024));
     chol_inv_packed_kernel<<<1, 1024, need_packed, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);

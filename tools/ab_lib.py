@@ -14,7 +14,7 @@ dev = lambda a: torch.from_numpy(a).cuda()
 rs = np.random.default_rng(0)
 d = torch.from_numpy(np.exp(rs.uniform(0, np.log(1e8), inst.A.shape[1]))).cuda()
 e = torch.zeros(m, dtype=torch.float64, device="cuda")
-for ell in (20, 50, 64):
+for ell in [int(v) for v in os.environ.get("AB_ELLS", "20,50,64").split(",")]:
     Om = torch.empty((ell, m), dtype=torch.float64, device="cuda")
     ctx.nys_gaussian(m, ell, 0, 1, Om)
     U = torch.empty_like(Om); lam = torch.empty(ell, dtype=torch.float64, device="cuda")
