@@ -52,7 +52,9 @@ typedef struct nys_ctx nys_ctx;
 /* Create a context bound to `device` and `cuda_stream` (a cudaStream_t; NULL -> the library
  * creates and owns a non-blocking stream).  nccl_unique_id: NULL for a single GPU, else a
  * pointer to the 128-byte ncclUniqueId shared by all `world` ranks (rank in [0, world)).
- * NCCL (libnccl.so.2) is loaded with dlopen only when world > 1. */
+ * world = 1 with a non-NULL id creates a ONE-rank NCCL communicator and every call takes the
+ * multi-rank path (local partials, ncclAllReduce, replicated terms): validation of the NCCL
+ * plumbing on a single GPU.  NCCL (libnccl.so.2) is loaded with dlopen only when an id is given. */
 int nys_create(nys_ctx** out, int device, void* cuda_stream,
                const void* nccl_unique_id, int rank, int world);
 int nys_destroy(nys_ctx* ctx);

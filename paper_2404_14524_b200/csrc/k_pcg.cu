@@ -703,7 +703,7 @@ static PcgKernel pcg_kernel_for(const PcgCfg& c) {
 }
 
 bool pcg_persistent_supported(nys_ctx* ctx, int64_t m, int64_t n, int ell) {
-  return ctx->world == 1 && m <= 8192 && n > 0 && ell <= 256 && getenv("NYS_NO_PERSISTENT") == nullptr;
+  return !ctx->multi() && m <= 8192 && n > 0 && ell <= 256 && getenv("NYS_NO_PERSISTENT") == nullptr;
 }
 
 // tolerance must already be in sc[S_TOL] and delta in sc[S_DELTA]

@@ -160,7 +160,7 @@ int launch_muaff(nys_ctx* ctx, int64_t n, const double* x, const double* dx, con
   const int g = reduce_grid(ctx, n);
   D.part = ctx->wsd("dot_part", (size_t)4 * g);
   D.counter = ctx->counters + counter_slot;
-  D.post = ctx->world > 1 ? DP_NONE : DP_MUAFF;
+  D.post = ctx->multi() ? DP_NONE : DP_MUAFF;
   D.post_a = n_total;
   dots_kernel<<<g, 256, 0, ctx->stream>>>(D);
   ctx->launches++;

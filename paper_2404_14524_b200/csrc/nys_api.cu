@@ -158,7 +158,7 @@ int loop_allreduce(nys_ctx* ctx, double* buf, size_t count, bool is_min) {
 }
 
 int allreduce(nys_ctx* ctx, double* buf, size_t count, bool is_min = false) {
-  if (ctx->world <= 1 || count == 0) return NYS_OK;
+  if (!ctx->multi() || count == 0) return NYS_OK;
   if (ctx->loop_comm) return loop_allreduce(ctx, buf, count, is_min);
   ncclResult_t r = g_nccl.allReduce(buf, buf, count, ncclFloat64, is_min ? ncclMin : ncclSum,
                                     (ncclComm_t)ctx->nccl_comm, ctx->stream);
@@ -202,7 +202,7 @@ int apply_normal(nys_ctx* ctx, const NormalOp& op, const double* z, const double
   c.m = op.m; c.n = op.n; c.lda = op.lda; c.A = op.A;
   c.z = z; c.p = p; c.beta = beta; c.p_out = p_out; c.d = op.d; c.done = done;
   c.out = w;
-  if (ctx->world == 1) {
+  if (!ctx->multi()) {
     c.use_delta = true; c.delta = op.delta; c.e = op.e; c.pcg_alpha = pcg_alpha;
     return launch_matvec(ctx, c);
   }
@@ -221,7 +221,7 @@ namespace {
 int apply_normal_full(nys_ctx* ctx, const NormalOp& op, const double* z, const double* p, const double* beta,
                       double* p_out, double* w, bool pcg_alpha, const double* done) {
   NYS_TRY(apply_normal(ctx, op, z, p, beta, p_out, w, pcg_alpha, done));
-  if (ctx->world > 1) {
+  if (ctx->multi()) {
     const double* v = p_out ? p_out : z;
     NYS_TRY(launch_finalize_terms(ctx, op.m, w, v, op.delta, op.e, pcg_alpha, done));
   }
@@ -234,7 +234,7 @@ int apply_A(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, co
   MatvecCall c;
   c.mode = MV_NONLY;
   c.m = m; c.n = n; c.lda = lda; c.A = A; c.u = u; c.out = out; c.sgn = sgn;
-  if (ctx->world == 1) {
+  if (!ctx->multi()) {
     c.add = add;
     return launch_matvec(ctx, c);
   }
@@ -343,11 +343,11 @@ int sketch_Y(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, c
   {
     GemmCall g;  // Y = A T (+ e o Omega)
     g.M = m; g.N = ell; g.K = n; g.A = A; g.lda = lda; g.a_kmajor = false; g.B = T; g.ldb = np_; g.C = Y; g.ldc = mp;
-    if (ctx->world == 1 && e) { g.addv = e; g.addm = Om; g.ldadd = mp; }
+    if (!ctx->multi() && e) { g.addv = e; g.addm = Om; g.ldadd = mp; }
     if (n == 0) NYS_CUDA_TRY(ctx, cudaMemsetAsync(Y, 0, sizeof(double) * mp * ell, ctx->stream));
     else NYS_TRY(launch_gemm(ctx, g));
   }
-  if (ctx->world > 1) {
+  if (ctx->multi()) {
     NYS_TRY(allreduce(ctx, Y, (size_t)mp * ell));
     if (e) NYS_TRY(launch_add_eomega(ctx, m, ell, e, Om, Y, mp));
   }
@@ -377,7 +377,7 @@ int chol_build(nys_ctx* ctx, const NormalOp& op, int ell, CholFactors& F) {
     MatvecCall c;
     c.mode = MV_DIAG; c.m = m; c.n = op.n; c.lda = op.lda; c.A = op.A; c.d = op.d; c.z = ones;
     c.out = F.diag;
-    if (ctx->world == 1) {
+    if (!ctx->multi()) {
       c.use_delta = true; c.delta = op.delta; c.e = op.e;
       NYS_TRY(launch_matvec(ctx, c));
     } else {
@@ -484,7 +484,7 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
                             max_iter, 0ull, false, chol != nullptr));
   if (chol) NYS_TRY(launch_chol_apply(ctx, *chol, r, z, 1, 1));
   else if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 1, m, r, z, U, ldu, ell, h));
-  if (ctx->world == 1 && getenv("NYS_NO_GRAPH") == nullptr) {  // NYS_NO_GRAPH: eager loop (profiling)
+  if (!ctx->multi() && getenv("NYS_NO_GRAPH") == nullptr) {  // NYS_NO_GRAPH: eager loop (profiling)
     // iterations 0 and 1 eagerly (they size every workspace), then the rest of the loop as ONE
     // graph launch: a conditional WHILE node whose body is two iterations (p double-buffer
     // parity); pcg_update's last block clears the condition when PCG is done.
@@ -654,7 +654,7 @@ struct AOps {
     if (structure == 0) { op = NormalOp{m, n, lda, A, d, nullptr, delta}; return NYS_OK; }
     if (structure == 2) {                 // e = sum_k scale_k^2 d_unit (global: a replicated term)
       NYS_TRY(launch_unit_fold(ctx, UB, m, d + nd, nullptr, 1, e));
-      if (ctx->world > 1) NYS_TRY(allreduce(ctx, e, (size_t)m));
+      if (ctx->multi()) NYS_TRY(allreduce(ctx, e, (size_t)m));
       op = NormalOp{m, nd, lda, A, d, e, delta};
       return NYS_OK;
     }
@@ -666,7 +666,7 @@ struct AOps {
   int Ax(const double* u, double* out, const double* add) {
     if (structure == 0) return apply_A(ctx, m, n, A, lda, u, out, 1.0, add);
     if (structure == 2) {
-      if (ctx->world == 1) {              // unit part + add folded into the matvec's add vector
+      if (!ctx->multi()) {              // unit part + add folded into the matvec's add vector
         NYS_TRY(launch_unit_fold(ctx, UB, m, u + nd, add, 0, addm));
         return apply_A(ctx, m, nd, A, lda, u, out, 1.0, addm);
       }
@@ -931,7 +931,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   NYS_TRY(launch_minsum(ctx, n, x, 0.0, S_TMP0, S_TMP1, 6));
   NYS_TRY(launch_minsum(ctx, n, z, 0.0, S_TMP2, S_TMP3, 7));
   NYS_TRY(D.dot(n, x, z, S_TMP4));
-  if (ctx->world > 1) {
+  if (ctx->multi()) {
     NYS_TRY(allreduce_slots(ctx, S_TMP0, 1, true));
     NYS_TRY(allreduce_slots(ctx, S_TMP2, 1, true));
     NYS_TRY(allreduce_slots(ctx, S_TMP1, 1));
@@ -1052,7 +1052,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(allreduce_slots(ctx, S_TMP0, 2, true));
     NYS_TRY(launch_steps_post(ctx));
     NYS_TRY(launch_muaff(ctx, n, x, dxp, z, dzp, n_total, 9, w, dwp, sv, dsp));
-    if (ctx->world > 1) {
+    if (ctx->multi()) {
       if (gen) NYS_TRY(allreduce_slots(ctx, S_TMP6, 2));
       else NYS_TRY(allreduce_slots(ctx, S_TMP7, 1));
       NYS_TRY(launch_muaff_post(ctx, n_total, gen ? 1 : 0));
@@ -1268,7 +1268,8 @@ int nys_create(nys_ctx** out, int device, void* cuda_stream, const void* nccl_un
     LoopComm* c = (LoopComm*)lc;
     if (!c || c->world != world) { ctx->set_error("loopback communicator / world mismatch"); return fail(NYS_EINVAL); }
     ctx->loop_comm = c;
-  } else if (world > 1) {
+  } else if (world > 1 || nccl_unique_id) {   // world = 1 with an id: a one-rank NCCL communicator
+    ctx->coll = true;
     std::string err;
     if (!g_nccl.load(err)) { ctx->set_error(err); return fail(NYS_ENCCL); }
     ncclUniqueId id;
@@ -1574,7 +1575,7 @@ static int nys_ipppmm_solve_body(nys_ctx* ctx, const nys_qp* qp, const nys_optio
     ctx->set_error("nys_ipppmm_solve: bad problem");
     return NYS_EINVAL;
   }
-  if (qp->structure == 1 && (qp->nd < 0 || qp->n != 2 * qp->nd + 2 * qp->m || ctx->world != 1)) {
+  if (qp->structure == 1 && (qp->nd < 0 || qp->n != 2 * qp->nd + 2 * qp->m || ctx->multi())) {
     ctx->set_error("nys_ipppmm_solve: structure 1 needs n = 2 nd + 2 m and one rank");
     return NYS_EINVAL;
   }

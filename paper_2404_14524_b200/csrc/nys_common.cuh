@@ -53,6 +53,8 @@ struct nys_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int rank = 0, world = 1;
+  bool coll = false;               // a one-rank NCCL communicator (world = 1 with an id): multi-rank path
+  bool multi() const { return world > 1 || coll; }
   void* nccl_comm = nullptr;
   void* loop_comm = nullptr;      // in-process loopback communicator (nys_loopback_comm_create)
   int num_sms = 148;

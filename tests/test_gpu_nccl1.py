@@ -1,0 +1,81 @@
+"""The REAL NCCL path on one B200: a context created with world = 1 and an ncclUniqueId holds a one-rank
+NCCL communicator (nys_create, include/nysipm.h) and takes every multi-rank branch — local partials,
+ncclAllReduce on the context's stream, replicated terms added after the reduction, the eager PCG loop.
+This exercises the dlopen of libnccl.so.2, ncclCommInitRank and ncclAllReduce exactly as a
+torchrun'ed N-GPU bench does, without ranks that wait on each other.  Results must match the
+single-GPU path and the oracle at the §8 tolerances.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import ippmm, linops  # noqa: E402
+from synth import make_config  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+
+
+def _nccl_ctx():
+    from paper_2404_14524_b200 import Context, nccl_unique_id
+    return Context(0, nccl_id=nccl_unique_id(), rank=0, world=1)
+
+
+def test_nccl_one_rank_matvec_sketch_pcg():
+    from paper_2404_14524_b200 import Context, colmajor_device
+    inst = make_config(1, m=300, n=1201, ell=20)
+    m, ell = inst.m, inst.ell
+    rs = np.random.default_rng(5)
+    d = rs.uniform(0.01, 3.0, inst.n)
+    v = rs.standard_normal(m)
+    e = rs.uniform(0.0, 0.5, m)
+    Ad, lda = colmajor_device(inst.A)
+    out = {}
+    for name, ctx in (("nccl", _nccl_ctx()), ("single", Context(0))):
+        w = torch.empty(m, dtype=torch.float64, device="cuda")
+        ctx.nys_normal_matvec(Ad, lda, m, dev(d), dev(e), 0.25, dev(v), w)
+        Om = torch.empty((ell, m), dtype=torch.float64, device="cuda")
+        U = torch.empty((ell, m), dtype=torch.float64, device="cuda")
+        lam = torch.empty(ell, dtype=torch.float64, device="cuda")
+        ctx.nys_gaussian(m, ell, 7, 3, Om)
+        ctx.nys_sketch(Ad, lda, m, dev(d), dev(e), 1e-2, ell, Om, U, lam)
+        torch.cuda.synchronize()
+        out[name] = (w.cpu().numpy(), U.cpu().numpy(), lam.cpu().numpy())
+        ctx.close()
+    ref = linops.normal_matvec(inst.A, d, v, 0.25) + e * v
+    for name in out:
+        assert np.linalg.norm(out[name][0] - ref) <= 1e-12 * np.linalg.norm(ref), name
+    Nh = [(U.T * lam) @ U for _, U, lam in out.values()]
+    assert np.linalg.norm(Nh[0] - Nh[1]) <= 1e-10 * np.linalg.norm(Nh[1])
+
+
+@pytest.mark.parametrize("cfg,kw", [(0, {}), (1, dict(m=200, n=800, ell=20))])
+def test_nccl_one_rank_ipppmm_matches_single_and_oracle(cfg, kw):
+    from paper_2404_14524_b200 import Context, colmajor_device
+    inst = make_config(cfg, **kw)
+    m = inst.m
+    Ad, lda = colmajor_device(inst.A)
+    args = (Ad, lda, m, dev(inst.q), dev(inst.b), dev(inst.c))
+    cn = _nccl_ctx()
+    g = cn.nys_ipppmm_solve(*args, ell=inst.ell)
+    torch.cuda.synchronize()
+    cn.close()
+    c1 = Context(0)
+    g1 = c1.nys_ipppmm_solve(*args, ell=inst.ell)
+    torch.cuda.synchronize()
+    c1.close()
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
+    assert ref.status == "optimal"
+    assert g["status"] == 0 and g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    assert abs(g["outer"] - g1["outer"]) <= 1 and abs(g["outer"] - ref.outer) <= 2
+    x, y, z = (g[k].cpu().numpy() for k in ("x", "y", "z"))
+    band = lambda p, d, xx, yy, zz: abs(p - d) + np.linalg.norm(xx) * np.linalg.norm(  # noqa: E731
+        inst.c + inst.q * xx - inst.A.T @ yy - zz) + np.linalg.norm(yy) * np.linalg.norm(inst.b - inst.A @ xx)
+    tol = max(1e-7 * max(1.0, abs(ref.obj)),
+              band(g["obj"], g["dual_obj"], x, y, z) + band(ref.obj, ref.dual_obj, ref.x, ref.y, ref.z))
+    assert abs(g["obj"] - ref.obj) <= tol
+    assert abs(g["obj"] - g1["obj"]) <= tol
