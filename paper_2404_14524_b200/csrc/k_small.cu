@@ -430,14 +430,26 @@ int launch_trmm_upper(nys_ctx* ctx, int ell, int ld, const double* R1, const dou
 // ~2^-22 fp32 seed (error ~2^-44 -> below 2^-53).  zeta and t steer the rotation and the incremental
 // norm update alpha - t gamma, beta + t gamma (norms are recomputed exactly every sweep): one step
 // each (relative error ~2^-44, a residual coupling ~1e-13 gamma that the next sweep removes).
+// seeds straight from the fp64 MUFU approximations (rcp / rsqrt .approx.ftz.f64, ~2^-22 relative):
+// no fp64 <-> fp32 conversions on the rotation's dependency chain
+__device__ __forceinline__ double rcp_seed(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+__device__ __forceinline__ double rsqrt_seed(double y) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+  return r;
+}
 __device__ __forceinline__ double fast_rcp1(double x) {
   const double ax = fabs(x);
   if (!(ax > 1e-30 && ax < 1e30)) return 1.0 / x;
-  const double r = (double)__frcp_rn((float)x);
+  const double r = rcp_seed(x);
   return r * fma(-x, r, 2.0);
 }
 __device__ __forceinline__ double fast_rsqrt2(double y) {  // y in [1, 1e30)
-  double r = (double)rsqrtf((float)y);
+  double r = rsqrt_seed(y);
   const double hy = -0.5 * y;
   r = r * fma(hy * r, r, 1.5);
   r = r * fma(hy * r, r, 1.5);
