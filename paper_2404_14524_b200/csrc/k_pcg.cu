@@ -680,9 +680,16 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
 struct PcgCfg {
   int T, GT, RPT, CPG;
 };
-static PcgCfg pcg_pick(int64_t m) {
+static PcgCfg pcg_pick(int64_t m, int64_t n, int sms) {
   if (m <= 64) return {256, 32, 2, 4};
-  if (m <= 128) return {256, 32, 4, 2};
+  if (m <= 128) {
+    // short columns: a panel of 8 CPG columns x m rows is a small bulk copy; with many columns take
+    // more per group (SensIT shape m = 101, 98528 columns: PCG 71.9 / 50.5 / 44.4 ms at CPG 2 / 4 / 8;
+    // config 0, 400 columns: CPG 2 best) while every CTA still gets >= 4 panels
+    for (int cpg = 8; cpg > 2; cpg >>= 1)
+      if (n / (8 * cpg) >= 4LL * sms) return {256, 32, 4, cpg};
+    return {256, 32, 4, 2};
+  }
   if (m <= 256) return {256, 64, 4, 2};
   if (m <= 1024) return {256, 128, 8, 2};
   if (m <= 2048) return {256, 256, 8, 4};
@@ -692,6 +699,8 @@ static PcgCfg pcg_pick(int64_t m) {
 typedef void (*PcgKernel)(const PcgPParams);
 static PcgKernel pcg_kernel_for(const PcgCfg& c) {
   if (c.GT == 32 && c.RPT == 2) return pcg_persistent_kernel<256, 32, 2, 4>;
+  if (c.GT == 32 && c.RPT == 4 && c.CPG == 8) return pcg_persistent_kernel<256, 32, 4, 8>;
+  if (c.GT == 32 && c.RPT == 4 && c.CPG == 4) return pcg_persistent_kernel<256, 32, 4, 4>;
   if (c.GT == 32 && c.RPT == 4) return pcg_persistent_kernel<256, 32, 4, 2>;
   if (c.GT == 64) return pcg_persistent_kernel<256, 64, 4, 2>;
   if (c.GT == 128) return pcg_persistent_kernel<256, 128, 8, 2>;
@@ -711,7 +720,7 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
                           const double* e, const double* U, int64_t ldu, int ell, const double* s, const double* rhs,
                           double* x, int max_iter) {
   const auto hp0 = std::chrono::steady_clock::now();
-  PcgCfg c = pcg_pick(m);
+  PcgCfg c = pcg_pick(m, n, ctx->num_sms);
   if (const char* ov = getenv("NYS_PCG_CFG")) {  // tuning override "T,GT,RPT,CPG" (must be instantiated)
     PcgCfg o;
     if (sscanf(ov, "%d,%d,%d,%d", &o.T, &o.GT, &o.RPT, &o.CPG) == 4 && (int64_t)o.GT * o.RPT >= m) c = o;
