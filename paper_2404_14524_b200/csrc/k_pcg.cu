@@ -681,7 +681,7 @@ struct PcgCfg {
   int T, GT, RPT, CPG;
 };
 static PcgCfg pcg_pick(int64_t m, int64_t n, int sms) {
-  if (m <= 64) return {256, 32, 2, 4};
+  if (m <= 64) return (n / 64 >= 4LL * sms) ? PcgCfg{256, 32, 2, 8} : PcgCfg{256, 32, 2, 4};   // config 3: 63.9 -> 47.7 us / it
   if (m <= 128) {
     // short columns: a panel of 8 CPG columns x m rows is a small bulk copy; with many columns take
     // more per group (SensIT shape m = 101, 98528 columns: PCG 71.9 / 50.5 / 44.4 ms at CPG 2 / 4 / 8;
@@ -698,6 +698,7 @@ static PcgCfg pcg_pick(int64_t m, int64_t n, int sms) {
 }
 typedef void (*PcgKernel)(const PcgPParams);
 static PcgKernel pcg_kernel_for(const PcgCfg& c) {
+  if (c.GT == 32 && c.RPT == 2 && c.CPG == 8) return pcg_persistent_kernel<256, 32, 2, 8>;
   if (c.GT == 32 && c.RPT == 2) return pcg_persistent_kernel<256, 32, 2, 4>;
   if (c.GT == 32 && c.RPT == 4 && c.CPG == 8) return pcg_persistent_kernel<256, 32, 4, 8>;
   if (c.GT == 32 && c.RPT == 4 && c.CPG == 4) return pcg_persistent_kernel<256, 32, 4, 4>;

@@ -224,7 +224,8 @@ def test_pcg_parity(ctx, cfg, kw, use_prec):
 
 @pytest.mark.parametrize("cfg,kw,iters", [(1, {}, 25), (1, dict(m=300, n=1200, ell=30), 15), (0, {}, 40),
                                            # short wide A: 8 / 4 columns per group in the persistent kernel
-                                           (1, dict(m=101, n=40000, ell=10), 20), (1, dict(m=120, n=20000, ell=10), 20)])
+                                           (1, dict(m=101, n=40000, ell=10), 20), (1, dict(m=120, n=20000, ell=10), 20),
+                                           (1, dict(m=60, n=40000, ell=10), 20)])
 def test_pcg_fixed_iterations_match_oracle(ctx, cfg, kw, iters):
     """Exactly `iters` PCG iterations (tol = 0) on the GPU and in the oracle: the iterates agree to
     rounding (every reduction of the persistent kernel — p^T N p, ||r||^2, U^T r, r^T z — enters x)."""
