@@ -22,4 +22,6 @@ Modules
   rng       Philox4x32-10 + Box-Muller Gaussian test matrix Omega_k
   partial_chol  partial Cholesky preconditioner of Chol-IP-PMM
   active_set brute-force active-set enumeration for tiny QPs
+  ssn       exact f* of a Q > 0 separable QP by dual semismooth Newton (independent pin, §8(c) P9)
+  svm       config 2's A = [Xt, -Xt, I, -I] as an operator + the exact Woodbury path D (A23)
 """

@@ -168,6 +168,8 @@ def initial_point(A, q, b, c, solve_aat):
 # ----------------------------------------------------------------------------------------
 
 def _direct_solver(A, d, delta):
+    if hasattr(A, "direct_solver"):            # structured operator (oracle.svm): Woodbury path D
+        return A.direct_solver(d, delta)
     L = sla.cho_factor(dense_normal_matrix(A, d, delta), lower=True)
 
     def solve(rhs, tol=None):
@@ -208,7 +210,10 @@ def build_preconditioner(A, d, ell, Omega):
 # ----------------------------------------------------------------------------------------
 
 def solve(A, q, b, c, opts: Options = Options()) -> Result:
-    A = np.asarray(A, dtype=np.float64)
+    """A: dense m x n array, or a structured operator with @, .T @, .shape and direct_solver
+    (oracle.svm.SvmOperator: config 2 without materialising its 40.8 GB A)."""
+    if not hasattr(A, "direct_solver"):
+        A = np.asarray(A, dtype=np.float64)
     m, n = A.shape
     omega_fn = opts.omega_fn or _default_omega(opts.seed)
     max_iter = opts.pcg_max_iter

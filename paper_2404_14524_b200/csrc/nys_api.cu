@@ -314,13 +314,15 @@ int nystrom_factor(nys_ctx* ctx, int64_t m, int ell, const double* Y, const doub
     NYS_TRY(launch_gemm(ctx, g));
   }
   NYS_TRY(launch_lambda_from_sigma(ctx, ell, sig, lam));              // line 8
+  if (info) NYS_TRY(launch_orth_err(ctx, m, ell, U, mp, S_TMP6));
+  // a failed shifted CholeskyQR pass leaves Gi / R stale: U would be silently non-orthonormal,
+  // so the flag is read on every build (one host sync per outer iteration), not only with info
+  NYS_TRY(read_slots(ctx));
+  if (ctx->h_sc[S_CHOLFAIL] != 0.0) {
+    ctx->set_error("nys_sketch: shifted CholeskyQR of B = Y_nu C^{-1} failed (B numerically rank deficient)");
+    return NYS_ECHOL;
+  }
   if (info) {
-    NYS_TRY(launch_orth_err(ctx, m, ell, U, mp, S_TMP6));
-    NYS_TRY(read_slots(ctx));
-    if (ctx->h_sc[S_CHOLFAIL] != 0.0) {
-      ctx->set_error("nys_sketch: CholeskyQR of B failed");
-      return NYS_ECHOL;
-    }
     info->nu = ctx->h_sc[S_NU];
     info->chol_retries = retries;
     info->orth_err = ctx->h_sc[S_TMP6];
@@ -489,10 +491,17 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
     // graph launch: a conditional WHILE node whose body is two iterations (p double-buffer
     // parity); pcg_update's last block clears the condition when PCG is done.
     for (int it = 0; it < 2; ++it) NYS_TRY(pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, it, max_iter, 0ull, chol));
-    char key[512];
-    snprintf(key, sizeof(key), "pcg%s:%lld:%lld:%lld:%p:%p:%p:%p:%lld:%p:%d:%p:%d:%lld", chol ? "C" : "N", (long long)m, (long long)op.n,
+    // the key holds every value the captured kernels take as an argument: for the partial-Cholesky
+    // path its rank, leading dimension and factor pointers too (a later build with a smaller rank
+    // grows no workspace, so ws_epoch alone would not tell the graphs apart)
+    char key[768];
+    snprintf(key, sizeof(key), "pcg%s:%lld:%lld:%lld:%p:%p:%p:%p:%lld:%p:%d:%p:%d:%lld:%d:%d:%p:%p:%p:%p:%p",
+             chol ? "C" : "N", (long long)m, (long long)op.n,
              (long long)op.lda, (const void*)op.A, (const void*)op.d, (const void*)op.e, (const void*)U,
-             (long long)ldu, (const void*)s, ell, (const void*)x, max_iter, (long long)ctx->ws_epoch);
+             (long long)ldu, (const void*)s, ell, (const void*)x, max_iter, (long long)ctx->ws_epoch,
+             chol ? chol->ell : -1, chol ? chol->ldr : -1, chol ? (const void*)chol->Zt : nullptr,
+             chol ? (const void*)chol->dS : nullptr, chol ? (const void*)chol->Rinv : nullptr,
+             chol ? (const void*)chol->piv : nullptr, chol ? (const void*)chol->pivpos : nullptr);
     auto itg = ctx->graphs.find(key);
     cudaGraphExec_t exec = nullptr;
     if (itg != ctx->graphs.end()) {
@@ -1472,8 +1481,26 @@ static int nys_partial_cholesky_body(nys_ctx* ctx, int64_t m, int64_t n, const d
   CholFactors F;
   NYS_TRY(chol_build(ctx, op, ell, F));
   {
+    // the factors nys_chol_precond_apply uses live in buffers only this call writes: chol_build's
+    // ch_* workspaces are overwritten (or reallocated) by every later build on the context,
+    // including each Chol-IP-PMM outer iteration
+    const int64_t mp = even(m);
+    const int le = ell > 0 ? ell : 1;
+    CholFactors K = F;
+    K.piv = (int64_t*)ctx->ws("abi_ch_piv", sizeof(int64_t) * le);
+    K.pivpos = (int*)ctx->ws("abi_ch_pivpos", sizeof(int) * mp);
+    K.Rinv = ctx->wsd("abi_ch_Rinv", (size_t)F.ldr * F.ldr);
+    K.Zt = ctx->wsd("abi_ch_Zt", (size_t)m * le);
+    K.dS = ctx->wsd("abi_ch_dS", (size_t)mp);
+    K.diag = ctx->wsd("abi_ch_diag", (size_t)mp);
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(K.piv, F.piv, sizeof(int64_t) * le, cudaMemcpyDeviceToDevice, ctx->stream));
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(K.pivpos, F.pivpos, sizeof(int) * mp, cudaMemcpyDeviceToDevice, ctx->stream));
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(K.Rinv, F.Rinv, sizeof(double) * F.ldr * F.ldr, cudaMemcpyDeviceToDevice, ctx->stream));
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(K.Zt, F.Zt, sizeof(double) * m * le, cudaMemcpyDeviceToDevice, ctx->stream));
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(K.dS, F.dS, sizeof(double) * mp, cudaMemcpyDeviceToDevice, ctx->stream));
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(K.diag, F.diag, sizeof(double) * mp, cudaMemcpyDeviceToDevice, ctx->stream));
     std::lock_guard<std::mutex> lk(g_chol_mu);
-    g_chol[ctx] = F;
+    g_chol[ctx] = K;
   }
   if (piv && ell > 0)
     NYS_CUDA_TRY(ctx, cudaMemcpyAsync(piv, F.piv, sizeof(int64_t) * ell, cudaMemcpyDeviceToDevice, ctx->stream));

@@ -739,3 +739,195 @@ def test_general_form_all_free_is_the_kkt_solution():
         assert r.status == "optimal"
         assert np.abs(r.x - x_kkt).max() <= 1e-7 and np.abs(r.y - y_kkt).max() <= 1e-7
         assert np.all(r.z == 0)
+
+
+# ------------------------------------------------------------------ App. B.2 initial point with shifts (round 2)
+def test_initial_point_shift_branch_hand_computed():
+    """App. B.2 with both shifts active and different (delta_p != delta_d > 0), so the
+    -1.5 min shifts, gamma and the delta~_d denominator reading A13
+    (sum(x~ + delta_p), P:1473 prints sum(x~ + delta_d)) are all exercised.
+    Worked by hand: A = [1 2], q = 0, b = -3, c = (1, -2); A A^T + 10 I = 15.
+      x~ = A^T (-3/15) = (-0.2, -0.4);  A (c + Q x~) = 1 - 4 = -3 -> y~ = -0.2
+      z~ = c - A^T y~ = (1.2, -1.6)
+      delta_p = -1.5 (-0.4) = 0.6,  delta_d = -1.5 (-1.6) = 2.4
+      x~ + delta_p = (0.4, 0.2),  z~ + delta_d = (3.6, 0.8),  gamma = 1.44 + 0.16 = 1.6
+      delta~_p = 0.6 + 0.8 / 4.4 = 0.6 + 2/11
+      delta~_d = 2.4 + 0.8 / 0.6 = 2.4 + 4/3   (printed denominator sum(x~ + delta_d) = 4.2 would give 2.4 + 4/21)
+    """
+    A = np.array([[1.0, 2.0]])
+    solve = lambda r: (r / 15.0, {"iters": 0})  # noqa: E731
+    x0, y0, z0, _ = ippmm.initial_point(A, np.zeros(2), np.array([-3.0]), np.array([1.0, -2.0]), solve)
+    dpt, ddt = 0.6 + 2.0 / 11.0, 2.4 + 4.0 / 3.0
+    np.testing.assert_allclose(x0, [-0.2 + dpt, -0.4 + dpt], rtol=1e-14)
+    np.testing.assert_allclose(y0, [-0.2], rtol=1e-14)
+    np.testing.assert_allclose(z0, [1.2 + ddt, -1.6 + ddt], rtol=1e-14)
+    # the alternative readings differ well above rounding: the pin can tell them apart
+    assert abs(z0[0] - (1.2 + 2.4 + 4.0 / 21.0)) > 1.0           # printed P:1473 denominator
+    assert abs(x0[0] - (-0.2 + 0.4 + 1.6 / 2.0 / (1.2 + 1.6 + 1.6 * 2 / 3 * 2))) > 0.05   # shift factor 1, not 1.5
+
+
+def test_initial_point_with_q_term_hand_computed():
+    """Same construction with Q != 0 (the Q x~ terms of y~ and z~):
+    A = [1 2], q = (1, 0), b = -3, c = (1, -2), A A^T + 10 I = 15.
+      x~ = (-0.2, -0.4);  c + Q x~ = (0.8, -2);  A(c + Q x~) = -3.2 -> y~ = -16/75
+      z~ = c - A^T y~ + Q x~ = (1 + 16/75 - 0.2, -2 + 32/75) = (76/75, -118/75)
+      delta_p = 0.6, delta_d = 1.5 * 118/75 = 2.36
+      x~ + delta_p = (0.4, 0.2), z~ + delta_d = (76/75 + 2.36, -118/75 + 2.36) = (253/75, 59/75)
+      gamma = 0.4 * 253/75 + 0.2 * 59/75 = 113/75;  sum(z~ + delta_d) = 312/75;  sum(x~ + delta_p) = 0.6
+      delta~_p = 0.6 + (113/150) / (312/75) = 0.6 + 113/624;  delta~_d = 2.36 + (113/150) / 0.6 = 2.36 + 113/90"""
+    A = np.array([[1.0, 2.0]])
+    solve = lambda r: (r / 15.0, {"iters": 0})  # noqa: E731
+    x0, y0, z0, _ = ippmm.initial_point(A, np.array([1.0, 0.0]), np.array([-3.0]), np.array([1.0, -2.0]), solve)
+    F = Fraction
+    dpt = F(3, 5) + F(113, 624)
+    ddt = F(236, 100) + F(113, 90)
+    np.testing.assert_allclose(x0, [float(F(-1, 5) + dpt), float(F(-2, 5) + dpt)], rtol=1e-14)
+    np.testing.assert_allclose(y0, [float(F(-16, 75))], rtol=1e-14)
+    np.testing.assert_allclose(z0, [float(F(76, 75) + ddt), float(F(-118, 75) + ddt)], rtol=1e-14)
+
+
+def test_general_initial_point_shift_branch_hand_computed():
+    """App. B.2 general form with I, J (box) and F (free) variables; readings G2 (delta~_d
+    denominator sum(x~_IJ + delta_p) + sum(w~_J + delta_p)) and G3 (A A^T + 10 I, x~_F not shifted).
+    Worked by hand: A = [1 2 1], vtype = (I, J, F), u = (0, 1, 0), q = 0, b = -3.8, c = (1, -2, 0.5);
+    A A^T + 10 I = 16.
+      x~ = u/2 + A^T (b - A u / 2)/16 = (0, 0.5, 0) + (-4.8/16) (1, 2, 1) = (-0.3, -0.1, -0.3)
+      y~ = A c / 16 = -2.5/16 = -0.15625;  g = c - A^T y~ = (1.15625, -1.6875, 0.65625)
+      z~ = (g_I, g_J / 2, 0) = (1.15625, -0.84375, 0);  s~_J = 0.84375;  w~_J = u_J - x~_J = 1.1
+      delta_p = max(-1.5 min(-0.3, -0.1), -1.5 (1.1), 0) = 0.45
+      delta_d = max(-1.5 min(1.15625, -0.84375), -1.5 (0.84375), 0) = 1.265625
+      gamma_xz = (0.15, 0.35).(2.421875, 0.421875) = 0.5109375
+      gamma_ws = (1.1 + 0.45)(0.84375 + 1.265625) = 3.26953125;  gamma = 3.78046875
+      den_p = 2.421875 + 0.421875 + 2.109375 = 4.953125;  den_d = 0.15 + 0.35 + 1.55 = 2.05
+      delta~_p = 0.45 + 1.890234375 / 4.953125;  delta~_d = 1.265625 + 1.890234375 / 2.05
+      x0 = (x~_I + delta~_p, x~_J + delta~_p, x~_F),  w0_J = 1.1 + delta~_p,
+      z0 = (z~_I + delta~_d, z~_J + delta~_d, 0),  s0_J = 0.84375 + delta~_d"""
+    from oracle import ippmm_gen
+    A = np.array([[1.0, 2.0, 1.0]])
+    solve = lambda r: (r / 16.0, {"iters": 0})  # noqa: E731
+    vtype = np.array([0, 2, 1], np.int8)
+    u = np.array([0.0, 1.0, 0.0])
+    x0, y0, z0, w0, s0 = ippmm_gen.initial_point_general(A, np.zeros(3), np.array([-3.8]),
+                                                         np.array([1.0, -2.0, 0.5]), vtype, u, solve)
+    dpt = 0.45 + 1.890234375 / 4.953125
+    ddt = 1.265625 + 1.890234375 / 2.05
+    np.testing.assert_allclose(x0, [-0.3 + dpt, -0.1 + dpt, -0.3], rtol=1e-14)
+    np.testing.assert_allclose(y0, [-0.15625], rtol=1e-14)
+    np.testing.assert_allclose(z0, [1.15625 + ddt, -0.84375 + ddt, 0.0], rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(w0, [0.0, 1.1 + dpt, 0.0], rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(s0, [0.0, 0.84375 + ddt, 0.0], rtol=1e-14, atol=1e-15)
+    # printed P:1473 denominators (x~ + delta_d, w~ + delta_d) give a different delta~_d
+    printed = 1.265625 + 1.890234375 / ((-0.3 + 1.265625) + (-0.1 + 1.265625) + (1.1 + 1.265625))
+    assert abs(ddt - printed) > 0.3
+
+
+# ------------------------------------------------------------------ exact f* by dual semismooth Newton (§8(c) P9)
+@pytest.mark.parametrize("seed", range(5))
+def test_ssn_matches_active_set_enumeration(seed):
+    from oracle import ssn
+    rs = np.random.default_rng(300 + seed)
+    m, n = 3, 9
+    A = rs.standard_normal((m, n))
+    x0 = rs.uniform(0.2, 1.5, n)
+    x0[rs.permutation(n)[:4]] = 0.0
+    b = A @ x0
+    q = rs.uniform(0.1, 2.0, n)
+    c = rs.standard_normal(n)
+    ref = enumerate_active_sets(A, q, b, c)
+    r = ssn.solve(A, q, b, c)
+    assert abs(r["obj"] - ref["obj"]) <= 1e-10 * max(1.0, abs(ref["obj"]))
+    np.testing.assert_allclose(r["x"], ref["x"], atol=1e-9)
+
+
+def test_ssn_exact_kkt_and_strong_duality_config3_full():
+    """SSN's point satisfies x >= 0, z >= 0 and x o z = 0 exactly (by construction of x(y)), the primal
+    residual is at rounding level and the primal and dual objectives coincide (strong duality, Q > 0)."""
+    from oracle import ssn
+    inst = make_config(3)
+    r = ssn.solve(inst.A, inst.q, inst.b, inst.c)
+    assert r["x"].min() >= 0 and r["z"].min() >= -1e-15 * np.abs(inst.c).max()
+    assert np.max(np.abs(r["x"] * r["z"])) <= 1e-15
+    assert r["rel_p"] <= 1e-10
+    assert abs(r["obj"] - r["dual_obj"]) <= 1e-12 * (1 + abs(r["obj"]))
+
+
+def _band(A, q, b, c, res):
+    rP = b - A @ res.x
+    rD = c + q * res.x - A.T @ res.y - res.z
+    return abs(res.obj - res.dual_obj) + np.linalg.norm(res.x) * np.linalg.norm(rD) + np.linalg.norm(res.y) * np.linalg.norm(rP)
+
+
+@pytest.mark.parametrize("idx,kw,path", [(3, {}, "krylov"), (1, dict(m=200, n=800, ell=20), "direct"),
+                                         (1, dict(m=200, n=800, ell=20), "krylov")])
+def test_ippmm_lands_within_its_certified_band_of_ssn_fstar(idx, kw, path):
+    """The IP-PMM oracle's objective at the paper's tolerance (1e-8) is within its certified band
+    (weak duality with residuals) of the EXACT f* from dual semismooth Newton — an
+    independent method (no barrier, no Krylov solve).  Full-size config 3; reduced config 1 on both paths."""
+    from oracle import ssn
+    inst = make_config(idx, **kw)
+    fstar = ssn.solve(inst.A, inst.q, inst.b, inst.c)
+    assert fstar["rel_p"] <= 1e-10
+    r = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path=path, ell=inst.ell))
+    assert r.status == "optimal"
+    band = _band(inst.A, inst.q, inst.b, inst.c, r)
+    assert abs(r.obj - fstar["obj"]) <= band + 1e-12 * abs(fstar["obj"])
+    # x* is unique (Q > 0, A19): the IP-PMM iterate is close to it
+    assert np.linalg.norm(r.x - fstar["x"]) <= 1e-4 * np.linalg.norm(fstar["x"])
+
+
+# ------------------------------------------------------------------ config 2 operator and Woodbury path D (A23)
+def test_svm_operator_equals_the_materialised_A():
+    from oracle import svm
+    from synth.configs import svm_dense_A
+    inst = make_config(2, m=60, n=7, ell=5)
+    A = svm_dense_A(inst)
+    op = svm.SvmOperator(inst.extra["Xt"])
+    rs = np.random.default_rng(1)
+    X = rs.standard_normal((inst.n, 3))
+    Y = rs.standard_normal((inst.m, 3))
+    assert op.shape == A.shape
+    np.testing.assert_allclose(op @ X, A @ X, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(op.T @ Y, A.T @ Y, rtol=0, atol=1e-13)
+    d = rs.uniform(0.1, 2.0, inst.n)
+    np.testing.assert_allclose(op.dense_normal_matrix(d, 0.3), linops.dense_normal_matrix(A, d, 0.3), rtol=1e-13, atol=1e-12)
+
+
+def test_woodbury_solve_equals_dense_solve():
+    """The capacitance form is an exact identity: it matches a dense LU solve of A D A^T + delta I."""
+    from oracle import svm
+    from synth.configs import svm_dense_A
+    inst = make_config(2, m=300, n=20, ell=10)
+    A = svm_dense_A(inst)
+    op = svm.SvmOperator(inst.extra["Xt"])
+    rs = np.random.default_rng(2)
+    for delta in (1e-8, 1e-3, 10.0):
+        d = np.exp(rs.uniform(-12, 4, inst.n))                    # IPM-like spread of D
+        r = rs.standard_normal(inst.m)
+        sol = op.direct_solver(d, delta)(r)[0]
+        M = linops.dense_normal_matrix(A, d, delta)
+        ref = np.linalg.solve(M, r)
+        # backward stable (residual at rounding of ||M|| ||sol||), forward error within kappa eps
+        nM = np.linalg.norm(M, 2)
+        assert np.linalg.norm(M @ sol - r) <= 1e-13 * (nM * np.linalg.norm(sol) + np.linalg.norm(r))
+        assert np.linalg.norm(sol - ref) <= 1e-14 * np.linalg.cond(M) * np.linalg.norm(ref)
+
+
+def test_svm_path_d_operator_agrees_with_dense_paths_and_brute_force():
+    """Path D through the operator (Woodbury) = path D on the materialised A = path K (Nystrom PCG),
+    and the tiny instance equals brute-force active-set enumeration."""
+    from oracle import svm
+    from synth.configs import svm_dense_A
+    inst = make_config(2, m=300, n=20, ell=10)
+    A = svm_dense_A(inst)
+    op = svm.SvmOperator(inst.extra["Xt"])
+    rw = ippmm.solve(op, inst.q, inst.b, inst.c, ippmm.Options(path="direct"))
+    rd = ippmm.solve(A, inst.q, inst.b, inst.c, ippmm.Options(path="direct"))
+    rk = ippmm.solve(A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=10))
+    assert rw.status == rd.status == rk.status == "optimal"
+    assert rw.outer == rd.outer
+    assert abs(rw.obj - rd.obj) <= 1e-10 * abs(rd.obj)
+    assert abs(rk.obj - rd.obj) <= _band(A, inst.q, inst.b, inst.c, rk) + _band(A, inst.q, inst.b, inst.c, rd)
+    tiny = make_config(2, m=4, n=2, ell=2)
+    ref = enumerate_active_sets(svm_dense_A(tiny), tiny.q, tiny.b, tiny.c)
+    rt = ippmm.solve(svm.SvmOperator(tiny.extra["Xt"]), tiny.q, tiny.b, tiny.c, ippmm.Options(path="direct"))
+    assert abs(rt.obj - ref["obj"]) <= 1e-6 * max(1.0, abs(ref["obj"]))
