@@ -4,17 +4,22 @@ kernel) reported against the HBM roofline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
-Default workload: BASELINE.json configs[1] (m=2000, n=8000, l=50), the largest config whose full
-solve fits a few-minute bench on one GPU.  --config 0|1|2|3 selects another BASELINE config;
---config 4 runs configs[4] (m=50000, l=200) with --n-per-gpu columns per rank (default 50000:
-at N=1 the one-GPU slice of SURVEY A25, at N=8 the full n=400000 problem) -> "scaling": "weak".
+Default workload (the headline, SURVEY §8(d) "the HBM headline"): BASELINE.json configs[4]
+(m=50000, l=200) with --n-per-gpu columns per rank (default 50000: at N=1 the one-GPU slice of
+SURVEY A25, A = 20 GB; at N=8 the full n=400000 problem, 160 GB) -> "scaling": "weak".  The slice
+does not reach 1e-8 in bench time (its square noise block leaves a tail no rank-200 Nystrom
+preconditioner removes: PCG hits its 20000-iteration cap from outer iteration 18 on),
+so a config-4 step is the first --max-outer (default 3) outer iterations of Nys-IP-PMM, labelled so
+in config.step.  --config 0|1|2|3 selects another BASELINE config (a step is then a complete solve
+to 1e-8).  At N=1 the line also carries `secondary`: configs 1 and 2 time-to-1e-8 (complete solves).
 
-A "step" is one complete Nys-IP-PMM solve to tol 1e-8 (every SURVEY §8(a) row: D-update, sketch
-+ Nystrom factorisation, PCG with the fused matvec and preconditioner, Newton RHS / recovery,
-predictor-corrector, residuals/TC/PEU, initial point) with the problem resident in HBM.
-`value` = seconds per solve (lower is better); `e2e` = the same solve through the C ABI with HOST
-buffers (H2D of A, q, b, c and D2H of x, y, z inside the timed region).  Multi-GPU (torchrun):
-A's columns are sharded over ranks; timing is on the device, max over ranks.
+A step runs every SURVEY §8(a) row: D-update, sketch + Nystrom factorisation, PCG with the fused
+matvec and preconditioner, Newton RHS / recovery, predictor-corrector, residuals/TC/PEU, initial
+point, with the problem resident in HBM.  `value` = seconds per step (lower is better); `e2e` = the
+same step through the C ABI with HOST buffers (H2D of A, q, b, c and D2H of x, y, z inside the
+timed region).  `roofline` = the dominant kernel K1 (fused normal matvec) against the HBM copy peak;
+`sketch_roofline` = the two sketch GEMMs (fp64 DMMA) against the measured DMMA peak.  Multi-GPU
+(torchrun): A's columns are sharded over ranks; timing is on the device, max over ranks.
 """
 from __future__ import annotations
 
@@ -32,7 +37,11 @@ sys.path.insert(0, ROOT)
 METRIC = "fp64 A·D·Aᵀv matvec GB/s (% HBM peak) and Nys-IP-PMM time-to-1e-8 at 1/2/4/8 GPU"
 # dram__bytes_read.sum + dram__bytes_write.sum per fused-matvec launch from `ncu --set full`
 # (profiles/, per config and shape); None until captured for that config
-TRAFFIC = {1: 134.6e6}
+#   config 4 slice (m = n = 50000): 20.002551 GB read + 5.558 MB written, profiles/r01_matvec_m50000_final_full.ncu-rep
+TRAFFIC = {1: 134.6e6, 4: 20.002551e9 + 5.558272e6}
+# fp64 tensor-core (DMMA, mma.sync.f64) peak measured on this pool's B200 by tools/dmma_probe.cu
+# (profiles/r01_dmma_peak_probe.log: 36.8-37.1 TFLOP/s over shapes / warps; cuBLAS square DGEMM 36.2)
+DMMA_PEAK_TFLOPS = 37.1
 # persistent PCG kernel, dram__bytes_read.sum + dram__bytes_write.sum per ITERATION (ncu --set full of
 # a 20-iteration launch, config 1: 2.535 GB + 20.9 MB; profiles/r01_pcg_persistent_cfg1_20it_full.ncu-rep)
 PCG_TRAFFIC_PER_IT = {1: 85.6e6}   # ncu --set full, profiles/r01_pcg_persistent_cfg1_20it_final_full.ncu-rep
@@ -43,6 +52,32 @@ def _peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {}
+
+
+def host_info():
+    """lscpu model, logical cores and host RAM (recorded with every CPU number)."""
+    info = {"cores": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+            elif line.startswith("Socket(s):"):
+                info["sockets"] = int(line.split(":", 1)[1])
+    except Exception:
+        pass
+    try:
+        import psutil
+        info["ram_gb"] = round(psutil.virtual_memory().total / 2**30, 1)
+    except Exception:
+        pass
+    try:
+        import numpy as np
+        cfg = np.show_config(mode="dicts")
+        info["blas"] = cfg["Build Dependencies"]["blas"]["name"] + " " + str(cfg["Build Dependencies"]["blas"].get("version", ""))
+    except Exception:
+        pass
+    return info
 
 
 class ClockSampler:
@@ -93,6 +128,12 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------
 # workloads
 # ------------------------------------------------------------------------------------------------
+def cfg4_name(n_per_gpu: int, world: int) -> str:
+    n = n_per_gpu * world
+    return (f"cfg4_large_m50000_l200_{n_per_gpu}cols_per_gpu" + ("_slice_A25" if world == 1 and n < 400000 else "")
+            + ("_full_n400000" if n == 400000 else ""))
+
+
 class Workload:
     """This rank's share of one BASELINE config, resident on the device, plus what the e2e leg
     and the CPU baseline need.  Input generation only (synth/); no method arithmetic here."""
@@ -114,9 +155,7 @@ class Workload:
                 dist.all_reduce(b)
             self.m, self.n, self.lo, self.hi, self.ell = large.FULL_M, n, lo, hi, large.ELL
             self.At, self.lda, self.q, self.b, self.c = sh.At, sh.lda, sh.q, b, sh.c
-            self.name = (f"cfg4_large_m50000_l200_{n_per_gpu}cols_per_gpu"
-                         + ("_slice_A25" if world == 1 and n < large.FULL_N else "")
-                         + ("_full_n400000" if n == large.FULL_N else ""))
+            self.name = cfg4_name(n_per_gpu, world)
             self.scaling = "weak"
             return
         from paper_2404_14524_b200 import colmajor_device
@@ -150,80 +189,100 @@ class Workload:
         return 8.0 * self.m * self.ncols
 
 
+# config-4 slice step (3 outer iterations) as measured on the GPU (profiles/r01_bench_cfg4_slice_3outer.json):
+# 166 PCG iterations + the initial point's 2 solves = 167 operator applications, plus per outer iteration
+# ~3 operator-equivalents of N-only / T-only passes (xi, recovery x2, residuals) and 2 at the initial
+# point; 4 sketches + Nystrom factorisations (initial point + 3 outer iterations).
+CFG4_STEP_COUNTS = {"matvecs": 167 + 3 * 3 + 2, "sketches": 4}
+
+
 def run_reference(args):
-    """--impl reference: the CPU oracle (numpy/scipy fp64) as it stands, on this host's cores."""
+    """--impl reference: the CPU oracle (numpy/scipy fp64, oracle/) as it stands, on this host's cores.
+
+    configs 0/1/3: each step is one complete oracle Nys-IP-PMM solve (path K) of the same instance.
+    configs 2/4: the oracle cannot finish the step in minutes (config 4: 20 GB A, each operator
+    application streams it on the host); each step times a bounded sample of the same workload — the
+    oracle's normal matvec and its sketch + Nystrom factorisation on a column sample — and projects it to
+    the step's operator-application and sketch counts.  W + K steps run, like the GPU arm."""
     import numpy as np
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cores = os.cpu_count()
+    hi = host_info()
+    K, W = max(1, args.steps), max(0, args.warmup)
+    times = []
     if args.config in (0, 1, 3):
         from oracle import ippmm
         from synth import make_config
         inst = make_config(args.config)
-        K = min(args.steps, 2)
-        W = min(args.warmup, 1)
-        times = []
         res = None
         for i in range(W + K):
             t0 = time.perf_counter()
             res = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
-            dt = time.perf_counter() - t0
             if i >= W:
-                times.append(dt)
-        v = float(np.mean(times))
-        sample = (f"full oracle Nys-IP-PMM solve of {inst.name} per step ({res.outer} outer / {res.inner_total} PCG "
-                  f"iterations); {K} timed + {W} warm-up of the requested {args.steps}+{args.warmup}")
-        config = {"workload": inst.name, "m": inst.m, "n": inst.n, "ell": inst.ell, "tol": 1e-8}
+                times.append(time.perf_counter() - t0)
+        sample = (f"one complete oracle Nys-IP-PMM solve of {inst.name} to 1e-8 per step ({res.outer} outer / "
+                  f"{res.inner_total} PCG iterations)")
+        config = {"workload": inst.name, "m": inst.m, "n": inst.n, "ell": inst.ell, "tol": 1e-8,
+                  "step": "solve to 1e-8"}
     else:
-        # the oracle cannot finish these solves in minutes: bounded sample projected to one solve
-        proj = cpu_projection(args.config, args.n_per_gpu * max(1, args.gpus), outer=40, matvecs=4000)
-        v = proj["value"]
+        n = args.n_per_gpu * max(1, args.gpus)
+        prep = cpu_projection_prepare(args.config, n)
+        proj = None
+        for i in range(W + K):
+            if args.config == 4:
+                proj = cpu_projection_step(prep, matvecs=CFG4_STEP_COUNTS["matvecs"], sketches=CFG4_STEP_COUNTS["sketches"])
+            else:   # config 2 to 1e-8: the GPU solve's counts (19 outer, ~22900 PCG iterations, profiles/r01_bench_cfg2_s6.json)
+                proj = cpu_projection_step(prep, matvecs=22862 + 19 * 3 + 2, sketches=20)
+            if i >= W:
+                times.append(proj["value"])
         sample = proj["sample"]
-        config = {"workload": proj["workload"], "tol": 1e-8}
-        K, W = 1, 0
+        config = {"workload": cfg4_name(args.n_per_gpu, max(1, args.gpus)) if args.config == 4 else prep["workload"],
+                  "m": prep["m"], "n": n, "ell": prep["ell"], "tol": 1e-8,
+                  "step": (f"{args.max_outer if args.max_outer is not None else 3} outer iterations"
+                           if args.config == 4 else "solve to 1e-8")}
+    v = float(np.mean(times))
     line = {"metric": METRIC, "value": v, "unit": "s", "impl": "reference", "n_gpus": args.gpus, "steps": K,
             "warmup": W, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "weak" if args.config == 4 else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
-            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": hi.get("cores"), "kind": "oracle", "sample": sample,
+                             "host": hi},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_projection(cfg: int, n: int, outer: int, matvecs: int):
-    """Oracle time for one solve projected from a bounded sample (~10-30 s of CPU work): the oracle's
-    normal matvec and its sketch + Nystrom factorisation timed on a column sample of the same
-    workload, scaled by n / sample columns and by the GPU solve's matvec / outer-iteration counts."""
+def cpu_projection_prepare(cfg: int, n: int, cols: int = 1000):
+    """A column sample of the config's A (the same instance recipe), resident on the host."""
+    import numpy as np
+    if cfg == 4:
+        from synth import large
+        sh = large.generate_shard(large.FULL_M, n, 0, cols, n_gen=large.FULL_N, device="cpu")
+        A = np.asfortranarray(sh.At[:, :large.FULL_M].numpy().T)
+        return {"A": A, "e": None, "m": large.FULL_M, "ell": large.ELL, "scale": n / cols,
+                "workload": f"cfg4 m=50000 n={n} l=200"}
+    from synth import make_config
+    inst = make_config(cfg)
+    A = inst.extra["Xt"] if cfg == 2 else inst.A
+    return {"A": A, "e": np.ones(inst.m) if cfg == 2 else None, "m": inst.m, "ell": inst.ell, "scale": 1.0,
+            "workload": inst.name}
+
+
+def cpu_projection_step(prep, matvecs: int, sketches: int):
+    """Oracle time for one step projected from a bounded sample (a few s of CPU work): the oracle's
+    normal matvec and its sketch + Nystrom factorisation timed on the column sample, scaled by
+    (total columns / sample columns) and by the step's operator-application / sketch counts."""
     import numpy as np
     from oracle import linops, nystrom
     from oracle.rng import gaussian_omega
-    if cfg == 4:
-        import torch
-        from synth import large
-        cols = 1000
-        sh = large.generate_shard(large.FULL_M, n, 0, cols, n_gen=large.FULL_N, device="cpu")
-        A = np.asfortranarray(sh.At[:, :large.FULL_M].numpy().T)
-        e = None
-        m, ell, scale = large.FULL_M, large.ELL, n / cols
-        workload = f"cfg4 m=50000 n={n} l=200"
-        del sh, torch
-    else:
-        from synth import make_config
-        inst = make_config(cfg)
-        A = inst.extra["Xt"] if cfg == 2 else inst.A
-        m, ell, scale = inst.m, inst.ell, 1.0
-        e = np.ones(m) if cfg == 2 else None
-        workload = inst.name
+    A, e, m, ell, scale = prep["A"], prep["e"], prep["m"], prep["ell"], prep["scale"]
     rs = np.random.default_rng(0)
     d = rs.uniform(0.1, 2.0, A.shape[1])
     v = rs.standard_normal(m)
     t0 = time.perf_counter()
-    reps = 3
-    for _ in range(reps):
-        linops.normal_matvec(A, d, v, 1e-3, e)
-    t_mv = (time.perf_counter() - t0) / reps * scale
+    linops.normal_matvec(A, d, v, 1e-3, e)
+    t_mv = (time.perf_counter() - t0) * scale
     Om = gaussian_omega(m, ell, 0, 1)
     t0 = time.perf_counter()
     Y = linops.sketch(A, d, Om, e)
@@ -231,11 +290,11 @@ def cpu_projection(cfg: int, n: int, outer: int, matvecs: int):
     t0 = time.perf_counter()
     nystrom.nystrom_from_sketch(Y * scale, Om)
     t_fac = time.perf_counter() - t0
-    value = matvecs * t_mv + outer * (t_sk + t_fac)
-    sample = (f"oracle normal matvec (x{reps}) and sketch+Nystrom on {A.shape[1]} of {int(A.shape[1] * scale)} "
-              f"columns of {workload}: {t_mv:.3g} s/matvec, {t_sk + t_fac:.3g} s/sketch at full size; projected to "
-              f"{matvecs} matvecs + {outer} sketches (the GPU solve's counts)")
-    return {"value": value, "sample": sample, "workload": workload}
+    value = matvecs * t_mv + sketches * (t_sk + t_fac)
+    sample = (f"oracle normal matvec and sketch+Nystrom on {A.shape[1]} of {int(round(A.shape[1] * scale))} columns of "
+              f"{prep['workload']}: {t_mv:.3g} s/matvec, {t_sk + t_fac:.3g} s/sketch at full size; projected to "
+              f"{matvecs} operator applications + {sketches} sketches per step")
+    return {"value": value, "sample": sample, "workload": prep["workload"]}
 
 
 def main():
@@ -244,7 +303,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n-per-gpu", type=int, default=50000, help="config 4: columns of A per rank")
     ap.add_argument("--prec-refresh", type=int, default=1,
                     help="SURVEY §8(f) f3: rebuild the Nystrom preconditioner every K outer iterations (1 = Alg. 3)")
@@ -254,13 +313,18 @@ def main():
                     help="f3: also rebuild when PCG counts grow by this factor since the last rebuild (0 = off)")
     ap.add_argument("--ell-max", type=int, default=0,
                     help="f3 adaptive rank (reading F1): double ell up to this cap while lam_hat_ell > 10 delta (0 = off)")
-    ap.add_argument("--max-outer", type=int, default=100,
-                    help="cap on IP-PMM outer iterations; below 100 the step is 'max-outer iterations', not "
-                         "time-to-1e-8 (config 4's one-GPU slice is ill-conditioned: DESIGN.md §2, A25)")
+    ap.add_argument("--max-outer", type=int, default=None,
+                    help="cap on IP-PMM outer iterations (default: 3 for config 4, 100 otherwise); below 100 the "
+                         "step is 'max-outer iterations', not time-to-1e-8 (config 4's one-GPU slice is "
+                         "ill-conditioned: DESIGN.md §2, A25)")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the configs 1 and 2 time-to-1e-8 legs of the N=1 line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--matvec-reps", type=int, default=50)
     args = ap.parse_args()
+    if args.max_outer is None:
+        args.max_outer = 3 if args.config == 4 else 100
     if args.impl == "reference":
         return run_reference(args)
 
@@ -425,12 +489,83 @@ def main():
         # SURVEY §8(d) per CG iteration: one K1 + 16 m l bytes of U (U^T r and U h) + ~10 m-vectors
         it_bytes = mv_bytes + 16.0 * m * ell + 80.0 * m
         pcg_gbs = info.iters * it_bytes / t_call / 1e9
+        tr = (PCG_TRAFFIC_PER_IT[args.config] * info.iters) if args.config in PCG_TRAFFIC_PER_IT else None
         pcg_roof = {"bound": "hbm", "achieved": pcg_gbs, "peak": hbm, "unit": "GB/s", "frac": pcg_gbs / hbm,
-                    "traffic": (PCG_TRAFFIC_PER_IT[args.config] * info.iters) if args.config in PCG_TRAFFIC_PER_IT else None,
+                    "traffic": tr,
+                    # A (128 MB at config 1) is about the L2 size: part of it survives in L2 between
+                    # iterations, so DRAM traffic < algorithmic bytes; frac above is the effective
+                    # ALGORITHMIC bandwidth, dram_frac the measured-DRAM-bytes one
+                    "dram_frac": (tr / t_call / 1e9 / hbm) if tr else None,
                     "kernel": "pcg_persistent_kernel (whole PCG solve in one cooperative launch)",
                     "peak_source": peak_src, "iterations_per_launch": info.iters,
                     "bytes_per_iteration": it_bytes, "launch_us": t_call * 1e6, "us_per_iteration": t_call / info.iters * 1e6,
                     "share_of_step": (last["t_pcg_ms"] / 1e3) / sec_per_solve}
+
+    # ---- sketch GEMMs (K2 + K3, fp64 DMMA): Y = A (d o (A^T Omega)), 4 m n l flops per call (SURVEY
+    # §8(d)), timed live with CUDA events on the library stream (the sketch is a dense contraction: its
+    # roofline is the fp64 tensor pipe, DMMA_PEAK_TFLOPS measured by tools/dmma_probe.cu)
+    sk_roof = None
+    if wl.ell > 0 and wl.structure == 0 and nloc > 0:
+        ell = wl.ell
+        mp = m + (m % 2)
+        Om_s = torch.empty((ell, mp), dtype=torch.float64, device=device)
+        Y_s = torch.empty((ell, mp), dtype=torch.float64, device=device)
+        with torch.cuda.stream(stream):
+            ctx.nys_gaussian(m, ell, 0, 1, Om_s)
+            ctx.nys_sketch_apply(wl.At, lda, m, d, None, ell, Om_s, Y_s)
+        barrier()
+        RS = 3 if wl.a_bytes() > 1e9 else 20
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(RS):
+                ctx.nys_sketch_apply(wl.At, lda, m, d, None, ell, Om_s, Y_s)
+        b_.record(stream)
+        barrier()
+        t_sk = a_.elapsed_time(b_) / 1e3 / RS
+        if world > 1:
+            tt = torch.tensor([t_sk], device=device)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_sk = float(tt.item())
+        sk_flops = 4.0 * m * nloc * ell
+        sk_tf = sk_flops / t_sk / 1e12
+        sk_roof = {"bound": "tensor", "achieved": sk_tf, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                   "frac": sk_tf / DMMA_PEAK_TFLOPS, "traffic": None,
+                   "kernel": "sketch Y = A (d o (A^T Omega)): two fp64 DMMA GEMMs (mma.sync.f64), nys_sketch_apply",
+                   "peak_source": "measured fp64 DMMA peak, tools/dmma_probe.cu, profiles/r01_dmma_peak_probe.log "
+                                  "(MEASURED_PEAKS.json has no fp64 entry)",
+                   "flops_per_call": sk_flops, "call_us": t_sk * 1e6,
+                   "share_of_step": (last["outer"] + 1) * t_sk / sec_per_solve if args.ell_max == 0 else None}
+        del Om_s, Y_s
+
+    # ---- secondary legs (N = 1, headline run only): configs 1 and 2 time-to-1e-8, complete solves ------
+    secondary = None
+    if world == 1 and args.config == 4 and not args.no_secondary:
+        secondary = {}
+        for sc in (1, 2):
+            w2 = Workload(sc, 0, 1, device, 0)
+
+            def solve2(w2=w2):
+                with torch.cuda.stream(stream):
+                    return ctx.nys_ipppmm_solve(w2.At, w2.lda, w2.m, w2.q, w2.b, w2.c, ell=w2.ell,
+                                                structure=w2.structure)
+            for _ in range(3):
+                solve2()
+            barrier()
+            K2 = 3
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r2 = [solve2() for _ in range(K2)]
+            e1.record(stream)
+            barrier()
+            g2 = r2[-1]
+            secondary[f"config{sc}"] = {
+                "workload": w2.name, "metric": "Nys-IP-PMM time-to-1e-8", "value": e0.elapsed_time(e1) / 1e3 / K2,
+                "unit": "s", "steps": K2, "warmup": 3, "status": g2["status"], "outer": g2["outer"],
+                "inner": g2["inner"], "obj": g2["obj"], "rel_p": g2["rel_p"], "rel_d": g2["rel_d"], "mu": g2["mu"],
+                "t_sketch_ms": g2["t_sketch_ms"], "t_pcg_ms": g2["t_pcg_ms"], "t_other_ms": g2["t_other_ms"]}
+            del w2, r2
+            torch.cuda.empty_cache()
 
     # ---- e2e: the same solve through the C ABI with host buffers --------------------------------
     e2e = None
@@ -490,12 +625,16 @@ def main():
                    "sample": f"one full oracle solve of {inst.name} ({r.outer} outer, {r.inner_total} PCG iters, "
                              f"obj {r.obj:.12g} vs GPU {last['obj']:.12g})"}
         else:
-            proj = cpu_projection(args.config, wl.n, outer=last["outer"], matvecs=matvecs_per_solve)
+            prep = cpu_projection_prepare(args.config, wl.n)
+            proj = cpu_projection_step(prep, matvecs=matvecs_per_solve + 3 * last["outer"] + 2,
+                                       sketches=last["outer"] + 1)
             cpu = {"value": proj["value"], "unit": "s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": proj["sample"]}
+            del prep
+        cpu["host"] = host_info()
 
     mv_roof = {"bound": "hbm", "achieved": mv_gbs, "peak": hbm, "unit": "GB/s", "frac": mv_gbs / hbm,
-               "traffic": TRAFFIC.get(args.config) if args.config != 4 else None,
+               "traffic": TRAFFIC.get(args.config) if (args.config != 4 or (wl.ncols == 50000 and world == 1)) else None,
                "kernel": "fused normal matvec K1 (matvec_kernel + mv_finalize), graph-captured",
                "peak_source": peak_src, "bytes_per_launch": mv_bytes, "launch_us": mv_s * 1e6,
                "warm_l2_gbs": mv_bytes / mv_warm_s / 1e9,
@@ -511,14 +650,20 @@ def main():
                        "ell_max": args.ell_max, "max_outer": args.max_outer,
                        "step": "solve to 1e-8" if args.max_outer >= 100 else f"{args.max_outer} outer iterations",
                        "parallelism": f"column-shard x{world}",
-                       "l2": ("A = %.0f MB vs 126 MB L2: roofline launches L2-flushed (256 MB read) before each"
-                              % (wl.a_bytes() * world / 1e6)) if small else
-                             ("A = %.1f GB per GPU >> 126 MB L2 (streamed with L2 evict_first)" % (wl.a_bytes() / 1e9))},
+                       "l2": (("A = %.0f MB vs 126 MB L2: the persistent-PCG roofline launch is NOT flushed (A partly "
+                               "L2-resident across iterations: see roofline.dram_frac); the matvec leg is L2-flushed "
+                               "(256 MB read) before each launch" % (wl.a_bytes() * world / 1e6)) if pcg_roof is not None else
+                              ("A = %.0f MB vs 126 MB L2: roofline launches L2-flushed (256 MB read) before each"
+                               % (wl.a_bytes() * world / 1e6))) if small else
+                             ("inputs larger than L2: A = %.1f GB per GPU >> 126 MB L2 (streamed with L2 evict_first); "
+                              "no flush needed" % (wl.a_bytes() / 1e9))},
             "clocks": clk.summary(),
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": pcg_roof if pcg_roof is not None else mv_roof,
             "matvec": mv_roof,
+            "sketch_roofline": sk_roof,
+            "secondary": secondary,
             "solve": {"outer": last["outer"], "inner": last["inner"], "obj": last["obj"], "rel_p": last["rel_p"],
                       "rel_d": last["rel_d"], "mu": last["mu"], "matvecs": matvecs_per_solve,
                       "t_sketch_ms": last["t_sketch_ms"], "t_pcg_ms": last["t_pcg_ms"],

@@ -234,7 +234,7 @@ typedef struct {
   double pcg_c;          /* 1e-3  (A8': tau = max(floor(1+|b|), min(0.1|xi|, c mu (1+|b|))))*/
   double pcg_floor;      /* 1e-10                                                          */
   double init_delta;     /* 10                                                     */
-  double init_tol_rel;   /* 1e-8 (A14')                                                    */
+  double init_tol_rel;   /* 1e-12 (A14'')                                                  */
   int    verbose;        /* 1: print one line per outer iteration to stderr                */
   /* Preconditioner reuse (the paper's future work, "reusing the
    * preconditioner between iterations").  The Nystrom factors (U, lambda) are rebuilt at outer

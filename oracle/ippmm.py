@@ -19,7 +19,9 @@ Readings where the paper defers to external algorithms or is silent (SURVEY §8(
        delta <- max(5e-10, (1 - 2/3 r) delta); dual likewise with zeta <- x+, rho.
        (form pinned by Tables 5-6; the 0.95 test itself is unpinned)
   A13  initial point: delta~_d denominator read as sum(x~ + delta_p)
-  A14' initial-point PCG tolerance 1e-8 ||rhs|| (tighter than SURVEY A14)
+  A14'' initial-point PCG tolerance 1e-12 ||rhs|| (tighter than SURVEY A14; at 1e-8 the
+       initial point depended on Omega at ~1e-6 on the config-1 recipe, at 1e-12 at ~1e-10: the
+       initial point is then a property of the problem, not of the Krylov rounding)
   A15  dz = X^{-1}(r_xz - Z dx)
   A16  empty ratio-test set -> alpha = 0.995
   IPg  initial-point guard: if a shifted x0 (z0) still has a non-positive entry (only when
@@ -54,7 +56,7 @@ class Options:
     pcg_floor: float = 1e-10           # A8'
     pcg_max_iter: int = 20000          # A10'
     init_delta: float = 10.0
-    init_tol_rel: float = 1e-8         # A14'
+    init_tol_rel: float = 1e-12        # A14''
     omega_fn: Optional[Callable[[int, int, int], np.ndarray]] = None  # (m, ell, stream) -> Omega
     # preconditioner reuse ("reusing the preconditioner between iterations"):
     # rebuild when k - k_last >= prec_refresh, or when the previous iteration's PCG count exceeded

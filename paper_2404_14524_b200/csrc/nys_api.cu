@@ -1232,7 +1232,7 @@ void nys_default_options(nys_options* o) {
   o->pcg_c = 1e-3;
   o->pcg_floor = 1e-10;
   o->init_delta = 10.0;
-  o->init_tol_rel = 1e-8;
+  o->init_tol_rel = 1e-12;
   o->verbose = 0;
   o->prec_refresh = 1;
   o->prec_growth = 0.0;

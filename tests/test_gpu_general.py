@@ -85,9 +85,10 @@ def test_general_ipppmm_matches_oracle(m, n, ff, fb, ell):
     assert abs(f - g["obj"]) <= 1e-10 * max(1.0, abs(f))
     dual = inst.b @ y - u[J] @ s[J] - 0.5 * x @ (inst.q * x)
     assert abs(dual - g["dual_obj"]) <= 1e-10 * max(1.0, abs(dual))
-    tol = max(1e-7 * max(1.0, abs(ref.obj)),
-              band_general(inst, x, y, z, s, g["obj"], g["dual_obj"]) +
+    band_ = (band_general(inst, x, y, z, s, g["obj"], g["dual_obj"]) +
               band_general(inst, ref.x, ref.y, ref.z, ref.s, ref.obj, ref.dual_obj))
+    tol = 1e-7 * max(1.0, abs(ref.obj))   # strict (north_star); the certified band is only reported
+    print(f"obj diff vs oracle: strict tol {tol:.3e}, certified bands {band_:.3e}")
     print(f"gpu obj {g['obj']!r} ref {ref.obj!r} outer {g['outer']}/{ref.outer} inner {g['inner']}/{ref.inner_total}")
     assert abs(g["obj"] - ref.obj) <= tol
     assert abs(g["outer"] - ref.outer) <= 2
@@ -186,9 +187,10 @@ def test_general_multirank_loopback():
     x = np.concatenate([g["x"] for g in res])
     z = np.concatenate([g["z"] for g in res])
     s = np.concatenate([g["s"] for g in res])
-    tol = max(1e-7 * max(1.0, abs(ref.obj)),
-              band_general(inst, x, res[0]["y"], z, s, res[0]["obj"], res[0]["dual_obj"]) +
+    band_ = (band_general(inst, x, res[0]["y"], z, s, res[0]["obj"], res[0]["dual_obj"]) +
               band_general(inst, ref.x, ref.y, ref.z, ref.s, ref.obj, ref.dual_obj))
+    tol = 1e-7 * max(1.0, abs(ref.obj))   # strict (north_star); the certified band is only reported
+    print(f"obj diff vs oracle: strict tol {tol:.3e}, certified bands {band_:.3e}")
     assert abs(res[0]["obj"] - ref.obj) <= tol
     assert abs(res[0]["outer"] - ref.outer) <= 2
 
@@ -233,7 +235,5 @@ def test_general_form_with_reuse_adaptive_and_chol(kw):
     rP = np.concatenate([inst.b - inst.A @ x, (u - x - w)[J]])
     assert np.linalg.norm(rP) / (1 + bn) <= 1.01e-8
     assert np.linalg.norm(inst.c + inst.q * x - inst.A.T @ y - z + s) / (1 + np.linalg.norm(inst.c)) <= 1.01e-8
-    tol = band_general(inst, x, y, z, s, g["obj"], g["dual_obj"]) + \
-        band_general(inst, _h(g0["x"]), _h(g0["y"]), _h(g0["z"]), _h(g0["s"]), g0["obj"], g0["dual_obj"])
-    assert abs(g["obj"] - g0["obj"]) <= max(tol, 1e-9 * abs(g0["obj"]))
+    assert abs(g["obj"] - g0["obj"]) <= 1e-7 * max(1.0, abs(g0["obj"]))
     ctx.close()

@@ -135,8 +135,9 @@ def test_multirank_ipppmm_matches_oracle(cfg, kw, world):
     # objective vs the oracle: within the two certified bands (A17')
     band = lambda p, d, xx, yy, zz: abs(p - d) + np.linalg.norm(xx) * np.linalg.norm(  # noqa: E731
         inst.c + inst.q * xx - inst.A.T @ yy - zz) + np.linalg.norm(yy) * np.linalg.norm(inst.b - inst.A @ xx)
-    tol = max(1e-7 * max(1.0, abs(ref.obj)),
-              band(res[0]["obj"], res[0]["dual_obj"], x, y, z) + band(ref.obj, ref.dual_obj, ref.x, ref.y, ref.z))
+    band_ = (band(res[0]["obj"], res[0]["dual_obj"], x, y, z) + band(ref.obj, ref.dual_obj, ref.x, ref.y, ref.z))
+    tol = 1e-7 * max(1.0, abs(ref.obj))   # strict (north_star); the certified band is only reported
+    print(f"obj diff vs oracle: strict tol {tol:.3e}, certified bands {band_:.3e}")
     assert abs(res[0]["obj"] - ref.obj) <= tol
     assert abs(res[0]["outer"] - ref.outer) <= 2
 
@@ -165,8 +166,9 @@ def test_multirank_chol_ipppmm_matches_oracle():
     y = res[0]["y"]
     band = lambda p, d, xx, yy, zz: abs(p - d) + np.linalg.norm(xx) * np.linalg.norm(  # noqa: E731
         inst.c + inst.q * xx - inst.A.T @ yy - zz) + np.linalg.norm(yy) * np.linalg.norm(inst.b - inst.A @ xx)
-    tol = max(1e-7 * max(1.0, abs(ref.obj)),
-              band(res[0]["obj"], res[0]["dual_obj"], x, y, z) + band(ref.obj, ref.dual_obj, ref.x, ref.y, ref.z))
+    band_ = (band(res[0]["obj"], res[0]["dual_obj"], x, y, z) + band(ref.obj, ref.dual_obj, ref.x, ref.y, ref.z))
+    tol = 1e-7 * max(1.0, abs(ref.obj))   # strict (north_star); the certified band is only reported
+    print(f"obj diff vs oracle: strict tol {tol:.3e}, certified bands {band_:.3e}")
     assert abs(res[0]["obj"] - ref.obj) <= tol
 
 
@@ -206,7 +208,7 @@ def test_multirank_rank_without_columns():
     assert res[2]["x"].size == 0
     x = np.concatenate([g["x"] for g in res])
     assert np.linalg.norm(b - A @ x) / (1 + np.linalg.norm(b)) <= 1.01e-8
-    assert abs(res[0]["obj"] - ref.obj) <= 1e-6 * max(1.0, abs(ref.obj))
+    assert abs(res[0]["obj"] - ref.obj) <= 1e-7 * max(1.0, abs(ref.obj))
 
 
 def test_multirank_failing_rank_releases_its_peers():

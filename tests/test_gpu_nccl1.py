@@ -75,7 +75,8 @@ def test_nccl_one_rank_ipppmm_matches_single_and_oracle(cfg, kw):
     x, y, z = (g[k].cpu().numpy() for k in ("x", "y", "z"))
     band = lambda p, d, xx, yy, zz: abs(p - d) + np.linalg.norm(xx) * np.linalg.norm(  # noqa: E731
         inst.c + inst.q * xx - inst.A.T @ yy - zz) + np.linalg.norm(yy) * np.linalg.norm(inst.b - inst.A @ xx)
-    tol = max(1e-7 * max(1.0, abs(ref.obj)),
-              band(g["obj"], g["dual_obj"], x, y, z) + band(ref.obj, ref.dual_obj, ref.x, ref.y, ref.z))
+    band_ = (band(g["obj"], g["dual_obj"], x, y, z) + band(ref.obj, ref.dual_obj, ref.x, ref.y, ref.z))
+    tol = 1e-7 * max(1.0, abs(ref.obj))   # strict (north_star); the certified band is only reported
+    print(f"obj diff vs oracle: strict tol {tol:.3e}, certified bands {band_:.3e}")
     assert abs(g["obj"] - ref.obj) <= tol
     assert abs(g["obj"] - g1["obj"]) <= tol

@@ -283,25 +283,43 @@ def _certified_band(A, q, b, c, x, y, z, p, d):
     return abs(p - d) + np.linalg.norm(x) * np.linalg.norm(rD) + np.linalg.norm(y) * np.linalg.norm(rP)
 
 
-def obj_agree(g, ref, rtol=1e-7, inst=None, A=None):
-    """|f_gpu - f_ref| <= 1e-7 max(1, |f_ref|), or within the two certified bands of f*.
+def obj_agree(g, ref, rtol=1e-7, inst=None, A=None, band_reason=None):
+    """|f_gpu - f_ref| <= 1e-7 max(1, |f_ref|)  (BASELINE north_star) — STRICT.
 
-    At the paper's tolerance (rel. infeasibility and mu <= 1e-8) the objective is only
-    determined up to the band of `_certified_band`; when the GPU and the oracle
-    trajectories separate by rounding late in the solve (unpreconditioned CG, ell = 0, is the
-    sensitive case), each objective lies within its own band of f*, so they may differ by at most
-    the sum of the two bands."""
+    Only a case that names its `band_reason` may fall back to the two certified bands of f*
+    (`_certified_band`): the GPU and oracle trajectories of unpreconditioned CG (ell = 0) on
+    kappa(N_delta) ~ 1e12 separate by rounding late in the solve, and each objective is then only
+    determined to its own band at the paper's tolerance.  Every use of the band is printed
+    with its reason and recorded in BAND_USES, so a drift up to the band never passes silently."""
     diff = abs(g["obj"] - ref.obj)
-    if inst is not None:
-        A = inst.A if A is None else A
-        host = lambda t: t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)  # noqa: E731
-        bands = (_certified_band(A, inst.q, inst.b, inst.c, host(g["x"]), host(g["y"]), host(g["z"]),
-                                 g["obj"], g["dual_obj"]) +
-                 _certified_band(A, inst.q, inst.b, inst.c, ref.x, ref.y, ref.z, ref.obj, ref.dual_obj))
-    else:
-        bands = abs(g["obj"] - g["dual_obj"]) + abs(ref.obj - ref.dual_obj)
-    print(f"obj gpu {g['obj']!r} ref {ref.obj!r} diff {diff:.3e} bands {bands:.3e}")
-    return diff <= rtol * max(1.0, abs(ref.obj)) or diff <= bands
+    strict = diff <= rtol * max(1.0, abs(ref.obj))
+    print(f"obj gpu {g['obj']!r} ref {ref.obj!r} diff {diff:.3e} rel {diff / max(1.0, abs(ref.obj)):.3e}")
+    if strict or band_reason is None:
+        return strict
+    A = inst.A if A is None else A
+    host = lambda t: t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)  # noqa: E731
+    bands = (_certified_band(A, inst.q, inst.b, inst.c, host(g["x"]), host(g["y"]), host(g["z"]),
+                             g["obj"], g["dual_obj"]) +
+             _certified_band(A, inst.q, inst.b, inst.c, ref.x, ref.y, ref.z, ref.obj, ref.dual_obj))
+    BAND_USES.append((getattr(inst, "name", "?"), diff, bands, band_reason))
+    print(f"  BAND USED ({band_reason}): diff {diff:.3e} <= bands {bands:.3e}?")
+    return diff <= bands
+
+
+BAND_USES = []
+
+
+def parity_tol(cfg, kw, ell=1):
+    """IP-PMM tolerance of an objective-parity case (both sides).  The paper's 1e-8 everywhere
+    except the REDUCED config-1 recipe with a preconditioner: there A = W H + 1e-3 G has kappa(A) ~ 1e5,
+    ||y*|| ~ 700, and at 1e-8 the objective is only determined to ~1.3e-7 relative (measured spread over
+    Omega seeds of the ORACLE alone, prec_refresh = 4), so a 1e-7 gate would test rounding luck; at
+    1e-10 the seed spread is <= 3e-8 and the 1e-7 gate is meaningful (reading A17\'\'\').
+    Full config 1 (spread 6e-10), configs 0 and 3 (< 1e-10) stay at 1e-8."""
+    return 1e-10 if (cfg == 1 and kw and ell > 0) else 1e-8
+
+
+ELL0_REASON = "ell = 0: unpreconditioned CG trajectories separate by rounding (kappa ~ 1e12)"
 
 
 IPM_CASES = [(0, {}, None), (1, dict(m=200, n=800, ell=20), None), (3, dict(m=16, n=2000, ell=16), None),
@@ -312,11 +330,12 @@ IPM_CASES = [(0, {}, None), (1, dict(m=200, n=800, ell=20), None), (3, dict(m=16
 def test_ipppmm_parity(ctx, cfg, kw, ell_override):
     inst = make_config(cfg, **kw)
     ell = inst.ell if ell_override is None else ell_override
-    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=ell))
-    g = _solve_gpu(ctx, inst, ell)
+    tol = parity_tol(cfg, kw, ell)
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=ell, tol=tol))
+    g = _solve_gpu(ctx, inst, ell, tol=tol)
     assert ref.status == "optimal" and g["status"] == 0
-    assert g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
-    assert obj_agree(g, ref, inst=inst)
+    assert g["rel_p"] <= tol and g["rel_d"] <= tol and g["mu"] <= tol
+    assert obj_agree(g, ref, inst=inst, band_reason=ELL0_REASON if ell == 0 else None)
     assert abs(g["outer"] - ref.outer) <= 2
     x = g["x"].cpu().numpy()
     assert np.min(x) > 0
@@ -444,11 +463,12 @@ def test_ipppmm_config3_full(ctx):
                                                    (0, {}, 10 ** 6, 1.5)])
 def test_ipppmm_prec_reuse_parity(ctx, cfg, kw, refresh, growth):
     inst = make_config(cfg, **kw)
+    tol = parity_tol(cfg, kw)
     ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c,
-                      ippmm.Options(path="krylov", ell=inst.ell, prec_refresh=refresh, prec_growth=growth))
-    g = _solve_gpu(ctx, inst, inst.ell, prec_refresh=refresh, prec_growth=growth)
+                      ippmm.Options(path="krylov", ell=inst.ell, prec_refresh=refresh, prec_growth=growth, tol=tol))
+    g = _solve_gpu(ctx, inst, inst.ell, prec_refresh=refresh, prec_growth=growth, tol=tol)
     assert ref.status == "optimal" and g["status"] == 0
-    assert g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    assert g["rel_p"] <= tol and g["rel_d"] <= tol and g["mu"] <= tol
     assert obj_agree(g, ref, inst=inst)
     assert abs(g["outer"] - ref.outer) <= 2
     built = [r["k"] for r in g["log"] if r["prec_built"]]
@@ -522,10 +542,11 @@ def test_partial_cholesky_ties_and_full_rank(ctx):
 def test_chol_ipppmm_parity(ctx, cfg, kw):
     """Chol-IP-PMM (precond = 1) against the oracle's precond='chol' path."""
     inst = make_config(cfg, **kw)
-    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell, precond="chol"))
-    g = _solve_gpu(ctx, inst, inst.ell, precond=1)
+    tol = parity_tol(cfg, kw)
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell, precond="chol", tol=tol))
+    g = _solve_gpu(ctx, inst, inst.ell, precond=1, tol=tol)
     assert ref.status == "optimal" and g["status"] == 0
-    assert g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    assert g["rel_p"] <= tol and g["rel_d"] <= tol and g["mu"] <= tol
     assert obj_agree(g, ref, inst=inst)
     assert abs(g["outer"] - ref.outer) <= 2
 
@@ -535,8 +556,10 @@ def test_adaptive_rank_matches_oracle(ctx):
     """The rank sequence (doubling while lam_hat_ell > tau delta_k, capped) and lam_hat_ell agree with
     the oracle; the solve reaches the oracle's optimum."""
     inst = make_config(1, m=200, n=800, ell=10)
-    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=10, ell_max=80, ell_tau=10.0))
-    g = _solve_gpu(ctx, inst, 10, ell_max=80, ell_tau=10.0)
+    tol = parity_tol(1, {"m": 200})
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=10, ell_max=80, ell_tau=10.0,
+                                                                    tol=tol))
+    g = _solve_gpu(ctx, inst, 10, ell_max=80, ell_tau=10.0, tol=tol)
     assert g["status"] == 0 and ref.status == "optimal"
     n_cmp = min(len(g["log"]), len(ref.log), 6)
     assert [r["ell"] for r in g["log"][:n_cmp]] == [r["ell"] for r in ref.log[:n_cmp]]
@@ -568,7 +591,7 @@ def test_ipppmm_degenerate_shapes(ctx, m, n):
     assert ref.status == "optimal" and g["status"] == 0
     x = g["x"].cpu().numpy()
     assert np.linalg.norm(b - A @ x) / (1 + np.linalg.norm(b)) <= 1.01e-8
-    assert abs(g["obj"] - ref.obj) <= 1e-6 * max(1.0, abs(ref.obj))
+    assert abs(g["obj"] - ref.obj) <= 1e-7 * max(1.0, abs(ref.obj))
 
 
 @pytest.mark.parametrize("lda_multiple", [2, 128, 512])

@@ -70,9 +70,10 @@ def test_structured_paper_formulations_match_oracle(kind, kw):
     rP = np.concatenate([inst.b - A @ x, (u - x - w)[J]])
     assert np.linalg.norm(rP) / (1 + bn) <= 1.01e-8                   # A u computed without the identity blocks
     assert np.linalg.norm(inst.c + inst.q * x - A.T @ y - z + s) / (1 + np.linalg.norm(inst.c)) <= 1.01e-8
-    tol = max(1e-7 * max(1.0, abs(ref.obj)),
-              band_general(A, inst, x, y, z, s, g["obj"], g["dual_obj"], w) +
+    band_ = (band_general(A, inst, x, y, z, s, g["obj"], g["dual_obj"], w) +
               band_general(A, inst, ref.x, ref.y, ref.z, ref.s, ref.obj, ref.dual_obj, ref.w))
+    tol = 1e-7 * max(1.0, abs(ref.obj))   # strict (north_star); the certified band is only reported
+    print(f"obj diff vs oracle: strict tol {tol:.3e}, certified bands {band_:.3e}")
     print(f"{inst.name}: gpu {g['obj']!r} ref {ref.obj!r} outer {g['outer']}/{ref.outer} "
           f"inner {g['inner']}/{ref.inner_total}")
     assert abs(g["obj"] - ref.obj) <= tol
@@ -114,9 +115,10 @@ def test_structured_chol_preconditioner():
     torch.cuda.synchronize()
     assert g["status"] == 0 and ref.status == "optimal"
     x, y, z, s = (_h(g[k]) for k in ("x", "y", "z", "s"))
-    tol = max(1e-7 * max(1.0, abs(ref.obj)),
-              band_general(A, inst, x, y, z, s, g["obj"], g["dual_obj"]) +
+    band_ = (band_general(A, inst, x, y, z, s, g["obj"], g["dual_obj"]) +
               band_general(A, inst, ref.x, ref.y, ref.z, ref.s, ref.obj, ref.dual_obj))
+    tol = 1e-7 * max(1.0, abs(ref.obj))   # strict (north_star); the certified band is only reported
+    print(f"obj diff vs oracle: strict tol {tol:.3e}, certified bands {band_:.3e}")
     assert abs(g["obj"] - ref.obj) <= tol
     ctx.close()
 
@@ -184,8 +186,9 @@ def test_structured_multirank_loopback():
     x[perm] = np.concatenate([g["x"] for g in res])
     z[perm] = np.concatenate([g["z"] for g in res])
     s[perm] = np.concatenate([g["s"] for g in res])
-    tol = max(1e-7 * max(1.0, abs(ref.obj)),
-              band_general(A, inst, x, res[0]["y"], z, s, res[0]["obj"], res[0]["dual_obj"]) +
+    band_ = (band_general(A, inst, x, res[0]["y"], z, s, res[0]["obj"], res[0]["dual_obj"]) +
               band_general(A, inst, ref.x, ref.y, ref.z, ref.s, ref.obj, ref.dual_obj))
+    tol = 1e-7 * max(1.0, abs(ref.obj))   # strict (north_star); the certified band is only reported
+    print(f"obj diff vs oracle: strict tol {tol:.3e}, certified bands {band_:.3e}")
     assert abs(res[0]["obj"] - ref.obj) <= tol
     assert abs(res[0]["outer"] - ref.outer) <= 2
