@@ -181,6 +181,26 @@ class LoopbackComm:
             self._buf = None
 
 
+def _ordered(fn):
+    """Stream semantics of the binding: the library works on the context's stream; a call made while
+    another torch stream is current first waits for that stream (inputs written there are visible) and
+    makes it wait for the library's work (outputs are visible to the caller's next torch op)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *a, **k):
+        cur = self.torch.cuda.current_stream(self.device)
+        other = cur.cuda_stream != self.stream.cuda_stream
+        if other:
+            self.stream.wait_stream(cur)
+        try:
+            return fn(self, *a, **k)
+        finally:
+            if other:
+                cur.wait_stream(self.stream)
+    return wrapper
+
+
 class Context:
     """One library context (device + stream [+ NCCL communicator])."""
 
@@ -193,8 +213,10 @@ class Context:
         self.torch = torch
         self.device = device
         torch.cuda.set_device(device)
-        if stream is None:
-            stream = torch.cuda.current_stream(device)
+        if stream is None or stream.cuda_stream == 0:
+            # the library needs a capturable (non-legacy) stream for its CUDA graphs: give it its own
+            # torch stream; every call below is ordered after / before the caller's current stream
+            stream = torch.cuda.Stream(device)
         self.stream = stream
         h = C.c_void_p()
         idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
@@ -226,16 +248,19 @@ class Context:
         return int(self.lib.nys_kernel_launches(self.h))
 
     # ---- the four hot-path calls (same names as the C ABI) -----------------------------
+    @_ordered
     def nys_normal_matvec(self, A, lda: int, m: int, d, e, delta: float, v, w):
         _check_cuda(A, d, e, v, w)
         n = A.shape[0]
         return self._rc(self.lib.nys_normal_matvec(self.h, m, n, _ptr(A), lda, _ptr(d), _ptr(e), float(delta),
                                                    _ptr(v), _ptr(w)))
 
+    @_ordered
     def nys_gaussian(self, m: int, ell: int, seed: int, stream: int, Omega):
         _check_cuda(Omega)
         return self._rc(self.lib.nys_gaussian(self.h, m, ell, seed, stream, _ptr(Omega)))
 
+    @_ordered
     def nys_sketch(self, A, lda: int, m: int, d, e, delta: float, ell: int, Omega, U, lam) -> SketchInfo:
         _check_cuda(A, d, e, Omega, U, lam)
         info = SketchInfo()
@@ -243,11 +268,13 @@ class Context:
                                      _ptr(Omega), _ptr(U), _ptr(lam), C.byref(info)))
         return info
 
+    @_ordered
     def nys_sketch_apply(self, A, lda: int, m: int, d, e, ell: int, Omega, Y):
         _check_cuda(A, d, e, Omega, Y)
         return self._rc(self.lib.nys_sketch_apply(self.h, m, A.shape[0], _ptr(A), lda, _ptr(d), _ptr(e), ell,
                                                   _ptr(Omega), _ptr(Y)))
 
+    @_ordered
     def nys_partial_cholesky(self, A, lda: int, m: int, d, e, delta: float, ell: int, piv=None, L=None, dS=None):
         _check_cuda(A, d, e, L, dS)
         if piv is not None and (not piv.is_cuda or piv.dtype.__repr__() != "torch.int64"):
@@ -255,10 +282,12 @@ class Context:
         return self._rc(self.lib.nys_partial_cholesky(self.h, m, A.shape[0], _ptr(A), lda, _ptr(d), _ptr(e),
                                                       float(delta), int(ell), _ptr(piv), _ptr(L), _ptr(dS)))
 
+    @_ordered
     def nys_chol_precond_apply(self, m: int, v, out):
         _check_cuda(v, out)
         return self._rc(self.lib.nys_chol_precond_apply(self.h, m, _ptr(v), _ptr(out)))
 
+    @_ordered
     def nys_pcg_solve(self, A, lda: int, m: int, d, e, delta: float, ell: int, U, lam, mu_prec: float, rhs, x,
                       tol_abs: float, max_iter: int) -> PcgInfo:
         _check_cuda(A, d, e, U, lam, rhs, x)
@@ -268,6 +297,7 @@ class Context:
                                         int(max_iter), C.byref(info)), allow=(0, 1))
         return info
 
+    @_ordered
     def nys_ipppmm_solve(self, A, lda: int, m: int, q, b, c, ell: int = 0, tol: float = 1e-8, seed: int = 0,
                          max_outer: int = 100, host: bool = False, max_records: int = 256, verbose: bool = False,
                          structure: int = 0, vtype=None, ub=None, unit_blocks=None, **opt_overrides):
@@ -301,6 +331,7 @@ class Context:
                 _check_cuda(ub)
             mk = lambda k: torch.zeros(k, dtype=torch.float64, device=A.device)  # noqa: E731
             x, y, z, w, s = mk(n), mk(m), mk(n), mk(n), mk(n)
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))   # outputs allocated there
         blocks = list(unit_blocks or [])
         ub_arr = (UnitBlock * max(1, len(blocks)))(*[UnitBlock(int(r), int(k), float(sc)) for r, k, sc in blocks])
         qp = QP(m, n, _ptr(A), lda, _ptr(q), _ptr(b), _ptr(c), 1 if host else 0, structure, nd if structure else 0,

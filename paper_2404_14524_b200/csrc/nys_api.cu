@@ -15,6 +15,8 @@
 #include <cstring>
 #include <stdexcept>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "k_vec.cuh"
 #include "nccl.h"
 
@@ -24,27 +26,70 @@ namespace {
 struct NysException {
   int code;
 };
+// NVTX range per phase of the hot path (visible in nsys / ncu --nvtx; header-only NVTX v3, a no-op
+// without an attached tool)
+struct NvtxRange {
+  explicit NvtxRange(const char* s) { nvtxRangePushA(s); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 }  // namespace
+
+static constexpr size_t kGuardBytes = 64 * 1024;
+static constexpr unsigned char kGuardByte = 0xA5;
 
 void* nys_ctx::ws(const char* name, size_t bytes) {
   if (bytes == 0) bytes = 8;
   auto it = bufs.find(name);
   if (it != bufs.end() && it->second.second >= bytes) return it->second.first;
   if (it != bufs.end()) {
+    if (debug_guard) cudaStreamSynchronize(stream);   // the guard check reads every live buffer
     cudaFree(it->second.first);
     bufs.erase(it);
   }
   void* p = nullptr;
   size_t alloc = bytes < 256 ? 256 : bytes;
-  cudaError_t e = cudaMalloc(&p, alloc);
+  alloc = (alloc + 255) & ~size_t(255);
+  cudaError_t e = cudaMalloc(&p, alloc + (debug_guard ? kGuardBytes : 0));
   if (e != cudaSuccess) {
     last_error = std::string("workspace '") + name + "': " + cudaGetErrorString(e);
     cudaGetLastError();
     throw NysException{NYS_ENOMEM};
   }
+  if (debug_guard) {                                   // NaN poison + canary (stream-ordered)
+    cudaMemsetAsync(p, 0xFF, alloc, stream);
+    cudaMemsetAsync((char*)p + alloc, kGuardByte, kGuardBytes, stream);
+  }
   bufs[name] = {p, alloc};
   ++ws_epoch;
   return p;
+}
+
+namespace {
+__global__ void guard_check_kernel(const unsigned char* g, size_t n, unsigned char expect, unsigned int* flag) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    if (g[i] != expect) { atomicOr(flag, 1u); return; }
+}
+}  // namespace
+
+int nys_ctx::check_guards() {
+  if (!debug_guard) return NYS_OK;
+  if (!guard_flag && cudaMalloc(&guard_flag, sizeof(unsigned int)) != cudaSuccess) return NYS_ENOMEM;
+  for (auto& kv : bufs) {
+    unsigned int h = 0;
+    cudaMemsetAsync(guard_flag, 0, sizeof(unsigned int), stream);
+    guard_check_kernel<<<64, 256, 0, stream>>>((const unsigned char*)kv.second.first + kv.second.second, kGuardBytes,
+                                                kGuardByte, guard_flag);
+    cudaMemcpyAsync(&h, guard_flag, sizeof(unsigned int), cudaMemcpyDeviceToHost, stream);
+    if (cudaStreamSynchronize(stream) != cudaSuccess) { set_error("guard check: CUDA error"); return NYS_ECUDA; }
+    if (h) {
+      set_error("NYS_DEBUG_GUARD: out-of-bounds write past workspace '" + kv.first + "' (" +
+                std::to_string(kv.second.second) + " bytes)");
+      return NYS_ECUDA;
+    }
+  }
+  return NYS_OK;
 }
 
 int nys_ctx::check_launch(const char* what) {
@@ -123,6 +168,10 @@ struct LoopComm {
 };
 // a failed collective call on one loopback rank must not leave its peers waiting forever
 int loop_abort_on_error(nys_ctx* ctx, int rc) {
+  if (ctx && ctx->debug_guard && (rc == NYS_OK || rc == NYS_NOTCONV || rc == NYS_EMAXITER)) {
+    const int g = ctx->check_guards();
+    if (g != NYS_OK) rc = g;
+  }
   if (rc != NYS_OK && rc != NYS_EMAXITER && rc != NYS_NOTCONV && ctx && ctx->loop_comm)
     static_cast<LoopComm*>(ctx->loop_comm)->abort();
   return rc;
@@ -359,6 +408,7 @@ int sketch_Y(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, c
 // Alg. 1: sketch, then lines 3-8
 int sketch_impl(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
                 int ell, const double* Om, double* U, double* lam, nys_sketch_info* info) {
+  NvtxRange nv("nystrom_sketch_and_factor");
   double* Y = ctx->wsd("sk_Y", (size_t)even(m) * ell);
   NYS_TRY(sketch_Y(ctx, m, n, A, lda, d, e, ell, Om, Y));
   return nystrom_factor(ctx, m, ell, Y, Om, even(m), U, lam, info);
@@ -368,6 +418,7 @@ int sketch_impl(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda
 // Partial Cholesky preconditioner of rank ell for N_delta = N + delta I (f2)
 // ------------------------------------------------------------------------------------------
 int chol_build(nys_ctx* ctx, const NormalOp& op, int ell, CholFactors& F) {
+  NvtxRange nv("partial_cholesky_build");
   const int64_t m = op.m, mp = even(m);
   F.m = m;
   F.ell = ell;
@@ -453,6 +504,7 @@ int pcg_iteration(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, in
 
 int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t ldu, const double* s,
              const double* rhs, double* x, int max_iter, PcgResult& res, const CholFactors* chol = nullptr) {
+  NvtxRange nv("pcg_solve");
   const int64_t m = op.m;
   const int64_t mp = even(m);
   if (chol) ell = 0;  // no Nystrom factors on the partial-Cholesky path
@@ -735,6 +787,7 @@ struct AOps {
 };
 
 int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solution* sol, nys_report* rep) {
+  NvtxRange nv_solve("nys_ipppmm_solve");
   auto t_start = std::chrono::steady_clock::now();
   const int64_t m = qp_in->m, n = qp_in->n;
   const int64_t mp = even(m), np_ = even(n);
@@ -881,6 +934,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   int total_inner = 0;
 
   // ---- initial point (App. B.2; u = 0) --------------------------------------
+  nvtxRangePushA("initial_point");
   NYS_CUDA_TRY(ctx, cudaMemsetAsync(ones, 0, nn * sizeof(double), ctx->stream));
   NYS_TRY(launch_shift(ctx, n, ones, 1.0));
   NormalOp op0;
@@ -963,6 +1017,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(launch_shift(ctx, n, z, ddt));
   }
   }
+  nvtxRangePop();
   // ---- PMM parameters --------------------------------------------------------------
   NYS_CUDA_TRY(ctx, cudaMemcpyAsync(lam, y, m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   if (n > 0) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(zeta, x, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -970,6 +1025,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
 
   auto residuals = [&]() -> int {
     // r_P = b - A x ; r_D = c + Q x - A^T y - z ; ||r_P||^2, ||r_D||^2, x^T z
+    NvtxRange nvr("residuals");
     NYS_TRY(AO.Ax(x, ax, nullptr));
     NYS_TRY(launch_axpby(ctx, m, 1.0, b, -1.0, ax, rP));
     NYS_TRY(AO.At_rd(y, c, q, x, z, rD));
@@ -1003,6 +1059,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     if (rel_p <= opt->tol && rel_d <= opt->tol && mu <= opt->tol) { status = NYS_OK; break; }   // A11
     if (k == opt->max_outer) break;
     if (!std::isfinite(mu) || !std::isfinite(nrP) || !std::isfinite(nrD)) { status = NYS_EBREAKDOWN; break; }
+    NvtxRange nv_outer("outer_iteration");
     nys_iter_record rec{};
     rec.k = k; rec.mu = mu; rec.rel_p = rel_p; rec.rel_d = rel_d; rec.rho = rho; rec.delta = delta;
     auto t_it = std::chrono::steady_clock::now();
@@ -1038,6 +1095,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[1], ctx->stream));
     NYS_TRY(launch_set_slots(ctx, S_MUCUR, mu));
     // ---- predictor ----
+    nvtxRangePushA("predictor");
     if (gen) NYS_TRY(launch_gen_pred_rhs(ctx, n, vt, ub, x, z, w, sv, zeta, rD, rho, d, rd, rxz, ru, rws, xiau, t));
     else NYS_TRY(launch_pred_rhs_n(ctx, n, x, z, zeta, rD, rho, d, rd, rxz, xiau, t));
     NYS_TRY(launch_pred_rhs_m(ctx, m, b, ax, y, lam, delta, rp));
@@ -1066,7 +1124,9 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
       else NYS_TRY(allreduce_slots(ctx, S_TMP7, 1));
       NYS_TRY(launch_muaff_post(ctx, n_total, gen ? 1 : 0));
     }
+    nvtxRangePop();
     // ---- corrector ----
+    nvtxRangePushA("corrector");
     if (gen) NYS_TRY(launch_gen_corr_rhs(ctx, n, vt, x, w, dxp, dzp, dwp, dsp, d, rxz, ru, rws, xiau, t));
     else NYS_TRY(launch_corr_rhs(ctx, n, x, dxp, dzp, d, rxz, xiau, t));
     NYS_TRY(AO.Ax(t, xi, nullptr));
@@ -1080,6 +1140,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     last_its = (int64_t)rec.pcg_pred + rec.pcg_corr;
     if (base_its < 0) base_its = last_its;
     NYS_TRY(AO.At_dx(dyc, nullptr, xiau, rxz, z, x, d, dxc, dzc));
+    nvtxRangePop();
     // ---- combine, stepsizes, update ----
     if (gen) {
       NYS_TRY(launch_gen_recover(ctx, n, vt, x, z, w, sv, dxc, rxz, ru, rws, dzc, dwc, dsc));
@@ -1250,6 +1311,7 @@ int nys_create(nys_ctx** out, int device, void* cuda_stream, const void* nccl_un
   ctx->device = device;
   ctx->rank = rank;
   ctx->world = world;
+  ctx->debug_guard = getenv("NYS_DEBUG_GUARD") != nullptr;
   auto fail = [&](int code) {
     *out = ctx;  // keep for nys_last_error; caller destroys
     return code;
@@ -1336,6 +1398,7 @@ int nys_destroy(nys_ctx* ctx) {
   for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
   if (ctx->sc) cudaFree(ctx->sc);
   if (ctx->counters) cudaFree(ctx->counters);
+  if (ctx->guard_flag) cudaFree(ctx->guard_flag);
   if (ctx->h_sc) cudaFreeHost(ctx->h_sc);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);

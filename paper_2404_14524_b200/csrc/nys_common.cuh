@@ -68,6 +68,13 @@ struct nys_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t ws_epoch = 0;           // bumped whenever a workspace buffer is (re)allocated
   std::map<std::string, std::pair<int64_t, std::pair<cudaGraphExec_t, cudaGraph_t>>> graphs;  // PCG loop graphs
+  // NYS_DEBUG_GUARD=1 (memcheck substitute; compute-sanitizer is closed on the GPU pool): every
+  // workspace buffer is poisoned with NaN bytes when (re)allocated and followed by a 64 KiB canary,
+  // verified after every ABI call (check_guards) -> an out-of-bounds write fails the call loudly,
+  // a read of never-written workspace turns results into NaN (caught by the parity checks)
+  bool debug_guard = false;
+  unsigned int* guard_flag = nullptr;
+  int check_guards();
 
   void set_error(const std::string& s) { last_error = s; }
   // named workspace, grown monotonically; contents are NOT preserved on growth

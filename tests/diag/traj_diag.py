@@ -1,8 +1,9 @@
 """Diagnostic: GPU vs oracle per-outer-iteration logs side by side for one IP-PMM case (prints only)."""
+import os
 import sys
 import numpy as np
 import torch
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2404_14524_b200 import Context, colmajor_device
 from oracle import ippmm
 from synth import make_config

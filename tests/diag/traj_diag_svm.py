@@ -1,8 +1,9 @@
 """Diagnostic: config-2 recipe (structure 1) GPU vs oracle trajectories over the first K outer iterations."""
+import os
 import sys
 import numpy as np
 import torch
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2404_14524_b200 import Context, colmajor_device
 from oracle import ippmm, svm
 from synth import make_config

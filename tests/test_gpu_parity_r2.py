@@ -187,7 +187,7 @@ def test_config2_recipe_capped_solve_m20000_matches_oracle(ctx):
     path on the same operator (oracle.svm.SvmOperator), compared per iteration and elementwise.
     (At N = 10000, d = 200, ell = 20 the corrector of iteration 2 stops at 83 vs 84 PCG iterations: its
     residual crosses tau_k within rounding — the trajectories agree to 1e-15 in mu up to that decision,
-    tools/traj_diag_svm.py, profiles/r02_traj_diag_svm.log.)"""
+    tests/diag/traj_diag_svm.py, profiles/r02_traj_diag_svm.log.)"""
     from paper_2404_14524_b200 import colmajor_device
     from oracle import svm
     inst = make_config(2, m=20000, n=100, ell=50)
