@@ -13,7 +13,7 @@
  *   - A is the caller's dense fp64 matrix, COLUMN-MAJOR, m rows x n columns, leading
  *     dimension lda >= m, lda EVEN, base pointer 16-byte aligned (the single-pass matvec
  *     streams column segments with 1-D bulk-async copies that need 16-byte alignment).
- *     m <= 139264 (= 16 x 8704: a column is split over at most a 16-CTA cluster); larger m
+ *     m <= 138240 (= 16 x 8640: a column is split over at most a 16-CTA cluster); larger m
  *     returns NYS_EINVAL.
  *     With world > 1 each rank passes ITS column shard (m x n_local) and the m-space
  *     results are summed over ranks (A = [A_0, A_1, ...]).

@@ -201,9 +201,13 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
 
   const int S = P.stages;
   const int64_t rs = P.rs;
+  // stage column stride: the cluster path pads each column slot to GT * RPT rows (>= rs), the rows a
+  // thread block covers, so the inner loops read every slot row without bounds checks (the pad rows
+  // are zero-filled once below and never written by the bulk copies)
+  const int64_t ss = CLU ? (int64_t)GT * RPT : rs;
   const int cl = CLU ? P.cl : 1;
   double* stage = reinterpret_cast<double*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage + (size_t)S * BN * rs);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage + (size_t)S * BN * ss);
   uint64_t* empty = full + S;
   uint64_t* dotbar = empty + S;                       // DB barriers (CLU)
   double* red = reinterpret_cast<double*>(dotbar + DB);
@@ -230,6 +234,15 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
     if (CLU)
       for (int s = 0; s < DB; ++s) mbar_init(&dotbar[s], 1);  // own arrive.expect_tx; peers complete_tx
     fence_mbar_init();
+  }
+  if (CLU) {
+    // zero the pad rows [copy rows, GT * RPT) of every stage slot once: disjoint from what the bulk
+    // copies write, so no proxy fence is needed (the cluster barrier below orders them before use)
+    const int64_t crow = (rows_valid + 1) & ~int64_t(1);
+    const int64_t npad = ss - crow;
+    if (npad > 0)
+      for (int64_t e = tid; e < (int64_t)S * BN * npad; e += T + 32)
+        stage[(e / npad) * ss + crow + (e % npad)] = 0.0;
   }
   if (CLU) cluster_sync_all(); else __syncthreads();
 
@@ -264,7 +277,7 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
         } else {
           mbar_arrive_expect_tx(&full[s], (uint32_t)ncols * copy_bytes);
           for (int c = 0; c < ncols; ++c)
-            bulk_g2s(stage + ((size_t)s * BN + c) * rs, P.A + (col0 + c) * P.lda + r0, copy_bytes, &full[s], pol);
+            bulk_g2s(stage + ((size_t)s * BN + c) * ss, P.A + (col0 + c) * P.lda + r0, copy_bytes, &full[s], pol);
         }
       }
     }
@@ -309,6 +322,11 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
       // Ring safety: a peer publishes panel j+DB only after consuming j+DB-2, which needs our
       // publish of j+DB-2, issued after our consume of j+DB-3 >= j for DB >= 3 (DB = 4 here).
       static_assert(WPG <= 32, "one lane per warp partial");
+      // an odd slice length copies one row past the slice (bulk sizes are 16-byte multiples): the
+      // thread owning that row zeroes it in every stage it reads (then fences the generic write
+      // against the next bulk copy into the stage), so garbage there can never reach a dot
+      const bool odd_owner = (rows_valid & 1) && (rows_valid % GT) == lig && rows_valid < ss;
+      const int ssi = (int)ss;
       double dprev[CPG];
       int64_t cprev = 0;
 #pragma unroll
@@ -320,19 +338,21 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
         const int64_t col0 = (int64_t)(cid + it * ncl) * BN;
         if (it < niter) {
           mbar_wait(&full[s], ph);
-          const double* sb = stage + (size_t)s * BN * rs;
+          double* sb = stage + (size_t)s * BN * ss;
+          if (odd_owner) {
+#pragma unroll
+            for (int c = 0; c < CPG; ++c) sb[c * ss + rows_valid] = 0.0;
+          }
 #pragma unroll
           for (int c = 0; c < CPG; ++c) dcur[c] = (MODE == MV_FUSED && col0 + c < P.n) ? __ldg(P.d + col0 + c) : 0.0;
           double pd[CPG];
 #pragma unroll
           for (int c = 0; c < CPG; ++c) {
-            const bool cv = (col0 + c) < P.n;
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            if (col0 + c < P.n) {      // warp-uniform; rows past the slice read the zero pad / vreg = 0
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-              const int rl = lig + GT * i;
-              const double a = (cv && rl < (int)rows_valid) ? sb[c * (int)rs + rl] : 0.0;
-              acc[i & 3] = fma(a, vreg[VS ? 0 : i], acc[i & 3]);
+              for (int i = 0; i < RPT; ++i)
+                acc[i & 3] = fma(sb[c * ssi + lig + GT * i], vreg[VS ? 0 : i], acc[i & 3]);
             }
             pd[c] = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
           }
@@ -365,16 +385,13 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
           double pd[CPG];
 #pragma unroll
           for (int c = 0; c < CPG; ++c) {
-            // pairwise tree in rank order (identical on every CTA of the cluster)
-            const double* sl = &slots[(size_t)db * cl * CPG + c];
-            double part[16];
+            // the cl (<= 16) CTA partials, lane r holding rank r's, summed by a 16-wide xor butterfly:
+            // fp addition is commutative, so every lane of every CTA of the cluster gets the same bits
+            // (the same t_j), at 1 load + 4 shuffle-adds per warp instead of cl loads + adds per thread
+            double x = ((lane & 15) < cl) ? slots[((size_t)db * cl + (lane & 15)) * CPG + c] : 0.0;
 #pragma unroll
-            for (int r = 0; r < 16; ++r) part[r] = (r < cl) ? sl[r * CPG] : 0.0;
-#pragma unroll
-            for (int w = 8; w > 0; w >>= 1)
-#pragma unroll
-              for (int r = 0; r < w; ++r) part[r] += part[r + w];
-            pd[c] = part[0];
+            for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            pd[c] = x;
           }
           if (MODE == MV_FUSED) {
             double t[CPG];
@@ -384,17 +401,13 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
 #pragma unroll
               for (int c = 0; c < CPG; ++c) pwacc = fma(t[c], pd[c], pwacc);  // d_j (a_j^T v)^2
             }
-            const double* sb = stage + (size_t)sp * BN * rs;
+            const double* sb = stage + (size_t)sp * BN * ss;
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-              const int rl = lig + GT * i;
-              double acc = wacc[i];
+            for (int c = 0; c < CPG; ++c) {
+              if (cprev + c < P.n) {   // warp-uniform
 #pragma unroll
-              for (int c = 0; c < CPG; ++c) {
-                const double a = (cprev + c < P.n && rl < (int)rows_valid) ? sb[c * (int)rs + rl] : 0.0;
-                acc = fma(a, t[c], acc);
+                for (int i = 0; i < RPT; ++i) wacc[i] = fma(sb[c * ssi + lig + GT * i], t[c], wacc[i]);
               }
-              wacc[i] = acc;
             }
           } else {  // MV_TONLY: raw dot to global; epilogue after the loop
             if (crank == 0) {
@@ -403,6 +416,7 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
                 if (lig == c && cprev + c < P.n) P.tbuf[cprev + c] = pd[c];
             }
           }
+          if (odd_owner) fence_proxy_async_shared();
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[sp]);
         }
@@ -423,14 +437,14 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
       const int64_t col0 = (int64_t)(cid + it * ncl) * BN + (int64_t)g * CPG;
       mbar_wait(&full[s], par);
       double a[CPG][RPT];
-      const double* sb = stage + ((size_t)s * BN + (size_t)g * CPG) * rs;
+      const double* sb = stage + ((size_t)s * BN + (size_t)g * CPG) * ss;
 #pragma unroll
       for (int c = 0; c < CPG; ++c) {
         const bool cv = (col0 + c) < P.n;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
           const int64_t rl = lig + (int64_t)GT * i;
-          a[c][i] = (cv && rl < rows_valid) ? sb[(size_t)c * rs + rl] : 0.0;
+          a[c][i] = (cv && rl < rows_valid) ? sb[(size_t)c * ss + rl] : 0.0;
         }
       }
       __syncwarp();
@@ -626,10 +640,13 @@ struct MvCfg {
 };
 
 static MvCfg pick_cfg(int64_t rs, bool clu) {
-  if (clu) {  // cluster path: rows split over the cluster, one group of 512 threads
-    if (rs <= 4096) return {512, 512, 8, 2};
-    if (rs <= 6656) return {512, 512, 13, 1};
-    return {512, 512, 17, 1};
+  if (clu) {  // cluster path: rows split over the cluster, one group of 480 consumer threads: with the
+              // producer warp 16 warps, 4 per SM sub-partition -> 128 registers per thread (measured on
+              // B200, m = 50000: 512 threads / 96 registers spill, 256 threads / 34 rows are DFMA-latency
+              // bound at 4.9 TB/s; 480 / 18 rows: 6.8 TB/s at full clock)
+    if (rs <= 3840) return {480, 480, 8, 2};
+    if (rs <= 6720) return {480, 480, 14, 1};
+    return {480, 480, 18, 1};
   }
   if (rs <= 64) return {256, 32, 2, 4};
   if (rs <= 128) return {256, 32, 4, 2};
@@ -645,9 +662,9 @@ typedef void (*MvKernel)(const MatvecParams);
 template <int MODE>
 static MvKernel kernel_for(const MvCfg& c, bool clu) {
   if (clu) {
-    if (c.RPT == 8 && c.CPG == 2) return matvec_kernel<512, 512, 8, 2, MODE, false, true>;
-    if (c.RPT == 13) return matvec_kernel<512, 512, 13, 1, MODE, false, true>;
-    return matvec_kernel<512, 512, 17, 1, MODE, false, true>;
+    if (c.RPT == 8 && c.CPG == 2) return matvec_kernel<480, 480, 8, 2, MODE, false, true>;
+    if (c.RPT == 14) return matvec_kernel<480, 480, 14, 1, MODE, false, true>;
+    return matvec_kernel<480, 480, 18, 1, MODE, false, true>;
   }
   if (c.T == 256 && c.GT == 32 && c.RPT == 2 && c.CPG == 4) return matvec_kernel<256, 32, 2, 4, MODE, false, false>;
   if (c.T == 256 && c.GT == 32 && c.RPT == 4 && c.CPG == 2) return matvec_kernel<256, 32, 4, 2, MODE, false, false>;
@@ -679,7 +696,8 @@ static bool cfg_vs(const MvCfg& c, bool clu) { return !clu && c.RPT >= 16; }
 static size_t mv_smem_bytes(const MvCfg& c, int64_t rs, int stages, int cl, bool clu) {
   const int NG = c.T / c.GT, WPG = c.GT / 32, BN = NG * c.CPG;
   constexpr int DB = 4;
-  size_t b = (size_t)stages * BN * rs * 8;
+  const int64_t ss = clu ? (int64_t)c.GT * c.RPT : rs;   // stage column stride (kernel: `ss`)
+  size_t b = (size_t)stages * BN * ss * 8;
   b += (size_t)2 * stages * 8 + (size_t)DB * 8;
   b += (size_t)2 * NG * WPG * c.CPG * 8;
   b += (size_t)DB * cl * c.CPG * 8;
@@ -720,7 +738,7 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, 
       if (sscanf(ov, "%d,%d,%d,%d", &o.T, &o.GT, &o.RPT, &o.CPG) == 4 && (int64_t)o.GT * o.RPT >= rs_) c_ = o;
     }
     const int BN_ = (c_.T / c_.GT) * c_.CPG;
-    const size_t stage_bytes = (size_t)BN_ * rs_ * 8;
+    const size_t stage_bytes = (size_t)BN_ * (clu_ ? (int64_t)c_.GT * c_.RPT : rs_) * 8;
     size_t budget = clu_ ? 212 * 1024 : (rs_ <= 1024) ? 96 * 1024 : 200 * 1024;
     if (const char* sb = getenv("NYS_MV_SMEM_KB")) budget = (size_t)atoi(sb) * 1024;
     if (cfg_vs(c_, clu_)) budget -= (size_t)rs_ * 8;
@@ -752,7 +770,7 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, 
     return ncl_ * cl_;
   };
   // m <= 8192: whole columns per CTA.  Larger m: split the rows over a cluster of cl CTAs with
-  // <= 8704 rows each (17 rows per thread: the register budget of the pipelined cluster path).
+  // <= 8640 rows each (18 rows per thread: the register budget of the pipelined cluster path).
   // Cluster sizes need not be powers of two; GPCs do not hold equal numbers of clusters of every
   // size, so pick the SMALLEST cl (largest row slice: per-panel overheads amortised over more
   // bytes) whose resident CTA count is within 5% of the best over all admissible cl
@@ -760,9 +778,9 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, 
   int cl = 1;
   Geo geo;
   if (m > 8192) {
-    int clmin = (int)((m + 8703) / 8704);
+    int clmin = (int)((m + 8639) / 8640);
     if (clmin < 2) clmin = 2;
-    if (clmin > 16) { ctx->set_error("matvec: m too large for the cluster split (m <= 16 * 8704)"); return NYS_EINVAL; }
+    if (clmin > 16) { ctx->set_error("matvec: m too large for the cluster split (m <= 16 * 8640)"); return NYS_EINVAL; }
     int forced = 0;
     if (const char* oc = getenv("NYS_MV_CL")) {  // tuning override of the cluster split
       const int o = atoi(oc);

@@ -50,7 +50,7 @@ def rel(a, b):
 MV_SHAPES = [(1, 5), (2, 0), (2, 3), (37, 401), (64, 3001), (100, 400), (130, 257), (300, 999), (1000, 1201),
              (2000, 801), (2001, 333), (4096, 300), (5000, 129), (8192, 77), (8193, 70), (13313, 150),
              (16384, 151), (20000, 40), (33001, 99), (50000, 17), (50000, 301), (70000, 33),
-             (139264, 9)]   # the largest m (a column split over 16 CTAs)
+             (138240, 9)]   # the largest m (a column split over 16 CTAs)
 
 
 @pytest.mark.parametrize("m,n", MV_SHAPES)
@@ -89,9 +89,9 @@ def test_normal_matvec_config_shapes_full(ctx):
 
 
 def test_normal_matvec_rejects_m_above_the_limit(ctx):
-    """m > 139264 (more than 16 CTAs per column) is rejected with an error, not computed wrongly."""
+    """m > 138240 (more than 16 CTAs per column) is rejected with an error, not computed wrongly."""
     from paper_2404_14524_b200 import NysError
-    m, n = 139266, 2
+    m, n = 138242, 2
     A = torch.zeros((n, m), dtype=torch.float64, device="cuda")
     w = torch.empty(m, dtype=torch.float64, device="cuda")
     with pytest.raises(NysError):
