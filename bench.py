@@ -37,8 +37,12 @@ sys.path.insert(0, ROOT)
 METRIC = "fp64 A·D·Aᵀv matvec GB/s (% HBM peak) and Nys-IP-PMM time-to-1e-8 at 1/2/4/8 GPU"
 # dram__bytes_read.sum + dram__bytes_write.sum per fused-matvec launch from `ncu --set full`
 # (profiles/, per config and shape); None until captured for that config
-#   config 4 slice (m = n = 50000): 20.002551 GB read + 5.558 MB written, profiles/r01_matvec_m50000_final_full.ncu-rep
-TRAFFIC = {1: 134.6e6, 4: 20.002551e9 + 5.558272e6}
+#   config 4 slice (m = n = 50000): 20.000958 GB read + 4.215 MB written, profiles/r02_matvec_m50000_full.ncu-rep
+TRAFFIC = {1: 134.6e6, 4: 20.000958e9 + 4.214784e6}
+# read-only stream ceiling on this pool's B200 (tools/hbm_sustained.py: torch.sum over 4 GB, burst 6863 GB/s,
+# sustained 6828 GB/s at full clocks; the read+write copy of MEASURED_PEAKS.json sustains 6520): K1 reads A
+# once and writes only partial rows, so it can exceed the copy figure
+READ_STREAM_GBS = 6863.0
 # fp64 tensor-core (DMMA, mma.sync.f64) peak measured on this pool's B200 by tools/dmma_probe.cu
 # (profiles/r01_dmma_peak_probe.log: 36.8-37.1 TFLOP/s over shapes / warps; cuBLAS square DGEMM 36.2)
 DMMA_PEAK_TFLOPS = 37.1
@@ -638,6 +642,7 @@ def main():
                "kernel": "fused normal matvec K1 (matvec_kernel + mv_finalize), graph-captured",
                "peak_source": peak_src, "bytes_per_launch": mv_bytes, "launch_us": mv_s * 1e6,
                "warm_l2_gbs": mv_bytes / mv_warm_s / 1e9,
+               "frac_of_read_stream": mv_gbs / READ_STREAM_GBS,
                "pcg_effective_gbs": (last["inner"] * mv_bytes / (last["t_pcg_ms"] / 1e3) / 1e9) if last["t_pcg_ms"] > 0 else None,
                "share_of_step": matvecs_per_solve * mv_s / sec_per_solve}
     if rank == 0:

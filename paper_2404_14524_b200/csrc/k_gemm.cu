@@ -8,6 +8,10 @@
 // ragged edges) shared-memory pipeline, padded layouts so every fragment load is
 // bank-conflict free.  Long K (the n-direction of Y = A T) is split across CTAs; partial
 // tiles are summed in a fixed order by gemm_reduce (deterministic).
+#include <cuda.h>   // CUtensorMap (the encode entry point is fetched through cudaGetDriverEntryPoint)
+
+#include <mutex>
+
 #include "k_vec.cuh"
 
 namespace nys {
@@ -328,6 +332,210 @@ __global__ void __launch_bounds__(128) dgemm_nt_kernel(const GemmParams G) {
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// TMA-fed, warp-specialised DMMA GEMM (the sketch products at large M and K).  CTA tile
+// 128 x (8 NT), BK = 16, TS-stage mbarrier ring; warp 4 is the producer, warps 0-3 the consumers
+// (32 rows each, m16n8k8 f64 MMAs exactly as dgemm_nt_kernel).
+//   * K-contiguous operands (B always; A when AK, i.e. A^T of a column-major matrix) arrive by
+//     cp.async.bulk.tensor.2d (UTMALDG) with the 128-byte swizzle: a 16-double row of the box is
+//     one 128-B line whose 16-B chunks are XOR-permuted by (row % 8), so the fragment loads (8 rows x
+//     4 k per instruction) touch every bank at most twice — the 2-wavefront minimum of 256 B.
+//     Out-of-range rows / columns are zero-filled by the tensor unit.
+//   * an M-contiguous A (Y = A T) arrives as 16 one-dimensional bulk copies per stage (UBLKCP), one
+//     per column segment, into rows padded to 136 doubles (conflict-free, as dgemm_nt_kernel).
+// The consumers release a stage with one mbarrier arrive per warp; no __syncthreads in the loop.
+// ------------------------------------------------------------------------------------------
+constexpr int TS = 3;                                    // stages (3 CTAs of 68 KB per SM)
+constexpr int TA_K_BYTES = HBM_ * HBK * 8;               // 16384: swizzled K-major A box
+constexpr int TA_M_BYTES = HBK * HLD_M * 8;              // 17408: padded M-major A rows
+constexpr int TA_BYTES = TA_M_BYTES;                     // the A slot (1 KB multiple: 17 KB)
+
+__host__ __device__ constexpr int tma_b_bytes(int nt) { return ((8 * nt * HBK * 8 + 1023) / 1024) * 1024; }
+__host__ __device__ constexpr int tma_stage_bytes(int nt) { return TA_BYTES + tma_b_bytes(nt); }
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// element (row, k) of a swizzled [rows][16] fp64 box (k in 0..15)
+__device__ __forceinline__ int swz(int row, int k) { return row * 16 + ((((k >> 1) ^ (row & 7)) << 1) | (k & 1)); }
+
+template <int NT, bool AK>
+__global__ void __launch_bounds__(160) dgemm_tma_kernel(const GemmParams G, const __grid_constant__ CUtensorMap mapA,
+                                                        const __grid_constant__ CUtensorMap mapB) {
+  constexpr int BN = 8 * NT;
+  constexpr int STAGE = tma_stage_bytes(NT);
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  // the dynamic window's base is only guaranteed 16-B aligned: round up to the 1 KB the swizzle needs
+  unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + (size_t)TS * STAGE);
+  uint64_t* empty = full + TS;
+  const int64_t j0 = (int64_t)blockIdx.x * BN;
+  const int64_t i0 = (int64_t)blockIdx.y * HBM_;
+  const int64_t kbeg = (int64_t)blockIdx.z * G.kchunk;
+  int64_t kend = kbeg + G.kchunk;
+  if (kend > G.K) kend = G.K;
+  const int nk = (kend > kbeg) ? (int)((kend - kbeg + HBK - 1) / HBK) : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    fence_mbar_init();
+  }
+  if (!AK) {   // stale-but-finite smem: padded rows / columns past K are never copied (their B is 0)
+    double* z = reinterpret_cast<double*>(tsm);
+    for (int e = threadIdx.x; e < TS * STAGE / 8; e += blockDim.x) z[e] = 0.0;
+  }
+  __syncthreads();
+
+  if (warp == 4) {
+    // ------------------------------ producer ------------------------------------------------
+    const uint64_t pol = l2_evict_first_policy();
+    int s = 0;
+    uint32_t eph = 1u;
+    for (int kt = 0; kt < nk; ++kt, ++s) {
+      if (s == TS) { s = 0; eph ^= 1u; }
+      if (kt >= TS) mbar_wait(&empty[s], eph);
+      unsigned char* st = tsm + (size_t)s * STAGE;
+      const int64_t k0 = kbeg + (int64_t)kt * HBK;
+      int ncols = (int)((kend - k0) < HBK ? (kend - k0) : HBK);
+      int64_t rows = G.M - i0;
+      rows = rows > HBM_ ? HBM_ : rows;
+      const uint32_t cbytes = (uint32_t)(((rows + 1) & ~int64_t(1)) * 8);
+      const uint32_t abytes = AK ? (uint32_t)TA_K_BYTES : (uint32_t)ncols * cbytes;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full[s], abytes + (uint32_t)(BN * HBK * 8));
+        if (AK) tma_load_2d(st, &mapA, (int)k0, (int)i0, &full[s]);
+        tma_load_2d(st + TA_BYTES, &mapB, (int)k0, (int)j0, &full[s]);
+      }
+      __syncwarp();
+      if (!AK && lane < ncols)
+        bulk_g2s(st + (size_t)lane * HLD_M * 8, G.A + i0 + (k0 + lane) * G.lda, cbytes, &full[s], pol);
+    }
+    return;
+  }
+  // ------------------------------ consumers --------------------------------------------------
+  const int gq = lane >> 2, tq = lane & 3;
+  double acc[2][NT][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int kt = 0; kt < nk; ++kt) {
+    mbar_wait(&full[s], ph);
+    const double* As = reinterpret_cast<const double*>(tsm + (size_t)s * STAGE);
+    const double* Bs = reinterpret_cast<const double*>(tsm + (size_t)s * STAGE + TA_BYTES);
+#pragma unroll
+    for (int kk = 0; kk < HBK / 8; ++kk) {
+      const int k = 8 * kk + tq;
+      double af[2][4], bf[NT][2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int r = 32 * warp + 16 * mt + gq;
+        if (AK) {
+          af[mt][0] = As[swz(r, k)];
+          af[mt][1] = As[swz(r + 8, k)];
+          af[mt][2] = As[swz(r, k + 4)];
+          af[mt][3] = As[swz(r + 8, k + 4)];
+        } else {
+          af[mt][0] = As[k * HLD_M + r];
+          af[mt][1] = As[k * HLD_M + r + 8];
+          af[mt][2] = As[(k + 4) * HLD_M + r];
+          af[mt][3] = As[(k + 4) * HLD_M + r + 8];
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        bf[nt][0] = Bs[swz(8 * nt + gq, k)];
+        bf[nt][1] = Bs[swz(8 * nt + gq, k + 4)];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma_16x8x8(acc[mt][nt], af[mt], bf[nt]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == TS) { s = 0; ph ^= 1u; }
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int64_t row = i0 + 32 * warp + 16 * mt + gq + 8 * (c >> 1);
+        const int64_t col = j0 + 8 * nt + 2 * tq + (c & 1);
+        if (row < G.M && col < G.N) {
+          double v = acc[mt][nt][c];
+          if (G.partial) {
+            G.C[(size_t)blockIdx.z * G.M * G.N + row + col * G.M] = v;
+          } else {
+            if (G.row_scale) v *= G.row_scale[row];
+            if (G.addv) v += G.addv[row] * G.addm[row + col * G.ldadd];
+            G.C[row + col * G.ldc] = v;
+          }
+        }
+      }
+    }
+  }
+}
+
+typedef void (*TmaKernel)(const GemmParams, const CUtensorMap, const CUtensorMap);
+template <bool AK>
+static TmaKernel tma_kernel(int nt) {
+  switch (nt) {
+    case 1: return dgemm_tma_kernel<1, AK>;
+    case 2: return dgemm_tma_kernel<2, AK>;
+    case 3: return dgemm_tma_kernel<3, AK>;
+    case 4: return dgemm_tma_kernel<4, AK>;
+    case 5: return dgemm_tma_kernel<5, AK>;
+    case 6: return dgemm_tma_kernel<6, AK>;
+    case 7: return dgemm_tma_kernel<7, AK>;
+    default: return dgemm_tma_kernel<8, AK>;
+  }
+}
+
+static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+// 2-D fp64 tensor (inner extent d0 contiguous, d1 columns of stride ld doubles), box {16, rows}, 128-B swizzle
+static bool make_map(CUtensorMap* map, const double* base, int64_t d0, int64_t d1, int64_t ld, int rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)d0, (cuuint64_t)d1};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)HBK, (cuuint32_t)rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 typedef void (*DgemmKernel)(const GemmParams);
 template <bool AK>
 static DgemmKernel nt_kernel(int nt) {
@@ -397,9 +605,21 @@ int launch_gemm(nys_ctx* ctx, const GemmCall& g) {
   if (g.M < min_m || g.K < min_k || getenv("NYS_GEMM_OLD")) return launch_gemm_old(ctx, g);
   const int NT = pick_nt(g.N);
   const int BN = 8 * NT;
-  const size_t smem = (size_t)HST * (HA_STAGE + BN * HLD_K) * sizeof(double);
+  // TMA path (default): tensor maps over A (K-major case) and B; the cp.async kernel stays as the
+  // fallback for operands the tensor unit cannot address (odd leading dimensions, misalignment) and
+  // as an A/B switch (NYS_GEMM_CPASYNC)
+  CUtensorMap mapA{}, mapB{};
+  bool tma = getenv("NYS_GEMM_CPASYNC") == nullptr && (g.lda % 2) == 0 && (g.ldb % 2) == 0 &&
+             aligned16(g.A) && aligned16(g.B) && g.K < (int64_t(1) << 31) && g.M < (int64_t(1) << 31);
+  if (tma) {
+    if (g.a_kmajor) tma = make_map(&mapA, g.A, g.K, g.M, g.lda, HBM_);
+    tma = tma && make_map(&mapB, g.B, g.K, g.N, g.ldb, BN);
+  }
+  const size_t smem = tma ? (size_t)TS * tma_stage_bytes(NT) + 2 * TS * 8 + 1024
+                          : (size_t)HST * (HA_STAGE + BN * HLD_K) * sizeof(double);
   DgemmKernel k = g.a_kmajor ? nt_kernel<true>(NT) : nt_kernel<false>(NT);
-  NYS_TRY(ensure_max_smem(ctx, (const void*)k, smem));
+  TmaKernel kt = g.a_kmajor ? tma_kernel<true>(NT) : tma_kernel<false>(NT);
+  NYS_TRY(ensure_max_smem(ctx, tma ? (const void*)kt : (const void*)k, smem));
   const int64_t mt = (g.M + HBM_ - 1) / HBM_, nt = (g.N + BN - 1) / BN;
   const int64_t kslabs = (g.K + HBK - 1) / HBK;
   int splits = g.splits;
@@ -429,7 +649,8 @@ int launch_gemm(nys_ctx* ctx, const GemmCall& g) {
   }
   if (mt > 65535) { ctx->set_error("dgemm: M too large for the grid"); return NYS_EINVAL; }
   dim3 grid((unsigned)nt, (unsigned)mt, (unsigned)splits);
-  k<<<grid, 128, smem, ctx->stream>>>(P);
+  if (tma) kt<<<grid, 160, smem, ctx->stream>>>(P, mapA, mapB);
+  else k<<<grid, 128, smem, ctx->stream>>>(P);
   ctx->launches++;
   NYS_TRY(ctx->check_launch("dgemm"));
   if (splits > 1) {
