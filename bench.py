@@ -147,6 +147,7 @@ class Workload:
         import torch
         self.cfg = cfg
         self.structure = 0
+        self.unit_blocks = None
         self.inst = None
         dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
         if cfg == 4:
@@ -169,14 +170,20 @@ class Workload:
         self.m, self.ell, self.name = inst.m, inst.ell, inst.name
         self.scaling = "strong"
         if cfg == 2:
-            # SVM-structured A = [Xt, -Xt, I, -I]: the dense block Xt is the operand
-            if world > 1:
-                raise SystemExit("config 2 (structured SVM operator) is single-GPU in this build")
+            # SVM-structured A = [Xt, -Xt, I, -I]: the dense block Xt is the operand.
+            # Multi-GPU: rank g holds feature columns Xt[:, f_g] (its w+ / w- variables) and the xi / s
+            # variables of one row range (one unit block); e and the A u partials are all-reduced.
             Xt = inst.extra["Xt"]
+            N, dd = Xt.shape
             self.structure = 1
-            self.n, self.lo, self.hi = inst.n, 0, inst.n
-            self.At, self.lda = colmajor_device(Xt, device=device)
-            self.q, self.b, self.c = dv(inst.q), dv(inst.b), dv(inst.c)
+            f0, f1 = (dd * rank) // world, (dd * (rank + 1)) // world
+            r0, r1 = (N * rank) // world, (N * (rank + 1)) // world
+            idx = np.concatenate([np.arange(f0, f1), dd + np.arange(f0, f1), 2 * dd + np.arange(r0, r1),
+                                  2 * dd + N + np.arange(r0, r1)])
+            self.n, self.lo, self.hi = inst.n, 0, len(idx)
+            self.unit_blocks = [(r0, r1 - r0, 1.0)]
+            self.At, self.lda = colmajor_device(np.asfortranarray(Xt[:, f0:f1]), device=device)
+            self.q, self.b, self.c = dv(inst.q[idx]), dv(inst.b), dv(inst.c[idx])
             self.A_dense_block = Xt
             return
         n = inst.n
@@ -365,7 +372,7 @@ def main():
     def one_solve():
         with torch.cuda.stream(stream):
             return ctx.nys_ipppmm_solve(wl.At, lda, m, wl.q, wl.b, wl.c, ell=wl.ell, structure=wl.structure,
-                                        prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
+                                        unit_blocks=wl.unit_blocks, prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
                                         precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max,
                                         max_outer=args.max_outer)
 
@@ -552,7 +559,7 @@ def main():
             def solve2(w2=w2):
                 with torch.cuda.stream(stream):
                     return ctx.nys_ipppmm_solve(w2.At, w2.lda, w2.m, w2.q, w2.b, w2.c, ell=w2.ell,
-                                                structure=w2.structure)
+                                                structure=w2.structure, unit_blocks=w2.unit_blocks)
             for _ in range(3):
                 solve2()
             barrier()
@@ -590,7 +597,7 @@ def main():
             A_host, qh, bh, ch = A_pin.numpy(), q_pin.numpy(), b_pin.numpy(), c_pin.numpy()
             with torch.cuda.stream(stream):  # one untimed e2e solve: workspace for the host path, graphs
                 ctx.nys_ipppmm_solve(A_host, lda, m, qh, bh, ch, ell=wl.ell, host=True, structure=wl.structure,
-                                     prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
+                                     unit_blocks=wl.unit_blocks, prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
                                      precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max,
                                         max_outer=args.max_outer)
             barrier()
@@ -599,7 +606,7 @@ def main():
             for _ in range(E_STEPS):
                 with torch.cuda.stream(stream):
                     ctx.nys_ipppmm_solve(A_host, lda, m, qh, bh, ch, ell=wl.ell, host=True, structure=wl.structure,
-                                         prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
+                                         unit_blocks=wl.unit_blocks, prec_refresh=args.prec_refresh, prec_growth=args.prec_growth,
                                          precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max,
                                         max_outer=args.max_outer)
             barrier()

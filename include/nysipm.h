@@ -199,7 +199,12 @@ typedef struct {
                             column-major, lda) passed in `A`; n = 2 nd + 2 m variables ordered
                             [w+, w-, xi, s].  The identity blocks are never materialised: they
                             contribute the diagonal term e = d_xi + d_s of the normal operator.
-                            Single rank.  2: dense block + scaled identity blocks (below).         */
+                            Multi-rank: each rank passes its feature columns Xt_g (nd_g) and owns
+                            the xi / s variables of ONE row range, given as a single unit block
+                            (row0, count, scale = 1) in unit_blocks; then n = 2 nd + 2 count,
+                            variables [w+_g, w-_g, xi_rows, s_rows], and the row ranges of the
+                            ranks partition [0, m).  No unit block: the whole range [0, m).
+                            2: dense block + scaled identity blocks (below).                    */
   int64_t nd;            /* structure 1 / 2: number of dense columns stored in `A`          */
   /* Free and box-constrained variables, problem (P~)/(D~) (Alg. 5; SURVEY
    * §8(f) f1).  vtype == NULL: every variable is in I (x >= 0), the form (P)/(D).  Otherwise

@@ -812,39 +812,44 @@ int launch_minsum(nys_ctx* ctx, int64_t n, const double* u, double shift, int mi
 }
 
 // ------------------------------------------------------------------------------------------
-// SVM-structured A = [Xt, -Xt, I, -I]: variables [w+ (nd), w- (nd), xi (m), s (m)]
+// SVM-structured A = [Xt, -Xt, I, -I]: variables [w+ (nd), w- (nd), xi (mr), s (mr)], the
+// xi / s variables of this rank being those of rows [r0, r0 + mr) (single rank: r0 = 0, mr = m)
 // ------------------------------------------------------------------------------------------
-// A^T y = [Xt^T y ; -Xt^T y ; y ; -y]   from g = Xt^T y
-__global__ void svm_expand_kernel(int64_t nd, int64_t m, const double* g, const double* y, double* atv) {
-  const int64_t n = 2 * nd + 2 * m;
+// A^T y = [Xt^T y ; -Xt^T y ; y_rows ; -y_rows]   from g = Xt^T y
+__global__ void svm_expand_kernel(int64_t nd, int64_t r0, int64_t mr, const double* g, const double* y, double* atv) {
+  const int64_t n = 2 * nd + 2 * mr;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     double v;
     if (j < nd) v = g[j];
     else if (j < 2 * nd) v = -g[j - nd];
-    else if (j < 2 * nd + m) v = y[j - 2 * nd];
-    else v = -y[j - 2 * nd - m];
+    else if (j < 2 * nd + mr) v = y[r0 + j - 2 * nd];
+    else v = -y[r0 + j - 2 * nd - mr];
     atv[j] = v;
   }
 }
-// A u = Xt (u_w+ - u_w-) + u_xi - u_s :  uw (nd) and the diagonal part addm (m) (+ add)
-__global__ void svm_fold_kernel(int64_t nd, int64_t m, const double* u, const double* add, double* uw, double* addm) {
+// A u = Xt (u_w+ - u_w-) + (u_xi - u_s on the own rows) :  uw (nd) and the diagonal part addm (m) (+ add)
+__global__ void svm_fold_kernel(int64_t nd, int64_t m, int64_t r0, int64_t mr, const double* u, const double* add,
+                                double* uw, double* addm) {
   const int64_t tot = nd + m;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < tot; j += (int64_t)gridDim.x * blockDim.x) {
     if (j < nd) uw[j] = u[j] - u[nd + j];
     else {
-      const int64_t i = j - nd;
-      addm[i] = u[2 * nd + i] - u[2 * nd + m + i] + (add ? add[i] : 0.0);
+      const int64_t i = j - nd, k = i - r0;
+      const double un = (k >= 0 && k < mr) ? u[2 * nd + k] - u[2 * nd + mr + k] : 0.0;
+      addm[i] = un + (add ? add[i] : 0.0);
     }
   }
 }
-// normal operator of the structured A: N = Xt diag(d_w+ + d_w-) Xt^T + diag(d_xi + d_s)
-__global__ void svm_scaling_fold_kernel(int64_t nd, int64_t m, const double* d, double* dw, double* e) {
+// normal operator of the structured A: N = Xt diag(d_w+ + d_w-) Xt^T + diag(d_xi + d_s) (own rows; the
+// other rows' terms come from their ranks through the all-reduce)
+__global__ void svm_scaling_fold_kernel(int64_t nd, int64_t m, int64_t r0, int64_t mr, const double* d, double* dw,
+                                        double* e) {
   const int64_t tot = nd + m;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < tot; j += (int64_t)gridDim.x * blockDim.x) {
     if (j < nd) dw[j] = d[j] + d[nd + j];
     else {
-      const int64_t i = j - nd;
-      e[i] = d[2 * nd + i] + d[2 * nd + m + i];
+      const int64_t i = j - nd, k = i - r0;
+      e[i] = (k >= 0 && k < mr) ? d[2 * nd + k] + d[2 * nd + mr + k] : 0.0;
     }
   }
 }
@@ -862,18 +867,21 @@ __global__ void epi_dx_kernel(int64_t n, const double* atv, const double* rd, co
     dz[j] = (rxz[j] - z[j] * v) / x[j];
   }
 }
-int launch_svm_expand(nys_ctx* ctx, int64_t nd, int64_t m, const double* g, const double* y, double* atv) {
-  svm_expand_kernel<<<ew_grid(ctx, 2 * nd + 2 * m), 256, 0, ctx->stream>>>(nd, m, g, y, atv);
+int launch_svm_expand(nys_ctx* ctx, int64_t nd, int64_t r0, int64_t mr, const double* g, const double* y, double* atv) {
+  if (2 * nd + 2 * mr <= 0) return NYS_OK;
+  svm_expand_kernel<<<ew_grid(ctx, 2 * nd + 2 * mr), 256, 0, ctx->stream>>>(nd, r0, mr, g, y, atv);
   ctx->launches++;
   return ctx->check_launch("svm_expand");
 }
-int launch_svm_fold(nys_ctx* ctx, int64_t nd, int64_t m, const double* u, const double* add, double* uw, double* addm) {
-  svm_fold_kernel<<<ew_grid(ctx, nd + m), 256, 0, ctx->stream>>>(nd, m, u, add, uw, addm);
+int launch_svm_fold(nys_ctx* ctx, int64_t nd, int64_t m, int64_t r0, int64_t mr, const double* u, const double* add,
+                    double* uw, double* addm) {
+  svm_fold_kernel<<<ew_grid(ctx, nd + m), 256, 0, ctx->stream>>>(nd, m, r0, mr, u, add, uw, addm);
   ctx->launches++;
   return ctx->check_launch("svm_fold");
 }
-int launch_svm_scaling_fold(nys_ctx* ctx, int64_t nd, int64_t m, const double* d, double* dw, double* e) {
-  svm_scaling_fold_kernel<<<ew_grid(ctx, nd + m), 256, 0, ctx->stream>>>(nd, m, d, dw, e);
+int launch_svm_scaling_fold(nys_ctx* ctx, int64_t nd, int64_t m, int64_t r0, int64_t mr, const double* d, double* dw,
+                            double* e) {
+  svm_scaling_fold_kernel<<<ew_grid(ctx, nd + m), 256, 0, ctx->stream>>>(nd, m, r0, mr, d, dw, e);
   ctx->launches++;
   return ctx->check_launch("svm_scaling_fold");
 }

@@ -132,9 +132,11 @@ int launch_mul(nys_ctx* ctx, int64_t n, const double* u, const double* v, double
 int launch_cpqx(nys_ctx* ctx, int64_t n, const double* c, const double* q, const double* x, double* t);
 int launch_shift(nys_ctx* ctx, int64_t n, double* u, double s);
 int launch_minsum(nys_ctx* ctx, int64_t n, const double* u, double shift, int min_slot, int sum_slot, int counter_slot);
-int launch_svm_expand(nys_ctx* ctx, int64_t nd, int64_t m, const double* g, const double* y, double* atv);
-int launch_svm_fold(nys_ctx* ctx, int64_t nd, int64_t m, const double* u, const double* add, double* uw, double* addm);
-int launch_svm_scaling_fold(nys_ctx* ctx, int64_t nd, int64_t m, const double* d, double* dw, double* e);
+int launch_svm_expand(nys_ctx* ctx, int64_t nd, int64_t r0, int64_t mr, const double* g, const double* y, double* atv);
+int launch_svm_fold(nys_ctx* ctx, int64_t nd, int64_t m, int64_t r0, int64_t mr, const double* u, const double* add,
+                    double* uw, double* addm);
+int launch_svm_scaling_fold(nys_ctx* ctx, int64_t nd, int64_t m, int64_t r0, int64_t mr, const double* d, double* dw,
+                            double* e);
 int launch_epi_rd(nys_ctx* ctx, int64_t n, const double* c, const double* q, const double* x, const double* atv,
                   const double* z, double* out);
 int launch_epi_dx(nys_ctx* ctx, int64_t n, const double* atv, const double* rd, const double* xiau, const double* rxz,

@@ -315,6 +315,16 @@ int nystrom_factor(nys_ctx* ctx, int64_t m, int ell, const double* Y, const doub
   double* W = ctx->wsd("nf_W", (size_t)ldl * ell);
   double* sig = ctx->wsd("nf_sig", (size_t)ell);
 
+  // NYS_FACT_TRACE: per-phase device times of this factorisation on stderr (development aid)
+  const bool ftrace = getenv("NYS_FACT_TRACE") != nullptr;
+  cudaEvent_t fev[8];
+  int nfev = 0;
+  auto fmark = [&]() {
+    if (!ftrace || nfev >= 8) return;
+    cudaEventCreate(&fev[nfev]);
+    cudaEventRecord(fev[nfev++], ctx->stream);
+  };
+  fmark();
   NYS_TRY(launch_fro_nu(ctx, m, ell, Y, mp, 0));                      // line 3
   int retries = 0;
   for (;;) {
@@ -333,6 +343,7 @@ int nystrom_factor(nys_ctx* ctx, int64_t m, int ell, const double* Y, const doub
     ++retries;
     NYS_TRY(launch_set_slots(ctx, S_NU, ctx->h_sc[S_NU] * 10.0));     // A4
   }
+  fmark();
   {                                                                    // line 6: B = Y_nu C^{-1}
     GemmCall g;
     g.M = m; g.N = ell; g.K = ell; g.A = Ynu; g.lda = mp; g.a_kmajor = false; g.B = Gi; g.ldb = ldl; g.C = Bm; g.ldc = mp;
@@ -354,15 +365,31 @@ int nystrom_factor(nys_ctx* ctx, int64_t m, int ell, const double* Y, const doub
     double* tmp = src; src = dst; dst = tmp;
   }
   // src now holds Q; R = R3 R2 R1
+  fmark();
   NYS_TRY(launch_trmm_upper(ctx, ell, ldl, R2, R1, Rt));
   NYS_TRY(launch_trmm_upper(ctx, ell, ldl, R3, Rt, G));
+  fmark();
   NYS_TRY(launch_jacobi_svd(ctx, ell, G, ldl, W, ldl, sig));
+  fmark();
   {                                                                    // U = Q W
     GemmCall g;
     g.M = m; g.N = ell; g.K = ell; g.A = src; g.lda = mp; g.a_kmajor = false; g.B = W; g.ldb = ldl; g.C = U; g.ldc = mp;
     NYS_TRY(launch_gemm(ctx, g));
   }
   NYS_TRY(launch_lambda_from_sigma(ctx, ell, sig, lam));              // line 8
+  fmark();
+  if (ftrace) {
+    cudaStreamSynchronize(ctx->stream);
+    const char* names[] = {"nu+Gram+chol(C)", "B GEMM + CholQR3", "trmm", "jacobi", "U GEMM + lambda"};
+    fprintf(stderr, "[fact] m=%lld ell=%d:", (long long)m, ell);
+    for (int i = 0; i + 1 < nfev; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, fev[i], fev[i + 1]);
+      fprintf(stderr, " %s %.3f ms;", names[i], ms);
+    }
+    fprintf(stderr, "\n");
+    for (int i = 0; i < nfev; ++i) cudaEventDestroy(fev[i]);
+  }
   if (info) NYS_TRY(launch_orth_err(ctx, m, ell, U, mp, S_TMP6));
   // a failed shifted CholeskyQR pass leaves Gi / R stale: U would be silently non-orthonormal,
   // so the flag is read on every build (one host sync per outer iteration), not only with info
@@ -599,21 +626,77 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
     res.iters = (int)ctx->h_sc[S_ITERS];
     ctx->matvecs += res.iters > 2 ? res.iters - 2 : 0;
   } else {
+    // multi-rank: every iteration all-reduces the matvec partial.  With NCCL the loop body is captured
+    // ONCE as a CUDA graph of kBatch iterations (matvec, ncclAllReduce, finalize, update, precond; the
+    // library's kernels return at once after convergence, the trailing all-reduces move stale data and
+    // are harmless) and replayed with one host check per replay; the loopback communicator (host
+    // barriers) cannot be captured and keeps the eager host loop.
+    constexpr int kBatch = 8;
+    auto one_iter = [&](int it) -> int {
+      const double* pold = (it == 0) ? nullptr : Pp[it & 1];
+      double* pnew = Pp[(it + 1) & 1];
+      NYS_TRY(apply_normal_full(ctx, op, z, pold, ctx->sc + S_BETA, pnew, w, true, done));
+      NYS_TRY(launch_pcg_update(ctx, 0, m, x, r, nullptr, pnew, w, nullptr, op.delta, op.e, U, ldu, ell, s, h,
+                                max_iter, 0ull, false, chol != nullptr));
+      if (chol) NYS_TRY(launch_chol_apply(ctx, *chol, r, z, 1, 0));
+      else if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 0, m, r, z, U, ldu, ell, h));
+      return NYS_OK;
+    };
+    const bool capture = ctx->nccl_comm != nullptr && ctx->loop_comm == nullptr && getenv("NYS_NO_GRAPH") == nullptr;
     int it = 0;
-    int batch = 4;
-    for (;;) {
-      for (int b = 0; b < batch; ++b, ++it) {
-        const double* pold = (it == 0) ? nullptr : Pp[it & 1];
-        double* pnew = Pp[(it + 1) & 1];
-        NYS_TRY(apply_normal_full(ctx, op, z, pold, ctx->sc + S_BETA, pnew, w, true, done));
-        NYS_TRY(launch_pcg_update(ctx, 0, m, x, r, nullptr, pnew, w, nullptr, op.delta, op.e, U, ldu, ell, s, h,
-                                  max_iter, 0ull, false, chol != nullptr));
-        if (chol) NYS_TRY(launch_chol_apply(ctx, *chol, r, z, 1, 0));
-        else if (ell > 0) NYS_TRY(launch_pcg_precond(ctx, 0, m, r, z, U, ldu, ell, h));
-      }
+    if (capture) {
+      for (; it < 2; ++it) NYS_TRY(one_iter(it));   // sizes every workspace before the capture
       NYS_TRY(read_slots(ctx));
-      if (ctx->h_sc[S_DONE] != 0.0) break;
-      if (batch < 32) batch *= 2;
+      if (ctx->h_sc[S_DONE] == 0.0) {
+        char key[768];
+        snprintf(key, sizeof(key), "mpcg%s:%lld:%lld:%lld:%p:%p:%p:%p:%lld:%p:%d:%p:%d:%lld:%d:%d:%p:%p:%p:%p:%p:%p",
+                 chol ? "C" : "N", (long long)m, (long long)op.n, (long long)op.lda, (const void*)op.A,
+                 (const void*)op.d, (const void*)op.e, (const void*)U, (long long)ldu, (const void*)s, ell,
+                 (const void*)x, max_iter, (long long)ctx->ws_epoch, chol ? chol->ell : -1, chol ? chol->ldr : -1,
+                 chol ? (const void*)chol->Zt : nullptr, chol ? (const void*)chol->dS : nullptr,
+                 chol ? (const void*)chol->Rinv : nullptr, chol ? (const void*)chol->piv : nullptr,
+                 chol ? (const void*)chol->pivpos : nullptr, (const void*)rhs);
+        char dkey[800];
+        snprintf(dkey, sizeof(dkey), "%s:%.17g", key, op.delta);   // delta is a captured kernel argument here
+        auto itg = ctx->graphs.find(dkey);
+        cudaGraphExec_t exec = nullptr;
+        if (itg != ctx->graphs.end()) {
+          exec = itg->second.second.first;
+        } else {
+          if (ctx->graphs.size() >= 64) {
+            for (auto& kv : ctx->graphs) {
+              cudaGraphExecDestroy(kv.second.second.first);
+              cudaGraphDestroy(kv.second.second.second);
+            }
+            ctx->graphs.clear();
+          }
+          const int64_t l0 = ctx->launches, mv0 = ctx->matvecs;
+          NYS_CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+          int rc = NYS_OK;
+          for (int b = 0; b < kBatch && rc == NYS_OK; ++b) rc = one_iter(2 + b);
+          cudaGraph_t g = nullptr;
+          const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &g);
+          ctx->launches = l0; ctx->matvecs = mv0;
+          if (rc != NYS_OK) { if (g) cudaGraphDestroy(g); return rc; }
+          if (ec != cudaSuccess) { ctx->set_error(std::string("multi-rank PCG graph capture: ") + cudaGetErrorString(ec)); return NYS_ECUDA; }
+          NYS_CUDA_TRY(ctx, cudaGraphInstantiate(&exec, g, 0));
+          ctx->graphs[dkey] = {ctx->ws_epoch, {exec, g}};
+        }
+        for (;;) {
+          NYS_CUDA_TRY(ctx, cudaGraphLaunch(exec, ctx->stream));
+          ctx->launches += kBatch * (chol ? 7 : (ell > 0 ? 5 : 4));
+          NYS_TRY(read_slots(ctx));
+          if (ctx->h_sc[S_DONE] != 0.0) break;
+        }
+      }
+    } else {
+      int batch = 4;
+      for (;;) {
+        for (int b = 0; b < batch; ++b, ++it) NYS_TRY(one_iter(it));
+        NYS_TRY(read_slots(ctx));
+        if (ctx->h_sc[S_DONE] != 0.0) break;
+        if (batch < 32) batch *= 2;
+      }
     }
     res.iters = (int)ctx->h_sc[S_ITERS];
   }
@@ -710,6 +793,7 @@ struct AOps {
   int64_t lda;
   double *g, *atv, *uw, *addm, *dw, *e;  // structure-1/2 work vectors
   UnitBlocks UB;                          // structure 2
+  int64_t r0 = 0, mr = 0;                 // structure 1: this rank's xi / s rows [r0, r0 + mr)
   // normal operator for the scaling d (n): dense -> (A, d); structured -> (Xt, d_w+ + d_w-, e)
   int normal_op(const double* d, double delta, NormalOp& op) {
     if (structure == 0) { op = NormalOp{m, n, lda, A, d, nullptr, delta}; return NYS_OK; }
@@ -719,7 +803,8 @@ struct AOps {
       op = NormalOp{m, nd, lda, A, d, e, delta};
       return NYS_OK;
     }
-    NYS_TRY(launch_svm_scaling_fold(ctx, nd, m, d, dw, e));
+    NYS_TRY(launch_svm_scaling_fold(ctx, nd, m, r0, mr, d, dw, e));
+    if (ctx->multi()) NYS_TRY(allreduce(ctx, e, (size_t)m));   // every row's d_xi + d_s, replicated
     op = NormalOp{m, nd, lda, A, dw, e, delta};
     return NYS_OK;
   }
@@ -739,8 +824,17 @@ struct AOps {
       if (add) NYS_TRY(launch_axpby(ctx, m, 1.0, out, 1.0, add, out));
       return NYS_OK;
     }
-    NYS_TRY(launch_svm_fold(ctx, nd, m, u, add, uw, addm));
-    return apply_A(ctx, m, nd, A, lda, uw, out, 1.0, addm);
+    if (!ctx->multi()) {
+      NYS_TRY(launch_svm_fold(ctx, nd, m, r0, mr, u, add, uw, addm));
+      return apply_A(ctx, m, nd, A, lda, uw, out, 1.0, addm);
+    }
+    NYS_TRY(launch_svm_fold(ctx, nd, m, r0, mr, u, nullptr, uw, addm));   // local partial: own rows only
+    MatvecCall c;
+    c.mode = MV_NONLY; c.m = m; c.n = nd; c.lda = lda; c.A = A; c.u = uw; c.out = out; c.sgn = 1.0; c.add = addm;
+    NYS_TRY(launch_matvec(ctx, c));
+    NYS_TRY(allreduce(ctx, out, (size_t)m));
+    if (add) NYS_TRY(launch_axpby(ctx, m, 1.0, out, 1.0, add, out));
+    return NYS_OK;
   }
   // structured: atv = A^T y (n-vector)
   int At_vec(const double* y) {
@@ -749,7 +843,7 @@ struct AOps {
     mc.t1 = structure == 2 ? atv : g;
     NYS_TRY(apply_At(ctx, mc));
     if (structure == 2) return launch_unit_expand(ctx, UB, y, atv + nd);
-    return launch_svm_expand(ctx, nd, m, g, y, atv);
+    return launch_svm_expand(ctx, nd, r0, mr, g, y, atv);
   }
   int At_plain(const double* y, double* out) {
     if (structure == 0) {
@@ -897,6 +991,8 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     AO.UB.total = off;
   }
   if (AO.structure == 1) {
+    AO.r0 = qp_in->n_unit_blocks == 1 ? qp_in->unit_blocks[0].row0 : 0;
+    AO.mr = qp_in->n_unit_blocks == 1 ? qp_in->unit_blocks[0].count : m;
     AO.g = ctx->wsd("svm_g", (size_t)even(ncolA) + 2);
     AO.atv = ctx->wsd("svm_atv", nn);
     AO.uw = ctx->wsd("svm_uw", (size_t)even(ncolA) + 2);
@@ -1665,9 +1761,17 @@ static int nys_ipppmm_solve_body(nys_ctx* ctx, const nys_qp* qp, const nys_optio
     ctx->set_error("nys_ipppmm_solve: bad problem");
     return NYS_EINVAL;
   }
-  if (qp->structure == 1 && (qp->nd < 0 || qp->n != 2 * qp->nd + 2 * qp->m || ctx->multi())) {
-    ctx->set_error("nys_ipppmm_solve: structure 1 needs n = 2 nd + 2 m and one rank");
-    return NYS_EINVAL;
+  if (qp->structure == 1) {
+    const bool one = qp->n_unit_blocks == 1 && qp->unit_blocks != nullptr;
+    const int64_t r0 = one ? qp->unit_blocks[0].row0 : 0, mr = one ? qp->unit_blocks[0].count : qp->m;
+    const bool ok = qp->nd >= 0 && (qp->n_unit_blocks == 0 || one) && r0 >= 0 && mr >= 0 && r0 + mr <= qp->m &&
+                    (!one || qp->unit_blocks[0].scale == 1.0) && qp->n == 2 * qp->nd + 2 * mr &&
+                    (ctx->multi() || (r0 == 0 && mr == qp->m));
+    if (!ok) {
+      ctx->set_error("nys_ipppmm_solve: structure 1 needs n = 2 nd + 2 count with this rank's xi / s rows given as one "
+                     "unit block (row0, count, scale 1) inside [0, m) (single rank: the whole range)");
+      return NYS_EINVAL;
+    }
   }
   if (qp->structure == 2) {
     bool ok = qp->nd >= 1 && qp->n_unit_blocks >= 0 && qp->n_unit_blocks <= 8 &&

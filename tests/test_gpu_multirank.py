@@ -253,3 +253,52 @@ def test_multirank_adaptive_rank_and_reuse_agree():
     assert res[0]["status"] == 0 and res[1]["status"] == 0
     assert res[0]["ells"] == res[1]["ells"] and res[0]["built"] == res[1]["built"]
     assert max(res[0]["ells"]) > 10 and np.array_equal(res[0]["y"], res[1]["y"])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multirank_svm_structure1_matches_single_and_oracle(world):
+    """Config 2's SVM operator (structure 1) sharded: rank g holds feature columns Xt[:, f_g] (its w+ / w-
+    variables) and the xi / s variables of one row range (a single unit block), the ranges partitioning
+    [0, m); e = d_xi + d_s and the A u partials are all-reduced.  The sharded solve
+    equals the single-rank structure-1 solve and the oracle on the materialised A."""
+    from paper_2404_14524_b200 import Context, colmajor_device
+    from synth.configs import svm_dense_A
+    N, dd, ell = 600, 30, 10
+    inst = make_config(2, m=N, n=dd, ell=ell)
+    Xt = inst.extra["Xt"]
+    q, c = inst.q, inst.c
+    parts = []
+    for r in range(world):
+        f0, f1 = (dd * r) // world, (dd * (r + 1)) // world
+        r0, r1 = (N * r) // world, (N * (r + 1)) // world
+        idx = np.concatenate([np.arange(f0, f1), dd + np.arange(f0, f1), 2 * dd + np.arange(r0, r1),
+                              2 * dd + N + np.arange(r0, r1)])
+        Xd, lda = colmajor_device(np.asfortranarray(Xt[:, f0:f1]))
+        parts.append((f1 - f0, r0, r1 - r0, idx, Xd, lda))
+    torch.cuda.synchronize()
+
+    def fn(ctx, r, st):
+        nd_, r0, mr, idx, Xd, lda = parts[r]
+        g = ctx.nys_ipppmm_solve(Xd, lda, N, dev(q[idx]), dev(inst.b), dev(c[idx]), ell=ell, structure=1,
+                                 unit_blocks=[(r0, mr, 1.0)])
+        st.synchronize()
+        return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in g.items() if k != "log"}
+
+    res = _run_ranks(world, fn)
+    for g in res:
+        assert g["status"] == 0
+        assert g["obj"] == res[0]["obj"] and np.array_equal(g["y"], res[0]["y"])   # replicated: bitwise
+    ctx1 = Context(0)
+    Xd, lda = colmajor_device(Xt)
+    g1 = ctx1.nys_ipppmm_solve(Xd, lda, N, dev(q), dev(inst.b), dev(c), ell=ell, structure=1)
+    ctx1.close()
+    A = svm_dense_A(inst)
+    ref = ippmm.solve(A, q, inst.b, c, ippmm.Options(path="krylov", ell=ell))
+    x = np.zeros(inst.n)
+    for (nd_, r0, mr, idx, Xd, lda), g in zip(parts, res):
+        x[idx] = g["x"]
+    assert np.linalg.norm(inst.b - A @ x) / (1 + np.linalg.norm(inst.b)) <= 1.01e-8
+    print(f"world {world}: sharded {res[0]['obj']!r} single {g1['obj']!r} oracle {ref.obj!r}")
+    assert abs(res[0]["obj"] - g1["obj"]) <= 1e-7 * max(1.0, abs(g1["obj"]))
+    assert abs(res[0]["obj"] - ref.obj) <= 1e-7 * max(1.0, abs(ref.obj))
+    assert abs(res[0]["outer"] - ref.outer) <= 2
