@@ -674,6 +674,7 @@ __global__ void corr_rhs_kernel(int64_t n, const double* x, const double* dxp, c
 }
 // iterate update: x += ap dx ; z += ad dz   (n-space)  and  y += ad dy (m-space)
 __global__ void update_n_kernel(int64_t n, double* x, const double* dx, double* z, const double* dz, const double* sc) {
+  if (sc[S_PCGBRK] != 0.0 || sc[S_NYSFAIL] != 0.0) return;   // discarded iteration: the iterate stays
   const double ap = sc[S_AP], ad = sc[S_AD];
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     x[j] = fma(ap, dx[j], x[j]);
@@ -681,6 +682,7 @@ __global__ void update_n_kernel(int64_t n, double* x, const double* dx, double* 
   }
 }
 __global__ void update_m_kernel(int64_t m, double* y, const double* dy1, const double* dy2, const double* sc) {
+  if (sc[S_PCGBRK] != 0.0 || sc[S_NYSFAIL] != 0.0) return;
   const double ad = sc[S_AD];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = fma(ad, dy1[i] + dy2[i], y[i]);
@@ -919,6 +921,23 @@ __global__ void set_slots_kernel(double* sc, int k0, double v0, int k1, double v
   if (k0 >= 0) sc[k0] = v0;
   if (k1 >= 0) sc[k1] = v1;
   if (k2 >= 0) sc[k2] = v2;
+}
+// latch a finished PCG solve: iteration count into `slot`, graph-loop iterations accumulated, breakdown flag
+__global__ void pcg_latch_kernel(double* sc, int slot) {
+  sc[slot] = sc[S_ITERS];
+  sc[S_GITACC] += sc[S_GITER];
+  if (sc[S_STATUS] == (double)NYS_EBREAKDOWN) sc[S_PCGBRK] = 1.0;
+}
+int launch_pcg_latch(nys_ctx* ctx, int slot) {
+  pcg_latch_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc, slot);
+  ctx->launches++;
+  return ctx->check_launch("pcg_latch");
+}
+__global__ void flag_max_kernel(double* sc, int dst, int src) { sc[dst] = fmax(sc[dst], sc[src]); }
+int launch_flag_max(nys_ctx* ctx, int dst, int src) {
+  flag_max_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc, dst, src);
+  ctx->launches++;
+  return ctx->check_launch("flag_max");
 }
 int launch_set_slots(nys_ctx* ctx, int k0, double v0, int k1, double v1, int k2, double v2) {
   set_slots_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc, k0, v0, k1, v1, k2, v2);

@@ -125,6 +125,8 @@ int launch_pred_rhs_m(nys_ctx* ctx, int64_t m, const double* b, const double* ax
                       double delta, double* rp);
 int launch_corr_rhs(nys_ctx* ctx, int64_t n, const double* x, const double* dxp, const double* dzp, const double* d,
                     double* rxz, double* xiau, double* t);
+int launch_pcg_latch(nys_ctx* ctx, int slot);
+int launch_flag_max(nys_ctx* ctx, int dst, int src);
 int launch_update_n(nys_ctx* ctx, int64_t n, double* x, const double* dx, double* z, const double* dz);
 int launch_update_m(nys_ctx* ctx, int64_t m, double* y, const double* dy1, const double* dy2);
 int launch_axpby(nys_ctx* ctx, int64_t n, double a, const double* u, double b, const double* v, double* out);

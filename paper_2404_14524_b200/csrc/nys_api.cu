@@ -300,8 +300,11 @@ int apply_At(nys_ctx* ctx, const MatvecCall& c) { return launch_matvec(ctx, c); 
 // ------------------------------------------------------------------------------------------
 // Alg. 1: Nystrom factors from the sketch Y (m x l, ld mp) and Omega (ld mp)
 // ------------------------------------------------------------------------------------------
+// defer: no host read at all (one host round trip per outer iteration, ipm_impl): a failed Cholesky of
+// Omega^T Y_nu or of a CholeskyQR pass only raises the device flag S_NYSFAIL; the caller discards the
+// iteration when it sees the flag and re-runs it with defer = false (the nu x 10 retries of A4)
 int nystrom_factor(nys_ctx* ctx, int64_t m, int ell, const double* Y, const double* Om, int64_t mp, double* U,
-                   double* lam, nys_sketch_info* info) {
+                   double* lam, nys_sketch_info* info, bool defer = false) {
   const int ldl = (int)even(ell);
   double* Ynu = ctx->wsd("nf_Ynu", (size_t)mp * ell);
   double* Bm = ctx->wsd("nf_B", (size_t)mp * ell);
@@ -334,6 +337,7 @@ int nystrom_factor(nys_ctx* ctx, int64_t m, int ell, const double* Y, const doub
     NYS_TRY(launch_gemm(ctx, g));
     NYS_TRY(launch_set_slots(ctx, S_CHOLFAIL, 0.0));
     NYS_TRY(launch_chol_inv(ctx, ell, G, ldl, Gi, ldl, 0));           // line 5: C (in G), C^{-1}
+    if (defer) { NYS_TRY(launch_flag_max(ctx, S_NYSFAIL, S_CHOLFAIL)); break; }
     NYS_TRY(read_slots(ctx));
     if (ctx->h_sc[S_CHOLFAIL] == 0.0) break;
     if (retries >= 3) {
@@ -391,8 +395,9 @@ int nystrom_factor(nys_ctx* ctx, int64_t m, int ell, const double* Y, const doub
     for (int i = 0; i < nfev; ++i) cudaEventDestroy(fev[i]);
   }
   if (info) NYS_TRY(launch_orth_err(ctx, m, ell, U, mp, S_TMP6));
-  // a failed shifted CholeskyQR pass leaves Gi / R stale: U would be silently non-orthonormal,
-  // so the flag is read on every build (one host sync per outer iteration), not only with info
+  // a failed shifted CholeskyQR pass leaves Gi / R stale: U would be silently non-orthonormal, so the
+  // flag is always checked: here, or (defer) through S_NYSFAIL with the caller's iteration read
+  if (defer) return launch_flag_max(ctx, S_NYSFAIL, S_CHOLFAIL);
   NYS_TRY(read_slots(ctx));
   if (ctx->h_sc[S_CHOLFAIL] != 0.0) {
     ctx->set_error("nys_sketch: shifted CholeskyQR of B = Y_nu C^{-1} failed (B numerically rank deficient)");
@@ -434,11 +439,11 @@ int sketch_Y(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, c
 
 // Alg. 1: sketch, then lines 3-8
 int sketch_impl(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
-                int ell, const double* Om, double* U, double* lam, nys_sketch_info* info) {
+                int ell, const double* Om, double* U, double* lam, nys_sketch_info* info, bool defer = false) {
   NvtxRange nv("nystrom_sketch_and_factor");
   double* Y = ctx->wsd("sk_Y", (size_t)even(m) * ell);
   NYS_TRY(sketch_Y(ctx, m, n, A, lda, d, e, ell, Om, Y));
-  return nystrom_factor(ctx, m, ell, Y, Om, even(m), U, lam, info);
+  return nystrom_factor(ctx, m, ell, Y, Om, even(m), U, lam, info, defer);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -529,8 +534,12 @@ int pcg_iteration(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, in
   return NYS_OK;
 }
 
+// defer_slot >= 0 (single GPU): no host read; the iteration count, the breakdown flag and the graph-loop
+// accounting are latched into device slots (launch_pcg_latch) for the caller's one read per outer
+// iteration, and res.iters = -1
 int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t ldu, const double* s,
-             const double* rhs, double* x, int max_iter, PcgResult& res, const CholFactors* chol = nullptr) {
+             const double* rhs, double* x, int max_iter, PcgResult& res, const CholFactors* chol = nullptr,
+             int defer_slot = -1) {
   NvtxRange nv("pcg_solve");
   const int64_t m = op.m;
   const int64_t mp = even(m);
@@ -547,6 +556,11 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
   if (!chol && pcg_persistent_supported(ctx, m, op.n, ell)) {
     // the whole solve is ONE cooperative launch (k_pcg.cu)
     NYS_TRY(launch_pcg_persistent(ctx, m, op.n, op.A, op.lda, op.d, op.e, U, ldu, ell, s, rhs, x, max_iter));
+    if (defer_slot >= 0) {
+      res.iters = -1;
+      res.status = 0;
+      return launch_pcg_latch(ctx, defer_slot);
+    }
     NYS_TRY(read_slots(ctx));
     res.iters = (int)ctx->h_sc[S_ITERS];
     res.status = (int)ctx->h_sc[S_STATUS];
@@ -618,6 +632,11 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
       ctx->graphs[key] = {ctx->ws_epoch, {exec, g}};
     }
     NYS_CUDA_TRY(ctx, cudaGraphLaunch(exec, ctx->stream));
+    if (defer_slot >= 0) {   // accounting and counts read later by the caller (S_GITACC, defer_slot)
+      res.iters = -1;
+      res.status = 0;
+      return launch_pcg_latch(ctx, defer_slot);
+    }
     NYS_TRY(read_slots(ctx));
     // accounting: each pcg_update run in the graph body stands for matvec + update + hred
     // (+ precond) launches of that iteration
@@ -702,6 +721,7 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
   }
   res.status = (int)ctx->h_sc[S_STATUS];
   res.rr = ctx->h_sc[S_RR];
+  if (defer_slot >= 0) NYS_TRY(launch_pcg_latch(ctx, defer_slot));   // host-loop paths: counts known, latched too
   return NYS_OK;
 }
 
@@ -1156,16 +1176,30 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     if (k == opt->max_outer) break;
     if (!std::isfinite(mu) || !std::isfinite(nrP) || !std::isfinite(nrD)) { status = NYS_EBREAKDOWN; break; }
     NvtxRange nv_outer("outer_iteration");
+    // One host round trip per outer iteration (f3): the Nystrom build, both PCG solves and the step
+    // run with deferred checks (device flags, latched counts) and everything is read with the
+    // residuals at the end.  Attempt 1 re-runs the iteration with the host checks when attempt 0
+    // raised S_NYSFAIL (the step was discarded on the device: the iterate is unchanged).
+    const int last_build0 = last_build, ell_built0 = ell_built;
+    const int64_t base_its0 = base_its;
+    const bool no_defer = getenv("NYS_NO_DEFER") != nullptr || use_chol;
     nys_iter_record rec{};
+    bool built_now = false;
+    bool broke = false;
+    const double delta_build = delta;
+    const auto t_it = std::chrono::steady_clock::now();
+    for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool defer = attempt == 0 && !no_defer;
+    last_build = last_build0; ell_built = ell_built0; base_its = base_its0;
+    rec = nys_iter_record{};
     rec.k = k; rec.mu = mu; rec.rel_p = rel_p; rec.rel_d = rel_d; rec.rho = rho; rec.delta = delta;
-    auto t_it = std::chrono::steady_clock::now();
     if (gen) NYS_TRY(launch_gen_scaling(ctx, n, vt, q, x, z, w, sv, rho, d));
     else NYS_TRY(launch_scaling(ctx, n, q, x, z, rho, d));
     NormalOp op;
     NYS_TRY(AO.normal_op(d, delta, op));
     NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[0], ctx->stream));
-    bool built_now = false;
-    const double delta_build = delta;
+    NYS_TRY(launch_set_slots(ctx, S_PCGBRK, 0.0, S_NYSFAIL, 0.0, S_GITACC, 0.0));
+    built_now = false;
     if (use_chol) {                                                   // P:250-349, every iteration
       NYS_TRY(chol_build(ctx, op, ell, CF));
       rec.prec_built = 1;
@@ -1176,7 +1210,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
                            ell_k != ell_built;
       if (rebuild) {                                                  // f3: reuse between rebuilds
         NYS_TRY(gen_omega(ctx, m, ell_k, opt->seed, (uint64_t)k + 1, Om));
-        NYS_TRY(sketch_impl(ctx, m, op.n, op.A, op.lda, op.d, op.e, ell_k, Om, U, lamh, nullptr));
+        NYS_TRY(sketch_impl(ctx, m, op.n, op.A, op.lda, op.d, op.e, ell_k, Om, U, lamh, nullptr, defer));
         last_build = k;
         base_its = -1;
         rec.prec_built = 1;
@@ -1200,9 +1234,10 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
     rec.ell = use_chol ? ell : ell_built;
     NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[2], ctx->stream));
-    NYS_TRY(pcg_impl(ctx, op, use_chol ? ell : ell_built, U, mp, scoef, xi, dyp, opt->pcg_max_iter, pr, cfp));
+    NYS_TRY(pcg_impl(ctx, op, use_chol ? ell : ell_built, U, mp, scoef, xi, dyp, opt->pcg_max_iter, pr, cfp,
+                     defer ? (int)S_PCGI0 : -1));
     NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[3], ctx->stream));
-    if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
+    if (pr.status == NYS_EBREAKDOWN) { broke = true; break; }
     rec.pcg_pred = pr.iters;
     NYS_TRY(AO.At_dx(dyp, rd, xiau, rxz, z, x, d, dxp, dzp));        // dx, dz (A15)
     if (gen) {
@@ -1229,12 +1264,11 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(D.dot(m, xi, xi, S_XINORM));
     NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
     NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[4], ctx->stream));
-    NYS_TRY(pcg_impl(ctx, op, use_chol ? ell : ell_built, U, mp, scoef, xi, dyc, opt->pcg_max_iter, pr, cfp));
+    NYS_TRY(pcg_impl(ctx, op, use_chol ? ell : ell_built, U, mp, scoef, xi, dyc, opt->pcg_max_iter, pr, cfp,
+                     defer ? (int)S_PCGI1 : -1));
     NYS_CUDA_TRY(ctx, cudaEventRecord(pev.e[5], ctx->stream));
-    if (pr.status == NYS_EBREAKDOWN) { status = NYS_EBREAKDOWN; break; }
+    if (pr.status == NYS_EBREAKDOWN) { broke = true; break; }
     rec.pcg_corr = pr.iters;
-    last_its = (int64_t)rec.pcg_pred + rec.pcg_corr;
-    if (base_its < 0) base_its = last_its;
     NYS_TRY(AO.At_dx(dyc, nullptr, xiau, rxz, z, x, d, dxc, dzc));
     nvtxRangePop();
     // ---- combine, stepsizes, update ----
@@ -1250,6 +1284,23 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     if (gen) NYS_TRY(launch_update_n(ctx, n, w, dw, sv, ds));         // w += ap dw ; s += ad ds
     NYS_TRY(launch_update_m(ctx, m, y, dyp, dyc));
     NYS_TRY(residuals());                                             // synchronises: events complete
+    if (defer) {
+      if (ctx->h_sc[S_NYSFAIL] != 0.0) continue;                       // step discarded: re-run with host checks
+      rec.pcg_pred = (int)ctx->h_sc[S_PCGI0];
+      rec.pcg_corr = (int)ctx->h_sc[S_PCGI1];
+      if (!ctx->multi()) {   // single-GPU accounting deferred by pcg_impl (multi-rank loops count as they go)
+        const bool persistent = pcg_persistent_supported(ctx, m, op.n, use_chol ? 0 : ell_built) && !use_chol;
+        ctx->matvecs += persistent ? rec.pcg_pred + rec.pcg_corr
+                                   : std::max(rec.pcg_pred - 2, 0) + std::max(rec.pcg_corr - 2, 0);
+        ctx->launches += (int64_t)ctx->h_sc[S_GITACC] * (ell_built > 0 ? 4 : 3);
+      }
+      if (ctx->h_sc[S_PCGBRK] != 0.0) { broke = true; break; }
+    }
+    break;
+    }
+    if (broke) { status = NYS_EBREAKDOWN; break; }
+    last_its = (int64_t)rec.pcg_pred + rec.pcg_corr;
+    if (base_its < 0) base_its = last_its;
     rec.t_sketch_ms = pev.ms(0, 1);
     rec.t_pcg_ms = pev.ms(2, 3) + pev.ms(4, 5);
     t_sketch += rec.t_sketch_ms;

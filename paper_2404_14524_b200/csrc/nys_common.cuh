@@ -40,6 +40,10 @@ enum Slot : int {
   S_NU, S_SHIFT, S_CHOLFAIL, S_FRO, S_JSWEEPS, S_DELTA, S_GITER,
   // general-form initial point statistics (f1, gen_init_stats): 4 minima then 8 sums
   S_G0, S_G1, S_G2, S_G3, S_G4, S_G5, S_G6, S_G7, S_G8, S_G9, S_G10, S_G11,
+  // one host round trip per outer iteration (ipm_impl): the two PCG solves' iteration counts, a
+  // breakdown flag, a Nystrom-factorisation failure flag and the graph-path iteration accounting are
+  // latched on the device and read with the iteration's residuals
+  S_PCGI0, S_PCGI1, S_PCGBRK, S_NYSFAIL, S_GITACC,
   S_COUNT = 64
 };
 constexpr int kMaxCounters = 64;
