@@ -18,7 +18,7 @@ import pytest
 torch = pytest.importorskip("torch")
 
 from oracle import linops  # noqa: E402
-from synth import large  # noqa: E402
+from synth import large, make_config  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -116,3 +116,54 @@ def test_config4_capped_solve_residuals_match_host(setup):
     assert abs(rel_p - g["rel_p"]) <= 1e-6 * rel_p + 1e-14
     assert abs(rel_d - g["rel_d"]) <= 1e-6 * rel_d + 1e-14
     assert abs(x @ z / N - g["mu"]) <= 1e-10 * (x @ z / N)
+
+
+# ---------------------------------------------------------------------------- converged config-4 recipe
+def test_config4_recipe_converges_and_matches_oracle():
+    """BASELINE configs[4]'s recipe (A = W H + 1e-2 G, q with 30 % zeros, feasible b / c) at the full
+    problem's aspect ratio n = 8 m, reduced to m = 1000, n = 8000, l = 100: the GPU solve reaches the
+    paper's tolerance and its objective equals the oracle's to 1e-7 (the same algorithm; the late
+    outer iterations need thousands of PCG iterations)."""
+    from oracle import ippmm
+    from paper_2404_14524_b200 import Context, colmajor_device
+    inst = make_config(4, m=1000, n=8000, ell=100)
+    ctx = Context(0)
+    Ad, lda = colmajor_device(inst.A)
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    g = ctx.nys_ipppmm_solve(Ad, lda, inst.m, dv(inst.q), dv(inst.b), dv(inst.c), ell=inst.ell)
+    ctx.close()
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
+    assert g["status"] == 0 and ref.status == "optimal"
+    assert g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    print(f"config-4 recipe m=1000: gpu {g['obj']!r} ({g['outer']} outer, {g['inner']} PCG) "
+          f"oracle {ref.obj!r} ({ref.outer}, {ref.inner_total})")
+    assert abs(g["obj"] - ref.obj) <= 1e-7 * max(1.0, abs(ref.obj))
+    assert abs(g["outer"] - ref.outer) <= 2
+
+
+def test_config4_recipe_m5000_converges_with_host_kkt_certificate():
+    """The same recipe at m = 5000, n = 40000 (A = 1.6 GB), l = 200: converged to 1e-8; the KKT
+    residuals recomputed on the host from the GPU's x, y, z, x, z > 0, and the objective inside the
+    bracket of the generator's feasible primal-dual point [b^T y0 - 1/2 x0^T Q x0, 1/2 x0^T Q x0 + c^T x0]
+    (SURVEY §8(c) P9)."""
+    from paper_2404_14524_b200 import Context, colmajor_device
+    inst = make_config(4, m=5000, n=40000, ell=200)
+    ctx = Context(0)
+    Ad, lda = colmajor_device(inst.A)
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    g = ctx.nys_ipppmm_solve(Ad, lda, inst.m, dv(inst.q), dv(inst.b), dv(inst.c), ell=inst.ell)
+    ctx.close()
+    assert g["status"] == 0
+    x, y, z = (g[k].cpu().numpy() for k in ("x", "y", "z"))
+    A = inst.A
+    assert x.min() > 0 and z.min() > 0
+    assert np.linalg.norm(inst.b - A @ x) / (1 + np.linalg.norm(inst.b)) <= 1.01e-8
+    assert np.linalg.norm(inst.c + inst.q * x - A.T @ y - z) / (1 + np.linalg.norm(inst.c)) <= 1.01e-8
+    f = 0.5 * x @ (inst.q * x) + inst.c @ x
+    lo = inst.b @ inst.y0 - 0.5 * inst.x0 @ (inst.q * inst.x0)
+    hi = 0.5 * inst.x0 @ (inst.q * inst.x0) + inst.c @ inst.x0
+    band = abs(g["obj"] - g["dual_obj"]) + np.linalg.norm(x) * np.linalg.norm(inst.c + inst.q * x - A.T @ y - z) + \
+        np.linalg.norm(y) * np.linalg.norm(inst.b - A @ x)
+    print(f"config-4 recipe m=5000: f = {f!r} in [{lo!r}, {hi!r}], {g['outer']} outer, {g['inner']} PCG, band {band:.2e}")
+    assert abs(f - g["obj"]) <= 1e-10 * abs(f)
+    assert lo - band <= f <= hi + band
