@@ -677,6 +677,190 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
 }
 
 // ------------------------------------------------------------------------------------------
+// Small problems (m <= 256, A <= ~1 MB, e.g. BASELINE config 0: m = 100, n = 400): the whole PCG solve
+// in ONE CTA of 1024 threads.  The persistent grid kernel above pays three grid barriers per
+// iteration (~13.6 us at config 0: pure synchronisation latency); here every synchronisation is a
+// __syncthreads and A (L2-resident after the first iteration) is read by 32 warps, one column per
+// warp per step: the dot a_j^T p (lanes over rows, a shuffle sum), t_j = d_j a_j^T p, and the rank-1
+// update of the warp's row accumulators — the fused one-pass matvec of k_matvec.cu in miniature.
+// Same recurrence as the oracle's textbook PCG: zero start, alpha = r^T z / p^T w with
+// p^T w formed from w, the absolute stop ||r|| <= tol checked before the first iteration and after
+// every update, breakdown on p^T w <= 0; r^T z = ||r||^2 + (U^T r)^T h (z = r + U h).
+// ------------------------------------------------------------------------------------------
+struct PcgSParams {
+  const double* A;
+  int64_t lda, m, n;
+  const double* d;
+  const double* e;
+  const double* U;
+  int64_t ldu;
+  int ell;
+  const double* s;
+  const double* rhs;
+  double* x;
+  double* sc;
+  int max_iter;
+};
+
+template <int MR, int NT>
+__global__ void __launch_bounds__(NT, 1) pcg_small_kernel(const PcgSParams P) {
+  constexpr int M32 = 32 * MR;
+  constexpr int NW = NT / 32;
+  extern __shared__ double wpart[];            // [NW warps][M32] row partials of w
+  __shared__ double r_s[M32], z_s[M32], p_s[M32], w_s[M32];
+  __shared__ double g_s[256], h_s[256];
+  __shared__ double red[32];
+  __shared__ double bsum;
+  const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31;
+  const int m = (int)P.m, ell = P.ell;
+  const int64_t n = P.n;
+  const double delta = P.sc[S_DELTA];
+  const double tol = P.sc[S_TOL];
+  // block sum in a fixed order (warp butterflies, then warp 0 over the 32 warp sums)
+  auto block_sum = [&](double v) -> double {
+    v = warp_sum(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      double t = (lane < NW) ? red[lane] : 0.0;
+      t = warp_sum(t);
+      if (lane == 0) bsum = t;
+    }
+    __syncthreads();
+    const double out = bsum;
+    __syncthreads();
+    return out;
+  };
+  // z = r + U h with h = s o (U^T r) (s_i = (lam_l + mu)/(lam_i + mu) - 1); returns r^T z
+  auto precond = [&](double rr) -> double {
+    if (ell == 0) {
+      for (int i = tid; i < m; i += blockDim.x) z_s[i] = r_s[i];
+      __syncthreads();
+      return rr;
+    }
+    for (int c = warp; c < ell; c += NW) {
+      const double* u = P.U + (size_t)c * P.ldu;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int i = lane + 32 * k;
+        if (i < m) acc = fma(u[i], r_s[i], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) { g_s[c] = acc; h_s[c] = P.s[c] * acc; }
+    }
+    __syncthreads();
+    for (int i = tid; i < m; i += blockDim.x) {
+      double acc = r_s[i];
+      for (int c = 0; c < ell; ++c) acc = fma(P.U[(size_t)c * P.ldu + i], h_s[c], acc);
+      z_s[i] = acc;
+    }
+    double gh = 0.0;
+    for (int c = tid; c < ell; c += blockDim.x) gh = fma(g_s[c], h_s[c], gh);
+    return rr + block_sum(gh);     // (its barriers also publish z_s)
+  };
+
+  for (int i = tid; i < m; i += blockDim.x) {
+    r_s[i] = P.rhs[i];
+    P.x[i] = 0.0;
+  }
+  __syncthreads();
+  double rr = block_sum(tid < m ? r_s[tid] * r_s[tid] : 0.0);
+  int iters = 0, status = 0;
+  bool conv = sqrt(rr) <= tol;
+  double rz = 0.0;
+  if (!conv) {
+    rz = precond(rr);
+    for (int i = tid; i < m; i += blockDim.x) p_s[i] = z_s[i];
+    __syncthreads();
+  }
+  while (!conv && iters < P.max_iter) {
+    // ---- w = A (d o (A^T p)) : one column per warp per step ----
+    double pr[MR], wacc[MR];
+#pragma unroll
+    for (int k = 0; k < MR; ++k) {
+      const int i = lane + 32 * k;
+      pr[k] = (i < m) ? p_s[i] : 0.0;
+      wacc[k] = 0.0;
+    }
+    for (int64_t j = warp; j < n; j += NW) {
+      const double* a = P.A + j * P.lda;
+      double av[MR];
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int i = lane + 32 * k;
+        av[k] = (i < m) ? __ldg(a + i) : 0.0;
+        acc = fma(av[k], pr[k], acc);
+      }
+      const double t = __ldg(P.d + j) * warp_sum(acc);
+#pragma unroll
+      for (int k = 0; k < MR; ++k) wacc[k] = fma(av[k], t, wacc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < MR; ++k) wpart[warp * M32 + lane + 32 * k] = wacc[k];
+    __syncthreads();
+    double pw = 0.0;
+    if (tid < m) {
+      double wsum = 0.0;
+      for (int q = 0; q < NW; ++q) wsum += wpart[q * M32 + tid];
+      const double wi = wsum + (delta + (P.e ? P.e[tid] : 0.0)) * p_s[tid];
+      w_s[tid] = wi;
+      pw = p_s[tid] * wi;
+    }
+    pw = block_sum(pw);
+    if (!(pw > 0.0) || !isfinite(pw)) { status = NYS_EBREAKDOWN; break; }
+    const double alpha = rz / pw;
+    double rloc = 0.0;
+    if (tid < m) {
+      P.x[tid] = fma(alpha, p_s[tid], P.x[tid]);
+      const double ri = fma(-alpha, w_s[tid], r_s[tid]);
+      r_s[tid] = ri;
+      rloc = ri * ri;
+    }
+    rr = block_sum(rloc);
+    ++iters;
+    if (sqrt(rr) <= tol) { conv = true; break; }
+    if (!isfinite(rr)) { status = NYS_EBREAKDOWN; break; }
+    const double rzn = precond(rr);
+    if (!(rzn > 0.0) || !isfinite(rzn)) { status = NYS_EBREAKDOWN; break; }
+    const double beta = rzn / rz;
+    rz = rzn;
+    if (tid < m) p_s[tid] = fma(beta, p_s[tid], z_s[tid]);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    P.sc[S_ITERS] = (double)iters;
+    P.sc[S_STATUS] = (double)status;
+    P.sc[S_DONE] = 1.0;
+    P.sc[S_RZ] = rz;
+    P.sc[S_RR] = rr;
+  }
+}
+
+bool pcg_small_supported(nys_ctx* ctx, int64_t m, int64_t n, int ell) {
+  return !ctx->multi() && m <= 256 && n > 0 && ell <= 256 && (double)m * (double)n * 8.0 <= 1.0e6 &&
+         getenv("NYS_NO_PCG_SMALL") == nullptr && getenv("NYS_NO_PERSISTENT") == nullptr;
+}
+
+int launch_pcg_small(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
+                     const double* U, int64_t ldu, int ell, const double* s, const double* rhs, double* x, int max_iter) {
+  PcgSParams P{};
+  P.A = A; P.lda = lda; P.m = m; P.n = n; P.d = d; P.e = e; P.U = U; P.ldu = ldu; P.ell = ell; P.s = s;
+  P.rhs = rhs; P.x = x; P.sc = ctx->sc; P.max_iter = max_iter;
+  // rows per lane MR and threads NT sized so the column loop stays in registers (64 / 128 registers)
+  if (m <= 64) {
+    pcg_small_kernel<2, 1024><<<1, 1024, 32 * 64 * 8, ctx->stream>>>(P);
+  } else if (m <= 128) {
+    pcg_small_kernel<4, 512><<<1, 512, 16 * 128 * 8, ctx->stream>>>(P);
+  } else {
+    pcg_small_kernel<8, 512><<<1, 512, 16 * 256 * 8, ctx->stream>>>(P);
+  }
+  ctx->launches++;
+  return ctx->check_launch("pcg_small");
+}
+
+// ------------------------------------------------------------------------------------------
 struct PcgCfg {
   int T, GT, RPT, CPG;
 };

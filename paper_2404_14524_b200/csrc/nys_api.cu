@@ -554,8 +554,11 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
   const double* done = ctx->sc + S_DONE;
   NYS_TRY(launch_set_slots(ctx, S_DELTA, op.delta, S_GITER, 0.0));
   if (!chol && pcg_persistent_supported(ctx, m, op.n, ell)) {
-    // the whole solve is ONE cooperative launch (k_pcg.cu)
-    NYS_TRY(launch_pcg_persistent(ctx, m, op.n, op.A, op.lda, op.d, op.e, U, ldu, ell, s, rhs, x, max_iter));
+    // the whole solve is ONE launch (k_pcg.cu): one CTA for small problems, else cooperative grid-wide
+    if (pcg_small_supported(ctx, m, op.n, ell))
+      NYS_TRY(launch_pcg_small(ctx, m, op.n, op.A, op.lda, op.d, op.e, U, ldu, ell, s, rhs, x, max_iter));
+    else
+      NYS_TRY(launch_pcg_persistent(ctx, m, op.n, op.A, op.lda, op.d, op.e, U, ldu, ell, s, rhs, x, max_iter));
     if (defer_slot >= 0) {
       res.iters = -1;
       res.status = 0;
