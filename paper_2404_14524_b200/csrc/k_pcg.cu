@@ -15,11 +15,15 @@
 // iterations (A does not depend on the iterate) and prefetches further panels into L2, so HBM keeps
 // streaming through the barrier phases.  Grid barriers involve the consumer threads only; the
 // producer polls a stop flag so it can never block the exit.
+#include <cooperative_groups.h>
+
 #include <chrono>
 #include <cstdlib>
 #include <vector>
 
 #include "k_vec.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace nys {
 
@@ -709,27 +713,25 @@ __global__ void __launch_bounds__(NT, 1) pcg_small_kernel(const PcgSParams P) {
   extern __shared__ double wpart[];            // [NW warps][M32] row partials of w
   __shared__ double r_s[M32], z_s[M32], p_s[M32], w_s[M32];
   __shared__ double g_s[256], h_s[256];
-  __shared__ double red[32];
-  __shared__ double bsum;
+  __shared__ double red[64];
   const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31;
   const int m = (int)P.m, ell = P.ell;
   const int64_t n = P.n;
   const double delta = P.sc[S_DELTA];
   const double tol = P.sc[S_TOL];
   // block sum in a fixed order (warp butterflies, then warp 0 over the 32 warp sums)
+  // block sum with ONE barrier: the warp sums go to alternating buffers and every thread adds the NW
+  // of them in the same order (a buffer is rewritten only after the next call's barrier)
+  int rb = 0;
   auto block_sum = [&](double v) -> double {
     v = warp_sum(v);
-    if (lane == 0) red[warp] = v;
+    if (lane == 0) red[rb * 32 + warp] = v;
     __syncthreads();
-    if (warp == 0) {
-      double t = (lane < NW) ? red[lane] : 0.0;
-      t = warp_sum(t);
-      if (lane == 0) bsum = t;
-    }
-    __syncthreads();
-    const double out = bsum;
-    __syncthreads();
-    return out;
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) t += red[rb * 32 + q];
+    rb ^= 1;
+    return t;
   };
   // z = r + U h with h = s o (U^T r) (s_i = (lam_l + mu)/(lam_i + mu) - 1); returns r^T z
   auto precond = [&](double rr) -> double {
@@ -838,6 +840,186 @@ __global__ void __launch_bounds__(NT, 1) pcg_small_kernel(const PcgSParams P) {
   }
 }
 
+// The same solve on a thread-block CLUSTER of C CTAs with A resident in shared memory: CTA r holds the
+// columns [r n / C, (r + 1) n / C) of A (and of d) in its shared memory for the whole solve (loaded
+// once), so the matvec never touches L2 again.  Per iteration ONE cluster barrier: every CTA writes its
+// partial w (own columns) into a double-buffered shared slot, the barrier publishes them, and every CTA
+// sums the C partials of every row in rank order through DSMEM — identical bits everywhere — and then
+// runs the m-space work (alpha, x, r, U^T r, z, beta, p) redundantly with __syncthreads only.  The
+// double buffer is safe with one barrier per iteration: a CTA can overwrite slot k & 1 only after the
+// barrier of iteration k + 1, which every peer reaches after its reads of iteration k.
+template <int MR, int NT>
+__global__ void __launch_bounds__(NT, 1) pcg_cluster_small_kernel(const PcgSParams P) {
+  constexpr int M32 = 32 * MR;
+  constexpr int NW = NT / 32;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
+  extern __shared__ double dsm[];
+  const int m = (int)P.m, ell = P.ell;
+  const int64_t n = P.n;
+  const int64_t c_lo = (n * rank) / C, c_hi = (n * (rank + 1)) / C;
+  const int ncols = (int)(c_hi - c_lo);
+  // the DSMEM-visible slot first: its offset must be the same in every CTA (map_shared_rank maps offsets)
+  double* part = dsm;                                // [2][M32] this CTA's partial w
+  double* wpart = part + 2 * M32;                    // [NW][M32]
+  double* As = wpart + NW * M32;                     // [ncols][M32], rows >= m zero
+  double* ds = As + (size_t)ncols * M32;             // [ncols]
+  __shared__ double r_s[M32], z_s[M32], p_s[M32], w_s[M32], x_s[M32];
+  __shared__ double g_s[256], h_s[256];
+  __shared__ double red[64];
+  const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31;
+  const double delta = P.sc[S_DELTA];
+  const double tol = P.sc[S_TOL];
+  for (int64_t e = tid; e < (int64_t)ncols * M32; e += NT) {
+    const int j = (int)(e / M32), i = (int)(e % M32);
+    As[e] = (i < m) ? P.A[(c_lo + j) * P.lda + i] : 0.0;
+  }
+  for (int j = tid; j < ncols; j += NT) ds[j] = P.d[c_lo + j];
+  // block sum with ONE barrier: the warp sums go to alternating buffers and every thread adds the NW
+  // of them in the same order (a buffer is rewritten only after the next call's barrier)
+  int rb = 0;
+  auto block_sum = [&](double v) -> double {
+    v = warp_sum(v);
+    if (lane == 0) red[rb * 32 + warp] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) t += red[rb * 32 + q];
+    rb ^= 1;
+    return t;
+  };
+  auto precond = [&](double rr) -> double {
+    if (ell == 0) {
+      for (int i = tid; i < m; i += NT) z_s[i] = r_s[i];
+      __syncthreads();
+      return rr;
+    }
+    for (int c = warp; c < ell; c += NW) {
+      const double* u = P.U + (size_t)c * P.ldu;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) {
+        const int i = lane + 32 * k;
+        if (i < m) acc = fma(__ldg(u + i), r_s[i], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) { g_s[c] = acc; h_s[c] = P.s[c] * acc; }
+    }
+    __syncthreads();
+    for (int i = tid; i < m; i += NT) {
+      double acc = r_s[i];
+#pragma unroll 8
+      for (int c = 0; c < ell; ++c) acc = fma(__ldg(P.U + (size_t)c * P.ldu + i), h_s[c], acc);
+      z_s[i] = acc;
+    }
+    double gh = 0.0;
+    for (int c = tid; c < ell; c += NT) gh = fma(g_s[c], h_s[c], gh);
+    return rr + block_sum(gh);
+  };
+  for (int i = tid; i < M32; i += NT) {
+    r_s[i] = (i < m) ? P.rhs[i] : 0.0;
+    x_s[i] = 0.0;
+    p_s[i] = 0.0;
+  }
+  __syncthreads();
+  double rr = block_sum(tid < m ? r_s[tid] * r_s[tid] : 0.0);
+  int iters = 0, status = 0;
+  bool conv = sqrt(rr) <= tol;
+  double rz = 0.0;
+  if (!conv) {
+    rz = precond(rr);
+    for (int i = tid; i < m; i += NT) p_s[i] = z_s[i];
+    __syncthreads();
+  }
+  cluster.sync();                                    // every CTA's A slice loaded before any DSMEM traffic
+  int k = 0;
+  while (!conv && iters < P.max_iter) {
+    double pr[MR], wacc[MR];
+#pragma unroll
+    for (int q = 0; q < MR; ++q) {
+      pr[q] = p_s[lane + 32 * q];
+      wacc[q] = 0.0;
+    }
+    for (int j = warp; j < ncols; j += NW) {
+      const double* a = As + (size_t)j * M32;
+      double av[MR];
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < MR; ++q) {
+        av[q] = a[lane + 32 * q];
+        acc = fma(av[q], pr[q], acc);
+      }
+      const double t = ds[j] * warp_sum(acc);
+#pragma unroll
+      for (int q = 0; q < MR; ++q) wacc[q] = fma(av[q], t, wacc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < MR; ++q) wpart[warp * M32 + lane + 32 * q] = wacc[q];
+    __syncthreads();
+    double* mypart = part + (k & 1) * M32;
+    for (int i = tid; i < m; i += NT) {
+      double v = 0.0;
+      for (int q = 0; q < NW; ++q) v += wpart[q * M32 + i];
+      mypart[i] = v;
+    }
+    cluster.sync();                                  // the C partials of this iteration are published
+    double pw = 0.0;
+    if (tid < m) {
+      // all C remote loads in flight at once, then the sum in rank order
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = (q < C) ? cluster.map_shared_rank(mypart, q)[tid] : 0.0;
+      double wsum = 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) wsum += v[q];
+      const double wi = wsum + (delta + (P.e ? P.e[tid] : 0.0)) * p_s[tid];
+      w_s[tid] = wi;
+      pw = p_s[tid] * wi;
+    }
+    pw = block_sum(pw);
+    ++k;
+    if (!(pw > 0.0) || !isfinite(pw)) { status = NYS_EBREAKDOWN; break; }
+    const double alpha = rz / pw;
+    double rloc = 0.0;
+    if (tid < m) {
+      x_s[tid] = fma(alpha, p_s[tid], x_s[tid]);
+      const double ri = fma(-alpha, w_s[tid], r_s[tid]);
+      r_s[tid] = ri;
+      rloc = ri * ri;
+    }
+    rr = block_sum(rloc);
+    ++iters;
+    if (sqrt(rr) <= tol) { conv = true; break; }
+    if (!isfinite(rr)) { status = NYS_EBREAKDOWN; break; }
+    const double rzn = precond(rr);
+    if (!(rzn > 0.0) || !isfinite(rzn)) { status = NYS_EBREAKDOWN; break; }
+    const double beta = rzn / rz;
+    rz = rzn;
+    if (tid < m) p_s[tid] = fma(beta, p_s[tid], z_s[tid]);
+    __syncthreads();
+  }
+  if (rank == 0) {
+    for (int i = tid; i < m; i += NT) P.x[i] = x_s[i];
+    if (tid == 0) {
+      P.sc[S_ITERS] = (double)iters;
+      P.sc[S_STATUS] = (double)status;
+      P.sc[S_DONE] = 1.0;
+      P.sc[S_RZ] = rz;
+      P.sc[S_RR] = rr;
+    }
+  }
+  cluster.sync();                                    // no CTA leaves while a peer may still read its partials
+}
+
+// the cluster variant holds A in shared memory: at most 16 CTAs x 150 KB of padded columns
+static int small_cluster_size(int64_t m, int64_t n) {
+  const int64_t m32 = m <= 64 ? 64 : m <= 128 ? 128 : 256;
+  const double bytes = (double)n * (double)m32 * 8.0;
+  int C = (int)((bytes + 64e3 - 1) / 64e3);          // ~64 KB of A per CTA
+  if (C < 2) C = 2;
+  if (bytes / C > 150e3) C = (int)((bytes + 150e3 - 1) / 150e3);
+  return C;
+}
 bool pcg_small_supported(nys_ctx* ctx, int64_t m, int64_t n, int ell) {
   return !ctx->multi() && m <= 256 && n > 0 && ell <= 256 && (double)m * (double)n * 8.0 <= 1.0e6 &&
          getenv("NYS_NO_PCG_SMALL") == nullptr && getenv("NYS_NO_PERSISTENT") == nullptr;
@@ -848,6 +1030,34 @@ int launch_pcg_small(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_
   PcgSParams P{};
   P.A = A; P.lda = lda; P.m = m; P.n = n; P.d = d; P.e = e; P.U = U; P.ldu = ldu; P.ell = ell; P.s = s;
   P.rhs = rhs; P.x = x; P.sc = ctx->sc; P.max_iter = max_iter;
+  // cluster variant (A in shared memory) unless disabled or A needs more than 16 CTAs
+  const int C = small_cluster_size(m, n);
+  if (C <= 16 && getenv("NYS_PCG_SMALL_1CTA") == nullptr) {
+    const int64_t m32 = m <= 64 ? 64 : m <= 128 ? 128 : 256;
+    const int64_t maxcols = (n + C - 1) / C;
+    const size_t smem = ((size_t)maxcols * m32 + ((maxcols + 1) & ~1) + 16 * m32 + 2 * m32) * 8;
+    const void* k = m <= 64 ? (const void*)pcg_cluster_small_kernel<2, 512>
+                  : m <= 128 ? (const void*)pcg_cluster_small_kernel<4, 512> : (const void*)pcg_cluster_small_kernel<8, 512>;
+    NYS_TRY(ensure_max_smem(ctx, k, smem));
+    if (C > 8) NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)C);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (m <= 64) NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, pcg_cluster_small_kernel<2, 512>, P));
+    else if (m <= 128) NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, pcg_cluster_small_kernel<4, 512>, P));
+    else NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, pcg_cluster_small_kernel<8, 512>, P));
+    ctx->launches++;
+    return ctx->check_launch("pcg_cluster_small");
+  }
   // rows per lane MR and threads NT sized so the column loop stays in registers (64 / 128 registers)
   if (m <= 64) {
     pcg_small_kernel<2, 1024><<<1, 1024, 32 * 64 * 8, ctx->stream>>>(P);
