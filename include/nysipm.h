@@ -129,7 +129,7 @@ typedef struct {
  *   Steps: Y = A(d o (A^T Omega)) (+ e o Omega) [fp64 DMMA GEMMs, allreduce over ranks];
  *   nu = eps(||Y||_F); Y_nu = Y + nu Omega; C = chol(Omega^T Y_nu); B = Y_nu C^{-1};
  *   thin SVD of B by shifted CholeskyQR3 + one-sided Jacobi on the ell x ell factor.
- *   Errors: NYS_EINVAL (ell < 1, ell > m, ell > 256, delta <= 0), NYS_ECHOL.
+ *   Errors: NYS_EINVAL (ell < 1, ell > m, ell > 1024, delta <= 0), NYS_ECHOL.
  * ------------------------------------------------------------------------------------- */
 int nys_sketch(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda,
                const double* d, const double* e, double delta, int ell,

@@ -119,8 +119,10 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(int ell, double* G, int l
   const int lx = n | 1;                   // odd leading dimension of X: conflict-free column access
   double* W = SM ? csm : gws;             // n x n, ld n : the factor
   double* X = W + (size_t)n * n;          // n x n, ld lx : R^{-1}
-  __shared__ double rsq[256];
-  __shared__ double rowk[256];  // row k gathered once per step (a strided, bank-conflicted read otherwise)
+  __shared__ double rsq_s[SM ? 256 : 1];
+  __shared__ double rowk_s[SM ? 256 : 1];  // row k gathered once per step (a strided, bank-conflicted read otherwise)
+  double* rsq = SM ? rsq_s : X + (size_t)n * lx;          // global variant (ell > 113): after X in gws
+  double* rowk = SM ? rowk_s : rsq + n;
   __shared__ double shift;
   const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31, nw = blockDim.x >> 5;
   for (int e = tid; e < n * n; e += blockDim.x) {
@@ -365,6 +367,95 @@ __global__ void __launch_bounds__(1024) chol_inv_small_kernel(int ell, double* G
   }
 }
 
+// Same contract as chol_inv_kernel for ell > 226 (no single-CTA shared-memory layout fits): the
+// same right-looking unblocked Cholesky and the same parallel back substitution for R^{-1}, spread
+// over a cooperative grid with a grid barrier between the steps (W, X, the pivot row in global memory,
+// L2-resident: 10 MB at ell = 800).  One CTA of 256 threads took 205 ms at ell = 800.
+__device__ __forceinline__ void cgrid_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++epoch;
+    const unsigned int target = epoch * nblocks;
+    red_add_release_gpu(bar, 1u);
+    while (ld_relaxed_gpu(bar) < target) {
+    }
+    fence_acquire_gpu();
+  }
+  __syncthreads();
+}
+__global__ void __launch_bounds__(1024) chol_inv_grid_kernel(int n, double* G, int ldg, double* Rinv, int ldr,
+                                                             int shift_mode, double* sc, double* W, double* X,
+                                                             double* rowk, double* rsq, double* shiftp,
+                                                             unsigned int* bar) {
+  const int lx = n | 1;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, GT = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = gt >> 5, GW = GT >> 5;
+  unsigned int epoch = 0;
+  for (int64_t e = gt; e < (int64_t)n * n; e += GT) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    W[i + (size_t)j * n] = 0.5 * (G[i + (size_t)j * ldg] + G[j + (size_t)i * ldg]);
+  }
+  for (int64_t e = gt; e < (int64_t)n * lx; e += GT) X[e] = 0.0;
+  cgrid_barrier(bar, gridDim.x, epoch);
+  if (gt == 0) {
+    double s = 0.0;
+    if (shift_mode == 1) {
+      double tr = 0.0;
+      for (int i = 0; i < n; ++i) tr += W[i + (size_t)i * n];
+      s = 11.0 * (sc[S_SHIFT] * n + (double)n * (n + 1)) * 0x1p-53 * tr;
+    }
+    *shiftp = s;
+  }
+  cgrid_barrier(bar, gridDim.x, epoch);
+  if (shift_mode == 1) {
+    const double sh = __ldcg(shiftp);
+    for (int64_t i = gt; i < n; i += GT) W[i + (size_t)i * n] += sh;
+    cgrid_barrier(bar, gridDim.x, epoch);
+  }
+  for (int k = 0; k < n; ++k) {
+    const double piv = __ldcg(W + k + (size_t)k * n);
+    if (!(piv > 0.0) || !isfinite(piv)) {        // grid-uniform: every thread read the same pivot
+      if (gt == 0) sc[S_CHOLFAIL] = 1.0;
+      return;
+    }
+    for (int64_t i = k + 1 + gt; i < n; i += GT) rowk[i] = __ldcg(W + k + (size_t)i * n);
+    cgrid_barrier(bar, gridDim.x, epoch);
+    const double inv = 1.0 / piv;
+    for (int64_t j = k + 1 + gw; j < n; j += GW) {
+      const double akj = __ldcg(rowk + j) * inv;
+      for (int64_t i = k + 1 + lane; i <= j; i += 32)
+        W[i + (size_t)j * n] = fma(-__ldcg(rowk + i), akj, __ldcg(W + i + (size_t)j * n));
+    }
+    cgrid_barrier(bar, gridDim.x, epoch);
+  }
+  for (int64_t i = gt; i < n; i += GT) rsq[i] = 1.0 / sqrt(__ldcg(W + i + (size_t)i * n));
+  cgrid_barrier(bar, gridDim.x, epoch);
+  for (int64_t e = gt; e < (int64_t)n * n; e += GT) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    const double w = __ldcg(W + i + (size_t)j * n);
+    W[i + (size_t)j * n] = (i <= j) ? w * __ldcg(rsq + i) : 0.0;
+  }
+  for (int64_t j = gt; j < n; j += GT) X[j + (size_t)j * lx] = 1.0;
+  cgrid_barrier(bar, gridDim.x, epoch);
+  for (int i = n - 1; i >= 0; --i) {
+    const double inv = 1.0 / __ldcg(W + i + (size_t)i * n);
+    for (int64_t j = i + gt; j < n; j += GT) X[i + (size_t)j * lx] *= inv;
+    cgrid_barrier(bar, gridDim.x, epoch);
+    const int64_t cols = n - i;
+    for (int64_t e = gt; e < (int64_t)i * cols; e += GT) {
+      const int k = (int)(e % i), j = i + (int)(e / i);
+      X[k + (size_t)j * lx] = fma(-__ldcg(W + k + (size_t)i * n), __ldcg(X + i + (size_t)j * lx), __ldcg(X + k + (size_t)j * lx));
+    }
+    cgrid_barrier(bar, gridDim.x, epoch);
+  }
+  for (int64_t e = gt; e < (int64_t)n * n; e += GT) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    G[i + (size_t)j * ldg] = __ldcg(W + i + (size_t)j * n);
+    Rinv[i + (size_t)j * ldr] = __ldcg(X + i + (size_t)j * lx);
+  }
+}
+
 int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int ldr, int shift_mode) {
   const size_t need = ((size_t)ell * ell + (size_t)ell * (ell | 1)) * sizeof(double);
   const size_t need_packed = (size_t)ell * (ell + 1) / 2 * sizeof(double);
@@ -386,9 +477,27 @@ int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int
   } else if (need <= 200 * 1024) {
     NYS_TRY(ensure_max_smem(ctx, (const void*)chol_inv_kernel<true>, 200 * 1024));
     chol_inv_kernel<true><<<1, 256, need, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc, nullptr);
-  } else {
-    double* gws = ctx->wsd("chol_ws", (size_t)ell * ell + (size_t)ell * (ell | 1));
+  } else if (getenv("NYS_CHOL_1CTA") != nullptr) {
+    double* gws = ctx->wsd("chol_ws", (size_t)ell * ell + (size_t)ell * (ell | 1) + 2 * (size_t)ell);
     chol_inv_kernel<false><<<1, 256, 0, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc, gws);
+  } else {
+    double* W = ctx->wsd("cg_W", (size_t)ell * ell);
+    double* X = ctx->wsd("cg_X", (size_t)ell * (ell | 1));
+    double* rowk = ctx->wsd("cg_rowk", (size_t)ell);
+    double* rsq = ctx->wsd("cg_rsq", (size_t)ell);
+    double* shiftp = ctx->wsd("cg_shift", 1);
+    unsigned int* bar = (unsigned int*)ctx->ws("cg_bar", 64);
+    NYS_CUDA_TRY(ctx, cudaMemsetAsync(bar, 0, 64, ctx->stream));
+    int blocks = (int)(((int64_t)ell * ell / 2 + 1023) / 1024);   // ~one element of the first update per thread
+    int occ = 0;
+    NYS_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chol_inv_grid_kernel, 1024, 0));
+    if (blocks > occ * ctx->num_sms) blocks = occ * ctx->num_sms;
+    if (blocks > 64) blocks = 64;                  // grid barriers get slower with more CTAs
+    if (blocks < 1) blocks = 1;
+    double* scp = ctx->sc;
+    void* args[] = {&ell, &G, &ldg, &Rinv, &ldr, &shift_mode, &scp, &W, &X, &rowk, &rsq, &shiftp, &bar};
+    NYS_CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)chol_inv_grid_kernel, dim3(blocks), dim3(1024), args, 0,
+                                                 ctx->stream));
   }
   ctx->launches++;
   return ctx->check_launch("chol_inv");
@@ -1087,7 +1196,179 @@ static int launch_jacobi_t(nys_ctx* ctx, int ell, const double* R, int ldr, doub
   return ctx->check_launch("jacobi");
 }
 
+// ------------------------------------------------------------------------------------------
+// The same one-sided Jacobi for ell > 256 (the paper's ell = 800 on STL-10): X (= R^T) and V
+// no longer fit any CTA or cluster's shared memory, so they live in global memory (L2-resident: 10 MB
+// at ell = 800) and the ell / 2 pairs of a round go to ell / 2 warps spread over a cooperative grid,
+// one pair per warp, columns streamed in 32-element chunks; a grid barrier (monotonic counter)
+// separates the rounds.  Same circle ordering, the same fp64 rotation, exact norms recomputed each
+// sweep and updated within it, the same absolute floor and convergence test as jacobi_kernel.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void jgrid_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++epoch;
+    const unsigned int target = epoch * nblocks;
+    red_add_release_gpu(bar, 1u);
+    while (ld_relaxed_gpu(bar) < target) {
+    }
+    fence_acquire_gpu();
+  }
+  __syncthreads();
+}
+
+template <int E>
+__global__ void __launch_bounds__(256) jacobi_grid_kernel(int n, const double* R, int ldr, double* Vout, int ldv,
+                                                           double* sigma, double* X, double* V, double* nrm,
+                                                           double* cmax, unsigned int* bar, double* jsweeps) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const int gw = blockIdx.x * nw + warp;                  // global warp id
+  const int W = gridDim.x * nw;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, GT = gridDim.x * blockDim.x;
+  unsigned int epoch = 0;
+  for (int64_t e = gt; e < (int64_t)n * n; e += GT) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    X[e] = R[j + (size_t)i * ldr];                        // X = R^T
+    V[e] = (i == j) ? 1.0 : 0.0;
+  }
+  jgrid_barrier(bar, gridDim.x, epoch);
+  const int P = (n % 2 == 0) ? n : n + 1;
+  const double tol = fmax(1e-15, (double)n * 0x1p-53);
+  const double tol2 = tol * tol;
+  __shared__ double smax[32];   // <= 8 warps (256 threads)
+  __shared__ int srot;
+  int sweep = 0;
+  for (; sweep < 30; ++sweep) {
+    double mx = 0.0;
+    for (int j = gw; j < n; j += W) {                     // exact column norms
+      double a = 0.0;
+      for (int i = lane; i < n; i += 32) a = fma(X[i + (size_t)j * n], X[i + (size_t)j * n], a);
+      a = warp_sum(a);
+      if (lane == 0) nrm[j] = a;
+      mx = fmax(mx, a);
+    }
+    if (lane == 0) smax[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int q = 0; q < nw; ++q) b = fmax(b, smax[q]);
+      cmax[blockIdx.x] = b;
+      srot = 0;
+    }
+    jgrid_barrier(bar, gridDim.x, epoch);
+    double gmax = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) gmax = fmax(gmax, __ldcg(cmax + b));
+    const double floor_g = 1e-2 * 0x1p-52 * gmax;
+    for (int r = 0; r < P - 1; ++r) {
+      for (int pi = gw; pi < P / 2; pi += W) {
+        int a, b;
+        if (pi == 0) { a = r; b = P - 1; }
+        else {
+          a = r + pi; if (a >= P - 1) a -= P - 1;
+          b = r - pi; if (b < 0) b += P - 1;
+        }
+        if (a >= n || b >= n) continue;
+        const int p = a < b ? a : b, q = a < b ? b : a;
+        double* xp = X + (size_t)p * n;
+        double* xq = X + (size_t)q * n;
+        // the two columns in registers (E elements per lane, every load in flight at once), one dot
+        double a0[E], a1[E];
+        double ga = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = lane + 32 * e;
+          a0[e] = (i < n) ? __ldcg(xp + i) : 0.0;
+          a1[e] = (i < n) ? __ldcg(xq + i) : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) ga = fma(a0[e], a1[e], ga);
+        ga = warp_sum(ga);
+        const double al = __ldcg(nrm + p), be = __ldcg(nrm + q);
+        if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {
+          double c, sn, t;
+          jacobi_rotation(al, be, ga, c, sn, t);
+          double* vp = V + (size_t)p * n;
+          double* vq = V + (size_t)q * n;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int i = lane + 32 * e;
+            if (i < n) {
+              xp[i] = c * a0[e] - sn * a1[e];
+              xq[i] = sn * a0[e] + c * a1[e];
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int i = lane + 32 * e;
+            a0[e] = (i < n) ? __ldcg(vp + i) : 0.0;
+            a1[e] = (i < n) ? __ldcg(vq + i) : 0.0;
+          }
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int i = lane + 32 * e;
+            if (i < n) {
+              vp[i] = c * a0[e] - sn * a1[e];
+              vq[i] = sn * a0[e] + c * a1[e];
+            }
+          }
+          if (lane == 0) {
+            nrm[p] = fmax(al - t * ga, 0.0);
+            nrm[q] = be + t * ga;
+            srot = 1;
+          }
+        }
+      }
+      jgrid_barrier(bar, gridDim.x, epoch);
+    }
+    // any rotation in the sweep, anywhere: per-CTA flags through cmax (reused), one more barrier
+    if (threadIdx.x == 0) cmax[gridDim.x + blockIdx.x] = (double)srot;
+    jgrid_barrier(bar, gridDim.x, epoch);
+    bool any = false;
+    for (int b = 0; b < (int)gridDim.x; ++b) any = any || (__ldcg(cmax + gridDim.x + b) != 0.0);
+    if (!any) break;
+  }
+  if (gt == 0) jsweeps[0] = (double)(sweep + 1);
+  // sigma_j = ||x_j||, rank sort descending (ties by index), V permuted
+  for (int j = gw; j < n; j += W) {
+    double a = 0.0;
+    for (int i = lane; i < n; i += 32) a = fma(__ldcg(X + i + (size_t)j * n), __ldcg(X + i + (size_t)j * n), a);
+    a = warp_sum(a);
+    if (lane == 0) nrm[j] = sqrt(a);
+  }
+  jgrid_barrier(bar, gridDim.x, epoch);
+  for (int j = gt; j < n; j += GT) {
+    const double sj = __ldcg(nrm + j);
+    int rk = 0;
+    for (int k = 0; k < n; ++k) {
+      const double sk = __ldcg(nrm + k);
+      rk += (sk > sj) || (sk == sj && k < j);
+    }
+    sigma[rk] = sj;
+    for (int i = 0; i < n; ++i) Vout[i + (size_t)rk * ldv] = __ldcg(V + i + (size_t)j * n);
+  }
+}
+
+static int launch_jacobi_grid(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+  const int pairs = (ell + 1) / 2;
+  const int blocks = (pairs + 7) / 8;                     // one warp per pair, 256-thread CTAs
+  double* X = ctx->wsd("jg_X", (size_t)ell * ell);
+  double* Vw = ctx->wsd("jg_V", (size_t)ell * ell);
+  double* nrm = ctx->wsd("jg_nrm", (size_t)ell);
+  double* cmax = ctx->wsd("jg_cmax", (size_t)2 * blocks);
+  unsigned int* bar = (unsigned int*)ctx->ws("jg_bar", 64);
+  NYS_CUDA_TRY(ctx, cudaMemsetAsync(bar, 0, 64, ctx->stream));
+  double* js = ctx->sc + S_JSWEEPS;
+  void* args[] = {&ell, &R, &ldr, &V, &ldv, &sigma, &X, &Vw, &nrm, &cmax, &bar, &js};
+  // E = 32 elements per lane: ell <= 1024 (kMaxEll)
+  NYS_CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)jacobi_grid_kernel<32>, dim3(blocks), dim3(256), args, 0,
+                                               ctx->stream));
+  ctx->launches++;
+  return ctx->check_launch("jacobi_grid");
+}
+
 int launch_jacobi_svd(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+  if (ell > 256) return launch_jacobi_grid(ctx, ell, R, ldr, V, ldv, sigma);
   // block Jacobi over an 8-CTA cluster from ell = block_min on (tuning override NYS_JACOBI_BLOCK_MIN)
   int block_min = 72;   // measured crossover (sketch at m = 20532): 64 equal, 80 2.65 vs 3.59 ms, 112 3.99 vs 6.21 ms
   if (const char* e = getenv("NYS_JACOBI_BLOCK_MIN")) block_min = atoi(e);

@@ -296,6 +296,9 @@ struct PcgUpdArgs {
 // accumulates in its own shared-memory row (tile after tile), then the 8 warp rows are summed in
 // a fixed order -> one (1 + ell)-row of block partials.  pcg_hred_kernel (one block per column)
 // finishes the reduction: rr, the convergence test, h = s o (U^T r).
+// BIG (ell > 256, up to 1024): the per-warp rows of U^T r partials live in dynamic shared memory and the
+// U^T r pass runs over column chunks of 256 (lane L of a warp covers chunk columns L, L + 32, ...)
+template <bool BIG>
 __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
   if (A.cond != 0ull && blockIdx.x == 0 && threadIdx.x == 0) A.sc[S_GITER] += 1.0;  // launch accounting
   if (A.sc[S_DONE] != 0.0) {  // converged / max_iter / breakdown: end the graph-resident loop
@@ -303,7 +306,10 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
     return;
   }
   const double delta = A.delta_slot ? A.sc[S_DELTA] : A.delta;
-  __shared__ double wred[8][257];   // [warp][1 + c] : rr and U^T r partials of this block
+  __shared__ double wred_s[BIG ? 1 : 8 * 257];  // [warp][1 + c] : rr and U^T r partials of this block
+  extern __shared__ double wred_d[];
+  const int wld = BIG ? 1 + A.ell : 257;
+  double* wred = BIG ? wred_d : wred_s;
   __shared__ double rsh[256];
   __shared__ double s_alpha;
   __shared__ int s_ok;
@@ -325,7 +331,7 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
     }
   }
   const int ncol = 1 + A.ell;
-  for (int c = lane; c < ncol; c += 32) wred[warp][c] = 0.0;
+  for (int c = lane; c < ncol; c += 32) wred[warp * wld + c] = 0.0;
   __syncthreads();
   if (!A.init && !s_ok) {
     if (blockIdx.x == 0 && tid == 0) { A.sc[S_STATUS] = (double)NYS_EBREAKDOWN; A.sc[S_DONE] = 1.0; }
@@ -364,12 +370,12 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
     }
     // rr: this warp's 32 rows
     const double rrw = warp_sum(ri * ri);
-    if (lane == 0) wred[warp][0] += rrw;
+    if (lane == 0) wred[warp * wld] += rrw;
     rsh[tid] = ri;  // rows past hi hold 0
     __syncthreads();
     // U^T r with U stored ROW-major (Ut[i][c], row stride ldu): warp w takes tile rows w, w+8, ...;
     // lane L accumulates columns L, L+32, ... (contiguous 256-B reads of each row, no shuffles)
-    {
+    for (int c0 = 0; c0 < (BIG ? A.ell : 1); c0 += 256) {
       double gacc[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) gacc[k] = 0.0;
@@ -381,7 +387,7 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
           const int row = rr0 + 8 * q;
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            const int c = lane + 32 * k;
+            const int c = c0 + lane + 32 * k;
             uv[q][k] = (row < tile_rows && c < A.ell) ? A.U[(size_t)(t0 + row) * A.ldu + c] : 0.0;
           }
         }
@@ -395,15 +401,16 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(const PcgUpdArgs A) {
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const int c = lane + 32 * k;
-        if (c < A.ell) wred[warp][1 + c] += gacc[k];
+        const int c = c0 + lane + 32 * k;
+        if (c < A.ell) wred[warp * wld + 1 + c] += gacc[k];
       }
     }
     __syncthreads();
   }
   __syncthreads();
   for (int c = tid; c < ncol; c += 256) {
-    const double v = ((wred[0][c] + wred[1][c]) + (wred[2][c] + wred[3][c])) + ((wred[4][c] + wred[5][c]) + (wred[6][c] + wred[7][c]));
+    const double v = ((wred[0 * wld + c] + wred[1 * wld + c]) + (wred[2 * wld + c] + wred[3 * wld + c])) +
+                     ((wred[4 * wld + c] + wred[5 * wld + c]) + (wred[6 * wld + c] + wred[7 * wld + c]));
     A.part[(size_t)c * gridDim.x + blockIdx.x] = v;
   }
 }
@@ -469,13 +476,14 @@ struct PcgPrecArgs {
 // row; rz = r^T z partials, the last block finishes rz and beta.
 __global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
   if (A.sc[S_DONE] != 0.0) return;
-  __shared__ double hsh[256];
+  __shared__ double hsh[1024];
   const int tid = threadIdx.x, lane = tid & 31;
   for (int c = tid; c < A.ell; c += blockDim.x) hsh[c] = __ldcg(A.h + c);
   __syncthreads();
-  double hl[8];
+  constexpr int KH = 32;                       // lane L covers columns L, L + 32, ... (ell <= 1024)
+  double hl[KH];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) hl[k] = (lane + 32 * k < A.ell) ? hsh[lane + 32 * k] : 0.0;
+  for (int k = 0; k < KH; ++k) hl[k] = (lane + 32 * k < A.ell) ? hsh[lane + 32 * k] : 0.0;
   const int64_t nw = (int64_t)gridDim.x * 8;
   const int64_t w0 = (int64_t)blockIdx.x * 8 + (tid >> 5);
   double rz = 0.0;
@@ -487,7 +495,7 @@ __global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
       double a = 0.0;
       if (i < A.m) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < KH; ++k) {
           const int c = lane + 32 * k;
           if (c < A.ell) a = fma(A.U[(size_t)i * A.ldu + c], hl[k], a);
         }
@@ -565,7 +573,13 @@ int launch_pcg_update(nys_ctx* ctx, int init, int64_t m, double* x, double* r, c
   A.rows_per_block = rpb;
   A.part = ctx->wsd("pcg_upd_part", (size_t)(1 + ell) * g);
   A.counter = ctx->counters + 1;
-  pcg_update_kernel<<<(unsigned)g, 256, 0, ctx->stream>>>(A);
+  if (ell > 256) {
+    const size_t sm = (size_t)8 * (1 + ell) * sizeof(double);
+    NYS_TRY(ensure_max_smem(ctx, (const void*)pcg_update_kernel<true>, sm));
+    pcg_update_kernel<true><<<(unsigned)g, 256, sm, ctx->stream>>>(A);
+  } else {
+    pcg_update_kernel<false><<<(unsigned)g, 256, 0, ctx->stream>>>(A);
+  }
   ctx->launches++;
   NYS_TRY(ctx->check_launch("pcg_update"));
   pcg_hred_kernel<<<(unsigned)(1 + ell), 256, 0, ctx->stream>>>(A, g);

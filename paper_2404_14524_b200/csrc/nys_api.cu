@@ -222,6 +222,10 @@ int allreduce_slots(nys_ctx* ctx, int first, int count, bool is_min = false) {
 }
 
 inline int64_t even(int64_t v) { return (v + 1) & ~int64_t(1); }
+// largest Nystrom rank: the sketch, factorisation (global-memory Cholesky and grid Jacobi above 256)
+// and graph-path PCG kernels take up to 1024 columns (the paper runs ell = 800 on STL-10);
+// the partial Cholesky preconditioner and the persistent PCG keep 256
+constexpr int kMaxEll = 1024;
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 int read_slots(nys_ctx* ctx) {
@@ -1618,8 +1622,8 @@ static int nys_sketch_body(nys_ctx* ctx, int64_t m, int64_t n, const double* A, 
                       double delta, int ell, const double* Omega, double* U, double* lambda, nys_sketch_info* info) {
   NYS_GUARD_BEGIN
   NYS_TRY(check_A(ctx, m, n, A, lda));
-  if (ell < 1 || ell > m || ell > 256 || !(delta > 0) || !Omega || !U || !lambda || (n > 0 && !d)) {
-    ctx->set_error("nys_sketch: need 1 <= ell <= min(m, 256), delta > 0, non-null buffers");
+  if (ell < 1 || ell > m || ell > kMaxEll || !(delta > 0) || !Omega || !U || !lambda || (n > 0 && !d)) {
+    ctx->set_error("nys_sketch: need 1 <= ell <= min(m, 1024), delta > 0, non-null buffers");
     return NYS_EINVAL;
   }
   cudaSetDevice(ctx->device);
@@ -1754,7 +1758,7 @@ static int nys_pcg_solve_body(nys_ctx* ctx, int64_t m, int64_t n, const double* 
                          double* x, double tol_abs, int max_iter, nys_pcg_info* info) {
   NYS_GUARD_BEGIN
   NYS_TRY(check_A(ctx, m, n, A, lda));
-  if (ell < 0 || ell > m || ell > 256 || (ell > 0 && (!U || !lambda)) || !rhs || !x || max_iter < 0 || delta < 0 ||
+  if (ell < 0 || ell > m || ell > kMaxEll || (ell > 0 && (!U || !lambda)) || !rhs || !x || max_iter < 0 || delta < 0 ||
       (n > 0 && !d) || (ell > 0 && !(mu_prec > 0))) {
     ctx->set_error("nys_pcg_solve: bad arguments");
     return NYS_EINVAL;
@@ -1847,7 +1851,7 @@ static int nys_ipppmm_solve_body(nys_ctx* ctx, const nys_qp* qp, const nys_optio
     return NYS_EINVAL;
   }
   if (!qp->host_ptrs) NYS_TRY(check_A(ctx, qp->m, qp->structure >= 1 ? qp->nd : qp->n, qp->A, qp->lda));
-  if (opt->ell < 0 || opt->ell > qp->m || opt->ell > 256 || !(opt->tol > 0)) {
+  if (opt->ell < 0 || opt->ell > qp->m || opt->ell > (opt->precond == 1 ? 256 : kMaxEll) || !(opt->tol > 0)) {
     ctx->set_error("nys_ipppmm_solve: bad options");
     return NYS_EINVAL;
   }

@@ -155,7 +155,10 @@ def _nys_gpu(ctx, A, d, ell, Om, delta=1e-2):
                                        (64, 3000, 64, 64), (501, 2000, 30, 500),
                                        # ell > 112: cluster Jacobi (C = 2 / 4 / 8) and the packed Cholesky
                                        (600, 2000, 128, 600), (900, 2500, 160, 900), (700, 3000, 200, 700),
-                                       (1000, 2000, 256, 80)])
+                                       (1000, 2000, 256, 80),
+                                       # ell > 256 (the paper's ell = 800): global-memory Cholesky,
+                                       # grid-wide Jacobi
+                                       (1200, 1600, 512, 1200), (1000, 2400, 800, 1000), (1200, 1600, 512, 100)])
 def test_nystrom_factors_parity(ctx, m, n, ell, r):
     rs = np.random.default_rng(m + ell)
     W = rs.standard_normal((m, r))
@@ -618,3 +621,37 @@ def test_pcg_leading_dimension_layouts(ctx, lda_multiple):
                              iters)
     assert info.iters == iters
     assert rel(xg.cpu().numpy(), xo) <= 1e-9
+
+
+@pytest.mark.parametrize("m,n,ell", [(1000, 1500, 512), (900, 1200, 800)])
+def test_pcg_large_rank_graph_path_matches_oracle(ctx, m, n, ell):
+    """ell > 256: the graph-path PCG (U^T r over column chunks, z = r + U h with 32 columns per lane)
+    for 15 fixed iterations against oracle.pcg with the same Nystrom factors."""
+    from paper_2404_14524_b200 import colmajor_device
+    rs = np.random.default_rng(m + ell)
+    A = rs.standard_normal((m, 60)) @ rs.standard_normal((60, n)) / np.sqrt(n) + 1e-2 * rs.standard_normal((m, n))
+    d = rs.uniform(0.01, 2.0, n)
+    delta, iters = 1e-4, 15
+    rhs = rs.standard_normal(m)
+    Om = orng.gaussian_omega(m, ell, 2, 3)
+    Uo, lamo, _ = nystrom.nystrom_from_sketch(linops.sketch(A, d, Om), Om)
+    pinv = lambda v: nystrom.precond_inv_apply(Uo, lamo, delta, v)  # noqa: E731
+    xo, io = oracle_pcg(lambda v: linops.normal_matvec(A, d, v, delta), rhs, pinv, tol_abs=0.0, max_iter=iters)
+    Ad, lda = colmajor_device(A)
+    xg = torch.empty(m, dtype=torch.float64, device="cuda")
+    info = ctx.nys_pcg_solve(Ad, lda, m, dev(d), None, delta, ell, dev_cm(Uo), dev(lamo), delta, dev(rhs), xg, 0.0,
+                             iters)
+    assert info.iters == io["iters"]
+    assert rel(xg.cpu().numpy(), xo) <= 1e-9
+
+
+def test_ipppmm_large_rank_matches_oracle(ctx):
+    """A Nys-IP-PMM solve with ell = 300 > 256 (every outer iteration: grid Jacobi, global Cholesky,
+    graph-path PCG) against the oracle at the strict objective gate."""
+    inst = make_config(0, m=400, n=1600, ell=300)
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=300))
+    g = _solve_gpu(ctx, inst, 300)
+    assert ref.status == "optimal" and g["status"] == 0
+    assert g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
+    assert obj_agree(g, ref, inst=inst)
+    assert abs(g["outer"] - ref.outer) <= 2
