@@ -43,7 +43,8 @@ with torch.cuda.stream(st):
     ctx.nys_sketch_apply(A, lda, m, d, None, ell, Om, Y)
 t_apply, t_apply_min = timed(lambda: ctx.nys_sketch_apply(A, lda, m, d, None, ell, Om, Y))
 with torch.cuda.stream(st):
-    ctx.nys_sketch(A, lda, m, d, None, 1e-3, ell, Om, U, lam)
+    info = ctx.nys_sketch(A, lda, m, d, None, 1e-3, ell, Om, U, lam)
+print(f"jacobi sweeps {info.jacobi_sweeps}, chol retries {info.chol_retries}, orth err {info.orth_err:.2e}")
 t_sk, t_sk_min = timed(lambda: ctx.nys_sketch(A, lda, m, d, None, 1e-3, ell, Om, U, lam))
 fl = 4.0 * m * n * ell
 print(f"m={m} n={n} ell={ell}: sketch GEMMs {t_apply * 1e3:.2f} ms (min {t_apply_min * 1e3:.2f}) = {fl / t_apply / 1e12:.2f} "
