@@ -16,8 +16,9 @@
 // partials in a fixed order (deterministic) and applies (delta + e) v, additive terms and
 // the optional PCG dot p^T w / alpha = rz / p^T w.
 //
-// The same kernel also provides the T-only pass (A^T v with IPM epilogues) and the N-only
-// pass (A u) that Alg. 4 needs.
+// The same kernel also provides the T-only pass (A^T v with IPM epilogues), the N-only
+// pass (A u) that Alg. 4 needs, and both at once on independent operands
+// (MV_BOTH: A^T y with an epilogue and A x from the same read of A — the residuals).
 #include <cstdlib>
 #include <mutex>
 
@@ -344,7 +345,8 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
             for (int c = 0; c < CPG; ++c) sb[c * ss + rows_valid] = 0.0;
           }
 #pragma unroll
-          for (int c = 0; c < CPG; ++c) dcur[c] = (MODE == MV_FUSED && col0 + c < P.n) ? __ldg(P.d + col0 + c) : 0.0;
+          for (int c = 0; c < CPG; ++c)   // FUSED: d_j;  BOTH: the N-part coefficient u_j
+            dcur[c] = (col0 + c < P.n) ? (MODE == MV_FUSED ? __ldg(P.d + col0 + c) : MODE == MV_BOTH ? __ldg(P.u + col0 + c) : 0.0) : 0.0;
           double pd[CPG];
 #pragma unroll
           for (int c = 0; c < CPG; ++c) {
@@ -393,11 +395,18 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
             for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
             pd[c] = x;
           }
-          if (MODE == MV_FUSED) {
+          if (MODE == MV_TONLY || MODE == MV_BOTH) {  // raw dot to global; epilogue after the loop
+            if (crank == 0) {
+#pragma unroll
+              for (int c = 0; c < CPG; ++c)
+                if (lig == c && cprev + c < P.n) P.tbuf[cprev + c] = pd[c];
+            }
+          }
+          if (MODE == MV_FUSED || MODE == MV_BOTH) {
             double t[CPG];
 #pragma unroll
-            for (int c = 0; c < CPG; ++c) t[c] = dprev[c] * pd[c];
-            if (lig == 0 && crank == 0) {
+            for (int c = 0; c < CPG; ++c) t[c] = MODE == MV_FUSED ? dprev[c] * pd[c] : dprev[c];
+            if (MODE == MV_FUSED && lig == 0 && crank == 0) {
 #pragma unroll
               for (int c = 0; c < CPG; ++c) pwacc = fma(t[c], pd[c], pwacc);  // d_j (a_j^T v)^2
             }
@@ -408,12 +417,6 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
 #pragma unroll
                 for (int i = 0; i < RPT; ++i) wacc[i] = fma(sb[c * ssi + lig + GT * i], t[c], wacc[i]);
               }
-            }
-          } else {  // MV_TONLY: raw dot to global; epilogue after the loop
-            if (crank == 0) {
-#pragma unroll
-              for (int c = 0; c < CPG; ++c)
-                if (lig == c && cprev + c < P.n) P.tbuf[cprev + c] = pd[c];
             }
           }
           if (odd_owner) fence_proxy_async_shared();
@@ -453,7 +456,8 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
       double dpre[CPG];  // scaling of this group's columns, loaded before the dot (hides L2 latency)
 #pragma unroll
       for (int c = 0; c < CPG; ++c)
-        dpre[c] = ((MODE == MV_FUSED || MODE == MV_DIAG) && col0 + c < P.n) ? __ldg(P.d + col0 + c) : 0.0;
+        dpre[c] = (col0 + c < P.n) ? ((MODE == MV_FUSED || MODE == MV_DIAG) ? __ldg(P.d + col0 + c)
+                                       : MODE == MV_BOTH ? __ldg(P.u + col0 + c) : 0.0) : 0.0;
       double t[CPG];
       if (MODE != MV_NONLY && MODE != MV_DIAG) {
         double pd[CPG];
@@ -490,11 +494,15 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
 #pragma unroll
             for (int c = 0; c < CPG; ++c) pwacc = fma(t[c], pd[c], pwacc);  // d_j (a_j^T v)^2
           }
-        } else {  // MV_TONLY: raw dot to global; the epilogue runs after the loop (no stall here)
+        } else {  // MV_TONLY / MV_BOTH: raw dot to global; the epilogue runs after the loop (no stall here)
           if (crank == 0) {
 #pragma unroll
             for (int c = 0; c < CPG; ++c)
               if (lig == c && col0 + c < P.n) P.tbuf[col0 + c] = pd[c];
+          }
+          if (MODE == MV_BOTH) {
+#pragma unroll
+            for (int c = 0; c < CPG; ++c) t[c] = dpre[c];
           }
         }
       } else if (MODE == MV_DIAG) {
@@ -516,7 +524,7 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
     }
     }
   }
-  if (MODE == MV_TONLY) {
+  if (MODE == MV_TONLY || MODE == MV_BOTH) {
     __syncthreads();  // this CTA's raw dots are visible to all its threads
     if (crank == 0) {
       for (int64_t e = tid; e < niter * BN; e += T + 32) {
@@ -678,6 +686,16 @@ static MvKernel kernel_for(const MvCfg& c, bool clu) {
   return matvec_kernel<512, 512, 16, 1, MODE, true, false>;
 }
 
+static MvKernel kernel_for_mode(int mode, const MvCfg& c, bool clu) {
+  switch (mode) {
+    case MV_FUSED: return kernel_for<MV_FUSED>(c, clu);
+    case MV_TONLY: return kernel_for<MV_TONLY>(c, clu);
+    case MV_NONLY: return kernel_for<MV_NONLY>(c, clu);
+    case MV_BOTH: return kernel_for<MV_BOTH>(c, clu);
+    default: return kernel_for<MV_DIAG>(c, clu);
+  }
+}
+
 struct MvPlan {
   MvCfg cfg;
   int cl = 1;
@@ -747,8 +765,7 @@ static int make_plan(nys_ctx* ctx, int mode, int64_t m, int64_t n, int64_t lda, 
     if (st < 2) st = 2;
     G.rs = rs_; G.c = c_; G.stages = st;
     G.smem = mv_smem_bytes(c_, rs_, st, cl_, clu_);
-    G.k = (mode == MV_FUSED) ? kernel_for<MV_FUSED>(c_, clu_) : (mode == MV_TONLY) ? kernel_for<MV_TONLY>(c_, clu_)
-          : (mode == MV_NONLY) ? kernel_for<MV_NONLY>(c_, clu_) : kernel_for<MV_DIAG>(c_, clu_);
+    G.k = kernel_for_mode(mode, c_, clu_);
     NYS_TRY(ensure_max_smem(ctx, (const void*)G.k, G.smem));
     if (cl_ > 8) NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(G.k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     return NYS_OK;
@@ -914,7 +931,7 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
   if (c.mode != MV_TONLY) Wp = ctx->wsd("mv_partials", (size_t)pl.nparts * wp_ld);
   double* pwp = nullptr;
   if (c.mode == MV_FUSED && c.pcg_fused) pwp = ctx->wsd("mv_pwp", (size_t)pl.grid);
-  double* tbuf = (c.mode == MV_TONLY) ? ctx->wsd("mv_tbuf", (size_t)(c.n > 0 ? c.n : 1)) : nullptr;
+  double* tbuf = (c.mode == MV_TONLY || c.mode == MV_BOTH) ? ctx->wsd("mv_tbuf", (size_t)(c.n > 0 ? c.n : 1)) : nullptr;
   // finalize parameters (used in-kernel when fusable, else by mv_finalize)
   FinParams F{};
   int fgrid = (int)((c.m + 15) / 16);
@@ -950,9 +967,7 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
     P.fuse_fin = fuse ? 1 : 0;
     P.fin = F;
     P.gbar = gbar;
-    MvKernel k = (c.mode == MV_FUSED) ? kernel_for<MV_FUSED>(pl.cfg, pl.cl > 1)
-                 : (c.mode == MV_TONLY) ? kernel_for<MV_TONLY>(pl.cfg, pl.cl > 1)
-                 : (c.mode == MV_NONLY) ? kernel_for<MV_NONLY>(pl.cfg, pl.cl > 1) : kernel_for<MV_DIAG>(pl.cfg, pl.cl > 1);
+    MvKernel k = kernel_for_mode(c.mode, pl.cfg, pl.cl > 1);
     if (c.n > 0) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)pl.grid);

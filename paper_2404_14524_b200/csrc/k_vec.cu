@@ -474,13 +474,15 @@ struct PcgPrecArgs {
 // z = r + U h with U stored ROW-major (Ut[i][c], row stride ldu): one warp per row, lane L
 // covering columns L, L+32, ... (contiguous reads), 4 rows in flight per warp, a shuffle sum per
 // row; rz = r^T z partials, the last block finishes rz and beta.
+// KH = columns per lane / 32: 8 for ell <= 256, 32 up to 1024 (the small variant keeps the unrolled
+// loop and the register footprint of the common case)
+template <int KH>
 __global__ void __launch_bounds__(256) pcg_precond_kernel(const PcgPrecArgs A) {
   if (A.sc[S_DONE] != 0.0) return;
-  __shared__ double hsh[1024];
+  __shared__ double hsh[32 * KH];
   const int tid = threadIdx.x, lane = tid & 31;
   for (int c = tid; c < A.ell; c += blockDim.x) hsh[c] = __ldcg(A.h + c);
   __syncthreads();
-  constexpr int KH = 32;                       // lane L covers columns L, L + 32, ... (ell <= 1024)
   double hl[KH];
 #pragma unroll
   for (int k = 0; k < KH; ++k) hl[k] = (lane + 32 * k < A.ell) ? hsh[lane + 32 * k] : 0.0;
@@ -597,7 +599,8 @@ int launch_pcg_precond(nys_ctx* ctx, int init, int64_t m, const double* r, doubl
   A.nsub = 0;
   A.part = ctx->wsd("pcg_prec_part", (size_t)g);
   A.counter = ctx->counters + 2;
-  pcg_precond_kernel<<<(unsigned)g, 256, 0, ctx->stream>>>(A);
+  if (ell > 256) pcg_precond_kernel<32><<<(unsigned)g, 256, 0, ctx->stream>>>(A);
+  else pcg_precond_kernel<8><<<(unsigned)g, 256, 0, ctx->stream>>>(A);
   ctx->launches++;
   return ctx->check_launch("pcg_precond");
 }

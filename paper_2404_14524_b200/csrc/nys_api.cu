@@ -893,6 +893,23 @@ struct AOps {
     NYS_TRY(At_vec(y));
     return launch_epi_rd(ctx, n, c, q, x, atv, z, out);
   }
+  // the residual products from ONE read of A (structure 0): ax = A x and rd = c + q x - A^T y - z
+  // by the MV_BOTH pass (NYS_NO_MV_BOTH=1: the two separate passes)
+  int Ax_At_rd(const double* x, double* ax, const double* y, const double* c, const double* q, const double* z,
+               double* rd) {
+    static const bool split = getenv("NYS_NO_MV_BOTH") != nullptr;
+    if (structure != 0 || split) {
+      NYS_TRY(Ax(x, ax, nullptr));
+      return At_rd(y, c, q, x, z, rd);
+    }
+    MatvecCall mc;
+    mc.mode = MV_BOTH; mc.m = m; mc.n = n; mc.lda = lda; mc.A = A;
+    mc.z = y; mc.tep = TE_RD; mc.t1 = rd; mc.ta = c; mc.tb = q; mc.tc = x; mc.td = z;
+    mc.u = x; mc.out = ax; mc.sgn = 1.0;
+    NYS_TRY(launch_matvec(ctx, mc));
+    if (ctx->multi()) NYS_TRY(allreduce(ctx, ax, (size_t)m));
+    return NYS_OK;
+  }
   // dx = d (A^T dy - r_d - xi_au); dz = (r_xz - z dx) / x
   int At_dx(const double* dy, const double* rd, const double* xiau, const double* rxz, const double* z,
             const double* x, const double* d, double* dx, double* dz) {
@@ -1149,9 +1166,8 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   auto residuals = [&]() -> int {
     // r_P = b - A x ; r_D = c + Q x - A^T y - z ; ||r_P||^2, ||r_D||^2, x^T z
     NvtxRange nvr("residuals");
-    NYS_TRY(AO.Ax(x, ax, nullptr));
+    NYS_TRY(AO.Ax_At_rd(x, ax, y, c, q, z, rD));
     NYS_TRY(launch_axpby(ctx, m, 1.0, b, -1.0, ax, rP));
-    NYS_TRY(AO.At_rd(y, c, q, x, z, rD));
     if (gen) {                                                        // G1: r_D += s ; r_U = u - x - w on J
       NYS_TRY(launch_axpby(ctx, n, 1.0, rD, 1.0, sv, rD));
       NYS_TRY(launch_gen_ru(ctx, n, vt, ub, x, w, ru));

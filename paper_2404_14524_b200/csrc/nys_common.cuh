@@ -277,7 +277,8 @@ namespace nys {
 int ensure_max_smem(nys_ctx* ctx, const void* fn, size_t bytes);
 
 // MV_DIAG: out_i = sum_j d_j A_ij^2 (the diagonal of A D A^T; partial Cholesky)
-enum MatvecMode { MV_FUSED = 0, MV_TONLY = 1, MV_NONLY = 2, MV_DIAG = 3 };
+// MV_BOTH: T-only pass on v (epilogue tep) AND out = sgn A u + add from the same read of A
+enum MatvecMode { MV_FUSED = 0, MV_TONLY = 1, MV_NONLY = 2, MV_DIAG = 3, MV_BOTH = 4 };
 
 // where the fused PCG matvec left its per-cluster w partials and per-CTA p^T N p partials
 struct FusedPartials {

@@ -271,3 +271,42 @@ def test_chol_ippmm_decreasing_rank_on_one_context():
     assert a["obj"] == b["obj"]
     c1.close()
     c2.close()
+
+
+# ------------------------------------------ residual products from one read of A (MV_BOTH)
+_BOTH_SCRIPT = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, {root!r})
+from synth import make_config
+from paper_2404_14524_b200 import Context, colmajor_device
+inst = make_config({cfg}, **{kw!r})
+ctx = Context(0)
+Ad, lda = colmajor_device(inst.A)
+dv = lambda a: torch.tensor(a, dtype=torch.float64, device="cuda")
+g = ctx.nys_ipppmm_solve(Ad, lda, inst.m, dv(inst.q), dv(inst.b), dv(inst.c), ell={ell}, max_outer={mo})
+np.save({out!r}, np.concatenate([g[k].cpu().numpy() for k in ("x", "y", "z")] + [np.array([g["obj"], g["inner"]])]))
+"""
+
+
+@pytest.mark.parametrize("cfg,kw,ell,mo", [(0, {}, 10, 100), (1, dict(m=300, n=1200, ell=30), 30, 100),
+                                           (0, dict(m=9000, n=12000), 20, 3)])
+def test_residual_pass_fusion_is_bitwise(tmp_path, cfg, kw, ell, mo):
+    """The residuals' A x and A^T y come from ONE pass over A (MV_BOTH); the same solve with the two
+    separate passes (NYS_NO_MV_BOTH=1) gives bitwise-identical x, y, z, objective and PCG counts (the
+    fused pass keeps each product's summation order).  m = 9000 takes the cluster path."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for split in (False, True):
+        out = str(tmp_path / f"r{int(split)}.npy")
+        env = dict(os.environ)
+        env.pop("NYS_NO_MV_BOTH", None)
+        if split:
+            env["NYS_NO_MV_BOTH"] = "1"
+        code = _BOTH_SCRIPT.format(root=root, cfg=cfg, kw=kw, ell=ell, mo=mo, out=out)
+        subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
