@@ -10,6 +10,7 @@
 // tiles are summed in a fixed order by gemm_reduce (deterministic).
 #include <cuda.h>   // CUtensorMap (the encode entry point is fetched through cudaGetDriverEntryPoint)
 
+#include <algorithm>
 #include <mutex>
 
 #include "k_vec.cuh"
@@ -630,6 +631,24 @@ int launch_gemm(nys_ctx* ctx, const GemmCall& g) {
     if (sp > smax) sp = smax;
     if (sp < 1) sp = 1;
     if (sp > 256) sp = 256;
+    if (sp == 1 && !getenv("NYS_GEMM_NO_WAVE_SPLIT")) {
+      // many tiles: split K only to fill the last wave.  Time ~ ceil(tiles * S / slots) / S (equal
+      // tiles, slots = resident CTAs); the smallest S (<= 4, >= 64 K-slabs per split) within 1 % of the
+      // best, if that gains >= 3 % over S = 1.  Measured on B200, the config-4 sketch (1955 tiles, 444 slots, 4.4 waves): the
+      // unsplit GEMM ran 0.84 of the DMMA peak with the SM pipes 84 % busy — the last wave's idle SMs
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tma ? (const void*)kt : (const void*)k, tma ? 160 : 128,
+                                                        smem) != cudaSuccess) { cudaGetLastError(); occ = 0; }
+      const int64_t slots = (int64_t)occ * ctx->num_sms, tiles = mt * nt;
+      if (slots > 0) {
+        auto cost = [&](int64_t S) { return (double)((tiles * S + slots - 1) / slots) / (double)S; };
+        double best = cost(1);
+        for (int64_t S = 2; S <= 4 && kslabs / S >= 64; ++S) best = std::min(best, cost(S));
+        if (cost(1) > best * 1.03)   // a split costs partials (S M N doubles) and a reduce: only for >= 3 %
+          for (int64_t S = 2; S <= 4 && kslabs / S >= 64; ++S)
+            if (cost(S) <= best * 1.01) { sp = S; break; }
+      }
+    }
     splits = (int)sp;
   }
   int64_t kchunk = (g.K + splits - 1) / splits;

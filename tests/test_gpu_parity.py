@@ -120,7 +120,9 @@ def test_gaussian_matches_oracle_philox(ctx, m, ell, seed, stream):
 SK_SHAPES = [(100, 400, 20), (64, 5000, 64), (257, 1031, 33), (2000, 8000, 50), (5000, 3000, 100), (20000, 700, 40),
              # the TMA-fed GEMM (M >= 16384, K >= 4096): Y = A T (M-major A, bulk copies), T = D A^T Omega
              # (K-major A, swizzled tensor boxes), ragged in every dimension
-             (20000, 5000, 40), (4500, 17000, 24), (16385, 4097, 33)]
+             (20000, 5000, 40), (4500, 17000, 24), (16385, 4097, 33),
+             # > 1.4 waves of tiles: the last wave filled by a K split (T = D A^T Omega / Y = A T)
+             (4096, 16400, 200), (17001, 4500, 200)]
 
 
 @pytest.mark.parametrize("m,n,ell", SK_SHAPES)
