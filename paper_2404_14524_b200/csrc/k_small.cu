@@ -3,6 +3,7 @@
 // of B = Y_nu C^{-1} finished on the ell x ell triangular factor by one-sided Jacobi.
 // All ell x ell routines run in ONE CTA (1024 threads) with the matrices in shared memory
 // when they fit, else in an L2-resident global workspace.
+#include <algorithm>
 #include <cooperative_groups.h>
 
 #include "k_vec.cuh"
@@ -577,6 +578,32 @@ __device__ __forceinline__ void jacobi_rotation(double al, double be, double ga,
   s = c * t;
 }
 
+// Rotation of the pair (x_p, x_q), al = ||x_p||^2, be = ||x_q||^2, ga = x_p^T x_q, d = al - be:
+// x_p' = c x_p - s x_q, x_q' = s x_p + c x_q with x_p'^T x_q' = (1/2) sin 2t d + cos 2t ga = 0, |t| <= pi/4:
+//   ir = (d^2 + 4 ga^2)^{-1/2}, cos 2t = |d| ir, c^2 = (1 + cos 2t) / 2, c = c^2 (c^2)^{-1/2},
+//   s = sin 2t / (2c) = -sgn(d) ga ir (c^2)^{-1/2}, tan t = s / c = s (c^2)^{-1/2};
+// c^2 + s^2 = 1 up to the two rsqrt roundings (each refined to full fp64 precision), and the norms
+// update as al - tan(t) ga, be + tan(t) ga (jacobi_kernel's incremental update).
+__device__ __forceinline__ bool jacobi_rotation_rsqrt(double al, double be, double ga, double& c, double& sn,
+                                                      double& t) {
+  const double d = al - be;
+  const double q = fma(d, d, 4.0 * ga * ga);
+  const bool ok = q >= 1e-290 && q <= 1e290;
+  const double ir = fast_rsqrt2(ok ? q : 1.0);
+  const double c2 = fma(0.5, fabs(d) * ir, 0.5);
+  const double rc = fast_rsqrt2(c2);                    // c2 in [1/2, 1]
+  const double g = (d < 0.0 ? ga : -ga) * ir;           // -sgn(d) ga ir  (sgn(0) = +1)
+  c = c2 * rc;
+  sn = g * rc;
+  t = sn * rc;
+  return ok;
+}
+
+// rsqrt form, with the zeta / t form for out-of-range inputs (warp-uniform in the one-warp-per-pair kernels)
+__device__ __forceinline__ void jacobi_rot(double al, double be, double ga, double& c, double& sn, double& t) {
+  if (!jacobi_rotation_rsqrt(al, be, ga, c, sn, t)) jacobi_rotation(al, be, ga, c, sn, t);
+}
+
 template <int NMAX, bool SM>
 __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, int ldr, double* Vout, int ldv,
                                                       double* sigma, double* gws, double* jsweeps, long long* jdbg) {
@@ -663,7 +690,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
         const double al = nrm[p], be = nrm[q];
         if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {   // warp-uniform
           double c, sn, t;
-          jacobi_rotation(al, be, ga, c, sn, t);
+          jacobi_rot(al, be, ga, c, sn, t);
           if (jtr) tj2 = clock64();
 #pragma unroll
           for (int e = 0; e < E; ++e) {
@@ -723,6 +750,162 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(int n, const double* R, in
     const int i = e % n, j = e / n;
     Vout[i + j * ldv] = V[i + order[j] * n];
   }
+}
+
+// The same one-sided Jacobi with G lanes per column pair (32 / G pairs per warp) for small ell.  A round
+// is a dependent chain (loads, dot, G-lane shuffle sum, rotation, update, barrier) with few warps to
+// hide it, so this variant is written for a short chain and few instructions:
+//   * X and V are stored with a padded leading dimension LD = G * E (rows n .. LD-1 stay zero: a
+//     rotation of zeros is zero), so the loads and stores need no predicates or zero-fills;
+//   * the rotation comes from two reciprocal square roots and no division (below), ~170 cycles of
+//     dependent fp64 latency instead of ~400 for the zeta / t form; out-of-range inputs (never seen
+//     in the Nystrom factor, whose column norms lie between nu and ||N||) take the zeta / t form for
+//     the whole warp;
+//   * a warp issues the rotation once for all its pairs.
+// Measured at ell = 50 with one warp per pair: ~2700 cycles per round.  Same circle ordering,
+// incremental norms, absolute floor, convergence test and output as jacobi_kernel.
+//
+template <int G, int E>
+__global__ void __launch_bounds__(32 * ((G * E / 2 + 32 / G - 1) / (32 / G))) jacobi_packed_kernel(
+    int n, const double* R, int ldr, double* Vout, int ldv, double* sigma, double* jsweeps) {
+  constexpr int PPW = 32 / G;
+  constexpr int LD = G * E;
+  extern __shared__ double jsm[];
+  double* X = jsm;                    // [n][LD]  X = R^T, zero rows n .. LD-1
+  double* V = X + (size_t)n * LD;     // [n][LD]
+  __shared__ int rotated;
+  __shared__ double abs_floor;
+  __shared__ double sv[LD];
+  __shared__ int order[LD];
+  __shared__ double nrm[LD];
+  for (int e = threadIdx.x; e < n * LD; e += blockDim.x) {
+    const int i = e % LD, j = e / LD;
+    X[e] = (i < n) ? R[j + i * ldr] : 0.0;
+    V[e] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int P = (n % 2 == 0) ? n : n + 1;
+  const int nwarp = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int pi = warp * PPW + lane / G;     // this group's pair slot (nwarp * PPW >= P / 2)
+  const int ngroups = nwarp * PPW;
+  const double tol = fmax(1e-15, (double)n * 0x1p-53);
+  const double tol2 = tol * tol;
+  auto gsum = [&](double v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  auto colnorm2 = [&](int j) {
+    const double* xj = X + (size_t)j * LD + gl;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (e & 1) a1 = fma(xj[G * e], xj[G * e], a1);
+      else a0 = fma(xj[G * e], xj[G * e], a0);
+    }
+    return gsum(a0 + a1);
+  };
+  int sweep = 0;
+  for (; sweep < 30; ++sweep) {
+    for (int j0 = 0; j0 < n; j0 += ngroups) {   // exact column norms (group-uniform trip count)
+      const int j = j0 + pi;
+      const double a = colnorm2(j < n ? j : 0);
+      if (gl == 0 && j < n) nrm[j] = a;
+    }
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    if (warp == 0) {   // absolute floor of the rotation test (as jacobi_kernel)
+      double mx = 0.0;
+      for (int j = lane; j < n; j += 32) mx = fmax(mx, nrm[j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) abs_floor = 1e-2 * 0x1p-52 * mx;
+    }
+    __syncthreads();
+    const double floor_g = abs_floor;
+    for (int r = 0; r < P - 1; ++r) {
+      int a, b;
+      if (pi == 0) { a = r; b = P - 1; }
+      else {
+        a = r + pi; if (a >= P - 1) a -= P - 1;
+        b = r - pi; if (b < 0) b += P - 1;
+      }
+      const bool valid = pi < P / 2 && a < n && b < n;   // group-uniform (the dummy column of odd n)
+      const int p = valid ? (a < b ? a : b) : 0, q = valid ? (a < b ? b : a) : 0;
+      double* xp_ = X + (size_t)p * LD + gl;
+      double* xq_ = X + (size_t)q * LD + gl;
+      double* vp_ = V + (size_t)p * LD + gl;
+      double* vq_ = V + (size_t)q * LD + gl;
+      const double al0 = nrm[p], be0 = nrm[q];
+      double xp[E], xq[E], vp[E], vq[E];
+      double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        xp[e] = xp_[G * e];
+        xq[e] = xq_[G * e];
+        vp[e] = vp_[G * e];
+        vq[e] = vq_[G * e];
+        if (e & 1) g1 = fma(xp[e], xq[e], g1);
+        else g0 = fma(xp[e], xq[e], g0);
+      }
+      const double ga = gsum(g0 + g1);
+      const double al = valid ? al0 : 1.0, be = valid ? be0 : 1.0;
+      const bool rot = valid && ga * ga > tol2 * al * be && fabs(ga) > floor_g;   // group-uniform
+      double c, sn, t;
+      const bool ok = jacobi_rotation_rsqrt(al, be, rot ? ga : 1.0, c, sn, t);   // once for all groups
+      if (__any_sync(0xffffffffu, rot && !ok)) jacobi_rotation(al, be, rot ? ga : 1.0, c, sn, t);
+      if (rot) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          xp_[G * e] = c * xp[e] - sn * xq[e];
+          xq_[G * e] = sn * xp[e] + c * xq[e];
+          vp_[G * e] = c * vp[e] - sn * vq[e];
+          vq_[G * e] = sn * vp[e] + c * vq[e];
+        }
+        if (gl == 0) {
+          nrm[p] = fmax(al - t * ga, 0.0);
+          nrm[q] = be + t * ga;
+          rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) jsweeps[0] = (double)(sweep + 1);
+  for (int j0 = 0; j0 < n; j0 += ngroups) {   // sigma_j = ||x_j||
+    const int j = j0 + pi;
+    const double a = colnorm2(j < n ? j : 0);
+    if (gl == 0 && j < n) sv[j] = sqrt(a);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {   // rank sort descending, ties by index
+    int rk = 0;
+    for (int k = 0; k < n; ++k) rk += (sv[k] > sv[j]) || (sv[k] == sv[j] && k < j);
+    order[rk] = j;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) sigma[j] = sv[order[j]];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    Vout[i + j * ldv] = V[i + (size_t)order[j] * LD];
+  }
+}
+
+template <int G, int E>
+static int launch_jacobi_packed(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+  constexpr int PPW = 32 / G;
+  const size_t need = 2 * (size_t)ell * G * E * sizeof(double);
+  const int pairs = (ell + 1) / 2;
+  const int warps = (pairs + PPW - 1) / PPW;
+  auto k = jacobi_packed_kernel<G, E>;
+  NYS_TRY(ensure_max_smem(ctx, (const void*)k, need > 48 * 1024 ? need : 48 * 1024));
+  k<<<1, 32 * warps, need, ctx->stream>>>(ell, R, ldr, V, ldv, sigma, ctx->sc + S_JSWEEPS);
+  ctx->launches++;
+  return ctx->check_launch("jacobi_packed");
 }
 
 // The same one-sided Jacobi for ell > 113 (X and V no longer fit one CTA's shared memory): a
@@ -816,7 +999,7 @@ __global__ void __launch_bounds__(1024) jacobi_cluster_kernel(int n, const doubl
         const double al = *np_, be = *nq_;
         if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {
           double c, sn, t;
-          jacobi_rotation(al, be, ga, c, sn, t);
+          jacobi_rot(al, be, ga, c, sn, t);
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int i = lane + 32 * e;
@@ -950,7 +1133,7 @@ __global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const 
     const double al = swp ? *nq_ : *np_, be = swp ? *np_ : *nq_;
     if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {
       double c, sn, t;
-      jacobi_rotation(al, be, ga, c, sn, t);
+      jacobi_rot(al, be, ga, c, sn, t);
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int i = lane + 32 * e;
@@ -1287,7 +1470,7 @@ __global__ void __launch_bounds__(256) jacobi_grid_kernel(int n, const double* R
         const double al = __ldcg(nrm + p), be = __ldcg(nrm + q);
         if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {
           double c, sn, t;
-          jacobi_rotation(al, be, ga, c, sn, t);
+          jacobi_rot(al, be, ga, c, sn, t);
           double* vp = V + (size_t)p * n;
           double* vq = V + (size_t)q * n;
 #pragma unroll
@@ -1372,10 +1555,30 @@ int launch_jacobi_svd(nys_ctx* ctx, int ell, const double* R, int ldr, double* V
   // block Jacobi over an 8-CTA cluster from ell = block_min on (tuning override NYS_JACOBI_BLOCK_MIN)
   int block_min = 72;   // measured crossover (sketch at m = 20532): 64 equal, 80 2.65 vs 3.59 ms, 112 3.99 vs 6.21 ms
   if (const char* e = getenv("NYS_JACOBI_BLOCK_MIN")) block_min = atoi(e);
-  if (ell >= block_min && ell >= 16 && ell <= 256 && getenv("NYS_JACOBI_CYCLIC") == nullptr) {
+  // packed single-CTA kernel up to packed_max (<= 112: X and V in 200 KB of shared memory)
+  static const int packed_max =
+      std::min(112, getenv("NYS_JACOBI_PACKED_MAX") ? atoi(getenv("NYS_JACOBI_PACKED_MAX")) : 64);
+  if (ell > packed_max && ell >= block_min && ell >= 16 && ell <= 256 && getenv("NYS_JACOBI_CYCLIC") == nullptr) {
     NYS_TRY(launch_jacobi_block(ctx, ell, R, ldr, V, ldv, sigma));
     ctx->launches++;
     return ctx->check_launch("jacobi_block");
+  }
+  // G lanes per pair (NYS_JACOBI_WARP=1: one warp per pair)
+  static const bool warp_pairs = getenv("NYS_JACOBI_WARP") != nullptr;
+  // lanes per pair: 8 up to ell = 56, 16 above (measured on B200 per sweep: ell = 50 37.9 vs 39.1 us,
+  // ell = 64 (G = 8 needs E = 8) 74 vs 55 us); NYS_JACOBI_G forces one (tuning)
+  static const int jg = getenv("NYS_JACOBI_G") ? atoi(getenv("NYS_JACOBI_G")) : 0;
+  const int G = jg ? jg : (ell <= 56 ? 8 : 16);
+  if (!warp_pairs && ell <= packed_max) {
+    if (G == 16) {
+      if (ell <= 32) return launch_jacobi_packed<16, 2>(ctx, ell, R, ldr, V, ldv, sigma);
+      if (ell <= 64) return launch_jacobi_packed<16, 4>(ctx, ell, R, ldr, V, ldv, sigma);
+      return launch_jacobi_packed<16, 7>(ctx, ell, R, ldr, V, ldv, sigma);
+    }
+    if (ell <= 24) return launch_jacobi_packed<8, 3>(ctx, ell, R, ldr, V, ldv, sigma);
+    if (ell <= 56) return launch_jacobi_packed<8, 7>(ctx, ell, R, ldr, V, ldv, sigma);
+    if (ell <= 64) return launch_jacobi_packed<8, 8>(ctx, ell, R, ldr, V, ldv, sigma);
+    return launch_jacobi_packed<16, 7>(ctx, ell, R, ldr, V, ldv, sigma);
   }
   if (ell <= 64) return launch_jacobi_t<64>(ctx, ell, R, ldr, V, ldv, sigma);
   if (ell <= 112) return launch_jacobi_t<128>(ctx, ell, R, ldr, V, ldv, sigma);   // above: cluster path
