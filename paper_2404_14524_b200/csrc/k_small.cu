@@ -1062,38 +1062,41 @@ __global__ void __launch_bounds__(1024) jacobi_cluster_kernel(int n, const doubl
 // rotation, incremental norms, convergence test and output as jacobi_kernel.  Shared memory is read
 // remotely only by the block moves, never per pair (per-pair DSMEM traffic made the column-cyclic
 // cluster kernel ~11 us per round).
-template <int NMAX, int C>
+template <int E, int C>
 __global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const double* R, int ldr, double* Vout,
                                                             int ldv, double* sigma, double* jsweeps) {
-  constexpr int E = NMAX / 32;
+  // Columns are stored with a padded stride LDc = 32 E (rows n .. LDc-1 zero: a rotation of zeros is
+  // zero), so a pair's loads and stores need no predicates; every slot access is an offset into the
+  // CTA's own shared array (LDS / STS, not generic loads); the roles of a pair (which column plays "p")
+  // are resolved once per pair, not per element.  (Measured on B200 at ell = 200 before these changes:
+  // ~650 instructions and ~5000 cycles per local round, mostly integer address arithmetic and selects.)
+  constexpr int LDc = 32 * E;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   extern __shared__ double jsm[];
-  // slot layout: X (bs columns x n), V (bs x n), nrm (bs), block id (1), pad
-  const size_t slot = ((size_t)2 * bs * n + bs + 2 + 1) & ~(size_t)1;   // even: 16-byte aligned slots
-  double* sl[3] = {jsm, jsm + slot, jsm + 2 * slot};
+  // slot layout (offsets into jsm): X (bs columns x LDc), V (bs x LDc), nrm (bs), block id (1), pad
+  const int slot = (2 * bs * LDc + bs + 2 + 1) & ~1;   // even: 16-byte aligned slots
   __shared__ int smap[3];             // this CTA's slot indices of (top, bottom, spare); read by peers
   __shared__ double flag_l[2];
-  __shared__ double sv_all[NMAX];
-  __shared__ int order[NMAX];
+  __shared__ double sv_all[256];
+  __shared__ int order[256];
   if (threadIdx.x == 0) { smap[0] = 0; smap[1] = 1; smap[2] = 2; }
   int top = 0, bot = 1, spare = 2;
   const int nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto Xc = [&](double* s, int j) { return s + (size_t)j * n; };
-  auto Vc = [&](double* s, int j) { return s + (size_t)bs * n + (size_t)j * n; };
-  auto Nr = [&](double* s) { return s + (size_t)2 * bs * n; };
-  auto Bid = [&](double* s) { return s + (size_t)2 * bs * n + bs; };
+  auto Xo = [&](int s, int j) { return s * slot + j * LDc; };
+  auto Vo = [&](int s, int j) { return s * slot + (bs + j) * LDc; };
+  auto No = [&](int s) { return s * slot + 2 * bs * LDc; };
+  auto Bo = [&](int s) { return s * slot + 2 * bs * LDc + bs; };
   auto cnt = [&](int b) { const int c0 = b * bs; return c0 >= n ? 0 : (n - c0 < bs ? n - c0 : bs); };
   // initial blocks: t_c = block c, b_c = block 2C - 1 - c
   for (int w = 0; w < 2; ++w) {
-    double* S = sl[w];
     const int b = (w == 0) ? rank : 2 * C - 1 - rank;
-    for (int e = threadIdx.x; e < bs * n; e += blockDim.x) {
-      const int j = e / n, i = e % n, gj = b * bs + j;
-      Xc(S, j)[i] = (j < cnt(b)) ? R[gj + (size_t)i * ldr] : 0.0;   // X = R^T
-      Vc(S, j)[i] = (j < cnt(b) && i == gj) ? 1.0 : 0.0;
+    for (int e = threadIdx.x; e < bs * LDc; e += blockDim.x) {
+      const int j = e / LDc, i = e % LDc, gj = b * bs + j;
+      jsm[Xo(w, j) + i] = (j < cnt(b) && i < n) ? R[gj + (size_t)i * ldr] : 0.0;   // X = R^T
+      jsm[Vo(w, j) + i] = (j < cnt(b) && i == gj) ? 1.0 : 0.0;
     }
-    if (threadIdx.x == 0) Bid(S)[0] = (double)b;
+    if (threadIdx.x == 0) jsm[Bo(w)] = (double)b;
   }
   const double tol = fmax(1e-15, (double)n * 0x1p-53);
   const double tol2 = tol * tol;
@@ -1102,90 +1105,82 @@ __global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const 
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
   };
+  auto colnorm2 = [&](int off) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const double x = jsm[off + lane + 32 * e];
+      if (e & 1) a1 = fma(x, x, a1);
+      else a0 = fma(x, x, a0);
+    }
+    return wsum(a0 + a1);
+  };
   __syncthreads();
-  // one pair (p, q) of LOCAL columns: p, q in [0, 2 bs) (< bs: top slot, else bottom slot)
-  auto do_pair = [&](int p, int q, double floor_g) {
-    double* Sp = sl[p < bs ? top : bot];
-    double* Sq = sl[q < bs ? top : bot];
+  // one pair (p, q) of LOCAL columns: p, q in [0, 2 bs) (< bs: top slot, else bottom slot); bt / bb:
+  // the block ids in the top / bottom slots
+  auto do_pair = [&](int p, int q, double floor_g, int bt, int bb) {
+    const int sp = p < bs ? top : bot, sq = q < bs ? top : bot;
     const int jp = p < bs ? p : p - bs, jq = q < bs ? q : q - bs;
-    const int bp = (int)Bid(Sp)[0], bq = (int)Bid(Sq)[0];
+    const int bp = p < bs ? bt : bb, bq = q < bs ? bt : bb;
     if (jp >= cnt(bp) || jq >= cnt(bq)) return;
-    double* Xp = Xc(Sp, jp);
-    double* Xq = Xc(Sq, jq);
-    double* Vp = Vc(Sp, jp);
-    double* Vq = Vc(Sq, jq);
-    double xp[E], xq[E], vp[E], vq[E];
-    double ga = 0.0;
+    // the global column with the smaller index plays "p" (as in the column-cyclic kernels)
+    const bool swp = (bp * bs + jp) > (bq * bs + jq);
+    const int s0 = swp ? sq : sp, j0 = swp ? jq : jp, s1 = swp ? sp : sq, j1 = swp ? jp : jq;
+    const int x0 = Xo(s0, j0), x1 = Xo(s1, j1), v0 = Vo(s0, j0), v1 = Vo(s1, j1);
+    const int n0 = No(s0) + j0, n1 = No(s1) + j1;
+    const double al = jsm[n0], be = jsm[n1];
+    double a0[E], a1[E], w0[E], w1[E];
+    double g0 = 0.0, g1 = 0.0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int i = lane + 32 * e;
-      xp[e] = (i < n) ? Xp[i] : 0.0;
-      xq[e] = (i < n) ? Xq[i] : 0.0;
-      vp[e] = (i < n) ? Vp[i] : 0.0;
-      vq[e] = (i < n) ? Vq[i] : 0.0;
-      ga = fma(xp[e], xq[e], ga);
+      a0[e] = jsm[x0 + i];
+      a1[e] = jsm[x1 + i];
+      w0[e] = jsm[v0 + i];
+      w1[e] = jsm[v1 + i];
+      if (e & 1) g1 = fma(a0[e], a1[e], g1);
+      else g0 = fma(a0[e], a1[e], g0);
     }
-    ga = wsum(ga);
-    // the global column with the smaller index plays "p" (as in the column-cyclic kernels)
-    const bool swp = (bp * bs + jp) > (bq * bs + jq);
-    double* np_ = Nr(Sp) + jp;
-    double* nq_ = Nr(Sq) + jq;
-    const double al = swp ? *nq_ : *np_, be = swp ? *np_ : *nq_;
-    if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {
+    const double ga = wsum(g0 + g1);
+    if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {   // warp-uniform
       double c, sn, t;
       jacobi_rot(al, be, ga, c, sn, t);
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int i = lane + 32 * e;
-        if (i < n) {
-          const double a0 = swp ? xq[e] : xp[e], a1 = swp ? xp[e] : xq[e];
-          const double w0 = swp ? vq[e] : vp[e], w1 = swp ? vp[e] : vq[e];
-          double* X0 = swp ? Xq : Xp;
-          double* X1 = swp ? Xp : Xq;
-          double* V0 = swp ? Vq : Vp;
-          double* V1 = swp ? Vp : Vq;
-          X0[i] = c * a0 - sn * a1;
-          X1[i] = sn * a0 + c * a1;
-          V0[i] = c * w0 - sn * w1;
-          V1[i] = sn * w0 + c * w1;
-        }
+        jsm[x0 + i] = c * a0[e] - sn * a1[e];
+        jsm[x1 + i] = sn * a0[e] + c * a1[e];
+        jsm[v0 + i] = c * w0[e] - sn * w1[e];
+        jsm[v1 + i] = sn * w0[e] + c * w1[e];
       }
       if (lane == 0) {
-        double* n0 = swp ? nq_ : np_;
-        double* n1 = swp ? np_ : nq_;
-        *n0 = fmax(al - t * ga, 0.0);
-        *n1 = be + t * ga;
+        jsm[n0] = fmax(al - t * ga, 0.0);
+        jsm[n1] = be + t * ga;
         flag_l[1] = 1.0;
       }
     }
   };
   // move a slot's contents (X, V, nrm, id) into a peer's slot (DSMEM, 16-byte stores)
-  auto push = [&](double* src, int dst_rank, int dst_slot_idx) {
-    double* dst = cl.map_shared_rank(sl[dst_slot_idx], dst_rank);
-    const size_t nv = slot / 2;
-    const double2* s2 = reinterpret_cast<const double2*>(src);
+  auto push = [&](int src_slot, int dst_rank, int dst_slot_idx) {
+    double* dst = cl.map_shared_rank(jsm + (size_t)dst_slot_idx * slot, dst_rank);
+    const int nv = slot / 2;
+    const double2* s2 = reinterpret_cast<const double2*>(jsm + (size_t)src_slot * slot);
     double2* d2 = reinterpret_cast<double2*>(dst);
-    for (size_t e = threadIdx.x; e < nv; e += blockDim.x) d2[e] = s2[e];
+    for (int e = threadIdx.x; e < nv; e += blockDim.x) d2[e] = s2[e];
   };
   int sweep = 0;
   for (; sweep < 30; ++sweep) {
     for (int w = 0; w < 2; ++w) {  // exact norms of the local columns
-      double* S = w == 0 ? sl[top] : sl[bot];
+      const int S = w == 0 ? top : bot;
       for (int j = warp; j < bs; j += nwarp) {
-        double a = 0.0;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int i = lane + 32 * e;
-          if (i < n) a = fma(Xc(S, j)[i], Xc(S, j)[i], a);
-        }
-        a = wsum(a);
-        if (lane == 0) Nr(S)[j] = a;
+        const double a = colnorm2(Xo(S, j));
+        if (lane == 0) jsm[No(S) + j] = a;
       }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       double mx = 0.0;
-      for (int j = 0; j < bs; ++j) mx = fmax(mx, fmax(Nr(sl[top])[j], Nr(sl[bot])[j]));
+      for (int j = 0; j < bs; ++j) mx = fmax(mx, fmax(jsm[No(top) + j], jsm[No(bot) + j]));
       flag_l[0] = mx;
       flag_l[1] = 0.0;
     }
@@ -1194,6 +1189,7 @@ __global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const 
     for (int r = 0; r < C; ++r) mxall = fmax(mxall, *cl.map_shared_rank(&flag_l[0], r));
     const double floor_g = 1e-2 * 0x1p-52 * mxall;
     for (int br = 0; br < 2 * C - 1; ++br) {
+      const int bt = (int)jsm[Bo(top)], bb = (int)jsm[Bo(bot)];
       if (br == 0) {                                   // all pairs of the 2 bs local columns
         const int P2 = 2 * bs;                         // even
         for (int r = 0; r < P2 - 1; ++r) {
@@ -1204,25 +1200,29 @@ __global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const 
               a = r + pi; if (a >= P2 - 1) a -= P2 - 1;
               b = r - pi; if (b < 0) b += P2 - 1;
             }
-            do_pair(a < b ? a : b, a < b ? b : a, floor_g);
+            do_pair(a < b ? a : b, a < b ? b : a, floor_g, bt, bb);
           }
           __syncthreads();
         }
       } else {                                         // cross pairs (top i, bottom (i + r) mod bs)
         for (int r = 0; r < bs; ++r) {
-          for (int i = warp; i < bs; i += nwarp) do_pair(i, bs + (i + r) % bs, floor_g);
+          for (int i = warp; i < bs; i += nwarp) {
+            int k = i + r;
+            if (k >= bs) k -= bs;
+            do_pair(i, bs + k, floor_g, bt, bb);
+          }
           __syncthreads();
         }
       }
       // ---- move the blocks one position along the ring -----------------------------------------
       cl.sync();                                       // every CTA finished with its blocks
       // phase A: t_c -> t_{c+1} (c = 1 .. C-2), b_0 -> t_1; t_{C-1} becomes b_{C-1} locally (below)
-      if (rank >= 1 && rank <= C - 2) push(sl[top], rank + 1, *cl.map_shared_rank(&smap[2], rank + 1));
-      if (rank == 0) push(sl[bot], 1, *cl.map_shared_rank(&smap[2], 1));
+      if (rank >= 1 && rank <= C - 2) push(top, rank + 1, *cl.map_shared_rank(&smap[2], rank + 1));
+      if (rank == 0) push(bot, 1, *cl.map_shared_rank(&smap[2], 1));
       cl.sync();
       // phase B: b_c -> b_{c-1} (c = 1 .. C-1) into the slot freed in phase A
       //   (CTA c - 1 >= 1: its old top slot; CTA 0: its old bottom slot)
-      if (rank >= 1) push(sl[bot], rank - 1, *cl.map_shared_rank(&smap[rank - 1 >= 1 ? 0 : 1], rank - 1));
+      if (rank >= 1) push(bot, rank - 1, *cl.map_shared_rank(&smap[rank - 1 >= 1 ? 0 : 1], rank - 1));
       cl.sync();
       // slot renaming: CTA 0 keeps its slots (its bottom slot was refilled in phase B); the others take
       // the spare (filled in phase A) as top, the old top (refilled in B, or relabelled at C - 1) as
@@ -1242,25 +1242,19 @@ __global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const 
   if (rank == 0 && threadIdx.x == 0) jsweeps[0] = (double)(sweep + 1);
   // sigma of the local columns
   for (int w = 0; w < 2; ++w) {
-    double* S = w == 0 ? sl[top] : sl[bot];
+    const int S = w == 0 ? top : bot;
     for (int j = warp; j < bs; j += nwarp) {
-      double a = 0.0;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int i = lane + 32 * e;
-        if (i < n) a = fma(Xc(S, j)[i], Xc(S, j)[i], a);
-      }
-      a = wsum(a);
-      if (lane == 0) Nr(S)[j] = sqrt(a);
+      const double a = colnorm2(Xo(S, j));
+      if (lane == 0) jsm[No(S) + j] = sqrt(a);
     }
   }
   __syncthreads();
   // every CTA publishes (global index -> sigma) of its two live blocks into sv_all of every peer
   for (int w = 0; w < 2; ++w) {
-    double* S = w == 0 ? sl[top] : sl[bot];
-    const int b = (int)Bid(S)[0];
+    const int S = w == 0 ? top : bot;
+    const int b = (int)jsm[Bo(S)];
     for (int j = threadIdx.x; j < cnt(b); j += blockDim.x)
-      for (int r = 0; r < C; ++r) *cl.map_shared_rank(&sv_all[b * bs + j], r) = Nr(S)[j];
+      for (int r = 0; r < C; ++r) *cl.map_shared_rank(&sv_all[b * bs + j], r) = jsm[No(S) + j];
   }
   cl.sync();
   for (int j = threadIdx.x; j < n; j += blockDim.x) {  // rank sort, ties by index (the same in every CTA)
@@ -1271,14 +1265,14 @@ __global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const 
   __syncthreads();
   // each CTA writes the output columns whose source column it holds
   for (int w = 0; w < 2; ++w) {
-    double* S = w == 0 ? sl[top] : sl[bot];
-    const int b = (int)Bid(S)[0];
+    const int S = w == 0 ? top : bot;
+    const int b = (int)jsm[Bo(S)];
     for (int jo = 0; jo < n; ++jo) {
       const int src = order[jo];
       if (src / bs != b || src - b * bs >= cnt(b)) continue;
-      const double* vcol = Vc(S, src - b * bs);
+      const int vo = Vo(S, src - b * bs);
       if (threadIdx.x == 0) sigma[jo] = sv_all[src];
-      for (int i = threadIdx.x; i < n; i += blockDim.x) Vout[i + (size_t)jo * ldv] = vcol[i];
+      for (int i = threadIdx.x; i < n; i += blockDim.x) Vout[i + (size_t)jo * ldv] = jsm[vo + i];
     }
   }
   cl.sync();
@@ -1307,13 +1301,13 @@ static int launch_jacobi_cluster(nys_ctx* ctx, int ell, const double* R, int ldr
   return NYS_OK;
 }
 
-template <int C>
-static int launch_jacobi_block_c(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+template <int E, int C>
+static int launch_jacobi_block_ec(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
   const int bs = (ell + 2 * C - 1) / (2 * C);
-  const size_t slot = ((size_t)2 * bs * ell + bs + 2 + 1) & ~(size_t)1;
+  const size_t slot = ((size_t)2 * bs * 32 * E + bs + 2 + 1) & ~(size_t)1;
   const size_t smem = 3 * slot * sizeof(double);
   if (smem > 220 * 1024) { ctx->set_error("jacobi_block: blocks do not fit shared memory"); return NYS_EINVAL; }
-  auto k = jacobi_block_kernel<256, C>;
+  auto k = jacobi_block_kernel<E, C>;
   NYS_TRY(ensure_max_smem(ctx, (const void*)k, smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C);
@@ -1329,6 +1323,17 @@ static int launch_jacobi_block_c(nys_ctx* ctx, int ell, const double* R, int ldr
   cfg.numAttrs = 1;
   NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, ell, bs, R, ldr, V, ldv, sigma, ctx->sc + S_JSWEEPS));
   return NYS_OK;
+}
+template <int C>
+static int launch_jacobi_block_c(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+  switch ((ell + 31) / 32) {   // E = elements per lane (padded column stride 32 E)
+    case 1: case 2: case 3: return launch_jacobi_block_ec<3, C>(ctx, ell, R, ldr, V, ldv, sigma);
+    case 4: return launch_jacobi_block_ec<4, C>(ctx, ell, R, ldr, V, ldv, sigma);
+    case 5: return launch_jacobi_block_ec<5, C>(ctx, ell, R, ldr, V, ldv, sigma);
+    case 6: return launch_jacobi_block_ec<6, C>(ctx, ell, R, ldr, V, ldv, sigma);
+    case 7: return launch_jacobi_block_ec<7, C>(ctx, ell, R, ldr, V, ldv, sigma);
+    default: return launch_jacobi_block_ec<8, C>(ctx, ell, R, ldr, V, ldv, sigma);
+  }
 }
 // cluster size 8 (measured best or equal from ell = 64 to 200 against clusters of 2 and 4); the
 // override must keep bs = ceil(ell / 2C) <= 16 (one warp per pair, 512 threads)
