@@ -178,10 +178,9 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(int ell, double* G, int l
     const double inv = 1.0 / W[i + i * n];
     for (int j = i + tid; j < n; j += blockDim.x) X[i + j * lx] *= inv;
     __syncthreads();
-    const int cols = n - i;
-    for (int e = tid; e < i * cols; e += blockDim.x) {
-      const int k = e % i, j = i + e / i;
-      X[k + j * lx] = fma(-W[k + i * n], X[i + j * lx], X[k + j * lx]);
+    for (int j = i + warp; j < n; j += nw) {   // warps over columns, lanes over rows (no index decode)
+      const double xij = X[i + j * lx];
+      for (int k = lane; k < i; k += 32) X[k + j * lx] = fma(-W[k + i * n], xij, X[k + j * lx]);
     }
     __syncthreads();
   }
@@ -267,12 +266,16 @@ __global__ void __launch_bounds__(1024) chol_inv_packed_kernel(int ell, double* 
       row[i] = inv;
     }
     __syncthreads();
-    const int cols = n - i;
-    for (int e = tid; e < i * cols; e += blockDim.x) {
-      const int k = e % i, j = i + e / i;
+    // warps over the columns j >= i, lanes over the rows k < i (no index decode: a flattened
+    // e -> (e % i, e / i) loop spent most of this kernel's time in integer divisions)
+    for (int j = i + warp; j < n; j += nw) {
       const double xij = row[j];
       double* cj = pk + pidx(0, j);
-      cj[k] = (j == i) ? -tmp[k] * xij : fma(-tmp[k], xij, cj[k]);
+      if (j == i) {
+        for (int k = lane; k < i; k += 32) cj[k] = -tmp[k] * xij;
+      } else {
+        for (int k = lane; k < i; k += 32) cj[k] = fma(-tmp[k], xij, cj[k]);
+      }
     }
     __syncthreads();
   }
@@ -443,10 +446,10 @@ __global__ void __launch_bounds__(1024) chol_inv_grid_kernel(int n, double* G, i
     const double inv = 1.0 / __ldcg(W + i + (size_t)i * n);
     for (int64_t j = i + gt; j < n; j += GT) X[i + (size_t)j * lx] *= inv;
     cgrid_barrier(bar, gridDim.x, epoch);
-    const int64_t cols = n - i;
-    for (int64_t e = gt; e < (int64_t)i * cols; e += GT) {
-      const int k = (int)(e % i), j = i + (int)(e / i);
-      X[k + (size_t)j * lx] = fma(-__ldcg(W + k + (size_t)i * n), __ldcg(X + i + (size_t)j * lx), __ldcg(X + k + (size_t)j * lx));
+    for (int64_t j = i + gw; j < n; j += GW) {   // warps over columns, lanes over rows (no index decode)
+      const double xij = __ldcg(X + i + (size_t)j * lx);
+      for (int k = lane; k < i; k += 32)
+        X[k + (size_t)j * lx] = fma(-__ldcg(W + k + (size_t)i * n), xij, __ldcg(X + k + (size_t)j * lx));
     }
     cgrid_barrier(bar, gridDim.x, epoch);
   }
@@ -466,11 +469,12 @@ int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int
   }();
   if (ell <= small_max && ell <= 128) {
     const size_t sm = (size_t)ell * ell * sizeof(double);
+    static const int thr = getenv("NYS_CHOL_THREADS") ? atoi(getenv("NYS_CHOL_THREADS")) : 1024;   // tuning
     if (ell <= 64) {
-      chol_inv_small_kernel<2><<<1, 1024, sm, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);
+      chol_inv_small_kernel<2><<<1, thr, sm, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);
     } else {
       NYS_TRY(ensure_max_smem(ctx, (const void*)chol_inv_small_kernel<4>, 128 * 1024));
-      chol_inv_small_kernel<4><<<1, 1024, sm, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);
+      chol_inv_small_kernel<4><<<1, thr, sm, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc);
     }
   } else if (need > 200 * 1024 && need_packed <= 208 * 1024) {
     NYS_TRY(ensure_max_smem(ctx, (const void*)chol_inv_packed_kernel, 208 * 1024));
