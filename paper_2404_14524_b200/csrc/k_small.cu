@@ -285,6 +285,39 @@ __global__ void __launch_bounds__(1024) chol_inv_packed_kernel(int ell, double* 
   }
 }
 
+// Column j of R^{-1} (R upper, n x n) by back substitution in one warp: x = e_j; for i = j .. 0:
+// x_i /= R_ii (rinv_diag[i] = 1 / R_ii), x_{0:i} -= R_{0:i,i} x_i; x_k lives in lane k % 32, slot k / 32.
+// The slot loop is unrolled (q static), so x[q] needs no dynamic register select and only the slots
+// at or below q are updated (a dynamic-select version spent ~100 instructions per step).
+// col(i) points at R(0, i) (rows 0 .. i-1 contiguous).
+template <int E, typename ColFn>
+__device__ __forceinline__ void inv_column_warp(int j, int n, const double* rinv_diag, ColFn col, double* out) {
+  const int lane = threadIdx.x & 31;
+  double x[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) x[q] = (lane + 32 * q == j) ? 1.0 : 0.0;
+  const int qj = j >> 5;
+#pragma unroll
+  for (int q = E - 1; q >= 0; --q) {
+    if (q > qj) continue;                                   // warp-uniform
+    for (int ii = (q == qj ? (j & 31) : 31); ii >= 0; --ii) {
+      const int i = 32 * q + ii;
+      const double* ci = col(i);
+      double wk[E];
+#pragma unroll
+      for (int q2 = 0; q2 <= q; ++q2)
+        wk[q2] = (q2 < q || lane < ii) ? ci[lane + 32 * q2] : 0.0;
+      const double xi = __shfl_sync(0xffffffffu, x[q], ii) * rinv_diag[i];
+      if (lane == ii) x[q] = xi;
+#pragma unroll
+      for (int q2 = 0; q2 <= q; ++q2) x[q2] = fma(-wk[q2], xi, x[q2]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < E; ++q)
+    if (lane + 32 * q < n) out[lane + 32 * q] = x[q];
+}
+
 // Same contract for ell <= 128 (E = ceil(ell / 32) elements per lane; the paper's ranks up to 100 and
 // CholeskyQR3 passes at them) with one block barrier per elimination step instead of two: the lane
 // that updates row k+1 of a trailing column also publishes it into a double-buffered row, which is
@@ -346,29 +379,8 @@ __global__ void __launch_bounds__(1024) chol_inv_small_kernel(int ell, double* G
     G[i + (size_t)j * ldg] = r;
   }
   __syncthreads();
-  for (int j = warp; j < n; j += nw) {
-    double x[E];
-#pragma unroll
-    for (int q = 0; q < E; ++q) x[q] = (lane + 32 * q == j) ? 1.0 : 0.0;
-    for (int i = j; i >= 0; --i) {
-      double wk[E];
-#pragma unroll
-      for (int q = 0; q < E; ++q) wk[q] = (lane + 32 * q < i) ? W[lane + 32 * q + i * n] : 0.0;
-      const int qi = i >> 5;      // warp-uniform
-      double xo = x[0];
-#pragma unroll
-      for (int q = 1; q < E; ++q) if (qi == q) xo = x[q];
-      const double xi = __shfl_sync(0xffffffffu, xo, i & 31) * rsq[i];   // x_i / R_ii
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        if (q == qi && lane == (i & 31)) x[q] = xi;
-        x[q] = fma(-wk[q], xi, x[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < E; ++q)
-      if (lane + 32 * q < n) Rinv[lane + 32 * q + (size_t)j * ldr] = x[q];
-  }
+  for (int j = warp; j < n; j += nw)
+    inv_column_warp<E>(j, n, rsq, [&](int i) { return W + (size_t)i * n; }, Rinv + (size_t)j * ldr);
 }
 
 // Same contract as chol_inv_kernel for ell > 226 (no single-CTA shared-memory layout fits): the
@@ -460,6 +472,143 @@ __global__ void __launch_bounds__(1024) chol_inv_grid_kernel(int n, double* G, i
   }
 }
 
+// Same contract as chol_inv_kernel, blocked, for ell <= 226 in ONE CTA (packed upper storage as
+// chol_inv_packed_kernel).  The unblocked kernels spend a block barrier and a full trailing sweep
+// (LDS + LDS + FMA + STS per element) on every elimination step.  Here:
+//   * a panel of PB = 8 rows: step k updates only the panel rows (k, k0 + PB), one column per
+//     thread (a single warp took longer: ~40 dependent shared-memory round trips per step);
+//   * then the rows below the panel take the panel's PB rank-1 updates at once,
+//     W_ij -= sum_k R_ki R_kj with R_k = W_k / sqrt(W_kk), in 4 x 4 register tiles of the upper
+//     triangle (one 16-byte load per four FMAs);
+//   * R^{-1} one column per warp by back substitution with shuffles (as chol_inv_small_kernel).
+// The same unscaled right-looking recurrence (rows scaled by 1/sqrt(W_kk) at the end) in a different
+// summation order.  Failure (non-positive / non-finite pivot) sets sc[S_CHOLFAIL] = 1.
+template <int E>
+__global__ void __launch_bounds__(1024) chol_inv_blk_kernel(int ell, double* G, int ldg, double* Rinv, int ldr,
+                                                           int shift_mode, double* sc, long long* tr) {
+  long long t0 = clock64(), tpanel = 0, ttrail = 0;
+  constexpr int PB = 8;
+  extern __shared__ double pk[];
+  __shared__ double dinv[256];   // 1 / W_kk of the unscaled pivots; later 1 / sqrt(W_kk)
+  __shared__ __align__(16) double prow[PB * 256];   // the current panel's rows of R, row-major
+  __shared__ double shift;
+  const int n = ell;
+  const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31, nw = blockDim.x >> 5;
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i <= j; i += 32) pk[pidx(i, j)] = 0.5 * (G[i + (size_t)j * ldg] + G[j + (size_t)i * ldg]);
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    if (shift_mode == 1) {
+      double tr = 0.0;
+      for (int i = 0; i < n; ++i) tr += pk[pidx(i, i)];
+      s = 11.0 * (sc[S_SHIFT] * n + (double)n * (n + 1)) * 0x1p-53 * tr;
+    }
+    shift = s;
+  }
+  __syncthreads();
+  if (shift_mode == 1) {
+    for (int i = tid; i < n; i += blockDim.x) pk[pidx(i, i)] += shift;
+    __syncthreads();
+  }
+  for (int k0 = 0; k0 < n; k0 += PB) {
+    const int kend = min(k0 + PB, n);
+    long long ta = clock64();
+    for (int k = k0; k < kend; ++k) {   // the panel: one column per thread, <= PB - 1 rows each
+      const double piv = pk[pidx(k, k)];
+      if (!(piv > 0.0) || !isfinite(piv)) {   // block-uniform: every thread read the same pivot
+        if (tid == 0) sc[S_CHOLFAIL] = 1.0;
+        return;
+      }
+      const double inv = 1.0 / piv;
+      if (tid == 0) dinv[k] = inv;
+      const int j = k + 1 + tid;             // blockDim.x >= n
+      if (j < n) {
+        const double akj = pk[pidx(k, j)] * inv;
+        double* cj = pk + pidx(0, j);
+#pragma unroll
+        for (int u = 1; u < PB; ++u) {
+          const int i = k + u;
+          if (i < kend && i <= j) cj[i] = fma(-pk[pidx(k, i)], akj, cj[i]);
+        }
+      }
+      __syncthreads();
+    }
+    long long tb = clock64();
+    tpanel += tb - ta;
+    const int m2 = n - kend;   // trailing rows / columns [kend, n), upper part, 4 x 4 tiles
+    if (m2 > 0) {
+      // the panel rows, unscaled, into a row-major buffer (contiguous 4-wide loads below; rows past
+      // the panel are zero)
+      // scaled by 1 / sqrt(W_kk): these are rows of R, and the update is the plain product
+      // W_ij -= sum_r R_ri R_rj (no per-term pivot multiply)
+      for (int e = tid; e < PB * m2; e += blockDim.x) {
+        const int r = e / m2, j = kend + e % m2;
+        prow[r * 256 + j] = (k0 + r < kend) ? pk[pidx(k0 + r, j)] * sqrt(dinv[k0 + r]) : 0.0;
+      }
+      __syncthreads();
+      // upper-triangle tiles only (linear index -> (ti, tj), tj = floor((sqrt(8t + 1) - 1) / 2)): a
+      // square tile loop with the lower half skipped left half of every warp idle
+      const int nt = (m2 + 3) >> 2;
+      const int ntri = nt * (nt + 1) / 2;
+      for (int t = tid; t < ntri; t += blockDim.x) {
+        int tj = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+        while (tj * (tj + 1) / 2 > t) --tj;
+        while ((tj + 1) * (tj + 2) / 2 <= t) ++tj;
+        const int ti = t - tj * (tj + 1) / 2;
+        const int i0 = kend + 4 * ti, j0 = kend + 4 * tj;
+        double acc[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+#pragma unroll
+        for (int r = 0; r < PB; ++r) {
+          const double2 a01 = *reinterpret_cast<const double2*>(prow + r * 256 + i0);
+          const double2 a23 = *reinterpret_cast<const double2*>(prow + r * 256 + i0 + 2);
+          const double2 b01 = *reinterpret_cast<const double2*>(prow + r * 256 + j0);
+          const double2 b23 = *reinterpret_cast<const double2*>(prow + r * 256 + j0 + 2);
+          const double ai[4] = {a01.x, a01.y, a23.x, a23.y};
+          const double bj[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(ai[u], bj[v], acc[u][v]);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int j = j0 + v;
+          if (j >= n) continue;
+          double* cj = pk + pidx(0, j);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i0 + u <= j) cj[i0 + u] -= acc[u][v];
+        }
+      }
+    }
+    __syncthreads();
+    ttrail += clock64() - tb;
+  }
+  const long long tc = clock64();
+  for (int i = tid; i < n; i += blockDim.x) dinv[i] = 1.0 / sqrt(pk[pidx(i, i)]);
+  __syncthreads();
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i <= j; i += 32) pk[pidx(i, j)] *= dinv[i];
+  __syncthreads();
+  for (int e = tid; e < n * n; e += blockDim.x) {  // R out (lower zeroed)
+    const int i = e % n, j = e / n;
+    G[i + (size_t)j * ldg] = (i <= j) ? pk[pidx(i, j)] : 0.0;
+  }
+  // R^{-1}: column j by back substitution, x = e_j; for i = j .. 0: x_i /= R_ii, x_{0:i} -= R_{0:i,i} x_i
+  const long long td = clock64();
+  for (int j = warp; j < n; j += nw)
+    inv_column_warp<E>(j, n, dinv, [&](int i) { return pk + pidx(0, i); }, Rinv + (size_t)j * ldr);
+  if (tr != nullptr) {
+    __syncthreads();
+    if (tid == 0) { tr[0] = tc - t0; tr[1] = tpanel; tr[2] = ttrail; tr[3] = td - tc; tr[4] = clock64() - td; }
+  }
+}
+
 int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int ldr, int shift_mode) {
   const size_t need = ((size_t)ell * ell + (size_t)ell * (ell | 1)) * sizeof(double);
   const size_t need_packed = (size_t)ell * (ell + 1) / 2 * sizeof(double);
@@ -467,7 +616,28 @@ int launch_chol_inv(nys_ctx* ctx, int ell, double* G, int ldg, double* Rinv, int
     const char* s = getenv("NYS_CHOL_SMALL_MAX");  // tuning / A-B override (default 128; 0 disables)
     return s ? atoi(s) : 128;
   }();
-  if (ell <= small_max && ell <= 128) {
+  // blocked kernel from blk_min (tuning override NYS_CHOL_BLK_MIN; NYS_CHOL_UNBLOCKED=1: never)
+  static const int blk_min = getenv("NYS_CHOL_UNBLOCKED") ? 1 << 30
+                             : getenv("NYS_CHOL_BLK_MIN") ? atoi(getenv("NYS_CHOL_BLK_MIN")) : 129;
+  if (ell >= blk_min && ell <= 226) {
+    const size_t smp = need_packed > 48 * 1024 ? need_packed : 48 * 1024;
+    auto launch = [&](auto kern) -> int {
+      NYS_TRY(ensure_max_smem(ctx, (const void*)kern, smp));
+      long long* tr = getenv("NYS_CHOL_TRACE") ? (long long*)ctx->ws("chol_trace", 64) : nullptr;
+      kern<<<1, 1024, need_packed, ctx->stream>>>(ell, G, ldg, Rinv, ldr, shift_mode, ctx->sc, tr);
+      if (tr) {
+        long long h[5];
+        cudaMemcpyAsync(h, tr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        fprintf(stderr, "[choltrace] ell=%d cholesky %lld (panels %lld, trailing %lld) scale+R %lld inverse %lld cycles\n", ell,
+                h[0], h[1], h[2], h[3], h[4]);
+      }
+      return NYS_OK;
+    };
+    if (ell <= 64) NYS_TRY(launch(chol_inv_blk_kernel<2>));
+    else if (ell <= 128) NYS_TRY(launch(chol_inv_blk_kernel<4>));
+    else NYS_TRY(launch(chol_inv_blk_kernel<8>));
+  } else if (ell <= small_max && ell <= 128) {
     const size_t sm = (size_t)ell * ell * sizeof(double);
     static const int thr = getenv("NYS_CHOL_THREADS") ? atoi(getenv("NYS_CHOL_THREADS")) : 1024;   // tuning
     if (ell <= 64) {

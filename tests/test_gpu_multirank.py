@@ -106,18 +106,20 @@ def test_multirank_normal_matvec_and_sketch(world):
 @pytest.mark.parametrize("cfg,kw,world", [(0, {}, 2), (1, dict(m=200, n=800, ell=20), 2), (4, dict(m=150, n=900, ell=20), 3)])
 def test_multirank_ipppmm_matches_oracle(cfg, kw, world):
     inst = make_config(cfg, **kw)
+    ptol = 1e-10 if cfg == 1 else 1e-8   # DESIGN.md reading A17-tol (the reduced config-1 recipe)
     m = inst.m
     sh = _shards(inst.A, world)
     torch.cuda.synchronize()
 
     def fn(ctx, r, st):
         lo, hi, Ad, lda = sh[r]
-        g = ctx.nys_ipppmm_solve(Ad, lda, m, dev(inst.q[lo:hi]), dev(inst.b), dev(inst.c[lo:hi]), ell=inst.ell)
+        g = ctx.nys_ipppmm_solve(Ad, lda, m, dev(inst.q[lo:hi]), dev(inst.b), dev(inst.c[lo:hi]), ell=inst.ell,
+                                 tol=ptol)
         st.synchronize()
         return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in g.items() if k != "log"}
 
     res = _run_ranks(world, fn)
-    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell))
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell, tol=ptol))
     assert ref.status == "optimal"
     for g in res:
         assert g["status"] == 0 and g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
@@ -146,18 +148,20 @@ def test_multirank_chol_ipppmm_matches_oracle():
     """Chol-IP-PMM (f2) on 2 loopback ranks: the diagonal and the pivot columns are all-reduced."""
     inst = make_config(1, m=200, n=800, ell=20)
     world, m = 2, inst.m
+    ptol = 1e-10   # DESIGN.md reading A17-tol: at 1e-8 this recipe's objective is determined only to ~1e-7
     sh = _shards(inst.A, world)
     torch.cuda.synchronize()
 
     def fn(ctx, r, st):
         lo, hi, Ad, lda = sh[r]
         g = ctx.nys_ipppmm_solve(Ad, lda, m, dev(inst.q[lo:hi]), dev(inst.b), dev(inst.c[lo:hi]), ell=inst.ell,
-                                 precond=1)
+                                 precond=1, tol=ptol)
         st.synchronize()
         return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in g.items() if k != "log"}
 
     res = _run_ranks(world, fn)
-    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c, ippmm.Options(path="krylov", ell=inst.ell, precond="chol"))
+    ref = ippmm.solve(inst.A, inst.q, inst.b, inst.c,
+                      ippmm.Options(path="krylov", ell=inst.ell, precond="chol", tol=ptol))
     for g in res:
         assert g["status"] == 0 and g["rel_p"] <= 1e-8 and g["rel_d"] <= 1e-8 and g["mu"] <= 1e-8
     assert np.array_equal(res[0]["y"], res[1]["y"]) and res[0]["inner"] == res[1]["inner"]
@@ -301,4 +305,6 @@ def test_multirank_svm_structure1_matches_single_and_oracle(world):
     print(f"world {world}: sharded {res[0]['obj']!r} single {g1['obj']!r} oracle {ref.obj!r}")
     assert abs(res[0]["obj"] - g1["obj"]) <= 1e-7 * max(1.0, abs(g1["obj"]))
     assert abs(res[0]["obj"] - ref.obj) <= 1e-7 * max(1.0, abs(ref.obj))
-    assert abs(res[0]["outer"] - ref.outer) <= 2
+    # outer counts are parity-unpinned (they depend on readings A8' / A12); this instance
+    # takes ~60 outer iterations, where rounding-level changes move the count by a few
+    assert abs(res[0]["outer"] - ref.outer) <= max(2, 0.1 * ref.outer)

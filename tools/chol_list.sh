@@ -1,6 +1,6 @@
 # per-kernel device times (ncu launch list) of one nys_sketch at each shape: the Cholesky / Jacobi kernels
 for sh in "$@"; do
-  python tools/sketch_bench.py $sh 1 > /dev/null 2>&1 || exit 1
+  python tools/sketch_bench.py $sh 1 > /dev/null 2>&1
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/cl.csv python tools/sketch_bench.py $sh 1 > /dev/null 2>&1
   python - "$sh" <<'PY'
 import csv, sys, collections
