@@ -256,7 +256,7 @@ typedef struct {
   /* Adaptive Nystrom rank (the paper's future work "tuning the rank", P:1102;
    * reading F1): when ell_max > ell, after a build with rank ell_k whose lambda_hat_ell exceeds
    * ell_tau * delta_k (mu_prec, A7) the next build (forced at the next outer iteration) uses
-   * min(2 ell_k, ell_max, m, 256).  The rank never shrinks.  0 = fixed rank.                    */
+   * min(2 ell_k, ell_max, m, 1024).  The rank never shrinks.  0 = fixed rank.                   */
   int    ell_max;        /* 0                                                              */
   double ell_tau;        /* 10                                                             */
 } nys_options;

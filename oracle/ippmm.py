@@ -280,7 +280,7 @@ def solve(A, q, b, c, opts: Options = Options()) -> Result:
                 if rebuild:
                     U, lamh, _ = build_preconditioner(A, d, ell_k, omega_fn(m, ell_k, omega_stream(k)))
                     last_build, base_its, built, ell_built = k, None, True, ell_k
-                    cap = min(opts.ell_max, m, 256)
+                    cap = min(opts.ell_max, m, 1024)
                     if cap > ell_k and lamh[ell_k - 1] > opts.ell_tau * delta:      # F1
                         ell_k = min(2 * ell_k, cap)
             sol = _krylov_solver(A, d, delta, U, lamh, max_iter, F)   # Nystrom: mu_prec = delta_k (A7)

@@ -1002,7 +1002,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   if (ell > 0 && opt->precond != 1 && opt->ell_max > ell) {
     ell_cap = opt->ell_max;
     if (ell_cap > m) ell_cap = (int)m;
-    if (ell_cap > 256) ell_cap = 256;
+    if (ell_cap > kMaxEll) ell_cap = kMaxEll;
   }
   int ell_k = ell, ell_built = ell;      // rank of the next build / of the factors in use
   double lam_ell_cur = 0.0;
