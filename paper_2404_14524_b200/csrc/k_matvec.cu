@@ -163,6 +163,7 @@ struct MatvecParams {
   int64_t rs;
   int64_t npanels;
   int stages;
+  int l2pf;             // producer: L2 prefetch this many panels beyond the shared-memory ring
   int cl;
   int rc;               // reduction cluster size (cl == 1 only): CTAs of a cluster sum their w partials via DSMEM
   const double* delta_slot;  // if set, delta = *delta_slot
@@ -263,8 +264,26 @@ __global__ void __launch_bounds__(T + 32, 1) matvec_kernel(const MatvecParams P)
       const bool contig = !CLU && P.lda == rs;
       int s = 0;
       uint32_t eph = 1u;  // parity of the empty-barrier phase to wait for (first pass: none)
+      const int PF = P.l2pf;
       for (int64_t it = 0; it < niter; ++it, ++s) {
         if (s == S) { s = 0; eph ^= 1u; }
+        // L2 prefetch of the panel PF stages beyond the ring: more bytes in flight per SM than the
+        // shared-memory stages hold (the bulk copies then hit L2)
+        if (PF > 0) {
+          const int64_t itp = (it == 0) ? -1 : it + S - 1 + PF;   // the first call covers S..S+PF-1 below
+          for (int64_t q = (it == 0 ? S : itp); q <= (it == 0 ? S + PF - 1 : itp); ++q) {
+            if (q >= niter) break;
+            const int64_t c0 = (int64_t)(cid + q * ncl) * BN;
+            int64_t nc = P.n - c0;
+            nc = nc > BN ? BN : nc;
+            if (nc <= 0) break;
+            if (contig) {
+              bulk_prefetch_l2(P.A + c0 * P.lda, (uint32_t)((nc - 1) * rs * 8) + copy_bytes);
+            } else {
+              for (int c = 0; c < nc; ++c) bulk_prefetch_l2(P.A + (c0 + c) * P.lda + r0, copy_bytes);
+            }
+          }
+        }
         if (it >= S) mbar_wait(&empty[s], eph);
         const int64_t col0 = (int64_t)(cid + it * ncl) * BN;
         int64_t ncols = P.n - col0;
@@ -962,6 +981,8 @@ int launch_matvec(nys_ctx* ctx, const MatvecCall& c) {
     P.Wp = Wp; P.wp_ld = wp_ld;
     P.tep = c.tep; P.t1 = c.t1; P.t2 = c.t2; P.ta = c.ta; P.tb = c.tb; P.tc = c.tc; P.td = c.td; P.tx = c.tx; P.tdd = c.tdd;
     P.done = c.done; P.rs = pl.rs; P.npanels = pl.npanels; P.stages = pl.stages; P.cl = pl.cl;
+    static const int l2pf = getenv("NYS_MV_PF") ? atoi(getenv("NYS_MV_PF")) : 0;
+    P.l2pf = l2pf;
     P.pwp = pwp; P.delta = c.delta; P.e = c.e; P.tbuf = tbuf; P.rc = pl.rc;
     P.delta_slot = c.delta_from_slot ? ctx->sc + S_DELTA : nullptr;
     P.fuse_fin = fuse ? 1 : 0;

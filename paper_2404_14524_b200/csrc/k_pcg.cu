@@ -704,6 +704,7 @@ struct PcgSParams {
   double* x;
   double* sc;
   int max_iter;
+  int u_smem;           // cluster variant: U staged in shared memory
 };
 
 template <int MR, int NT>
@@ -859,22 +860,37 @@ __global__ void __launch_bounds__(NT, 1) pcg_cluster_small_kernel(const PcgSPara
   const int64_t n = P.n;
   const int64_t c_lo = (n * rank) / C, c_hi = (n * (rank + 1)) / C;
   const int ncols = (int)(c_hi - c_lo);
-  // the DSMEM-visible slot first: its offset must be the same in every CTA (map_shared_rank maps offsets)
-  double* part = dsm;                                // [2][M32] this CTA's partial w
-  double* wpart = part + 2 * M32;                    // [NW][M32]
+  // the DSMEM-visible receive buffer first: its offset must be the same in every CTA (mapa maps
+  // offsets); recv[b][q][.] holds CTA q's partial w of an iteration of parity b, pushed by CTA q
+  double* recv = dsm;                                // [2][C][M32]
+  double* wpart = recv + 2 * (size_t)C * M32;        // [NW][M32]
   double* As = wpart + NW * M32;                     // [ncols][M32], rows >= m zero
-  double* ds = As + (size_t)ncols * M32;             // [ncols]
+  double* ds = As + (size_t)ncols * M32;             // [ncols] (even count)
+  double* Us = ds + ((ncols + 1) & ~1);              // [ell][M32] when P.u_smem (U read from global otherwise)
   __shared__ double r_s[M32], z_s[M32], p_s[M32], w_s[M32], x_s[M32];
-  __shared__ double g_s[256], h_s[256];
+  __shared__ double g_s[257], h_s[256];
   __shared__ double red[64];
+  __shared__ __align__(8) uint64_t rbar[2];          // receive barriers (parity of the iteration)
   const int tid = threadIdx.x, warp = warp_uniform_id(), lane = tid & 31;
   const double delta = P.sc[S_DELTA];
   const double tol = P.sc[S_TOL];
+  if (tid == 0) {
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    fence_mbar_init();
+  }
   for (int64_t e = tid; e < (int64_t)ncols * M32; e += NT) {
     const int j = (int)(e / M32), i = (int)(e % M32);
     As[e] = (i < m) ? P.A[(c_lo + j) * P.lda + i] : 0.0;
   }
   for (int j = tid; j < ncols; j += NT) ds[j] = P.d[c_lo + j];
+  const bool us = P.u_smem != 0;
+  if (us)
+    for (int e = tid; e < ell * M32; e += NT) {
+      const int c = e / M32, i = e % M32;
+      Us[e] = (i < m) ? P.U[(size_t)c * P.ldu + i] : 0.0;
+    }
+  auto Ucol = [&](int c) -> const double* { return us ? Us + (size_t)c * M32 : P.U + (size_t)c * P.ldu; };
   // block sum with ONE barrier: the warp sums go to alternating buffers and every thread adds the NW
   // of them in the same order (a buffer is rewritten only after the next call's barrier)
   int rb = 0;
@@ -888,33 +904,36 @@ __global__ void __launch_bounds__(NT, 1) pcg_cluster_small_kernel(const PcgSPara
     rb ^= 1;
     return t;
   };
-  auto precond = [&](double rr) -> double {
-    if (ell == 0) {
-      for (int i = tid; i < m; i += NT) z_s[i] = r_s[i];
-      __syncthreads();
-      return rr;
-    }
-    for (int c = warp; c < ell; c += NW) {
-      const double* u = P.U + (size_t)c * P.ldu;
+  // g_c = U_c^T r for c < ell and g_ell = r^T r, one warp per entry (r_s complete on entry); a barrier
+  auto gpass = [&]() {
+    for (int c = warp; c <= ell; c += NW) {
+      const double* u = (c < ell) ? Ucol(c) : r_s;
       double acc = 0.0;
 #pragma unroll
       for (int k = 0; k < MR; ++k) {
         const int i = lane + 32 * k;
-        if (i < m) acc = fma(__ldg(u + i), r_s[i], acc);
+        if (i < m) acc = fma(u[i], r_s[i], acc);
       }
       acc = warp_sum(acc);
-      if (lane == 0) { g_s[c] = acc; h_s[c] = P.s[c] * acc; }
+      if (lane == 0) {
+        g_s[c] = acc;
+        if (c < ell) h_s[c] = P.s[c] * acc;
+      }
     }
     __syncthreads();
-    for (int i = tid; i < m; i += NT) {
-      double acc = r_s[i];
-#pragma unroll 8
-      for (int c = 0; c < ell; ++c) acc = fma(__ldg(P.U + (size_t)c * P.ldu + i), h_s[c], acc);
-      z_s[i] = acc;
-    }
+  };
+  // r^T z = r^T r + sum_c s_c g_c^2 (h = s o g: no further reduction), the same order in every thread;
+  // then own rows z = r + U h and p = z + beta p
+  auto rz_of = [&](double rr) -> double {
     double gh = 0.0;
-    for (int c = tid; c < ell; c += NT) gh = fma(g_s[c], h_s[c], gh);
-    return rr + block_sum(gh);
+    for (int c = 0; c < ell; ++c) gh = fma(h_s[c], g_s[c], gh);
+    return rr + gh;
+  };
+  auto z_row = [&](int i) -> double {
+    double acc = r_s[i];
+#pragma unroll 4
+    for (int c = 0; c < ell; ++c) acc = fma(Ucol(c)[i], h_s[c], acc);
+    return acc;
   };
   for (int i = tid; i < M32; i += NT) {
     r_s[i] = (i < m) ? P.rhs[i] : 0.0;
@@ -922,13 +941,14 @@ __global__ void __launch_bounds__(NT, 1) pcg_cluster_small_kernel(const PcgSPara
     p_s[i] = 0.0;
   }
   __syncthreads();
-  double rr = block_sum(tid < m ? r_s[tid] * r_s[tid] : 0.0);
+  gpass();
+  double rr = g_s[ell];
   int iters = 0, status = 0;
   bool conv = sqrt(rr) <= tol;
   double rz = 0.0;
   if (!conv) {
-    rz = precond(rr);
-    for (int i = tid; i < m; i += NT) p_s[i] = z_s[i];
+    rz = rz_of(rr);
+    if (tid < m) p_s[tid] = z_row(tid);
     __syncthreads();
   }
   cluster.sync();                                    // every CTA's A slice loaded before any DSMEM traffic
@@ -940,38 +960,53 @@ __global__ void __launch_bounds__(NT, 1) pcg_cluster_small_kernel(const PcgSPara
       pr[q] = p_s[lane + 32 * q];
       wacc[q] = 0.0;
     }
-    for (int j = warp; j < ncols; j += NW) {
+    // two columns per warp step: their dot reductions overlap
+    for (int j = warp; j < ncols; j += 2 * NW) {
+      const int j2 = j + NW;
+      const bool two = j2 < ncols;                   // warp-uniform
       const double* a = As + (size_t)j * M32;
-      double av[MR];
-      double acc = 0.0;
+      const double* b = As + (size_t)(two ? j2 : j) * M32;
+      double av[MR], bv[MR];
+      double acc = 0.0, bcc = 0.0;
 #pragma unroll
       for (int q = 0; q < MR; ++q) {
         av[q] = a[lane + 32 * q];
+        bv[q] = b[lane + 32 * q];
         acc = fma(av[q], pr[q], acc);
+        bcc = fma(bv[q], pr[q], bcc);
       }
-      const double t = ds[j] * warp_sum(acc);
 #pragma unroll
-      for (int q = 0; q < MR; ++q) wacc[q] = fma(av[q], t, wacc[q]);
+      for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        bcc += __shfl_xor_sync(0xffffffffu, bcc, o);
+      }
+      const double t = ds[j] * acc;
+      const double tb = two ? ds[j2] * bcc : 0.0;
+#pragma unroll
+      for (int q = 0; q < MR; ++q) wacc[q] = fma(bv[q], tb, fma(av[q], t, wacc[q]));
     }
 #pragma unroll
     for (int q = 0; q < MR; ++q) wpart[warp * M32 + lane + 32 * q] = wacc[q];
     __syncthreads();
-    double* mypart = part + (k & 1) * M32;
-    for (int i = tid; i < m; i += NT) {
+    // this CTA's partial w pushed into every CTA's receive buffer (st.async completing bytes on the
+    // receiver's barrier), then a local wait for all C partials: no cluster barrier and no remote load
+    // on the critical path.  Ring safety: a peer pushes into the same buffer again two iterations later,
+    // only after our push of the next iteration, which we issue after reading this one.
+    const int b = k & 1;
+    if (tid == 0) mbar_arrive_expect_tx(&rbar[b], (uint32_t)(C * m * 8));
+    if (tid < m) {
       double v = 0.0;
-      for (int q = 0; q < NW; ++q) v += wpart[q * M32 + i];
-      mypart[i] = v;
+      for (int q = 0; q < NW; ++q) v += wpart[q * M32 + tid];
+      const uint32_t la = smem_u32(recv + ((size_t)b * C + rank) * M32 + tid);
+      const uint32_t lb = smem_u32(&rbar[b]);
+      for (int q = 0; q < C; ++q) st_async_f64(mapa_shared(la, (uint32_t)q), v, mapa_shared(lb, (uint32_t)q));
     }
-    cluster.sync();                                  // the C partials of this iteration are published
+    mbar_wait(&rbar[b], (uint32_t)((k >> 1) & 1));
     double pw = 0.0;
     if (tid < m) {
-      // all C remote loads in flight at once, then the sum in rank order
-      double v[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = (q < C) ? cluster.map_shared_rank(mypart, q)[tid] : 0.0;
+      const double* rv = recv + (size_t)b * C * M32 + tid;
       double wsum = 0.0;
-#pragma unroll
-      for (int q = 0; q < 16; ++q) wsum += v[q];
+      for (int q = 0; q < C; ++q) wsum += rv[(size_t)q * M32];   // rank order
       const double wi = wsum + (delta + (P.e ? P.e[tid] : 0.0)) * p_s[tid];
       w_s[tid] = wi;
       pw = p_s[tid] * wi;
@@ -980,22 +1015,21 @@ __global__ void __launch_bounds__(NT, 1) pcg_cluster_small_kernel(const PcgSPara
     ++k;
     if (!(pw > 0.0) || !isfinite(pw)) { status = NYS_EBREAKDOWN; break; }
     const double alpha = rz / pw;
-    double rloc = 0.0;
     if (tid < m) {
       x_s[tid] = fma(alpha, p_s[tid], x_s[tid]);
-      const double ri = fma(-alpha, w_s[tid], r_s[tid]);
-      r_s[tid] = ri;
-      rloc = ri * ri;
+      r_s[tid] = fma(-alpha, w_s[tid], r_s[tid]);
     }
-    rr = block_sum(rloc);
+    __syncthreads();
+    gpass();                                         // ||r||^2 and U^T r in one pass
+    rr = g_s[ell];
     ++iters;
     if (sqrt(rr) <= tol) { conv = true; break; }
     if (!isfinite(rr)) { status = NYS_EBREAKDOWN; break; }
-    const double rzn = precond(rr);
+    const double rzn = rz_of(rr);
     if (!(rzn > 0.0) || !isfinite(rzn)) { status = NYS_EBREAKDOWN; break; }
     const double beta = rzn / rz;
     rz = rzn;
-    if (tid < m) p_s[tid] = fma(beta, p_s[tid], z_s[tid]);
+    if (tid < m) p_s[tid] = fma(beta, p_s[tid], z_row(tid));
     __syncthreads();
   }
   if (rank == 0) {
@@ -1035,7 +1069,10 @@ int launch_pcg_small(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_
   if (C <= 16 && getenv("NYS_PCG_SMALL_1CTA") == nullptr) {
     const int64_t m32 = m <= 64 ? 64 : m <= 128 ? 128 : 256;
     const int64_t maxcols = (n + C - 1) / C;
-    const size_t smem = ((size_t)maxcols * m32 + ((maxcols + 1) & ~1) + 16 * m32 + 2 * m32) * 8;
+    size_t smem = ((size_t)maxcols * m32 + ((maxcols + 1) & ~1) + 16 * m32 + 2 * (size_t)C * m32) * 8;
+    const size_t ubytes = (size_t)ell * m32 * 8;
+    P.u_smem = (smem + ubytes <= 200 * 1024 && getenv("NYS_PCG_SMALL_UGLOBAL") == nullptr) ? 1 : 0;
+    if (P.u_smem) smem += ubytes;
     const void* k = m <= 64 ? (const void*)pcg_cluster_small_kernel<2, 512>
                   : m <= 128 ? (const void*)pcg_cluster_small_kernel<4, 512> : (const void*)pcg_cluster_small_kernel<8, 512>;
     NYS_TRY(ensure_max_smem(ctx, k, smem));
