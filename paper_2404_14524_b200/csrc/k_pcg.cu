@@ -1069,17 +1069,22 @@ int launch_pcg_small(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_
   if (C <= 16 && getenv("NYS_PCG_SMALL_1CTA") == nullptr) {
     const int64_t m32 = m <= 64 ? 64 : m <= 128 ? 128 : 256;
     const int64_t maxcols = (n + C - 1) / C;
-    size_t smem = ((size_t)maxcols * m32 + ((maxcols + 1) & ~1) + 16 * m32 + 2 * (size_t)C * m32) * 8;
+    // 256 threads (measured at config 0: 3.47 vs 3.63 us per iteration with 512; NYS_PCG_SMALL_NT=512)
+    static const int nt = getenv("NYS_PCG_SMALL_NT") ? atoi(getenv("NYS_PCG_SMALL_NT")) : 256;
+    size_t smem = ((size_t)maxcols * m32 + ((maxcols + 1) & ~1) + (size_t)(nt / 32) * m32 + 2 * (size_t)C * m32) * 8;
     const size_t ubytes = (size_t)ell * m32 * 8;
     P.u_smem = (smem + ubytes <= 200 * 1024 && getenv("NYS_PCG_SMALL_UGLOBAL") == nullptr) ? 1 : 0;
     if (P.u_smem) smem += ubytes;
-    const void* k = m <= 64 ? (const void*)pcg_cluster_small_kernel<2, 512>
-                  : m <= 128 ? (const void*)pcg_cluster_small_kernel<4, 512> : (const void*)pcg_cluster_small_kernel<8, 512>;
+    const void* k = nt == 512 ? (m <= 64 ? (const void*)pcg_cluster_small_kernel<2, 512>
+                                         : m <= 128 ? (const void*)pcg_cluster_small_kernel<4, 512>
+                                                    : (const void*)pcg_cluster_small_kernel<8, 512>)
+                  : m <= 64 ? (const void*)pcg_cluster_small_kernel<2, 256>
+                  : m <= 128 ? (const void*)pcg_cluster_small_kernel<4, 256> : (const void*)pcg_cluster_small_kernel<8, 256>;
     NYS_TRY(ensure_max_smem(ctx, k, smem));
     if (C > 8) NYS_CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)C);
-    cfg.blockDim = dim3(512);
+    cfg.blockDim = dim3((unsigned)(nt == 512 ? 512 : 256));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
     cudaLaunchAttribute at[1];
@@ -1089,9 +1094,7 @@ int launch_pcg_small(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (m <= 64) NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, pcg_cluster_small_kernel<2, 512>, P));
-    else if (m <= 128) NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, pcg_cluster_small_kernel<4, 512>, P));
-    else NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, pcg_cluster_small_kernel<8, 512>, P));
+    NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, (void (*)(const PcgSParams))k, P));
     ctx->launches++;
     return ctx->check_launch("pcg_cluster_small");
   }
