@@ -155,7 +155,7 @@ def _nys_gpu(ctx, A, d, ell, Om, delta=1e-2):
 
 @pytest.mark.parametrize("m,n,ell,r", [(100, 400, 20, 100), (300, 900, 40, 12), (2000, 8000, 50, 40),
                                        (64, 3000, 64, 64), (501, 2000, 30, 500),
-                                       # ell > 112: cluster Jacobi (C = 2 / 4 / 8) and the packed Cholesky
+                                       # ell > 112: block Jacobi (8-CTA cluster) and the blocked Cholesky
                                        (600, 2000, 128, 600), (900, 2500, 160, 900), (700, 3000, 200, 700),
                                        (1000, 2000, 256, 80),
                                        # ell > 256 (the paper's ell = 800): global-memory Cholesky,
