@@ -1236,15 +1236,17 @@ __global__ void __launch_bounds__(1024) jacobi_cluster_kernel(int n, const doubl
 // rotation, incremental norms, convergence test and output as jacobi_kernel.  Shared memory is read
 // remotely only by the block moves, never per pair (per-pair DSMEM traffic made the column-cyclic
 // cluster kernel ~11 us per round).
-template <int E, int C>
-__global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const double* R, int ldr, double* Vout,
+template <int G, int E, int C>
+__global__ void __launch_bounds__(512 * G / 32) jacobi_block_kernel(int n, int bs, const double* R, int ldr, double* Vout,
                                                             int ldv, double* sigma, double* jsweeps) {
   // Columns are stored with a padded stride LDc = 32 E (rows n .. LDc-1 zero: a rotation of zeros is
   // zero), so a pair's loads and stores need no predicates; every slot access is an offset into the
   // CTA's own shared array (LDS / STS, not generic loads); the roles of a pair (which column plays "p")
   // are resolved once per pair, not per element.  (Measured on B200 at ell = 200 before these changes:
   // ~650 instructions and ~5000 cycles per local round, mostly integer address arithmetic and selects.)
-  constexpr int LDc = 32 * E;
+  // G lanes per column pair (32 / G pairs per warp, as jacobi_packed_kernel): E = ceil(n / G)
+  constexpr int LDc = G * E;
+  constexpr int PPW = 32 / G;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   extern __shared__ double jsm[];
@@ -1257,6 +1259,7 @@ __global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const 
   if (threadIdx.x == 0) { smap[0] = 0; smap[1] = 1; smap[2] = 2; }
   int top = 0, bot = 1, spare = 2;
   const int nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gl = lane % G, gslot = warp * PPW + lane / G, ngs = nwarp * PPW;   // pair slot of this lane group
   auto Xo = [&](int s, int j) { return s * slot + j * LDc; };
   auto Vo = [&](int s, int j) { return s * slot + (bs + j) * LDc; };
   auto No = [&](int s) { return s * slot + 2 * bs * LDc; };
@@ -1274,40 +1277,39 @@ __global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const 
   }
   const double tol = fmax(1e-15, (double)n * 0x1p-53);
   const double tol2 = tol * tol;
-  auto wsum = [&](double v) {
+  auto gsum = [&](double v) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
   };
-  auto colnorm2 = [&](int off) {
-    double a0 = 0.0, a1 = 0.0;
+  auto colnorm2 = [&](int off) {   // a whole warp per column
+    double a0 = 0.0;
+    for (int i = lane; i < LDc; i += 32) a0 = fma(jsm[off + i], jsm[off + i], a0);
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const double x = jsm[off + lane + 32 * e];
-      if (e & 1) a1 = fma(x, x, a1);
-      else a0 = fma(x, x, a0);
-    }
-    return wsum(a0 + a1);
+    for (int o = 16; o > 0; o >>= 1) a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    return a0;
   };
   __syncthreads();
   // one pair (p, q) of LOCAL columns: p, q in [0, 2 bs) (< bs: top slot, else bottom slot); bt / bb:
   // the block ids in the top / bottom slots
-  auto do_pair = [&](int p, int q, double floor_g, int bt, int bb) {
+  // (valid: group-uniform; every lane of the warp runs the shuffles)
+  auto do_pair = [&](int p, int q, bool valid, double floor_g, int bt, int bb) {
     const int sp = p < bs ? top : bot, sq = q < bs ? top : bot;
     const int jp = p < bs ? p : p - bs, jq = q < bs ? q : q - bs;
     const int bp = p < bs ? bt : bb, bq = q < bs ? bt : bb;
-    if (jp >= cnt(bp) || jq >= cnt(bq)) return;
+    valid = valid && jp < cnt(bp) && jq < cnt(bq);
     // the global column with the smaller index plays "p" (as in the column-cyclic kernels)
     const bool swp = (bp * bs + jp) > (bq * bs + jq);
     const int s0 = swp ? sq : sp, j0 = swp ? jq : jp, s1 = swp ? sp : sq, j1 = swp ? jp : jq;
-    const int x0 = Xo(s0, j0), x1 = Xo(s1, j1), v0 = Vo(s0, j0), v1 = Vo(s1, j1);
+    const int x0 = valid ? Xo(s0, j0) : 0, x1 = valid ? Xo(s1, j1) : 0, v0 = valid ? Vo(s0, j0) : 0,
+              v1 = valid ? Vo(s1, j1) : 0;
     const int n0 = No(s0) + j0, n1 = No(s1) + j1;
-    const double al = jsm[n0], be = jsm[n1];
+    const double al = valid ? jsm[n0] : 1.0, be = valid ? jsm[n1] : 1.0;
     double a0[E], a1[E], w0[E], w1[E];
     double g0 = 0.0, g1 = 0.0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const int i = lane + 32 * e;
+      const int i = gl + G * e;
       a0[e] = jsm[x0 + i];
       a1[e] = jsm[x1 + i];
       w0[e] = jsm[v0 + i];
@@ -1315,19 +1317,21 @@ __global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const 
       if (e & 1) g1 = fma(a0[e], a1[e], g1);
       else g0 = fma(a0[e], a1[e], g0);
     }
-    const double ga = wsum(g0 + g1);
-    if (ga * ga > tol2 * al * be && fabs(ga) > floor_g) {   // warp-uniform
-      double c, sn, t;
-      jacobi_rot(al, be, ga, c, sn, t);
+    const double ga = gsum(g0 + g1);
+    const bool rot = valid && ga * ga > tol2 * al * be && fabs(ga) > floor_g;   // group-uniform
+    double c, sn, t;
+    const bool ok = jacobi_rotation_rsqrt(al, be, rot ? ga : 1.0, c, sn, t);   // once for all groups
+    if (__any_sync(0xffffffffu, rot && !ok)) jacobi_rotation(al, be, rot ? ga : 1.0, c, sn, t);
+    if (rot) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const int i = lane + 32 * e;
+        const int i = gl + G * e;
         jsm[x0 + i] = c * a0[e] - sn * a1[e];
         jsm[x1 + i] = sn * a0[e] + c * a1[e];
         jsm[v0 + i] = c * w0[e] - sn * w1[e];
         jsm[v1 + i] = sn * w0[e] + c * w1[e];
       }
-      if (lane == 0) {
+      if (gl == 0) {
         jsm[n0] = fmax(al - t * ga, 0.0);
         jsm[n1] = be + t * ga;
         flag_l[1] = 1.0;
@@ -1367,23 +1371,27 @@ __global__ void __launch_bounds__(512) jacobi_block_kernel(int n, int bs, const 
       if (br == 0) {                                   // all pairs of the 2 bs local columns
         const int P2 = 2 * bs;                         // even
         for (int r = 0; r < P2 - 1; ++r) {
-          for (int pi = warp; pi < P2 / 2; pi += nwarp) {
+          for (int base = 0; base < P2 / 2; base += ngs) {   // warp-uniform trip count
+            const int pi = base + gslot;
             int a, b;
             if (pi == 0) { a = r; b = P2 - 1; }
             else {
               a = r + pi; if (a >= P2 - 1) a -= P2 - 1;
               b = r - pi; if (b < 0) b += P2 - 1;
             }
-            do_pair(a < b ? a : b, a < b ? b : a, floor_g, bt, bb);
+            const bool v = pi < P2 / 2;
+            do_pair(v ? (a < b ? a : b) : 0, v ? (a < b ? b : a) : 1, v, floor_g, bt, bb);
           }
           __syncthreads();
         }
       } else {                                         // cross pairs (top i, bottom (i + r) mod bs)
         for (int r = 0; r < bs; ++r) {
-          for (int i = warp; i < bs; i += nwarp) {
+          for (int base = 0; base < bs; base += ngs) {
+            const int i = base + gslot;
             int k = i + r;
             if (k >= bs) k -= bs;
-            do_pair(i, bs + k, floor_g, bt, bb);
+            const bool v = i < bs;
+            do_pair(v ? i : 0, v ? bs + k : bs, v, floor_g, bt, bb);
           }
           __syncthreads();
         }
@@ -1475,17 +1483,17 @@ static int launch_jacobi_cluster(nys_ctx* ctx, int ell, const double* R, int ldr
   return NYS_OK;
 }
 
-template <int E, int C>
+template <int G, int E, int C>
 static int launch_jacobi_block_ec(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
   const int bs = (ell + 2 * C - 1) / (2 * C);
-  const size_t slot = ((size_t)2 * bs * 32 * E + bs + 2 + 1) & ~(size_t)1;
+  const size_t slot = ((size_t)2 * bs * G * E + bs + 2 + 1) & ~(size_t)1;
   const size_t smem = 3 * slot * sizeof(double);
   if (smem > 220 * 1024) { ctx->set_error("jacobi_block: blocks do not fit shared memory"); return NYS_EINVAL; }
-  auto k = jacobi_block_kernel<E, C>;
+  auto k = jacobi_block_kernel<G, E, C>;
   NYS_TRY(ensure_max_smem(ctx, (const void*)k, smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C);
-  cfg.blockDim = dim3(32 * (bs < 1 ? 1 : bs));
+  cfg.blockDim = dim3(32 * ((bs < 1 ? 1 : bs) + 32 / G - 1) / (32 / G));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;
   cudaLaunchAttribute at[1];
@@ -1500,13 +1508,15 @@ static int launch_jacobi_block_ec(nys_ctx* ctx, int ell, const double* R, int ld
 }
 template <int C>
 static int launch_jacobi_block_c(nys_ctx* ctx, int ell, const double* R, int ldr, double* V, int ldv, double* sigma) {
+  // (16 lanes per pair measured at ell = 200: 2.81 vs 3.06 ms but one more sweep on other inputs, and
+  //  no gain at ell = 80 / 100: one warp per pair here)
   switch ((ell + 31) / 32) {   // E = elements per lane (padded column stride 32 E)
-    case 1: case 2: case 3: return launch_jacobi_block_ec<3, C>(ctx, ell, R, ldr, V, ldv, sigma);
-    case 4: return launch_jacobi_block_ec<4, C>(ctx, ell, R, ldr, V, ldv, sigma);
-    case 5: return launch_jacobi_block_ec<5, C>(ctx, ell, R, ldr, V, ldv, sigma);
-    case 6: return launch_jacobi_block_ec<6, C>(ctx, ell, R, ldr, V, ldv, sigma);
-    case 7: return launch_jacobi_block_ec<7, C>(ctx, ell, R, ldr, V, ldv, sigma);
-    default: return launch_jacobi_block_ec<8, C>(ctx, ell, R, ldr, V, ldv, sigma);
+    case 1: case 2: case 3: return launch_jacobi_block_ec<32, 3, C>(ctx, ell, R, ldr, V, ldv, sigma);
+    case 4: return launch_jacobi_block_ec<32, 4, C>(ctx, ell, R, ldr, V, ldv, sigma);
+    case 5: return launch_jacobi_block_ec<32, 5, C>(ctx, ell, R, ldr, V, ldv, sigma);
+    case 6: return launch_jacobi_block_ec<32, 6, C>(ctx, ell, R, ldr, V, ldv, sigma);
+    case 7: return launch_jacobi_block_ec<32, 7, C>(ctx, ell, R, ldr, V, ldv, sigma);
+    default: return launch_jacobi_block_ec<32, 8, C>(ctx, ell, R, ldr, V, ldv, sigma);
   }
 }
 // cluster size 8 (measured best or equal from ell = 64 to 200 against clusters of 2 and 4); the
