@@ -679,7 +679,10 @@ def main():
             "solve": {"outer": last["outer"], "inner": last["inner"], "obj": last["obj"], "rel_p": last["rel_p"],
                       "rel_d": last["rel_d"], "mu": last["mu"], "matvecs": matvecs_per_solve,
                       "t_sketch_ms": last["t_sketch_ms"], "t_pcg_ms": last["t_pcg_ms"],
-                      "t_other_ms": last["t_other_ms"], "kernel_launches": last["kernel_launches"]},
+                      "t_other_ms": last["t_other_ms"], "kernel_launches": last["kernel_launches"],
+                      # PCG iterations (predictor, corrector) per outer iteration; the rest of "inner"
+                      # is the initial point's two solves (App. B.2, reading A14'')
+                      "pcg_per_outer": [[r["pcg_pred"], r["pcg_corr"]] for r in last.get("log", [])]},
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

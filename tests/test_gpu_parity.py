@@ -155,6 +155,10 @@ def _nys_gpu(ctx, A, d, ell, Om, delta=1e-2):
 
 @pytest.mark.parametrize("m,n,ell,r", [(100, 400, 20, 100), (300, 900, 40, 12), (2000, 8000, 50, 40),
                                        (64, 3000, 64, 64), (501, 2000, 30, 500),
+                                       # odd ranks (the circle ordering's dummy column): packed Jacobi with
+                                       # 8 / 16 lanes per pair, the block Jacobi, the blocked Cholesky
+                                       (300, 900, 37, 300), (400, 1200, 61, 400), (700, 2000, 101, 700),
+                                       (900, 2500, 171, 900),
                                        # ell > 112: block Jacobi (8-CTA cluster) and the blocked Cholesky
                                        (600, 2000, 128, 600), (900, 2500, 160, 900), (700, 3000, 200, 700),
                                        (1000, 2000, 256, 80),
