@@ -19,7 +19,9 @@ __device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_
   c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
 }
 
-__global__ void gaussian_kernel(double* __restrict__ O, int64_t total, uint64_t seed, uint64_t stream) {
+__global__ void gaussian_kernel(double* __restrict__ O, int64_t total, uint64_t seed, uint64_t stream,
+                                const double* kslot) {
+  if (kslot != nullptr) stream = (uint64_t)(*kslot) + 1u;   // graph-resident loop: stream k + 1 (A6)
   const int64_t npairs = (total + 1) >> 1;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
     uint32_t c0 = (uint32_t)p, c1 = (uint32_t)((uint64_t)p >> 32), c2 = (uint32_t)stream, c3 = (uint32_t)(stream >> 32);
@@ -46,7 +48,7 @@ int launch_gaussian(nys_ctx* ctx, double* O, int64_t total, uint64_t seed, uint6
   int64_t npairs = (total + 1) / 2;
   int grid = (int)((npairs + 255) / 256);
   if (grid > 8 * ctx->num_sms) grid = 8 * ctx->num_sms;
-  gaussian_kernel<<<grid, 256, 0, ctx->stream>>>(O, total, seed, stream);
+  gaussian_kernel<<<grid, 256, 0, ctx->stream>>>(O, total, seed, stream, ctx->gloop ? ctx->sc + S_KOUT : nullptr);
   ctx->launches++;
   return ctx->check_launch("gaussian");
 }
@@ -606,13 +608,14 @@ int launch_pcg_precond(nys_ctx* ctx, int init, int64_t m, const double* r, doubl
 }
 
 // s_i = (lam_l + mu) / (lam_i + mu) - 1
-__global__ void prec_coef_kernel(const double* lam, int ell, double mu, double* s) {
+__global__ void prec_coef_kernel(const double* lam, int ell, double mu, double* s, const double* muslot) {
+  if (muslot != nullptr) mu = *muslot;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < ell) s[i] = (lam[ell - 1] + mu) / (lam[i] + mu) - 1.0;
 }
 int launch_prec_coef(nys_ctx* ctx, const double* lam, int ell, double mu, double* s) {
   if (ell <= 0) return NYS_OK;
-  prec_coef_kernel<<<(ell + 127) / 128, 128, 0, ctx->stream>>>(lam, ell, mu, s);
+  prec_coef_kernel<<<(ell + 127) / 128, 128, 0, ctx->stream>>>(lam, ell, mu, s, ctx->gloop ? ctx->sc + S_DELTA : nullptr);
   ctx->launches++;
   return ctx->check_launch("prec_coef");
 }
@@ -650,7 +653,9 @@ int launch_pcg_setup(nys_ctx* ctx, int mode, double tol_abs, double c, double fl
 // IPM elementwise kernels (Alg. 4 / Alg. 5 for I-only variables)
 // ------------------------------------------------------------------------------------------
 // d_j = 1 / (q_j + z_j / x_j + rho)
-__global__ void scaling_kernel(int64_t n, const double* q, const double* x, const double* z, double rho, double* d) {
+__global__ void scaling_kernel(int64_t n, const double* q, const double* x, const double* z, double rho, double* d,
+                               const double* rslot) {
+  if (rslot != nullptr) rho = *rslot;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
     d[j] = 1.0 / (q[j] + z[j] / x[j] + rho);
 }
@@ -659,7 +664,9 @@ __global__ void scaling_kernel(int64_t n, const double* q, const double* x, cons
 // [rD = dual residual at the current iterate]; r_xz = -x z ; xi_au = -r_xz / x (= z) ;
 // t = d (r_d + xi_au)
 __global__ void pred_rhs_n_kernel(int64_t n, const double* x, const double* z, const double* zeta, const double* rD,
-                                  double rho, const double* d, double* rd, double* rxz, double* xiau, double* t) {
+                                  double rho, const double* d, double* rd, double* rxz, double* xiau, double* t,
+                                  const double* rslot) {
+  if (rslot != nullptr) rho = *rslot;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const double xj = x[j], zj = z[j];
     const double r = rD[j] + rho * (xj - zeta[j]);
@@ -673,7 +680,8 @@ __global__ void pred_rhs_n_kernel(int64_t n, const double* x, const double* z, c
 }
 // r_p = b - A x - delta (y - lambda) [ax = A x given]
 __global__ void pred_rhs_m_kernel(int64_t m, const double* b, const double* ax, const double* y, const double* lam,
-                                  double delta, double* rp) {
+                                  double delta, double* rp, const double* dslot) {
+  if (dslot != nullptr) delta = *dslot;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
     rp[i] = b[i] - ax[i] - delta * (y[i] - lam[i]);
 }
@@ -763,20 +771,22 @@ static int ew_grid(nys_ctx* ctx, int64_t n) {
 
 int launch_scaling(nys_ctx* ctx, int64_t n, const double* q, const double* x, const double* z, double rho, double* d) {
   if (n <= 0) return NYS_OK;
-  scaling_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, q, x, z, rho, d);
+  scaling_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, q, x, z, rho, d, ctx->gloop ? ctx->sc + S_RHO : nullptr);
   ctx->launches++;
   return ctx->check_launch("scaling");
 }
 int launch_pred_rhs_n(nys_ctx* ctx, int64_t n, const double* x, const double* z, const double* zeta, const double* rD,
                       double rho, const double* d, double* rd, double* rxz, double* xiau, double* t) {
   if (n <= 0) return NYS_OK;
-  pred_rhs_n_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, x, z, zeta, rD, rho, d, rd, rxz, xiau, t);
+  pred_rhs_n_kernel<<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, x, z, zeta, rD, rho, d, rd, rxz, xiau, t,
+                                                               ctx->gloop ? ctx->sc + S_RHO : nullptr);
   ctx->launches++;
   return ctx->check_launch("pred_rhs_n");
 }
 int launch_pred_rhs_m(nys_ctx* ctx, int64_t m, const double* b, const double* ax, const double* y, const double* lam,
                       double delta, double* rp) {
-  pred_rhs_m_kernel<<<ew_grid(ctx, m), 256, 0, ctx->stream>>>(m, b, ax, y, lam, delta, rp);
+  pred_rhs_m_kernel<<<ew_grid(ctx, m), 256, 0, ctx->stream>>>(m, b, ax, y, lam, delta, rp,
+                                                               ctx->gloop ? ctx->sc + S_DELTA : nullptr);
   ctx->launches++;
   return ctx->check_launch("pred_rhs_m");
 }
@@ -962,4 +972,90 @@ int launch_set_slots(nys_ctx* ctx, int k0, double v0, int k1, double v1, int k2,
   return ctx->check_launch("set_slots");
 }
 
+}  // namespace nys
+
+// ------------------------------------------------------------------------------------------
+// graph-resident outer loop (f3): the host loop's end-of-iteration logic on the device
+// ------------------------------------------------------------------------------------------
+namespace nys {
+__global__ void stamp_kernel(double* sc, int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  sc[slot] = (double)t;
+}
+int launch_stamp(nys_ctx* ctx, int slot) {
+  stamp_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc, slot);
+  ctx->launches++;
+  return ctx->check_launch("stamp");
+}
+
+// One thread, after the iteration's residual norms are in S_TMP0..4: the iteration record, the PEU
+// (reading A12: the factor 1 - r when the residual improved to <= 0.95 of its reference, else
+// 1 - 2r/3, floored), the copies lambda <- y / zeta <- x flagged for cond_copy_kernel, the termination
+// criterion of the next iteration (A11) and the iteration cap — the same arithmetic and order as the host
+// loop of ipm_impl — then the WHILE condition.  Stop codes: 1 converged, 2 Nystrom factorisation failure
+// (the host re-runs the iteration with its checks), 3 breakdown / non-finite, 4 iteration cap.
+__global__ void ipm_control_kernel(double* sc, double* rec, cudaGraphConditionalHandle h) {
+  const double tol = sc[S_GPAR0], bnorm = sc[S_GPAR1], cnorm = sc[S_GPAR2], n_total = sc[S_GPAR3];
+  const double max_outer = sc[S_GPAR4], floor_ = sc[S_GPAR5], max_rec = sc[S_GPAR6];
+  const int k = (int)sc[S_KOUT];
+  if (sc[S_NYSFAIL] != 0.0 || sc[S_PCGBRK] != 0.0) {
+    sc[S_GSTOP] = sc[S_NYSFAIL] != 0.0 ? 2.0 : 3.0;
+    cudaGraphSetConditional(h, 0u);
+    return;
+  }
+  const double tsk = (sc[S_TS1] - sc[S_TS0]) * 1e-6;
+  const double tpcg = ((sc[S_TS3] - sc[S_TS2]) + (sc[S_TS5] - sc[S_TS4])) * 1e-6;
+  const double mu = sc[S_OMU], nrP = sc[S_NRP], nrD = sc[S_NRD];
+  const double rho = sc[S_RHO], delta = sc[S_DELTA];
+  const double pred = sc[S_PCGI0], corr = sc[S_PCGI1];
+  if (k < max_rec) {
+    double* r = rec + (size_t)k * 16;
+    r[0] = k; r[1] = mu; r[2] = nrP / (1.0 + bnorm); r[3] = nrD / (1.0 + cnorm);
+    r[4] = sc[S_AP]; r[5] = sc[S_AD]; r[6] = pred; r[7] = corr; r[8] = rho; r[9] = delta;
+    r[10] = tsk; r[11] = tpcg; r[12] = sc[S_LAML];
+  }
+  const double mu_new = n_total > 0 ? (sc[S_TMP2] + sc[S_TMP4]) / n_total : 0.0;
+  const double nrPn = sqrt(sc[S_TMP0] + sc[S_TMP3]), nrDn = sqrt(sc[S_TMP1]);
+  const double rr = (mu > 0) ? fmin(fmax(1.0 - mu_new / mu, 0.0), 1.0) : (n_total > 0 ? 0.0 : 1.0);
+  const bool p_imp = nrPn <= 0.95 * sc[S_NRPREF];
+  const bool d_imp = nrDn <= 0.95 * sc[S_NRDREF];
+  sc[S_CPLAM] = p_imp ? 1.0 : 0.0;
+  sc[S_CPZETA] = d_imp ? 1.0 : 0.0;
+  if (p_imp) sc[S_NRPREF] = nrPn;
+  if (d_imp) sc[S_NRDREF] = nrDn;
+  sc[S_DELTA] = fmax(floor_, (p_imp ? (1.0 - rr) : (1.0 - 2.0 / 3.0 * rr)) * delta);
+  sc[S_RHO] = fmax(floor_, (d_imp ? (1.0 - rr) : (1.0 - 2.0 / 3.0 * rr)) * rho);
+  sc[S_INNER] += pred + corr;
+  sc[S_TSK] += tsk;
+  sc[S_TPCG] += tpcg;
+  sc[S_OMU] = mu_new;
+  sc[S_MUCUR] = mu_new;
+  sc[S_NRP] = nrPn;
+  sc[S_NRD] = nrDn;
+  sc[S_KOUT] = k + 1;
+  double stop = 0.0;
+  if (nrPn / (1.0 + bnorm) <= tol && nrDn / (1.0 + cnorm) <= tol && mu_new <= tol) stop = 1.0;   // A11
+  else if (k + 1 >= max_outer) stop = 4.0;
+  else if (!isfinite(mu_new) || !isfinite(nrPn) || !isfinite(nrDn)) stop = 3.0;
+  sc[S_GSTOP] = stop;
+  cudaGraphSetConditional(h, stop == 0.0 ? 1u : 0u);
+}
+int launch_ipm_control(nys_ctx* ctx, double* rec, cudaGraphConditionalHandle h) {
+  ipm_control_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc, rec, h);
+  ctx->launches++;
+  return ctx->check_launch("ipm_control");
+}
+// dst <- src when the flag slot is set (the PEU's lambda <- y and zeta <- x)
+__global__ void cond_copy_kernel(const double* sc, int flag, double* dst, const double* src, int64_t len) {
+  if (sc[flag] == 0.0) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+int launch_cond_copy(nys_ctx* ctx, int flag, double* dst, const double* src, int64_t len) {
+  if (len <= 0) return NYS_OK;
+  cond_copy_kernel<<<ew_grid(ctx, len), 256, 0, ctx->stream>>>(ctx->sc, flag, dst, src, len);
+  ctx->launches++;
+  return ctx->check_launch("cond_copy");
+}
 }  // namespace nys

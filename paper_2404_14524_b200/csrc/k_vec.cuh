@@ -55,6 +55,10 @@ int launch_muaff_post(nys_ctx* ctx, double n_total, int gen = 0);
 int launch_ratio(nys_ctx* ctx, int64_t n, const double* x, double* dx, const double* dx1, const double* dx2,
                  const double* z, double* dz, const double* dz1, const double* dz2, int counter_slot);
 int launch_steps_post(nys_ctx* ctx);
+// graph-resident outer loop (ipm_impl, f3)
+int launch_stamp(nys_ctx* ctx, int slot);
+int launch_ipm_control(nys_ctx* ctx, double* rec, cudaGraphConditionalHandle h);
+int launch_cond_copy(nys_ctx* ctx, int flag, double* dst, const double* src, int64_t len);
 // structure 2 (k_gen.cu): scaled identity blocks of A (nys_unit_block); off = column offsets in the unit part
 struct UnitBlocks {
   int nb = 0;

@@ -556,7 +556,8 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
   double* h = ctx->wsd("pcg_h", (size_t)(ell > 0 ? ell : 1));
   double* Pp[2] = {P0, P1};
   const double* done = ctx->sc + S_DONE;
-  NYS_TRY(launch_set_slots(ctx, S_DELTA, op.delta, S_GITER, 0.0));
+  if (ctx->gloop) NYS_TRY(launch_set_slots(ctx, S_GITER, 0.0));   // delta lives in S_DELTA (control kernel)
+  else NYS_TRY(launch_set_slots(ctx, S_DELTA, op.delta, S_GITER, 0.0));
   if (!chol && pcg_persistent_supported(ctx, m, op.n, ell)) {
     // the whole solve is ONE launch (k_pcg.cu): one CTA for small problems, else cooperative grid-wide
     if (pcg_small_supported(ctx, m, op.n, ell))
@@ -1163,7 +1164,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   if (n > 0) NYS_CUDA_TRY(ctx, cudaMemcpyAsync(zeta, x, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   double rho = opt->rho0, delta = opt->delta0;
 
-  auto residuals = [&]() -> int {
+  auto residuals = [&](bool read = true) -> int {
     // r_P = b - A x ; r_D = c + Q x - A^T y - z ; ||r_P||^2, ||r_D||^2, x^T z
     NvtxRange nvr("residuals");
     NYS_TRY(AO.Ax_At_rd(x, ax, y, c, q, z, rD));
@@ -1180,6 +1181,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(D.dot(n, rD, rD, S_TMP1));
     NYS_TRY(D.dot(n, x, z, S_TMP2));
     NYS_TRY(allreduce_slots(ctx, S_TMP1, gen ? 4 : 2));
+    if (!read) return NYS_OK;                                         // graph-resident loop: no host read
     NYS_TRY(read_slots(ctx));
     ctx->h_sc[S_TMP0] += ctx->h_sc[S_TMP3];                           // ||[r_P; r_U]||^2
     ctx->h_sc[S_TMP2] += ctx->h_sc[S_TMP4];                           // x^T z + w^T s
@@ -1193,11 +1195,169 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   int k = 0;
   int last_build = -1;          // outer iteration of the last preconditioner build (f3)
   int64_t base_its = -1, last_its = 0;
+  // ---- graph-resident outer loop (f3) ------------------------------------------------
+  // After iteration 0 (which sizes every workspace) the remaining outer iterations run as ONE graph launch:
+  // a conditional WHILE node whose body is the iteration's kernel sequence (exactly the deferred host
+  // loop's, with rho, delta, mu and the outer index read from device slots) followed by
+  // ipm_control_kernel (record, PEU, termination test -> the WHILE condition) and the PEU copies.  The host
+  // reads the device state once, when the graph returns.  Single GPU, standard form, Nystrom with a fixed
+  // rank rebuilt every outer iteration (Alg. 3 as written), one-launch PCG (m <= 8192); NYS_NO_GRAPH_LOOP=1
+  // keeps the host loop.  A Nystrom factorisation failure stops the graph, and the host loop re-runs that
+  // iteration with its checks (A4 retries).
+  const bool gl_ok = !ctx->multi() && !use_chol && !gen && ell > 0 && ell_cap == ell && opt->prec_refresh <= 1 &&
+                     !(opt->prec_growth > 0.0) && !opt->verbose && getenv("NYS_NO_GRAPH_LOOP") == nullptr &&
+                     pcg_persistent_supported(ctx, m, ncolA, ell);
+  bool gl_tried = false;
+  auto gl_body = [&]() -> int {   // one outer iteration, deferred checks, no host read
+    NYS_TRY(launch_stamp(ctx, S_TS0));
+    NYS_TRY(launch_scaling(ctx, n, q, x, z, rho, d));                // rho from S_RHO
+    NormalOp op;
+    NYS_TRY(AO.normal_op(d, delta, op));                               // op.delta unused: S_DELTA
+    NYS_TRY(launch_set_slots(ctx, S_PCGBRK, 0.0, S_NYSFAIL, 0.0, S_GITACC, 0.0));
+    NYS_TRY(gen_omega(ctx, m, ell, opt->seed, 0, Om));                 // stream S_KOUT + 1 (A6)
+    NYS_TRY(sketch_impl(ctx, m, op.n, op.A, op.lda, op.d, op.e, ell, Om, U, lamh, nullptr, true));
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->sc + S_LAML, lamh + ell - 1, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    NYS_TRY(launch_prec_coef(ctx, lamh, ell, delta, scoef));           // mu_prec = S_DELTA (A7)
+    NYS_TRY(launch_stamp(ctx, S_TS1));
+    PcgResult pr;
+    NYS_TRY(launch_pred_rhs_n(ctx, n, x, z, zeta, rD, rho, d, rd, rxz, xiau, t));
+    NYS_TRY(launch_pred_rhs_m(ctx, m, b, ax, y, lam, delta, rp));
+    NYS_TRY(AO.Ax(t, xi, rp));
+    NYS_TRY(D.dot(m, xi, xi, S_XINORM));
+    NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
+    NYS_TRY(launch_stamp(ctx, S_TS2));
+    NYS_TRY(pcg_impl(ctx, op, ell, U, mp, scoef, xi, dyp, opt->pcg_max_iter, pr, nullptr, (int)S_PCGI0));
+    NYS_TRY(launch_stamp(ctx, S_TS3));
+    NYS_TRY(AO.At_dx(dyp, rd, xiau, rxz, z, x, d, dxp, dzp));
+    NYS_TRY(launch_ratio(ctx, n, x, dxp, nullptr, nullptr, z, dzp, nullptr, nullptr, 8));
+    NYS_TRY(launch_steps_post(ctx));
+    NYS_TRY(launch_muaff(ctx, n, x, dxp, z, dzp, n_total, 9, w, dwp, sv, dsp));
+    NYS_TRY(launch_corr_rhs(ctx, n, x, dxp, dzp, d, rxz, xiau, t));
+    NYS_TRY(AO.Ax(t, xi, nullptr));
+    NYS_TRY(D.dot(m, xi, xi, S_XINORM));
+    NYS_TRY(launch_pcg_setup(ctx, 1, 0, opt->pcg_c, opt->pcg_floor, S_XINORM, S_BNORM, S_MUCUR, 0));
+    NYS_TRY(launch_stamp(ctx, S_TS4));
+    NYS_TRY(pcg_impl(ctx, op, ell, U, mp, scoef, xi, dyc, opt->pcg_max_iter, pr, nullptr, (int)S_PCGI1));
+    NYS_TRY(launch_stamp(ctx, S_TS5));
+    NYS_TRY(AO.At_dx(dyc, nullptr, xiau, rxz, z, x, d, dxc, dzc));
+    NYS_TRY(launch_ratio(ctx, n, x, dx, dxp, dxc, z, dz, dzp, dzc, 8));
+    NYS_TRY(launch_steps_post(ctx));
+    NYS_TRY(launch_update_n(ctx, n, x, dx, z, dz));
+    NYS_TRY(launch_update_m(ctx, m, y, dyp, dyc));
+    return residuals(false);
+  };
+  // runs the graph loop from the current host state; gst: -1 not run (capture failed), else the stop code
+  auto run_gloop = [&](int& gst) -> int {
+    gst = -1;
+    const int maxrec = std::max(1, opt->max_outer + 1);
+    double* grec = ctx->wsd("gl_rec", (size_t)16 * maxrec);
+    NYS_TRY(launch_set_slots(ctx, S_RHO, rho, S_DELTA, delta, S_OMU, mu));
+    NYS_TRY(launch_set_slots(ctx, S_NRP, nrP, S_NRD, nrD, S_NRPREF, nrP_ref));
+    NYS_TRY(launch_set_slots(ctx, S_NRDREF, nrD_ref, S_KOUT, (double)k, S_GSTOP, 0.0));
+    NYS_TRY(launch_set_slots(ctx, S_INNER, 0.0, S_TSK, 0.0, S_TPCG, 0.0));
+    NYS_TRY(launch_set_slots(ctx, S_MUCUR, mu, S_GPAR0, opt->tol, S_GPAR1, bnorm));
+    NYS_TRY(launch_set_slots(ctx, S_GPAR2, cnorm, S_GPAR3, n_total, S_GPAR4, (double)opt->max_outer));
+    NYS_TRY(launch_set_slots(ctx, S_GPAR5, opt->reg_floor, S_GPAR6, (double)maxrec));
+    char key[512];
+    snprintf(key, sizeof(key), "gloop:%lld:%lld:%lld:%p:%p:%p:%p:%lld:%d:%llu:%d:%lld:%.17g:%.17g:%d:%d:%p:%.17g",
+             (long long)ctx->ws_epoch, (long long)m, (long long)n, (const void*)A, (const void*)q, (const void*)b,
+             (const void*)c, (long long)lda, ell, (unsigned long long)opt->seed, qp_in->structure, (long long)ncolA,
+             opt->pcg_c, opt->pcg_floor, opt->pcg_max_iter, qp_in->n_unit_blocks,
+             (const void*)qp_in->unit_blocks, n_total);
+    cudaGraphExec_t exec = nullptr;
+    int64_t body_launches = 0;
+    auto itg = ctx->graphs.find(key);
+    if (itg != ctx->graphs.end()) {
+      exec = itg->second.second.first;
+      body_launches = itg->second.first;
+    } else {
+      cudaGraph_t g;
+      NYS_CUDA_TRY(ctx, cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle hc;
+      NYS_CUDA_TRY(ctx, cudaGraphConditionalHandleCreate(&hc, g, 1u, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = hc;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t wnode;
+      NYS_CUDA_TRY(ctx, cudaGraphAddNode(&wnode, g, nullptr, 0, &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      const int64_t l0 = ctx->launches, mv0 = ctx->matvecs;
+      const int64_t ep0 = ctx->ws_epoch;
+      NYS_CUDA_TRY(ctx, cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+                                                       cudaStreamCaptureModeThreadLocal));
+      ctx->gloop = true;
+      int rc = gl_body();
+      if (rc == NYS_OK) rc = launch_ipm_control(ctx, grec, hc);
+      if (rc == NYS_OK) rc = launch_cond_copy(ctx, S_CPLAM, lam, y, m);
+      if (rc == NYS_OK) rc = launch_cond_copy(ctx, S_CPZETA, zeta, x, n);
+      ctx->gloop = false;
+      cudaGraph_t cap = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &cap);
+      body_launches = ctx->launches - l0;
+      ctx->launches = l0;
+      ctx->matvecs = mv0;
+      cudaError_t ie = cudaErrorUnknown;
+      if (rc == NYS_OK && ce == cudaSuccess && ctx->ws_epoch == ep0) ie = cudaGraphInstantiate(&exec, g, 0);
+      if (ie != cudaSuccess) {   // not capturable here (or a workspace grew): keep the host loop
+        cudaGetLastError();
+        cudaGraphDestroy(g);
+        if (getenv("NYS_DEBUG"))
+          fprintf(stderr, "[nys] graph loop not used (rc %d, capture %d, instantiate %d)\n", rc, (int)ce, (int)ie);
+        return NYS_OK;
+      }
+      if (ctx->graphs.size() >= 64) {
+        for (auto& kv : ctx->graphs) {
+          cudaGraphExecDestroy(kv.second.second.first);
+          cudaGraphDestroy(kv.second.second.second);
+        }
+        ctx->graphs.clear();
+      }
+      ctx->graphs[key] = std::make_pair(body_launches, std::make_pair(exec, g));
+    }
+    const int k0 = k;
+    NYS_CUDA_TRY(ctx, cudaGraphLaunch(exec, ctx->stream));
+    NYS_TRY(read_slots(ctx));
+    gst = (int)ctx->h_sc[S_GSTOP];
+    const int k1 = (int)ctx->h_sc[S_KOUT];
+    rho = ctx->h_sc[S_RHO]; delta = ctx->h_sc[S_DELTA]; mu = ctx->h_sc[S_OMU];
+    nrP = ctx->h_sc[S_NRP]; nrD = ctx->h_sc[S_NRD]; nrP_ref = ctx->h_sc[S_NRPREF]; nrD_ref = ctx->h_sc[S_NRDREF];
+    const int inner = (int)ctx->h_sc[S_INNER];
+    total_inner += inner;
+    t_sketch += ctx->h_sc[S_TSK];
+    t_pcg += ctx->h_sc[S_TPCG];
+    ctx->matvecs += inner;                                             // one-launch PCG: one matvec per iteration
+    ctx->launches += body_launches * (int64_t)(k1 - k0 + (gst == 2 || gst == 3 ? 1 : 0));
+    if (k1 > k0) {
+      std::vector<double> hr((size_t)16 * (k1 - k0));
+      NYS_CUDA_TRY(ctx, cudaMemcpy(hr.data(), grec + (size_t)16 * k0, hr.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int i = 0; i < k1 - k0; ++i) {
+        const double* r = hr.data() + (size_t)16 * i;
+        nys_iter_record rc2{};
+        rc2.k = (int)r[0]; rc2.mu = r[1]; rc2.rel_p = r[2]; rc2.rel_d = r[3]; rc2.alpha_p = r[4]; rc2.alpha_d = r[5];
+        rc2.pcg_pred = (int)r[6]; rc2.pcg_corr = (int)r[7]; rc2.rho = r[8]; rc2.delta = r[9];
+        rc2.t_sketch_ms = r[10]; rc2.t_pcg_ms = r[11]; rc2.t_other_ms = 0.0; rc2.lam_ell = r[12];
+        rc2.prec_built = 1; rc2.ell = ell;
+        if (R.records && R.n_records < R.max_records) R.records[R.n_records++] = rc2;
+      }
+    }
+    if (getenv("NYS_DEBUG")) fprintf(stderr, "[nys] graph loop: outer %d -> %d, stop code %d, %d PCG iterations\n", k0, k1, gst, inner);
+    k = k1;
+    return NYS_OK;
+  };
   for (k = 0; k <= opt->max_outer; ++k) {
     const double rel_p = nrP / (1.0 + bnorm), rel_d = nrD / (1.0 + cnorm);
     if (rel_p <= opt->tol && rel_d <= opt->tol && mu <= opt->tol) { status = NYS_OK; break; }   // A11
     if (k == opt->max_outer) break;
     if (!std::isfinite(mu) || !std::isfinite(nrP) || !std::isfinite(nrD)) { status = NYS_EBREAKDOWN; break; }
+    if (gl_ok && !gl_tried && k >= 1) {
+      gl_tried = true;
+      int gst = -1;
+      NYS_TRY(run_gloop(gst));
+      if (gst == 3) { status = NYS_EBREAKDOWN; break; }
+      if (gst >= 0) { --k; continue; }   // the loop head re-tests TC / the cap at the new k, or re-runs a failed build
+    }
     NvtxRange nv_outer("outer_iteration");
     // One host round trip per outer iteration (f3): the Nystrom build, both PCG solves and the step
     // run with deferred checks (device flags, latched counts) and everything is read with the

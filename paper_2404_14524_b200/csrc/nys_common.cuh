@@ -44,7 +44,13 @@ enum Slot : int {
   // breakdown flag, a Nystrom-factorisation failure flag and the graph-path iteration accounting are
   // latched on the device and read with the iteration's residuals
   S_PCGI0, S_PCGI1, S_PCGBRK, S_NYSFAIL, S_GITACC,
-  S_COUNT = 64
+  // graph-resident outer loop (f3, ipm_impl): the loop state lives on the device — rho, delta (S_DELTA),
+  // mu, the residual norms and the PEU references, the outer index, a stop code, the PEU copy flags,
+  // accumulated PCG iterations and phase times (globaltimer stamps), and the per-solve constants
+  S_RHO, S_OMU, S_NRP, S_NRD, S_NRPREF, S_NRDREF, S_KOUT, S_GSTOP, S_CPLAM, S_CPZETA, S_INNER, S_TSK, S_TPCG,
+  S_TS0, S_TS1, S_TS2, S_TS3, S_TS4, S_TS5,
+  S_GPAR0, S_GPAR1, S_GPAR2, S_GPAR3, S_GPAR4, S_GPAR5, S_GPAR6,
+  S_COUNT = 96
 };
 constexpr int kMaxCounters = 64;
 }  // namespace nys
@@ -59,6 +65,7 @@ struct nys_ctx {
   int rank = 0, world = 1;
   bool coll = false;               // a one-rank NCCL communicator (world = 1 with an id): multi-rank path
   bool multi() const { return world > 1 || coll; }
+  bool gloop = false;              // capturing the graph-resident outer loop: per-iteration scalars from slots
   void* nccl_comm = nullptr;
   void* loop_comm = nullptr;      // in-process loopback communicator (nys_loopback_comm_create)
   int num_sms = 148;

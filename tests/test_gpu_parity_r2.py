@@ -310,3 +310,47 @@ def test_residual_pass_fusion_is_bitwise(tmp_path, cfg, kw, ell, mo):
         subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
         outs.append(np.load(out))
     assert np.array_equal(outs[0], outs[1])
+
+
+# ------------------------------------------ graph-resident outer loop (f3) vs the host loop
+_LOOP_SCRIPT = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, {root!r})
+from synth import make_config
+from paper_2404_14524_b200 import Context, colmajor_device
+inst = make_config({cfg}, **{kw!r})
+ctx = Context(0)
+Ad, lda = colmajor_device(inst.A)
+dv = lambda a: torch.tensor(a, dtype=torch.float64, device="cuda")
+g = ctx.nys_ipppmm_solve(Ad, lda, inst.m, dv(inst.q), dv(inst.b), dv(inst.c), ell={ell}, max_outer={mo})
+recs = [[r[f] for f in ("k", "mu", "rel_p", "rel_d", "alpha_p", "alpha_d", "pcg_pred", "pcg_corr", "rho", "delta")]
+        for r in g["log"]]
+np.save({out!r}, np.concatenate([g[k].cpu().numpy() for k in ("x", "y", "z")]
+                                + [np.array([g["obj"], g["inner"], g["outer"], g["status"]]), np.ravel(recs)]))
+"""
+
+
+@pytest.mark.parametrize("cfg,kw,ell,mo", [(0, {}, 20, 100), (1, dict(m=300, n=1200, ell=30), 30, 100),
+                                           (3, dict(m=16, n=4000, ell=16), 16, 100), (1, dict(m=300, n=1200), 20, 4)])
+def test_graph_resident_outer_loop_equals_host_loop(tmp_path, cfg, kw, ell, mo):
+    """The outer iterations after the first run as ONE graph launch (conditional WHILE node, device-side
+    PEU / termination test / records); the same solve with the host loop (NYS_NO_GRAPH_LOOP=1) gives
+    bitwise-identical iterates, objective, counts, status and per-iteration records (mu, alpha, PCG
+    counts, rho, delta).  The last case stops at the outer-iteration cap inside the graph."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for host in (False, True):
+        out = str(tmp_path / f"l{int(host)}.npy")
+        env = dict(os.environ)
+        env.pop("NYS_NO_GRAPH_LOOP", None)
+        if host:
+            env["NYS_NO_GRAPH_LOOP"] = "1"
+        code = _LOOP_SCRIPT.format(root=root, cfg=cfg, kw=kw, ell=ell, mo=mo, out=out)
+        subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+        outs.append(np.load(out))
+    assert outs[0].shape == outs[1].shape
+    assert np.array_equal(outs[0], outs[1])
