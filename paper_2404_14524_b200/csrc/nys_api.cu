@@ -1259,14 +1259,20 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(launch_set_slots(ctx, S_GPAR2, cnorm, S_GPAR3, n_total, S_GPAR4, (double)opt->max_outer));
     NYS_TRY(launch_set_slots(ctx, S_GPAR5, opt->reg_floor, S_GPAR6, (double)maxrec));
     char key[512];
-    snprintf(key, sizeof(key), "gloop:%lld:%lld:%lld:%p:%p:%p:%p:%lld:%d:%llu:%d:%lld:%.17g:%.17g:%d:%d:%p:%.17g",
+    snprintf(key, sizeof(key), "gloop:%lld:%lld:%lld:%p:%p:%p:%p:%lld:%d:%llu:%d:%lld:%.17g:%.17g:%d:%d:%.17g:",
              (long long)ctx->ws_epoch, (long long)m, (long long)n, (const void*)A, (const void*)q, (const void*)b,
              (const void*)c, (long long)lda, ell, (unsigned long long)opt->seed, qp_in->structure, (long long)ncolA,
-             opt->pcg_c, opt->pcg_floor, opt->pcg_max_iter, qp_in->n_unit_blocks,
-             (const void*)qp_in->unit_blocks, n_total);
+             opt->pcg_c, opt->pcg_floor, opt->pcg_max_iter, qp_in->n_unit_blocks, n_total);
+    std::string gkey(key);
+    for (int ib = 0; ib < qp_in->n_unit_blocks; ++ib) {   // the unit blocks are kernel arguments (by value)
+      char ub_[96];
+      snprintf(ub_, sizeof(ub_), "%lld,%lld,%.17g;", (long long)qp_in->unit_blocks[ib].row0,
+               (long long)qp_in->unit_blocks[ib].count, qp_in->unit_blocks[ib].scale);
+      gkey += ub_;
+    }
     cudaGraphExec_t exec = nullptr;
     int64_t body_launches = 0;
-    auto itg = ctx->graphs.find(key);
+    auto itg = ctx->graphs.find(gkey);
     if (itg != ctx->graphs.end()) {
       exec = itg->second.second.first;
       body_launches = itg->second.first;
@@ -1314,7 +1320,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
         }
         ctx->graphs.clear();
       }
-      ctx->graphs[key] = std::make_pair(body_launches, std::make_pair(exec, g));
+      ctx->graphs[gkey] = std::make_pair(body_launches, std::make_pair(exec, g));
     }
     const int k0 = k;
     NYS_CUDA_TRY(ctx, cudaGraphLaunch(exec, ctx->stream));
