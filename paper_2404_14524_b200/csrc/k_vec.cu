@@ -1027,6 +1027,7 @@ __global__ void ipm_control_kernel(double* sc, double* rec, cudaGraphConditional
   sc[S_DELTA] = fmax(floor_, (p_imp ? (1.0 - rr) : (1.0 - 2.0 / 3.0 * rr)) * delta);
   sc[S_RHO] = fmax(floor_, (d_imp ? (1.0 - rr) : (1.0 - 2.0 / 3.0 * rr)) * rho);
   sc[S_INNER] += pred + corr;
+  sc[S_GLACC] += sc[S_GITACC];   // graph-path PCG iterations run by the nested WHILE bodies (accounting)
   sc[S_TSK] += tsk;
   sc[S_TPCG] += tpcg;
   sc[S_OMU] = mu_new;
@@ -1057,5 +1058,15 @@ int launch_cond_copy(nys_ctx* ctx, int flag, double* dst, const double* src, int
   cond_copy_kernel<<<ew_grid(ctx, len), 256, 0, ctx->stream>>>(ctx->sc, flag, dst, src, len);
   ctx->launches++;
   return ctx->check_launch("cond_copy");
+}
+}  // namespace nys
+
+namespace nys {
+// re-arm a WHILE node's condition (a nested conditional node gets its default only at graph launch)
+__global__ void set_cond_kernel(cudaGraphConditionalHandle h, unsigned int v) { cudaGraphSetConditional(h, v); }
+int launch_set_cond(nys_ctx* ctx, unsigned long long h, unsigned int v) {
+  set_cond_kernel<<<1, 1, 0, ctx->stream>>>((cudaGraphConditionalHandle)h, v);
+  ctx->launches++;
+  return ctx->check_launch("set_cond");
 }
 }  // namespace nys

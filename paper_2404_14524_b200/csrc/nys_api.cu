@@ -592,6 +592,55 @@ int pcg_impl(nys_ctx* ctx, const NormalOp& op, int ell, const double* U, int64_t
     // graph launch: a conditional WHILE node whose body is two iterations (p double-buffer
     // parity); pcg_update's last block clears the condition when PCG is done.
     for (int it = 0; it < 2; ++it) NYS_TRY(pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, it, max_iter, 0ull, chol));
+    if (ctx->gloop) {
+      // inside the graph-resident outer loop's capture: the WHILE node goes straight into the capturing
+      // graph (its handle created there), its two-iteration body captured on a side stream, and the outer
+      // capture continues after the node
+      cudaStreamCaptureStatus cst;
+      unsigned long long cid = 0;
+      cudaGraph_t cg_ = nullptr;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t ndeps = 0;
+      NYS_CUDA_TRY(ctx, cudaStreamGetCaptureInfo(ctx->stream, &cst, &cid, &cg_, &deps, &ndeps));
+      if (cst != cudaStreamCaptureStatusActive || cg_ == nullptr) {
+        ctx->set_error("PCG: nested graph capture without an active capture");
+        return NYS_ECUDA;
+      }
+      cudaGraphConditionalHandle hc;
+      NYS_CUDA_TRY(ctx, cudaGraphConditionalHandleCreate(&hc, cg_, 1, cudaGraphCondAssignDefault));
+      // the default applies only when the whole graph is launched: re-arm before every execution
+      NYS_TRY(launch_set_cond(ctx, (unsigned long long)hc, 1u));
+      NYS_CUDA_TRY(ctx, cudaStreamGetCaptureInfo(ctx->stream, &cst, &cid, &cg_, &deps, &ndeps));
+      cudaGraphNodeParams gp = {};
+      gp.type = cudaGraphNodeTypeConditional;
+      gp.conditional.handle = hc;
+      gp.conditional.type = cudaGraphCondTypeWhile;
+      gp.conditional.size = 1;
+      cudaGraphNode_t wn;
+      NYS_CUDA_TRY(ctx, cudaGraphAddNode(&wn, cg_, deps, ndeps, &gp));
+      cudaGraph_t body = gp.conditional.phGraph_out[0];
+      if (!ctx->side_stream) NYS_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+      cudaStream_t main_stream = ctx->stream;
+      ctx->stream = ctx->side_stream;
+      int rc = NYS_OK;
+      cudaError_t eb = cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+      if (eb == cudaSuccess) {
+        rc = pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, 2, max_iter, (unsigned long long)hc, chol);
+        if (rc == NYS_OK) rc = pcg_iteration(ctx, op, ell, U, ldu, s, x, r, z, Pp, h, 3, max_iter, (unsigned long long)hc, chol);
+        cudaGraph_t bo = body;
+        const cudaError_t ee = cudaStreamEndCapture(ctx->stream, &bo);
+        if (rc == NYS_OK && ee != cudaSuccess) rc = NYS_ECUDA;
+      }
+      ctx->stream = main_stream;
+      if (eb != cudaSuccess || rc != NYS_OK) {
+        ctx->set_error("PCG: nested graph capture failed");
+        return rc != NYS_OK ? rc : NYS_ECUDA;
+      }
+      NYS_CUDA_TRY(ctx, cudaStreamUpdateCaptureDependencies(ctx->stream, &wn, 1, cudaStreamSetCaptureDependencies));
+      res.iters = -1;
+      res.status = 0;
+      return launch_pcg_latch(ctx, defer_slot);
+    }
     // the key holds every value the captured kernels take as an argument: for the partial-Cholesky
     // path its rank, leading dimension and factor pointers too (a later build with a smaller rank
     // grows no workspace, so ws_epoch alone would not tell the graphs apart)
@@ -1206,7 +1255,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
   // iteration with its checks (A4 retries).
   const bool gl_ok = !ctx->multi() && !use_chol && !gen && ell > 0 && ell_cap == ell && opt->prec_refresh <= 1 &&
                      !(opt->prec_growth > 0.0) && !opt->verbose && getenv("NYS_NO_GRAPH_LOOP") == nullptr &&
-                     pcg_persistent_supported(ctx, m, ncolA, ell);
+                     getenv("NYS_NO_GRAPH") == nullptr;
   bool gl_tried = false;
   auto gl_body = [&]() -> int {   // one outer iteration, deferred checks, no host read
     NYS_TRY(launch_stamp(ctx, S_TS0));
@@ -1255,6 +1304,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(launch_set_slots(ctx, S_NRP, nrP, S_NRD, nrD, S_NRPREF, nrP_ref));
     NYS_TRY(launch_set_slots(ctx, S_NRDREF, nrD_ref, S_KOUT, (double)k, S_GSTOP, 0.0));
     NYS_TRY(launch_set_slots(ctx, S_INNER, 0.0, S_TSK, 0.0, S_TPCG, 0.0));
+    NYS_TRY(launch_set_slots(ctx, S_GLACC, 0.0));
     NYS_TRY(launch_set_slots(ctx, S_MUCUR, mu, S_GPAR0, opt->tol, S_GPAR1, bnorm));
     NYS_TRY(launch_set_slots(ctx, S_GPAR2, cnorm, S_GPAR3, n_total, S_GPAR4, (double)opt->max_outer));
     NYS_TRY(launch_set_slots(ctx, S_GPAR5, opt->reg_floor, S_GPAR6, (double)maxrec));
@@ -1334,7 +1384,8 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     t_sketch += ctx->h_sc[S_TSK];
     t_pcg += ctx->h_sc[S_TPCG];
     ctx->matvecs += inner;                                             // one-launch PCG: one matvec per iteration
-    ctx->launches += body_launches * (int64_t)(k1 - k0 + (gst == 2 || gst == 3 ? 1 : 0));
+    ctx->launches += body_launches * (int64_t)(k1 - k0 + (gst == 2 || gst == 3 ? 1 : 0)) +
+                     (int64_t)ctx->h_sc[S_GLACC] * (ell > 0 ? 4 : 3);
     if (k1 > k0) {
       std::vector<double> hr((size_t)16 * (k1 - k0));
       NYS_CUDA_TRY(ctx, cudaMemcpy(hr.data(), grec + (size_t)16 * k0, hr.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1744,6 +1795,7 @@ int nys_destroy(nys_ctx* ctx) {
   }
   if (ctx->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)ctx->nccl_comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
   delete ctx;
   return NYS_OK;
 }

@@ -49,7 +49,7 @@ enum Slot : int {
   // accumulated PCG iterations and phase times (globaltimer stamps), and the per-solve constants
   S_RHO, S_OMU, S_NRP, S_NRD, S_NRPREF, S_NRDREF, S_KOUT, S_GSTOP, S_CPLAM, S_CPZETA, S_INNER, S_TSK, S_TPCG,
   S_TS0, S_TS1, S_TS2, S_TS3, S_TS4, S_TS5,
-  S_GPAR0, S_GPAR1, S_GPAR2, S_GPAR3, S_GPAR4, S_GPAR5, S_GPAR6,
+  S_GPAR0, S_GPAR1, S_GPAR2, S_GPAR3, S_GPAR4, S_GPAR5, S_GPAR6, S_GLACC,
   S_COUNT = 96
 };
 constexpr int kMaxCounters = 64;
@@ -66,6 +66,7 @@ struct nys_ctx {
   bool coll = false;               // a one-rank NCCL communicator (world = 1 with an id): multi-rank path
   bool multi() const { return world > 1 || coll; }
   bool gloop = false;              // capturing the graph-resident outer loop: per-iteration scalars from slots
+  cudaStream_t side_stream = nullptr;  // nested captures (the PCG WHILE body inside the outer loop's body)
   void* nccl_comm = nullptr;
   void* loop_comm = nullptr;      // in-process loopback communicator (nys_loopback_comm_create)
   int num_sms = 148;

@@ -322,9 +322,14 @@ from synth import make_config
 from paper_2404_14524_b200 import Context, colmajor_device
 inst = make_config({cfg}, **{kw!r})
 ctx = Context(0)
-Ad, lda = colmajor_device(inst.A)
 dv = lambda a: torch.tensor(a, dtype=torch.float64, device="cuda")
-g = ctx.nys_ipppmm_solve(Ad, lda, inst.m, dv(inst.q), dv(inst.b), dv(inst.c), ell={ell}, max_outer={mo})
+if {cfg} == 2:   # the SVM operator (structure 1): m > 8192 -> the PCG's own WHILE node nested in the loop's
+    Ad, lda = colmajor_device(inst.extra["Xt"])
+    g = ctx.nys_ipppmm_solve(Ad, lda, inst.m, dv(inst.q), dv(inst.b), dv(inst.c), ell={ell}, max_outer={mo},
+                             structure=1)
+else:
+    Ad, lda = colmajor_device(inst.A)
+    g = ctx.nys_ipppmm_solve(Ad, lda, inst.m, dv(inst.q), dv(inst.b), dv(inst.c), ell={ell}, max_outer={mo})
 recs = [[r[f] for f in ("k", "mu", "rel_p", "rel_d", "alpha_p", "alpha_d", "pcg_pred", "pcg_corr", "rho", "delta")]
         for r in g["log"]]
 np.save({out!r}, np.concatenate([g[k].cpu().numpy() for k in ("x", "y", "z")]
@@ -333,12 +338,15 @@ np.save({out!r}, np.concatenate([g[k].cpu().numpy() for k in ("x", "y", "z")]
 
 
 @pytest.mark.parametrize("cfg,kw,ell,mo", [(0, {}, 20, 100), (1, dict(m=300, n=1200, ell=30), 30, 100),
-                                           (3, dict(m=16, n=4000, ell=16), 16, 100), (1, dict(m=300, n=1200), 20, 4)])
+                                           (3, dict(m=16, n=4000, ell=16), 16, 100), (1, dict(m=300, n=1200), 20, 4),
+                                           (2, dict(m=20000, n=100, ell=50), 50, 100),
+                                           (1, dict(m=9000, n=3000, ell=40), 40, 6)])
 def test_graph_resident_outer_loop_equals_host_loop(tmp_path, cfg, kw, ell, mo):
     """The outer iterations after the first run as ONE graph launch (conditional WHILE node, device-side
     PEU / termination test / records); the same solve with the host loop (NYS_NO_GRAPH_LOOP=1) gives
     bitwise-identical iterates, objective, counts, status and per-iteration records (mu, alpha, PCG
-    counts, rho, delta).  The last case stops at the outer-iteration cap inside the graph."""
+    counts, rho, delta).  The fourth case stops at the outer-iteration cap inside the graph; the last two
+    have m > 8192, where each PCG solve is itself a graph WHILE node, nested in the loop's body."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
