@@ -1001,6 +1001,8 @@ __global__ void ipm_control_kernel(double* sc, double* rec, cudaGraphConditional
   const int k = (int)sc[S_KOUT];
   if (sc[S_NYSFAIL] != 0.0 || sc[S_PCGBRK] != 0.0) {
     sc[S_GSTOP] = sc[S_NYSFAIL] != 0.0 ? 2.0 : 3.0;
+    sc[S_CPLAM] = 0.0;   // the discarded iteration copies nothing
+    sc[S_CPZETA] = 0.0;
     cudaGraphSetConditional(h, 0u);
     return;
   }
@@ -1062,6 +1064,15 @@ int launch_cond_copy(nys_ctx* ctx, int flag, double* dst, const double* src, int
 }  // namespace nys
 
 namespace nys {
+// test hook (NYS_INJECT_NYSFAIL=k): raise the factorisation-failure flag in outer iteration k
+__global__ void inject_nysfail_kernel(double* sc, int k) {
+  if ((int)sc[S_KOUT] == k) sc[S_NYSFAIL] = 1.0;
+}
+int launch_inject_nysfail(nys_ctx* ctx, int k) {
+  inject_nysfail_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sc, k);
+  ctx->launches++;
+  return ctx->check_launch("inject_nysfail");
+}
 // re-arm a WHILE node's condition (a nested conditional node gets its default only at graph launch)
 __global__ void set_cond_kernel(cudaGraphConditionalHandle h, unsigned int v) { cudaGraphSetConditional(h, v); }
 int launch_set_cond(nys_ctx* ctx, unsigned long long h, unsigned int v) {

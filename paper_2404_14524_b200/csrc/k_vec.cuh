@@ -60,6 +60,7 @@ int launch_stamp(nys_ctx* ctx, int slot);
 int launch_ipm_control(nys_ctx* ctx, double* rec, cudaGraphConditionalHandle h);
 int launch_cond_copy(nys_ctx* ctx, int flag, double* dst, const double* src, int64_t len);
 int launch_set_cond(nys_ctx* ctx, unsigned long long h, unsigned int v);
+int launch_inject_nysfail(nys_ctx* ctx, int k);
 // structure 2 (k_gen.cu): scaled identity blocks of A (nys_unit_block); off = column offsets in the unit part
 struct UnitBlocks {
   int nb = 0;

@@ -1257,6 +1257,8 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
                      !(opt->prec_growth > 0.0) && !opt->verbose && getenv("NYS_NO_GRAPH_LOOP") == nullptr &&
                      getenv("NYS_NO_GRAPH") == nullptr;
   bool gl_tried = false;
+  // test hook: NYS_INJECT_NYSFAIL=k raises the factorisation-failure flag in deferred outer iteration k
+  static const int inject_k = getenv("NYS_INJECT_NYSFAIL") ? atoi(getenv("NYS_INJECT_NYSFAIL")) : -1;
   auto gl_body = [&]() -> int {   // one outer iteration, deferred checks, no host read
     NYS_TRY(launch_stamp(ctx, S_TS0));
     NYS_TRY(launch_scaling(ctx, n, q, x, z, rho, d));                // rho from S_RHO
@@ -1265,6 +1267,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
     NYS_TRY(launch_set_slots(ctx, S_PCGBRK, 0.0, S_NYSFAIL, 0.0, S_GITACC, 0.0));
     NYS_TRY(gen_omega(ctx, m, ell, opt->seed, 0, Om));                 // stream S_KOUT + 1 (A6)
     NYS_TRY(sketch_impl(ctx, m, op.n, op.A, op.lda, op.d, op.e, ell, Om, U, lamh, nullptr, true));
+    if (inject_k >= 0) NYS_TRY(launch_inject_nysfail(ctx, inject_k));   // test hook
     NYS_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->sc + S_LAML, lamh + ell - 1, 8, cudaMemcpyDeviceToDevice, ctx->stream));
     NYS_TRY(launch_prec_coef(ctx, lamh, ell, delta, scoef));           // mu_prec = S_DELTA (A7)
     NYS_TRY(launch_stamp(ctx, S_TS1));
@@ -1451,6 +1454,7 @@ int ipm_impl(nys_ctx* ctx, const nys_qp* qp_in, const nys_options* opt, nys_solu
       if (rebuild) {                                                  // f3: reuse between rebuilds
         NYS_TRY(gen_omega(ctx, m, ell_k, opt->seed, (uint64_t)k + 1, Om));
         NYS_TRY(sketch_impl(ctx, m, op.n, op.A, op.lda, op.d, op.e, ell_k, Om, U, lamh, nullptr, defer));
+        if (defer && inject_k == k) NYS_TRY(launch_set_slots(ctx, S_NYSFAIL, 1.0));   // test hook
         last_build = k;
         base_its = -1;
         rec.prec_built = 1;

@@ -362,3 +362,28 @@ def test_graph_resident_outer_loop_equals_host_loop(tmp_path, cfg, kw, ell, mo):
         outs.append(np.load(out))
     assert outs[0].shape == outs[1].shape
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("host_loop", [False, True])
+def test_failed_factorisation_iteration_is_rerun_bitwise(tmp_path, host_loop):
+    """A Nystrom factorisation failure in a deferred outer iteration (injected: NYS_INJECT_NYSFAIL=2)
+    discards that iteration on the device and the host re-runs it with its checks; the solve ends
+    bitwise where the undisturbed one does — from inside the graph-resident loop (which stops and
+    hands over to the host loop) and in the host loop itself."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for inject in (False, True):
+        out = str(tmp_path / f"f{int(inject)}.npy")
+        env = dict(os.environ)
+        env.pop("NYS_INJECT_NYSFAIL", None)
+        env.pop("NYS_NO_GRAPH_LOOP", None)
+        if inject:
+            env["NYS_INJECT_NYSFAIL"] = "2"
+        if host_loop:
+            env["NYS_NO_GRAPH_LOOP"] = "1"
+        code = _LOOP_SCRIPT.format(root=root, cfg=1, kw=dict(m=300, n=1200, ell=30), ell=30, mo=100, out=out)
+        subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
