@@ -143,18 +143,21 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       // L2 prefetch runs PF panels ahead of the smem ring: the reduction / barrier phases of an
       // iteration leave HBM idle, so the next matvec's panels are pulled into L2 meanwhile
       long long pf = 0;
+      int64_t pfi = 0;        // pf mod niter, kept incrementally (no 64-bit division per panel)
       const int PF = P.l2_prefetch;
-      for (;;) {
-        const int s = (int)(q % S);
+      int s = -1;
+      uint32_t par = 1u;      // parity of the empty-barrier phase to wait for (first pass: none)
+      int64_t it = 0;         // q mod niter
+      for (;; ++q) {
+        if (++s == S) { s = 0; par ^= 1u; }
         for (; pf < q + S + PF; ++pf) {
-          const int64_t itp = pf % niter;
-          const int64_t c0 = c_lo + itp * BN;
+          const int64_t c0 = c_lo + pfi * BN;
+          if (++pfi == niter) pfi = 0;
           int64_t nc = c_hi - c0;
           nc = nc > BN ? BN : nc;
           if (pf >= q + S) bulk_prefetch_l2(P.A + c0 * P.lda, (uint32_t)(((nc - 1) * P.lda) * 8) + copy_bytes);
         }
         if (q >= S) {
-          const uint32_t par = (uint32_t)(((q / S) - 1) & 1);
           bool stop = false;
           for (;;) {
             uint32_t ok;
@@ -169,7 +172,6 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
           if (stop) break;
         }
         if (s_stop) break;
-        const int64_t it = q % niter;
         const int64_t col0 = c_lo + it * BN;
         int64_t ncols = c_hi - col0;
         ncols = ncols > BN ? BN : ncols;
@@ -184,7 +186,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
             bulk_g2s(stage + ((size_t)s * BN + c) * rs, P.A + (col0 + c) * P.lda, copy_bytes, &full[s],
                      it < P.l2_keep ? pol_keep : pol_stream);
         }
-        ++q;
+        if (++it == niter) it = 0;
       }
       s_issued = q;
     }
@@ -199,6 +201,8 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   const int row16 = tid & 15, grp16 = (tid >> 4) & 15;  // first 256 threads: 16 rows x 16 groups
   const int hrow = lane & 15, hw = 2 * warp + (lane >> 4);
   long long qc = 0;  // consumed stage counter
+  int cs = 0;        // its stage index and full-barrier parity (kept incrementally)
+  uint32_t cph = 0u;
   unsigned int bar_epoch = 0;  // grid barriers passed (thread 0)
   unsigned int red_epoch = 0;  // column reductions done (thread 0)
   int trace_k = 0;
@@ -536,8 +540,9 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       dnext[c] = (niter > 0 && col < c_hi) ? __ldg(P.d + col) : 0.0;
     }
     for (int64_t it = 0; it < niter; ++it, ++qc) {
-      const int s = (int)(qc % S);
-      const uint32_t par = (uint32_t)((qc / S) & 1);
+      const int s = cs;
+      const uint32_t par = cph;
+      if (++cs == S) { cs = 0; cph ^= 1u; }
       const int64_t col0 = c_lo + it * BN + (int64_t)g * CPG;
       double dpre[CPG];
 #pragma unroll
@@ -671,7 +676,10 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   if (tid == 0) s_stop = 1;
   named_bar_sync(10, T + 32);
   const long long issued = s_issued;
-  for (; qc < issued; ++qc) mbar_wait(&full[(int)(qc % S)], (uint32_t)((qc / S) & 1));
+  for (; qc < issued; ++qc) {
+    mbar_wait(&full[cs], cph);
+    if (++cs == S) { cs = 0; cph ^= 1u; }
+  }
   if (cid == 0 && tid == 0) {
     P.sc[S_ITERS] = (double)iters;
     P.sc[S_STATUS] = (double)status;
@@ -1147,13 +1155,15 @@ static PcgKernel pcg_kernel_for(const PcgCfg& c) {
 }
 
 bool pcg_persistent_supported(nys_ctx* ctx, int64_t m, int64_t n, int ell) {
-  return !ctx->multi() && m <= 8192 && n > 0 && ell <= 256 && getenv("NYS_NO_PERSISTENT") == nullptr;
+  if (m > 8192) return pcg_cluster_supported(ctx, m, n, ell);
+  return !ctx->multi() && n > 0 && ell <= 256 && getenv("NYS_NO_PERSISTENT") == nullptr;
 }
 
 // tolerance must already be in sc[S_TOL] and delta in sc[S_DELTA]
 int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
                           const double* e, const double* U, int64_t ldu, int ell, const double* s, const double* rhs,
                           double* x, int max_iter) {
+  if (m > 8192) return launch_pcg_cluster(ctx, m, n, A, lda, d, e, U, ldu, ell, s, rhs, x, max_iter);
   const auto hp0 = std::chrono::steady_clock::now();
   PcgCfg c = pcg_pick(m, n, ctx->num_sms);
   if (const char* ov = getenv("NYS_PCG_CFG")) {  // tuning override "T,GT,RPT,CPG" (must be instantiated)

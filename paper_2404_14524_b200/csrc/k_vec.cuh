@@ -156,6 +156,11 @@ int launch_set_slots(nys_ctx* ctx, int k0, double v0, int k1 = -1, double v1 = 0
 bool pcg_small_supported(nys_ctx* ctx, int64_t m, int64_t n, int ell);
 int launch_pcg_small(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d, const double* e,
                      const double* U, int64_t ldu, int ell, const double* s, const double* rhs, double* x, int max_iter);
+// m > 8192 on one GPU: the persistent cluster PCG (k_pcgc.cu), dispatched by launch_pcg_persistent
+bool pcg_cluster_supported(nys_ctx* ctx, int64_t m, int64_t n, int ell);
+int launch_pcg_cluster(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
+                       const double* e, const double* U, int64_t ldu, int ell, const double* s, const double* rhs,
+                       double* x, int max_iter);
 bool pcg_persistent_supported(nys_ctx* ctx, int64_t m, int64_t n, int ell);
 int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, const double* d,
                           const double* e, const double* U, int64_t ldu, int ell, const double* s, const double* rhs,

@@ -124,13 +124,19 @@ GRAPH_PCG = [(8193, 300, 30, False), (8193, 300, 0, False), (20000, 200, 40, Fal
              (50000, 120, 100, False), (50000, 120, 100, True), (50000, 120, 0, True)]
 
 
+@pytest.mark.parametrize("path", ["cluster", "graph"])
 @pytest.mark.parametrize("m,n,ell,use_e", GRAPH_PCG)
-def test_graph_path_pcg_fixed_iterations_match_oracle(ctx, m, n, ell, use_e):
-    """Exactly 15 iterations (tol = 0) of the single-GPU graph-path PCG (cluster matvec in pcg_fused
-    mode, pcg_update / hred / precond kernels inside a conditional-WHILE graph) against oracle.pcg on
-    the same operator A D A^T (+ diag(e)) + delta I and the same Nystrom factors; use_e is the
-    structure-1 (config 2) operator's diagonal term."""
+def test_graph_path_pcg_fixed_iterations_match_oracle(ctx, m, n, ell, use_e, path, monkeypatch):
+    """Exactly 15 iterations (tol = 0) of the single-GPU PCG for m > 8192 against oracle.pcg on the same
+    operator A D A^T (+ diag(e)) + delta I and the same Nystrom factors; use_e is the structure-1
+    (config 2) operator's diagonal term.  path "cluster": the persistent cluster kernel (k_pcgc.cu, the
+    default); "graph" (NYS_NO_PCG_CLUSTER=1): cluster matvec in pcg_fused mode, pcg_update / hred /
+    precond kernels inside a conditional-WHILE graph (the multi-rank and partial-Cholesky loop)."""
     from paper_2404_14524_b200 import colmajor_device
+    if path == "graph":
+        monkeypatch.setenv("NYS_NO_PCG_CLUSTER", "1")
+    else:
+        monkeypatch.delenv("NYS_NO_PCG_CLUSTER", raising=False)
     rs = np.random.default_rng(m + n + ell)
     A = rs.standard_normal((m, n)) / np.sqrt(n)
     d = rs.uniform(0.01, 2.0, n)
@@ -340,13 +346,19 @@ np.save({out!r}, np.concatenate([g[k].cpu().numpy() for k in ("x", "y", "z")]
 @pytest.mark.parametrize("cfg,kw,ell,mo", [(0, {}, 20, 100), (1, dict(m=300, n=1200, ell=30), 30, 100),
                                            (3, dict(m=16, n=4000, ell=16), 16, 100), (1, dict(m=300, n=1200), 20, 4),
                                            (2, dict(m=20000, n=100, ell=50), 50, 100),
-                                           (1, dict(m=9000, n=3000, ell=40), 40, 6)])
+                                           (1, dict(m=9000, n=3000, ell=40), 40, 6),
+                                           (2, dict(m=20000, n=100, ell=50), 50, "nopc"),
+                                           (1, dict(m=9000, n=3000, ell=40), 40, "nopc")])
 def test_graph_resident_outer_loop_equals_host_loop(tmp_path, cfg, kw, ell, mo):
     """The outer iterations after the first run as ONE graph launch (conditional WHILE node, device-side
     PEU / termination test / records); the same solve with the host loop (NYS_NO_GRAPH_LOOP=1) gives
     bitwise-identical iterates, objective, counts, status and per-iteration records (mu, alpha, PCG
-    counts, rho, delta).  The fourth case stops at the outer-iteration cap inside the graph; the last two
-    have m > 8192, where each PCG solve is itself a graph WHILE node, nested in the loop's body."""
+    counts, rho, delta).  The fourth case stops at the outer-iteration cap inside the graph; the last four
+    have m > 8192: each PCG solve is one persistent cluster-kernel launch, and with NYS_NO_PCG_CLUSTER=1
+    ("nopc", the full solve) a graph WHILE node nested in the loop's body."""
+    env_extra = {}
+    if mo == "nopc":
+        env_extra, mo = {"NYS_NO_PCG_CLUSTER": "1"}, 100
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -357,6 +369,7 @@ def test_graph_resident_outer_loop_equals_host_loop(tmp_path, cfg, kw, ell, mo):
         env.pop("NYS_NO_GRAPH_LOOP", None)
         if host:
             env["NYS_NO_GRAPH_LOOP"] = "1"
+        env.update(env_extra)
         code = _LOOP_SCRIPT.format(root=root, cfg=cfg, kw=kw, ell=ell, mo=mo, out=out)
         subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
         outs.append(np.load(out))

@@ -13,7 +13,7 @@ needing a reset).  Run with NYS_DEBUG_GUARD=1:
 
 Cases cover every kernel family: fused matvec (whole-column and cluster/DSMEM split), sketch GEMMs +
 CholQR3 + one-sided Jacobi (single CTA, block-cluster), persistent PCG (cooperative grid barriers),
-graph-path PCG (conditional WHILE graph), partial Cholesky, capped Nys-IP-PMM solves (dense,
+persistent cluster PCG (m > 8192), graph-path PCG (conditional WHILE graph), partial Cholesky, capped Nys-IP-PMM solves (dense,
 structured) and the loopback multi-rank path.  Exit code != 0 on any failure."""
 import os
 import sys
@@ -136,8 +136,7 @@ def _(rs):
     return {"x": x.check("pcg_persistent x")}
 
 
-@case("pcg_graph")
-def _(rs):
+def _pcg_large(rs, name):
     m, n, ell = 20000, 60, 30
     A = rs.standard_normal((m, n)) / np.sqrt(n)
     Ad, lda = colmajor_device(A)
@@ -146,7 +145,21 @@ def _(rs):
     x = Guarded(m)
     ctx.nys_pcg_solve(Ad, lda, m, d, dv(rs.uniform(0, 1, m)), 1e-3, ell, U, lam, 1e-3, dv(rs.standard_normal(m)),
                       x.t, 0.0, 6)
-    return {"x": x.check("pcg_graph x")}
+    return {"x": x.check(f"{name} x")}
+
+
+@case("pcg_cluster")      # m > 8192: the persistent cluster kernel (cluster DSMEM exchange, grid barriers)
+def _(rs):
+    return _pcg_large(rs, "pcg_cluster")
+
+
+@case("pcg_graph")        # the same solve through the conditional-WHILE graph path
+def _(rs):
+    os.environ["NYS_NO_PCG_CLUSTER"] = "1"
+    try:
+        return _pcg_large(rs, "pcg_graph")
+    finally:
+        del os.environ["NYS_NO_PCG_CLUSTER"]
 
 
 @case("chol")
