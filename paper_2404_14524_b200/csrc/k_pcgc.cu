@@ -53,6 +53,7 @@ struct PcgCParams {
   int cl;
   int64_t rs;            // rows per cluster rank (even)
   int64_t rpc;           // rows per CTA in the vector phases
+  unsigned long long* trace;   // debug (NYS_PCG_TRACE): [2 CTAs][16 iterations][8] globaltimer stamps
 };
 
 constexpr int PC_T = 480;              // consumer threads (15 warps) + 1 producer warp
@@ -188,6 +189,14 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
   int status = 0;
   const double delta = P.sc[S_DELTA];
   const int ncol = 1 + ell;
+  int trace_k = -1;
+  auto stamp = [&](int slot) {
+    if (P.trace != nullptr && tid == 0 && (bid == 0 || bid == G - 1) && trace_k >= 0 && trace_k < 16) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      P.trace[((bid == 0 ? 0 : 1) * 16 + trace_k) * 8 + slot] = t;
+    }
+  };
 
   // ---- the CTA's own rows: (init) x = 0, r = rhs | x += alpha p_k, r -= alpha w; rr, U^T r row -------
   auto rows_phase = [&](bool init, double alpha, const double* pk) {
@@ -358,6 +367,8 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
   for (int k = 0; !stop; ++k) {
     const double* pk = (k & 1) ? P.P0 : P.P1;   // p_k
     double* pn = (k & 1) ? P.P1 : P.P0;         // receives p_{k+1}
+    trace_k = k;
+    stamp(0);
     // ---- P1: p_k slice; fused matvec over this cluster's panels (lag-1 dot exchange) --------------
     double vreg[RPT], wacc[RPT];
 #pragma unroll
@@ -440,7 +451,9 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
         P.pwp[bid] = b;
       }
     }
+    stamp(1);
     pcgc_grid_barrier(P.bar, G, bar_epoch);
+    stamp(2);
     // ---- P2: alpha, own rows, partial rows -------------------------------------------------------
     if (warp == 0) {
       const double pw = warp_sum_array(P.pwp, (int)G);
@@ -451,15 +464,19 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
     if (!(pw > 0.0) || !isfinite(pw)) { status = NYS_EBREAKDOWN; break; }
     const double alpha = rz / pw;
     rows_phase(false, alpha, pk);
+    stamp(3);
     // ---- P3: reduction, stop test, p_{k+1} -------------------------------------------------------
     reduce_rows();
+    stamp(4);
     if (converged(false)) break;
     const double rzn = s_scal[1];
     if (!(rzn > 0.0) || !isfinite(rzn)) { status = NYS_EBREAKDOWN; break; }
     const double beta = rzn / rz;
     rz = rzn;
     prec_rows(false, beta, pk, pn);
+    stamp(5);
     pcgc_grid_barrier(P.bar, G, bar_epoch);
+    stamp(6);
   }
 
   // ---- exit: stop the producer, drain in-flight bulk copies, publish the scalars ------------------
@@ -590,8 +607,26 @@ int launch_pcg_cluster(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int6
     fprintf(stderr, "[nys] cluster PCG m=%lld n=%lld ell=%d: cl=%d clusters=%lld G=%d rs=%lld rpc=%lld stages=%d smem=%zu\n",
             (long long)m, (long long)n, ell, pl.cl, (long long)ncl, G, (long long)P.rs, (long long)P.rpc, pl.stages,
             pl.smem);
+  const bool trace = getenv("NYS_PCG_TRACE") != nullptr;
+  if (trace) {
+    P.trace = (unsigned long long*)ctx->ws("pc_trace", 2 * 16 * 8 * 8);
+    NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.trace, 0, 2 * 16 * 8 * 8, ctx->stream));
+  }
   NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, P));
   ctx->launches++;
+  if (trace) {
+    unsigned long long h[2 * 16 * 8];
+    NYS_CUDA_TRY(ctx, cudaMemcpyAsync(h, P.trace, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int c = 0; c < 2; ++c)
+      for (int it = 8; it < 12; ++it) {
+        const unsigned long long* r = h + (c * 16 + it) * 8;
+        if (r[0] == 0 || r[6] == 0) continue;
+        fprintf(stderr, "[pcgctrace] cta=%s it=%d matvec=%.2f bar1=%.2f rows=%.2f reduce=%.2f prec=%.2f bar3=%.2f total=%.2f us\n",
+                c ? "last" : "0", it, (r[1] - r[0]) * 1e-3, (r[2] - r[1]) * 1e-3, (r[3] - r[2]) * 1e-3,
+                (r[4] - r[3]) * 1e-3, (r[5] - r[4]) * 1e-3, (r[6] - r[5]) * 1e-3, (r[6] - r[0]) * 1e-3);
+      }
+  }
   return ctx->check_launch("pcg_cluster");
 }
 
