@@ -376,6 +376,38 @@ def main():
                                         precond=1 if args.precond == "chol" else 0, ell_max=args.ell_max,
                                         max_outer=args.max_outer)
 
+    # ---- secondary legs (N = 1, headline run only): configs 1 and 2 time-to-1e-8, complete solves ------
+    # run BEFORE the headline: the 20 GB headline step drives the GPU into its power cap (SM clock
+    # ~1650-1870 MHz), and the short config-1 solves measured right after it ran ~15 % slower (95.7 vs
+    # 82.8 ms on one box) than on a GPU that was not just throttled
+    secondary = None
+    if world == 1 and args.config == 4 and not args.no_secondary:
+        secondary = {}
+        for sc in (1, 2):
+            w2 = Workload(sc, 0, 1, device, 0)
+
+            def solve2(w2=w2):
+                with torch.cuda.stream(stream):
+                    return ctx.nys_ipppmm_solve(w2.At, w2.lda, w2.m, w2.q, w2.b, w2.c, ell=w2.ell,
+                                                structure=w2.structure, unit_blocks=w2.unit_blocks)
+            for _ in range(3):
+                solve2()
+            barrier()
+            K2 = 3
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r2 = [solve2() for _ in range(K2)]
+            e1.record(stream)
+            barrier()
+            g2 = r2[-1]
+            secondary[f"config{sc}"] = {
+                "workload": w2.name, "metric": "Nys-IP-PMM time-to-1e-8", "value": e0.elapsed_time(e1) / 1e3 / K2,
+                "unit": "s", "steps": K2, "warmup": 3, "status": g2["status"], "outer": g2["outer"],
+                "inner": g2["inner"], "obj": g2["obj"], "rel_p": g2["rel_p"], "rel_d": g2["rel_d"], "mu": g2["mu"],
+                "t_sketch_ms": g2["t_sketch_ms"], "t_pcg_ms": g2["t_pcg_ms"], "t_other_ms": g2["t_other_ms"]}
+            del w2, r2
+            torch.cuda.empty_cache()
+
     # ---- warm-up ------------------------------------------------------------------------------
     W = max(args.warmup, 3)
     for _ in range(W):
@@ -548,35 +580,6 @@ def main():
                    "flops_per_call": sk_flops, "call_us": t_sk * 1e6,
                    "share_of_step": (last["outer"] + 1) * t_sk / sec_per_solve if args.ell_max == 0 else None}
         del Om_s, Y_s
-
-    # ---- secondary legs (N = 1, headline run only): configs 1 and 2 time-to-1e-8, complete solves ------
-    secondary = None
-    if world == 1 and args.config == 4 and not args.no_secondary:
-        secondary = {}
-        for sc in (1, 2):
-            w2 = Workload(sc, 0, 1, device, 0)
-
-            def solve2(w2=w2):
-                with torch.cuda.stream(stream):
-                    return ctx.nys_ipppmm_solve(w2.At, w2.lda, w2.m, w2.q, w2.b, w2.c, ell=w2.ell,
-                                                structure=w2.structure, unit_blocks=w2.unit_blocks)
-            for _ in range(3):
-                solve2()
-            barrier()
-            K2 = 3
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            r2 = [solve2() for _ in range(K2)]
-            e1.record(stream)
-            barrier()
-            g2 = r2[-1]
-            secondary[f"config{sc}"] = {
-                "workload": w2.name, "metric": "Nys-IP-PMM time-to-1e-8", "value": e0.elapsed_time(e1) / 1e3 / K2,
-                "unit": "s", "steps": K2, "warmup": 3, "status": g2["status"], "outer": g2["outer"],
-                "inner": g2["inner"], "obj": g2["obj"], "rel_p": g2["rel_p"], "rel_d": g2["rel_d"], "mu": g2["mu"],
-                "t_sketch_ms": g2["t_sketch_ms"], "t_pcg_ms": g2["t_pcg_ms"], "t_other_ms": g2["t_other_ms"]}
-            del w2, r2
-            torch.cuda.empty_cache()
 
     # ---- e2e: the same solve through the C ABI with host buffers --------------------------------
     e2e = None

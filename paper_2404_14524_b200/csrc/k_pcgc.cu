@@ -199,31 +199,59 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
   };
 
   // ---- the CTA's own rows: (init) x = 0, r = rhs | x += alpha p_k, r -= alpha w; rr, U^T r row -------
-  auto rows_phase = [&](bool init, double alpha, const double* pk) {
+  // alpha = rz / p^T N p is formed by warp 0 from the pwp partials while the row operands (p, e, x, r
+  // and the cluster partial rows of w) are in flight; returns false on a p^T N p breakdown (uniform)
+  auto rows_phase = [&](bool init, const double* pk) -> bool {
     double rr = 0.0;
+    double alpha = 0.0;
     for (int c = tid; c < ell; c += PC_T) gpart[c] = 0.0;
-    for (int64_t i0 = v_lo; i0 < v_hi; i0 += PC_T) {
+    for (int64_t i0 = v_lo; i0 < v_hi || (!init && i0 == v_lo); i0 += PC_T) {
       const int64_t i = i0 + tid;
-      double ri = 0.0;
-      if (i < v_hi) {
+      const bool own = i < v_hi;
+      double ri = 0.0, pi = 0.0, wi = 0.0, xi = 0.0;
+      if (own) {
         if (init) {
           ri = P.rhs[i];
+        } else {
+          pi = __ldcg(pk + i);
+          xi = P.x[i];
+          ri = P.r[i];
+          const double ei = P.e ? P.e[i] : 0.0;
+          double acc = 0.0;
+          for (uint32_t k0 = 0; k0 < ncl; k0 += 24) {   // the cluster partial rows, in cluster order
+            double v[24];
+#pragma unroll
+            for (int u = 0; u < 24; ++u) v[u] = (k0 + u < ncl) ? __ldcg(P.Wp + (size_t)(k0 + u) * P.wp_ld + i) : 0.0;
+#pragma unroll
+            for (int w = 16; w > 0; w >>= 1)
+#pragma unroll
+              for (int u = 0; u < w; ++u)
+                if (u + w < 24) v[u] += v[u + w];
+            acc += v[0];
+          }
+          wi = acc + (delta + ei) * pi;
+        }
+      }
+      if (!init && i0 == v_lo) {
+        if (warp == 0) {
+          const double pw = warp_sum_array(P.pwp, (int)G);
+          if (lane == 0) s_scal[2] = pw;
+        }
+        named_bar_sync(9, PC_T);
+        const double pw = s_scal[2];
+        if (!(pw > 0.0) || !isfinite(pw)) return false;
+        alpha = rz / pw;
+      }
+      if (own) {
+        if (init) {
           P.x[i] = 0.0;
         } else {
-          const double pi = __ldcg(pk + i);
-          double acc = 0.0;
-          for (uint32_t k0 = 0; k0 < ncl; k0 += 8) {   // the cluster partial rows, in cluster order
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = (k0 + u < ncl) ? __ldcg(P.Wp + (size_t)(k0 + u) * P.wp_ld + i) : 0.0;
-            acc += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
-          }
-          const double wi = acc + (delta + (P.e ? P.e[i] : 0.0)) * pi;
-          P.x[i] = fma(alpha, pi, P.x[i]);
-          ri = fma(-alpha, wi, P.r[i]);
+          P.x[i] = fma(alpha, pi, xi);
+          ri = fma(-alpha, wi, ri);
         }
         P.r[i] = ri;
       }
+      if (i0 >= v_hi) break;   // (a CTA without rows only formed alpha)
       rr = fma(ri, ri, rr);
       rsh[tid] = ri;
       named_bar_sync(9, PC_T);
@@ -267,6 +295,7 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
       row[0] = b;
     }
     for (int c = tid; c < ell; c += PC_T) row[1 + c] = gpart[c];
+    return true;
   };
 
   // ---- grid barrier, then every CTA sums the G partial rows itself in one fixed order ----------------
@@ -350,7 +379,7 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
   };
 
   // initialisation (k = -1): x = 0, r = rhs, p_0 = z_0 -> P1
-  rows_phase(true, 0.0, nullptr);
+  rows_phase(true, nullptr);
   reduce_rows();
   bool stop = converged(true);
   if (!stop) {
@@ -455,15 +484,7 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
     pcgc_grid_barrier(P.bar, G, bar_epoch);
     stamp(2);
     // ---- P2: alpha, own rows, partial rows -------------------------------------------------------
-    if (warp == 0) {
-      const double pw = warp_sum_array(P.pwp, (int)G);
-      if (lane == 0) s_scal[2] = pw;
-    }
-    named_bar_sync(9, PC_T);
-    const double pw = s_scal[2];
-    if (!(pw > 0.0) || !isfinite(pw)) { status = NYS_EBREAKDOWN; break; }
-    const double alpha = rz / pw;
-    rows_phase(false, alpha, pk);
+    if (!rows_phase(false, pk)) { status = NYS_EBREAKDOWN; break; }
     stamp(3);
     // ---- P3: reduction, stop test, p_{k+1} -------------------------------------------------------
     reduce_rows();
