@@ -226,9 +226,12 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
   bool conv = false;
 
   // ---- init: x = 0, r = rhs, rr, U^T r  ------------------------------------------------------
-  auto rows_phase_rr_ut = [&](bool init, double alpha, const double* pnew, const double* Wp, double delta) {
-    // own rows in chunks of 16: (init) x = 0, r = rhs | x += alpha p, r -= alpha w ; partials
+  auto rows_phase_rr_ut = [&](bool init, double alpha, const double* pnew, const double* Wp, double delta) -> bool {
+    // own rows in chunks of 16: (init) x = 0, r = rhs | x += alpha p, r -= alpha w ; partials.
+    // (!init) alpha = rz / p^T N p is formed here by warp 0 from the pwp partials while the first
+    // chunk's row operands and partial-row sums are in flight; false on a p^T N p breakdown (no update)
     double rr = 0.0;
+    bool first = true;
     double gacc[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) gacc[k] = 0.0;
@@ -270,7 +273,17 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
         }
         chunk_red[row16][grp16] = acc;
       }
+      if (!init && first && warp == 0) {
+        const double pw = warp_sum_array(P.pwp, G);
+        if (lane == 0) s_scal[2] = pw;
+      }
       named_bar_sync(9, T);
+      if (!init && first) {
+        first = false;
+        const double pw = s_scal[2];
+        if (!(pw > 0.0) || !isfinite(pw)) return false;
+        alpha = rz / pw;
+      }
       if (tid < 16) {
         double ri = 0.0;
         if (i < r_hi) {
@@ -306,6 +319,15 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       }
       named_bar_sync(9, T);
     }
+    if (!init && first) {   // a CTA without rows takes the same breakdown decision
+      if (warp == 0) {
+        const double pw = warp_sum_array(P.pwp, G);
+        if (lane == 0) s_scal[2] = pw;
+      }
+      named_bar_sync(9, T);
+      const double pw = s_scal[2];
+      if (!(pw > 0.0) || !isfinite(pw)) return false;
+    }
     // write partials: rr (threads < 16 hold pieces) and U^T r (half-warps)
     double rrw = warp_sum(rr);
     if (tid == 0) P.part1[(size_t)cid * (1 + ell)] = rrw;
@@ -323,6 +345,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
         }
       }
     }
+    return true;
   };
 
   // P3: converged? then h = s o (U^T r), r^T z = r^T r + (U^T r)^T h (no extra reduction), beta, and
@@ -649,17 +672,12 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     arrive_stamp(0);
     pcg_grid_barrier(P.bar, G, T, bar_epoch);
     stamp(2);
-    // ---- P2: alpha, own-row updates, partials --------------------------------------------------
-    if (warp == 0) {
-      const double pw = warp_sum_array(P.pwp, G);
-      if (lane == 0) s_scal[2] = pw;
-    }
-    named_bar_sync(9, T);
-    const double pw = s_scal[2];
-    if (!(pw > 0.0) || !isfinite(pw)) { status = NYS_EBREAKDOWN; break; }
-    alpha = rz / pw;
     }  // !init
-    rows_phase_rr_ut(init, alpha, init ? nullptr : pnew, init ? nullptr : P.Wp, delta);
+    // ---- P2: alpha, own-row updates, partials --------------------------------------------------
+    if (!rows_phase_rr_ut(init, alpha, init ? nullptr : pnew, init ? nullptr : P.Wp, delta)) {
+      status = NYS_EBREAKDOWN;
+      break;
+    }
     if (!init) {
       stamp(3);
       stamp(4);

@@ -121,7 +121,9 @@ def test_trajectory_first_three_outer_iterations(ctx, cfg, kw, ell_override):
 
 # ------------------------------------------------------------------ graph-path PCG (m > 8192; forced at small m)
 GRAPH_PCG = [(8193, 300, 30, False), (8193, 300, 0, False), (20000, 200, 40, False), (20000, 200, 40, True),
-             (50000, 120, 100, False), (50000, 120, 100, True), (50000, 120, 0, True)]
+             (50000, 120, 100, False), (50000, 120, 100, True), (50000, 120, 0, True),
+             # fewer columns than clusters (idle clusters), the largest rank, the largest m (16-CTA clusters)
+             (30001, 10, 16, True), (20000, 300, 256, False), (138240, 24, 8, True)]
 
 
 @pytest.mark.parametrize("path", ["cluster", "graph"])
