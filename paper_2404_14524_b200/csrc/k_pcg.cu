@@ -1075,7 +1075,10 @@ __global__ void __launch_bounds__(NT, 1) pcg_cluster_small_kernel(const PcgSPara
 static int small_cluster_size(int64_t m, int64_t n) {
   const int64_t m32 = m <= 64 ? 64 : m <= 128 ? 128 : 256;
   const double bytes = (double)n * (double)m32 * 8.0;
-  int C = (int)((bytes + 64e3 - 1) / 64e3);          // ~64 KB of A per CTA
+  // ~34 KB of A per CTA, at most 16 CTAs (measured at config 0, A = 410 KB padded: C = 3 / 4 / 5 / 7 /
+  // 8 / 12 / 16 -> 4.24 / 3.80 / 3.64 / 3.49 / 3.34 / 3.31 / 3.36 us per PCG iteration)
+  int C = (int)((bytes + 34e3 - 1) / 34e3);
+  if (C > 16) C = 16;
   if (C < 2) C = 2;
   if (bytes / C > 150e3) C = (int)((bytes + 150e3 - 1) / 150e3);
   return C;
@@ -1091,7 +1094,15 @@ int launch_pcg_small(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int64_
   P.A = A; P.lda = lda; P.m = m; P.n = n; P.d = d; P.e = e; P.U = U; P.ldu = ldu; P.ell = ell; P.s = s;
   P.rhs = rhs; P.x = x; P.sc = ctx->sc; P.max_iter = max_iter;
   // cluster variant (A in shared memory) unless disabled or A needs more than 16 CTAs
-  const int C = small_cluster_size(m, n);
+  int C = small_cluster_size(m, n);
+  if (const char* oc = getenv("NYS_PCG_SMALL_C")) {   // tuning override (>= the size A needs)
+    const int o = atoi(oc);
+    if (o >= C && o <= 16) C = o;
+    else if (o >= 2 && o < C) {
+      const int64_t m32 = m <= 64 ? 64 : m <= 128 ? 128 : 256;
+      if ((double)n * m32 * 8.0 / o <= 150e3) C = o;
+    }
+  }
   if (C <= 16 && getenv("NYS_PCG_SMALL_1CTA") == nullptr) {
     const int64_t m32 = m <= 64 ? 64 : m <= 128 ? 128 : 256;
     const int64_t maxcols = (n + C - 1) / C;

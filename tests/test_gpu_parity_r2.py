@@ -122,8 +122,10 @@ def test_trajectory_first_three_outer_iterations(ctx, cfg, kw, ell_override):
 # ------------------------------------------------------------------ graph-path PCG (m > 8192; forced at small m)
 GRAPH_PCG = [(8193, 300, 30, False), (8193, 300, 0, False), (20000, 200, 40, False), (20000, 200, 40, True),
              (50000, 120, 100, False), (50000, 120, 100, True), (50000, 120, 0, True),
-             # fewer columns than clusters (idle clusters), the largest rank, the largest m (16-CTA clusters)
-             (30001, 10, 16, True), (20000, 300, 256, False), (138240, 24, 8, True)]
+             # 4-CTA clusters with an odd last slice, the largest rank, the largest m (16-CTA clusters).  (n = 10,
+             # ell = 16 was tried: PCG does not converge there and both paths drift from the oracle by rounding
+             # amplification — 1e-10 / 1e-13 after 8 iterations, 2e-6 / 5e-8 after 15: tools/pcg_edge_probe.py)
+             (30001, 40, 16, True), (20000, 300, 256, False), (138240, 24, 8, True)]
 
 
 @pytest.mark.parametrize("path", ["cluster", "graph"])
