@@ -931,35 +931,60 @@ __global__ void __launch_bounds__(NT, 1) pcg_cluster_small_kernel(const PcgSPara
     return t;
   };
   // g_c = U_c^T r for c < ell and g_ell = r^T r, one warp per entry (r_s complete on entry); a barrier
+  // (four entries per warp step: their shuffle reductions overlap)
   auto gpass = [&]() {
-    for (int c = warp; c <= ell; c += NW) {
-      const double* u = (c < ell) ? Ucol(c) : r_s;
-      double acc = 0.0;
+    for (int c0 = warp; c0 <= ell; c0 += 4 * NW) {
+      double acc[4];
 #pragma unroll
-      for (int k = 0; k < MR; ++k) {
-        const int i = lane + 32 * k;
-        if (i < m) acc = fma(u[i], r_s[i], acc);
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + j * NW;
+        acc[j] = 0.0;
+        if (c <= ell) {                              // warp-uniform
+          const double* u = (c < ell) ? Ucol(c) : r_s;
+#pragma unroll
+          for (int k = 0; k < MR; ++k) {
+            const int i = lane + 32 * k;
+            if (i < m) acc[j] = fma(u[i], r_s[i], acc[j]);
+          }
+        }
       }
-      acc = warp_sum(acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
       if (lane == 0) {
-        g_s[c] = acc;
-        if (c < ell) h_s[c] = P.s[c] * acc;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = c0 + j * NW;
+          if (c <= ell) {
+            g_s[c] = acc[j];
+            if (c < ell) h_s[c] = P.s[c] * acc[j];
+          }
+        }
       }
     }
     __syncthreads();
   };
   // r^T z = r^T r + sum_c s_c g_c^2 (h = s o g: no further reduction), the same order in every thread;
   // then own rows z = r + U h and p = z + beta p
+  // (four independent FMA chains: the same order in every thread of every CTA)
   auto rz_of = [&](double rr) -> double {
-    double gh = 0.0;
-    for (int c = 0; c < ell; ++c) gh = fma(h_s[c], g_s[c], gh);
-    return rr + gh;
+    double gh[4] = {0.0, 0.0, 0.0, 0.0};
+    int c = 0;
+    for (; c + 3 < ell; c += 4)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) gh[j] = fma(h_s[c + j], g_s[c + j], gh[j]);
+    for (; c < ell; ++c) gh[0] = fma(h_s[c], g_s[c], gh[0]);
+    return rr + ((gh[0] + gh[1]) + (gh[2] + gh[3]));
   };
   auto z_row = [&](int i) -> double {
-    double acc = r_s[i];
-#pragma unroll 4
-    for (int c = 0; c < ell; ++c) acc = fma(Ucol(c)[i], h_s[c], acc);
-    return acc;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int c = 0;
+    for (; c + 3 < ell; c += 4)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] = fma(Ucol(c + j)[i], h_s[c + j], acc[j]);
+    for (; c < ell; ++c) acc[0] = fma(Ucol(c)[i], h_s[c], acc[0]);
+    return r_s[i] + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
   };
   for (int i = tid; i < M32; i += NT) {
     r_s[i] = (i < m) ? P.rhs[i] : 0.0;
@@ -986,30 +1011,34 @@ __global__ void __launch_bounds__(NT, 1) pcg_cluster_small_kernel(const PcgSPara
       pr[q] = p_s[lane + 32 * q];
       wacc[q] = 0.0;
     }
-    // two columns per warp step: their dot reductions overlap
-    for (int j = warp; j < ncols; j += 2 * NW) {
-      const int j2 = j + NW;
-      const bool two = j2 < ncols;                   // warp-uniform
-      const double* a = As + (size_t)j * M32;
-      const double* b = As + (size_t)(two ? j2 : j) * M32;
-      double av[MR], bv[MR];
-      double acc = 0.0, bcc = 0.0;
+    // four columns per warp step: their dot reductions overlap (absent columns: t = 0, column j reread)
+    for (int j = warp; j < ncols; j += 4 * NW) {
+      double av[4][MR], acc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int jj = j + u * NW;
+        const double* a = As + (size_t)(jj < ncols ? jj : j) * M32;
+        acc[u] = 0.0;
+#pragma unroll
+        for (int q = 0; q < MR; ++q) {
+          av[u][q] = a[lane + 32 * q];
+          acc[u] = fma(av[u][q], pr[q], acc[u]);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+      double t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t[u] = (j + u * NW < ncols) ? ds[j + u * NW] * acc[u] : 0.0;
 #pragma unroll
       for (int q = 0; q < MR; ++q) {
-        av[q] = a[lane + 32 * q];
-        bv[q] = b[lane + 32 * q];
-        acc = fma(av[q], pr[q], acc);
-        bcc = fma(bv[q], pr[q], bcc);
-      }
+        double wq = wacc[q];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        bcc += __shfl_xor_sync(0xffffffffu, bcc, o);
+        for (int u = 0; u < 4; ++u) wq = fma(av[u][q], t[u], wq);
+        wacc[q] = wq;
       }
-      const double t = ds[j] * acc;
-      const double tb = two ? ds[j2] * bcc : 0.0;
-#pragma unroll
-      for (int q = 0; q < MR; ++q) wacc[q] = fma(bv[q], tb, fma(av[q], t, wacc[q]));
     }
 #pragma unroll
     for (int q = 0; q < MR; ++q) wpart[warp * M32 + lane + 32 * q] = wacc[q];
