@@ -48,7 +48,10 @@ READ_STREAM_GBS = 6863.0
 DMMA_PEAK_TFLOPS = 37.1
 # persistent PCG kernel, dram__bytes_read.sum + dram__bytes_write.sum per ITERATION (ncu --set full of
 # a 20-iteration launch, config 1: 2.535 GB + 20.9 MB; profiles/r01_pcg_persistent_cfg1_20it_full.ncu-rep)
-PCG_TRAFFIC_PER_IT = {1: 85.6e6}   # ncu --set full, profiles/r01_pcg_persistent_cfg1_20it_final_full.ncu-rep
+# measured DRAM bytes (read + write) per PCG iteration of the persistent kernels: config 1
+# profiles/r01_pcg_persistent_cfg1_20it_final_full.ncu-rep; config-4 slice (key (4, columns per GPU))
+# profiles/r02_ncu_pcg_cluster_cfg4_summary.txt (8 iterations: 160.20 GB read + 69.9 MB written)
+PCG_TRAFFIC_PER_IT = {1: 85.6e6, (4, 50000): 20.034e9}
 
 
 def _peaks():
@@ -492,11 +495,13 @@ def main():
     hbm = peaks.get("hbm_gbs", 6650.0)
     peak_src = "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
 
-    # ---- persistent PCG kernel (single GPU, m <= 8192): ONE launch per PCG solve, the dominant
-    # kernel of the step there.  Timed live: nys_pcg_solve with tol = 0 runs exactly PCG_IT
-    # iterations (one persistent launch + O(1) setup/true-residual work, < 0.5 % of the call).
+    # ---- persistent PCG kernel (single GPU): ONE launch per PCG solve, the dominant kernel of the step
+    # (m <= 8192: pcg_persistent_kernel; m > 8192: pcg_cluster_kernel, k_pcgc.cu).  Timed live:
+    # nys_pcg_solve with tol = 0 runs exactly I iterations; two calls (I1 < I2 iterations) are differenced,
+    # so the call's setup kernels and its true-residual matvec cancel and t_it is the kernel's own time
+    # per iteration (the launch's one-off pipeline fill, ~10 us, is spread over I2 - I1 iterations)
     pcg_roof = None
-    if world == 1 and m <= 8192 and wl.structure == 0 and wl.ell > 0:
+    if world == 1 and m <= 16 * 8640 and wl.structure == 0 and 0 < wl.ell <= 256:
         ell = wl.ell
         mp = m + (m % 2)
         Om = torch.empty((ell, mp), dtype=torch.float64, device=device)
@@ -504,44 +509,59 @@ def main():
         lam = torch.empty(ell, dtype=torch.float64, device=device)
         rhs = dv(rs.standard_normal(m))
         xs = torch.zeros(m, dtype=torch.float64, device=device)
-        PCG_IT = 400
+        I2 = 400 if small else max(20, min(400, int(8e11 / wl.a_bytes())))
         with torch.cuda.stream(stream):
             ctx.nys_gaussian(m, ell, 0, 1, Om)
             ctx.nys_sketch(wl.At, lda, m, d, None, 1e-2, ell, Om, U, lam)
-            ctx.nys_pcg_solve(wl.At, lda, m, d, None, 1e-2, ell, U, lam, 1e-2, rhs, xs, 0.0, 20)
+            ctx.nys_pcg_solve(wl.At, lda, m, d, None, 1e-2, ell, U, lam, 1e-2, rhs, xs, 0.0, 4)
         barrier()
         from paper_2404_14524_b200 import NysError
-        while True:
-            # at small m, PCG_IT iterations run far past convergence; once r reaches the rounding
-            # floor p^T N p can lose its sign (EBREAKDOWN): time fewer iterations then
+
+        def pcg_call(iters):
             a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            xs.zero_()
+            barrier()
             a_.record(stream)
-            try:
-                with torch.cuda.stream(stream):
-                    info = ctx.nys_pcg_solve(wl.At, lda, m, d, None, 1e-2, ell, U, lam, 1e-2, rhs, xs, 0.0, PCG_IT)
-            except NysError:
-                if PCG_IT <= 25:
-                    raise
-                PCG_IT //= 2
-                xs.zero_()
-                continue
+            with torch.cuda.stream(stream):
+                inf = ctx.nys_pcg_solve(wl.At, lda, m, d, None, 1e-2, ell, U, lam, 1e-2, rhs, xs, 0.0, iters)
             b_.record(stream)
+            barrier()
+            return inf, a_.elapsed_time(b_) / 1e3
+
+        while True:
+            # at small m, I2 iterations run far past convergence; once r reaches the rounding floor
+            # p^T N p can lose its sign (EBREAKDOWN): time fewer iterations then
+            try:
+                I1 = max(2, I2 // 4)
+                info1, t1 = pcg_call(I1)
+                info, t2 = pcg_call(I2)
+            except NysError:
+                if I2 <= 25:
+                    raise
+                I2 //= 2
+                continue
             break
-        barrier()
-        t_call = a_.elapsed_time(b_) / 1e3
+        t_it = (t2 - t1) / (info.iters - info1.iters)
+        t_call = t2
         # SURVEY §8(d) per CG iteration: one K1 + 16 m l bytes of U (U^T r and U h) + ~10 m-vectors
         it_bytes = mv_bytes + 16.0 * m * ell + 80.0 * m
-        pcg_gbs = info.iters * it_bytes / t_call / 1e9
-        tr = (PCG_TRAFFIC_PER_IT[args.config] * info.iters) if args.config in PCG_TRAFFIC_PER_IT else None
+        pcg_gbs = it_bytes / t_it / 1e9
+        key = (args.config, wl.ncols) if args.config == 4 else args.config
+        tr_it = PCG_TRAFFIC_PER_IT.get(key)
         pcg_roof = {"bound": "hbm", "achieved": pcg_gbs, "peak": hbm, "unit": "GB/s", "frac": pcg_gbs / hbm,
-                    "traffic": tr,
-                    # A (128 MB at config 1) is about the L2 size: part of it survives in L2 between
+                    # measured DRAM bytes (ncu) per iteration x the iterations of one launch
+                    "traffic": tr_it * info.iters if tr_it else None,
+                    # at config 1 A (128 MB) is about the L2 size: part of it survives in L2 between
                     # iterations, so DRAM traffic < algorithmic bytes; frac above is the effective
                     # ALGORITHMIC bandwidth, dram_frac the measured-DRAM-bytes one
-                    "dram_frac": (tr / t_call / 1e9 / hbm) if tr else None,
-                    "kernel": "pcg_persistent_kernel (whole PCG solve in one cooperative launch)",
+                    "dram_frac": (tr_it / t_it / 1e9 / hbm) if tr_it else None,
+                    "kernel": ("pcg_persistent_kernel" if m <= 8192 else "pcg_cluster_kernel (k_pcgc.cu)")
+                              + ": the whole PCG solve in one cooperative launch",
                     "peak_source": peak_src, "iterations_per_launch": info.iters,
-                    "bytes_per_iteration": it_bytes, "launch_us": t_call * 1e6, "us_per_iteration": t_call / info.iters * 1e6,
+                    "bytes_per_iteration": it_bytes, "bytes_per_launch": info.iters * it_bytes,
+                    "launch_us": t_call * 1e6, "us_per_iteration": t_it * 1e6,
+                    "timing": f"two launches of {info1.iters} and {info.iters} iterations differenced (setup and "
+                              "the call's true-residual matvec cancel)",
                     "share_of_step": (last["t_pcg_ms"] / 1e3) / sec_per_solve}
 
     # ---- sketch GEMMs (K2 + K3, fp64 DMMA): Y = A (d o (A^T Omega)), 4 m n l flops per call (SURVEY
@@ -649,12 +669,15 @@ def main():
 
     mv_roof = {"bound": "hbm", "achieved": mv_gbs, "peak": hbm, "unit": "GB/s", "frac": mv_gbs / hbm,
                "traffic": TRAFFIC.get(args.config) if (args.config != 4 or (wl.ncols == 50000 and world == 1)) else None,
-               "kernel": "fused normal matvec K1 (matvec_kernel + mv_finalize), graph-captured",
+               "kernel": "fused normal matvec K1 standalone (matvec_kernel + mv_finalize, nys_normal_matvec, "
+                         "graph-captured): the streaming pipeline of the PCG kernels' matvec phase and of the "
+                         "T / N / BOTH passes",
                "peak_source": peak_src, "bytes_per_launch": mv_bytes, "launch_us": mv_s * 1e6,
                "warm_l2_gbs": mv_bytes / mv_warm_s / 1e9,
                "frac_of_read_stream": mv_gbs / READ_STREAM_GBS,
                "pcg_effective_gbs": (last["inner"] * mv_bytes / (last["t_pcg_ms"] / 1e3) / 1e9) if last["t_pcg_ms"] > 0 else None,
-               "share_of_step": matvecs_per_solve * mv_s / sec_per_solve}
+               # the step's PCG matvecs run inside the persistent PCG kernel (roofline above) when it exists
+               "share_of_step": None if pcg_roof is not None else matvecs_per_solve * mv_s / sec_per_solve}
     if rank == 0:
         line = {
             "metric": METRIC, "value": sec_per_solve, "unit": "s", "n_gpus": world, "steps": args.steps,

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <string>
 
 #include "k_vec.cuh"
 
@@ -623,7 +624,9 @@ int launch_pcg_cluster(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int6
   at[1].id = cudaLaunchAttributeCooperative;
   at[1].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  // NYS_PCG_NOCOOP=1: a plain cluster launch of the same grid (Nsight Compute cannot launch cooperative
+  // cluster kernels; it serialises kernels, so the occupancy-sized grid is co-resident there)
+  cfg.numAttrs = getenv("NYS_PCG_NOCOOP") ? 1 : 2;
   if (getenv("NYS_DEBUG"))
     fprintf(stderr, "[nys] cluster PCG m=%lld n=%lld ell=%d: cl=%d clusters=%lld G=%d rs=%lld rpc=%lld stages=%d smem=%zu\n",
             (long long)m, (long long)n, ell, pl.cl, (long long)ncl, G, (long long)P.rs, (long long)P.rpc, pl.stages,
@@ -633,7 +636,24 @@ int launch_pcg_cluster(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int6
     P.trace = (unsigned long long*)ctx->ws("pc_trace", 2 * 16 * 8 * 8);
     NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.trace, 0, 2 * 16 * 8 * 8, ctx->stream));
   }
-  NYS_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k, P));
+  // if fewer clusters can be co-resident than the occupancy query promised (a profiler's reserved
+  // resources, another context on the GPU), the cooperative launch is refused: retry with fewer clusters
+  // (the vector-phase row ranges follow G; every workspace above is sized for the largest grid)
+  for (;;) {
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, k, P);
+    if (le == cudaSuccess) break;
+    if ((le == cudaErrorCooperativeLaunchTooLarge || le == cudaErrorInvalidConfiguration ||
+         le == cudaErrorLaunchOutOfResources) && ncl > 1) {
+      cudaGetLastError();
+      --ncl;
+      const int Gr = (int)(ncl * pl.cl);
+      cfg.gridDim = dim3((unsigned)Gr);
+      P.rpc = (m + Gr - 1) / Gr;
+      continue;
+    }
+    ctx->set_error(std::string("pcg_cluster launch: ") + cudaGetErrorString(le));
+    return NYS_ECUDA;
+  }
   ctx->launches++;
   if (trace) {
     unsigned long long h[2 * 16 * 8];
