@@ -587,6 +587,13 @@ __global__ void gemm_k0_kernel(int64_t M, int64_t N, double* C, int64_t ldc, con
   }
 }
 
+// tuning override of the split-K count (per operand layout: K-major A, i.e. T = A^T Omega, or M-major
+// A, i.e. Y = A T): NYS_GEMM_SPLITS_K / NYS_GEMM_SPLITS_M, read per call
+static int split_override(const GemmCall& g) {
+  const char* e = getenv(g.a_kmajor ? "NYS_GEMM_SPLITS_K" : "NYS_GEMM_SPLITS_M");
+  return e ? atoi(e) : 0;
+}
+
 int launch_gemm(nys_ctx* ctx, const GemmCall& g) {
   if (g.M <= 0 || g.N <= 0) return NYS_OK;
   if (g.K <= 0) {
@@ -596,9 +603,11 @@ int launch_gemm(nys_ctx* ctx, const GemmCall& g) {
     ctx->launches++;
     return ctx->check_launch("gemm_k0");
   }
-  // the 128-row kernel pays off on tall products (the sketch at large n or m); short-M products
-  // (split-K Gram / Y = A T at small m) keep the 64 x 64 kernel (measured on B200)
-  int64_t min_m = 16384, min_k = 4096;   // tuning overrides: NYS_GEMM_NT_MIN="M,K"
+  // the 128-row kernel pays off on the sketch products once both M and K reach ~1000 (measured on
+  // B200, tools/gemm_sweep.py: config-1 sketch 196 -> 165-177 us, config-2 shape 955 -> 892-912 us,
+  // 20000 x 5000 x 300 4280 -> 3989-4002 us); short products (the Gram and small factorisation GEMMs,
+  // config 3's K = 64 / M = 64 sketch) keep the 64 x 64 kernel.  Tuning override NYS_GEMM_NT_MIN="M,K".
+  int64_t min_m = 512, min_k = 1024;
   if (const char* e = getenv("NYS_GEMM_NT_MIN")) {
     long long a = 0, b = 0;
     if (sscanf(e, "%lld,%lld", &a, &b) == 2) { min_m = a; min_k = b; }
@@ -610,7 +619,9 @@ int launch_gemm(nys_ctx* ctx, const GemmCall& g) {
   // fallback for operands the tensor unit cannot address (odd leading dimensions, misalignment) and
   // as an A/B switch (NYS_GEMM_CPASYNC)
   CUtensorMap mapA{}, mapB{};
-  bool tma = getenv("NYS_GEMM_CPASYNC") == nullptr && (g.lda % 2) == 0 && (g.ldb % 2) == 0 &&
+  // the TMA kernel from M K >= 2.5e7 (config-1 sketch, M K = 1.6e7: the cp.async kernel, 165 vs 173 us)
+  bool tma = getenv("NYS_GEMM_CPASYNC") == nullptr && (double)g.M * (double)g.K >= 2.5e7 &&
+             (g.lda % 2) == 0 && (g.ldb % 2) == 0 &&
              aligned16(g.A) && aligned16(g.B) && g.K < (int64_t(1) << 31) && g.M < (int64_t(1) << 31);
   if (tma) {
     if (g.a_kmajor) tma = make_map(&mapA, g.A, g.K, g.M, g.lda, HBM_);
@@ -623,31 +634,34 @@ int launch_gemm(nys_ctx* ctx, const GemmCall& g) {
   NYS_TRY(ensure_max_smem(ctx, tma ? (const void*)kt : (const void*)k, smem));
   const int64_t mt = (g.M + HBM_ - 1) / HBM_, nt = (g.N + BN - 1) / BN;
   const int64_t kslabs = (g.K + HBK - 1) / HBK;
-  int splits = g.splits;
+  int splits = g.splits > 0 ? g.splits : split_override(g);
   if (splits <= 0) {
-    const int64_t target = 2LL * ctx->num_sms;
-    int64_t sp = (target + mt * nt - 1) / (mt * nt);
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tma ? (const void*)kt : (const void*)k, tma ? 160 : 128,
+                                                      smem) != cudaSuccess) { cudaGetLastError(); occ = 0; }
+    const int64_t slots = (int64_t)(occ > 0 ? occ : 2) * ctx->num_sms, tiles = mt * nt;
     const int64_t smax = kslabs / 8 > 0 ? kslabs / 8 : 1;
-    if (sp > smax) sp = smax;
-    if (sp < 1) sp = 1;
-    if (sp > 256) sp = 256;
-    if (sp == 1 && !getenv("NYS_GEMM_NO_WAVE_SPLIT")) {
+    int64_t sp = 1;
+    if (tiles < slots) {
+      // few tiles: split K so that tiles x S fits ONE wave of the resident slots (a split that spills a
+      // few CTAs into a second wave nearly doubles the time: config-1 Y = A T, 16 tiles, S = 19 on 296
+      // slots: 0.194 ms for the sketch pair, S = 18: 0.165), at most 16 (the S M N partials and their
+      // reduce grow with S: config-2 shape T = A^T Omega, 16 tiles: S = 27 0.924 ms, 16 0.871, 8 0.886)
+      sp = slots / tiles;
+      if (sp > smax) sp = smax;
+      if (sp > 16) sp = 16;
+      if (sp < 1) sp = 1;
+    } else if (!getenv("NYS_GEMM_NO_WAVE_SPLIT")) {
       // many tiles: split K only to fill the last wave.  Time ~ ceil(tiles * S / slots) / S (equal
-      // tiles, slots = resident CTAs); the smallest S (<= 4, >= 64 K-slabs per split) within 1 % of the
-      // best, if that gains >= 3 % over S = 1.  Measured on B200, the config-4 sketch (1955 tiles, 444 slots, 4.4 waves): the
+      // tiles); the smallest S (<= 4, >= 64 K-slabs per split) within 1 % of the best, if that gains
+      // >= 3 % over S = 1.  Measured on B200, the config-4 sketch (1955 tiles, 444 slots, 4.4 waves): the
       // unsplit GEMM ran 0.84 of the DMMA peak with the SM pipes 84 % busy — the last wave's idle SMs
-      int occ = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tma ? (const void*)kt : (const void*)k, tma ? 160 : 128,
-                                                        smem) != cudaSuccess) { cudaGetLastError(); occ = 0; }
-      const int64_t slots = (int64_t)occ * ctx->num_sms, tiles = mt * nt;
-      if (slots > 0) {
-        auto cost = [&](int64_t S) { return (double)((tiles * S + slots - 1) / slots) / (double)S; };
-        double best = cost(1);
-        for (int64_t S = 2; S <= 4 && kslabs / S >= 64; ++S) best = std::min(best, cost(S));
-        if (cost(1) > best * 1.03)   // a split costs partials (S M N doubles) and a reduce: only for >= 3 %
-          for (int64_t S = 2; S <= 4 && kslabs / S >= 64; ++S)
-            if (cost(S) <= best * 1.01) { sp = S; break; }
-      }
+      auto cost = [&](int64_t S) { return (double)((tiles * S + slots - 1) / slots) / (double)S; };
+      double best = cost(1);
+      for (int64_t S = 2; S <= 4 && kslabs / S >= 64; ++S) best = std::min(best, cost(S));
+      if (cost(1) > best * 1.03)   // a split costs partials (S M N doubles) and a reduce: only for >= 3 %
+        for (int64_t S = 2; S <= 4 && kslabs / S >= 64; ++S)
+          if (cost(S) <= best * 1.01) { sp = S; break; }
     }
     splits = (int)sp;
   }
@@ -690,7 +704,7 @@ static int launch_gemm_old(nys_ctx* ctx, const GemmCall& g) {
   else NYS_TRY(ensure_max_smem(ctx, (const void*)dgemm_kernel<false>, smem));
   const int64_t mt = (g.M + GBM - 1) / GBM, nt = (g.N + GBN - 1) / GBN;
   const int64_t kslabs = (g.K + GBK - 1) / GBK;
-  int splits = g.splits;
+  int splits = g.splits > 0 ? g.splits : split_override(g);
   if (splits <= 0) {
     const int64_t target = 3LL * ctx->num_sms;
     int64_t s = (target + mt * nt - 1) / (mt * nt);
