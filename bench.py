@@ -541,7 +541,13 @@ def main():
                 I2 //= 2
                 continue
             break
-        t_it = (t2 - t1) / (info.iters - info1.iters)
+        if info.iters - info1.iters >= 2:
+            t_it = (t2 - t1) / (info.iters - info1.iters)
+            timing = (f"two launches of {info1.iters} and {info.iters} iterations differenced (setup and the "
+                      "call's true-residual matvec cancel)")
+        else:   # the solve reaches the rounding floor (r = 0) within I1 iterations (config 3: l = m)
+            t_it = t2 / max(1, info.iters)
+            timing = f"one launch of {info.iters} iterations (the call's setup and true-residual matvec included)"
         t_call = t2
         # SURVEY §8(d) per CG iteration: one K1 + 16 m l bytes of U (U^T r and U h) + ~10 m-vectors
         it_bytes = mv_bytes + 16.0 * m * ell + 80.0 * m
@@ -560,8 +566,7 @@ def main():
                     "peak_source": peak_src, "iterations_per_launch": info.iters,
                     "bytes_per_iteration": it_bytes, "bytes_per_launch": info.iters * it_bytes,
                     "launch_us": t_call * 1e6, "us_per_iteration": t_it * 1e6,
-                    "timing": f"two launches of {info1.iters} and {info.iters} iterations differenced (setup and "
-                              "the call's true-residual matvec cancel)",
+                    "timing": timing,
                     "share_of_step": (last["t_pcg_ms"] / 1e3) / sec_per_solve}
 
     # ---- sketch GEMMs (K2 + K3, fp64 DMMA): Y = A (d o (A^T Omega)), 4 m n l flops per call (SURVEY
