@@ -401,13 +401,20 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
     stamp(0);
     // ---- P1: p_k slice; fused matvec over this cluster's panels (lag-1 dot exchange) --------------
     double vreg[RPT], wacc[RPT];
+    double pwacc = 0.0;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int64_t rl = tid + (int64_t)PC_T * i;
       vreg[i] = (rl < rows_valid) ? __ldcg(pk + r0 + rl) : 0.0;
       wacc[i] = 0.0;
     }
-    double pwacc = 0.0;
+    if (cid == 0) {   // the row part p^T (delta I + diag e) p, with the p loads (off the end of the phase)
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t rl = tid + (int64_t)PC_T * i;
+        if (rl < rows_valid) pwacc = fma((delta + (P.e ? P.e[r0 + rl] : 0.0)) * vreg[i], vreg[i], pwacc);
+      }
+    }
     double dprev = 0.0;
     int sp = 0;
     for (int64_t it = 0; it <= niter; ++it) {
@@ -467,10 +474,7 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const int64_t rl = tid + (int64_t)PC_T * i;
-        if (rl < rows_valid) {
-          outp[rl] = wacc[i];
-          if (cid == 0) pwacc = fma((delta + (P.e ? P.e[r0 + rl] : 0.0)) * vreg[i], vreg[i], pwacc);
-        }
+        if (rl < rows_valid) outp[rl] = wacc[i];
       }
       const double wsum = warp_sum(pwacc);
       if (lane == 0) wsh[warp] = wsum;
