@@ -24,6 +24,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "k_vec.cuh"
 
@@ -45,7 +46,8 @@ struct PcgCParams {
   double* P1;
   double* Wp;            // [clusters][wp_ld] partial w rows
   int64_t wp_ld;
-  double* pwp;           // [G]
+  double* pwp;           // [G] CTA partials of sum_j d_j (a_j^T p)^2
+  double* pwrow;         // [G] CTA partials of the row part p^T (delta I + diag e) p (own rows, formed with p)
   double* part1;         // [G][1 + ell]
   double* sc;
   unsigned int* bar;     // grid barrier counter (zeroed before the launch)
@@ -55,6 +57,7 @@ struct PcgCParams {
   int64_t rs;            // rows per cluster rank (even)
   int64_t rpc;           // rows per CTA in the vector phases
   unsigned long long* trace;   // debug (NYS_PCG_TRACE): [2 CTAs][16 iterations][8] globaltimer stamps
+  unsigned long long* trace_mv;  // debug: [G] matvec-phase duration of every CTA at iteration 9
 };
 
 constexpr int PC_T = 480;              // consumer threads (15 warps) + 1 producer warp
@@ -107,7 +110,10 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
   int64_t rows_valid = P.m - r0;
   rows_valid = rows_valid < 0 ? 0 : (rows_valid > P.rs ? P.rs : rows_valid);
   const uint32_t copy_bytes = (uint32_t)(((rows_valid + 1) & ~int64_t(1)) * 8);
-  const int64_t niter = ((int64_t)cid < P.n) ? (P.n - cid + ncl - 1) / ncl : 0;
+  // columns c = ccol + i ncl (ccol = the cluster ids in reverse: cluster 0, which takes the first share
+  // of the vector phases' rows, gets the shorter column list when n is not a multiple of the clusters)
+  const uint32_t ccol = ncl - 1 - cid;
+  const int64_t niter = ((int64_t)ccol < P.n) ? (P.n - ccol + ncl - 1) / ncl : 0;
   const int ell = P.ell;
   int64_t v_lo = (int64_t)bid * P.rpc;
   v_lo = v_lo > P.m ? P.m : v_lo;
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
           if (stop) break;
         }
         if (s_stop) break;
-        const int64_t col = (int64_t)cid + itp * ncl;
+        const int64_t col = (int64_t)ccol + itp * ncl;
         if (++itp == niter) itp = 0;
         if (copy_bytes > 0) {
           mbar_arrive_expect_tx(&full[s], copy_bytes);
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
       }
       if (!init && i0 == v_lo) {
         if (warp == 0) {
-          const double pw = warp_sum_array(P.pwp, (int)G);
+          const double pw = warp_sum_array(P.pwp, (int)G) + warp_sum_array(P.pwrow, (int)G);
           if (lane == 0) s_scal[2] = pw;
         }
         named_bar_sync(9, PC_T);
@@ -349,10 +355,13 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
   };
 
   // ---- own rows: p_next = r + U h + beta p_cur (U h: 20 column loads in flight per row) -------------
+  // (with the row part of the next p^T N p: (delta + e_i) p_i^2 over the own rows -> pwrow[bid])
   auto prec_rows = [&](bool init, double beta, const double* pcur, double* pnext) {
+    double prow = 0.0;
     for (int64_t i0 = v_lo; i0 < v_hi; i0 += PC_T) {
       const int64_t i = i0 + tid;
       if (i >= v_hi) continue;
+      const double ei = P.e ? P.e[i] : 0.0;
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       for (int c0 = 0; c0 < ell; c0 += 20) {
         double v[20];
@@ -362,7 +371,17 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
         for (int k = 0; k < 20; ++k) acc[k & 3] = fma(v[k], hsh[c0 + k], acc[k & 3]);
       }
       const double zi = __ldcg(P.r + i) + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
-      pnext[i] = init ? zi : fma(beta, __ldcg(pcur + i), zi);
+      const double pi = init ? zi : fma(beta, __ldcg(pcur + i), zi);
+      pnext[i] = pi;
+      prow = fma((delta + ei) * pi, pi, prow);
+    }
+    const double pw_w = warp_sum(prow);
+    if (lane == 0) wsh[warp] = pw_w;
+    named_bar_sync(9, PC_T);
+    if (tid == 0) {
+      double b = 0.0;
+      for (int w = 0; w < PC_W; ++w) b += wsh[w];
+      P.pwrow[bid] = b;
     }
   };
 
@@ -399,6 +418,8 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
     double* pn = (k & 1) ? P.P1 : P.P0;         // receives p_{k+1}
     trace_k = k;
     stamp(0);
+    unsigned long long t_mv0 = 0;
+    if (P.trace_mv != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_mv0));
     // ---- P1: p_k slice; fused matvec over this cluster's panels (lag-1 dot exchange) --------------
     double vreg[RPT], wacc[RPT];
     double pwacc = 0.0;
@@ -408,13 +429,6 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
       vreg[i] = (rl < rows_valid) ? __ldcg(pk + r0 + rl) : 0.0;
       wacc[i] = 0.0;
     }
-    if (cid == 0) {   // the row part p^T (delta I + diag e) p, with the p loads (off the end of the phase)
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const int64_t rl = tid + (int64_t)PC_T * i;
-        if (rl < rows_valid) pwacc = fma((delta + (P.e ? P.e[r0 + rl] : 0.0)) * vreg[i], vreg[i], pwacc);
-      }
-    }
     double dprev = 0.0;
     int sp = 0;
     for (int64_t it = 0; it <= niter; ++it) {
@@ -423,7 +437,7 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
         mbar_wait(&full[cs], cph);
         double* sb = stage + (size_t)cs * SS;
         if (odd_owner) sb[rows_valid] = 0.0;
-        dcur = __ldg(P.d + (int64_t)cid + it * ncl);
+        dcur = __ldg(P.d + (int64_t)ccol + it * ncl);
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int i = 0; i < RPT; ++i) acc[i & 3] = fma(sb[tid + PC_T * i], vreg[i], acc[i & 3]);
@@ -486,6 +500,11 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
       }
     }
     stamp(1);
+    if (P.trace_mv != nullptr && tid == 0 && k == 9) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      P.trace_mv[bid] = t - t_mv0;
+    }
     pcgc_grid_barrier(P.bar, G, bar_epoch);
     stamp(2);
     // ---- P2: alpha, own rows, partial rows -------------------------------------------------------
@@ -604,6 +623,7 @@ int launch_pcg_cluster(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int6
   P.wp_ld = mp;
   P.Wp = ctx->wsd("pc_Wp", (size_t)ncl * mp);
   P.pwp = ctx->wsd("pc_pwp", (size_t)G);
+  P.pwrow = ctx->wsd("pc_pwrow", (size_t)G);
   P.part1 = ctx->wsd("pc_part1", (size_t)G * (1 + ell));
   P.bar = (unsigned int*)ctx->ws("pc_bar", 64);
   P.sc = ctx->sc;
@@ -639,6 +659,8 @@ int launch_pcg_cluster(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int6
   if (trace) {
     P.trace = (unsigned long long*)ctx->ws("pc_trace", 2 * 16 * 8 * 8);
     NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.trace, 0, 2 * 16 * 8 * 8, ctx->stream));
+    P.trace_mv = (unsigned long long*)ctx->ws("pc_trace_mv", (size_t)G * 8);
+    NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.trace_mv, 0, (size_t)G * 8, ctx->stream));
   }
   // if fewer clusters can be co-resident than the occupancy query promised (a profiler's reserved
   // resources, another context on the GPU), the cooperative launch is refused: retry with fewer clusters
@@ -663,6 +685,19 @@ int launch_pcg_cluster(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int6
     unsigned long long h[2 * 16 * 8];
     NYS_CUDA_TRY(ctx, cudaMemcpyAsync(h, P.trace, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     NYS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    {
+      std::vector<unsigned long long> mvt((size_t)G);
+      NYS_CUDA_TRY(ctx, cudaMemcpy(mvt.data(), P.trace_mv, (size_t)G * 8, cudaMemcpyDeviceToHost));
+      std::string line;
+      for (int q = 0; q < G; q += pl.cl) {   // per cluster: the slowest CTA's matvec phase (us)
+        unsigned long long mx = 0;
+        for (int r = 0; r < pl.cl && q + r < G; ++r) mx = mvt[q + r] > mx ? mvt[q + r] : mx;
+        char b[32];
+        snprintf(b, sizeof(b), " %.1f", mx * 1e-3);
+        line += b;
+      }
+      fprintf(stderr, "[pcgctrace] it=9 matvec phase per cluster (us):%s\n", line.c_str());
+    }
     for (int c = 0; c < 2; ++c)
       for (int it = 8; it < 12; ++it) {
         const unsigned long long* r = h + (c * 16 + it) * 8;
