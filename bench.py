@@ -88,48 +88,67 @@ def host_info():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    """Clocks / throttle reasons sampled DURING the timed region, as the profiling recipe does: ONE
+    `nvidia-smi --query-gpu=... -lms 200` process started before the warm-up (its NVML start-up stays
+    out of the timed region; an nvidia-smi process spawned per sample stalled the short solves' host
+    calls: config 3 measured 41.6 vs 30.9 ms per solve) and stopped after; a reader thread stamps each
+    line, and summary() keeps the lines that arrived between mark_start() and mark_end()."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int = 0):
         self.gpu = gpu
-        self.samples = []
-        self._stop = threading.Event()
+        self.lines = []
+        self.t0 = self.t1 = None
+        self._p = None
         self._t = None
 
-    def _run(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def start(self):
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "200"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self._p = None
+            return self
 
-    def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
+        def reader():
+            for line in self._p.stdout:
+                self.lines.append((time.time(), [x.strip() for x in line.strip().split(",")]))
+        self._t = threading.Thread(target=reader, daemon=True)
         self._t.start()
         return self
 
-    def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=10)
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time() + 0.25   # the sample that was being taken at the end
+        time.sleep(0.3)
+
+    def stop(self):
+        if self._p is not None:
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except Exception:
+                self._p.kill()
+        if self._t is not None:
+            self._t.join(timeout=5)
 
     def summary(self):
         import statistics
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        samples = [f for t, f in self.lines if self.t0 is not None and self.t0 <= t <= (self.t1 or t)]
+        if not samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(x[0]) for x in samples if x[0].replace(".", "").isdigit()]
+        mx = [float(x[1]) for x in samples if len(x) > 1 and x[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        reasons = sorted({names[k] for x in samples for k in range(4) if len(x) > 3 + k and x[3 + k] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(samples), "sampler": "nvidia-smi -lms 200 (one process)"}
 
 
 # ------------------------------------------------------------------------------------------------
@@ -412,6 +431,7 @@ def main():
             torch.cuda.empty_cache()
 
     # ---- warm-up ------------------------------------------------------------------------------
+    clk = ClockSampler(local).start()
     W = max(args.warmup, 3)
     for _ in range(W):
         g = one_solve()
@@ -420,11 +440,13 @@ def main():
     barrier()
     launches0 = ctx.kernel_launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        results = [one_solve() for _ in range(args.steps)]
-        ev1.record(stream)
-        barrier()
+    clk.mark_start()
+    ev0.record(stream)
+    results = [one_solve() for _ in range(args.steps)]
+    ev1.record(stream)
+    barrier()
+    clk.mark_end()
+    clk.stop()
     launches = ctx.kernel_launches - launches0
     t_dev = ev0.elapsed_time(ev1) / 1e3
     if world > 1:
