@@ -552,10 +552,21 @@ static DgemmKernel nt_kernel(int nt) {
   }
 }
 // pick NT (1..8) minimising the padded width ceil(N / 8NT) * 8NT, ties -> larger NT
+// least padded width over NT in [2, 7], ties -> the smaller NT (NT = 1 only for N <= 8).  Measured on B200
+// (tools/gemm_vs_cublas.py with NYS_GEMM_NT, ms per sketch pair): NT = 1 re-reads the A tile once per
+// 8-column tile and NT = 8 holds 64 accumulators per thread — both the slowest at every width tried
+// (l = 100: NT 1..8 = 0.922 0.841 0.843 0.886 0.835 0.991 0.847 0.892; l = 128: NT 2 2.07, NT 8 2.61;
+// l = 256: NT 3 3.41, NT 8 3.92) while the exact fits NT = 7 (l = 50) and NT = 5 (l = 200, the headline
+// 61.0 ms vs 64.8-72.9 for NT 2, 3, 4, 7) stay
 static int pick_nt(int64_t N) {
-  int best = 8;
-  int64_t best_w = ((N + 63) / 64) * 64;
-  for (int nt = 7; nt >= 1; --nt) {
+  if (const char* e = getenv("NYS_GEMM_NT")) {   // tuning override (1..8)
+    const int o = atoi(e);
+    if (o >= 1 && o <= 8) return o;
+  }
+  if (N <= 8) return 1;
+  int best = 2;
+  int64_t best_w = ((N + 15) / 16) * 16;
+  for (int nt = 3; nt <= 7; ++nt) {
     const int64_t w = ((N + 8 * nt - 1) / (8 * nt)) * (8 * nt);
     if (w < best_w) { best_w = w; best = nt; }
   }
