@@ -1060,8 +1060,15 @@ __global__ void __launch_bounds__(NT, 1) pcg_cluster_small_kernel(const PcgSPara
     double pw = 0.0;
     if (tid < m) {
       const double* rv = recv + (size_t)b * C * M32 + tid;
-      double wsum = 0.0;
-      for (int q = 0; q < C; ++q) wsum += rv[(size_t)q * M32];   // rank order
+      // the C (<= 16) partials in a fixed pairwise tree (depth 4 instead of a C-long add chain)
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = (q < C) ? rv[(size_t)q * M32] : 0.0;
+#pragma unroll
+      for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+        for (int q = 0; q < w; ++q) v[q] += v[q + w];
+      const double wsum = v[0];
       const double wi = wsum + (delta + (P.e ? P.e[tid] : 0.0)) * p_s[tid];
       w_s[tid] = wi;
       pw = p_s[tid] * wi;
