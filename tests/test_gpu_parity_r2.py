@@ -156,12 +156,20 @@ def test_graph_path_pcg_fixed_iterations_match_oracle(ctx, m, n, ell, use_e, pat
     xo, io = oracle_pcg(lambda v: linops.normal_matvec(A, d, v, delta, e), rhs, pinv, tol_abs=0.0, max_iter=iters)
     Ad, lda = colmajor_device(A)
     xg = torch.empty(m, dtype=torch.float64, device="cuda")
+    l0 = ctx.kernel_launches
     info = ctx.nys_pcg_solve(Ad, lda, m, dev(d), dev(e) if use_e else None, delta, ell,
                              dev_cm(Uo) if ell else None, dev(lamo) if ell else None, delta, dev(rhs), xg, 0.0, iters)
+    launches = ctx.kernel_launches - l0
     assert info.iters == iters == io["iters"]
     err = rel(xg.cpu().numpy(), xo)
-    print(f"graph-path PCG m={m} n={n} ell={ell} e={use_e}: rel err {err:.3e}")
+    print(f"{path} PCG m={m} n={n} ell={ell} e={use_e}: rel err {err:.3e}, {launches} kernel launches")
     assert err <= 1e-9
+    # the path that ran: ONE persistent cluster launch (plus the call's setup and true-residual kernels)
+    # against >= 3 launches per iteration on the graph path
+    if path == "cluster":
+        assert launches <= 12, launches
+    else:
+        assert launches >= 3 * iters, launches
 
 
 @pytest.mark.parametrize("ell", [20, 0])
