@@ -61,21 +61,27 @@ struct PcgPParams {
   int64_t npanels;
   int64_t rows_per_cta;
   int64_t ss;                 // stage row stride (lda when near-tight, else even(m))
+  int acq_spin;               // grid barrier: acquire-load spin (1) or relaxed spin + acq_rel fence (0)
 };
 
 // Grid barrier on a monotonically increasing arrival counter (zeroed before the launch): each CTA
 // adds 1 (fire-and-forget reduction) and polls until the counter reaches epoch * G.  No "last
 // arriver" reset round trip, no sleep granularity on the release.
 __device__ __forceinline__ void pcg_grid_barrier(unsigned int* bar, unsigned int nblocks, int nthreads,
-                                                 unsigned int& epoch) {
+                                                 unsigned int& epoch, bool bar_acquire_spin) {
   named_bar_sync(9, nthreads);
   if (threadIdx.x == 0) {
     ++epoch;
     const unsigned int target = epoch * nblocks;
     red_add_release_gpu(bar, 1u);
-    while (ld_relaxed_gpu(bar) < target) {
+    if (bar_acquire_spin) {
+      while (ld_acquire_gpu(bar) < target) {
+      }
+    } else {
+      while (ld_relaxed_gpu(bar) < target) {
+      }
+      fence_acquire_gpu();
     }
-    fence_acquire_gpu();
   }
   named_bar_sync(9, nthreads);
 }
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       if (P.flat_red) {
       named_bar_sync(9, T);  // this CTA's partial row is written
       if (!init) arrive_stamp(1);
-      pcg_grid_barrier(P.bar, G, T, bar_epoch);
+      pcg_grid_barrier(P.bar, G, T, bar_epoch, P.acq_spin != 0);
       constexpr int LB = 38;
       const int CP = (ncol <= 32) ? 32 : (ncol <= 64) ? 64 : (ncol <= 128 || T <= 128) ? 128 : (T <= 256 ? 256 : 512);
       const int NS = T / CP;
@@ -503,7 +509,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       }
       if (!init) stamp(7);
       if (!init) arrive_stamp(2);
-      pcg_grid_barrier(P.bar, G, T, bar_epoch);   // p_next complete on every row
+      pcg_grid_barrier(P.bar, G, T, bar_epoch, P.acq_spin != 0);   // p_next complete on every row
     } else {
       beta = init ? 0.0 : rrt / rz;
       rz = rrt;
@@ -670,7 +676,7 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     }
     stamp(1);
     arrive_stamp(0);
-    pcg_grid_barrier(P.bar, G, T, bar_epoch);
+    pcg_grid_barrier(P.bar, G, T, bar_epoch, P.acq_spin != 0);
     stamp(2);
     }  // !init
     // ---- P2: alpha, own-row updates, partials --------------------------------------------------
@@ -1278,6 +1284,7 @@ int launch_pcg_persistent(nys_ctx* ctx, int64_t m, int64_t n, const double* A, i
   P.npanels = npanels;
   P.ss = ss;
   P.rows_per_cta = (m + G - 1) / G;
+  P.acq_spin = getenv("NYS_BAR_FENCE") ? 0 : 1;
   {
     // L2 prefetch depth beyond the smem ring: ~40 MB of A (about a third of L2) pulled into L2 while
     // the CTAs sit in the reduction / barrier phases, so HBM keeps streaming there.  Measured at

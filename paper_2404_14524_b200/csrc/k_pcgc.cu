@@ -58,6 +58,7 @@ struct PcgCParams {
   int64_t rpc;           // rows per CTA in the vector phases
   unsigned long long* trace;   // debug (NYS_PCG_TRACE): [2 CTAs][16 iterations][8] globaltimer stamps
   unsigned long long* trace_mv;  // debug: [G] matvec-phase duration of every CTA at iteration 9
+  int acq_spin;                  // grid barrier: acquire-load spin (1) or relaxed spin + acq_rel fence (0)
 };
 
 constexpr int PC_T = 480;              // consumer threads (15 warps) + 1 producer warp
@@ -65,15 +66,21 @@ constexpr int PC_W = PC_T / 32;
 constexpr int PC_DB = 4;               // dot-exchange ring depth (lag-1 argument of k_matvec.cu)
 constexpr int PC_LMAX = 256;
 
-__device__ __forceinline__ void pcgc_grid_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& epoch) {
+__device__ __forceinline__ void pcgc_grid_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& epoch,
+                                                  bool bar_acquire_spin) {
   named_bar_sync(9, PC_T);
   if (threadIdx.x == 0) {
     ++epoch;
     const unsigned int target = epoch * nblocks;
     red_add_release_gpu(bar, 1u);
-    while (ld_relaxed_gpu(bar) < target) {
+    if (bar_acquire_spin) {
+      while (ld_acquire_gpu(bar) < target) {
+      }
+    } else {
+      while (ld_relaxed_gpu(bar) < target) {
+      }
+      fence_acquire_gpu();
     }
-    fence_acquire_gpu();
   }
   named_bar_sync(9, PC_T);
 }
@@ -310,7 +317,7 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
   // the NS slice sums are added in order: s_scal[0] = ||r||^2, gsh = U^T r, hsh = s o U^T r,
   // s_scal[1] = r^T z = ||r||^2 + (U^T r)^T h
   auto reduce_rows = [&]() {
-    pcgc_grid_barrier(P.bar, G, bar_epoch);
+    pcgc_grid_barrier(P.bar, G, bar_epoch, P.acq_spin != 0);
     const int CP = ncol <= 120 ? 120 : (ncol <= 240 ? 240 : 480);
     const int NS = PC_T / CP;
     const int sl = tid / CP, c = tid % CP;
@@ -410,7 +417,7 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
     } else {
       rz = rzn;
       prec_rows(true, 0.0, nullptr, P.P1);
-      pcgc_grid_barrier(P.bar, G, bar_epoch);
+      pcgc_grid_barrier(P.bar, G, bar_epoch, P.acq_spin != 0);
     }
   }
   for (int k = 0; !stop; ++k) {
@@ -505,7 +512,7 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       P.trace_mv[bid] = t - t_mv0;
     }
-    pcgc_grid_barrier(P.bar, G, bar_epoch);
+    pcgc_grid_barrier(P.bar, G, bar_epoch, P.acq_spin != 0);
     stamp(2);
     // ---- P2: alpha, own rows, partial rows -------------------------------------------------------
     if (!rows_phase(false, pk)) { status = NYS_EBREAKDOWN; break; }
@@ -520,7 +527,7 @@ __global__ void __launch_bounds__(PC_T + 32, 1) pcg_cluster_kernel(const PcgCPar
     rz = rzn;
     prec_rows(false, beta, pk, pn);
     stamp(5);
-    pcgc_grid_barrier(P.bar, G, bar_epoch);
+    pcgc_grid_barrier(P.bar, G, bar_epoch, P.acq_spin != 0);
     stamp(6);
   }
 
@@ -632,6 +639,7 @@ int launch_pcg_cluster(nys_ctx* ctx, int64_t m, int64_t n, const double* A, int6
   P.cl = pl.cl;
   P.rs = (((m + pl.cl - 1) / pl.cl) + 1) & ~int64_t(1);
   P.rpc = (m + G - 1) / G;
+  P.acq_spin = getenv("NYS_BAR_FENCE") ? 0 : 1;
   NYS_CUDA_TRY(ctx, cudaMemsetAsync(P.bar, 0, 64, ctx->stream));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)G);
