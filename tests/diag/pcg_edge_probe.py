@@ -1,7 +1,7 @@
 """Cluster vs graph PCG against the oracle on edge shapes, error vs iteration count."""
 import os, sys
-sys.path.insert(0, "/root/repo")
-sys.path.insert(0, "/root/repo/tests")
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 from paper_2404_14524_b200 import Context, colmajor_device
 from oracle import linops, nystrom, rng as orng

@@ -124,7 +124,7 @@ GRAPH_PCG = [(8193, 300, 30, False), (8193, 300, 0, False), (20000, 200, 40, Fal
              (50000, 120, 100, False), (50000, 120, 100, True), (50000, 120, 0, True),
              # 4-CTA clusters with an odd last slice, the largest rank, the largest m (16-CTA clusters).  (n = 10,
              # ell = 16 was tried: PCG does not converge there and both paths drift from the oracle by rounding
-             # amplification — 1e-10 / 1e-13 after 8 iterations, 2e-6 / 5e-8 after 15: tools/pcg_edge_probe.py)
+             # amplification — 1e-10 / 1e-13 after 8 iterations, 2e-6 / 5e-8 after 15: tests/diag/pcg_edge_probe.py)
              (30001, 40, 16, True), (20000, 300, 256, False), (138240, 24, 8, True)]
 
 
