@@ -363,6 +363,25 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
     // flight (one L2 round trip at G = 148), then the NS slice sums are added in order.  Measured:
     // the previous two-level "last arriver reduces" chain released CTAs 6.7 us after the last
     // arrival, this 1.5 us barrier + the flat read about half of that.
+    // the first own-row chunk's z-row operands (U rows, r, p_k: none depends on the reduction) are
+    // loaded BEFORE the grid barrier, so their L2 latency hides behind it
+    // (T = 256 only: the 512-thread variants have no registers to spare)
+    constexpr bool PRE_Z = (T == 256);
+    constexpr int UZ = 4;   // columns per group preloaded (ell <= 64 entirely; the rest loads after)
+    double uz[UZ];
+    double zr0 = 0.0, zp0 = 0.0;
+    if constexpr (PRE_Z) {
+      const int64_t i = r_lo + row16;
+#pragma unroll
+      for (int k = 0; k < UZ; ++k) {
+        const int c = grp16 + 16 * k;
+        uz[k] = (warp < 8 && c < ell && i < r_hi) ? __ldg(P.U + (size_t)c * P.ldu + i) : 0.0;
+      }
+      if (tid < 16 && i < r_hi) {
+        zr0 = P.r[i];
+        zp0 = init ? 0.0 : __ldcg(pcur + i);
+      }
+    }
     {
       const int ncol = 1 + ell;
       if (P.flat_red) {
@@ -485,15 +504,24 @@ __global__ void __launch_bounds__(T + 32, 1) pcg_persistent_kernel(const PcgPPar
       rz = rzn;
       for (int64_t i0 = r_lo; i0 < r_hi; i0 += 16) {
         const int64_t i = i0 + row16;
+        const bool first = PRE_Z && i0 == r_lo;
         double pre_r = 0.0, pre_p = 0.0;
         if (tid < 16 && i < r_hi) {
-          pre_r = P.r[i];
-          pre_p = init ? 0.0 : __ldcg(pcur + i);
+          pre_r = first ? zr0 : P.r[i];
+          pre_p = first ? zp0 : (init ? 0.0 : __ldcg(pcur + i));
         }
         if (warp < 8) {
           double acc = 0.0;
-          if (i < r_hi)
-            for (int c = grp16; c < ell; c += 16) acc = fma(P.U[(size_t)c * P.ldu + i], hsh[c], acc);
+          if (i < r_hi) {
+            if (first) {
+#pragma unroll
+              for (int k = 0; k < UZ; ++k)
+                if (grp16 + 16 * k < ell) acc = fma(uz[k], hsh[grp16 + 16 * k], acc);
+              for (int c = grp16 + 16 * UZ; c < ell; c += 16) acc = fma(P.U[(size_t)c * P.ldu + i], hsh[c], acc);
+            } else {
+              for (int c = grp16; c < ell; c += 16) acc = fma(P.U[(size_t)c * P.ldu + i], hsh[c], acc);
+            }
+          }
           chunk_red[row16][grp16] = acc;
         }
         named_bar_sync(9, T);
