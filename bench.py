@@ -222,11 +222,11 @@ class Workload:
         return 8.0 * self.m * self.ncols
 
 
-# config-4 slice step (3 outer iterations) as measured on the GPU (profiles/r01_bench_cfg4_slice_3outer.json):
-# 166 PCG iterations + the initial point's 2 solves = 167 operator applications, plus per outer iteration
-# ~3 operator-equivalents of N-only / T-only passes (xi, recovery x2, residuals) and 2 at the initial
-# point; 4 sketches + Nystrom factorisations (initial point + 3 outer iterations).
-CFG4_STEP_COUNTS = {"matvecs": 167 + 3 * 3 + 2, "sketches": 4}
+# config-4 slice step (3 outer iterations) as measured on the GPU (profiles/r02_bench_cfg4_slice_final4.json):
+# 124 PCG iterations incl. the initial point's 2 solves = 124 operator applications, plus per outer
+# iteration ~3 operator-equivalents of N-only / T-only passes (xi, recovery x2, residuals) and 2 at the
+# initial point; 4 sketches + Nystrom factorisations (initial point + 3 outer iterations).
+CFG4_STEP_COUNTS = {"matvecs": 124 + 3 * 3 + 2, "sketches": 4}
 
 
 def run_reference(args):
