@@ -222,7 +222,7 @@ class Workload:
         return 8.0 * self.m * self.ncols
 
 
-# config-4 slice step (3 outer iterations) as measured on the GPU (profiles/r02_bench_cfg4_slice_final4.json):
+# config-4 slice step (3 outer iterations) as measured on the GPU (profiles/r02_bench_cfg4_slice_final5.json):
 # 124 PCG iterations incl. the initial point's 2 solves = 124 operator applications, plus per outer
 # iteration ~3 operator-equivalents of N-only / T-only passes (xi, recovery x2, residuals) and 2 at the
 # initial point; 4 sketches + Nystrom factorisations (initial point + 3 outer iterations).
